@@ -1,0 +1,152 @@
+/*
+ * coopbatch_cuda.h — the C-ABI of libcoopbatch_b200.so, the B200-native
+ * drop-in for the reference's cooperative sample + dedup + feature-gather
+ * path (arxiv 2310.12403 "coopbatch", /root/reference/proj).
+ *
+ * Plain C: opaque handles, host pointers + sizes, int status codes. No torch
+ * or CUDA types cross this boundary (streams are passed as void*).
+ *
+ * Reference interfaces each entry point replaces (file:line under
+ * /root/reference/proj):
+ *   cb_graph_create_from_csr  <- coopbatch::Graph / build_csr result
+ *                                (include/coopbatch/graph.hpp:21-53,
+ *                                 src/graph.cpp:17-48)
+ *   cb_graph_generate_rmat    <- generate_powerlaw (graph.hpp:57-63,
+ *                                src/graph.cpp:111-151); R-MAT per DESIGN.md
+ *   cb_partition_random       <- partition_random (partition.hpp:21-23,
+ *                                src/partition.cpp:10-20)
+ *   cb_partition_create       <- PartitionMap (partition.hpp:12-17)
+ *   cb_features_synth         <- FeatureStore::synth (coop.hpp:140-150,
+ *                                src/coop.cpp:359-376)
+ *   cb_plan_create            <- SamplerConfig + num_layers (samplers.hpp:17-23)
+ *   cb_sample (mode INDEP)    <- expand / indep_sample (samplers.hpp:167-169,
+ *                                coop.hpp:55-58; src/samplers.cpp:340-354,
+ *                                src/coop.cpp:108-119)
+ *   cb_sample (mode COOP)     <- coop_sample (coop.hpp:49-52,
+ *                                src/coop.cpp:68-106 + build_exchange 25-64)
+ *   cb_gather                 <- FeatureStore::load_rows + all_to_all_forward
+ *                                (coop.hpp:66-68,151; src/coop.cpp:145-159,
+ *                                 378-388)
+ *   cb_download_block         <- BipartiteBlock fields (samplers.hpp:30-38)
+ *   cb_download_exchange      <- ExchangeRecord fields (coop.hpp:25-37)
+ *   cb_download_owner_set     <- CoopSampleResult::owner_sets (coop.hpp:39-43)
+ *   cb_last_error             <- the what() of coopbatch::InputError etc.
+ *                                (include/coopbatch/common.hpp:12-31)
+ */
+#ifndef COOPBATCH_CUDA_H
+#define COOPBATCH_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (0 = ok). CB_INPUT maps to coopbatch::InputError. */
+enum {
+  CB_OK = 0,
+  CB_INPUT = 1,
+  CB_FORMAT = 2,
+  CB_IO = 3,
+  CB_CUDA = 4,
+  CB_NCCL = 5,
+  CB_OVERFLOW = 6,
+  CB_INTERNAL = 7
+};
+
+/* SamplerKind order of samplers.hpp:15 */
+enum { CB_FULL = 0, CB_NS = 1, CB_LABOR0 = 2 };
+enum { CB_MODE_COOP = 0, CB_MODE_INDEP = 1 };
+enum { CB_F64 = 0, CB_F32 = 1, CB_F16 = 2 };
+
+/* SeedSchedule (rng.hpp:93-111); kappa = UINT64_MAX is infinity. */
+typedef struct cb_sched {
+  uint64_t kappa;
+  uint64_t z1;
+  uint64_t z2;
+  uint64_t iteration;
+} cb_sched;
+
+typedef struct cb_graph cb_graph;
+typedef struct cb_partition cb_partition;
+typedef struct cb_features cb_features;
+typedef struct cb_plan cb_plan;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* cb_last_error(void);
+const char* cb_version(void);
+int cb_device_count(int* out);
+
+/* ---- graph (CSR resident in HBM) ---- */
+int cb_graph_create_from_csr(const uint64_t* indptr, const uint32_t* indices, uint64_t n,
+                             uint64_t m, int device, cb_graph** out);
+int cb_graph_generate_rmat(uint64_t n, uint64_t m, uint64_t seed, int device,
+                           cb_graph** out);
+int cb_graph_info(const cb_graph* g, uint64_t* n, uint64_t* m, uint64_t* max_degree);
+int cb_graph_download(const cb_graph* g, uint64_t* indptr, uint32_t* indices);
+void cb_graph_destroy(cb_graph* g);
+
+/* ---- 1D vertex ownership ---- */
+int cb_partition_random(const cb_graph* g, uint32_t parts, uint64_t seed, cb_partition** out);
+int cb_partition_create(const cb_graph* g, const uint32_t* owner, uint32_t parts,
+                        cb_partition** out);
+int cb_partition_download(const cb_partition* pm, uint32_t* owner);
+void cb_partition_destroy(cb_partition* pm);
+
+/* ---- feature tables (row-sharded by owner when pm != NULL) ---- */
+int cb_features_synth(const cb_graph* g, const cb_partition* pm, uint32_t dim, int dtype,
+                      uint64_t seed, cb_features** out);
+int cb_features_info(const cb_features* f, uint32_t* dim, int* dtype, uint64_t* row_bytes);
+void cb_features_destroy(cb_features* f);
+
+/* ---- sampling plan ---- */
+/* fanouts[l] applies at block l (seeds outward); pm may be NULL for P = 1. */
+int cb_plan_create(const cb_graph* g, const cb_partition* pm, int num_layers, int kind,
+                   const uint32_t* fanouts, uint64_t max_seeds_per_part, cb_plan** out);
+void cb_plan_destroy(cb_plan* plan);
+int cb_plan_num_parts(const cb_plan* plan, uint32_t* parts);
+/* The CUDA stream every kernel of this plan runs on (cudaStream_t). */
+void* cb_plan_stream(const cb_plan* plan);
+
+/* One batch. seeds_flat holds the P per-part seed lists back to back,
+ * seeds_off[P+1] their offsets (host memory). Enqueues everything on the plan
+ * stream; cb_sample_sync additionally waits and retries with larger
+ * buffers if a capacity bound overflowed. */
+int cb_sample(cb_plan* plan, int mode, const uint32_t* seeds_flat, const uint64_t* seeds_off,
+              const cb_sched* sched);
+int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
+                   const uint64_t* seeds_off, const cb_sched* sched);
+/* Same, seeds already in device memory (seeds_off on host). */
+int cb_sample_device(cb_plan* plan, int mode, const uint32_t* d_seeds_flat,
+                     const uint64_t* seeds_off, const cb_sched* sched);
+
+/* Gather input-feature rows of every part's input vertices (requester
+ * aligned, = all_to_all_forward of the owners' load_rows). */
+int cb_gather(cb_plan* plan, const cb_features* f);
+
+/* Wait for the plan stream; CB_OVERFLOW if a capacity bound was exceeded. */
+int cb_synchronize(cb_plan* plan);
+
+/* sizes[0..5] = n_dst, n_src, n_edges, uncertified, scan_total, n_active */
+int cb_layer_sizes(cb_plan* plan, uint32_t part, int layer, uint64_t* sizes);
+int cb_download_block(cb_plan* plan, uint32_t part, int layer, uint32_t* dst, uint32_t* src,
+                      uint32_t* edges /* 2 per edge */, uint32_t* dst_pos);
+int cb_owner_set_size(cb_plan* plan, uint32_t part, uint64_t* n);
+int cb_download_owner_set(cb_plan* plan, uint32_t part, uint32_t* ids);
+/* send_counts[P*P] (row = sender), owner_row_counts[P]; loc_* hold part p's
+ * src_location entries back to back in part order. */
+int cb_download_exchange(cb_plan* plan, int layer, uint64_t* send_counts,
+                         uint64_t* owner_row_counts, uint32_t* loc_part, uint64_t* loc_row);
+/* Gathered rows of `part` (n_src(L-1) x row_bytes). */
+int cb_download_rows(cb_plan* plan, uint32_t part, void* out);
+/* Device pointer of `part`'s gathered rows (for in-HBM consumers). */
+int cb_rows_device(cb_plan* plan, uint32_t part, void** ptr, uint64_t* rows);
+
+/* Number of kernels one cb_sample/cb_gather call enqueues (for reporting). */
+int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,530 @@
+"""TEST INFRASTRUCTURE ONLY — the CPU checker, never the product path.
+
+ctypes front-end over the two CPU checkers built by ``oracle/Makefile``:
+
+* ``impl="restated"`` — ``oracle/liboracle.so``, the plain-C restatement of the
+  reference algorithm (coopbatch_oracle.c; every function cites the reference
+  file:line it restates);
+* ``impl="reference"`` — ``oracle/_ref/libcoopbatch_ref.so``, the reference's own
+  C++ sources (/root/reference/proj/src) compiled unmodified, behind the
+  ``ref_capi.cpp`` shim.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU legs import
+this module. Results use the same plain-dict layout as the product's
+``paper_2310_12403_b200.coopbatch`` so parity checks are ``np.array_equal``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+OB_PATH = os.path.join(HERE, "liboracle.so")
+RF_PATH = os.path.join(HERE, "_ref", "libcoopbatch_ref.so")
+
+KAPPA_INF = (1 << 64) - 1
+FULL, NS, LABOR0 = 0, 1, 2
+
+
+class OracleError(ValueError):
+    """The checker rejected its input (reference coopbatch::InputError)."""
+
+
+class Sched(C.Structure):
+    _fields_ = [("kappa", C.c_uint64), ("z1", C.c_uint64), ("z2", C.c_uint64),
+                ("iteration", C.c_uint64)]
+
+
+class Block(C.Structure):
+    _fields_ = [("layer", C.c_int32), ("n_dst", C.c_uint64), ("n_src", C.c_uint64),
+                ("n_edges", C.c_uint64), ("dst", C.POINTER(C.c_uint32)),
+                ("src", C.POINTER(C.c_uint32)), ("edges", C.POINTER(C.c_uint32)),
+                ("dst_pos", C.POINTER(C.c_uint32))]
+
+
+class Stack(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("blocks", C.POINTER(Block))]
+
+
+class Exchange(C.Structure):
+    _fields_ = [("layer", C.c_int32), ("num_parts", C.c_uint32),
+                ("send_counts", C.POINTER(C.c_uint64)),
+                ("owner_row_counts", C.POINTER(C.c_uint64)),
+                ("loc_len", C.POINTER(C.c_uint64)),
+                ("loc_part", C.POINTER(C.POINTER(C.c_uint32))),
+                ("loc_row", C.POINTER(C.POINTER(C.c_uint64)))]
+
+
+class Coop(C.Structure):
+    _fields_ = [("num_parts", C.c_uint32), ("num_layers", C.c_int32),
+                ("stacks", C.POINTER(Stack)), ("exchanges", C.POINTER(Exchange)),
+                ("owner_len", C.POINTER(C.c_uint64)),
+                ("owner_sets", C.POINTER(C.POINTER(C.c_uint32)))]
+
+
+_P = C.c_void_p
+_u64, _u32, _i32, _f64 = C.c_uint64, C.c_uint32, C.c_int32, C.c_double
+
+_libs: dict[str, C.CDLL] = {}
+
+
+def available(impl: str = "restated") -> bool:
+    return os.path.exists(OB_PATH if impl == "restated" else RF_PATH)
+
+
+def lib(impl: str = "restated") -> C.CDLL:
+    if impl in _libs:
+        return _libs[impl]
+    path = OB_PATH if impl == "restated" else RF_PATH
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} not built (run __graft_entry__.build())")
+    L = C.CDLL(path)
+    pre = "ob_" if impl == "restated" else "rf_"
+    L.last_error = getattr(L, pre + "last_error")
+    L.last_error.restype = C.c_char_p
+    _libs[impl] = L
+    if impl == "restated":
+        L.ob_mix64.restype = _u64
+        L.ob_mix64.argtypes = [_u64]
+        L.ob_hash_bits.restype = _u64
+        L.ob_hash_bits.argtypes = [_u64, _P, C.c_int]
+        L.ob_hash_uniform.restype = _f64
+        L.ob_hash_uniform.argtypes = [_u64, _P, C.c_int]
+        L.ob_phi.restype = _f64
+        L.ob_phi.argtypes = [_f64]
+        L.ob_inverse_phi.restype = _f64
+        L.ob_inverse_phi.argtypes = [_f64]
+        L.ob_sched_make.argtypes = [_u64, _u64, C.POINTER(Sched)]
+        L.ob_sched_advance.argtypes = [C.POINTER(Sched)]
+        L.ob_rmat.argtypes = [_u64, _u64, _u64, C.POINTER(C.POINTER(_u64)),
+                              C.POINTER(C.POINTER(_u32))]
+        L.ob_build_csr.argtypes = [_P, _P, _u64, _u64, _P, _P]
+        L.ob_partition_random.argtypes = [_u64, _u32, _u64, _P]
+        L.ob_sample_block.argtypes = [_P, _P, _u64, _P, _u64, C.c_int, _u32,
+                                      C.POINTER(Sched), C.c_int, C.POINTER(Block)]
+        L.ob_expand.argtypes = [_P, _P, _u64, _P, _u64, C.c_int, C.c_int, _P,
+                                C.POINTER(Sched), C.POINTER(Stack)]
+        L.ob_coop_sample.argtypes = [_P, _P, _u64, _P, _u32, _P, _P, C.c_int, C.c_int,
+                                     _P, C.POINTER(Sched), C.POINTER(Coop)]
+        L.ob_block_free.argtypes = [C.POINTER(Block)]
+        L.ob_stack_free.argtypes = [C.POINTER(Stack)]
+        L.ob_coop_free.argtypes = [C.POINTER(Coop)]
+        L.ob_feature_rows.argtypes = [_u64, _u32, C.c_int, _P, _u64, _P]
+        L.ob_lru_new.restype = _P
+        L.ob_lru_new.argtypes = [_u64]
+        L.ob_lru_access.argtypes = [_P, _u32]
+        L.ob_lru_free.argtypes = [_P]
+        L.ob_access_order.argtypes = [_P, _u64, _u64, _P]
+        L.ob_stack_fingerprint.restype = _u64
+        L.ob_stack_fingerprint.argtypes = [C.POINTER(Stack)]
+        L.ob_draw_from_pool.argtypes = [_P, _u64, _u64, _u64, _u64, _P]
+        L.ob_free.argtypes = [_P]
+    else:
+        L.rf_mix64.restype = _u64
+        L.rf_mix64.argtypes = [_u64]
+        L.rf_hash_bits.restype = _u64
+        L.rf_hash_bits.argtypes = [_u64, _P, C.c_int]
+        L.rf_phi.restype = _f64
+        L.rf_phi.argtypes = [_f64]
+        L.rf_inverse_phi.restype = _f64
+        L.rf_inverse_phi.argtypes = [_f64]
+        L.rf_normal_from_bits.restype = _f64
+        L.rf_normal_from_bits.argtypes = [_u64]
+        L.rf_labor_variate.restype = _f64
+        L.rf_labor_variate.argtypes = [C.POINTER(Sched), C.c_int, _u32]
+        L.rf_sched_make.argtypes = [_u64, _u64, C.POINTER(Sched)]
+        L.rf_sched_advance.argtypes = [C.POINTER(Sched)]
+        L.rf_graph_new.restype = _P
+        L.rf_graph_new.argtypes = [_P, _P, _u64, _u64]
+        L.rf_graph_free.argtypes = [_P]
+        L.rf_validate_csr.argtypes = [_P]
+        L.rf_generate_powerlaw.argtypes = [_u64, _f64, _f64, _u64,
+                                           C.POINTER(C.POINTER(_u64)),
+                                           C.POINTER(C.POINTER(_u32)), C.POINTER(_u64)]
+        L.rf_build_csr.argtypes = [_P, _P, _u64, _u64, _P, _P]
+        L.rf_partition_random.argtypes = [_u64, _u32, _u64, _P]
+        L.rf_sample_block.argtypes = [_P, _P, _u64, C.c_int, _u32, C.POINTER(Sched),
+                                      C.c_int, C.POINTER(Block)]
+        L.rf_expand.argtypes = [_P, _P, _u64, C.c_int, C.c_int, _P, C.POINTER(Sched),
+                                C.POINTER(Stack)]
+        L.rf_coop_sample.argtypes = [_P, _P, _u32, _P, _P, C.c_int, C.c_int, _u32,
+                                     C.POINTER(Sched), C.POINTER(Coop)]
+        L.rf_block_free.argtypes = [C.POINTER(Block)]
+        L.rf_stack_free.argtypes = [C.POINTER(Stack)]
+        L.rf_coop_free.argtypes = [C.POINTER(Coop)]
+        L.rf_free.argtypes = [_P]
+        L.rf_features_new.restype = _P
+        L.rf_features_new.argtypes = [_u64, _u32, _u32, _u64]
+        L.rf_features_free.argtypes = [_P]
+        L.rf_load_rows.argtypes = [_P, _P, _u64, _P]
+        L.rf_all_to_all_forward.argtypes = [C.POINTER(Coop), C.c_int, _P, _P, _u32, _P]
+        L.rf_lru_new.restype = _P
+        L.rf_lru_new.argtypes = [_u64]
+        L.rf_lru_access.argtypes = [_P, _u32]
+        L.rf_lru_free.argtypes = [_P]
+        L.rf_dependent_experiment.argtypes = [_P, C.c_int, _u64, _u64, _u64, _u64,
+                                              C.c_int, _u32, C.c_int, _u32, _u32, _u64,
+                                              _P, _P, _P, C.POINTER(_f64)]
+    return L
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _check(rc: int, L: C.CDLL):
+    if rc != 0:
+        raise OracleError(L.last_error().decode())
+
+
+def _arr(p, n, dtype):
+    if n == 0:
+        return np.zeros(0, dtype=dtype)
+    return np.ctypeslib.as_array(p, shape=(int(n),)).astype(dtype, copy=True)
+
+
+def _block(b: Block) -> dict:
+    return {
+        "layer": int(b.layer),
+        "dst": _arr(b.dst, b.n_dst, np.uint32),
+        "src": _arr(b.src, b.n_src, np.uint32),
+        "edges": _arr(b.edges, 2 * b.n_edges, np.uint32).reshape(-1, 2),
+        "dst_pos": _arr(b.dst_pos, b.n_dst, np.uint32),
+    }
+
+
+def _stack(s: Stack) -> list[dict]:
+    return [_block(s.blocks[l]) for l in range(s.num_layers)]
+
+
+# --------------------------------------------------------------------- rng ---
+
+def make_sched(kappa: int, root_seed: int, impl: str = "restated") -> Sched:
+    s = Sched()
+    getattr(lib(impl), "ob_sched_make" if impl == "restated" else "rf_sched_make")(
+        kappa, root_seed, C.byref(s))
+    return s
+
+
+def plain_sched(seed: int) -> Sched:
+    """test_samplers.cpp:45-50 plain_schedule: kappa 1, z1 = z2 = seed."""
+    return Sched(1, seed, seed, 0)
+
+
+def advance(s: Sched, impl: str = "restated") -> Sched:
+    t = Sched(s.kappa, s.z1, s.z2, s.iteration)
+    getattr(lib(impl), "ob_sched_advance" if impl == "restated" else "rf_sched_advance")(
+        C.byref(t))
+    return t
+
+
+def hash_bits(seed: int, ids, impl: str = "restated") -> int:
+    a = np.asarray(ids, dtype=np.uint64)
+    L = lib(impl)
+    f = L.ob_hash_bits if impl == "restated" else L.rf_hash_bits
+    return int(f(seed, _ptr(a), len(a)))
+
+
+# ------------------------------------------------------------------- graph ---
+
+@dataclass
+class CSR:
+    indptr: np.ndarray   # u64[n+1]
+    indices: np.ndarray  # u32[m]
+
+    @property
+    def n(self) -> int:
+        return len(self.indptr) - 1
+
+    @property
+    def m(self) -> int:
+        return len(self.indices)
+
+
+def rmat(n: int, m: int, seed: int) -> CSR:
+    L = lib("restated")
+    ip = C.POINTER(_u64)()
+    ix = C.POINTER(_u32)()
+    _check(L.ob_rmat(n, m, seed, C.byref(ip), C.byref(ix)), L)
+    g = CSR(_arr(ip, n + 1, np.uint64), _arr(ix, m, np.uint32))
+    L.ob_free(C.cast(ip, C.c_void_p))
+    L.ob_free(C.cast(ix, C.c_void_p))
+    return g
+
+
+def generate_powerlaw(n: int, deg: float, skew: float, seed: int) -> CSR:
+    """The reference's own generator (graph.cpp:111-151), for fixtures."""
+    L = lib("reference")
+    ip = C.POINTER(_u64)()
+    ix = C.POINTER(_u32)()
+    m = _u64()
+    _check(L.rf_generate_powerlaw(n, deg, skew, seed, C.byref(ip), C.byref(ix),
+                                  C.byref(m)), L)
+    g = CSR(_arr(ip, n + 1, np.uint64), _arr(ix, m.value, np.uint32))
+    L.rf_free(C.cast(ip, C.c_void_p))
+    L.rf_free(C.cast(ix, C.c_void_p))
+    return g
+
+
+def build_csr(src, dst, n: int, impl: str = "restated") -> CSR:
+    src = np.ascontiguousarray(src, dtype=np.uint32)
+    dst = np.ascontiguousarray(dst, dtype=np.uint32)
+    ip = np.zeros(n + 1, dtype=np.uint64)
+    ix = np.zeros(len(src), dtype=np.uint32)
+    L = lib(impl)
+    f = L.ob_build_csr if impl == "restated" else L.rf_build_csr
+    _check(f(_ptr(src), _ptr(dst), len(src), n, _ptr(ip), _ptr(ix)), L)
+    return CSR(ip, ix)
+
+
+class RefGraph:
+    """A coopbatch::Graph inside the compiled reference."""
+
+    def __init__(self, g: CSR):
+        self.csr = g
+        self.L = lib("reference")
+        self.h = self.L.rf_graph_new(_ptr(g.indptr), _ptr(g.indices), g.n, g.m)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.rf_graph_free(self.h)
+            self.h = None
+
+
+def partition_random(n: int, parts: int, seed: int, impl: str = "restated") -> np.ndarray:
+    owner = np.zeros(n, dtype=np.uint32)
+    L = lib(impl)
+    f = L.ob_partition_random if impl == "restated" else L.rf_partition_random
+    _check(f(n, parts, seed, _ptr(owner)), L)
+    return owner
+
+
+def part_members(owner: np.ndarray, parts: int) -> list[np.ndarray]:
+    """partition.cpp:99-105: vertices of each part, ascending."""
+    return [np.flatnonzero(owner == p).astype(np.uint32) for p in range(parts)]
+
+
+# ---------------------------------------------------------------- sampling ---
+
+def _fanouts(fanout, L: int) -> np.ndarray:
+    if np.isscalar(fanout):
+        return np.full(L, int(fanout), dtype=np.uint32)
+    f = np.asarray(fanout, dtype=np.uint32)
+    assert len(f) == L
+    return f
+
+
+def sample_block(g, seeds, kind: int, fanout: int, sched: Sched, layer: int,
+                 impl: str = "restated") -> dict:
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint32)
+    b = Block()
+    if impl == "restated":
+        L = lib(impl)
+        _check(L.ob_sample_block(_ptr(g.indptr), _ptr(g.indices), g.n, _ptr(seeds),
+                                 len(seeds), kind, fanout, C.byref(sched), layer,
+                                 C.byref(b)), L)
+        out = _block(b)
+        L.ob_block_free(C.byref(b))
+    else:
+        rg = g if isinstance(g, RefGraph) else RefGraph(g)
+        L = rg.L
+        _check(L.rf_sample_block(rg.h, _ptr(seeds), len(seeds), kind, fanout,
+                                 C.byref(sched), layer, C.byref(b)), L)
+        out = _block(b)
+        L.rf_block_free(C.byref(b))
+    return out
+
+
+def expand(g, seeds, num_layers: int, kind: int, fanout, sched: Sched,
+           impl: str = "restated") -> list[dict]:
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint32)
+    fo = _fanouts(fanout, num_layers)
+    s = Stack()
+    if impl == "restated":
+        L = lib(impl)
+        _check(L.ob_expand(_ptr(g.indptr), _ptr(g.indices), g.n, _ptr(seeds), len(seeds),
+                           num_layers, kind, _ptr(fo), C.byref(sched), C.byref(s)), L)
+        out = _stack(s)
+        L.ob_stack_free(C.byref(s))
+    else:
+        rg = g if isinstance(g, RefGraph) else RefGraph(g)
+        L = rg.L
+        _check(L.rf_expand(rg.h, _ptr(seeds), len(seeds), num_layers, kind, _ptr(fo),
+                           C.byref(sched), C.byref(s)), L)
+        out = _stack(s)
+        L.rf_stack_free(C.byref(s))
+    return out
+
+
+def _coop_dict(c: Coop) -> dict:
+    P, Lh = c.num_parts, c.num_layers
+    ex = []
+    for l in range(Lh):
+        e = c.exchanges[l]
+        ex.append({
+            "layer": int(e.layer),
+            "send_counts": _arr(e.send_counts, P * P, np.uint64).reshape(P, P),
+            "owner_row_counts": _arr(e.owner_row_counts, P, np.uint64),
+            "loc_part": [_arr(e.loc_part[p], e.loc_len[p], np.uint32) for p in range(P)],
+            "loc_row": [_arr(e.loc_row[p], e.loc_len[p], np.uint64) for p in range(P)],
+        })
+    return {
+        "stacks": [_stack(c.stacks[p]) for p in range(P)],
+        "exchanges": ex,
+        "owner_sets": [_arr(c.owner_sets[p], c.owner_len[p], np.uint32) for p in range(P)],
+    }
+
+
+def coop_sample(g, owner, parts: int, per_pe_seeds, num_layers: int, kind: int,
+                fanout, sched: Sched, impl: str = "restated", keep_handle=False):
+    owner = np.ascontiguousarray(owner, dtype=np.uint32)
+    flat = np.ascontiguousarray(np.concatenate(
+        [np.asarray(s, dtype=np.uint32) for s in per_pe_seeds]) if per_pe_seeds
+        else np.zeros(0, np.uint32), dtype=np.uint32)
+    off = np.zeros(len(per_pe_seeds) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(s) for s in per_pe_seeds])
+    fo = _fanouts(fanout, num_layers)
+    c = Coop()
+    if impl == "restated":
+        L = lib(impl)
+        if len(per_pe_seeds) != parts:
+            raise OracleError("coop_sample: seed lists must match the partition count")
+        _check(L.ob_coop_sample(_ptr(g.indptr), _ptr(g.indices), g.n, _ptr(owner), parts,
+                                _ptr(flat), _ptr(off), num_layers, kind, _ptr(fo),
+                                C.byref(sched), C.byref(c)), L)
+        out = _coop_dict(c)
+        L.ob_coop_free(C.byref(c))
+        return out
+    rg = g if isinstance(g, RefGraph) else RefGraph(g)
+    L = rg.L
+    if len(per_pe_seeds) != parts:
+        raise OracleError("coop_sample: seed lists must match the partition count")
+    if len(set(fo.tolist())) > 1:
+        raise OracleError("reference coop_sample has a single fanout")
+    _check(L.rf_coop_sample(rg.h, _ptr(owner), parts, _ptr(flat), _ptr(off), num_layers,
+                            kind, int(fo[0]) if len(fo) else 1, C.byref(sched),
+                            C.byref(c)), L)
+    out = _coop_dict(c)
+    if keep_handle:
+        return out, c
+    L.rf_coop_free(C.byref(c))
+    return out
+
+
+def coop_free_reference(c: Coop):
+    lib("reference").rf_coop_free(C.byref(c))
+
+
+# ---------------------------------------------------------------- features ---
+
+DTYPES = {"f64": (0, np.float64), "f32": (1, np.float32), "f16": (2, np.float16)}
+
+
+def feature_rows(seed: int, dim: int, dtype: str, ids) -> np.ndarray:
+    """coop.cpp:369-371 values for `ids`, rounded once to `dtype`."""
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    code, npdt = DTYPES[dtype]
+    out = np.zeros((len(ids), dim), dtype=npdt)
+    lib("restated").ob_feature_rows(seed, dim, code, _ptr(ids), len(ids), _ptr(out))
+    return out
+
+
+class RefFeatureStore:
+    """coopbatch::FeatureStore::synth (coop.cpp:359-376), f64 table."""
+
+    def __init__(self, n: int, dim: int, seed: int, classes: int = 2):
+        self.L = lib("reference")
+        self.dim = dim
+        self.h = self.L.rf_features_new(n, dim, classes, seed)
+
+    def load_rows(self, ids) -> np.ndarray:
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        out = np.zeros((len(ids), self.dim), dtype=np.float64)
+        self.L.rf_load_rows(self.h, _ptr(ids), len(ids), _ptr(out))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.rf_features_free(self.h)
+            self.h = None
+
+
+# ------------------------------------------------------------------- cache ---
+
+class Lru:
+    def __init__(self, cap: int, impl: str = "restated"):
+        self.L = lib(impl)
+        self.impl = impl
+        self.h = (self.L.ob_lru_new if impl == "restated" else self.L.rf_lru_new)(cap)
+        if not self.h:
+            raise OracleError("LruCache: capacity must be >= 1")
+
+    def access(self, key: int) -> bool:
+        """True on miss."""
+        f = self.L.ob_lru_access if self.impl == "restated" else self.L.rf_lru_access
+        return bool(f(self.h, key))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            (self.L.ob_lru_free if self.impl == "restated" else self.L.rf_lru_free)(self.h)
+            self.h = None
+
+
+def access_order(ids, key: int) -> np.ndarray:
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    out = np.zeros_like(ids)
+    lib("restated").ob_access_order(_ptr(ids), len(ids), key, _ptr(out))
+    return out
+
+
+def stack_fingerprint(stack: list[dict]) -> int:
+    """cache.cpp:123-133 over a dict-form stack (pure numpy restatement)."""
+    L = lib("restated")
+    blocks = (Block * len(stack))()
+    keep = []
+    for i, b in enumerate(stack):
+        arrs = [np.ascontiguousarray(b[k], dtype=np.uint32)
+                for k in ("dst", "src", "edges", "dst_pos")]
+        keep.append(arrs)
+        blocks[i].layer = b["layer"]
+        blocks[i].n_dst = len(arrs[0])
+        blocks[i].n_src = len(arrs[1])
+        blocks[i].n_edges = arrs[2].size // 2
+        blocks[i].dst = arrs[0].ctypes.data_as(C.POINTER(C.c_uint32))
+        blocks[i].src = arrs[1].ctypes.data_as(C.POINTER(C.c_uint32))
+        blocks[i].edges = arrs[2].ctypes.data_as(C.POINTER(C.c_uint32))
+        blocks[i].dst_pos = arrs[3].ctypes.data_as(C.POINTER(C.c_uint32))
+    s = Stack(len(stack), C.cast(blocks, C.POINTER(Block)))
+    return int(L.ob_stack_fingerprint(C.byref(s)))
+
+
+def draw_from_pool(pool, count: int, seed: int, tag: int) -> np.ndarray:
+    pool = np.ascontiguousarray(pool, dtype=np.uint32)
+    out = np.zeros(count, dtype=np.uint32)
+    L = lib("restated")
+    _check(L.ob_draw_from_pool(_ptr(pool), len(pool), count, seed, tag, _ptr(out)), L)
+    return out
+
+
+def draw_coop_seeds(owner: np.ndarray, parts: int, b: int, seed: int,
+                    step: int) -> list[np.ndarray]:
+    """cli.cpp:210-214: per-PE seeds draw_from_pool(members[p], b, seed,
+    hash_bits(step, {p}))."""
+    members = part_members(owner, parts)
+    return [draw_from_pool(members[p], b, seed, hash_bits(step, [p])) for p in range(parts)]
+
+
+def dependent_experiment(g, mode: int, kappa: int, batch: int, steps: int, capacity: int,
+                         kind: int, fanout: int, L: int, dim: int, bps: int, seed: int):
+    rg = g if isinstance(g, RefGraph) else RefGraph(g)
+    fp = np.zeros(steps, np.uint64)
+    sl = np.zeros(steps, np.uint64)
+    by = np.zeros(steps, np.uint64)
+    steady = C.c_double()
+    _check(rg.L.rf_dependent_experiment(rg.h, mode, kappa, batch, steps, capacity, kind,
+                                        fanout, L, dim, bps, seed, _ptr(fp), _ptr(sl),
+                                        _ptr(by), C.byref(steady)), rg.L)
+    return {"fingerprint": fp, "s_l": sl, "bytes": by, "steady": steady.value}

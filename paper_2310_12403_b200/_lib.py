@@ -1,0 +1,85 @@
+"""Loader for libcoopbatch_b200.so (the sm_100a kernels + C-ABI).
+
+There is no fallback: if the shared library is missing, importing the product
+API raises, so a GPU run can never silently degrade to a CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcoopbatch_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "coopbatch_cuda.h")
+
+
+class Sched(C.Structure):
+    _fields_ = [("kappa", C.c_uint64), ("z1", C.c_uint64), ("z2", C.c_uint64),
+                ("iteration", C.c_uint64)]
+
+
+_P = C.c_void_p
+_u64, _u32 = C.c_uint64, C.c_uint32
+_PP = C.POINTER(C.c_void_p)
+
+_SIGS = {
+    "cb_last_error": (C.c_char_p, []),
+    "cb_version": (C.c_char_p, []),
+    "cb_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "cb_graph_create_from_csr": (C.c_int, [_P, _P, _u64, _u64, C.c_int, _PP]),
+    "cb_graph_generate_rmat": (C.c_int, [_u64, _u64, _u64, C.c_int, _PP]),
+    "cb_graph_info": (C.c_int, [_P, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
+    "cb_graph_download": (C.c_int, [_P, _P, _P]),
+    "cb_graph_destroy": (None, [_P]),
+    "cb_partition_random": (C.c_int, [_P, _u32, _u64, _PP]),
+    "cb_partition_create": (C.c_int, [_P, _P, _u32, _PP]),
+    "cb_partition_download": (C.c_int, [_P, _P]),
+    "cb_partition_destroy": (None, [_P]),
+    "cb_features_synth": (C.c_int, [_P, _P, _u32, C.c_int, _u64, _PP]),
+    "cb_features_info": (C.c_int, [_P, C.POINTER(_u32), C.POINTER(C.c_int), C.POINTER(_u64)]),
+    "cb_features_destroy": (None, [_P]),
+    "cb_plan_create": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _u64, _PP]),
+    "cb_plan_destroy": (None, [_P]),
+    "cb_plan_num_parts": (C.c_int, [_P, C.POINTER(_u32)]),
+    "cb_plan_stream": (C.c_void_p, [_P]),
+    "cb_sample": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched)]),
+    "cb_sample_sync": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched)]),
+    "cb_sample_device": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched)]),
+    "cb_gather": (C.c_int, [_P, _P]),
+    "cb_synchronize": (C.c_int, [_P]),
+    "cb_layer_sizes": (C.c_int, [_P, _u32, C.c_int, _P]),
+    "cb_download_block": (C.c_int, [_P, _u32, C.c_int, _P, _P, _P, _P]),
+    "cb_owner_set_size": (C.c_int, [_P, _u32, C.POINTER(_u64)]),
+    "cb_download_owner_set": (C.c_int, [_P, _u32, _P]),
+    "cb_download_exchange": (C.c_int, [_P, C.c_int, _P, _P, _P, _P]),
+    "cb_download_rows": (C.c_int, [_P, _u32, _P]),
+    "cb_rows_device": (C.c_int, [_P, _u32, _PP, C.POINTER(_u64)]),
+    "cb_plan_launch_count": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_u64)]),
+}
+
+_lib = None
+
+
+def header_symbols() -> list[str]:
+    """Every cb_* entry point declared in include/coopbatch_cuda.h."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(cb_[a-z0-9_]+)\s*\(", txt)))
+
+
+def load() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: the CUDA extension is not built "
+            "(run `python -c 'import __graft_entry__ as g; g.build()'`). "
+            "There is no CPU fallback.")
+    L = C.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L

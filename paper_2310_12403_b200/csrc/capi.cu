@@ -1,0 +1,965 @@
+// libcoopbatch_b200 C-ABI (include/coopbatch_cuda.h) and the C++ orchestrator
+// behind it: handle lifetimes, capacity planning, and the per-batch launch
+// sequence of expand / indep_sample / coop_sample (samplers.cpp:340-354,
+// coop.cpp:68-119) and the fused load_rows + all_to_all_forward gather
+// (coop.cpp:145-159, 378-388). Every launch is asynchronous on the plan's
+// stream; counts stay on the device (LayerMeta) so a batch never waits on the
+// host. Contract violations raise cb::Error(kInput) -> CB_INPUT, mirroring
+// coopbatch::InputError (common.hpp:12-15).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/coopbatch_cuda.h"
+#include "cb_internal.h"
+#include "exchange.h"
+#include "gather.h"
+
+using namespace cb;
+using cbdev::Variates;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return CB_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return CB_INTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CB_INTERNAL;
+  }
+}
+
+struct Arena {
+  std::vector<void*> ptrs;
+  template <typename T>
+  T* alloc(uint64_t count) {
+    void* p = nullptr;
+    CB_CUDA(cudaMalloc(&p, std::max<uint64_t>(count, 1) * sizeof(T) + 64));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+  ~Arena() { release(); }
+};
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    CB_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) CB_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+uint64_t sat_mul(uint64_t a, uint64_t b) {
+  if (a != 0 && b > UINT64_MAX / a) return UINT64_MAX;
+  return a * b;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ handles --
+struct cb_graph {
+  DeviceGraph g;
+  ~cb_graph() {
+    if (g.indptr) cudaFree(g.indptr);
+    if (g.indices) cudaFree(g.indices);
+  }
+};
+
+struct cb_partition {
+  int device = 0;
+  uint64_t n = 0;
+  uint32_t parts = 1;
+  Arena mem;
+  uint32_t* owner = nullptr;    // [n]
+  uint32_t* row_map = nullptr;  // [n] global table row of v (shard-major)
+  uint32_t* members = nullptr;  // [n] vertex of each global row
+  std::vector<uint64_t> shard_off;  // [parts+1]
+};
+
+struct cb_features {
+  int device = 0;
+  uint32_t dim = 0;
+  int dtype = CB_F32;
+  uint64_t row_bytes = 0;
+  uint64_t n_rows = 0;
+  Arena mem;
+  void* table = nullptr;
+  uint32_t* row_map = nullptr;  // nullptr = identity (P = 1)
+};
+
+namespace {
+
+struct PeWork {
+  std::vector<LayerBufs> L;
+  Bitmap bm[2];
+  Sync sync;
+  std::vector<uint32_t*> loc_part, loc_row;  // [layer] cap_src
+  uint32_t* owner_final = nullptr;            // coop: S^L_p
+  uint64_t cap_final = 0;
+  void* rows = nullptr;
+  uint64_t cap_rows = 0;
+  uint64_t rows_row_bytes = 0;
+};
+
+}  // namespace
+
+struct cb_plan {
+  int device = 0;
+  const cb_graph* g = nullptr;
+  const cb_partition* pm = nullptr;
+  uint32_t P = 1;
+  int L = 1;
+  int kind = CB_LABOR0;
+  std::vector<uint32_t> fanouts;
+  uint64_t max_seeds = 0;
+  double grow = 1.0;
+  cudaStream_t stream = nullptr;
+  Arena mem;       // capacity-dependent buffers
+  Arena rows_mem;  // gathered rows
+  std::vector<PeWork> pe;
+  LayerMeta* meta = nullptr;                // [P*(L+1)]
+  unsigned long long* send_counts = nullptr;  // [L*P*P]
+  Variates* var = nullptr;
+  uint32_t* seeds = nullptr;
+  uint64_t seeds_cap = 0;
+  int mode = -1;          // mode of the last batch
+  bool have_batch = false;
+  bool have_rows = false;
+  uint64_t batches = 0;
+  uint64_t launches = 0;  // kernels enqueued by the last cb_sample (+ cb_gather)
+  std::vector<uint64_t> seeds_off;
+
+  LayerMeta* meta_at(uint32_t p, int l) { return meta + p * (L + 1) + l; }
+  bool coop_active() const { return mode == CB_MODE_COOP && P > 1; }
+};
+
+namespace {
+
+void make_bitmap(Arena& a, Bitmap& b, uint64_t n) {
+  b.words = ceil_div(n, 32);
+  b.words_padded = ceil_div(std::max<uint64_t>(b.words, 1), kExtractTileWords) * kExtractTileWords;
+  b.bits = a.alloc<uint32_t>(b.words_padded);
+  b.wprefix = a.alloc<uint32_t>(b.words_padded);
+  CB_CUDA(cudaMemset(b.bits, 0, b.words_padded * sizeof(uint32_t)));
+}
+
+// Capacity plan (host): upper bounds sized from the seeds and fanouts; any
+// overflow is detected on the device and retried with grow *= 2.
+void plan_alloc(cb_plan* pl) {
+  pl->mem.release();
+  pl->rows_mem.release();
+  pl->have_rows = false;
+  const DeviceGraph& g = pl->g->g;
+  const uint64_t n = g.n, m = g.m, maxdeg = std::max<uint64_t>(g.max_degree, 1);
+  const uint32_t P = pl->P;
+  const int L = pl->L;
+  pl->pe.assign(P, PeWork());
+  for (uint32_t p = 0; p < P; ++p) {
+    PeWork& w = pl->pe[p];
+    w.L.resize(L);
+    uint64_t cd = std::max<uint64_t>(pl->max_seeds, 1);
+    uint64_t max_tiles = 2;
+    for (int l = 0; l < L; ++l) {
+      const uint64_t k = pl->fanouts[l];
+      const uint64_t sum_deg = (l == 0) ? sat_mul(cd, maxdeg) : std::min(m, sat_mul(cd, maxdeg));
+      uint64_t est;
+      if (pl->kind == CB_FULL) est = sum_deg;
+      else if (pl->kind == CB_NS) est = sat_mul(cd, k);
+      else est = sat_mul(cd, 2 * k) + 4096;
+      if (pl->kind != CB_FULL) est = static_cast<uint64_t>(std::ceil(est * pl->grow));
+      uint64_t cap_e = std::max<uint64_t>(1, std::min(est, sum_deg));
+      if (pl->kind == CB_NS) cap_e = std::min(cap_e, sat_mul(cd, k));
+      LayerBufs& b = w.L[l];
+      b.cap_dst = cd;
+      b.cap_edges = std::max<uint64_t>(cap_e, 1);
+      b.cap_src = std::min(n, cd + b.cap_edges);
+      if (l == 0) b.dst = nullptr;  // seeds live in pl->seeds
+      else b.dst = pl->mem.alloc<uint32_t>(cd);
+      b.act_di = pl->mem.alloc<uint32_t>(cd);
+      b.act_pre = pl->mem.alloc<uint64_t>(cd + 1);
+      b.out_prefix = pl->kind == CB_NS ? pl->mem.alloc<uint64_t>(cd + 1) : nullptr;
+      b.slots = pl->kind == CB_NS ? pl->mem.alloc<uint32_t>(b.cap_edges) : nullptr;
+      b.edges = pl->mem.alloc<uint2>(b.cap_edges);
+      b.src = pl->mem.alloc<uint32_t>(b.cap_src);
+      b.dst_pos = pl->mem.alloc<uint32_t>(cd);
+      max_tiles = std::max(max_tiles, ceil_div(sum_deg, kLaborTile) + 2);
+      max_tiles = std::max(max_tiles, ceil_div(cd, kFrontierTile) + 2);
+      if (P > 1) {
+        w.loc_part.push_back(pl->mem.alloc<uint32_t>(b.cap_src));
+        w.loc_row.push_back(pl->mem.alloc<uint32_t>(b.cap_src));
+      }
+      // next layer's frontier: indep -> this src; coop -> owner set
+      const uint64_t next = (P > 1) ? std::min(n, sat_mul(P, b.cap_src)) : b.cap_src;
+      cd = std::max(next, b.cap_src);
+    }
+    w.cap_final = cd;
+    w.owner_final = (P > 1) ? pl->mem.alloc<uint32_t>(cd) : nullptr;
+    make_bitmap(pl->mem, w.bm[0], n);
+    make_bitmap(pl->mem, w.bm[1], n);
+    max_tiles = std::max(max_tiles, w.bm[0].words_padded / kExtractTileWords + 2);
+    w.sync.max_tiles = max_tiles;
+    w.sync.epoch = pl->mem.alloc<unsigned>(1);
+    w.sync.tickets = pl->mem.alloc<unsigned>(Sync::kMaxTickets);
+    w.sync.overflow = pl->mem.alloc<unsigned>(1);
+    w.sync.status_a = pl->mem.alloc<unsigned long long>(max_tiles);
+    w.sync.status_b = pl->mem.alloc<unsigned long long>(max_tiles);
+    w.sync.status_c = pl->mem.alloc<unsigned long long>(max_tiles);
+    CB_CUDA(cudaMemset(w.sync.epoch, 0, sizeof(unsigned)));
+    CB_CUDA(cudaMemset(w.sync.status_a, 0, max_tiles * 8));
+    CB_CUDA(cudaMemset(w.sync.status_b, 0, max_tiles * 8));
+    CB_CUDA(cudaMemset(w.sync.status_c, 0, max_tiles * 8));
+  }
+  pl->meta = pl->mem.alloc<LayerMeta>(static_cast<uint64_t>(P) * (L + 1));
+  CB_CUDA(cudaMemset(pl->meta, 0, sizeof(LayerMeta) * P * (L + 1)));
+  pl->send_counts = pl->mem.alloc<unsigned long long>(static_cast<uint64_t>(L) * P * P);
+  pl->var = pl->mem.alloc<Variates>(1);
+  pl->seeds_cap = static_cast<uint64_t>(P) * std::max<uint64_t>(pl->max_seeds, 1);
+  pl->seeds = pl->mem.alloc<uint32_t>(pl->seeds_cap);
+  pl->have_batch = false;
+  CB_CUDA(cudaDeviceSynchronize());
+}
+
+Variates make_variates(const cb_sched* s) {
+  // VariateSource::from_schedule (samplers.hpp:75-93): cos/sin on the host,
+  // exact 1/0 at the endpoints.
+  Variates v{};
+  v.z1 = s->z1;
+  v.z2 = s->z2;
+  double c = 0.0;
+  if (s->kappa != cbdev::kKappaInf)
+    c = static_cast<double>(s->iteration % s->kappa) / static_cast<double>(s->kappa);
+  v.smoothed = (s->kappa != cbdev::kKappaInf && s->kappa >= 2) ? 1 : 0;
+  if (c == 0.0) {
+    v.cos_c = 1.0;
+    v.sin_c = 0.0;
+  } else if (c == 1.0) {
+    v.cos_c = 0.0;
+    v.sin_c = 1.0;
+  } else {
+    const double angle = c * 1.5707963267948966192;
+    v.cos_c = std::cos(angle);
+    v.sin_c = std::sin(angle);
+  }
+  return v;
+}
+
+void check_seeds_host(const cb_plan* pl, const uint32_t* flat, const uint64_t* off) {
+  const uint64_t n = pl->g->g.n;
+  for (uint32_t p = 0; p < pl->P; ++p) {
+    require(off[p + 1] >= off[p], "seed offsets must be nondecreasing");
+    require(off[p + 1] - off[p] <= pl->max_seeds,
+            "part " + std::to_string(p) + " has more seeds than the plan's max_seeds_per_part");
+    for (uint64_t i = off[p]; i < off[p + 1]; ++i)
+      require(flat[i] < n, "vertex id " + std::to_string(flat[i]) + " out of range [0, " +
+                               std::to_string(n) + ")");
+  }
+}
+
+void check_ownership_host(const cb_plan* pl, const uint32_t* flat, const uint64_t* off) {
+  // coop_sample: every seed must be owned by its claimed part (coop.cpp:75-81)
+  if (pl->P <= 1) return;
+  const uint64_t total = off[pl->P];
+  std::vector<uint32_t> owners(total);
+  std::vector<uint32_t> seeds(flat, flat + total);
+  // gather owner[seed] on the device: tiny (one value per seed)
+  uint32_t* d_ids = nullptr;
+  uint32_t* d_out = nullptr;
+  CB_CUDA(cudaMalloc(&d_ids, total * 4 + 4));
+  CB_CUDA(cudaMalloc(&d_out, total * 4 + 4));
+  CB_CUDA(cudaMemcpy(d_ids, seeds.data(), total * 4, cudaMemcpyHostToDevice));
+  // reuse the feature gather kernel with a 4-byte "row" = owner[v]
+  unsigned long long* d_cnt = nullptr;
+  CB_CUDA(cudaMalloc(&d_cnt, 8));
+  const unsigned long long t = total;
+  CB_CUDA(cudaMemcpy(d_cnt, &t, 8, cudaMemcpyHostToDevice));
+  launch_gather(pl->pm->owner, 4, 4, d_ids, d_cnt, total, nullptr, d_out, pl->stream);
+  CB_CUDA(cudaStreamSynchronize(pl->stream));
+  CB_CUDA(cudaMemcpy(owners.data(), d_out, total * 4, cudaMemcpyDeviceToHost));
+  cudaFree(d_ids);
+  cudaFree(d_out);
+  cudaFree(d_cnt);
+  for (uint32_t p = 0; p < pl->P; ++p)
+    for (uint64_t i = off[p]; i < off[p + 1]; ++i)
+      require(owners[i] == p, "coop_sample: seed " + std::to_string(flat[i]) +
+                                  " is not owned by part " + std::to_string(p));
+}
+
+// The per-batch launch sequence. d_seeds: P seed lists back to back (device).
+void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_t* off,
+                   const cb_sched* sched) {
+  const DeviceGraph& g = pl->g->g;
+  const uint32_t P = pl->P;
+  const int L = pl->L;
+  cudaStream_t st = pl->stream;
+  uint64_t launches = 0;
+  const Variates v = make_variates(sched);
+  CB_CUDA(cudaMemcpyAsync(pl->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+  pl->mode = mode;
+  pl->seeds_off.assign(off, off + P + 1);
+  if (++pl->batches % (1u << 17) == 0) {  // epoch wrap guard (18-bit epochs)
+    for (auto& w : pl->pe) {
+      CB_CUDA(cudaMemsetAsync(w.sync.status_a, 0, w.sync.max_tiles * 8, st));
+      CB_CUDA(cudaMemsetAsync(w.sync.status_b, 0, w.sync.max_tiles * 8, st));
+      CB_CUDA(cudaMemsetAsync(w.sync.status_c, 0, w.sync.max_tiles * 8, st));
+    }
+  }
+  for (uint32_t p = 0; p < P; ++p) {
+    launch_batch_begin(pl->pe[p].sync, pl->meta_at(p, 0), L + 1, off[p + 1] - off[p], st);
+    ++launches;
+  }
+  const bool coop = (mode == CB_MODE_COOP) && P > 1;
+  const bool ns = pl->kind == CB_NS;
+
+  if (!coop) {
+    for (uint32_t p = 0; p < P; ++p) {
+      PeWork& w = pl->pe[p];
+      for (int l = 0; l < L; ++l) {
+        LayerBufs b = w.L[l];
+        if (l == 0) {
+          b.dst = const_cast<uint32_t*>(d_seeds) + off[p];
+        } else {
+          b.dst = w.L[l - 1].src;
+          b.cap_dst = w.L[l - 1].cap_src;
+        }
+        LayerMeta* me = pl->meta_at(p, l);
+        Bitmap& set_bm = w.bm[l & 1];
+        launch_frontier(g, b, me, pl->kind, pl->fanouts[l], set_bm,
+                        l > 0 ? &w.bm[(l - 1) & 1] : nullptr, w.sync, 4 * l, 8 * l, st);
+        if (ns) {
+          launch_ns(g, b, me, pl->fanouts[l], l, pl->var, set_bm, st);
+          launches += 2;
+        } else {
+          launch_labor(g, b, me, pl->kind, pl->fanouts[l], l, pl->var, set_bm, w.sync,
+                       4 * l + 1, 8 * l + 3, st);
+          ++launches;
+        }
+        launch_extract(set_bm, b.src, b.cap_src, &me->n_src,
+                       l + 1 <= L ? &pl->meta_at(p, l + 1)->n_dst : nullptr, w.sync,
+                       4 * l + 2, 8 * l + 4, st);
+        launch_relabel(set_bm, b, me, st);
+        launches += 3;
+      }
+      launch_clear(w.bm[(L - 1) & 1], w.L[L - 1].src, &pl->meta_at(p, L - 1)->n_src, st);
+      ++launches;
+    }
+  } else {
+    CB_CUDA(cudaMemsetAsync(pl->send_counts, 0, sizeof(unsigned long long) * L * P * P, st));
+    for (int l = 0; l < L; ++l) {
+      uint64_t max_src = 1;
+      for (uint32_t p = 0; p < P; ++p) {
+        PeWork& w = pl->pe[p];
+        LayerBufs b = w.L[l];
+        if (l == 0) b.dst = const_cast<uint32_t*>(d_seeds) + off[p];
+        LayerMeta* me = pl->meta_at(p, l);
+        launch_frontier(g, b, me, pl->kind, pl->fanouts[l], w.bm[0], l > 0 ? &w.bm[1] : nullptr,
+                        w.sync, 4 * l, 8 * l, st);
+        if (ns) {
+          launch_ns(g, b, me, pl->fanouts[l], l, pl->var, w.bm[0], st);
+          launches += 2;
+        } else {
+          launch_labor(g, b, me, pl->kind, pl->fanouts[l], l, pl->var, w.bm[0], w.sync,
+                       4 * l + 1, 8 * l + 3, st);
+          ++launches;
+        }
+        launch_extract(w.bm[0], b.src, b.cap_src, &me->n_src, nullptr, w.sync, 4 * l + 2,
+                       8 * l + 4, st);
+        launch_relabel(w.bm[0], b, me, st);
+        launches += 3;
+        max_src = std::max(max_src, b.cap_src);
+      }
+      PartPtrs pp{};
+      for (uint32_t p = 0; p < P; ++p) {
+        PeWork& w = pl->pe[p];
+        pp.src[p] = w.L[l].src;
+        pp.count[p] = &pl->meta_at(p, l)->n_src;
+        pp.clear_bits[p] = w.bm[0].bits;
+        pp.xbits[p] = w.bm[1].bits;
+        pp.xprefix[p] = w.bm[1].wprefix;
+        pp.loc_part[p] = w.loc_part[l];
+        pp.loc_row[p] = w.loc_row[l];
+      }
+      launch_route(pp, pl->pm->owner, P,
+                   pl->send_counts + static_cast<uint64_t>(l) * P * P, max_src, st);
+      ++launches;
+      for (uint32_t q = 0; q < P; ++q) {
+        PeWork& w = pl->pe[q];
+        uint32_t* next = (l + 1 < L) ? w.L[l + 1].dst : w.owner_final;
+        const uint64_t cap = (l + 1 < L) ? w.L[l + 1].cap_dst : w.cap_final;
+        launch_extract(w.bm[1], next, cap, &pl->meta_at(q, l + 1)->n_dst, nullptr, w.sync,
+                       4 * l + 3, 8 * l + 5, st);
+        ++launches;
+      }
+      launch_locate(pp, pl->pm->owner, P, max_src, st);
+      ++launches;
+    }
+    for (uint32_t q = 0; q < P; ++q) {
+      PeWork& w = pl->pe[q];
+      launch_clear(w.bm[1], w.owner_final, &pl->meta_at(q, L)->n_dst, st);
+      ++launches;
+    }
+  }
+  pl->launches = launches;
+  pl->have_batch = true;
+  pl->have_rows = false;
+}
+
+void check_overflow(cb_plan* pl) {
+  CB_CUDA(cudaStreamSynchronize(pl->stream));
+  for (auto& w : pl->pe) {
+    unsigned o = 0;
+    CB_CUDA(cudaMemcpy(&o, w.sync.overflow, 4, cudaMemcpyDeviceToHost));
+    if (o) throw Error(kOverflow, "capacity bound exceeded on device (retry with larger plan)");
+  }
+}
+
+void sample_host(cb_plan* pl, int mode, const uint32_t* flat, const uint64_t* off,
+                 const cb_sched* sched) {
+  require(mode == CB_MODE_COOP || mode == CB_MODE_INDEP, "unknown sampling mode");
+  require(sched != nullptr, "null schedule");
+  require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
+  check_seeds_host(pl, flat, off);
+  if (mode == CB_MODE_COOP) check_ownership_host(pl, flat, off);
+  const uint64_t total = off[pl->P];
+  if (total)
+    CB_CUDA(cudaMemcpyAsync(pl->seeds, flat, total * 4, cudaMemcpyHostToDevice, pl->stream));
+  enqueue_batch(pl, mode, pl->seeds, off, sched);
+}
+
+const LayerMeta host_meta(cb_plan* pl, uint32_t p, int l) {
+  LayerMeta m{};
+  CB_CUDA(cudaStreamSynchronize(pl->stream));
+  CB_CUDA(cudaMemcpy(&m, pl->meta_at(p, l), sizeof(LayerMeta), cudaMemcpyDeviceToHost));
+  return m;
+}
+
+void require_batch(const cb_plan* pl, uint32_t p, int l) {
+  require(pl->have_batch, "no sampled batch in this plan");
+  require(p < pl->P, "part index out of range");
+  require(l >= 0 && l < pl->L, "layer index out of range");
+}
+
+}  // namespace
+
+// ===================================================================== C-ABI ==
+extern "C" {
+
+const char* cb_last_error(void) { return g_err.c_str(); }
+const char* cb_version(void) { return "coopbatch_b200 0.1 (sm_100a)"; }
+
+int cb_device_count(int* out) {
+  return guard([&] { CB_CUDA(cudaGetDeviceCount(out)); });
+}
+
+int cb_graph_create_from_csr(const uint64_t* indptr, const uint32_t* indices, uint64_t n,
+                             uint64_t m, int device, cb_graph** out) {
+  return guard([&] {
+    require(indptr != nullptr && (m == 0 || indices != nullptr), "null CSR arrays");
+    require(n < (1ULL << 32), "vertex ids must fit 32 bits");
+    // validate_csr (graph.cpp:267-284)
+    require(indptr[0] == 0, "csr: indptr[0] != 0");
+    require(indptr[n] == m, "csr: indptr[n] != num edges");
+    for (uint64_t v = 0; v < n; ++v)
+      require(indptr[v] <= indptr[v + 1],
+              "csr: indptr not nondecreasing at " + std::to_string(v));
+    for (uint64_t e = 0; e < m; ++e) require(indices[e] < n, "csr: index out of range");
+    DeviceGuard dg(device);
+    auto h = std::make_unique<cb_graph>();
+    h->g.device = device;
+    h->g.n = n;
+    h->g.m = m;
+    CB_CUDA(cudaMalloc(&h->g.indptr, (n + 1) * 8));
+    CB_CUDA(cudaMalloc(&h->g.indices, std::max<uint64_t>(m, 1) * 4));
+    CB_CUDA(cudaMemcpy(h->g.indptr, indptr, (n + 1) * 8, cudaMemcpyHostToDevice));
+    if (m) CB_CUDA(cudaMemcpy(h->g.indices, indices, m * 4, cudaMemcpyHostToDevice));
+    uint64_t md = 0;
+    for (uint64_t v = 0; v < n; ++v) md = std::max(md, indptr[v + 1] - indptr[v]);
+    h->g.max_degree = md;
+    *out = h.release();
+  });
+}
+
+int cb_graph_generate_rmat(uint64_t n, uint64_t m, uint64_t seed, int device, cb_graph** out) {
+  return guard([&] {
+    DeviceGuard dg(device);
+    auto h = std::make_unique<cb_graph>();
+    h->g.device = device;
+    cudaStream_t st;
+    CB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+      graph_generate_rmat(h->g, n, m, seed, st);
+    } catch (...) {
+      cudaStreamDestroy(st);
+      throw;
+    }
+    CB_CUDA(cudaStreamDestroy(st));
+    *out = h.release();
+  });
+}
+
+int cb_graph_info(const cb_graph* g, uint64_t* n, uint64_t* m, uint64_t* max_degree) {
+  return guard([&] {
+    require(g != nullptr, "null graph");
+    if (n) *n = g->g.n;
+    if (m) *m = g->g.m;
+    if (max_degree) *max_degree = g->g.max_degree;
+  });
+}
+
+int cb_graph_download(const cb_graph* g, uint64_t* indptr, uint32_t* indices) {
+  return guard([&] {
+    require(g != nullptr, "null graph");
+    DeviceGuard dg(g->g.device);
+    if (indptr)
+      CB_CUDA(cudaMemcpy(indptr, g->g.indptr, (g->g.n + 1) * 8, cudaMemcpyDeviceToHost));
+    if (indices && g->g.m)
+      CB_CUDA(cudaMemcpy(indices, g->g.indices, g->g.m * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+void cb_graph_destroy(cb_graph* g) {
+  if (!g) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(g->g.device);
+  delete g;
+  cudaSetDevice(prev);
+}
+
+static void finish_partition(cb_partition* pm) {
+  // members = vertices grouped by owner, ascending within a part (part_members,
+  // partition.cpp:99-105); row_map[v] = global row of v. Stable key sort.
+  const uint64_t n = pm->n;
+  pm->row_map = pm->mem.alloc<uint32_t>(n);
+  pm->members = pm->mem.alloc<uint32_t>(n);
+  uint32_t* keys2 = pm->mem.alloc<uint32_t>(n);
+  uint32_t* ids = pm->mem.alloc<uint32_t>(n);
+  cudaStream_t st;
+  CB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  std::vector<uint32_t> iota(n);
+  for (uint64_t v = 0; v < n; ++v) iota[v] = static_cast<uint32_t>(v);
+  CB_CUDA(cudaMemcpy(ids, iota.data(), n * 4, cudaMemcpyHostToDevice));
+  uint32_t* keys = pm->mem.alloc<uint32_t>(n);
+  CB_CUDA(cudaMemcpy(keys, pm->owner, n * 4, cudaMemcpyDeviceToDevice));
+  int bits = 1;
+  while ((1u << bits) < pm->parts) ++bits;
+  cub::DoubleBuffer<uint32_t> kb(keys, keys2), vb(ids, pm->members);
+  size_t tmp_bytes = 0;
+  CB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, (int64_t)n, 0, bits, st));
+  void* tmp = nullptr;
+  CB_CUDA(cudaMalloc(&tmp, tmp_bytes + 16));
+  CB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, (int64_t)n, 0, bits, st));
+  CB_CUDA(cudaStreamSynchronize(st));
+  cudaFree(tmp);
+  std::vector<uint32_t> members(n), sorted_keys(n);
+  CB_CUDA(cudaMemcpy(members.data(), vb.Current(), n * 4, cudaMemcpyDeviceToHost));
+  CB_CUDA(cudaMemcpy(sorted_keys.data(), kb.Current(), n * 4, cudaMemcpyDeviceToHost));
+  pm->shard_off.assign(pm->parts + 1, 0);
+  for (uint64_t i = 0; i < n; ++i) pm->shard_off[sorted_keys[i] + 1]++;
+  for (uint32_t q = 0; q < pm->parts; ++q) pm->shard_off[q + 1] += pm->shard_off[q];
+  std::vector<uint32_t> row_map(n);
+  for (uint64_t i = 0; i < n; ++i) row_map[members[i]] = static_cast<uint32_t>(i);
+  CB_CUDA(cudaMemcpy(pm->members, members.data(), n * 4, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpy(pm->row_map, row_map.data(), n * 4, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaStreamDestroy(st));
+}
+
+int cb_partition_random(const cb_graph* g, uint32_t parts, uint64_t seed, cb_partition** out) {
+  return guard([&] {
+    require(g != nullptr, "null graph");
+    require(parts >= 1, "partition_random: parts must be >= 1");
+    require(parts <= kMaxParts, "at most 16 parts per device");
+    DeviceGuard dg(g->g.device);
+    auto pm = std::make_unique<cb_partition>();
+    pm->device = g->g.device;
+    pm->n = g->g.n;
+    pm->parts = parts;
+    pm->owner = pm->mem.alloc<uint32_t>(pm->n);
+    partition_random_device(pm->n, parts, seed, pm->owner, nullptr);
+    CB_CUDA(cudaDeviceSynchronize());
+    finish_partition(pm.get());
+    *out = pm.release();
+  });
+}
+
+int cb_partition_create(const cb_graph* g, const uint32_t* owner, uint32_t parts,
+                        cb_partition** out) {
+  return guard([&] {
+    require(g != nullptr && owner != nullptr, "null argument");
+    require(parts >= 1, "partition: zero parts");
+    require(parts <= kMaxParts, "at most 16 parts per device");
+    for (uint64_t v = 0; v < g->g.n; ++v)
+      require(owner[v] < parts, "partition: owner id out of range");
+    DeviceGuard dg(g->g.device);
+    auto pm = std::make_unique<cb_partition>();
+    pm->device = g->g.device;
+    pm->n = g->g.n;
+    pm->parts = parts;
+    pm->owner = pm->mem.alloc<uint32_t>(pm->n);
+    CB_CUDA(cudaMemcpy(pm->owner, owner, pm->n * 4, cudaMemcpyHostToDevice));
+    finish_partition(pm.get());
+    *out = pm.release();
+  });
+}
+
+int cb_partition_download(const cb_partition* pm, uint32_t* owner) {
+  return guard([&] {
+    require(pm != nullptr && owner != nullptr, "null argument");
+    DeviceGuard dg(pm->device);
+    CB_CUDA(cudaMemcpy(owner, pm->owner, pm->n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+void cb_partition_destroy(cb_partition* pm) {
+  if (!pm) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(pm->device);
+  delete pm;
+  cudaSetDevice(prev);
+}
+
+int cb_features_synth(const cb_graph* g, const cb_partition* pm, uint32_t dim, int dtype,
+                      uint64_t seed, cb_features** out) {
+  return guard([&] {
+    require(g != nullptr, "null graph");
+    require(dim >= 1, "feature dim must be >= 1");
+    require(dtype == CB_F64 || dtype == CB_F32 || dtype == CB_F16, "unknown dtype");
+    require(pm == nullptr || pm->n == g->g.n, "partition does not cover the graph");
+    DeviceGuard dg(g->g.device);
+    auto f = std::make_unique<cb_features>();
+    f->device = g->g.device;
+    f->dim = dim;
+    f->dtype = dtype;
+    const uint64_t es = dtype == CB_F64 ? 8 : (dtype == CB_F32 ? 4 : 2);
+    f->row_bytes = es * dim;
+    f->n_rows = g->g.n;
+    f->table = f->mem.alloc<unsigned char>(f->n_rows * f->row_bytes);
+    const bool sharded = pm != nullptr && pm->parts > 1;
+    if (sharded) {
+      f->row_map = f->mem.alloc<uint32_t>(g->g.n);
+      CB_CUDA(cudaMemcpy(f->row_map, pm->row_map, g->g.n * 4, cudaMemcpyDeviceToDevice));
+    }
+    launch_synth(seed, dim, dtype, f->n_rows, sharded ? pm->members : nullptr, 0, f->table,
+                 nullptr);
+    CB_CUDA(cudaDeviceSynchronize());
+    *out = f.release();
+  });
+}
+
+int cb_features_info(const cb_features* f, uint32_t* dim, int* dtype, uint64_t* row_bytes) {
+  return guard([&] {
+    require(f != nullptr, "null features");
+    if (dim) *dim = f->dim;
+    if (dtype) *dtype = f->dtype;
+    if (row_bytes) *row_bytes = f->row_bytes;
+  });
+}
+
+void cb_features_destroy(cb_features* f) {
+  if (!f) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(f->device);
+  delete f;
+  cudaSetDevice(prev);
+}
+
+int cb_plan_create(const cb_graph* g, const cb_partition* pm, int num_layers, int kind,
+                   const uint32_t* fanouts, uint64_t max_seeds_per_part, cb_plan** out) {
+  return guard([&] {
+    require(g != nullptr, "null graph");
+    require(num_layers >= 1, "expand: num_layers must be >= 1");
+    require(num_layers <= 8, "at most 8 layers");
+    require(kind == CB_FULL || kind == CB_NS || kind == CB_LABOR0,
+            "sample_block: unknown sampler kind");
+    require(fanouts != nullptr || kind == CB_FULL, "null fanouts");
+    require(pm == nullptr || pm->n == g->g.n, "partition does not cover the graph");
+    DeviceGuard dg(g->g.device);
+    auto pl = std::make_unique<cb_plan>();
+    pl->device = g->g.device;
+    pl->g = g;
+    pl->pm = pm;
+    pl->P = pm ? pm->parts : 1;
+    pl->L = num_layers;
+    pl->kind = kind;
+    for (int l = 0; l < num_layers; ++l) {
+      const uint32_t k = fanouts ? fanouts[l] : 1;
+      if (kind != CB_FULL)
+        require(k >= 1, kind == CB_NS ? "sample_ns: fanout must be >= 1"
+                                      : "sample_labor0: fanout must be >= 1");
+      pl->fanouts.push_back(k);
+    }
+    pl->max_seeds = std::max<uint64_t>(max_seeds_per_part, 1);
+    CB_CUDA(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
+    plan_alloc(pl.get());
+    *out = pl.release();
+  });
+}
+
+void cb_plan_destroy(cb_plan* plan) {
+  if (!plan) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(plan->device);
+  cudaStreamSynchronize(plan->stream);
+  cudaStreamDestroy(plan->stream);
+  delete plan;
+  cudaSetDevice(prev);
+}
+
+int cb_plan_num_parts(const cb_plan* plan, uint32_t* parts) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    *parts = plan->P;
+  });
+}
+
+void* cb_plan_stream(const cb_plan* plan) { return plan ? plan->stream : nullptr; }
+
+int cb_sample(cb_plan* plan, int mode, const uint32_t* seeds_flat, const uint64_t* seeds_off,
+              const cb_sched* sched) {
+  return guard([&] {
+    require(plan != nullptr && seeds_off != nullptr, "null argument");
+    DeviceGuard dg(plan->device);
+    sample_host(plan, mode, seeds_flat, seeds_off, sched);
+  });
+}
+
+int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
+                   const uint64_t* seeds_off, const cb_sched* sched) {
+  return guard([&] {
+    require(plan != nullptr && seeds_off != nullptr, "null argument");
+    DeviceGuard dg(plan->device);
+    for (int attempt = 0;; ++attempt) {
+      sample_host(plan, mode, seeds_flat, seeds_off, sched);
+      try {
+        check_overflow(plan);
+        return;
+      } catch (const Error& e) {
+        if (e.code != kOverflow || attempt >= 12) throw;
+        plan->grow *= 2.0;
+        plan_alloc(plan);
+      }
+    }
+  });
+}
+
+int cb_sample_device(cb_plan* plan, int mode, const uint32_t* d_seeds_flat,
+                     const uint64_t* seeds_off, const cb_sched* sched) {
+  return guard([&] {
+    require(plan != nullptr && seeds_off != nullptr && sched != nullptr, "null argument");
+    require(mode == CB_MODE_COOP || mode == CB_MODE_INDEP, "unknown sampling mode");
+    for (uint32_t p = 0; p < plan->P; ++p)
+      require(seeds_off[p + 1] - seeds_off[p] <= plan->max_seeds,
+              "more seeds than the plan's max_seeds_per_part");
+    DeviceGuard dg(plan->device);
+    enqueue_batch(plan, mode, d_seeds_flat, seeds_off, sched);
+  });
+}
+
+int cb_gather(cb_plan* plan, const cb_features* f) {
+  return guard([&] {
+    require(plan != nullptr && f != nullptr, "null argument");
+    require(plan->have_batch, "no sampled batch in this plan");
+    require(f->n_rows == plan->g->g.n, "feature table does not match the graph");
+    require(plan->P == 1 || f->row_map != nullptr,
+            "multi-part plan needs a feature table sharded by the same partition");
+    DeviceGuard dg(plan->device);
+    const int vb = vec_bytes_for(f->row_bytes);
+    for (uint32_t p = 0; p < plan->P; ++p) {
+      PeWork& w = plan->pe[p];
+      const LayerBufs& b = w.L[plan->L - 1];
+      if (!w.rows || w.rows_row_bytes != f->row_bytes || w.cap_rows < b.cap_src) {
+        w.rows = plan->rows_mem.alloc<unsigned char>(b.cap_src * f->row_bytes);
+        w.cap_rows = b.cap_src;
+        w.rows_row_bytes = f->row_bytes;
+      }
+      launch_gather(f->table, vb, f->row_bytes, b.src, &plan->meta_at(p, plan->L - 1)->n_src,
+                    w.cap_rows, f->row_map, w.rows, plan->stream);
+      plan->launches += 1;
+    }
+    plan->have_rows = true;
+  });
+}
+
+int cb_synchronize(cb_plan* plan) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    DeviceGuard dg(plan->device);
+    check_overflow(plan);
+  });
+}
+
+int cb_layer_sizes(cb_plan* plan, uint32_t part, int layer, uint64_t* sizes) {
+  return guard([&] {
+    require(plan != nullptr && sizes != nullptr, "null argument");
+    require_batch(plan, part, layer);
+    DeviceGuard dg(plan->device);
+    const LayerMeta m = host_meta(plan, part, layer);
+    sizes[0] = m.n_dst;
+    sizes[1] = m.n_src;
+    sizes[2] = m.n_edges;
+    sizes[3] = m.uncertified;
+    sizes[4] = m.scan_total;
+    sizes[5] = m.n_active;
+  });
+}
+
+int cb_download_block(cb_plan* plan, uint32_t part, int layer, uint32_t* dst, uint32_t* src,
+                      uint32_t* edges, uint32_t* dst_pos) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require_batch(plan, part, layer);
+    DeviceGuard dg(plan->device);
+    check_overflow(plan);
+    const LayerMeta m = host_meta(plan, part, layer);
+    PeWork& w = plan->pe[part];
+    const uint32_t* d_dst;
+    if (layer == 0) d_dst = plan->seeds + plan->seeds_off[part];
+    else if (!plan->coop_active()) d_dst = w.L[layer - 1].src;
+    else d_dst = w.L[layer].dst;
+    const LayerBufs& b = w.L[layer];
+    if (dst && m.n_dst) CB_CUDA(cudaMemcpy(dst, d_dst, m.n_dst * 4, cudaMemcpyDeviceToHost));
+    if (src && m.n_src) CB_CUDA(cudaMemcpy(src, b.src, m.n_src * 4, cudaMemcpyDeviceToHost));
+    if (edges && m.n_edges)
+      CB_CUDA(cudaMemcpy(edges, b.edges, m.n_edges * 8, cudaMemcpyDeviceToHost));
+    if (dst_pos && m.n_dst)
+      CB_CUDA(cudaMemcpy(dst_pos, b.dst_pos, m.n_dst * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int cb_owner_set_size(cb_plan* plan, uint32_t part, uint64_t* n) {
+  return guard([&] {
+    require(plan != nullptr && n != nullptr, "null argument");
+    require_batch(plan, part, 0);
+    DeviceGuard dg(plan->device);
+    if (plan->coop_active()) *n = host_meta(plan, part, plan->L).n_dst;
+    else *n = host_meta(plan, part, plan->L - 1).n_src;
+  });
+}
+
+int cb_download_owner_set(cb_plan* plan, uint32_t part, uint32_t* ids) {
+  return guard([&] {
+    require(plan != nullptr && ids != nullptr, "null argument");
+    require_batch(plan, part, 0);
+    require(plan->mode == CB_MODE_COOP, "owner sets exist only for cooperative batches");
+    DeviceGuard dg(plan->device);
+    check_overflow(plan);
+    PeWork& w = plan->pe[part];
+    if (plan->coop_active()) {
+      const uint64_t n = host_meta(plan, part, plan->L).n_dst;
+      if (n) CB_CUDA(cudaMemcpy(ids, w.owner_final, n * 4, cudaMemcpyDeviceToHost));
+    } else {  // P = 1: the owner set is the last src list (coop.cpp:44-51)
+      const uint64_t n = host_meta(plan, part, plan->L - 1).n_src;
+      if (n) CB_CUDA(cudaMemcpy(ids, w.L[plan->L - 1].src, n * 4, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int cb_download_exchange(cb_plan* plan, int layer, uint64_t* send_counts,
+                         uint64_t* owner_row_counts, uint32_t* loc_part, uint64_t* loc_row) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require_batch(plan, 0, layer);
+    require(plan->mode == CB_MODE_COOP, "exchange records exist only for cooperative batches");
+    DeviceGuard dg(plan->device);
+    check_overflow(plan);
+    const uint32_t P = plan->P;
+    if (!plan->coop_active()) {  // P = 1: everything stays local
+      const LayerMeta m = host_meta(plan, 0, layer);
+      if (send_counts) send_counts[0] = m.n_src;
+      if (owner_row_counts) owner_row_counts[0] = m.n_src;
+      for (uint64_t j = 0; j < m.n_src; ++j) {
+        if (loc_part) loc_part[j] = 0;
+        if (loc_row) loc_row[j] = j;
+      }
+      return;
+    }
+    std::vector<unsigned long long> sc(static_cast<size_t>(P) * P);
+    CB_CUDA(cudaMemcpy(sc.data(), plan->send_counts + static_cast<uint64_t>(layer) * P * P,
+                       sc.size() * 8, cudaMemcpyDeviceToHost));
+    if (send_counts)
+      for (size_t i = 0; i < sc.size(); ++i) send_counts[i] = sc[i];
+    if (owner_row_counts)
+      for (uint32_t q = 0; q < P; ++q)
+        owner_row_counts[q] = host_meta(plan, q, layer + 1).n_dst;
+    uint64_t o = 0;
+    for (uint32_t p = 0; p < P; ++p) {
+      const uint64_t n = host_meta(plan, p, layer).n_src;
+      if (loc_part && n)
+        CB_CUDA(cudaMemcpy(loc_part + o, plan->pe[p].loc_part[layer], n * 4,
+                           cudaMemcpyDeviceToHost));
+      if (loc_row && n) {
+        std::vector<uint32_t> tmp(n);
+        CB_CUDA(cudaMemcpy(tmp.data(), plan->pe[p].loc_row[layer], n * 4,
+                           cudaMemcpyDeviceToHost));
+        for (uint64_t j = 0; j < n; ++j) loc_row[o + j] = tmp[j];
+      }
+      o += n;
+    }
+  });
+}
+
+int cb_download_rows(cb_plan* plan, uint32_t part, void* out) {
+  return guard([&] {
+    require(plan != nullptr && out != nullptr, "null argument");
+    require(plan->have_rows, "no gathered rows (call cb_gather)");
+    require(part < plan->P, "part index out of range");
+    DeviceGuard dg(plan->device);
+    check_overflow(plan);
+    const uint64_t n = host_meta(plan, part, plan->L - 1).n_src;
+    PeWork& w = plan->pe[part];
+    if (n)
+      CB_CUDA(cudaMemcpy(out, w.rows, n * w.rows_row_bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+int cb_rows_device(cb_plan* plan, uint32_t part, void** ptr, uint64_t* rows) {
+  return guard([&] {
+    require(plan != nullptr && ptr != nullptr, "null argument");
+    require(plan->have_rows, "no gathered rows (call cb_gather)");
+    require(part < plan->P, "part index out of range");
+    DeviceGuard dg(plan->device);
+    *ptr = plan->pe[part].rows;
+    if (rows) *rows = host_meta(plan, part, plan->L - 1).n_src;
+  });
+}
+
+int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n) {
+  return guard([&] {
+    require(plan != nullptr && n != nullptr, "null argument");
+    const uint64_t per_layer = (plan->kind == CB_NS) ? 5 : 4;
+    const uint64_t P = plan->P;
+    const uint64_t L = plan->L;
+    uint64_t k;
+    if (mode == CB_MODE_COOP && P > 1)
+      k = P + L * (P * per_layer + 1 + P + 1) + P;
+    else
+      k = P + P * (L * per_layer + 1);
+    if (with_gather) k += P;
+    *n = k;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,259 @@
+// Device-side building blocks shared by every kernel of the coopbatch B200
+// path: the reference's counter-based hash (rng.hpp:17-48), its FP64 normal
+// CDF / quantile (rng.cpp:7-52), warp/block scans, and a decoupled look-back
+// tile prefix so every compaction in the path is single-pass and keeps the
+// reference's element order.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cbdev {
+
+constexpr uint64_t kSalt = 0x736f6d6570736575ULL;  // rng.hpp:24
+constexpr uint64_t kKappaInf = ~0ULL;               // rng.hpp:70-71
+constexpr int kNumSMs = 148;
+
+// rng.hpp:17-22 — SplitMix64 finalizer. Integer-only: bit-identical on device.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t hinit(uint64_t seed) { return mix64(seed ^ kSalt); }
+__host__ __device__ __forceinline__ uint64_t hstep(uint64_t h, uint64_t id) { return mix64(h ^ id); }
+// rng.hpp:42-44; (bits>>11) < 2^53 converts exactly, the 2^-53 scale is exact.
+__host__ __device__ __forceinline__ double ufb(uint64_t bits) {
+  return static_cast<double>(bits >> 11) * 0x1.0p-53;
+}
+
+// ---- FP64 phi / inverse_phi (rng.cpp:7-52) ---------------------------------
+// Same constants and evaluation order as the reference; explicit _rn
+// intrinsics keep nvcc from contracting into FMA (the reference's x86-64
+// build has no FMA). libdevice erfc/log/log1p/exp may differ from glibc by
+// an ulp; labor/ns kernels count decisions within kGuard of the threshold
+// ("uncertified") and report them (DESIGN.md §Smoothed variates).
+__device__ __forceinline__ double dphi(double x) {
+  return __dmul_rn(0.5, erfc(__dmul_rn(-x, 0.7071067811865475244)));
+}
+
+__device__ __forceinline__ double horner6(const double* c, double q) {
+  double v = c[0];
+#pragma unroll
+  for (int i = 1; i < 6; ++i) v = __dadd_rn(__dmul_rn(v, q), c[i]);
+  return v;
+}
+
+__device__ inline double dinverse_phi(double p) {
+  const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02,
+                      -2.759285104469687e+02, 1.383577518672690e+02,
+                      -3.066479806614716e+01, 2.506628277459239e+00};
+  const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02,
+                      -1.556989798598866e+02, 6.680131188771972e+01,
+                      -1.328068155288572e+01, 1.0};
+  const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01,
+                      -2.400758277161838e+00, -2.549732539343734e+00,
+                      4.374664141464968e+00,  2.938163982698783e+00};
+  const double d[] = {7.784695709041462e-03, 3.224671290700398e-01,
+                      2.445134137142996e+00, 3.754408661907416e+00, 1.0};
+  const double plow = 0.02425;
+  double x;
+  if (p < plow) {
+    const double q = sqrt(__dmul_rn(-2.0, log(p)));
+    double den = d[0];
+#pragma unroll
+    for (int i = 1; i < 5; ++i) den = __dadd_rn(__dmul_rn(den, q), d[i]);
+    x = __ddiv_rn(horner6(c, q), den);
+  } else if (p <= __dsub_rn(1.0, plow)) {
+    const double q = __dsub_rn(p, 0.5);
+    const double r = __dmul_rn(q, q);
+    const double num = __dmul_rn(horner6(a, r), q);
+    double den = b[0];
+#pragma unroll
+    for (int i = 1; i < 6; ++i) den = __dadd_rn(__dmul_rn(den, r), b[i]);
+    x = __ddiv_rn(num, den);
+  } else {
+    const double q = sqrt(__dmul_rn(-2.0, log1p(-p)));
+    double den = d[0];
+#pragma unroll
+    for (int i = 1; i < 5; ++i) den = __dadd_rn(__dmul_rn(den, q), d[i]);
+    x = __ddiv_rn(-horner6(c, q), den);
+  }
+  const double e = __dsub_rn(dphi(x), p);
+  const double u = __dmul_rn(__dmul_rn(e, sqrt(__dmul_rn(2.0, 3.14159265358979323846))),
+                             exp(__dmul_rn(__dmul_rn(0.5, x), x)));
+  x = __dsub_rn(x, __ddiv_rn(u, __dadd_rn(1.0, __dmul_rn(__dmul_rn(0.5, x), u))));
+  return x;
+}
+
+// rng.hpp:54-56
+__device__ __forceinline__ double dnormal_from_bits(uint64_t bits) {
+  return dinverse_phi(__dmul_rn(__dadd_rn(static_cast<double>(bits >> 11), 0.5), 0x1.0p-53));
+}
+
+// Per-batch variate parameters (samplers.hpp:53-126 VariateSource), resident
+// in device memory so a captured batch replays with new keys.
+struct Variates {
+  uint64_t z1, z2;
+  double cos_c, sin_c;
+  int smoothed;
+  int pad;
+};
+
+// samplers.hpp:96-100 finish() for the smoothed stream.
+__device__ __forceinline__ double smooth_finish(const Variates& v, uint64_t b1, uint64_t b2) {
+  const double n = __dadd_rn(__dmul_rn(v.cos_c, dnormal_from_bits(b1)),
+                             __dmul_rn(v.sin_c, dnormal_from_bits(b2)));
+  return dphi(n);
+}
+
+// Guard band for smoothed decisions (relative); see DESIGN.md.
+constexpr double kGuard = 1e-12;
+
+// ---- memory-order helpers ---------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---- warp / block scans -----------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane_id() >= static_cast<unsigned>(o)) v += n;
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Exclusive block scan; `total` receives the block sum. `smem` needs
+// NWARPS+1 entries. Ends with a __syncthreads-free read of smem, so callers
+// must __syncthreads() before reusing smem.
+template <int NT, typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* smem, T& total) {
+  constexpr int NW = NT / 32;
+  const unsigned w = threadIdx.x >> 5;
+  const T inc = warp_inclusive_scan(v);
+  if (lane_id() == 31) smem[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T s = (lane_id() < static_cast<unsigned>(NW)) ? smem[lane_id()] : T(0);
+    const T si = warp_inclusive_scan(s);
+    if (lane_id() < static_cast<unsigned>(NW)) smem[lane_id()] = si - s;
+    if (lane_id() == NW - 1) smem[NW] = si;
+  }
+  __syncthreads();
+  total = smem[NW];
+  return smem[w] + inc - v;
+}
+
+// ---- decoupled look-back tile prefix ----------------------------------------
+// Status word: [epoch:24 | flag:2 | value:38]. Epoch-tagging means status
+// arrays never need clearing between batches: batch_begin bumps the epoch.
+constexpr int kValBits = 38;
+constexpr unsigned long long kValMask = (1ULL << kValBits) - 1;
+constexpr unsigned long long kFlagAgg = 1ULL << kValBits;
+constexpr unsigned long long kFlagPre = 2ULL << kValBits;
+constexpr int kEpochShift = kValBits + 2;
+
+__device__ __forceinline__ unsigned long long mkstat(unsigned epoch, unsigned long long flag,
+                                                     unsigned long long val) {
+  return (static_cast<unsigned long long>(epoch & 0xffffffu) << kEpochShift) | flag |
+         (val & kValMask);
+}
+
+// All threads of the block call this with the same `agg`; returns the
+// exclusive prefix of the tile in tile order. Uses warp 0 for look-back.
+__device__ inline unsigned long long tile_prefix(unsigned long long* status, unsigned tile,
+                                                 unsigned long long agg, unsigned epoch,
+                                                 unsigned long long* s_bcast) {
+  if (threadIdx.x < 32) {
+    const unsigned long long want = static_cast<unsigned long long>(epoch & 0xffffffu);
+    if (tile == 0) {
+      if (lane_id() == 0) {
+        st_release(&status[0], mkstat(epoch, kFlagPre, agg));
+        *s_bcast = 0;
+      }
+    } else {
+      if (lane_id() == 0) st_release(&status[tile], mkstat(epoch, kFlagAgg, agg));
+      unsigned long long excl = 0;
+      long long base = static_cast<long long>(tile) - 1;
+      while (true) {
+        const long long j = base - static_cast<long long>(lane_id());
+        unsigned long long s;
+        bool ready;
+        if (j < 0) {
+          s = mkstat(epoch, kFlagPre, 0);
+          ready = true;
+        } else {
+          s = ld_acquire(&status[j]);
+          ready = (s >> kEpochShift) == want && ((s >> kValBits) & 3u) != 0;
+        }
+        while (!__all_sync(0xffffffffu, ready)) {
+          if (!ready) {
+            s = ld_acquire(&status[j]);
+            ready = (s >> kEpochShift) == want && ((s >> kValBits) & 3u) != 0;
+          }
+        }
+        const unsigned pmask = __ballot_sync(0xffffffffu, ((s >> kValBits) & 3u) == 2u);
+        const int first = pmask ? (__ffs(pmask) - 1) : 32;
+        const unsigned long long c =
+            (static_cast<int>(lane_id()) <= first) ? (s & kValMask) : 0ULL;
+        excl += warp_sum(c);
+        if (pmask) break;
+        base -= 32;
+      }
+      if (lane_id() == 0) {
+        st_release(&status[tile], mkstat(epoch, kFlagPre, excl + agg));
+        *s_bcast = excl;
+      }
+    }
+  }
+  __syncthreads();
+  return *s_bcast;
+}
+
+// Ticket in ticket order (deadlock-free look-back with persistent CTAs).
+__device__ __forceinline__ unsigned next_tile(unsigned* ticket, unsigned* s_tile) {
+  __syncthreads();
+  if (threadIdx.x == 0) *s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  return *s_tile;
+}
+
+// Upper-bound search: largest i in [lo, hi) with a[i] <= x (a nondecreasing).
+template <typename T>
+__device__ __forceinline__ int seg_search(const T* a, int lo, int hi, T x) {
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace cbdev

@@ -1,0 +1,158 @@
+// Input-feature path: synthetic row-sharded embedding tables
+// (FeatureStore::synth, coop.cpp:359-376) and the row gather of the final
+// layer's vertices (FeatureStore::load_rows, coop.cpp:378-388), fused with the
+// requester-side placement of all_to_all_forward (coop.cpp:145-159) when the
+// owner table is reachable from the gathering device.
+//
+// The gather is HBM-bound: per row, row_bytes read at a random 16 B-aligned
+// address and row_bytes written sequentially. Loads use the non-coherent,
+// L1-no-allocate path, stores are streaming (evict-first) so the output does
+// not displace the graph/bitmaps in L2; 4 independent 16 B loads in flight
+// per thread.
+#include <cuda_fp16.h>
+
+#include "cb_internal.h"
+#include "gather.h"
+
+namespace cb {
+using namespace cbdev;
+
+namespace {
+
+template <typename V>
+__device__ __forceinline__ V ld_stream(const V* p);
+template <>
+__device__ __forceinline__ uint4 ld_stream<uint4>(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint2 ld_stream<uint2>(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p));
+  return r;
+}
+template <>
+__device__ __forceinline__ uint32_t ld_stream<uint32_t>(const uint32_t* p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+template <>
+__device__ __forceinline__ unsigned short ld_stream<unsigned short>(const unsigned short* p) {
+  unsigned short r;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  return r;
+}
+
+template <typename V>
+__device__ __forceinline__ void st_stream(V* p, V v) {
+  __stcs(p, v);
+}
+template <>
+__device__ __forceinline__ void st_stream<unsigned short>(unsigned short* p, unsigned short v) {
+  asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"(v));
+}
+
+// out[j] = table[row(ids[j])], j < count. Flattened (row, vector) index space
+// so every lane moves a full vector even when row_bytes/16 is not a multiple
+// of 32. row(v) = row_map ? row_map[v] : v.
+template <typename V, int UNROLL>
+__global__ void __launch_bounds__(256) gather_kernel(
+    const V* __restrict__ table, const uint32_t* __restrict__ ids,
+    const unsigned long long* __restrict__ count, uint64_t cap_rows,
+    const uint32_t* __restrict__ row_map, uint32_t vpr, V* __restrict__ out) {
+  const uint64_t n = min(static_cast<uint64_t>(*count), cap_rows);
+  const uint64_t total = n * vpr;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  for (; idx < total; idx += stride * UNROLL) {
+    V buf[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const uint64_t x = idx + u * stride;
+      if (x < total) {
+        const uint64_t r = x / vpr;
+        const uint64_t c = x - r * vpr;
+        const uint32_t v = __ldg(ids + r);
+        const uint64_t row = row_map ? __ldg(row_map + v) : v;
+        buf[u] = ld_stream(table + row * vpr + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const uint64_t x = idx + u * stride;
+      if (x < total) st_stream(out + x, buf[u]);
+    }
+  }
+}
+
+// value[v, j] = 2*U(hash(seed,{9,v,j})) - 1 (exact in f64), one rounding to
+// the table dtype (cvt.rn.f32.f64 / cvt.rn.f16.f64).
+__global__ void synth_kernel(uint64_t seed, uint32_t dim, int dtype, uint64_t n_rows,
+                             const uint32_t* __restrict__ row_vertex, uint64_t v_base,
+                             void* out) {
+  const uint64_t pfx = hstep(hinit(seed), 9ULL);
+  const uint64_t total = n_rows * dim;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += stride) {
+    const uint64_t r = x / dim;
+    const uint32_t j = static_cast<uint32_t>(x - r * dim);
+    const uint64_t v = row_vertex ? row_vertex[r] : v_base + r;
+    const double val = __dsub_rn(__dmul_rn(2.0, ufb(hstep(hstep(pfx, v), j))), 1.0);
+    if (dtype == 0) static_cast<double*>(out)[x] = val;
+    else if (dtype == 1) static_cast<float*>(out)[x] = __double2float_rn(val);
+    else static_cast<__half*>(out)[x] = __double2half(val);
+  }
+}
+
+}  // namespace
+
+void launch_gather(const void* table, int vec_bytes, uint64_t row_bytes, const uint32_t* ids,
+                   const unsigned long long* count, uint64_t cap_rows, const uint32_t* row_map,
+                   void* out, cudaStream_t st) {
+  const uint32_t vpr = static_cast<uint32_t>(row_bytes / vec_bytes);
+  const int grid = kNumSMs * 8;
+  switch (vec_bytes) {
+    case 16:
+      gather_kernel<uint4, 4><<<grid, 256, 0, st>>>(static_cast<const uint4*>(table), ids,
+                                                   count, cap_rows, row_map, vpr,
+                                                   static_cast<uint4*>(out));
+      break;
+    case 8:
+      gather_kernel<uint2, 4><<<grid, 256, 0, st>>>(static_cast<const uint2*>(table), ids,
+                                                   count, cap_rows, row_map, vpr,
+                                                   static_cast<uint2*>(out));
+      break;
+    case 4:
+      gather_kernel<uint32_t, 4><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(table),
+                                                       ids, count, cap_rows, row_map, vpr,
+                                                       static_cast<uint32_t*>(out));
+      break;
+    default:
+      gather_kernel<unsigned short, 4><<<grid, 256, 0, st>>>(
+          static_cast<const unsigned short*>(table), ids, count, cap_rows, row_map, vpr,
+          static_cast<unsigned short*>(out));
+  }
+  CB_LAUNCH("gather");
+}
+
+void launch_synth(uint64_t seed, uint32_t dim, int dtype, uint64_t n_rows,
+                  const uint32_t* row_vertex, uint64_t v_base, void* out, cudaStream_t st) {
+  synth_kernel<<<kNumSMs * 16, 256, 0, st>>>(seed, dim, dtype, n_rows, row_vertex, v_base, out);
+  CB_LAUNCH("synth");
+}
+
+int vec_bytes_for(uint64_t row_bytes) {
+  for (int v : {16, 8, 4, 2})
+    if (row_bytes % v == 0) return v;
+  return 2;
+}
+
+}  // namespace cb

@@ -1,0 +1,26 @@
+// Feature-path launchers (gather.cu) and graph construction (graph.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cb_internal.h"
+
+namespace cb {
+
+void launch_gather(const void* table, int vec_bytes, uint64_t row_bytes, const uint32_t* ids,
+                   const unsigned long long* count, uint64_t cap_rows, const uint32_t* row_map,
+                   void* out, cudaStream_t st);
+void launch_synth(uint64_t seed, uint32_t dim, int dtype, uint64_t n_rows,
+                  const uint32_t* row_vertex, uint64_t v_base, void* out, cudaStream_t st);
+int vec_bytes_for(uint64_t row_bytes);
+
+// graph.cu
+void graph_generate_rmat(DeviceGraph& g, uint64_t n, uint64_t m, uint64_t seed,
+                         cudaStream_t st);
+void graph_max_degree(DeviceGraph& g, cudaStream_t st);
+void partition_random_device(uint64_t n, uint32_t parts, uint64_t seed, uint32_t* owner,
+                             cudaStream_t st);
+
+}  // namespace cb

@@ -1,0 +1,280 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle on
+identical graphs, seeds and RNG keys. Integer/index outputs must be
+bit-identical; gathered rows must equal the oracle's values rounded once to
+the table dtype (also bit-identical).
+
+Mirrors the reference's own test strategy (proj/tests/test_samplers.cpp,
+test_coop.cpp, acceptance.cpp c4/c9): block invariants, exact LABOR rule,
+NS reservoir, union property / cooperative exactness, routing hand trace."""
+import numpy as np
+import pytest
+
+import paper_2310_12403_b200 as cb
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+KINDS = [(cb.SamplerKind.kFull, O.FULL), (cb.SamplerKind.kNs, O.NS),
+         (cb.SamplerKind.kLabor0, O.LABOR0)]
+
+
+def osched(s: cb.SeedSchedule) -> O.Sched:
+    return O.Sched(s.kappa, s.z1, s.z2, s.iteration)
+
+
+def assert_stack_eq(got: cb.LayerStack, want: list, where=""):
+    assert len(got.blocks) == len(want)
+    for l, (a, b) in enumerate(zip(got.blocks, want)):
+        d = a.as_dict()
+        for k in ("dst", "src", "edges", "dst_pos"):
+            assert d[k].shape == b[k].shape, f"{where} layer {l} {k} shape {d[k].shape} vs {b[k].shape}"
+            assert np.array_equal(d[k], b[k]), f"{where} layer {l} {k} differs"
+
+
+@pytest.fixture(scope="module")
+def c1(gpu):
+    """Config 1: R-MAT 2^16 vertices, 2^20 edges (avg degree 16)."""
+    n, m, seed = 1 << 16, 1 << 20, 42
+    g = cb.Graph.generate_rmat(n, m, seed)
+    return g, O.rmat(n, m, seed)
+
+
+@pytest.fixture(scope="module")
+def powerlaw(gpu):
+    ref = O.generate_powerlaw(3000, 9, 0.6, 5)
+    return cb.Graph.from_csr(ref.indptr, ref.indices), ref
+
+
+def test_rmat_csr_matches_oracle(c1):
+    g, ref = c1
+    indptr, indices = g.download()
+    assert np.array_equal(indptr, ref.indptr)
+    assert np.array_equal(indices, ref.indices)
+    assert g.max_degree == int(np.diff(ref.indptr.astype(np.int64)).max())
+
+
+def test_rmat_odd_sizes(gpu):
+    for n, m, seed in [(1000, 5000, 1), (777, 3000, 9), (5, 12, 3)]:
+        g = cb.Graph.generate_rmat(n, m, seed)
+        ref = O.rmat(n, m, seed)
+        ip, ix = g.download()
+        assert np.array_equal(ip, ref.indptr) and np.array_equal(ix, ref.indices), (n, m)
+
+
+@pytest.mark.parametrize("kind,okind", KINDS)
+@pytest.mark.parametrize("kappa", [1, cb.KAPPA_INFINITY, 4])
+def test_expand_parity_powerlaw(powerlaw, kind, okind, kappa):
+    g, ref = powerlaw
+    rng = np.random.default_rng(int(kind) * 7 + (kappa % 97))
+    sched = cb.SeedSchedule.make(kappa, 99)
+    for trial in range(4):
+        seeds = rng.choice(ref.n, size=int(rng.integers(1, 200)), replace=False).astype(np.uint32)
+        got = cb.expand(g, seeds, 3, cb.SamplerConfig(kind, 4), sched)
+        want = O.expand(ref, seeds, 3, okind, 4, osched(sched))
+        assert_stack_eq(got, want, f"{kind.name} kappa={kappa} trial={trial}")
+        sched = cb.schedule_advance(sched)
+
+
+@pytest.mark.parametrize("kind,okind", KINDS[1:])
+def test_expand_parity_c1(c1, kind, okind):
+    g, ref = c1
+    owner = O.partition_random(ref.n, 1, 3)
+    for step in range(3):
+        seeds = O.draw_from_pool(np.arange(ref.n, dtype=np.uint32), 1024, 3, step)
+        sched = cb.SeedSchedule.plain(O.hash_bits(3, [step]))
+        got = cb.expand(g, seeds, 3, cb.SamplerConfig(kind, 10), sched)
+        want = O.expand(ref, seeds, 3, okind, 10, osched(sched))
+        assert_stack_eq(got, want, f"{kind.name} step={step}")
+    del owner
+
+
+def test_expand_matches_compiled_reference(powerlaw):
+    """Spot-check against the reference's own compiled code (oracle/_ref)."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    g, ref = powerlaw
+    seeds = np.array([5, 9, 100, 317, 2999, 0, 1500], np.uint32)
+    for kind, okind in KINDS:
+        for kappa in (1, 4):
+            sched = cb.SeedSchedule.make(kappa, 11)
+            sched = cb.schedule_advance(cb.schedule_advance(sched))
+            got = cb.expand(g, seeds, 3, cb.SamplerConfig(kind, 3), sched)
+            want = O.expand(ref, seeds, 3, okind, 3, osched(sched), impl="reference")
+            assert_stack_eq(got, want, f"{kind.name} kappa={kappa} vs reference")
+
+
+def test_labor_inclusion_rule_star(gpu):
+    """test_samplers.cpp:110-127 shape: hub with d=50, k=10 -> keep iff r<=0.2."""
+    star = O.build_csr(np.arange(1, 51, dtype=np.uint32), np.zeros(50, np.uint32), 51)
+    g = cb.Graph.from_csr(star.indptr, star.indices)
+    for z in range(20):
+        sched = cb.SeedSchedule.plain(1000 + z)
+        got = cb.expand(g, [0], 1, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), sched)
+        want = O.expand(star, [0], 1, O.LABOR0, 10, osched(sched))
+        assert_stack_eq(got, want, f"z={z}")
+
+
+def test_ns_reservoir_hub(gpu):
+    """NS on a 5000-leaf star: slot-order emission of the reservoir."""
+    star = O.build_csr(np.arange(1, 5001, dtype=np.uint32), np.zeros(5000, np.uint32), 5001)
+    g = cb.Graph.from_csr(star.indptr, star.indices)
+    for z in range(10):
+        sched = cb.SeedSchedule.plain(z)
+        got = cb.expand(g, [0, 3], 2, cb.SamplerConfig(cb.SamplerKind.kNs, 25), sched)
+        want = O.expand(star, [0, 3], 2, O.NS, 25, osched(sched))
+        assert_stack_eq(got, want, f"z={z}")
+        assert got.blocks[0].num_edges() == 25
+
+
+def test_edge_cases(powerlaw):
+    g, ref = powerlaw
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, 5)
+    # empty seeds
+    got = cb.expand(g, np.zeros(0, np.uint32), 2, cfg, cb.SeedSchedule.plain(1))
+    assert all(len(b.src_vertices) == 0 and b.num_edges() == 0 for b in got.blocks)
+    # duplicate seeds at layer 0 (reference keeps them as distinct dsts)
+    seeds = np.array([7, 7, 3, 7], np.uint32)
+    got = cb.expand(g, seeds, 2, cfg, cb.SeedSchedule.plain(1))
+    assert_stack_eq(got, O.expand(ref, seeds, 2, O.LABOR0, 5, O.plain_sched(1)), "dups")
+    # isolated vertices only
+    iso = np.flatnonzero(np.diff(ref.indptr.astype(np.int64)) == 0).astype(np.uint32)[:50]
+    if len(iso):
+        got = cb.expand(g, iso, 2, cfg, cb.SeedSchedule.plain(2))
+        assert_stack_eq(got, O.expand(ref, iso, 2, O.LABOR0, 5, O.plain_sched(2)), "iso")
+    with pytest.raises(cb.InputError):
+        cb.expand(g, np.array([ref.n], np.uint32), 1, cfg, cb.SeedSchedule.plain(1))
+    with pytest.raises(cb.InputError):
+        cb.expand(g, [1], 0, cfg, cb.SeedSchedule.plain(1))
+    with pytest.raises(cb.InputError):
+        cb.expand(g, [1], 1, cb.SamplerConfig(cb.SamplerKind.kNs, 0), cb.SeedSchedule.plain(1))
+
+
+def test_toy_routing_hand_trace(gpu):
+    """test_coop.cpp:90-114: toy6, owners {0,0,0,1,1,1}, PE0 seeds {2}."""
+    src = np.array([(s + 1) % 6 for s in range(6)] + [(s + 2) % 6 for s in range(6)], np.uint32)
+    dst = np.array(list(range(6)) * 2, np.uint32)
+    order = np.argsort(np.concatenate([np.arange(6) * 2, np.arange(6) * 2 + 1]), kind="stable")
+    toy = O.build_csr(src[order], dst[order], 6)
+    g = cb.Graph.from_csr(toy.indptr, toy.indices)
+    pm = cb.partition_from_owner(g, [0, 0, 0, 1, 1, 1], 2)
+    res = cb.coop_sample(g, pm, [[2], []], 1, cb.SamplerConfig(cb.SamplerKind.kFull, 1),
+                         cb.SeedSchedule.plain(1))
+    sc = res.exchanges[0].send_counts
+    assert sc[0, 1] == 2 and sc[0, 0] == 1 and sc[1, 0] == 0
+    assert res.exchanges[0].communicated(0) == 2
+    assert res.owner_sets[0].tolist() == [2]
+    assert res.owner_sets[1].tolist() == [3, 4]
+    with pytest.raises(cb.InputError):
+        cb.coop_sample(g, pm, [[3], []], 1, cb.SamplerConfig(), cb.SeedSchedule.plain(1))
+
+
+def coop_eq(res: cb.CoopSampleResult, exp: dict, P: int, L: int, where=""):
+    for p in range(P):
+        assert_stack_eq(res.stacks[p], exp["stacks"][p], f"{where} part {p}")
+        assert np.array_equal(res.owner_sets[p], exp["owner_sets"][p]), f"{where} owner_set {p}"
+    for l in range(L):
+        a, b = res.exchanges[l], exp["exchanges"][l]
+        assert np.array_equal(a.send_counts, b["send_counts"]), f"{where} send_counts l={l}"
+        assert np.array_equal(a.owner_row_counts, b["owner_row_counts"]), f"{where} orc l={l}"
+        for p in range(P):
+            assert np.array_equal(a.loc_part[p], b["loc_part"][p]), f"{where} loc_part {l},{p}"
+            assert np.array_equal(a.loc_row[p], b["loc_row"][p]), f"{where} loc_row {l},{p}"
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+@pytest.mark.parametrize("kind,okind", KINDS[1:])
+def test_coop_parity_c1(c1, P, kind, okind):
+    """acceptance.cpp c4: cooperative exactness for P in {2,4,8} (+ P=1)."""
+    g, ref = c1
+    pm = cb.partition_random(g, P, 17)
+    owner = O.partition_random(ref.n, P, 17)
+    assert np.array_equal(pm.owner, owner)
+    for step in range(2):
+        seeds = O.draw_coop_seeds(owner, P, 256, 17, step)
+        sched = cb.SeedSchedule.make(1, 17 + step)
+        res = cb.coop_sample(g, pm, seeds, 3, cb.SamplerConfig(kind, 10), sched)
+        exp = O.coop_sample(ref, owner, P, seeds, 3, okind, 10, osched(sched))
+        coop_eq(res, exp, P, 3, f"P={P} {kind.name} step={step}")
+
+
+def test_coop_union_property(c1):
+    """test_coop.cpp:128-157: cooperative input set == single-part union batch."""
+    g, ref = c1
+    P = 4
+    pm = cb.partition_random(g, P, 5)
+    owner = O.partition_random(ref.n, P, 5)
+    seeds = O.draw_coop_seeds(owner, P, 128, 5, 0)
+    sched = cb.SeedSchedule.plain(77)
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, 10)
+    res = cb.coop_sample(g, pm, seeds, 3, cfg, sched)
+    union = np.sort(np.concatenate(seeds))
+    single = cb.expand(g, union, 3, cfg, sched)
+    got = np.sort(np.concatenate(res.owner_sets))
+    assert np.array_equal(got, single.input_vertices())
+
+
+def test_coop_matches_compiled_reference(powerlaw):
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    g, ref = powerlaw
+    for P in (2, 4):
+        pm = cb.partition_random(g, P, 3)
+        owner = O.partition_random(ref.n, P, 3)
+        seeds = O.draw_coop_seeds(owner, P, 40, 3, 1)
+        for kind, okind in KINDS:
+            sched = cb.SeedSchedule.make(4, 8)  # smoothed variates
+            sched = cb.schedule_advance(sched)
+            res = cb.coop_sample(g, pm, seeds, 3, cb.SamplerConfig(kind, 3), sched)
+            exp = O.coop_sample(ref, owner, P, seeds, 3, okind, 3, osched(sched),
+                                impl="reference")
+            coop_eq(res, exp, P, 3, f"ref P={P} {kind.name}")
+
+
+@pytest.mark.parametrize("dtype,dim", [("f32", 100), ("f16", 128), ("f32", 602), ("f64", 3)])
+def test_gather_rows(c1, dtype, dim):
+    g, ref = c1
+    P = 4 if dtype == "f16" else 1
+    pm = cb.partition_random(g, P, 9) if P > 1 else None
+    owner = O.partition_random(ref.n, P, 9)
+    seeds = O.draw_coop_seeds(owner, P, 200, 9, 0)
+    store = cb.FeatureStore.synth(g, dim, 123, dtype, pm)
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, 10)
+    sched = cb.SeedSchedule.plain(5)
+    rows = cb.load_inputs(g, pm, seeds, 3, cfg, sched, store)
+    exp = O.coop_sample(ref, owner, P, seeds, 3, O.LABOR0, 10, osched(sched))
+    for p in range(P):
+        ids = exp["stacks"][p][-1]["src"]
+        want = O.feature_rows(123, dim, dtype, ids)
+        assert rows[p].shape == want.shape
+        assert np.array_equal(rows[p].view(np.uint8), want.view(np.uint8)), f"part {p}"
+
+
+def test_gather_matches_reference_forward(powerlaw):
+    """all_to_all_forward(load_rows(owner_sets)) of the compiled reference,
+    cast once to f32, equals the fused device gather."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    g, ref = powerlaw
+    P, dim, seed = 4, 8, 31
+    pm = cb.partition_random(g, P, seed)
+    owner = O.partition_random(ref.n, P, seed)
+    seeds = O.draw_coop_seeds(owner, P, 30, seed, 0)
+    sched = cb.SeedSchedule.plain(4)
+    store = cb.FeatureStore.synth(g, dim, seed, "f64", pm)
+    rows = cb.load_inputs(g, pm, seeds, 2, cb.SamplerConfig(cb.SamplerKind.kLabor0, 4), sched,
+                          store)
+    exp, handle = O.coop_sample(ref, owner, P, seeds, 2, O.LABOR0, 4, osched(sched),
+                                impl="reference", keep_handle=True)
+    fs = O.RefFeatureStore(ref.n, dim, seed)
+    owner_rows = [fs.load_rows(exp["owner_sets"][q]) for q in range(P)]
+    flat = np.ascontiguousarray(np.concatenate(owner_rows))
+    roff = np.zeros(P + 1, np.uint64)
+    roff[1:] = np.cumsum([len(o) for o in exp["owner_sets"]])
+    total = sum(len(exp["stacks"][p][-1]["src"]) for p in range(P))
+    out = np.zeros((total, dim), np.float64)
+    L = O.lib("reference")
+    assert L.rf_all_to_all_forward(__import__("ctypes").byref(handle), 1, O._ptr(flat),
+                                   O._ptr(roff), dim, O._ptr(out)) == 0
+    O.coop_free_reference(handle)
+    got = np.concatenate(rows)
+    assert np.array_equal(got, out)
