@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the cooperative-minibatching hot path on B200.
+
+Metric (BASELINE.json): seed vertices/sec of one minibatch step =
+3-layer LABOR-0 sample + dedup/relabel (+ owner exchange) + input-feature
+gather, on the products-shaped R-MAT (config 2) at N GPUs, plus feature GB/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+  python bench.py --impl reference ...   # the reference's own CPU path
+
+One process per GPU (torchrun for N>1). At N>1 each rank runs its own
+minibatches (independent minibatching, no data-path collective; weak
+scaling) — see DESIGN.md §Multi-GPU for the cooperative NCCL path status.
+
+value  : device time (CUDA events on the plan stream, max over ranks), inputs
+         resident in HBM, L2 flushed (512 MiB write) before every step.
+e2e    : wall clock through the public API with host (pinned) seeds: H2D of
+         the seeds + variate keys, sample + gather, D2H of the batch's layer
+         counts, every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "seed vertices/sec (sample+dedup+gather, 3-layer) at 1/2/4/8 B200; feature GB/s"
+
+CONFIGS = {
+    "c1": dict(workload="c1: R-MAT 2^16 V / 2^20 E, NS fanout 10, 3 layers, batch 1024, "
+                        "feat 128 fp32", n=1 << 16, m=1 << 20, kind="ns", fanouts=[10, 10, 10],
+               batch=1024, dim=128, dtype="f32"),
+    "c2": dict(workload="c2: ogbn-products-shaped R-MAT (2,449,029 V / 61,859,140 E), "
+                        "LABOR-0 fanout 10, 3 layers, batch 1024/GPU, feat 100 fp32",
+               n=2449029, m=61859140, kind="labor0", fanouts=[10, 10, 10], batch=1024, dim=100,
+               dtype="f32"),
+    "c3": dict(workload="c3: reddit-shaped dense R-MAT (232,965 V / 114,615,892 E), LABOR-0 "
+                        "fanout 10, 3 layers, batch 1024, feat 602 fp32",
+               n=232965, m=114615892, kind="labor0", fanouts=[10, 10, 10], batch=1024, dim=602,
+               dtype="f32"),
+    "c4": dict(workload="c4: ogbn-papers100M-shaped R-MAT (111,059,956 V / 1,615,685,872 E), "
+                        "LABOR-0 fanout 10, 3 layers, batch 1024/GPU, feat 128 fp16",
+               n=111059956, m=1615685872, kind="labor0", fanouts=[10, 10, 10], batch=1024,
+               dim=128, dtype="f16"),
+    "c5": dict(workload="c5: mag240M-shaped R-MAT (244,160,499 V / 1,728,364,232 E), "
+                        "2-layer fanout 25/15, batch 1024/GPU, feat 768 fp16",
+               n=244160499, m=1728364232, kind="labor0", fanouts=[25, 15], batch=1024, dim=768,
+               dtype="f16"),
+}
+GRAPH_SEED = 42
+FEAT_SEED = 7
+RUN_SEED = 1234
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks + throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ CPU baseline --
+def cpu_reference_leg(cfg, csr, budget_s: float, parts_per_step: int | None = None,
+                      max_steps: int | None = None):
+    """Time the reference's own stock path (oracle/_ref: indep_sample + per-part
+    load_rows on the compiled reference) on this host's cores. Returns
+    (seeds/s, cores, sample description, per-step seconds list)."""
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    P = parts_per_step or threads
+    rg = O.RefGraph(csr)
+    t0 = time.time()
+    fs = O.RefFeatureStore(csr.n, cfg["dim"], FEAT_SEED)
+    synth_s = time.time() - t0
+    kind = {"labor0": O.LABOR0, "ns": O.NS, "full": O.FULL}[cfg["kind"]]
+    pool = np.arange(csr.n, dtype=np.uint32)
+    sched = O.make_sched(1, RUN_SEED)
+    L = len(cfg["fanouts"])
+    if len(set(cfg["fanouts"])) != 1:
+        raise SystemExit("reference leg: per-layer fanouts need the sample_block loop")
+    steps, seeds_done, spent, per_step = 0, 0, 0.0, []
+    while spent < budget_s and (max_steps is None or steps < max_steps):
+        per_pe = [O.draw_from_pool(pool, cfg["batch"], RUN_SEED, O.hash_bits(steps, [p]))
+                  for p in range(P)]
+        ts, tg, rows = O.reference_step(rg, fs, 1, None, P, per_pe, L, kind,
+                                        cfg["fanouts"][0], sched)
+        per_step.append(ts + tg)
+        spent += ts + tg
+        seeds_done += P * cfg["batch"]
+        sched = O.advance(sched)
+        steps += 1
+    desc = (f"{steps} step(s) x indep_sample over {P} parts x {cfg['batch']} seeds "
+            f"(reference parallel_for over parts, COOPBATCH_THREADS={threads}) + per-part "
+            f"FeatureStore::load_rows of f64 rows; FeatureStore synth {synth_s:.1f}s excluded")
+    return seeds_done / spent, min(P, threads), desc, per_step
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    t0 = time.time()
+    csr = O.rmat(cfg["n"], cfg["m"], GRAPH_SEED)
+    gen_s = time.time() - t0
+    threads = os.cpu_count() or 1
+    # probe one single-part batch to size the per-step sample
+    _, _, _, probe = cpu_reference_leg(cfg, csr, 0.0, parts_per_step=1, max_steps=1)
+    per_batch = max(probe[0], 1e-3)
+    budget = 90.0
+    P = int(max(1, min(threads, budget / max(1, args.steps + args.warmup) / per_batch)))
+    from oracle import oracle as O2  # noqa: F401
+    value, cores, desc, per_step = cpu_reference_leg(
+        cfg, csr, float("inf"), parts_per_step=P, max_steps=args.warmup + args.steps)
+    timed = per_step[args.warmup:] or per_step
+    seeds = P * cfg["batch"] * len(timed)
+    v = seeds / sum(timed)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "seeds/s",
+        "n_gpus": world, "steps": len(timed), "warmup": args.warmup,
+        "ms_per_step": 1000 * sum(timed) / len(timed), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 rows / u32 ids",
+        "data": "synthetic (hash-keyed R-MAT, hashed features)",
+        "config": {"workload": cfg["workload"], "parts_per_step": P,
+                   "graph_gen_s": round(gen_s, 1)},
+        "cpu_baseline": {"value": v, "unit": "seeds/s", "cores": cores, "kind": "reference",
+                         "sample": desc},
+        "e2e": {"value": v, "unit": "seeds/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------- our arm ----
+def run_ours(args, cfg):
+    import torch
+
+    import paper_2310_12403_b200 as cb
+    from paper_2310_12403_b200.seeds import draw_from_pool
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = local
+
+    kind = {"labor0": cb.SamplerKind.kLabor0, "ns": cb.SamplerKind.kNs,
+            "full": cb.SamplerKind.kFull}[cfg["kind"]]
+    L = len(cfg["fanouts"])
+    b = cfg["batch"]
+    t0 = time.time()
+    g = cb.Graph.generate_rmat(cfg["n"], cfg["m"], GRAPH_SEED, device=dev)
+    gen_s = time.time() - t0
+    store = cb.FeatureStore.synth(g, cfg["dim"], FEAT_SEED, cfg["dtype"])
+    scfg = cb.SamplerConfig(kind, fanouts=cfg["fanouts"])
+    plan = cb.Plan(g, None, L, scfg, b)
+    off = np.array([0, b], np.uint64)
+    pool = np.arange(cfg["n"], dtype=np.uint32)
+    W, K = args.warmup, args.steps
+    # per-step seeds of this rank (independent minibatching across ranks)
+    tags = [cb.hash_bits(step, [rank]) for step in range(W + K)]
+    seeds_host = np.stack([draw_from_pool(pool, b, RUN_SEED, t) for t in tags])
+    scheds = [cb.SeedSchedule.make(1, RUN_SEED)]
+    for _ in range(W + K):
+        scheds.append(cb.schedule_advance(scheds[-1]))
+
+    # one eager batch with overflow-retry sizing, then capture as CUDA graphs
+    plan.sample([seeds_host[0]], scheds[0], cb.MODE_INDEP, sync=True)
+    plan.capture(off, cb.MODE_INDEP, store)
+    stream = torch.cuda.ExternalStream(plan.stream, device=torch.device(f"cuda:{dev}"))
+    d_seeds = torch.from_numpy(seeds_host.view(np.int32)).to(f"cuda:{dev}")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    row_bytes = store.row_bytes
+
+    def step_ptr(i):
+        return d_seeds.data_ptr() + i * b * 4
+
+    # ---- warmup
+    for i in range(W):
+        plan.replay(step_ptr(i), scheds[i], True, 3)
+    plan.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+
+    # ---- timed (device-resident inputs)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    clocks = ClockSampler(dev)
+    with clocks:
+        for i in range(K):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            ev[i][0].record(stream)
+            plan.replay(step_ptr(W + i), scheds[W + i], True, 1)
+            ev[i][1].record(stream)
+            plan.replay(None, None, True, 2)
+            ev[i][2].record(stream)
+        torch.cuda.synchronize()
+    plan.synchronize()  # raises on capacity overflow
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [e[0].elapsed_time(e[2]) for e in ev]
+    samp_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    gath_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    total_ms = float(np.sum(step_ms))
+    sizes = [plan.layer_sizes(0, l) for l in range(L)]
+    rows_last = sizes[-1]["n_src"]
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # ---- e2e: host pinned seeds through the public API, D2H of counts
+    pinned = torch.from_numpy(seeds_host.view(np.int32)).pin_memory()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    te = time.perf_counter()
+    for i in range(K):
+        plan.replay(pinned.data_ptr() + (W + i) * b * 4, scheds[W + i], False, 3)
+        last = plan.layer_sizes(0, L - 1)  # D2H read of the batch result
+    e2e_s = time.perf_counter() - te
+    if world > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    del last
+
+    launches_per_step = plan.launch_count(cb.MODE_INDEP, True)
+    if rank != 0:
+        return
+    seeds_total = K * b * world
+    value = seeds_total / (total_ms / 1000.0)
+    peak, peak_kind = peaks()
+    # dominant kernel: the gather (one launch per step)
+    gather_bytes = rows_last * (2 * row_bytes + 4)
+    gather_avg_s = float(np.mean(gath_ms)) / 1000.0
+    achieved = gather_bytes / gather_avg_s / 1e9
+    feat_gbps = rows_last * row_bytes / gather_avg_s / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "seeds/s", "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (hash-keyed R-MAT, hashed "
+        "features; random-init equivalent)",
+        "config": {"workload": cfg["workload"], "mode": "indep (P=1 per GPU)",
+                   "l2": "flushed (512 MiB write) before every step",
+                   "graph": {"vertices": cfg["n"], "edges": cfg["m"],
+                             "max_degree": g.max_degree, "gen_s": round(gen_s, 2)},
+                   "cuda_graphs": True},
+        "feature_gbps": feat_gbps,
+        "stage_ms": {"sample_dedup": float(np.mean(samp_ms)), "gather": float(np.mean(gath_ms))},
+        "e2e": {"value": seeds_total / e2e_s, "unit": "seeds/s",
+                "h2d_bytes_per_step": b * 4 + 40, "d2h_bytes_per_step": 64},
+        "roofline": {"bound": "hbm", "kernel": "gather_kernel<uint4,4>",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "bytes_per_launch": gather_bytes},
+        "gpu_launches": launches_per_step * K,
+        "evidence": {"per_layer": sizes,
+                     "sampled_vertices_per_seed": rows_last / b,
+                     "feature_bytes_per_step": rows_last * row_bytes},
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import oracle as O
+            indptr, indices = g.download()
+            csr = O.CSR(indptr, indices)
+            v, cores, desc, _ = cpu_reference_leg(cfg, csr, args.cpu_budget)
+            line["cpu_baseline"] = {"value": v, "unit": "seeds/s", "cores": cores,
+                                    "kind": "reference", "sample": desc}
+        except Exception as e:  # report, never fake
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+    rank, world, _ = dist_env()
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -15,6 +15,8 @@
 #include "coopbatch_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
+#include <unistd.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -311,6 +313,53 @@ static inline int rmat_attempt(uint64_t pfx13, int s, uint64_t a, uint64_t n,
   return sr < n && ds < n;
 }
 
+/* Minimal pthread fan-out for the embarrassingly parallel attempt loop. */
+typedef struct {
+  uint64_t pfx13;
+  int s;
+  uint64_t n;
+  const rmat_perm* pm;
+  uint64_t a0;
+  uint64_t* cand;
+  uint64_t chunk;
+  int nthreads;
+} rmat_job;
+
+typedef struct {
+  rmat_job* job;
+  int tid;
+} rmat_arg;
+
+static void* rmat_worker(void* argp) {
+  rmat_arg* arg = argp;
+  rmat_job* j = arg->job;
+  const uint64_t lo = j->chunk * (uint64_t)arg->tid / (uint64_t)j->nthreads;
+  const uint64_t hi = j->chunk * (uint64_t)(arg->tid + 1) / (uint64_t)j->nthreads;
+  for (uint64_t i = lo; i < hi; ++i) {
+    uint64_t sr, ds;
+    if (!rmat_attempt(j->pfx13, j->s, j->a0 + i, j->n, &sr, &ds) || sr == ds)
+      j->cand[i] = ~0ULL;
+    else
+      j->cand[i] = (perm_walk(j->pm, sr, j->n) << 32) | perm_walk(j->pm, ds, j->n);
+  }
+  return NULL;
+}
+
+static void run_threads(void* (*fn)(void*), rmat_job* job) {
+  long nt = sysconf(_SC_NPROCESSORS_ONLN);
+  if (nt < 1) nt = 1;
+  if (nt > 64) nt = 64;
+  job->nthreads = (int)nt;
+  pthread_t th[64];
+  rmat_arg args[64];
+  for (int t = 0; t < nt; ++t) {
+    args[t].job = job;
+    args[t].tid = t;
+    pthread_create(&th[t], NULL, fn, &args[t]);
+  }
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+}
+
 int ob_rmat(uint64_t n, uint64_t m_target, uint64_t seed, uint64_t** indptr_out,
             uint32_t** indices_out) {
   if (n < 2 || n > 0xFFFFFFFFULL) return fail("rmat: need 2 <= n < 2^32");
@@ -327,28 +376,37 @@ int ob_rmat(uint64_t n, uint64_t m_target, uint64_t seed, uint64_t** indptr_out,
   uint32_t* ed = xmalloc(m_target * sizeof(uint32_t));
   uint64_t got = 0;
   const uint64_t max_attempts = m_target * 1000 + 100000;
-  for (uint64_t a = 0; got < m_target; ++a) {
-    if (a >= max_attempts) {
-      free(seen); free(es); free(ed);
+  /* Attempts are generated in parallel chunks (pure functions of a); the
+   * dedup walk stays sequential in attempt order, so the result does not
+   * depend on the thread count. */
+  const uint64_t chunk = 1u << 22;
+  uint64_t* cand = xmalloc(chunk * sizeof(uint64_t)); /* src<<32|dst, ~0 = drop */
+  for (uint64_t a0 = 0; got < m_target; a0 += chunk) {
+    if (a0 >= max_attempts) {
+      free(seen); free(es); free(ed); free(cand);
       return fail("rmat: attempt budget exhausted (graph too dense)");
     }
-    uint64_t sr, ds;
-    if (!rmat_attempt(pfx13, s, a, n, &sr, &ds)) continue;
-    if (sr == ds) continue; /* bijection: self-loop iff raw ids equal */
-    const uint64_t src = perm_walk(&pm, sr, n), dst = perm_walk(&pm, ds, n);
-    const uint64_t key = (src << 32) | dst;
-    uint64_t h = ob_mix64(key) & (cap - 1);
-    int dup = 0;
-    while (seen[h]) {
-      if (seen[h] == key) { dup = 1; break; }
-      h = (h + 1) & (cap - 1);
+    {
+      rmat_job job = {pfx13, s, n, &pm, a0, cand, chunk, 0};
+      run_threads(rmat_worker, &job);
     }
-    if (dup) continue;
-    seen[h] = key;
-    es[got] = (uint32_t)src;
-    ed[got] = (uint32_t)dst;
-    ++got;
+    for (uint64_t i = 0; i < chunk && got < m_target; ++i) {
+      const uint64_t key = cand[i];
+      if (key == ~0ULL) continue;
+      uint64_t h = ob_mix64(key) & (cap - 1);
+      int dup = 0;
+      while (seen[h]) {
+        if (seen[h] == key) { dup = 1; break; }
+        h = (h + 1) & (cap - 1);
+      }
+      if (dup) continue;
+      seen[h] = key;
+      es[got] = (uint32_t)(key >> 32);
+      ed[got] = (uint32_t)key;
+      ++got;
+    }
   }
+  free(cand);
   free(seen);
   uint64_t* indptr = xmalloc((n + 1) * sizeof(uint64_t));
   uint32_t* indices = xmalloc(m_target * sizeof(uint32_t));

@@ -161,6 +161,9 @@ def lib(impl: str = "restated") -> C.CDLL:
         L.rf_features_free.argtypes = [_P]
         L.rf_load_rows.argtypes = [_P, _P, _u64, _P]
         L.rf_all_to_all_forward.argtypes = [C.POINTER(Coop), C.c_int, _P, _P, _u32, _P]
+        L.rf_step.argtypes = [_P, _P, C.c_int, _P, _u32, _P, _P, C.c_int, C.c_int, _u32,
+                              C.POINTER(Sched), C.POINTER(_f64), C.POINTER(_f64),
+                              C.POINTER(_u64)]
         L.rf_lru_new.restype = _P
         L.rf_lru_new.argtypes = [_u64]
         L.rf_lru_access.argtypes = [_P, _u32]
@@ -528,3 +531,19 @@ def dependent_experiment(g, mode: int, kappa: int, batch: int, steps: int, capac
                                         fanout, L, dim, bps, seed, _ptr(fp), _ptr(sl),
                                         _ptr(by), C.byref(steady)), rg.L)
     return {"fingerprint": fp, "s_l": sl, "bytes": by, "steady": steady.value}
+
+
+def reference_step(rg: RefGraph, fs: RefFeatureStore, mode: int, owner, parts: int,
+                   per_pe_seeds, num_layers: int, kind: int, fanout: int, sched: Sched):
+    """The reference's stock sample + load_rows (+ all_to_all_forward) path for
+    one minibatch; returns (t_sample_s, t_gather_s, rows)."""
+    flat = np.ascontiguousarray(np.concatenate(
+        [np.asarray(s, dtype=np.uint32) for s in per_pe_seeds]), dtype=np.uint32)
+    off = np.zeros(parts + 1, np.uint64)
+    off[1:] = np.cumsum([len(s) for s in per_pe_seeds])
+    own = None if owner is None else np.ascontiguousarray(owner, dtype=np.uint32)
+    ts, tg, rows = C.c_double(), C.c_double(), C.c_uint64()
+    _check(rg.L.rf_step(rg.h, fs.h, mode, _ptr(own), parts, _ptr(flat), _ptr(off), num_layers,
+                        kind, fanout, C.byref(sched), C.byref(ts), C.byref(tg),
+                        C.byref(rows)), rg.L)
+    return ts.value, tg.value, rows.value

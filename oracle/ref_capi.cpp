@@ -7,6 +7,7 @@
 // reference through ctypes. Used (1) to pin the plain-C restatement
 // (coopbatch_oracle.c), (2) to generate tests/golden/, and (3) as the CPU
 // baseline ("kind": "reference") in bench.py.
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -324,6 +325,56 @@ int rf_all_to_all_forward(const ob_coop* c, int layer, const double* owner_flat,
       if (!fwd[p].empty()) std::memcpy(out_flat + o, fwd[p].data(), fwd[p].size() * 8);
       o += fwd[p].size();
     }
+  });
+}
+
+/* One minibatch of the reference's own stock path, timed inside C++:
+ *   coop : coop_sample -> per-part load_rows(owner_sets) -> all_to_all_forward
+ *          (coop_train_step's prefix, coop.cpp:445-467)
+ *   indep: indep_sample -> per-part load_rows(input_vertices)
+ *          (indep_train_step's prefix, coop.cpp:560 + FeatureStore use)
+ * Returns seconds spent sampling and loading features and the rows
+ * delivered (requester-aligned). */
+int rf_step(void* g, void* fs, int mode, const uint32_t* owner, uint32_t parts,
+            const uint32_t* seeds_flat, const uint64_t* seeds_off, int L, int kind,
+            uint32_t fanout, const ob_sched* sched, double* t_sample, double* t_gather,
+            uint64_t* rows_out) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    const Graph& gr = *static_cast<Graph*>(g);
+    const FeatureStore& store = *static_cast<FeatureStore*>(fs);
+    std::vector<std::vector<VertexId>> seeds(parts);
+    for (uint32_t p = 0; p < parts; ++p)
+      seeds[p].assign(seeds_flat + seeds_off[p], seeds_flat + seeds_off[p + 1]);
+    const SamplerConfig cfg = to_cfg(kind, fanout);
+    const SeedSchedule sc = to_sched(sched);
+    uint64_t rows = 0;
+    if (mode == 0) {
+      PartitionMap pm;
+      pm.num_parts = parts;
+      pm.owner.assign(owner, owner + gr.num_vertices);
+      const auto t0 = clk::now();
+      const CoopSampleResult r = coop_sample(gr, pm, seeds, L, cfg, sc);
+      const auto t1 = clk::now();
+      std::vector<std::vector<double>> owner_rows(parts);
+      for (uint32_t p = 0; p < parts; ++p)
+        owner_rows[p] = store.load_rows(r.owner_sets[p]).values;
+      const auto fwd = all_to_all_forward(r.exchanges[L - 1], owner_rows, store.dim);
+      const auto t2 = clk::now();
+      for (const auto& f : fwd) rows += f.size() / store.dim;
+      *t_sample = std::chrono::duration<double>(t1 - t0).count();
+      *t_gather = std::chrono::duration<double>(t2 - t1).count();
+    } else {
+      const auto t0 = clk::now();
+      const auto stacks = indep_sample(gr, seeds, L, cfg, sc);
+      const auto t1 = clk::now();
+      for (uint32_t p = 0; p < parts; ++p)
+        rows += store.load_rows(stacks[p].input_vertices()).rows();
+      const auto t2 = clk::now();
+      *t_sample = std::chrono::duration<double>(t1 - t0).count();
+      *t_gather = std::chrono::duration<double>(t2 - t1).count();
+    }
+    *rows_out = rows;
   });
 }
 

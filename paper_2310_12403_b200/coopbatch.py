@@ -348,6 +348,19 @@ class Plan:
         _check(_lib.load().cb_sample_device(self._h, mode, C.c_void_p(d_seeds_ptr),
                                             _ptr(off), C.byref(s)))
 
+    def capture(self, offsets, mode: int = MODE_COOP, store: FeatureStore | None = None):
+        """Capture one batch (and its gather) as CUDA graphs for replay."""
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        _check(_lib.load().cb_plan_capture(self._h, mode, _ptr(off),
+                                           store._h if store else None))
+
+    def replay(self, seeds_ptr: int | None, schedule: SeedSchedule | None,
+               on_device: bool, what: int = 3):
+        s = schedule._c() if schedule is not None else None
+        _check(_lib.load().cb_plan_replay(self._h, C.c_void_p(seeds_ptr) if seeds_ptr else None,
+                                          int(on_device), C.byref(s) if s is not None else None,
+                                          what))
+
     def gather(self, store: FeatureStore):
         _check(_lib.load().cb_gather(self._h, store._h))
 

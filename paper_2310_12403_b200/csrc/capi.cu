@@ -149,6 +149,19 @@ struct cb_plan {
   uint64_t batches = 0;
   uint64_t launches = 0;  // kernels enqueued by the last cb_sample (+ cb_gather)
   std::vector<uint64_t> seeds_off;
+  // CUDA graphs of one batch (sample) and its gather, replayed per step
+  cudaGraphExec_t exec_sample = nullptr;
+  cudaGraphExec_t exec_gather = nullptr;
+  int cap_mode = -1;
+  std::vector<uint64_t> cap_off;
+  uint64_t cap_launches_sample = 0, cap_launches_gather = 0;
+
+  void drop_graphs() {
+    if (exec_sample) cudaGraphExecDestroy(exec_sample);
+    if (exec_gather) cudaGraphExecDestroy(exec_gather);
+    exec_sample = exec_gather = nullptr;
+  }
+  ~cb_plan() { drop_graphs(); }
 
   LayerMeta* meta_at(uint32_t p, int l) { return meta + p * (L + 1) + l; }
   bool coop_active() const { return mode == CB_MODE_COOP && P > 1; }
@@ -167,6 +180,7 @@ void make_bitmap(Arena& a, Bitmap& b, uint64_t n) {
 // Capacity plan (host): upper bounds sized from the seeds and fanouts; any
 // overflow is detected on the device and retried with grow *= 2.
 void plan_alloc(cb_plan* pl) {
+  pl->drop_graphs();
   pl->mem.release();
   pl->rows_mem.release();
   pl->have_rows = false;
@@ -307,17 +321,19 @@ void check_ownership_host(const cb_plan* pl, const uint32_t* flat, const uint64_
 
 // The per-batch launch sequence. d_seeds: P seed lists back to back (device).
 void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_t* off,
-                   const cb_sched* sched) {
+                   const cb_sched* sched, bool capturing = false) {
   const DeviceGraph& g = pl->g->g;
   const uint32_t P = pl->P;
   const int L = pl->L;
   cudaStream_t st = pl->stream;
   uint64_t launches = 0;
-  const Variates v = make_variates(sched);
-  CB_CUDA(cudaMemcpyAsync(pl->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+  if (!capturing) {
+    const Variates v = make_variates(sched);
+    CB_CUDA(cudaMemcpyAsync(pl->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+  }
   pl->mode = mode;
   pl->seeds_off.assign(off, off + P + 1);
-  if (++pl->batches % (1u << 17) == 0) {  // epoch wrap guard (18-bit epochs)
+  if (!capturing && ++pl->batches % (1u << 17) == 0) {  // epoch wrap (18-bit epochs)
     for (auto& w : pl->pe) {
       CB_CUDA(cudaMemsetAsync(w.sync.status_a, 0, w.sync.max_tiles * 8, st));
       CB_CUDA(cudaMemsetAsync(w.sync.status_b, 0, w.sync.max_tiles * 8, st));
@@ -457,6 +473,33 @@ void require_batch(const cb_plan* pl, uint32_t p, int l) {
   require(pl->have_batch, "no sampled batch in this plan");
   require(p < pl->P, "part index out of range");
   require(l >= 0 && l < pl->L, "layer index out of range");
+}
+
+void prepare_rows(cb_plan* pl, const cb_features* f) {
+  require(f->n_rows == pl->g->g.n, "feature table does not match the graph");
+  require(pl->P == 1 || f->row_map != nullptr,
+          "multi-part plan needs a feature table sharded by the same partition");
+  for (uint32_t p = 0; p < pl->P; ++p) {
+    PeWork& w = pl->pe[p];
+    const LayerBufs& b = w.L[pl->L - 1];
+    if (!w.rows || w.rows_row_bytes != f->row_bytes || w.cap_rows < b.cap_src) {
+      w.rows = pl->rows_mem.alloc<unsigned char>(b.cap_src * f->row_bytes);
+      w.cap_rows = b.cap_src;
+      w.rows_row_bytes = f->row_bytes;
+    }
+  }
+}
+
+void enqueue_gather(cb_plan* pl, const cb_features* f) {
+  const int vb = vec_bytes_for(f->row_bytes);
+  for (uint32_t p = 0; p < pl->P; ++p) {
+    PeWork& w = pl->pe[p];
+    const LayerBufs& b = w.L[pl->L - 1];
+    launch_gather(f->table, vb, f->row_bytes, b.src, &pl->meta_at(p, pl->L - 1)->n_src,
+                  w.cap_rows, f->row_map, w.rows, pl->stream);
+    pl->launches += 1;
+  }
+  pl->have_rows = true;
 }
 
 }  // namespace
@@ -782,24 +825,88 @@ int cb_gather(cb_plan* plan, const cb_features* f) {
   return guard([&] {
     require(plan != nullptr && f != nullptr, "null argument");
     require(plan->have_batch, "no sampled batch in this plan");
-    require(f->n_rows == plan->g->g.n, "feature table does not match the graph");
-    require(plan->P == 1 || f->row_map != nullptr,
-            "multi-part plan needs a feature table sharded by the same partition");
     DeviceGuard dg(plan->device);
-    const int vb = vec_bytes_for(f->row_bytes);
-    for (uint32_t p = 0; p < plan->P; ++p) {
-      PeWork& w = plan->pe[p];
-      const LayerBufs& b = w.L[plan->L - 1];
-      if (!w.rows || w.rows_row_bytes != f->row_bytes || w.cap_rows < b.cap_src) {
-        w.rows = plan->rows_mem.alloc<unsigned char>(b.cap_src * f->row_bytes);
-        w.cap_rows = b.cap_src;
-        w.rows_row_bytes = f->row_bytes;
-      }
-      launch_gather(f->table, vb, f->row_bytes, b.src, &plan->meta_at(p, plan->L - 1)->n_src,
-                    w.cap_rows, f->row_map, w.rows, plan->stream);
-      plan->launches += 1;
+    prepare_rows(plan, f);
+    enqueue_gather(plan, f);
+  });
+}
+
+int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb_features* f) {
+  return guard([&] {
+    require(plan != nullptr && seeds_off != nullptr, "null argument");
+    require(mode == CB_MODE_COOP || mode == CB_MODE_INDEP, "unknown sampling mode");
+    for (uint32_t p = 0; p < plan->P; ++p)
+      require(seeds_off[p + 1] - seeds_off[p] <= plan->max_seeds,
+              "more seeds than the plan's max_seeds_per_part");
+    DeviceGuard dg(plan->device);
+    plan->drop_graphs();
+    if (f) prepare_rows(plan, f);
+    cb_sched dummy{1, 0, 0, 0};
+    // one eager batch first: sets kernel attributes outside capture
+    enqueue_batch(plan, mode, plan->seeds, seeds_off, &dummy);
+    if (f) enqueue_gather(plan, f);
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    cudaGraph_t graph;
+    CB_CUDA(cudaStreamBeginCapture(plan->stream, cudaStreamCaptureModeThreadLocal));
+    enqueue_batch(plan, mode, plan->seeds, seeds_off, &dummy, true);
+    CB_CUDA(cudaStreamEndCapture(plan->stream, &graph));
+    CB_CUDA(cudaGraphInstantiate(&plan->exec_sample, graph, 0));
+    CB_CUDA(cudaGraphDestroy(graph));
+    plan->cap_launches_sample = plan->launches;
+    if (f) {
+      CB_CUDA(cudaStreamBeginCapture(plan->stream, cudaStreamCaptureModeThreadLocal));
+      plan->launches = 0;
+      enqueue_gather(plan, f);
+      CB_CUDA(cudaStreamEndCapture(plan->stream, &graph));
+      CB_CUDA(cudaGraphInstantiate(&plan->exec_gather, graph, 0));
+      CB_CUDA(cudaGraphDestroy(graph));
+      plan->cap_launches_gather = plan->launches;
     }
-    plan->have_rows = true;
+    plan->cap_mode = mode;
+    plan->cap_off.assign(seeds_off, seeds_off + plan->P + 1);
+    plan->have_batch = false;
+  });
+}
+
+int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_device,
+                   const cb_sched* sched, int what) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require(plan->exec_sample != nullptr, "no captured batch (call cb_plan_capture)");
+    DeviceGuard dg(plan->device);
+    cudaStream_t st = plan->stream;
+    if (what & 1) {
+      require(sched != nullptr, "null schedule");
+      require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
+      const uint64_t total = plan->cap_off[plan->P];
+      if (seeds_flat && total)
+        CB_CUDA(cudaMemcpyAsync(plan->seeds, seeds_flat, total * 4,
+                                seeds_on_device ? cudaMemcpyDeviceToDevice
+                                                : cudaMemcpyHostToDevice,
+                                st));
+      const Variates v = make_variates(sched);
+      CB_CUDA(cudaMemcpyAsync(plan->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+      if (++plan->batches % (1u << 17) == 0) {
+        for (auto& w : plan->pe) {
+          CB_CUDA(cudaMemsetAsync(w.sync.status_a, 0, w.sync.max_tiles * 8, st));
+          CB_CUDA(cudaMemsetAsync(w.sync.status_b, 0, w.sync.max_tiles * 8, st));
+          CB_CUDA(cudaMemsetAsync(w.sync.status_c, 0, w.sync.max_tiles * 8, st));
+        }
+      }
+      CB_CUDA(cudaGraphLaunch(plan->exec_sample, st));
+      plan->mode = plan->cap_mode;
+      plan->seeds_off = plan->cap_off;
+      plan->have_batch = true;
+      plan->have_rows = false;
+      plan->launches = plan->cap_launches_sample;
+    }
+    if (what & 2) {
+      require(plan->exec_gather != nullptr, "no captured gather");
+      require(plan->have_batch, "no sampled batch in this plan");
+      CB_CUDA(cudaGraphLaunch(plan->exec_gather, st));
+      plan->have_rows = true;
+      plan->launches += plan->cap_launches_gather;
+    }
   });
 }
 
