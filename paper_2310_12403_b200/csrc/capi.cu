@@ -144,6 +144,7 @@ struct cb_plan {
   uint32_t* seeds = nullptr;
   uint64_t seeds_cap = 0;
   int mode = -1;          // mode of the last batch
+  int dirty_mode = -1;    // mode whose final bitmap still holds bits (-1: clean)
   bool have_batch = false;
   bool have_rows = false;
   uint64_t batches = 0;
@@ -210,8 +211,7 @@ void plan_alloc(cb_plan* pl) {
       b.cap_src = std::min(n, cd + b.cap_edges);
       if (l == 0) b.dst = nullptr;  // seeds live in pl->seeds
       else b.dst = pl->mem.alloc<uint32_t>(cd);
-      b.act_di = pl->mem.alloc<uint32_t>(cd);
-      b.act_pre = pl->mem.alloc<uint64_t>(cd + 1);
+      b.act = pl->mem.alloc<ActRec>(cd + 1);
       b.out_prefix = pl->kind == CB_NS ? pl->mem.alloc<uint64_t>(cd + 1) : nullptr;
       b.slots = pl->kind == CB_NS ? pl->mem.alloc<uint32_t>(b.cap_edges) : nullptr;
       b.edges = pl->mem.alloc<uint2>(b.cap_edges);
@@ -233,8 +233,13 @@ void plan_alloc(cb_plan* pl) {
     make_bitmap(pl->mem, w.bm[1], n);
     max_tiles = std::max(max_tiles, w.bm[0].words_padded / kExtractTileWords + 2);
     w.sync.max_tiles = max_tiles;
+    for (int l = 0; l < L; ++l) {
+      w.L[l].tile_first = pl->mem.alloc<uint32_t>(max_tiles + 1);
+      CB_CUDA(cudaMemset(w.L[l].tile_first, 0, (max_tiles + 1) * 4));
+    }
     w.sync.epoch = pl->mem.alloc<unsigned>(1);
-    w.sync.tickets = pl->mem.alloc<unsigned>(Sync::kMaxTickets);
+    w.sync.tickets = pl->mem.alloc<unsigned>(2 * Sync::kMaxTickets);
+    CB_CUDA(cudaMemset(w.sync.tickets, 0, 2 * Sync::kMaxTickets * sizeof(unsigned)));
     w.sync.overflow = pl->mem.alloc<unsigned>(1);
     w.sync.status_a = pl->mem.alloc<unsigned long long>(max_tiles);
     w.sync.status_b = pl->mem.alloc<unsigned long long>(max_tiles);
@@ -251,6 +256,7 @@ void plan_alloc(cb_plan* pl) {
   pl->seeds_cap = static_cast<uint64_t>(P) * std::max<uint64_t>(pl->max_seeds, 1);
   pl->seeds = pl->mem.alloc<uint32_t>(pl->seeds_cap);
   pl->have_batch = false;
+  pl->dirty_mode = -1;
   CB_CUDA(cudaDeviceSynchronize());
 }
 
@@ -319,10 +325,131 @@ void check_ownership_host(const cb_plan* pl, const uint32_t* flat, const uint64_
                                   " is not owned by part " + std::to_string(p));
 }
 
+// Which bitmap still holds bits after a batch of `mode`, and the id list
+// (with its device count) that names every set word.
+struct Dirty {
+  uint32_t* bits = nullptr;
+  const uint32_t* list = nullptr;
+  const unsigned long long* count = nullptr;
+  uint64_t cap = 0;
+};
+
+Dirty dirty_of(cb_plan* pl, uint32_t p, int mode) {
+  Dirty d;
+  if (mode < 0) return d;
+  PeWork& w = pl->pe[p];
+  const int L = pl->L;
+  if (mode == CB_MODE_COOP && pl->P > 1) {
+    d.bits = w.bm[1].bits;
+    d.list = w.owner_final;
+    d.count = &pl->meta_at(p, L)->n_dst;
+    d.cap = w.cap_final;
+  } else {
+    d.bits = w.bm[(L - 1) & 1].bits;
+    d.list = w.L[L - 1].src;
+    d.count = &pl->meta_at(p, L - 1)->n_src;
+    d.cap = w.L[L - 1].cap_src;
+  }
+  return d;
+}
+
+ExtractArgs extract_args(PeWork& w, const Bitmap& bm, uint32_t* zero_bits, uint32_t* out,
+                         uint64_t cap, unsigned long long* c1, unsigned long long* c2,
+                         int ticket, int slot) {
+  ExtractArgs e{};
+  e.bits = bm.bits;
+  e.wprefix = bm.wprefix;
+  e.zero_bits = zero_bits;
+  e.words_padded = bm.words_padded;
+  e.out = out;
+  e.cap_out = cap;
+  e.count_out = c1;
+  e.count_out2 = c2;
+  e.ticket = w.sync.tickets + ticket;
+  e.exit_ctr = w.sync.tickets + Sync::kMaxTickets + ticket;
+  e.status = w.sync.status_a;
+  e.epoch = w.sync.epoch;
+  e.slot = slot;
+  e.overflow = w.sync.overflow;
+  return e;
+}
+
+RelabelArgs relabel_args(const Bitmap& bm, const LayerBufs& b, const uint32_t* D,
+                         const LayerMeta* me) {
+  RelabelArgs r{};
+  r.bits = bm.bits;
+  r.wprefix = bm.wprefix;
+  r.meta = me;
+  r.edges = b.edges;
+  r.cap_edges = b.cap_edges;
+  r.D = D;
+  r.dst_pos = b.dst_pos;
+  return r;
+}
+
+// Frontier + sampling of one layer of one part (sample.cu kernels).
+uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* D,
+                       uint64_t cap_dst, uint64_t n_dst_param, Bitmap& set_bm,
+                       const RelabelArgs& fused, uint64_t fused_work) {
+  const DeviceGraph& g = pl->g->g;
+  const LayerBufs& b = w.L[l];
+  LayerMeta* me = pl->meta_at(p, l);
+  cudaStream_t st = pl->stream;
+  FrontierArgs fa{};
+  fa.D = D;
+  fa.meta = me;
+  fa.n_dst_param = n_dst_param;
+  fa.indptr = g.indptr;
+  fa.kind = pl->kind;
+  fa.k = pl->fanouts[l];
+  fa.layer = l;
+  fa.var = pl->var;
+  fa.set_bits = set_bm.bits;
+  fa.act = b.act;
+  fa.tile_first = b.tile_first;
+  fa.out_prefix = b.out_prefix;
+  fa.slots = b.slots;
+  fa.cap_edges = b.cap_edges;
+  fa.ticket = w.sync.tickets + 3 * l;
+  fa.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l;
+  fa.st_a = w.sync.status_a;
+  fa.st_b = w.sync.status_b;
+  fa.st_c = w.sync.status_c;
+  fa.epoch = w.sync.epoch;
+  fa.slot = 8 * l;
+  fa.overflow = w.sync.overflow;
+  launch_frontier(fa, fused, cap_dst, fused_work, st);
+  LaborArgs la{};
+  la.meta = me;
+  la.act = b.act;
+  la.tile_first = b.tile_first;
+  la.D = D;
+  la.indices = g.indices;
+  la.kind = pl->kind;
+  la.k = pl->fanouts[l];
+  la.layer = l;
+  la.var = pl->var;
+  la.bits = set_bm.bits;
+  la.edges = b.edges;
+  la.slots = b.slots;
+  la.cap_edges = b.cap_edges;
+  la.ticket = w.sync.tickets + 3 * l + 1;
+  la.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l + 1;
+  la.status = w.sync.status_a;
+  la.epoch = w.sync.epoch;
+  la.slot = 8 * l + 3;
+  la.overflow = w.sync.overflow;
+  if (pl->kind == CB_NS) {
+    launch_ns(la, D, b.out_prefix, g.indptr, g.indices, cap_dst, st);
+    return 3;
+  }
+  launch_labor(la, w.sync.max_tiles, st);
+  return 2;
+}
+
 // The per-batch launch sequence. d_seeds: P seed lists back to back (device).
 void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_t* off,
                    const cb_sched* sched, bool capturing = false) {
-  const DeviceGraph& g = pl->g->g;
   const uint32_t P = pl->P;
   const int L = pl->L;
   cudaStream_t st = pl->stream;
@@ -340,43 +467,42 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
       CB_CUDA(cudaMemsetAsync(w.sync.status_c, 0, w.sync.max_tiles * 8, st));
     }
   }
+  const bool coop = (mode == CB_MODE_COOP) && P > 1;
+  // during capture the graph must clear what a batch of its own mode leaves
+  const int dm = capturing ? mode : pl->dirty_mode;
   for (uint32_t p = 0; p < P; ++p) {
-    launch_batch_begin(pl->pe[p].sync, pl->meta_at(p, 0), L + 1, off[p + 1] - off[p], st);
+    const Dirty d = dirty_of(pl, p, dm);
+    launch_batch_begin(pl->pe[p].sync, d.bits, d.list, d.count, d.cap,
+                       pl->pe[p].bm[0].words_padded, st);
     ++launches;
   }
-  const bool coop = (mode == CB_MODE_COOP) && P > 1;
-  const bool ns = pl->kind == CB_NS;
+  const RelabelArgs none{};
 
   if (!coop) {
     for (uint32_t p = 0; p < P; ++p) {
       PeWork& w = pl->pe[p];
       for (int l = 0; l < L; ++l) {
-        LayerBufs b = w.L[l];
-        if (l == 0) {
-          b.dst = const_cast<uint32_t*>(d_seeds) + off[p];
-        } else {
-          b.dst = w.L[l - 1].src;
-          b.cap_dst = w.L[l - 1].cap_src;
+        const uint32_t* D = (l == 0) ? d_seeds + off[p] : w.L[l - 1].src;
+        const uint64_t cap_dst = (l == 0) ? w.L[0].cap_dst : w.L[l - 1].cap_src;
+        RelabelArgs fused = none;
+        uint64_t fused_work = 0;
+        if (l > 0) {
+          const uint32_t* Dp = (l == 1) ? d_seeds + off[p] : w.L[l - 2].src;
+          fused = relabel_args(w.bm[(l - 1) & 1], w.L[l - 1], Dp, pl->meta_at(p, l - 1));
+          fused_work = w.L[l - 1].cap_edges;
         }
-        LayerMeta* me = pl->meta_at(p, l);
-        Bitmap& set_bm = w.bm[l & 1];
-        launch_frontier(g, b, me, pl->kind, pl->fanouts[l], set_bm,
-                        l > 0 ? &w.bm[(l - 1) & 1] : nullptr, w.sync, 4 * l, 8 * l, st);
-        if (ns) {
-          launch_ns(g, b, me, pl->fanouts[l], l, pl->var, set_bm, st);
-          launches += 2;
-        } else {
-          launch_labor(g, b, me, pl->kind, pl->fanouts[l], l, pl->var, set_bm, w.sync,
-                       4 * l + 1, 8 * l + 3, st);
-          ++launches;
-        }
-        launch_extract(set_bm, b.src, b.cap_src, &me->n_src,
-                       l + 1 <= L ? &pl->meta_at(p, l + 1)->n_dst : nullptr, w.sync,
-                       4 * l + 2, 8 * l + 4, st);
-        launch_relabel(set_bm, b, me, st);
-        launches += 3;
+        launches += enqueue_layer(pl, w, p, l, D, cap_dst,
+                                  l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[l & 1], fused,
+                                  fused_work);
+        launch_extract(extract_args(w, w.bm[l & 1], w.bm[(l + 1) & 1].bits, w.L[l].src,
+                                    w.L[l].cap_src, &pl->meta_at(p, l)->n_src,
+                                    &pl->meta_at(p, l + 1)->n_dst, 3 * l + 2, 8 * l + 4),
+                       st);
+        ++launches;
       }
-      launch_clear(w.bm[(L - 1) & 1], w.L[L - 1].src, &pl->meta_at(p, L - 1)->n_src, st);
+      const uint32_t* Dl = (L == 1) ? d_seeds + off[p] : w.L[L - 2].src;
+      launch_relabel(relabel_args(w.bm[(L - 1) & 1], w.L[L - 1], Dl, pl->meta_at(p, L - 1)),
+                     std::max(w.L[L - 1].cap_edges, w.L[L - 1].cap_dst), st);
       ++launches;
     }
   } else {
@@ -385,24 +511,16 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
       uint64_t max_src = 1;
       for (uint32_t p = 0; p < P; ++p) {
         PeWork& w = pl->pe[p];
-        LayerBufs b = w.L[l];
-        if (l == 0) b.dst = const_cast<uint32_t*>(d_seeds) + off[p];
-        LayerMeta* me = pl->meta_at(p, l);
-        launch_frontier(g, b, me, pl->kind, pl->fanouts[l], w.bm[0], l > 0 ? &w.bm[1] : nullptr,
-                        w.sync, 4 * l, 8 * l, st);
-        if (ns) {
-          launch_ns(g, b, me, pl->fanouts[l], l, pl->var, w.bm[0], st);
-          launches += 2;
-        } else {
-          launch_labor(g, b, me, pl->kind, pl->fanouts[l], l, pl->var, w.bm[0], w.sync,
-                       4 * l + 1, 8 * l + 3, st);
-          ++launches;
-        }
-        launch_extract(w.bm[0], b.src, b.cap_src, &me->n_src, nullptr, w.sync, 4 * l + 2,
-                       8 * l + 4, st);
-        launch_relabel(w.bm[0], b, me, st);
-        launches += 3;
-        max_src = std::max(max_src, b.cap_src);
+        const uint32_t* D = (l == 0) ? d_seeds + off[p] : w.L[l].dst;
+        launches += enqueue_layer(pl, w, p, l, D, w.L[l].cap_dst,
+                                  l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[0], none, 0);
+        launch_extract(extract_args(w, w.bm[0], w.bm[1].bits, w.L[l].src, w.L[l].cap_src,
+                                    &pl->meta_at(p, l)->n_src, nullptr, 3 * l + 2, 8 * l + 4),
+                       st);
+        launch_relabel(relabel_args(w.bm[0], w.L[l], D, pl->meta_at(p, l)),
+                       std::max(w.L[l].cap_edges, w.L[l].cap_dst), st);
+        launches += 2;
+        max_src = std::max(max_src, w.L[l].cap_src);
       }
       PartPtrs pp{};
       for (uint32_t p = 0; p < P; ++p) {
@@ -422,22 +540,20 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
         PeWork& w = pl->pe[q];
         uint32_t* next = (l + 1 < L) ? w.L[l + 1].dst : w.owner_final;
         const uint64_t cap = (l + 1 < L) ? w.L[l + 1].cap_dst : w.cap_final;
-        launch_extract(w.bm[1], next, cap, &pl->meta_at(q, l + 1)->n_dst, nullptr, w.sync,
-                       4 * l + 3, 8 * l + 5, st);
+        launch_extract(extract_args(w, w.bm[1], nullptr, next, cap,
+                                    &pl->meta_at(q, l + 1)->n_dst, nullptr, 3 * L + l,
+                                    8 * l + 5),
+                       st);
         ++launches;
       }
       launch_locate(pp, pl->pm->owner, P, max_src, st);
-      ++launches;
-    }
-    for (uint32_t q = 0; q < P; ++q) {
-      PeWork& w = pl->pe[q];
-      launch_clear(w.bm[1], w.owner_final, &pl->meta_at(q, L)->n_dst, st);
       ++launches;
     }
   }
   pl->launches = launches;
   pl->have_batch = true;
   pl->have_rows = false;
+  pl->dirty_mode = mode;
 }
 
 void check_overflow(cb_plan* pl) {
@@ -893,7 +1009,15 @@ int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_devic
           CB_CUDA(cudaMemsetAsync(w.sync.status_c, 0, w.sync.max_tiles * 8, st));
         }
       }
+      if (plan->dirty_mode >= 0 && plan->dirty_mode != plan->cap_mode) {
+        for (uint32_t p = 0; p < plan->P; ++p) {
+          const Dirty d = dirty_of(plan, p, plan->dirty_mode);
+          launch_batch_begin(plan->pe[p].sync, d.bits, d.list, d.count, d.cap,
+                             plan->pe[p].bm[0].words_padded, st);
+        }
+      }
       CB_CUDA(cudaGraphLaunch(plan->exec_sample, st));
+      plan->dirty_mode = plan->cap_mode;
       plan->mode = plan->cap_mode;
       plan->seeds_off = plan->cap_off;
       plan->have_batch = true;
@@ -1056,14 +1180,14 @@ int cb_rows_device(cb_plan* plan, uint32_t part, void** ptr, uint64_t* rows) {
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n) {
   return guard([&] {
     require(plan != nullptr && n != nullptr, "null argument");
-    const uint64_t per_layer = (plan->kind == CB_NS) ? 5 : 4;
+    const uint64_t samp = (plan->kind == CB_NS) ? 3 : 2;  // frontier + labor | ns x2
     const uint64_t P = plan->P;
     const uint64_t L = plan->L;
     uint64_t k;
     if (mode == CB_MODE_COOP && P > 1)
-      k = P + L * (P * per_layer + 1 + P + 1) + P;
+      k = P + L * (P * (samp + 2) + 1 + P + 1);
     else
-      k = P + P * (L * per_layer + 1);
+      k = P * (1 + L * (samp + 1) + 1);
     if (with_gather) k += P;
     *n = k;
   });

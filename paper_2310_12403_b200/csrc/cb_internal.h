@@ -65,8 +65,8 @@ struct LayerMeta {
 
 struct LayerBufs {
   uint32_t* dst = nullptr;          // D_l        (cap_dst)
-  uint32_t* act_di = nullptr;       // dst index of each active dst (cap_dst)
-  uint64_t* act_pre = nullptr;      // scan prefix of active dsts (cap_dst+1)
+  struct ActRec* act = nullptr;     // records of active dsts (cap_dst+1)
+  uint32_t* tile_first = nullptr;   // scan tile -> first record (max_tiles+1)
   uint64_t* out_prefix = nullptr;   // NS output prefix (cap_dst+1)
   uint32_t* slots = nullptr;        // NS reservoir slots (cap_edges)
   uint2* edges = nullptr;           // (src_idx, dst_idx) (cap_edges)
@@ -79,7 +79,7 @@ struct LayerBufs {
 // Device scratch shared by every kernel of a PE's batch.
 struct Sync {
   unsigned* epoch = nullptr;                  // [1] batch epoch (device)
-  unsigned* tickets = nullptr;                // [kMaxTickets]
+  unsigned* tickets = nullptr;                // [2*kMaxTickets]: ticket, exit ctr
   unsigned long long* status_a = nullptr;     // [max_tiles]
   unsigned long long* status_b = nullptr;     // [max_tiles]
   unsigned long long* status_c = nullptr;     // [max_tiles]
@@ -95,26 +95,110 @@ struct Bitmap {
   uint64_t words = 0, words_padded = 0;
 };
 
+// Packed record of one active dst (scan work > 0), written by the frontier
+// kernel so the scan-space kernels need one 32-byte load per dst.
+//   LABOR/FULL: a = row base (indices[a + x] is the neighbour at position x),
+//               b = integer keep threshold floor((k/d)*2^53) (plain), the
+//                   double bits of k/d (smoothed), or ~0 = keep all
+//   NS        : a = output offset of the dst's k slots, b = hash prefix
+//               {kStreamNs, layer, s} under z1
+struct ActRec {
+  unsigned long long pre;  // scan-space prefix
+  unsigned long long a;
+  unsigned long long b;
+  uint32_t di;             // index into D
+  uint32_t d;              // degree
+};
+
+struct FrontierArgs {
+  const uint32_t* D;
+  LayerMeta* meta;
+  unsigned long long n_dst_param;  // ~0 = read meta->n_dst
+  const uint64_t* indptr;
+  int kind;
+  uint32_t k;
+  int layer;
+  const cbdev::Variates* var;
+  uint32_t* set_bits;
+  ActRec* act;
+  uint32_t* tile_first;
+  uint64_t* out_prefix;
+  uint32_t* slots;
+  uint64_t cap_edges;
+  unsigned* ticket;
+  unsigned* exit_ctr;
+  unsigned long long *st_a, *st_b, *st_c;
+  const unsigned* epoch;
+  int slot;
+  unsigned* overflow;
+};
+
+struct LaborArgs {
+  LayerMeta* meta;
+  const ActRec* act;
+  const uint32_t* tile_first;
+  const uint32_t* D;
+  const uint32_t* indices;
+  int kind;
+  uint32_t k;
+  int layer;
+  const cbdev::Variates* var;
+  uint32_t* bits;
+  uint2* edges;
+  uint32_t* slots;
+  uint64_t cap_edges;
+  unsigned* ticket;
+  unsigned* exit_ctr;
+  unsigned long long* status;
+  const unsigned* epoch;
+  int slot;
+  unsigned* overflow;
+};
+
+struct ExtractArgs {
+  const uint32_t* bits;
+  uint32_t* wprefix;
+  uint32_t* zero_bits;  // optional: bitmap zeroed word-for-word on the way
+  uint64_t words_padded;
+  uint32_t* out;
+  uint64_t cap_out;
+  unsigned long long* count_out;
+  unsigned long long* count_out2;
+  unsigned* ticket;
+  unsigned* exit_ctr;
+  unsigned long long* status;
+  const unsigned* epoch;
+  int slot;
+  unsigned* overflow;
+};
+
+struct RelabelArgs {  // edges == nullptr disables
+  const uint32_t* bits;
+  const uint32_t* wprefix;
+  const LayerMeta* meta;
+  uint2* edges;
+  uint64_t cap_edges;
+  const uint32_t* D;
+  uint32_t* dst_pos;
+};
+
+constexpr int kExtractTileWords = 512;
+constexpr int kLaborTile = 2048;
+constexpr int kFrontierTile = 1024;
+
 // ----------------------------------------------------- kernel launchers ----
 // sample.cu
-void launch_batch_begin(const Sync& s, LayerMeta* meta, int num_layers, uint64_t n_seeds,
-                        cudaStream_t st);
-void launch_frontier(const DeviceGraph& g, const LayerBufs& b, LayerMeta* meta, int kind,
-                     uint32_t fanout, Bitmap& set_bm, const Bitmap* clear_bm,
-                     const Sync& s, int ticket_base, int epoch_slot, cudaStream_t st);
-void launch_labor(const DeviceGraph& g, const LayerBufs& b, LayerMeta* meta, int kind,
-                  uint32_t fanout, int layer, const cbdev::Variates* var, Bitmap& bm,
-                  const Sync& s, int ticket, int epoch_slot, cudaStream_t st);
-void launch_ns(const DeviceGraph& g, const LayerBufs& b, LayerMeta* meta, uint32_t fanout,
-               int layer, const cbdev::Variates* var, Bitmap& bm, cudaStream_t st);
-void launch_extract(const Bitmap& bm, uint32_t* out, uint64_t cap_out,
-                    unsigned long long* count_out, unsigned long long* count_out2,
-                    const Sync& s, int ticket, int epoch_slot, cudaStream_t st);
-constexpr int kExtractTileWords = 2048;
-constexpr int kLaborTile = 1024;
-constexpr int kFrontierTile = 1024;
-void launch_relabel(const Bitmap& bm, const LayerBufs& b, const LayerMeta* meta,
-                    cudaStream_t st);
+void launch_batch_begin(const Sync& s, uint32_t* clear_bits, const uint32_t* clear_list,
+                        const unsigned long long* clear_count, uint64_t clear_cap,
+                        uint64_t nwords, cudaStream_t st);
+void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_dst,
+                     uint64_t relabel_work, cudaStream_t st);
+void launch_labor(const LaborArgs& a, uint64_t max_tiles, cudaStream_t st);
+void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix,
+               const uint64_t* indptr, const uint32_t* indices, uint64_t cap_dst,
+               cudaStream_t st);
+void launch_extract(const ExtractArgs& a, cudaStream_t st);
+void launch_relabel(const RelabelArgs& r, uint64_t work, cudaStream_t st);
 void launch_clear(Bitmap& bm, const uint32_t* list, const unsigned long long* count,
                   cudaStream_t st);
 void launch_rank(const Bitmap& bm, const uint32_t* ids, const unsigned long long* count,

@@ -2,18 +2,23 @@
 // (samplers.cpp:62-136, 289-296) plus the bitmap dedup/relabel that replaces
 // BlockBuilder::finish (samplers.cpp:28-54).
 //
-// Per layer the pipeline is
-//   frontier  : degree scan of D (scan-space prefix), marks D in the bitmap,
-//               clears the previous layer's bitmap words, NS slot init
-//   labor/ns  : scan-space tiles over all neighbour positions; keep rule /
-//               reservoir; order-preserving compaction via ballot + decoupled
-//               look-back (edges land grouped by dst, CSR order inside a dst,
-//               slot order for NS hubs — exactly the reference order);
-//               kept ids are OR-ed into the bitmap
-//   extract   : bitmap popcount scan -> sorted unique src list + word ranks
-//   relabel   : edge (t, di) -> (rank(t), di); dst_pos = rank(D)
-// No host synchronisation: every count lives in device LayerMeta and all
-// kernels are persistent (ticketed) loops bounded by those counts.
+// Per layer (indep / P = 1 order):
+//   frontier(l) : [relabel of layer l-1 fused in] degree scan of D_l with
+//                 three look-back scans -> packed records of the active dsts
+//                 (ActRec: scan prefix, row base, threshold / NS hash prefix),
+//                 a scan-tile -> first-record map, NS output prefix and slot
+//                 init; marks D_l in the layer bitmap
+//   labor(l)    : scan-space tiles over every neighbour position; keep rule;
+//                 order-preserving compaction (ballot + decoupled look-back),
+//                 so edges land grouped by dst, CSR order inside a dst — the
+//                 reference order; kept ids OR-ed into the bitmap
+//   ns(l)       : reservoir via per-slot atomicMax, then slot-order emission
+//   extract(l)  : bitmap popcount scan -> sorted unique src list + word ranks;
+//                 zeroes the other (previous-layer) bitmap on the way
+//   relabel     : edge (t, di) -> (rank(t), di); dst_pos = rank(D) (fused into
+//                 the next frontier; standalone only after the last layer)
+// No host synchronisation: all counts live in device LayerMeta; every kernel
+// is a persistent ticketed loop bounded by those counts.
 #include "cb_internal.h"
 
 namespace cb {
@@ -37,55 +42,96 @@ __device__ __forceinline__ uint32_t bm_rank(const uint32_t* bits, const uint32_t
   return wprefix[w] + __popc(bits[w] & ((1u << (v & 31u)) - 1u));
 }
 
+// Reset a ticket counter once every CTA of the launch is done with it, so no
+// per-batch memset of the tickets is needed.
+__device__ __forceinline__ void retire_ticket(unsigned* ticket, unsigned* exit_ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(exit_ctr, 1u) == gridDim.x - 1) {
+      *ticket = 0;
+      *exit_ctr = 0;
+      __threadfence();
+    }
+  }
+}
+
+__device__ void relabel_range(const RelabelArgs& r, uint64_t tid, uint64_t stride) {
+  const uint64_t ne = min(static_cast<uint64_t>(r.meta->n_edges), r.cap_edges);
+  const uint64_t nd = r.meta->n_dst;
+  for (uint64_t e = tid; e < ne; e += stride) {
+    uint2 x = r.edges[e];
+    x.x = bm_rank(r.bits, r.wprefix, x.x);
+    r.edges[e] = x;
+  }
+  for (uint64_t i = tid; i < nd; i += stride) r.dst_pos[i] = bm_rank(r.bits, r.wprefix, r.D[i]);
+}
+
 // ------------------------------------------------------------ batch begin --
-__global__ void batch_begin_kernel(unsigned* epoch, unsigned* tickets, int n_tickets,
-                                   LayerMeta* meta, int n_meta, unsigned long long n_seeds,
-                                   unsigned* overflow) {
-  const int t = threadIdx.x;
-  if (t == 0) {
+// Clears the previous batch's last bitmap (its final id list), bumps the
+// look-back epoch, resets the overflow flag. One launch per batch.
+__global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, uint32_t* clear_bits,
+                                   const uint32_t* __restrict__ clear_list,
+                                   const unsigned long long* clear_count, uint64_t cap,
+                                   uint64_t nwords) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     *epoch = *epoch + 1;
     *overflow = 0;
   }
-  for (int i = t; i < n_tickets; i += blockDim.x) tickets[i] = 0;
-  for (int i = t; i < n_meta * 8; i += blockDim.x)
-    reinterpret_cast<unsigned long long*>(meta)[i] = 0;
-  __syncthreads();
-  if (t == 0) meta[0].n_dst = n_seeds;
+  if (!clear_bits) return;
+  const uint64_t n = min(static_cast<uint64_t>(*clear_count), cap);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += stride) {
+    const uint32_t w = clear_list[i] >> 5;
+    if (w < nwords) clear_bits[w] = 0u;
+  }
 }
 
 // ---------------------------------------------------------------- frontier --
 // kind: 0 FULL, 1 NS, 2 LABOR0 (samplers.hpp:15). Per dst: scan work q
 // (LABOR/FULL: d; NS: reservoir positions max(d-k,0)), active flag q>0 and,
-// for NS, the output count min(d,k). Three look-back scans give the active
-// list (bounded dsts per scan tile), its scan prefix and the NS out prefix.
+// for NS, the output count min(d,k).
 template <int IPT>
-__global__ void __launch_bounds__(kNT) frontier_kernel(
-    const uint32_t* __restrict__ D, LayerMeta* meta, const uint64_t* __restrict__ indptr,
-    int kind, uint32_t k, uint32_t* set_bits, uint32_t* clear_bits, uint32_t* act_di,
-    uint64_t* act_pre, uint64_t* out_prefix, uint32_t* slots, uint64_t cap_edges,
-    unsigned* ticket, unsigned long long* st_a, unsigned long long* st_b,
-    unsigned long long* st_c, const unsigned* epoch_p, int slot, unsigned* overflow) {
+__global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelArgs r) {
   __shared__ unsigned long long s_scan[3][kNT / 32 + 1];
   __shared__ unsigned long long s_bc[3];
   __shared__ unsigned s_tile;
-  const uint64_t n = meta->n_dst;
+  if (r.edges) {  // relabel of the previous layer (independent work)
+    relabel_range(r, blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
+                  static_cast<uint64_t>(gridDim.x) * blockDim.x);
+  }
+  LayerMeta* meta = a.meta;
+  if (a.n_dst_param != ~0ULL && blockIdx.x == 0 && threadIdx.x == 0)
+    meta->n_dst = a.n_dst_param;
+  const uint64_t n = (a.n_dst_param != ~0ULL) ? a.n_dst_param : meta->n_dst;
   constexpr int TILE = kNT * IPT;
   const uint64_t ntiles = (n + TILE - 1) / TILE;
-  const bool is_ns = (kind == 1);
-  for (unsigned tile = next_tile(ticket, &s_tile); tile < ntiles;
-       tile = next_tile(ticket, &s_tile)) {
+  const bool is_ns = (a.kind == 1);
+  const bool full = (a.kind == 0);
+  const Variates v = *a.var;
+  const bool smooth = v.smoothed != 0;
+  const uint64_t z1p = hstep(hstep(hinit(v.z1), 1ULL), static_cast<uint64_t>(a.layer));
+  const uint32_t k = a.k;
+  for (unsigned tile = next_tile(a.ticket, &s_tile); tile < ntiles;
+       tile = next_tile(a.ticket, &s_tile)) {
     const uint64_t i0 = static_cast<uint64_t>(tile) * TILE + threadIdx.x * IPT;
     unsigned long long q[IPT], o[IPT];
+    uint32_t vv[IPT];
+    uint64_t rs[IPT];
     unsigned long long qs = 0, as = 0, os = 0;
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const uint64_t i = i0 + j;
       q[j] = o[j] = 0;
+      vv[j] = 0;
+      rs[j] = 0;
       if (i < n) {
-        const uint32_t v = D[i];
-        const uint64_t d = indptr[v + 1] - indptr[v];
-        set_bit(set_bits, v);
-        if (clear_bits) clear_bits[v >> 5] = 0u;
+        const uint32_t vx = a.D[i];
+        vv[j] = vx;
+        rs[j] = a.indptr[vx];
+        const uint64_t d = a.indptr[vx + 1] - rs[j];
+        set_bit(a.set_bits, vx);
         if (is_ns) {
           q[j] = d > k ? d - k : 0;
           o[j] = d < k ? d : k;
@@ -102,11 +148,12 @@ __global__ void __launch_bounds__(kNT) frontier_kernel(
     unsigned long long ea = block_exclusive_scan<kNT>(as, s_scan[1], ta);
     unsigned long long eo = 0;
     if (is_ns) eo = block_exclusive_scan<kNT>(os, s_scan[2], to);
-    const unsigned long long bq = tile_prefix(st_a, tile, tq, inv_epoch(epoch_p, slot), &s_bc[0]);
+    const unsigned long long bq =
+        tile_prefix(a.st_a, tile, tq, inv_epoch(a.epoch, a.slot), &s_bc[0]);
     const unsigned long long ba =
-        tile_prefix(st_b, tile, ta, inv_epoch(epoch_p, slot + 1), &s_bc[1]);
+        tile_prefix(a.st_b, tile, ta, inv_epoch(a.epoch, a.slot + 1), &s_bc[1]);
     unsigned long long bo = 0;
-    if (is_ns) bo = tile_prefix(st_c, tile, to, inv_epoch(epoch_p, slot + 2), &s_bc[2]);
+    if (is_ns) bo = tile_prefix(a.st_c, tile, to, inv_epoch(a.epoch, a.slot + 2), &s_bc[2]);
     eq += bq;
     ea += ba;
     eo += bo;
@@ -115,123 +162,120 @@ __global__ void __launch_bounds__(kNT) frontier_kernel(
       const uint64_t i = i0 + j;
       if (i < n) {
         if (q[j] > 0) {
-          act_di[ea] = static_cast<uint32_t>(i);
-          act_pre[ea] = eq;
+          ActRec rec;
+          rec.pre = eq;
+          rec.di = static_cast<uint32_t>(i);
+          const uint64_t d = is_ns ? q[j] + k : q[j];
+          rec.d = static_cast<uint32_t>(d);
+          if (is_ns) {
+            rec.a = eo;                  // output offset of the slots
+            rec.b = hstep(z1p, vv[j]);   // prefix({kStreamNs, layer, s}) under z1
+            if (eo + k <= a.cap_edges)   // hub: slots start as the identity
+              for (uint32_t r2 = 0; r2 < k; ++r2) a.slots[eo + r2] = r2;
+          } else {
+            rec.a = rs[j] - eq;          // indices[rec.a + x] = neighbour at x
+            if (full || d <= k) {
+              rec.b = ~0ULL;
+            } else {
+              const double thr = __ddiv_rn(static_cast<double>(k), static_cast<double>(d));
+              rec.b = smooth ? static_cast<unsigned long long>(__double_as_longlong(thr))
+                             : __double2ull_rz(__dmul_rn(thr, 0x1.0p53));
+            }
+          }
+          a.act[ea] = rec;
+          // scan tiles whose first position falls inside this record
+          const uint64_t t_first = (eq + kLaborTile - 1) / kLaborTile;
+          const uint64_t t_last = (eq + q[j] - 1) / kLaborTile;
+          for (uint64_t t = t_first; t <= t_last; ++t) a.tile_first[t] = static_cast<uint32_t>(ea);
           ++ea;
         }
-        if (is_ns) {
-          out_prefix[i] = eo;
-          if (q[j] > 0 && eo + k <= cap_edges)  // hub: slots start as identity
-            for (uint32_t r = 0; r < k; ++r) slots[eo + r] = r;
-        }
+        if (is_ns) a.out_prefix[i] = eo;
       }
       eq += q[j];
       eo += o[j];
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
-      act_pre[ba + ta] = bq + tq;
-      meta->scan_total = bq + tq;
-      meta->n_active = ba + ta;
+      const uint64_t tot = bq + tq, nact = ba + ta;
+      ActRec sent{};
+      sent.pre = tot;
+      a.act[nact] = sent;
+      a.tile_first[(tot + kLaborTile - 1) / kLaborTile] = static_cast<uint32_t>(nact);
+      meta->scan_total = tot;
+      meta->n_active = nact;
+      meta->uncertified = 0;
       if (is_ns) {
-        out_prefix[n] = bo + to;
+        a.out_prefix[n] = bo + to;
         meta->n_edges = bo + to;
-        if (bo + to > cap_edges) atomicExch(overflow, 1u);
+        if (bo + to > a.cap_edges) atomicExch(a.overflow, 1u);
       }
     }
   }
   if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
-    act_pre[0] = 0;
-    if (is_ns) out_prefix[0] = 0;
+    ActRec sent{};
+    a.act[0] = sent;
+    a.tile_first[0] = 0;
+    meta->scan_total = 0;
+    meta->n_active = 0;
+    meta->uncertified = 0;
+    meta->n_edges = 0;
+    if (is_ns) a.out_prefix[0] = 0;
   }
+  retire_ticket(a.ticket, a.exit_ctr);
 }
 
-// ---------------------------------------------------------- segment tiles --
-// Active entries [a0, a1] covering scan positions [x0, x1): at most
-// x1-x0 entries because every active dst owns >= 1 position.
-__device__ __forceinline__ void tile_segment(const uint64_t* prefix, uint64_t n_act,
-                                             uint64_t x0, uint64_t x1, int* s_range) {
-  if (threadIdx.x == 0) {
-    int lo = 0, hi = static_cast<int>(n_act);
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (prefix[mid] <= x0) lo = mid;
-      else hi = mid;
-    }
-    s_range[0] = lo;
-    int lo2 = lo;
-    hi = static_cast<int>(n_act);
-    while (hi - lo2 > 1) {
-      const int mid = (lo2 + hi) >> 1;
-      if (prefix[mid] <= x1 - 1) lo2 = mid;
-      else hi = mid;
-    }
-    s_range[1] = lo2;
+// Largest record index in [lo, hi] whose scan prefix is <= x.
+__device__ __forceinline__ uint32_t rec_search(const ActRec* __restrict__ act, uint32_t lo,
+                                               uint32_t hi, uint64_t x) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(&act[mid].pre) <= x) lo = mid;
+    else hi = mid - 1;
   }
-  __syncthreads();
+  return lo;
+}
+
+// Record range [a0, a1] overlapping scan tile [x0, x1).
+__device__ __forceinline__ void tile_records(const ActRec* act, const uint32_t* tile_first,
+                                             uint64_t n_act, uint64_t tile, uint64_t x1,
+                                             uint32_t& a0, uint32_t& a1) {
+  a0 = __ldg(&tile_first[tile]);
+  const uint32_t ae = __ldg(&tile_first[tile + 1]);
+  a1 = (ae < n_act && __ldg(&act[ae].pre) < x1) ? ae : ae - 1;
 }
 
 // ------------------------------------------------------------- LABOR/FULL --
 // keep(t -> s) iff U(hash(z1,{2,layer,t})) <= k/d_s  (samplers.cpp:117-134);
 // plain stream compared in integers: (h>>11) <= floor((k/d)*2^53), exact.
 template <int IPT>
-__global__ void __launch_bounds__(kNT) labor_kernel(
-    const uint32_t* __restrict__ D, LayerMeta* meta, const uint32_t* __restrict__ act_di,
-    const uint64_t* __restrict__ act_pre, const uint64_t* __restrict__ indptr,
-    const uint32_t* __restrict__ indices, int kind, uint32_t k, int layer,
-    const Variates* __restrict__ var, uint32_t* bits, uint2* edges, uint64_t cap_edges,
-    unsigned* ticket, unsigned long long* status, const unsigned* epoch_p, int slot,
-    unsigned* overflow) {
+__global__ void __launch_bounds__(kNT) labor_kernel(LaborArgs a) {
   constexpr int TILE = kNT * IPT;
+  static_assert(TILE == kLaborTile, "tile size shared with frontier");
   constexpr int NW = kNT / 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* s_dp = reinterpret_cast<uint64_t*>(smem_raw);  // [TILE+1]
-  uint64_t* s_rs = s_dp + (TILE + 1);                      // [TILE]
-  uint64_t* s_th = s_rs + TILE;                            // [TILE]
-  uint32_t* s_di = reinterpret_cast<uint32_t*>(s_th + TILE);  // [TILE]
   __shared__ unsigned s_cnt[IPT * NW];
   __shared__ unsigned s_base[IPT * NW];
   __shared__ unsigned long long s_b;
   __shared__ unsigned s_tile;
-  __shared__ int s_range[2];
   __shared__ unsigned s_total;
 
+  LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
   const uint64_t n_act = meta->n_active;
   const uint64_t ntiles = (total + TILE - 1) / TILE;
-  const unsigned ep = inv_epoch(epoch_p, slot);
-  const Variates v = *var;
-  const bool full = (kind == 0);
-  const bool smooth = v.smoothed != 0 && !full;
+  const unsigned ep = inv_epoch(a.epoch, a.slot);
+  const Variates v = *a.var;
+  const bool smooth = v.smoothed != 0 && a.kind != 0;
   // prefix({kStreamLabor, layer}) under z1 (and z2 when smoothed)
-  const uint64_t p1 = hstep(hstep(hinit(v.z1), 2ULL), static_cast<uint64_t>(layer));
-  const uint64_t p2 = hstep(hstep(hinit(v.z2), 2ULL), static_cast<uint64_t>(layer));
+  const uint64_t p1 = hstep(hstep(hinit(v.z1), 2ULL), static_cast<uint64_t>(a.layer));
+  const uint64_t p2 = hstep(hstep(hinit(v.z2), 2ULL), static_cast<uint64_t>(a.layer));
   const unsigned w = threadIdx.x >> 5;
   unsigned long long uncert = 0;
 
-  for (unsigned tile = next_tile(ticket, &s_tile); tile < ntiles;
-       tile = next_tile(ticket, &s_tile)) {
+  for (unsigned tile = next_tile(a.ticket, &s_tile); tile < ntiles;
+       tile = next_tile(a.ticket, &s_tile)) {
     const uint64_t x0 = static_cast<uint64_t>(tile) * TILE;
     const uint64_t x1 = min(x0 + TILE, total);
-    tile_segment(act_pre, n_act, x0, x1, s_range);
-    const int a0 = s_range[0];
-    const int nd = s_range[1] - a0 + 1;
-    for (int i = threadIdx.x; i <= nd; i += kNT) s_dp[i] = act_pre[a0 + i];
-    __syncthreads();
-    for (int i = threadIdx.x; i < nd; i += kNT) {
-      const uint32_t di = act_di[a0 + i];
-      const uint32_t s = D[di];
-      s_di[i] = di;
-      s_rs[i] = indptr[s] - s_dp[i];  // indices[s_rs + x] is the neighbour at x
-      const uint64_t d = s_dp[i + 1] - s_dp[i];
-      if (full) {
-        s_th[i] = ~0ULL;
-      } else {
-        const double thr = __ddiv_rn(static_cast<double>(k), static_cast<double>(d));
-        if (smooth) s_th[i] = static_cast<uint64_t>(__double_as_longlong(thr));
-        else s_th[i] = (d <= k) ? ~0ULL : __double2ull_rz(__dmul_rn(thr, 0x1.0p53));
-      }
-    }
-    __syncthreads();
+    uint32_t a0, a1;
+    tile_records(a.act, a.tile_first, n_act, tile, x1, a0, a1);
 
     uint32_t tv[IPT];
     uint32_t dv[IPT];
@@ -239,31 +283,29 @@ __global__ void __launch_bounds__(kNT) labor_kernel(
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const uint64_t x = x0 + static_cast<uint64_t>(j) * kNT + threadIdx.x;
-      bool keep = false;
       tv[j] = 0;
-      dv[j] = 0;
+      dv[j] = 0xffffffffu;
       if (x < x1) {
-        const int li = seg_search(s_dp, 0, nd, x);
-        const uint32_t t = __ldg(indices + s_rs[li] + x);
-        tv[j] = t;
-        dv[j] = s_di[li];
-        const uint64_t th = s_th[li];
-        if (!smooth) {
-          keep = (th == ~0ULL) || (hstep(p1, t) >> 11) <= th;
+        const uint32_t li = rec_search(a.act, a0, a1, x);
+        const ActRec rec = a.act[li];
+        tv[j] = __ldg(a.indices + rec.a + x);
+        dv[j] = rec.di;
+        if (rec.b == ~0ULL) {
+          keepmask |= 1u << j;
+        } else if (!smooth) {
+          if ((hstep(p1, tv[j]) >> 11) <= rec.b) keepmask |= 1u << j;
         } else {
-          const double thr = __longlong_as_double(static_cast<long long>(th));
-          if (thr >= 1.0) {
-            keep = true;  // r < 1 always (phi of a finite normal)
-          } else {
-            const double r = smooth_finish(v, hstep(p1, t), hstep(p2, t));
-            keep = r <= thr;
-            if (fabs(r - thr) <= kGuard * thr) ++uncert;
-          }
+          const double thr = __longlong_as_double(static_cast<long long>(rec.b));
+          const double r = smooth_finish(v, hstep(p1, tv[j]), hstep(p2, tv[j]));
+          if (r <= thr) keepmask |= 1u << j;
+          if (fabs(r - thr) <= kGuard * thr) ++uncert;
         }
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    }
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const unsigned bal = __ballot_sync(0xffffffffu, (keepmask >> j) & 1u);
       if (lane_id() == 0) s_cnt[j * NW + w] = __popc(bal);
-      if (keep) keepmask |= 1u << j;
     }
     __syncthreads();
     if (w == 0) {  // exclusive scan over IPT*NW (j-major) counters, 2 per lane
@@ -279,26 +321,27 @@ __global__ void __launch_bounds__(kNT) labor_kernel(
     }
     __syncthreads();
     const unsigned agg = s_total;
-    const unsigned long long gb = tile_prefix(status, tile, agg, ep, &s_b);
+    const unsigned long long gb = tile_prefix(a.status, tile, agg, ep, &s_b);
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const bool keep = (keepmask >> j) & 1u;
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (keep) {
         const unsigned long long pos = gb + s_base[j * NW + w] + __popc(bal & lanemask_lt());
-        if (pos < cap_edges) edges[pos] = make_uint2(tv[j], dv[j]);
-        set_bit(bits, tv[j]);
+        if (pos < a.cap_edges) a.edges[pos] = make_uint2(tv[j], dv[j]);
+        set_bit(a.bits, tv[j]);
       }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       meta->n_edges = gb + agg;
-      if (gb + agg > cap_edges) atomicExch(overflow, 1u);
+      if (gb + agg > a.cap_edges) atomicExch(a.overflow, 1u);
     }
   }
   if (smooth) {
     uncert = warp_sum(uncert);
     if (lane_id() == 0 && uncert) atomicAdd(&meta->uncertified, uncert);
   }
+  retire_ticket(a.ticket, a.exit_ctr);
 }
 
 // ---------------------------------------------------------------- NS -------
@@ -306,62 +349,45 @@ __global__ void __launch_bounds__(kNT) labor_kernel(
 // j is the largest i in [k, d) with floor(U_i*(i+1)) == j, else j. Every
 // position is an independent atomicMax, so hub rows split across CTAs.
 template <int IPT>
-__global__ void __launch_bounds__(kNT) ns_reservoir_kernel(
-    const uint32_t* __restrict__ D, LayerMeta* meta, const uint32_t* __restrict__ act_di,
-    const uint64_t* __restrict__ act_pre, const uint64_t* __restrict__ out_prefix,
-    uint32_t k, int layer, const Variates* __restrict__ var, uint32_t* slots,
-    uint64_t cap_edges) {
+__global__ void __launch_bounds__(kNT) ns_reservoir_kernel(LaborArgs a) {
   constexpr int TILE = kNT * IPT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* s_dp = reinterpret_cast<uint64_t*>(smem_raw);  // [TILE+1]
-  uint64_t* s_op = s_dp + (TILE + 1);                      // [TILE]
-  uint64_t* s_h1 = s_op + TILE;                            // [TILE]
-  uint64_t* s_h2 = s_h1 + TILE;                            // [TILE]
-  __shared__ int s_range[2];
+  static_assert(TILE == kLaborTile, "tile size shared with frontier");
+  LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
   const uint64_t n_act = meta->n_active;
   const uint64_t ntiles = (total + TILE - 1) / TILE;
-  const Variates v = *var;
+  const Variates v = *a.var;
   const bool smooth = v.smoothed != 0;
-  const uint64_t z1p = hstep(hstep(hinit(v.z1), 1ULL), static_cast<uint64_t>(layer));
-  const uint64_t z2p = hstep(hstep(hinit(v.z2), 1ULL), static_cast<uint64_t>(layer));
+  const uint64_t z2p = hstep(hstep(hinit(v.z2), 1ULL), static_cast<uint64_t>(a.layer));
+  const uint32_t k = a.k;
   unsigned long long uncert = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t x0 = tile * TILE;
     const uint64_t x1 = min(x0 + TILE, total);
-    __syncthreads();
-    tile_segment(act_pre, n_act, x0, x1, s_range);
-    const int a0 = s_range[0];
-    const int nd = s_range[1] - a0 + 1;
-    for (int i = threadIdx.x; i <= nd; i += kNT) s_dp[i] = act_pre[a0 + i];
-    for (int i = threadIdx.x; i < nd; i += kNT) {
-      const uint32_t di = act_di[a0 + i];
-      const uint32_t s = D[di];
-      s_op[i] = out_prefix[di];
-      s_h1[i] = hstep(z1p, s);  // prefix({kStreamNs, layer, s})
-      s_h2[i] = smooth ? hstep(z2p, s) : 0;
-    }
-    __syncthreads();
+    uint32_t a0, a1;
+    tile_records(a.act, a.tile_first, n_act, tile, x1, a0, a1);
 #pragma unroll 4
     for (int j = 0; j < IPT; ++j) {
       const uint64_t x = x0 + static_cast<uint64_t>(j) * kNT + threadIdx.x;
       if (x < x1) {
-        const int li = seg_search(s_dp, 0, nd, x);
-        const uint64_t i = k + (x - s_dp[li]);
+        const uint32_t li = rec_search(a.act, a0, a1, x);
+        const ActRec rec = a.act[li];
+        const uint64_t i = k + (x - rec.pre);
         const double scale = static_cast<double>(i + 1);
         double u;
         if (!smooth) {
-          u = ufb(hstep(s_h1[li], i));
+          u = ufb(hstep(rec.b, i));
         } else {
-          u = smooth_finish(v, hstep(s_h1[li], i), hstep(s_h2[li], i));
+          const uint64_t h2 = hstep(z2p, a.D[rec.di]);
+          u = smooth_finish(v, hstep(rec.b, i), hstep(h2, i));
           const double y = __dmul_rn(u, scale);
           const double fr = y - floor(y + 0.5);
           if (fabs(fr) <= kGuard * y && y >= 0.5) ++uncert;
         }
         const uint64_t r = __double2ull_rz(__dmul_rn(u, scale));
         if (r < k) {
-          const uint64_t pos = s_op[li] + r;
-          if (pos < cap_edges) atomicMax(&slots[pos], static_cast<uint32_t>(i));
+          const uint64_t pos = rec.a + r;
+          if (pos < a.cap_edges) atomicMax(&a.slots[pos], static_cast<uint32_t>(i));
         }
       }
     }
@@ -412,30 +438,25 @@ __global__ void __launch_bounds__(kNT) ns_emit_kernel(
 
 // ---------------------------------------------------------------- extract --
 // Sorted unique list = set bits in id order; wprefix[w] = rank of word w.
-constexpr int kWPT = 8;  // words per thread (two 16-byte loads)
-__global__ void __launch_bounds__(kNT) extract_kernel(
-    const uint32_t* __restrict__ bits, uint32_t* wprefix, uint64_t words_padded,
-    uint32_t* out, uint64_t cap_out, unsigned long long* count_out,
-    unsigned long long* count_out2, unsigned* ticket, unsigned long long* status,
-    const unsigned* epoch_p, int slot, unsigned* overflow) {
+constexpr int kWPT = 2;  // words per thread (one 8-byte load)
+static_assert(kNT * kWPT == kExtractTileWords, "extract tile");
+__global__ void __launch_bounds__(kNT) extract_kernel(ExtractArgs a) {
   __shared__ unsigned long long s_scan[kNT / 32 + 1];
   __shared__ unsigned long long s_b;
   __shared__ unsigned s_tile;
   constexpr int TILE = kNT * kWPT;
-  const uint64_t ntiles = words_padded / TILE;
-  const unsigned ep = inv_epoch(epoch_p, slot);
-  for (unsigned tile = next_tile(ticket, &s_tile); tile < ntiles;
-       tile = next_tile(ticket, &s_tile)) {
+  const uint64_t ntiles = a.words_padded / TILE;
+  const unsigned ep = inv_epoch(a.epoch, a.slot);
+  for (unsigned tile = next_tile(a.ticket, &s_tile); tile < ntiles;
+       tile = next_tile(a.ticket, &s_tile)) {
     const uint64_t w0 = static_cast<uint64_t>(tile) * TILE + threadIdx.x * kWPT;
-    const uint4 a = *reinterpret_cast<const uint4*>(bits + w0);
-    const uint4 b = *reinterpret_cast<const uint4*>(bits + w0 + 4);
-    const uint32_t wv[kWPT] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    unsigned long long c = 0;
-#pragma unroll
-    for (int j = 0; j < kWPT; ++j) c += __popc(wv[j]);
+    const uint2 wv2 = *reinterpret_cast<const uint2*>(a.bits + w0);
+    if (a.zero_bits) *reinterpret_cast<uint2*>(a.zero_bits + w0) = make_uint2(0u, 0u);
+    const uint32_t wv[kWPT] = {wv2.x, wv2.y};
+    unsigned long long c = __popc(wv[0]) + __popc(wv[1]);
     unsigned long long tot;
     const unsigned long long ex = block_exclusive_scan<kNT>(c, s_scan, tot);
-    const unsigned long long gb = tile_prefix(status, tile, tot, ep, &s_b);
+    const unsigned long long gb = tile_prefix(a.status, tile, tot, ep, &s_b);
     unsigned long long pos = gb + ex;
     uint32_t pw[kWPT];
 #pragma unroll
@@ -445,37 +466,24 @@ __global__ void __launch_bounds__(kNT) extract_kernel(
       while (x) {
         const int bit = __ffs(x) - 1;
         x &= x - 1;
-        if (pos < cap_out) out[pos] = static_cast<uint32_t>((w0 + j) * 32 + bit);
+        if (pos < a.cap_out) a.out[pos] = static_cast<uint32_t>((w0 + j) * 32 + bit);
         ++pos;
       }
     }
-    *reinterpret_cast<uint4*>(wprefix + w0) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-    *reinterpret_cast<uint4*>(wprefix + w0 + 4) = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+    *reinterpret_cast<uint2*>(a.wprefix + w0) = make_uint2(pw[0], pw[1]);
     if (tile == ntiles - 1 && threadIdx.x == 0) {
-      *count_out = gb + tot;
-      if (count_out2) *count_out2 = gb + tot;
-      if (gb + tot > cap_out) atomicExch(overflow, 1u);
+      *a.count_out = gb + tot;
+      if (a.count_out2) *a.count_out2 = gb + tot;
+      if (gb + tot > a.cap_out) atomicExch(a.overflow, 1u);
     }
   }
+  retire_ticket(a.ticket, a.exit_ctr);
 }
 
 // ---------------------------------------------------------------- relabel --
-__global__ void relabel_kernel(const uint32_t* __restrict__ bits,
-                               const uint32_t* __restrict__ wprefix, const LayerMeta* meta,
-                               uint2* edges, uint64_t cap_edges,
-                               const uint32_t* __restrict__ D, uint32_t* dst_pos) {
-  const uint64_t ne = min(static_cast<uint64_t>(meta->n_edges), cap_edges);
-  const uint64_t nd = meta->n_dst;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < ne;
-       e += stride) {
-    uint2 x = edges[e];
-    x.x = bm_rank(bits, wprefix, x.x);
-    edges[e] = x;
-  }
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < nd;
-       i += stride)
-    dst_pos[i] = bm_rank(bits, wprefix, D[i]);
+__global__ void relabel_kernel(RelabelArgs r) {
+  relabel_range(r, blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
+                static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
 
 __global__ void rank_kernel(const uint32_t* __restrict__ bits,
@@ -499,8 +507,7 @@ __global__ void clear_kernel(uint32_t* bits, const uint32_t* __restrict__ list,
 }
 
 constexpr int kFrontierIPT = 4;
-constexpr int kLaborIPT = 4;
-constexpr int kNsIPT = 4;
+constexpr int kLaborIPT = kLaborTile / kNT;
 
 }  // namespace
 
@@ -510,78 +517,49 @@ int grid_for(uint64_t work_items, int per_block, int max_per_sm) {
   return static_cast<int>(std::max<uint64_t>(1, std::min(blocks, cap)));
 }
 
-void launch_batch_begin(const Sync& s, LayerMeta* meta, int num_layers, uint64_t n_seeds,
-                        cudaStream_t st) {
-  batch_begin_kernel<<<1, 256, 0, st>>>(s.epoch, s.tickets, Sync::kMaxTickets, meta,
-                                        num_layers, n_seeds, s.overflow);
+void launch_batch_begin(const Sync& s, uint32_t* clear_bits, const uint32_t* clear_list,
+                        const unsigned long long* clear_count, uint64_t clear_cap,
+                        uint64_t nwords, cudaStream_t st) {
+  const int grid = grid_for(clear_cap, 256, 4);
+  batch_begin_kernel<<<grid, 256, 0, st>>>(s.epoch, s.overflow, clear_bits, clear_list,
+                                           clear_count, clear_cap, nwords);
   CB_LAUNCH("batch_begin");
 }
 
-void launch_frontier(const DeviceGraph& g, const LayerBufs& b, LayerMeta* meta, int kind,
-                     uint32_t fanout, Bitmap& set_bm, const Bitmap* clear_bm,
-                     const Sync& s, int ticket, int epoch_slot, cudaStream_t st) {
-  const int grid = grid_for(b.cap_dst, kNT * kFrontierIPT, 8);
-  frontier_kernel<kFrontierIPT><<<grid, kNT, 0, st>>>(
-      b.dst, meta, g.indptr, kind, fanout, set_bm.bits, clear_bm ? clear_bm->bits : nullptr,
-      b.act_di, b.act_pre, b.out_prefix, b.slots, b.cap_edges, s.tickets + ticket,
-      s.status_a, s.status_b, s.status_c, s.epoch, epoch_slot, s.overflow);
+void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_dst,
+                     uint64_t relabel_work, cudaStream_t st) {
+  const int grid = std::max(grid_for(cap_dst, kNT * kFrontierIPT, 8),
+                            r.edges ? grid_for(relabel_work, kNT * 4, 8) : 1);
+  frontier_kernel<kFrontierIPT><<<grid, kNT, 0, st>>>(a, r);
   CB_LAUNCH("frontier");
 }
 
-void launch_labor(const DeviceGraph& g, const LayerBufs& b, LayerMeta* meta, int kind,
-                  uint32_t fanout, int layer, const cbdev::Variates* var, Bitmap& bm,
-                  const Sync& s, int ticket, int epoch_slot, cudaStream_t st) {
-  constexpr int TILE = kNT * kLaborIPT;
-  const size_t smem = (3 * TILE + 1) * sizeof(uint64_t) + TILE * sizeof(uint32_t);
-  static bool attr = false;
-  if (!attr) {
-    CB_CUDA(cudaFuncSetAttribute(labor_kernel<kLaborIPT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
-  const int grid = grid_for(s.max_tiles * TILE, TILE, 6);
-  labor_kernel<kLaborIPT><<<grid, kNT, smem, st>>>(
-      b.dst, meta, b.act_di, b.act_pre, g.indptr, g.indices, kind, fanout, layer, var,
-      bm.bits, b.edges, b.cap_edges, s.tickets + ticket, s.status_a, s.epoch, epoch_slot,
-      s.overflow);
+void launch_labor(const LaborArgs& a, uint64_t max_tiles, cudaStream_t st) {
+  const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, 8);
+  labor_kernel<kLaborIPT><<<grid, kNT, 0, st>>>(a);
   CB_LAUNCH("labor");
 }
 
-void launch_ns(const DeviceGraph& g, const LayerBufs& b, LayerMeta* meta, uint32_t fanout,
-               int layer, const cbdev::Variates* var, Bitmap& bm, cudaStream_t st) {
-  constexpr int TILE = kNT * kNsIPT;
-  const size_t smem_r = (4 * TILE + 1) * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
-    CB_CUDA(cudaFuncSetAttribute(ns_reservoir_kernel<kNsIPT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
-    attr = true;
-  }
-  ns_reservoir_kernel<kNsIPT><<<kNumSMs * 4, kNT, smem_r, st>>>(
-      b.dst, meta, b.act_di, b.act_pre, b.out_prefix, fanout, layer, var, b.slots,
-      b.cap_edges);
+void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix,
+               const uint64_t* indptr, const uint32_t* indices, uint64_t cap_dst,
+               cudaStream_t st) {
+  ns_reservoir_kernel<kLaborIPT><<<kNumSMs * 8, kNT, 0, st>>>(a);
   CB_LAUNCH("ns_reservoir");
-  const int grid = grid_for(b.cap_dst, kEmitDst, 8);
-  ns_emit_kernel<<<grid, kNT, 0, st>>>(b.dst, meta, b.out_prefix, g.indptr, g.indices,
-                                       fanout, b.slots, bm.bits, b.edges, b.cap_edges);
+  const int grid = grid_for(cap_dst, kEmitDst, 8);
+  ns_emit_kernel<<<grid, kNT, 0, st>>>(D, a.meta, out_prefix, indptr, indices, a.k, a.slots,
+                                       a.bits, a.edges, a.cap_edges);
   CB_LAUNCH("ns_emit");
 }
 
-void launch_extract(const Bitmap& bm, uint32_t* out, uint64_t cap_out,
-                    unsigned long long* count_out, unsigned long long* count_out2,
-                    const Sync& s, int ticket, int epoch_slot, cudaStream_t st) {
-  const int grid = grid_for(bm.words_padded, kNT * kWPT, 8);
-  extract_kernel<<<grid, kNT, 0, st>>>(bm.bits, bm.wprefix, bm.words_padded, out, cap_out,
-                                       count_out, count_out2, s.tickets + ticket, s.status_a,
-                                       s.epoch, epoch_slot, s.overflow);
+void launch_extract(const ExtractArgs& a, cudaStream_t st) {
+  const int grid = grid_for(a.words_padded, kNT * kWPT, 8);
+  extract_kernel<<<grid, kNT, 0, st>>>(a);
   CB_LAUNCH("extract");
 }
 
-void launch_relabel(const Bitmap& bm, const LayerBufs& b, const LayerMeta* meta,
-                    cudaStream_t st) {
-  const int grid = grid_for(std::max(b.cap_edges, b.cap_dst), 256, 8);
-  relabel_kernel<<<grid, 256, 0, st>>>(bm.bits, bm.wprefix, meta, b.edges, b.cap_edges, b.dst,
-                                       b.dst_pos);
+void launch_relabel(const RelabelArgs& r, uint64_t work, cudaStream_t st) {
+  const int grid = grid_for(work, 256 * 4, 8);
+  relabel_kernel<<<grid, 256, 0, st>>>(r);
   CB_LAUNCH("relabel");
 }
 
