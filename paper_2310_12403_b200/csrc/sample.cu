@@ -251,8 +251,13 @@ __global__ void __launch_bounds__(kNT) labor_kernel(LaborArgs a) {
   constexpr int TILE = kNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
   constexpr int NW = kNT / 32;
+  constexpr int kRecs = 512;  // records staged in smem (else global search)
+  __shared__ unsigned long long s_pre[kRecs + 1];
+  __shared__ unsigned long long s_base[kRecs];
+  __shared__ unsigned long long s_th[kRecs];
+  __shared__ uint32_t s_di[kRecs];
   __shared__ unsigned s_cnt[IPT * NW];
-  __shared__ unsigned s_base[IPT * NW];
+  __shared__ unsigned s_off[IPT * NW];
   __shared__ unsigned long long s_b;
   __shared__ unsigned s_tile;
   __shared__ unsigned s_total;
@@ -276,26 +281,58 @@ __global__ void __launch_bounds__(kNT) labor_kernel(LaborArgs a) {
     const uint64_t x1 = min(x0 + TILE, total);
     uint32_t a0, a1;
     tile_records(a.act, a.tile_first, n_act, tile, x1, a0, a1);
-
+    const uint32_t nd = a1 - a0 + 1;
+    const bool staged = nd <= kRecs;
+    if (staged) {
+      for (uint32_t i = threadIdx.x; i < nd; i += kNT) {
+        const ActRec rec = a.act[a0 + i];
+        s_pre[i] = rec.pre;
+        s_base[i] = rec.a;
+        s_th[i] = rec.b;
+        s_di[i] = rec.di;
+      }
+      if (threadIdx.x == 0) s_pre[nd] = ~0ULL;
+      __syncthreads();
+    }
+    // phase 1: locate every item's record and issue all index loads
     uint32_t tv[IPT];
     uint32_t dv[IPT];
+    uint64_t th[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const uint64_t x = x0 + static_cast<uint64_t>(j) * kNT + threadIdx.x;
+      uint64_t base;
+      if (staged) {
+        uint32_t lo = 0, hi = nd - 1;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi + 1) >> 1;
+          if (s_pre[mid] <= x) lo = mid;
+          else hi = mid - 1;
+        }
+        base = s_base[lo];
+        th[j] = s_th[lo];
+        dv[j] = s_di[lo];
+      } else {
+        const uint32_t li = rec_search(a.act, a0, a1, x);
+        const ActRec rec = a.act[li];
+        base = rec.a;
+        th[j] = rec.b;
+        dv[j] = rec.di;
+      }
+      tv[j] = (x < x1) ? __ldg(a.indices + base + x) : 0u;
+    }
+    // phase 2: keep rule
     unsigned keepmask = 0;
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const uint64_t x = x0 + static_cast<uint64_t>(j) * kNT + threadIdx.x;
-      tv[j] = 0;
-      dv[j] = 0xffffffffu;
       if (x < x1) {
-        const uint32_t li = rec_search(a.act, a0, a1, x);
-        const ActRec rec = a.act[li];
-        tv[j] = __ldg(a.indices + rec.a + x);
-        dv[j] = rec.di;
-        if (rec.b == ~0ULL) {
+        if (th[j] == ~0ULL) {
           keepmask |= 1u << j;
         } else if (!smooth) {
-          if ((hstep(p1, tv[j]) >> 11) <= rec.b) keepmask |= 1u << j;
+          if ((hstep(p1, tv[j]) >> 11) <= th[j]) keepmask |= 1u << j;
         } else {
-          const double thr = __longlong_as_double(static_cast<long long>(rec.b));
+          const double thr = __longlong_as_double(static_cast<long long>(th[j]));
           const double r = smooth_finish(v, hstep(p1, tv[j]), hstep(p2, tv[j]));
           if (r <= thr) keepmask |= 1u << j;
           if (fabs(r - thr) <= kGuard * thr) ++uncert;
@@ -315,8 +352,8 @@ __global__ void __launch_bounds__(kNT) labor_kernel(LaborArgs a) {
       const unsigned c1 = (2 * lane_id() + 1 < NC) ? s_cnt[2 * lane_id() + 1] : 0u;
       const unsigned inc = warp_inclusive_scan(c0 + c1);
       const unsigned ex = inc - c0 - c1;
-      if (2 * lane_id() < NC) s_base[2 * lane_id()] = ex;
-      if (2 * lane_id() + 1 < NC) s_base[2 * lane_id() + 1] = ex + c0;
+      if (2 * lane_id() < NC) s_off[2 * lane_id()] = ex;
+      if (2 * lane_id() + 1 < NC) s_off[2 * lane_id() + 1] = ex + c0;
       if (lane_id() == 31) s_total = inc;
     }
     __syncthreads();
@@ -327,7 +364,7 @@ __global__ void __launch_bounds__(kNT) labor_kernel(LaborArgs a) {
       const bool keep = (keepmask >> j) & 1u;
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (keep) {
-        const unsigned long long pos = gb + s_base[j * NW + w] + __popc(bal & lanemask_lt());
+        const unsigned long long pos = gb + s_off[j * NW + w] + __popc(bal & lanemask_lt());
         if (pos < a.cap_edges) a.edges[pos] = make_uint2(tv[j], dv[j]);
         set_bit(a.bits, tv[j]);
       }
