@@ -187,7 +187,10 @@ __device__ __forceinline__ unsigned long long mkstat(unsigned epoch, unsigned lo
 }
 
 // All threads of the block call this with the same `agg`; returns the
-// exclusive prefix of the tile in tile order. Uses warp 0 for look-back.
+// exclusive prefix of the tile in tile order. Warp 0 looks back over W*32
+// predecessors per step (lane l reads tiles base - l*W - j), so the
+// inclusive-prefix front advances W*32 tiles per L2 round trip.
+template <int W = 4>
 __device__ inline unsigned long long tile_prefix(unsigned long long* status, unsigned tile,
                                                  unsigned long long agg, unsigned epoch,
                                                  unsigned long long* s_bcast) {
@@ -203,29 +206,47 @@ __device__ inline unsigned long long tile_prefix(unsigned long long* status, uns
       unsigned long long excl = 0;
       long long base = static_cast<long long>(tile) - 1;
       while (true) {
-        const long long j = base - static_cast<long long>(lane_id());
-        unsigned long long s;
-        bool ready;
-        if (j < 0) {
-          s = mkstat(epoch, kFlagPre, 0);
-          ready = true;
-        } else {
-          s = ld_acquire(&status[j]);
-          ready = (s >> kEpochShift) == want && ((s >> kValBits) & 3u) != 0;
-        }
-        while (!__all_sync(0xffffffffu, ready)) {
-          if (!ready) {
-            s = ld_acquire(&status[j]);
-            ready = (s >> kEpochShift) == want && ((s >> kValBits) & 3u) != 0;
+        unsigned long long s[W];
+        bool ready[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const long long idx = base - static_cast<long long>(lane_id()) * W - j;
+          if (idx < 0) {
+            s[j] = mkstat(epoch, kFlagPre, 0);
+            ready[j] = true;
+          } else {
+            s[j] = ld_acquire(&status[idx]);
+            ready[j] = (s[j] >> kEpochShift) == want && ((s[j] >> kValBits) & 3u) != 0;
           }
         }
-        const unsigned pmask = __ballot_sync(0xffffffffu, ((s >> kValBits) & 3u) == 2u);
+        while (true) {
+          bool all = true;
+#pragma unroll
+          for (int j = 0; j < W; ++j) all = all && ready[j];
+          if (__all_sync(0xffffffffu, all)) break;
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            if (!ready[j]) {
+              const long long idx = base - static_cast<long long>(lane_id()) * W - j;
+              s[j] = ld_acquire(&status[idx]);
+              ready[j] = (s[j] >> kEpochShift) == want && ((s[j] >> kValBits) & 3u) != 0;
+            }
+          }
+        }
+        int fj = W;  // first (nearest) PREFIX inside this lane's group
+#pragma unroll
+        for (int j = W - 1; j >= 0; --j)
+          if (((s[j] >> kValBits) & 3u) == 2u) fj = j;
+        const unsigned pmask = __ballot_sync(0xffffffffu, fj < W);
         const int first = pmask ? (__ffs(pmask) - 1) : 32;
-        const unsigned long long c =
-            (static_cast<int>(lane_id()) <= first) ? (s & kValMask) : 0ULL;
+        unsigned long long c = 0;
+        const int me = static_cast<int>(lane_id());
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+          if (me < first || (me == first && j <= fj)) c += s[j] & kValMask;
         excl += warp_sum(c);
         if (pmask) break;
-        base -= 32;
+        base -= 32 * W;
       }
       if (lane_id() == 0) {
         st_release(&status[tile], mkstat(epoch, kFlagPre, excl + agg));

@@ -183,7 +183,7 @@ struct RelabelArgs {  // edges == nullptr disables
 };
 
 constexpr int kExtractTileWords = 512;
-constexpr int kLaborTile = 2048;
+constexpr int kLaborTile = 4096;
 constexpr int kFrontierTile = 1024;
 
 // ----------------------------------------------------- kernel launchers ----

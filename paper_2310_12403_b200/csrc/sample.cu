@@ -149,11 +149,11 @@ __global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelAr
     unsigned long long eo = 0;
     if (is_ns) eo = block_exclusive_scan<kNT>(os, s_scan[2], to);
     const unsigned long long bq =
-        tile_prefix(a.st_a, tile, tq, inv_epoch(a.epoch, a.slot), &s_bc[0]);
+        tile_prefix<4>(a.st_a, tile, tq, inv_epoch(a.epoch, a.slot), &s_bc[0]);
     const unsigned long long ba =
-        tile_prefix(a.st_b, tile, ta, inv_epoch(a.epoch, a.slot + 1), &s_bc[1]);
+        tile_prefix<4>(a.st_b, tile, ta, inv_epoch(a.epoch, a.slot + 1), &s_bc[1]);
     unsigned long long bo = 0;
-    if (is_ns) bo = tile_prefix(a.st_c, tile, to, inv_epoch(a.epoch, a.slot + 2), &s_bc[2]);
+    if (is_ns) bo = tile_prefix<4>(a.st_c, tile, to, inv_epoch(a.epoch, a.slot + 2), &s_bc[2]);
     eq += bq;
     ea += ba;
     eo += bo;
@@ -247,17 +247,19 @@ __device__ __forceinline__ void tile_records(const ActRec* act, const uint32_t* 
 // keep(t -> s) iff U(hash(z1,{2,layer,t})) <= k/d_s  (samplers.cpp:117-134);
 // plain stream compared in integers: (h>>11) <= floor((k/d)*2^53), exact.
 template <int IPT>
-__global__ void __launch_bounds__(kNT) labor_kernel(LaborArgs a) {
+__global__ void __launch_bounds__(kNT, 3) labor_kernel(LaborArgs a) {
   constexpr int TILE = kNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
   constexpr int NW = kNT / 32;
-  constexpr int kRecs = 512;  // records staged in smem (else global search)
+  constexpr int NC = IPT * NW;  // (item, warp) counters, item-major
+  static_assert(NC % 32 == 0 && NC <= 256, "counter scan layout");
+  constexpr int kRecs = 512;    // records staged in smem (else global path)
   __shared__ unsigned long long s_pre[kRecs + 1];
   __shared__ unsigned long long s_base[kRecs];
   __shared__ unsigned long long s_th[kRecs];
   __shared__ uint32_t s_di[kRecs];
-  __shared__ unsigned s_cnt[IPT * NW];
-  __shared__ unsigned s_off[IPT * NW];
+  __shared__ unsigned s_cnt[NC];
+  __shared__ unsigned s_off[NC];
   __shared__ unsigned long long s_b;
   __shared__ unsigned s_tile;
   __shared__ unsigned s_total;
@@ -291,13 +293,11 @@ __global__ void __launch_bounds__(kNT) labor_kernel(LaborArgs a) {
         s_th[i] = rec.b;
         s_di[i] = rec.di;
       }
-      if (threadIdx.x == 0) s_pre[nd] = ~0ULL;
       __syncthreads();
     }
     // phase 1: locate every item's record and issue all index loads
     uint32_t tv[IPT];
-    uint32_t dv[IPT];
-    uint64_t th[IPT];
+    uint32_t li[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const uint64_t x = x0 + static_cast<uint64_t>(j) * kNT + threadIdx.x;
@@ -309,15 +309,11 @@ __global__ void __launch_bounds__(kNT) labor_kernel(LaborArgs a) {
           if (s_pre[mid] <= x) lo = mid;
           else hi = mid - 1;
         }
+        li[j] = lo;
         base = s_base[lo];
-        th[j] = s_th[lo];
-        dv[j] = s_di[lo];
       } else {
-        const uint32_t li = rec_search(a.act, a0, a1, x);
-        const ActRec rec = a.act[li];
-        base = rec.a;
-        th[j] = rec.b;
-        dv[j] = rec.di;
+        li[j] = rec_search(a.act, a0, a1, x);
+        base = a.act[li[j]].a;
       }
       tv[j] = (x < x1) ? __ldg(a.indices + base + x) : 0u;
     }
@@ -327,45 +323,51 @@ __global__ void __launch_bounds__(kNT) labor_kernel(LaborArgs a) {
     for (int j = 0; j < IPT; ++j) {
       const uint64_t x = x0 + static_cast<uint64_t>(j) * kNT + threadIdx.x;
       if (x < x1) {
-        if (th[j] == ~0ULL) {
+        const uint64_t th = staged ? s_th[li[j]] : a.act[li[j]].b;
+        if (th == ~0ULL) {
           keepmask |= 1u << j;
         } else if (!smooth) {
-          if ((hstep(p1, tv[j]) >> 11) <= th[j]) keepmask |= 1u << j;
+          if ((hstep(p1, tv[j]) >> 11) <= th) keepmask |= 1u << j;
         } else {
-          const double thr = __longlong_as_double(static_cast<long long>(th[j]));
+          const double thr = __longlong_as_double(static_cast<long long>(th));
           const double r = smooth_finish(v, hstep(p1, tv[j]), hstep(p2, tv[j]));
           if (r <= thr) keepmask |= 1u << j;
           if (fabs(r - thr) <= kGuard * thr) ++uncert;
         }
       }
-    }
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
       const unsigned bal = __ballot_sync(0xffffffffu, (keepmask >> j) & 1u);
       if (lane_id() == 0) s_cnt[j * NW + w] = __popc(bal);
     }
     __syncthreads();
-    if (w == 0) {  // exclusive scan over IPT*NW (j-major) counters, 2 per lane
-      constexpr int NC = IPT * NW;
-      static_assert(NC <= 64, "scan width");
-      const unsigned c0 = (2 * lane_id() < NC) ? s_cnt[2 * lane_id()] : 0u;
-      const unsigned c1 = (2 * lane_id() + 1 < NC) ? s_cnt[2 * lane_id() + 1] : 0u;
-      const unsigned inc = warp_inclusive_scan(c0 + c1);
-      const unsigned ex = inc - c0 - c1;
-      if (2 * lane_id() < NC) s_off[2 * lane_id()] = ex;
-      if (2 * lane_id() + 1 < NC) s_off[2 * lane_id() + 1] = ex + c0;
+    if (w == 0) {  // exclusive scan over the NC (item-major) counters
+      constexpr int PER = NC / 32;
+      unsigned c[PER];
+      unsigned sum = 0;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        c[q] = s_cnt[lane_id() * PER + q];
+        sum += c[q];
+      }
+      const unsigned inc = warp_inclusive_scan(sum);
+      unsigned run = inc - sum;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        s_off[lane_id() * PER + q] = run;
+        run += c[q];
+      }
       if (lane_id() == 31) s_total = inc;
     }
     __syncthreads();
     const unsigned agg = s_total;
-    const unsigned long long gb = tile_prefix(a.status, tile, agg, ep, &s_b);
+    const unsigned long long gb = tile_prefix<4>(a.status, tile, agg, ep, &s_b);
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const bool keep = (keepmask >> j) & 1u;
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (keep) {
         const unsigned long long pos = gb + s_off[j * NW + w] + __popc(bal & lanemask_lt());
-        if (pos < a.cap_edges) a.edges[pos] = make_uint2(tv[j], dv[j]);
+        const uint32_t di = staged ? s_di[li[j]] : a.act[li[j]].di;
+        if (pos < a.cap_edges) a.edges[pos] = make_uint2(tv[j], di);
         set_bit(a.bits, tv[j]);
       }
     }
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__(kNT) extract_kernel(ExtractArgs a) {
     unsigned long long c = __popc(wv[0]) + __popc(wv[1]);
     unsigned long long tot;
     const unsigned long long ex = block_exclusive_scan<kNT>(c, s_scan, tot);
-    const unsigned long long gb = tile_prefix(a.status, tile, tot, ep, &s_b);
+    const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
     unsigned long long pos = gb + ex;
     uint32_t pw[kWPT];
 #pragma unroll
@@ -572,7 +574,7 @@ void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_d
 }
 
 void launch_labor(const LaborArgs& a, uint64_t max_tiles, cudaStream_t st) {
-  const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, 8);
+  const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, 3);
   labor_kernel<kLaborIPT><<<grid, kNT, 0, st>>>(a);
   CB_LAUNCH("labor");
 }
