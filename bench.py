@@ -234,7 +234,7 @@ def run_ours(args, cfg):
 
     # one eager batch with overflow-retry sizing, then capture as CUDA graphs
     plan.sample([seeds_host[0]], scheds[0], cb.MODE_INDEP, sync=True)
-    plan.capture(off, cb.MODE_INDEP, store)
+    plan.capture(off, scheds[0], cb.MODE_INDEP, store)
     stream = torch.cuda.ExternalStream(plan.stream, device=torch.device(f"cuda:{dev}"))
     d_seeds = torch.from_numpy(seeds_host.view(np.int32)).to(f"cuda:{dev}")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")

@@ -145,9 +145,11 @@ int cb_rows_device(cb_plan* plan, uint32_t part, void** ptr, uint64_t* rows);
 
 /* CUDA-graph form of one batch: capture the launch sequence for fixed
  * per-part seed counts (seeds_off) once, then replay per step with new seeds
- * (host or device pointer) and new variate keys. what: 1 = sample,
- * 2 = gather (needs f at capture), 3 = both. */
-int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb_features* f);
+ * (host or device pointer) and new variate keys. `sched` fixes whether the
+ * smoothed (2 <= kappa < inf) kernels are captured; replays must match.
+ * what: 1 = sample, 2 = gather (needs f at capture), 3 = both. */
+int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb_features* f,
+                    const cb_sched* sched);
 int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_device,
                    const cb_sched* sched, int what);
 

@@ -348,11 +348,13 @@ class Plan:
         _check(_lib.load().cb_sample_device(self._h, mode, C.c_void_p(d_seeds_ptr),
                                             _ptr(off), C.byref(s)))
 
-    def capture(self, offsets, mode: int = MODE_COOP, store: FeatureStore | None = None):
+    def capture(self, offsets, schedule: SeedSchedule, mode: int = MODE_COOP,
+                store: FeatureStore | None = None):
         """Capture one batch (and its gather) as CUDA graphs for replay."""
         off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        s = schedule._c()
         _check(_lib.load().cb_plan_capture(self._h, mode, _ptr(off),
-                                           store._h if store else None))
+                                           store._h if store else None, C.byref(s)))
 
     def replay(self, seeds_ptr: int | None, schedule: SeedSchedule | None,
                on_device: bool, what: int = 3):

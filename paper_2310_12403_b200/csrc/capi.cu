@@ -145,6 +145,8 @@ struct cb_plan {
   uint64_t seeds_cap = 0;
   int mode = -1;          // mode of the last batch
   int dirty_mode = -1;    // mode whose final bitmap still holds bits (-1: clean)
+  bool smooth = false;    // kernels of the last enqueue used smoothed variates
+  bool cap_smooth = false;
   bool have_batch = false;
   bool have_rows = false;
   uint64_t batches = 0;
@@ -390,7 +392,7 @@ RelabelArgs relabel_args(const Bitmap& bm, const LayerBufs& b, const uint32_t* D
 // Frontier + sampling of one layer of one part (sample.cu kernels).
 uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* D,
                        uint64_t cap_dst, uint64_t n_dst_param, Bitmap& set_bm,
-                       const RelabelArgs& fused, uint64_t fused_work) {
+                       const RelabelArgs& fused, uint64_t fused_work, bool smooth) {
   const DeviceGraph& g = pl->g->g;
   const LayerBufs& b = w.L[l];
   LayerMeta* me = pl->meta_at(p, l);
@@ -440,10 +442,10 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   la.slot = 8 * l + 3;
   la.overflow = w.sync.overflow;
   if (pl->kind == CB_NS) {
-    launch_ns(la, D, b.out_prefix, g.indptr, g.indices, cap_dst, st);
+    launch_ns(la, D, b.out_prefix, g.indptr, g.indices, cap_dst, smooth, st);
     return 3;
   }
-  launch_labor(la, w.sync.max_tiles, st);
+  launch_labor(la, w.sync.max_tiles, smooth, st);
   return 2;
 }
 
@@ -468,6 +470,8 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
     }
   }
   const bool coop = (mode == CB_MODE_COOP) && P > 1;
+  const bool smooth = sched->kappa != cbdev::kKappaInf && sched->kappa >= 2;
+  pl->smooth = smooth;
   // during capture the graph must clear what a batch of its own mode leaves
   const int dm = capturing ? mode : pl->dirty_mode;
   for (uint32_t p = 0; p < P; ++p) {
@@ -493,7 +497,7 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
         }
         launches += enqueue_layer(pl, w, p, l, D, cap_dst,
                                   l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[l & 1], fused,
-                                  fused_work);
+                                  fused_work, smooth);
         launch_extract(extract_args(w, w.bm[l & 1], w.bm[(l + 1) & 1].bits, w.L[l].src,
                                     w.L[l].cap_src, &pl->meta_at(p, l)->n_src,
                                     &pl->meta_at(p, l + 1)->n_dst, 3 * l + 2, 8 * l + 4),
@@ -513,7 +517,8 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
         PeWork& w = pl->pe[p];
         const uint32_t* D = (l == 0) ? d_seeds + off[p] : w.L[l].dst;
         launches += enqueue_layer(pl, w, p, l, D, w.L[l].cap_dst,
-                                  l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[0], none, 0);
+                                  l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[0], none, 0,
+                                  smooth);
         launch_extract(extract_args(w, w.bm[0], w.bm[1].bits, w.L[l].src, w.L[l].cap_src,
                                     &pl->meta_at(p, l)->n_src, nullptr, 3 * l + 2, 8 * l + 4),
                        st);
@@ -947,9 +952,11 @@ int cb_gather(cb_plan* plan, const cb_features* f) {
   });
 }
 
-int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb_features* f) {
+int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb_features* f,
+                    const cb_sched* sched) {
   return guard([&] {
-    require(plan != nullptr && seeds_off != nullptr, "null argument");
+    require(plan != nullptr && seeds_off != nullptr && sched != nullptr, "null argument");
+    require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
     require(mode == CB_MODE_COOP || mode == CB_MODE_INDEP, "unknown sampling mode");
     for (uint32_t p = 0; p < plan->P; ++p)
       require(seeds_off[p + 1] - seeds_off[p] <= plan->max_seeds,
@@ -957,7 +964,7 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
     DeviceGuard dg(plan->device);
     plan->drop_graphs();
     if (f) prepare_rows(plan, f);
-    cb_sched dummy{1, 0, 0, 0};
+    const cb_sched& dummy = *sched;
     // one eager batch first: sets kernel attributes outside capture
     enqueue_batch(plan, mode, plan->seeds, seeds_off, &dummy);
     if (f) enqueue_gather(plan, f);
@@ -979,6 +986,7 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
       plan->cap_launches_gather = plan->launches;
     }
     plan->cap_mode = mode;
+    plan->cap_smooth = plan->smooth;
     plan->cap_off.assign(seeds_off, seeds_off + plan->P + 1);
     plan->have_batch = false;
   });
@@ -994,6 +1002,9 @@ int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_devic
     if (what & 1) {
       require(sched != nullptr, "null schedule");
       require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
+      const bool sm = sched->kappa != cbdev::kKappaInf && sched->kappa >= 2;
+      require(sm == plan->cap_smooth,
+              "schedule smoothing differs from the captured batch (re-capture)");
       const uint64_t total = plan->cap_off[plan->P];
       if (seeds_flat && total)
         CB_CUDA(cudaMemcpyAsync(plan->seeds, seeds_flat, total * 4,

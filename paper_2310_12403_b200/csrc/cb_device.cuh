@@ -101,8 +101,9 @@ struct Variates {
   int pad;
 };
 
-// samplers.hpp:96-100 finish() for the smoothed stream.
-__device__ __forceinline__ double smooth_finish(const Variates& v, uint64_t b1, uint64_t b2) {
+// samplers.hpp:96-100 finish() for the smoothed stream. Out of line: it is
+// FP64-transcendental heavy and only runs for 2 <= kappa < inf.
+static __device__ __noinline__ double smooth_finish(const Variates& v, uint64_t b1, uint64_t b2) {
   const double n = __dadd_rn(__dmul_rn(v.cos_c, dnormal_from_bits(b1)),
                              __dmul_rn(v.sin_c, dnormal_from_bits(b2)));
   return dphi(n);

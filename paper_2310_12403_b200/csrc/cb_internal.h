@@ -193,9 +193,9 @@ void launch_batch_begin(const Sync& s, uint32_t* clear_bits, const uint32_t* cle
                         uint64_t nwords, cudaStream_t st);
 void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_dst,
                      uint64_t relabel_work, cudaStream_t st);
-void launch_labor(const LaborArgs& a, uint64_t max_tiles, cudaStream_t st);
+void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStream_t st);
 void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix,
-               const uint64_t* indptr, const uint32_t* indices, uint64_t cap_dst,
+               const uint64_t* indptr, const uint32_t* indices, uint64_t cap_dst, bool smooth,
                cudaStream_t st);
 void launch_extract(const ExtractArgs& a, cudaStream_t st);
 void launch_relabel(const RelabelArgs& r, uint64_t work, cudaStream_t st);

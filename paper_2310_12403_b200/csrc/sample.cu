@@ -246,7 +246,7 @@ __device__ __forceinline__ void tile_records(const ActRec* act, const uint32_t* 
 // ------------------------------------------------------------- LABOR/FULL --
 // keep(t -> s) iff U(hash(z1,{2,layer,t})) <= k/d_s  (samplers.cpp:117-134);
 // plain stream compared in integers: (h>>11) <= floor((k/d)*2^53), exact.
-template <int IPT>
+template <int IPT, bool SMOOTH>
 __global__ void __launch_bounds__(kNT, 3) labor_kernel(LaborArgs a) {
   constexpr int TILE = kNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
@@ -270,10 +270,10 @@ __global__ void __launch_bounds__(kNT, 3) labor_kernel(LaborArgs a) {
   const uint64_t ntiles = (total + TILE - 1) / TILE;
   const unsigned ep = inv_epoch(a.epoch, a.slot);
   const Variates v = *a.var;
-  const bool smooth = v.smoothed != 0 && a.kind != 0;
+  constexpr bool smooth = SMOOTH;
   // prefix({kStreamLabor, layer}) under z1 (and z2 when smoothed)
   const uint64_t p1 = hstep(hstep(hinit(v.z1), 2ULL), static_cast<uint64_t>(a.layer));
-  const uint64_t p2 = hstep(hstep(hinit(v.z2), 2ULL), static_cast<uint64_t>(a.layer));
+  const uint64_t p2 = SMOOTH ? hstep(hstep(hinit(v.z2), 2ULL), static_cast<uint64_t>(a.layer)) : 0;
   const unsigned w = threadIdx.x >> 5;
   unsigned long long uncert = 0;
 
@@ -303,11 +303,26 @@ __global__ void __launch_bounds__(kNT, 3) labor_kernel(LaborArgs a) {
       const uint64_t x = x0 + static_cast<uint64_t>(j) * kNT + threadIdx.x;
       uint64_t base;
       if (staged) {
+        // the warp's 32 consecutive positions usually share one record:
+        // lane 0 finds the record of the warp's first position, the others
+        // only search forward from there when they cross a record boundary
+        const uint64_t xw = x0 + static_cast<uint64_t>(j) * kNT + (threadIdx.x & ~31u);
         uint32_t lo = 0, hi = nd - 1;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi + 1) >> 1;
-          if (s_pre[mid] <= x) lo = mid;
-          else hi = mid - 1;
+        if (lane_id() == 0) {
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (s_pre[mid] <= xw) lo = mid;
+            else hi = mid - 1;
+          }
+        }
+        lo = __shfl_sync(0xffffffffu, lo, 0);
+        if (lo + 1 < nd && s_pre[lo + 1] <= x) {
+          hi = nd - 1;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (s_pre[mid] <= x) lo = mid;
+            else hi = mid - 1;
+          }
         }
         li[j] = lo;
         base = s_base[lo];
@@ -387,7 +402,7 @@ __global__ void __launch_bounds__(kNT, 3) labor_kernel(LaborArgs a) {
 // Reservoir (samplers.cpp:75-84) restated per slot: the final content of slot
 // j is the largest i in [k, d) with floor(U_i*(i+1)) == j, else j. Every
 // position is an independent atomicMax, so hub rows split across CTAs.
-template <int IPT>
+template <int IPT, bool SMOOTH>
 __global__ void __launch_bounds__(kNT) ns_reservoir_kernel(LaborArgs a) {
   constexpr int TILE = kNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
@@ -396,7 +411,7 @@ __global__ void __launch_bounds__(kNT) ns_reservoir_kernel(LaborArgs a) {
   const uint64_t n_act = meta->n_active;
   const uint64_t ntiles = (total + TILE - 1) / TILE;
   const Variates v = *a.var;
-  const bool smooth = v.smoothed != 0;
+  constexpr bool smooth = SMOOTH;
   const uint64_t z2p = hstep(hstep(hinit(v.z2), 1ULL), static_cast<uint64_t>(a.layer));
   const uint32_t k = a.k;
   unsigned long long uncert = 0;
@@ -573,16 +588,18 @@ void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_d
   CB_LAUNCH("frontier");
 }
 
-void launch_labor(const LaborArgs& a, uint64_t max_tiles, cudaStream_t st) {
+void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStream_t st) {
   const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, 3);
-  labor_kernel<kLaborIPT><<<grid, kNT, 0, st>>>(a);
+  if (smooth && a.kind != 0) labor_kernel<kLaborIPT, true><<<grid, kNT, 0, st>>>(a);
+  else labor_kernel<kLaborIPT, false><<<grid, kNT, 0, st>>>(a);
   CB_LAUNCH("labor");
 }
 
 void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix,
-               const uint64_t* indptr, const uint32_t* indices, uint64_t cap_dst,
+               const uint64_t* indptr, const uint32_t* indices, uint64_t cap_dst, bool smooth,
                cudaStream_t st) {
-  ns_reservoir_kernel<kLaborIPT><<<kNumSMs * 8, kNT, 0, st>>>(a);
+  if (smooth) ns_reservoir_kernel<kLaborIPT, true><<<kNumSMs * 8, kNT, 0, st>>>(a);
+  else ns_reservoir_kernel<kLaborIPT, false><<<kNumSMs * 8, kNT, 0, st>>>(a);
   CB_LAUNCH("ns_reservoir");
   const int grid = grid_for(cap_dst, kEmitDst, 8);
   ns_emit_kernel<<<grid, kNT, 0, st>>>(D, a.meta, out_prefix, indptr, indices, a.k, a.slots,
