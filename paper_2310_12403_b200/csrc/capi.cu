@@ -243,6 +243,7 @@ void plan_alloc(cb_plan* pl) {
     w.sync.tickets = pl->mem.alloc<unsigned>(2 * Sync::kMaxTickets);
     CB_CUDA(cudaMemset(w.sync.tickets, 0, 2 * Sync::kMaxTickets * sizeof(unsigned)));
     w.sync.overflow = pl->mem.alloc<unsigned>(1);
+    w.sync.keep_words = pl->mem.alloc<uint32_t>(max_tiles * kLaborTile / 32 + 1);
     w.sync.status_a = pl->mem.alloc<unsigned long long>(max_tiles);
     w.sync.status_b = pl->mem.alloc<unsigned long long>(max_tiles);
     w.sync.status_c = pl->mem.alloc<unsigned long long>(max_tiles);
@@ -434,6 +435,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   la.bits = set_bm.bits;
   la.edges = b.edges;
   la.slots = b.slots;
+  la.keep_words = w.sync.keep_words;
   la.cap_edges = b.cap_edges;
   la.ticket = w.sync.tickets + 3 * l + 1;
   la.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l + 1;
@@ -446,7 +448,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
     return 3;
   }
   launch_labor(la, w.sync.max_tiles, smooth, st);
-  return 2;
+  return 3;
 }
 
 // The per-batch launch sequence. d_seeds: P seed lists back to back (device).
@@ -1191,7 +1193,7 @@ int cb_rows_device(cb_plan* plan, uint32_t part, void** ptr, uint64_t* rows) {
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n) {
   return guard([&] {
     require(plan != nullptr && n != nullptr, "null argument");
-    const uint64_t samp = (plan->kind == CB_NS) ? 3 : 2;  // frontier + labor | ns x2
+    const uint64_t samp = 3;  // frontier + labor mark/emit | ns reservoir/emit
     const uint64_t P = plan->P;
     const uint64_t L = plan->L;
     uint64_t k;

@@ -206,47 +206,46 @@ __device__ inline unsigned long long tile_prefix(unsigned long long* status, uns
       if (lane_id() == 0) st_release(&status[tile], mkstat(epoch, kFlagAgg, agg));
       unsigned long long excl = 0;
       long long base = static_cast<long long>(tile) - 1;
+      const int me = static_cast<int>(lane_id());
       while (true) {
         unsigned long long s[W];
-        bool ready[W];
 #pragma unroll
         for (int j = 0; j < W; ++j) {
-          const long long idx = base - static_cast<long long>(lane_id()) * W - j;
-          if (idx < 0) {
-            s[j] = mkstat(epoch, kFlagPre, 0);
-            ready[j] = true;
-          } else {
-            s[j] = ld_acquire(&status[idx]);
-            ready[j] = (s[j] >> kEpochShift) == want && ((s[j] >> kValBits) & 3u) != 0;
-          }
+          const long long idx = base - static_cast<long long>(me) * W - j;
+          s[j] = (idx < 0) ? mkstat(epoch, kFlagPre, 0) : ld_acquire(&status[idx]);
         }
+        int first;      // lane holding the nearest inclusive prefix (32 = none)
+        int fj = W;     // its entry
         while (true) {
-          bool all = true;
+          unsigned inval = 0;
+          fj = W;
 #pragma unroll
-          for (int j = 0; j < W; ++j) all = all && ready[j];
-          if (__all_sync(0xffffffffu, all)) break;
-#pragma unroll
-          for (int j = 0; j < W; ++j) {
-            if (!ready[j]) {
-              const long long idx = base - static_cast<long long>(lane_id()) * W - j;
-              s[j] = ld_acquire(&status[idx]);
-              ready[j] = (s[j] >> kEpochShift) == want && ((s[j] >> kValBits) & 3u) != 0;
-            }
+          for (int j = W - 1; j >= 0; --j) {
+            const bool ok = (s[j] >> kEpochShift) == want && ((s[j] >> kValBits) & 3u) != 0;
+            if (!ok) inval |= 1u << j;
+            else if (((s[j] >> kValBits) & 3u) == 2u) fj = j;
           }
-        }
-        int fj = W;  // first (nearest) PREFIX inside this lane's group
+          // an entry only matters if it is nearer than the nearest prefix
+          const unsigned pmask = __ballot_sync(0xffffffffu, fj < W);
+          first = pmask ? (__ffs(pmask) - 1) : 32;
+          unsigned need = 0;
+          if (me < first) need = inval;
+          else if (me == first) need = inval & ((1u << fj) - 1u);
+          if (!__any_sync(0xffffffffu, need != 0)) break;
+          __nanosleep(64);
 #pragma unroll
-        for (int j = W - 1; j >= 0; --j)
-          if (((s[j] >> kValBits) & 3u) == 2u) fj = j;
-        const unsigned pmask = __ballot_sync(0xffffffffu, fj < W);
-        const int first = pmask ? (__ffs(pmask) - 1) : 32;
+          for (int j = 0; j < W; ++j)
+            if ((need >> j) & 1u) {
+              const long long idx = base - static_cast<long long>(me) * W - j;
+              s[j] = ld_acquire(&status[idx]);
+            }
+        }
         unsigned long long c = 0;
-        const int me = static_cast<int>(lane_id());
 #pragma unroll
         for (int j = 0; j < W; ++j)
           if (me < first || (me == first && j <= fj)) c += s[j] & kValMask;
         excl += warp_sum(c);
-        if (pmask) break;
+        if (first < 32) break;
         base -= 32 * W;
       }
       if (lane_id() == 0) {

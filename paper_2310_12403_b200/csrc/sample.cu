@@ -246,67 +246,58 @@ __device__ __forceinline__ void tile_records(const ActRec* act, const uint32_t* 
 // ------------------------------------------------------------- LABOR/FULL --
 // keep(t -> s) iff U(hash(z1,{2,layer,t})) <= k/d_s  (samplers.cpp:117-134);
 // plain stream compared in integers: (h>>11) <= floor((k/d)*2^53), exact.
+//
+// Two phases so the hashing never waits on an ordered scan:
+//   labor_mark : every scan position independently (grid-stride tiles); lane
+//                l of a warp owns position xw+l, so the warp ballot IS the
+//                keep word of 32 consecutive positions; kept ids are OR-ed
+//                into the layer bitmap (order-free)
+//   labor_emit : ordered popcount compaction of the keep words (decoupled
+//                look-back over 64K-position tiles) -> edges in scan order =
+//                grouped by dst, CSR order inside a dst (the reference order)
 template <int IPT, bool SMOOTH>
-__global__ void __launch_bounds__(kNT, 3) labor_kernel(LaborArgs a) {
+__global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
   constexpr int TILE = kNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
-  constexpr int NW = kNT / 32;
-  constexpr int NC = IPT * NW;  // (item, warp) counters, item-major
-  static_assert(NC % 32 == 0 && NC <= 256, "counter scan layout");
-  constexpr int kRecs = 512;    // records staged in smem (else global path)
-  __shared__ unsigned long long s_pre[kRecs + 1];
+  constexpr int kRecs = 512;  // records staged in smem (else global path)
+  __shared__ unsigned long long s_pre[kRecs];
   __shared__ unsigned long long s_base[kRecs];
   __shared__ unsigned long long s_th[kRecs];
-  __shared__ uint32_t s_di[kRecs];
-  __shared__ unsigned s_cnt[NC];
-  __shared__ unsigned s_off[NC];
-  __shared__ unsigned long long s_b;
-  __shared__ unsigned s_tile;
-  __shared__ unsigned s_total;
-
   LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
   const uint64_t n_act = meta->n_active;
   const uint64_t ntiles = (total + TILE - 1) / TILE;
-  const unsigned ep = inv_epoch(a.epoch, a.slot);
   const Variates v = *a.var;
-  constexpr bool smooth = SMOOTH;
   // prefix({kStreamLabor, layer}) under z1 (and z2 when smoothed)
   const uint64_t p1 = hstep(hstep(hinit(v.z1), 2ULL), static_cast<uint64_t>(a.layer));
   const uint64_t p2 = SMOOTH ? hstep(hstep(hinit(v.z2), 2ULL), static_cast<uint64_t>(a.layer)) : 0;
-  const unsigned w = threadIdx.x >> 5;
   unsigned long long uncert = 0;
-
-  for (unsigned tile = next_tile(a.ticket, &s_tile); tile < ntiles;
-       tile = next_tile(a.ticket, &s_tile)) {
-    const uint64_t x0 = static_cast<uint64_t>(tile) * TILE;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t x0 = tile * TILE;
     const uint64_t x1 = min(x0 + TILE, total);
     uint32_t a0, a1;
     tile_records(a.act, a.tile_first, n_act, tile, x1, a0, a1);
     const uint32_t nd = a1 - a0 + 1;
     const bool staged = nd <= kRecs;
+    __syncthreads();  // previous tile done with the staging buffers
     if (staged) {
       for (uint32_t i = threadIdx.x; i < nd; i += kNT) {
         const ActRec rec = a.act[a0 + i];
         s_pre[i] = rec.pre;
         s_base[i] = rec.a;
         s_th[i] = rec.b;
-        s_di[i] = rec.di;
       }
       __syncthreads();
     }
-    // phase 1: locate every item's record and issue all index loads
     uint32_t tv[IPT];
     uint32_t li[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
-      const uint64_t x = x0 + static_cast<uint64_t>(j) * kNT + threadIdx.x;
+      const uint64_t xw = x0 + static_cast<uint64_t>(j) * kNT + (threadIdx.x & ~31u);
+      const uint64_t x = xw + lane_id();
       uint64_t base;
       if (staged) {
-        // the warp's 32 consecutive positions usually share one record:
-        // lane 0 finds the record of the warp's first position, the others
-        // only search forward from there when they cross a record boundary
-        const uint64_t xw = x0 + static_cast<uint64_t>(j) * kNT + (threadIdx.x & ~31u);
+        // the warp's 32 consecutive positions usually share one record
         uint32_t lo = 0, hi = nd - 1;
         if (lane_id() == 0) {
           while (lo < hi) {
@@ -327,73 +318,92 @@ __global__ void __launch_bounds__(kNT, 3) labor_kernel(LaborArgs a) {
         li[j] = lo;
         base = s_base[lo];
       } else {
-        li[j] = rec_search(a.act, a0, a1, x);
+        li[j] = rec_search(a.act, a0, a1, x < x1 ? x : x1 - 1);
         base = a.act[li[j]].a;
       }
       tv[j] = (x < x1) ? __ldg(a.indices + base + x) : 0u;
     }
-    // phase 2: keep rule
-    unsigned keepmask = 0;
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
-      const uint64_t x = x0 + static_cast<uint64_t>(j) * kNT + threadIdx.x;
+      const uint64_t xw = x0 + static_cast<uint64_t>(j) * kNT + (threadIdx.x & ~31u);
+      const uint64_t x = xw + lane_id();
+      bool keep = false;
       if (x < x1) {
         const uint64_t th = staged ? s_th[li[j]] : a.act[li[j]].b;
         if (th == ~0ULL) {
-          keepmask |= 1u << j;
-        } else if (!smooth) {
-          if ((hstep(p1, tv[j]) >> 11) <= th) keepmask |= 1u << j;
+          keep = true;
+        } else if (!SMOOTH) {
+          keep = (hstep(p1, tv[j]) >> 11) <= th;
         } else {
           const double thr = __longlong_as_double(static_cast<long long>(th));
           const double r = smooth_finish(v, hstep(p1, tv[j]), hstep(p2, tv[j]));
-          if (r <= thr) keepmask |= 1u << j;
+          keep = r <= thr;
           if (fabs(r - thr) <= kGuard * thr) ++uncert;
         }
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, (keepmask >> j) & 1u);
-      if (lane_id() == 0) s_cnt[j * NW + w] = __popc(bal);
-    }
-    __syncthreads();
-    if (w == 0) {  // exclusive scan over the NC (item-major) counters
-      constexpr int PER = NC / 32;
-      unsigned c[PER];
-      unsigned sum = 0;
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        c[q] = s_cnt[lane_id() * PER + q];
-        sum += c[q];
-      }
-      const unsigned inc = warp_inclusive_scan(sum);
-      unsigned run = inc - sum;
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        s_off[lane_id() * PER + q] = run;
-        run += c[q];
-      }
-      if (lane_id() == 31) s_total = inc;
-    }
-    __syncthreads();
-    const unsigned agg = s_total;
-    const unsigned long long gb = tile_prefix<4>(a.status, tile, agg, ep, &s_b);
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-      const bool keep = (keepmask >> j) & 1u;
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        const unsigned long long pos = gb + s_off[j * NW + w] + __popc(bal & lanemask_lt());
-        const uint32_t di = staged ? s_di[li[j]] : a.act[li[j]].di;
-        if (pos < a.cap_edges) a.edges[pos] = make_uint2(tv[j], di);
-        set_bit(a.bits, tv[j]);
+      if (lane_id() == 0 && xw < x1) a.keep_words[xw >> 5] = bal;
+      if (keep) set_bit(a.bits, tv[j]);
+    }
+  }
+  if (SMOOTH) {
+    uncert = warp_sum(uncert);
+    if (lane_id() == 0 && uncert) atomicAdd(&meta->uncertified, uncert);
+  }
+}
+
+constexpr int kEmitWPT = 8;                    // keep words per thread
+constexpr int kEmitTileWords = kNT * kEmitWPT;  // 2048 words = 65536 positions
+
+__global__ void __launch_bounds__(kNT) labor_emit_kernel(LaborArgs a) {
+  __shared__ unsigned long long s_scan[kNT / 32 + 1];
+  __shared__ unsigned long long s_b;
+  __shared__ unsigned s_tile;
+  LayerMeta* meta = a.meta;
+  const uint64_t total = meta->scan_total;
+  const uint64_t n_act = meta->n_active;
+  const uint64_t nwords = (total + 31) / 32;
+  const uint64_t ntiles = (nwords + kEmitTileWords - 1) / kEmitTileWords;
+  const unsigned ep = inv_epoch(a.epoch, a.slot);
+  for (unsigned tile = next_tile(a.ticket, &s_tile); tile < ntiles;
+       tile = next_tile(a.ticket, &s_tile)) {
+    const uint64_t w0 = static_cast<uint64_t>(tile) * kEmitTileWords + threadIdx.x * kEmitWPT;
+    uint32_t wv[kEmitWPT];
+    unsigned long long c = 0;
+#pragma unroll
+    for (int j = 0; j < kEmitWPT; ++j) {
+      wv[j] = (w0 + j < nwords) ? a.keep_words[w0 + j] : 0u;
+      c += __popc(wv[j]);
+    }
+    unsigned long long tot;
+    const unsigned long long ex = block_exclusive_scan<kNT>(c, s_scan, tot);
+    const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
+    unsigned long long pos = gb + ex;
+    uint32_t rec_i = 0xffffffffu;
+    ActRec rec{};
+#pragma unroll 1
+    for (int j = 0; j < kEmitWPT; ++j) {
+      uint32_t m = wv[j];
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        const uint64_t x = (w0 + j) * 32 + bit;
+        if (rec_i == 0xffffffffu || x >= a.act[rec_i + 1].pre) {
+          const uint64_t tt = x / kLaborTile;
+          uint32_t r0 = __ldg(&a.tile_first[tt]);
+          uint32_t r1 = __ldg(&a.tile_first[tt + 1]);
+          if (r1 >= n_act) r1 = static_cast<uint32_t>(n_act) - 1;
+          rec_i = rec_search(a.act, r0, r1, x);
+          rec = a.act[rec_i];
+        }
+        if (pos < a.cap_edges) a.edges[pos] = make_uint2(__ldg(a.indices + rec.a + x), rec.di);
+        ++pos;
       }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
-      meta->n_edges = gb + agg;
-      if (gb + agg > a.cap_edges) atomicExch(a.overflow, 1u);
+      meta->n_edges = gb + tot;
+      if (gb + tot > a.cap_edges) atomicExch(a.overflow, 1u);
     }
-  }
-  if (smooth) {
-    uncert = warp_sum(uncert);
-    if (lane_id() == 0 && uncert) atomicAdd(&meta->uncertified, uncert);
   }
   retire_ticket(a.ticket, a.exit_ctr);
 }
@@ -590,9 +600,13 @@ void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_d
 
 void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStream_t st) {
   const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, 3);
-  if (smooth && a.kind != 0) labor_kernel<kLaborIPT, true><<<grid, kNT, 0, st>>>(a);
-  else labor_kernel<kLaborIPT, false><<<grid, kNT, 0, st>>>(a);
-  CB_LAUNCH("labor");
+  if (smooth && a.kind != 0) labor_mark_kernel<kLaborIPT, true><<<grid, kNT, 0, st>>>(a);
+  else labor_mark_kernel<kLaborIPT, false><<<grid, kNT, 0, st>>>(a);
+  CB_LAUNCH("labor_mark");
+  const uint64_t words = (max_tiles * kLaborTile + 31) / 32;
+  const int g2 = grid_for(words, kEmitTileWords, 4);
+  labor_emit_kernel<<<g2, kNT, 0, st>>>(a);
+  CB_LAUNCH("labor_emit");
 }
 
 void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix,

@@ -278,3 +278,27 @@ def test_gather_matches_reference_forward(powerlaw):
     O.coop_free_reference(handle)
     got = np.concatenate(rows)
     assert np.array_equal(got, out)
+
+
+@pytest.mark.parametrize("kappa", [1, 4])
+def test_graph_replay_matches_eager(c1, kappa):
+    """cb_plan_capture/cb_plan_replay (the bench path) == eager batches."""
+    g, ref = c1
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, 10)
+    store = cb.FeatureStore.synth(g, 32, 3, "f32")
+    plan = cb.Plan(g, None, 3, cfg, 512)
+    pool = np.arange(ref.n, dtype=np.uint32)
+    sched = cb.SeedSchedule.make(kappa, 5)
+    seeds0 = O.draw_from_pool(pool, 512, 5, 0)
+    plan.sample([seeds0], sched, cb.MODE_INDEP)
+    plan.capture(np.array([0, 512], np.uint64), sched, cb.MODE_INDEP, store)
+    for step in range(1, 4):
+        sched = cb.schedule_advance(sched)
+        seeds = O.draw_from_pool(pool, 512, 5, step)
+        plan.replay(seeds.ctypes.data, sched, False, 3)
+        plan.synchronize()
+        got = plan.stack(0)
+        want = O.expand(ref, seeds, 3, O.LABOR0, 10, osched(sched))
+        assert_stack_eq(got, want, f"replay step {step}")
+        rows = plan.rows(0, store)
+        assert np.array_equal(rows, O.feature_rows(3, 32, "f32", want[-1]["src"]))
