@@ -244,6 +244,7 @@ void plan_alloc(cb_plan* pl) {
     CB_CUDA(cudaMemset(w.sync.tickets, 0, 2 * Sync::kMaxTickets * sizeof(unsigned)));
     w.sync.overflow = pl->mem.alloc<unsigned>(1);
     w.sync.keep_words = pl->mem.alloc<uint32_t>(max_tiles * kLaborTile / 32 + 1);
+    w.sync.word_rec = pl->mem.alloc<uint32_t>(max_tiles * kLaborTile / 32 + 1);
     w.sync.status_a = pl->mem.alloc<unsigned long long>(max_tiles);
     w.sync.status_b = pl->mem.alloc<unsigned long long>(max_tiles);
     w.sync.status_c = pl->mem.alloc<unsigned long long>(max_tiles);
@@ -436,6 +437,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   la.edges = b.edges;
   la.slots = b.slots;
   la.keep_words = w.sync.keep_words;
+  la.word_rec = w.sync.word_rec;
   la.cap_edges = b.cap_edges;
   la.ticket = w.sync.tickets + 3 * l + 1;
   la.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l + 1;

@@ -85,6 +85,7 @@ struct Sync {
   unsigned long long* status_c = nullptr;     // [max_tiles]
   unsigned* overflow = nullptr;               // [1]
   uint32_t* keep_words = nullptr;             // [max_tiles*kLaborTile/32]
+  uint32_t* word_rec = nullptr;               // [max_tiles*kLaborTile/32]
   uint64_t max_tiles = 0;
   static constexpr int kMaxTickets = 256;
 };
@@ -148,6 +149,7 @@ struct LaborArgs {
   uint2* edges;
   uint32_t* slots;
   uint32_t* keep_words;  // 1 bit per scan position (labor_mark -> labor_emit)
+  uint32_t* word_rec;    // record holding the first position of each keep word
   uint64_t cap_edges;
   unsigned* ticket;
   unsigned* exit_ctr;

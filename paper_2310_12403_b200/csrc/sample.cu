@@ -342,7 +342,10 @@ __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
         }
       }
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (lane_id() == 0 && xw < x1) a.keep_words[xw >> 5] = bal;
+      if (lane_id() == 0 && xw < x1) {
+        a.keep_words[xw >> 5] = bal;
+        a.word_rec[xw >> 5] = staged ? a0 + li[j] : li[j];  // record of position xw
+      }
       if (keep) set_bit(a.bits, tv[j]);
     }
   }
@@ -355,50 +358,58 @@ __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
 constexpr int kEmitWPT = 8;                    // keep words per thread
 constexpr int kEmitTileWords = kNT * kEmitWPT;  // 2048 words = 65536 positions
 
+// Ordered compaction of the keep words. The tile's kept items are spread
+// over all threads (item q -> its word by binary search over the per-word
+// output bases in smem), so every kept edge is an independent chain:
+// word_rec -> record -> neighbour id -> store.
 __global__ void __launch_bounds__(kNT) labor_emit_kernel(LaborArgs a) {
   __shared__ unsigned long long s_scan[kNT / 32 + 1];
+  __shared__ uint32_t s_wbase[kEmitTileWords + 1];
+  __shared__ uint32_t s_word[kEmitTileWords];
   __shared__ unsigned long long s_b;
   __shared__ unsigned s_tile;
   LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
-  const uint64_t n_act = meta->n_active;
   const uint64_t nwords = (total + 31) / 32;
   const uint64_t ntiles = (nwords + kEmitTileWords - 1) / kEmitTileWords;
   const unsigned ep = inv_epoch(a.epoch, a.slot);
   for (unsigned tile = next_tile(a.ticket, &s_tile); tile < ntiles;
        tile = next_tile(a.ticket, &s_tile)) {
-    const uint64_t w0 = static_cast<uint64_t>(tile) * kEmitTileWords + threadIdx.x * kEmitWPT;
+    const uint64_t wt = static_cast<uint64_t>(tile) * kEmitTileWords;
+    const uint32_t l0 = threadIdx.x * kEmitWPT;
     uint32_t wv[kEmitWPT];
     unsigned long long c = 0;
 #pragma unroll
     for (int j = 0; j < kEmitWPT; ++j) {
-      wv[j] = (w0 + j < nwords) ? a.keep_words[w0 + j] : 0u;
+      wv[j] = (wt + l0 + j < nwords) ? a.keep_words[wt + l0 + j] : 0u;
       c += __popc(wv[j]);
     }
     unsigned long long tot;
     const unsigned long long ex = block_exclusive_scan<kNT>(c, s_scan, tot);
-    const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
-    unsigned long long pos = gb + ex;
-    uint32_t rec_i = 0xffffffffu;
-    ActRec rec{};
-#pragma unroll 1
+    uint32_t run = static_cast<uint32_t>(ex);
+#pragma unroll
     for (int j = 0; j < kEmitWPT; ++j) {
-      uint32_t m = wv[j];
-      while (m) {
-        const int bit = __ffs(m) - 1;
-        m &= m - 1;
-        const uint64_t x = (w0 + j) * 32 + bit;
-        if (rec_i == 0xffffffffu || x >= a.act[rec_i + 1].pre) {
-          const uint64_t tt = x / kLaborTile;
-          uint32_t r0 = __ldg(&a.tile_first[tt]);
-          uint32_t r1 = __ldg(&a.tile_first[tt + 1]);
-          if (r1 >= n_act) r1 = static_cast<uint32_t>(n_act) - 1;
-          rec_i = rec_search(a.act, r0, r1, x);
-          rec = a.act[rec_i];
-        }
-        if (pos < a.cap_edges) a.edges[pos] = make_uint2(__ldg(a.indices + rec.a + x), rec.di);
-        ++pos;
+      s_word[l0 + j] = wv[j];
+      s_wbase[l0 + j] = run;
+      run += __popc(wv[j]);
+    }
+    const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
+    // (tile_prefix ends with __syncthreads: s_word / s_wbase are visible)
+    for (uint32_t q = threadIdx.x; q < tot; q += kNT) {
+      uint32_t lo = 0, hi = kEmitTileWords - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (s_wbase[mid] <= q) lo = mid;
+        else hi = mid - 1;
       }
+      uint32_t word = s_word[lo];
+      for (uint32_t r = q - s_wbase[lo]; r > 0; --r) word &= word - 1;
+      const uint64_t x = (wt + lo) * 32 + (__ffs(word) - 1);
+      uint32_t ri = __ldg(&a.word_rec[wt + lo]);
+      while (__ldg(&a.act[ri + 1].pre) <= x) ++ri;
+      const ActRec rec = a.act[ri];
+      const unsigned long long pos = gb + q;
+      if (pos < a.cap_edges) a.edges[pos] = make_uint2(__ldg(a.indices + rec.a + x), rec.di);
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       meta->n_edges = gb + tot;
