@@ -394,7 +394,8 @@ RelabelArgs relabel_args(const Bitmap& bm, const LayerBufs& b, const uint32_t* D
 // Frontier + sampling of one layer of one part (sample.cu kernels).
 uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* D,
                        uint64_t cap_dst, uint64_t n_dst_param, Bitmap& set_bm,
-                       const RelabelArgs& fused, uint64_t fused_work, bool smooth) {
+                       const RelabelArgs& fused, uint64_t fused_work, bool smooth,
+                       const ExtractArgs& ex) {
   const DeviceGraph& g = pl->g->g;
   const LayerBufs& b = w.L[l];
   LayerMeta* me = pl->meta_at(p, l);
@@ -441,15 +442,17 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   la.cap_edges = b.cap_edges;
   la.ticket = w.sync.tickets + 3 * l + 1;
   la.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l + 1;
-  la.status = w.sync.status_a;
+  la.status = w.sync.status_b;  // emit runs concurrently with extract (status_a)
   la.epoch = w.sync.epoch;
   la.slot = 8 * l + 3;
   la.overflow = w.sync.overflow;
   if (pl->kind == CB_NS) {
     launch_ns(la, D, b.out_prefix, g.indptr, g.indices, cap_dst, smooth, st);
-    return 3;
+    launch_extract(ex, st);
+    return 4;
   }
-  launch_labor(la, w.sync.max_tiles, smooth, st);
+  launch_labor(la, w.sync.max_tiles, smooth, st);  // labor_mark
+  launch_labor_post(la, w.sync.max_tiles, ex, st);  // emit || extract
   return 3;
 }
 
@@ -499,14 +502,12 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
           fused = relabel_args(w.bm[(l - 1) & 1], w.L[l - 1], Dp, pl->meta_at(p, l - 1));
           fused_work = w.L[l - 1].cap_edges;
         }
-        launches += enqueue_layer(pl, w, p, l, D, cap_dst,
-                                  l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[l & 1], fused,
-                                  fused_work, smooth);
-        launch_extract(extract_args(w, w.bm[l & 1], w.bm[(l + 1) & 1].bits, w.L[l].src,
-                                    w.L[l].cap_src, &pl->meta_at(p, l)->n_src,
-                                    &pl->meta_at(p, l + 1)->n_dst, 3 * l + 2, 8 * l + 4),
-                       st);
-        ++launches;
+        launches += enqueue_layer(
+            pl, w, p, l, D, cap_dst, l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[l & 1], fused,
+            fused_work, smooth,
+            extract_args(w, w.bm[l & 1], w.bm[(l + 1) & 1].bits, w.L[l].src, w.L[l].cap_src,
+                         &pl->meta_at(p, l)->n_src, &pl->meta_at(p, l + 1)->n_dst, 3 * l + 2,
+                         8 * l + 4));
       }
       const uint32_t* Dl = (L == 1) ? d_seeds + off[p] : w.L[L - 2].src;
       launch_relabel(relabel_args(w.bm[(L - 1) & 1], w.L[L - 1], Dl, pl->meta_at(p, L - 1)),
@@ -520,15 +521,14 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
       for (uint32_t p = 0; p < P; ++p) {
         PeWork& w = pl->pe[p];
         const uint32_t* D = (l == 0) ? d_seeds + off[p] : w.L[l].dst;
-        launches += enqueue_layer(pl, w, p, l, D, w.L[l].cap_dst,
-                                  l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[0], none, 0,
-                                  smooth);
-        launch_extract(extract_args(w, w.bm[0], w.bm[1].bits, w.L[l].src, w.L[l].cap_src,
-                                    &pl->meta_at(p, l)->n_src, nullptr, 3 * l + 2, 8 * l + 4),
-                       st);
+        launches += enqueue_layer(
+            pl, w, p, l, D, w.L[l].cap_dst, l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[0], none,
+            0, smooth,
+            extract_args(w, w.bm[0], w.bm[1].bits, w.L[l].src, w.L[l].cap_src,
+                         &pl->meta_at(p, l)->n_src, nullptr, 3 * l + 2, 8 * l + 4));
         launch_relabel(relabel_args(w.bm[0], w.L[l], D, pl->meta_at(p, l)),
                        std::max(w.L[l].cap_edges, w.L[l].cap_dst), st);
-        launches += 2;
+        launches += 1;
         max_src = std::max(max_src, w.L[l].cap_src);
       }
       PartPtrs pp{};
@@ -1195,14 +1195,14 @@ int cb_rows_device(cb_plan* plan, uint32_t part, void** ptr, uint64_t* rows) {
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n) {
   return guard([&] {
     require(plan != nullptr && n != nullptr, "null argument");
-    const uint64_t samp = 3;  // frontier + labor mark/emit | ns reservoir/emit
+    const uint64_t samp = (plan->kind == CB_NS) ? 4 : 3;  // incl. extract
     const uint64_t P = plan->P;
     const uint64_t L = plan->L;
     uint64_t k;
     if (mode == CB_MODE_COOP && P > 1)
-      k = P + L * (P * (samp + 2) + 1 + P + 1);
+      k = P + L * (P * (samp + 1) + 1 + P + 1);
     else
-      k = P * (1 + L * (samp + 1) + 1);
+      k = P * (1 + L * samp + 1);
     if (with_gather) k += P;
     *n = k;
   });

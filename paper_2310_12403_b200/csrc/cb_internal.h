@@ -202,6 +202,8 @@ void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix
                const uint64_t* indptr, const uint32_t* indices, uint64_t cap_dst, bool smooth,
                cudaStream_t st);
 void launch_extract(const ExtractArgs& a, cudaStream_t st);
+void launch_labor_post(const LaborArgs& a, uint64_t max_tiles, const ExtractArgs& e,
+                       cudaStream_t st);
 void launch_relabel(const RelabelArgs& r, uint64_t work, cudaStream_t st);
 void launch_clear(Bitmap& bm, const uint32_t* list, const unsigned long long* count,
                   cudaStream_t st);

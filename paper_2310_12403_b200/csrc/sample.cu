@@ -44,11 +44,12 @@ __device__ __forceinline__ uint32_t bm_rank(const uint32_t* bits, const uint32_t
 
 // Reset a ticket counter once every CTA of the launch is done with it, so no
 // per-batch memset of the tickets is needed.
-__device__ __forceinline__ void retire_ticket(unsigned* ticket, unsigned* exit_ctr) {
+__device__ __forceinline__ void retire_ticket(unsigned* ticket, unsigned* exit_ctr,
+                                              unsigned ncta) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(exit_ctr, 1u) == gridDim.x - 1) {
+    if (atomicAdd(exit_ctr, 1u) == ncta - 1) {
       *ticket = 0;
       *exit_ctr = 0;
       __threadfence();
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelAr
     meta->n_edges = 0;
     if (is_ns) a.out_prefix[0] = 0;
   }
-  retire_ticket(a.ticket, a.exit_ctr);
+  retire_ticket(a.ticket, a.exit_ctr, gridDim.x);
 }
 
 // Largest record index in [lo, hi] whose scan prefix is <= x.
@@ -259,8 +260,9 @@ template <int IPT, bool SMOOTH>
 __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
   constexpr int TILE = kNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
-  constexpr int kRecs = 512;  // records staged in smem (else global path)
-  __shared__ unsigned long long s_pre[kRecs];
+  constexpr int WSPAN = 32 * IPT;  // contiguous positions owned by one warp
+  constexpr int kRecs = 512;       // records staged in smem (else global path)
+  __shared__ unsigned long long s_pre[kRecs + 1];
   __shared__ unsigned long long s_base[kRecs];
   __shared__ unsigned long long s_th[kRecs];
   LayerMeta* meta = a.meta;
@@ -271,6 +273,7 @@ __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
   // prefix({kStreamLabor, layer}) under z1 (and z2 when smoothed)
   const uint64_t p1 = hstep(hstep(hinit(v.z1), 2ULL), static_cast<uint64_t>(a.layer));
   const uint64_t p2 = SMOOTH ? hstep(hstep(hinit(v.z2), 2ULL), static_cast<uint64_t>(a.layer)) : 0;
+  const uint32_t warp = threadIdx.x >> 5;
   unsigned long long uncert = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t x0 = tile * TILE;
@@ -287,49 +290,56 @@ __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
         s_base[i] = rec.a;
         s_th[i] = rec.b;
       }
+      if (threadIdx.x == 0) s_pre[nd] = ~0ULL;
       __syncthreads();
     }
-    uint32_t tv[IPT];
-    uint32_t li[IPT];
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-      const uint64_t xw = x0 + static_cast<uint64_t>(j) * kNT + (threadIdx.x & ~31u);
-      const uint64_t x = xw + lane_id();
-      uint64_t base;
-      if (staged) {
-        // the warp's 32 consecutive positions usually share one record
-        uint32_t lo = 0, hi = nd - 1;
-        if (lane_id() == 0) {
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) >> 1;
-            if (s_pre[mid] <= xw) lo = mid;
-            else hi = mid - 1;
-          }
-        }
-        lo = __shfl_sync(0xffffffffu, lo, 0);
-        if (lo + 1 < nd && s_pre[lo + 1] <= x) {
-          hi = nd - 1;
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) >> 1;
-            if (s_pre[mid] <= x) lo = mid;
-            else hi = mid - 1;
-          }
-        }
-        li[j] = lo;
-        base = s_base[lo];
-      } else {
-        li[j] = rec_search(a.act, a0, a1, x < x1 ? x : x1 - 1);
-        base = a.act[li[j]].a;
+    const uint64_t xw0 = x0 + static_cast<uint64_t>(warp) * WSPAN;
+    if (xw0 >= x1) continue;
+    // record of the warp's first position (lane-parallel 32-ary search)
+    uint32_t cur;
+    if (staged) {
+      uint32_t lo = 0, hi = nd - 1;
+      while (lo < hi) {  // narrow by 32 candidates per step
+        const uint32_t step = (hi - lo + 32) / 32;
+        const uint32_t cand = lo + lane_id() * step;
+        const bool le = cand <= hi && s_pre[cand] <= xw0;
+        const unsigned m = __ballot_sync(0xffffffffu, le);
+        const uint32_t best = lo + (31 - __clz(m)) * step;
+        lo = best;
+        hi = min(hi, best + step - 1);
+        if (step == 1) break;
       }
-      tv[j] = (x < x1) ? __ldg(a.indices + base + x) : 0u;
+      cur = lo;
+    } else {
+      cur = rec_search(a.act, a0, a1, xw0) - a0;
+    }
+    auto pre_of = [&](uint32_t i) -> uint64_t {
+      return staged ? s_pre[i] : (a0 + i <= a1 ? a.act[a0 + i].pre : ~0ULL);
+    };
+    uint32_t li[IPT];
+    uint32_t tv[IPT];
+    {
+      uint32_t c = cur;
+      uint64_t nxt = pre_of(c + 1);
+#pragma unroll
+      for (int j = 0; j < IPT; ++j) {
+        const uint64_t x = xw0 + j * 32 + lane_id();
+        while (x >= nxt) {  // forward walk: only at record boundaries
+          ++c;
+          nxt = pre_of(c + 1);
+        }
+        li[j] = c;
+        const uint64_t base = staged ? s_base[c] : a.act[a0 + c].a;
+        tv[j] = (x < x1) ? __ldg(a.indices + base + x) : 0u;
+      }
     }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
-      const uint64_t xw = x0 + static_cast<uint64_t>(j) * kNT + (threadIdx.x & ~31u);
+      const uint64_t xw = xw0 + j * 32;
       const uint64_t x = xw + lane_id();
       bool keep = false;
       if (x < x1) {
-        const uint64_t th = staged ? s_th[li[j]] : a.act[li[j]].b;
+        const uint64_t th = staged ? s_th[li[j]] : a.act[a0 + li[j]].b;
         if (th == ~0ULL) {
           keep = true;
         } else if (!SMOOTH) {
@@ -344,7 +354,7 @@ __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane_id() == 0 && xw < x1) {
         a.keep_words[xw >> 5] = bal;
-        a.word_rec[xw >> 5] = staged ? a0 + li[j] : li[j];  // record of position xw
+        a.word_rec[xw >> 5] = a0 + li[j];  // record of position xw
       }
       if (keep) set_bit(a.bits, tv[j]);
     }
@@ -362,7 +372,7 @@ constexpr int kEmitTileWords = kNT * kEmitWPT;  // 2048 words = 65536 positions
 // over all threads (item q -> its word by binary search over the per-word
 // output bases in smem), so every kept edge is an independent chain:
 // word_rec -> record -> neighbour id -> store.
-__global__ void __launch_bounds__(kNT) labor_emit_kernel(LaborArgs a) {
+__device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned ncta) {
   __shared__ unsigned long long s_scan[kNT / 32 + 1];
   __shared__ uint32_t s_wbase[kEmitTileWords + 1];
   __shared__ uint32_t s_word[kEmitTileWords];
@@ -416,7 +426,7 @@ __global__ void __launch_bounds__(kNT) labor_emit_kernel(LaborArgs a) {
       if (gb + tot > a.cap_edges) atomicExch(a.overflow, 1u);
     }
   }
-  retire_ticket(a.ticket, a.exit_ctr);
+  retire_ticket(a.ticket, a.exit_ctr, ncta);
 }
 
 // ---------------------------------------------------------------- NS -------
@@ -515,7 +525,7 @@ __global__ void __launch_bounds__(kNT) ns_emit_kernel(
 // Sorted unique list = set bits in id order; wprefix[w] = rank of word w.
 constexpr int kWPT = 2;  // words per thread (one 8-byte load)
 static_assert(kNT * kWPT == kExtractTileWords, "extract tile");
-__global__ void __launch_bounds__(kNT) extract_kernel(ExtractArgs a) {
+__device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned ncta) {
   __shared__ unsigned long long s_scan[kNT / 32 + 1];
   __shared__ unsigned long long s_b;
   __shared__ unsigned s_tile;
@@ -552,7 +562,18 @@ __global__ void __launch_bounds__(kNT) extract_kernel(ExtractArgs a) {
       if (gb + tot > a.cap_out) atomicExch(a.overflow, 1u);
     }
   }
-  retire_ticket(a.ticket, a.exit_ctr);
+  retire_ticket(a.ticket, a.exit_ctr, ncta);
+}
+
+__global__ void __launch_bounds__(kNT) extract_kernel(ExtractArgs a) {
+  extract_body(a, gridDim.x);
+}
+
+// Extract (dedup of the layer) and the ordered LABOR edge emission only
+// depend on labor_mark, not on each other: one launch, CTAs split by role.
+__global__ void __launch_bounds__(kNT) post_kernel(ExtractArgs e, LaborArgs a, unsigned n_ext) {
+  if (blockIdx.x < n_ext) extract_body(e, n_ext);
+  else labor_emit_body(a, gridDim.x - n_ext);
 }
 
 // ---------------------------------------------------------------- relabel --
@@ -614,10 +635,15 @@ void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStrea
   if (smooth && a.kind != 0) labor_mark_kernel<kLaborIPT, true><<<grid, kNT, 0, st>>>(a);
   else labor_mark_kernel<kLaborIPT, false><<<grid, kNT, 0, st>>>(a);
   CB_LAUNCH("labor_mark");
+}
+
+void launch_labor_post(const LaborArgs& a, uint64_t max_tiles, const ExtractArgs& e,
+                       cudaStream_t st) {
   const uint64_t words = (max_tiles * kLaborTile + 31) / 32;
-  const int g2 = grid_for(words, kEmitTileWords, 4);
-  labor_emit_kernel<<<g2, kNT, 0, st>>>(a);
-  CB_LAUNCH("labor_emit");
+  const int g_emit = grid_for(words, kEmitTileWords, 4);
+  const int g_ext = grid_for(e.words_padded, kNT * kWPT, 4);
+  post_kernel<<<g_emit + g_ext, kNT, 0, st>>>(e, a, static_cast<unsigned>(g_ext));
+  CB_LAUNCH("post");
 }
 
 void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix,
