@@ -153,6 +153,12 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
 int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_device,
                    const cb_sched* sched, int what);
 
+/* One eager batch (+ gather when f != NULL) with a CUDA event after every
+ * launch: ms[i] = device time of launch i, in enqueue order. */
+int cb_plan_profile(cb_plan* plan, int mode, const uint32_t* seeds_flat,
+                    const uint64_t* seeds_off, const cb_sched* sched, const cb_features* f,
+                    float* ms, int max_n, int* n);
+
 /* Number of kernels one cb_sample/cb_gather call enqueues (for reporting). */
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n);
 

@@ -57,6 +57,8 @@ _SIGS = {
     "cb_rows_device": (C.c_int, [_P, _u32, _PP, C.POINTER(_u64)]),
     "cb_plan_capture": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched)]),
     "cb_plan_replay": (C.c_int, [_P, _P, C.c_int, C.POINTER(Sched), C.c_int]),
+    "cb_plan_profile": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched), _P, _P, C.c_int,
+                                  C.POINTER(C.c_int)]),
     "cb_plan_launch_count": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_u64)]),
 }
 

@@ -369,6 +369,18 @@ class Plan:
     def synchronize(self):
         _check(_lib.load().cb_synchronize(self._h))
 
+    def profile(self, per_pe_seeds, schedule: SeedSchedule, mode: int = MODE_COOP,
+                store: FeatureStore | None = None) -> list[float]:
+        """Per-launch device times (ms) of one eager batch, enqueue order."""
+        flat, off = self._flat(per_pe_seeds)
+        ms = np.zeros(256, np.float32)
+        n = C.c_int()
+        s = schedule._c()
+        _check(_lib.load().cb_plan_profile(self._h, mode, _ptr(flat), _ptr(off), C.byref(s),
+                                           store._h if store else None, _ptr(ms), 256,
+                                           C.byref(n)))
+        return ms[: n.value].tolist()
+
     def launch_count(self, mode: int, with_gather: bool) -> int:
         n = C.c_uint64()
         _check(_lib.load().cb_plan_launch_count(self._h, mode, int(with_gather), C.byref(n)))

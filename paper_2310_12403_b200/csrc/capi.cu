@@ -146,6 +146,7 @@ struct cb_plan {
   int mode = -1;          // mode of the last batch
   int dirty_mode = -1;    // mode whose final bitmap still holds bits (-1: clean)
   bool smooth = false;    // kernels of the last enqueue used smoothed variates
+  std::vector<cudaEvent_t>* prof = nullptr;  // per-launch events (cb_plan_profile)
   bool cap_smooth = false;
   bool have_batch = false;
   bool have_rows = false;
@@ -329,6 +330,14 @@ void check_ownership_host(const cb_plan* pl, const uint32_t* flat, const uint64_
                                   " is not owned by part " + std::to_string(p));
 }
 
+void prof_mark(cb_plan* pl) {
+  if (!pl->prof) return;
+  cudaEvent_t e;
+  CB_CUDA(cudaEventCreate(&e));
+  CB_CUDA(cudaEventRecord(e, pl->stream));
+  pl->prof->push_back(e);
+}
+
 // Which bitmap still holds bits after a batch of `mode`, and the id list
 // (with its device count) that names every set word.
 struct Dirty {
@@ -424,6 +433,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   fa.slot = 8 * l;
   fa.overflow = w.sync.overflow;
   launch_frontier(fa, fused, cap_dst, fused_work, st);
+  prof_mark(pl);
   LaborArgs la{};
   la.meta = me;
   la.act = b.act;
@@ -448,11 +458,15 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   la.overflow = w.sync.overflow;
   if (pl->kind == CB_NS) {
     launch_ns(la, D, b.out_prefix, g.indptr, g.indices, cap_dst, smooth, st);
+    prof_mark(pl);
     launch_extract(ex, st);
+    prof_mark(pl);
     return 4;
   }
   launch_labor(la, w.sync.max_tiles, smooth, st);  // labor_mark
+  prof_mark(pl);
   launch_labor_post(la, w.sync.max_tiles, ex, st);  // emit || extract
+  prof_mark(pl);
   return 3;
 }
 
@@ -486,6 +500,7 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
     launch_batch_begin(pl->pe[p].sync, d.bits, d.list, d.count, d.cap,
                        pl->pe[p].bm[0].words_padded, st);
     ++launches;
+    prof_mark(pl);
   }
   const RelabelArgs none{};
 
@@ -513,6 +528,7 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
       launch_relabel(relabel_args(w.bm[(L - 1) & 1], w.L[L - 1], Dl, pl->meta_at(p, L - 1)),
                      std::max(w.L[L - 1].cap_edges, w.L[L - 1].cap_dst), st);
       ++launches;
+      prof_mark(pl);
     }
   } else {
     CB_CUDA(cudaMemsetAsync(pl->send_counts, 0, sizeof(unsigned long long) * L * P * P, st));
@@ -623,6 +639,7 @@ void enqueue_gather(cb_plan* pl, const cb_features* f) {
     launch_gather(f->table, vb, f->row_bytes, b.src, &pl->meta_at(p, pl->L - 1)->n_src,
                   w.cap_rows, f->row_map, w.rows, pl->stream);
     pl->launches += 1;
+    prof_mark(pl);
   }
   pl->have_rows = true;
 }
@@ -1189,6 +1206,37 @@ int cb_rows_device(cb_plan* plan, uint32_t part, void** ptr, uint64_t* rows) {
     DeviceGuard dg(plan->device);
     *ptr = plan->pe[part].rows;
     if (rows) *rows = host_meta(plan, part, plan->L - 1).n_src;
+  });
+}
+
+int cb_plan_profile(cb_plan* plan, int mode, const uint32_t* seeds_flat,
+                    const uint64_t* seeds_off, const cb_sched* sched, const cb_features* f,
+                    float* ms, int max_n, int* n) {
+  return guard([&] {
+    require(plan != nullptr && ms != nullptr && n != nullptr, "null argument");
+    DeviceGuard dg(plan->device);
+    std::vector<cudaEvent_t> ev;
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    plan->prof = &ev;
+    try {
+      prof_mark(plan);
+      sample_host(plan, mode, seeds_flat, seeds_off, sched);
+      if (f) {
+        prepare_rows(plan, f);
+        enqueue_gather(plan, f);
+      }
+    } catch (...) {
+      plan->prof = nullptr;
+      for (auto e : ev) cudaEventDestroy(e);
+      throw;
+    }
+    plan->prof = nullptr;
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    int k = 0;
+    for (size_t i = 1; i < ev.size() && k < max_n; ++i, ++k)
+      CB_CUDA(cudaEventElapsedTime(&ms[k], ev[i - 1], ev[i]));
+    *n = k;
+    for (auto e : ev) cudaEventDestroy(e);
   });
 }
 

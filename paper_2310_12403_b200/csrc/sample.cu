@@ -405,21 +405,48 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned nct
     }
     const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
     // (tile_prefix ends with __syncthreads: s_word / s_wbase are visible)
-    for (uint32_t q = threadIdx.x; q < tot; q += kNT) {
-      uint32_t lo = 0, hi = kEmitTileWords - 1;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (s_wbase[mid] <= q) lo = mid;
-        else hi = mid - 1;
+    constexpr int B = 4;  // kept items per thread in flight
+    for (uint32_t q0 = threadIdx.x; q0 < tot; q0 += kNT * B) {
+      uint64_t x[B];
+      uint32_t ri[B];
+      bool ok[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const uint32_t q = q0 + u * kNT;
+        ok[u] = q < tot;
+        x[u] = 0;
+        ri[u] = 0;
+        if (ok[u]) {
+          uint32_t lo = 0, hi = kEmitTileWords - 1;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (s_wbase[mid] <= q) lo = mid;
+            else hi = mid - 1;
+          }
+          uint32_t word = s_word[lo];
+          for (uint32_t r = q - s_wbase[lo]; r > 0; --r) word &= word - 1;
+          x[u] = (wt + lo) * 32 + (__ffs(word) - 1);
+          ri[u] = __ldg(&a.word_rec[wt + lo]);
+        }
       }
-      uint32_t word = s_word[lo];
-      for (uint32_t r = q - s_wbase[lo]; r > 0; --r) word &= word - 1;
-      const uint64_t x = (wt + lo) * 32 + (__ffs(word) - 1);
-      uint32_t ri = __ldg(&a.word_rec[wt + lo]);
-      while (__ldg(&a.act[ri + 1].pre) <= x) ++ri;
-      const ActRec rec = a.act[ri];
-      const unsigned long long pos = gb + q;
-      if (pos < a.cap_edges) a.edges[pos] = make_uint2(__ldg(a.indices + rec.a + x), rec.di);
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        if (ok[u])
+          while (__ldg(&a.act[ri[u] + 1].pre) <= x[u]) ++ri[u];
+      uint32_t t[B], di[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        if (ok[u]) {
+          const ActRec rec = a.act[ri[u]];
+          di[u] = rec.di;
+          t[u] = __ldg(a.indices + rec.a + x[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const unsigned long long pos = gb + q0 + u * kNT;
+        if (ok[u] && pos < a.cap_edges) a.edges[pos] = make_uint2(t[u], di[u]);
+      }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       meta->n_edges = gb + tot;
