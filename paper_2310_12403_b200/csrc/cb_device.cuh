@@ -113,13 +113,16 @@ static __device__ __noinline__ double smooth_finish(const Variates& v, uint64_t 
 constexpr double kGuard = 1e-12;
 
 // ---- memory-order helpers ---------------------------------------------------
+// Look-back status words carry their own payload (the aggregate / prefix), and
+// consumers read nothing else a producer wrote, so relaxed gpu-scope
+// accesses suffice: no fence waits on the producer's outstanding bitmap REDs.
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;

@@ -48,11 +48,10 @@ __device__ __forceinline__ void retire_ticket(unsigned* ticket, unsigned* exit_c
                                               unsigned ncta) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    // every ticket atomic of this CTA has returned, i.e. is performed
     if (atomicAdd(exit_ctr, 1u) == ncta - 1) {
-      *ticket = 0;
-      *exit_ctr = 0;
-      __threadfence();
+      atomicExch(ticket, 0u);
+      atomicExch(exit_ctr, 0u);
     }
   }
 }
