@@ -255,14 +255,76 @@ __device__ __forceinline__ void tile_records(const ActRec* act, const uint32_t* 
 //   labor_emit : ordered popcount compaction of the keep words (decoupled
 //                look-back over 64K-position tiles) -> edges in scan order =
 //                grouped by dst, CSR order inside a dst (the reference order)
+// Per-warp body of labor_mark: IPT words of 32 consecutive positions starting
+// at tile-relative offset r0. Records come either from smem (STAGED) or
+// straight from the global record array (tiles spanning > kRecs records).
+template <int IPT, bool SMOOTH, bool STAGED>
+__device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v, uint64_t p1,
+                                          uint64_t p2, uint64_t x0, uint32_t r0, uint32_t rend,
+                                          uint32_t a0, uint32_t a1, uint32_t cur,
+                                          const uint32_t* s_nxt, const uint32_t* const* s_row,
+                                          const unsigned long long* s_th,
+                                          unsigned long long& uncert) {
+  const uint32_t lane = lane_id();
+  auto nxt_of = [&](uint32_t c) -> uint32_t {  // tile-relative start of record c+1
+    if (STAGED) return s_nxt[c];
+    if (a0 + c + 1 > a1) return 0xffffffffu;
+    const uint64_t pr = __ldg(&a.act[a0 + c + 1].pre);
+    return static_cast<uint32_t>(min(pr - x0, static_cast<uint64_t>(0xffffffffu)));
+  };
+  uint32_t li[IPT];
+  uint32_t tv[IPT];
+  uint32_t c = cur;
+  uint32_t nxt = nxt_of(c);
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const uint32_t r = r0 + j * 32 + lane;
+    while (r >= nxt) {  // forward walk, only at record boundaries
+      ++c;
+      nxt = nxt_of(c);
+    }
+    li[j] = c;
+    const uint32_t* row =
+        STAGED ? s_row[c] : a.indices + (a.act[a0 + c].a + x0);  // row + r = neighbour
+    tv[j] = (r < rend) ? __ldg(row + r) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const uint32_t rw = r0 + j * 32;
+    const uint32_t r = rw + lane;
+    bool keep = false;
+    if (r < rend) {
+      const uint64_t th = STAGED ? s_th[li[j]] : __ldg(&a.act[a0 + li[j]].b);
+      if (th == ~0ULL) {
+        keep = true;
+      } else if (!SMOOTH) {
+        keep = (hstep(p1, tv[j]) >> 11) <= th;
+      } else {
+        const double thr = __longlong_as_double(static_cast<long long>(th));
+        const double rr = smooth_finish(v, hstep(p1, tv[j]), hstep(p2, tv[j]));
+        keep = rr <= thr;
+        if (fabs(rr - thr) <= kGuard * thr) ++uncert;
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0 && rw < rend) {
+      const uint64_t wi = (x0 + rw) >> 5;
+      a.keep_words[wi] = bal;
+      a.word_rec[wi] = a0 + li[j];  // record of the word's first position
+    }
+    if (keep) set_bit(a.bits, tv[j]);
+  }
+}
+
 template <int IPT, bool SMOOTH>
 __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
   constexpr int TILE = kNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
-  constexpr int WSPAN = 32 * IPT;  // contiguous positions owned by one warp
-  constexpr int kRecs = 512;       // records staged in smem (else global path)
-  __shared__ unsigned long long s_pre[kRecs + 1];
-  __shared__ unsigned long long s_base[kRecs];
+  constexpr uint32_t WSPAN = 32 * IPT;  // contiguous positions owned by one warp
+  constexpr int kRecs = 512;            // records staged in smem (else global path)
+  __shared__ uint32_t s_pre[kRecs];     // tile-relative record starts (clamped at 0)
+  __shared__ uint32_t s_nxt[kRecs];     // tile-relative start of the next record
+  __shared__ const uint32_t* s_row[kRecs];
   __shared__ unsigned long long s_th[kRecs];
   LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
@@ -276,86 +338,44 @@ __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
   unsigned long long uncert = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t x0 = tile * TILE;
-    const uint64_t x1 = min(x0 + TILE, total);
+    const uint32_t rend = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), total - x0));
     uint32_t a0, a1;
-    tile_records(a.act, a.tile_first, n_act, tile, x1, a0, a1);
+    tile_records(a.act, a.tile_first, n_act, tile, x0 + rend, a0, a1);
     const uint32_t nd = a1 - a0 + 1;
     const bool staged = nd <= kRecs;
     __syncthreads();  // previous tile done with the staging buffers
     if (staged) {
       for (uint32_t i = threadIdx.x; i < nd; i += kNT) {
         const ActRec rec = a.act[a0 + i];
-        s_pre[i] = rec.pre;
-        s_base[i] = rec.a;
+        s_pre[i] = rec.pre > x0 ? static_cast<uint32_t>(rec.pre - x0) : 0u;
+        s_row[i] = a.indices + (rec.a + x0);
         s_th[i] = rec.b;
+        const uint64_t nx = (i + 1 < nd) ? a.act[a0 + i + 1].pre : ~0ULL;
+        s_nxt[i] = static_cast<uint32_t>(min(nx - x0, static_cast<uint64_t>(0xffffffffu)));
       }
-      if (threadIdx.x == 0) s_pre[nd] = ~0ULL;
       __syncthreads();
     }
-    const uint64_t xw0 = x0 + static_cast<uint64_t>(warp) * WSPAN;
-    if (xw0 >= x1) continue;
-    // record of the warp's first position (lane-parallel 32-ary search)
-    uint32_t cur;
+    const uint32_t r0 = warp * WSPAN;
+    if (r0 >= rend) continue;
     if (staged) {
+      // record of the warp's first position: 32-ary search over s_pre
       uint32_t lo = 0, hi = nd - 1;
-      while (lo < hi) {  // narrow by 32 candidates per step
+      while (lo < hi) {
         const uint32_t step = (hi - lo + 32) / 32;
         const uint32_t cand = lo + lane_id() * step;
-        const bool le = cand <= hi && s_pre[cand] <= xw0;
+        const bool le = cand <= hi && s_pre[cand] <= r0;
         const unsigned m = __ballot_sync(0xffffffffu, le);
         const uint32_t best = lo + (31 - __clz(m)) * step;
         lo = best;
         hi = min(hi, best + step - 1);
         if (step == 1) break;
       }
-      cur = lo;
+      mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, s_nxt, s_row, s_th,
+                                   uncert);
     } else {
-      cur = rec_search(a.act, a0, a1, xw0) - a0;
-    }
-    auto pre_of = [&](uint32_t i) -> uint64_t {
-      return staged ? s_pre[i] : (a0 + i <= a1 ? a.act[a0 + i].pre : ~0ULL);
-    };
-    uint32_t li[IPT];
-    uint32_t tv[IPT];
-    {
-      uint32_t c = cur;
-      uint64_t nxt = pre_of(c + 1);
-#pragma unroll
-      for (int j = 0; j < IPT; ++j) {
-        const uint64_t x = xw0 + j * 32 + lane_id();
-        while (x >= nxt) {  // forward walk: only at record boundaries
-          ++c;
-          nxt = pre_of(c + 1);
-        }
-        li[j] = c;
-        const uint64_t base = staged ? s_base[c] : a.act[a0 + c].a;
-        tv[j] = (x < x1) ? __ldg(a.indices + base + x) : 0u;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-      const uint64_t xw = xw0 + j * 32;
-      const uint64_t x = xw + lane_id();
-      bool keep = false;
-      if (x < x1) {
-        const uint64_t th = staged ? s_th[li[j]] : a.act[a0 + li[j]].b;
-        if (th == ~0ULL) {
-          keep = true;
-        } else if (!SMOOTH) {
-          keep = (hstep(p1, tv[j]) >> 11) <= th;
-        } else {
-          const double thr = __longlong_as_double(static_cast<long long>(th));
-          const double r = smooth_finish(v, hstep(p1, tv[j]), hstep(p2, tv[j]));
-          keep = r <= thr;
-          if (fabs(r - thr) <= kGuard * thr) ++uncert;
-        }
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (lane_id() == 0 && xw < x1) {
-        a.keep_words[xw >> 5] = bal;
-        a.word_rec[xw >> 5] = a0 + li[j];  // record of position xw
-      }
-      if (keep) set_bit(a.bits, tv[j]);
+      const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
+      mark_span<IPT, SMOOTH, false>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, s_nxt, s_row,
+                                    s_th, uncert);
     }
   }
   if (SMOOTH) {
