@@ -255,9 +255,23 @@ __device__ __forceinline__ void tile_records(const ActRec* act, const uint32_t* 
 //   labor_emit : ordered popcount compaction of the keep words (decoupled
 //                look-back over 64K-position tiles) -> edges in scan order =
 //                grouped by dst, CSR order inside a dst (the reference order)
+// Keep decision for neighbour t under threshold th (frontier ActRec.b). Plain
+// stream: th = ~0 (keep all) needs no special case since (h>>11) < 2^53.
+template <bool SMOOTH>
+__device__ __forceinline__ bool keep_rule(const Variates& v, uint64_t p1, uint64_t p2,
+                                          uint32_t t, uint64_t th, unsigned long long& uncert) {
+  if (!SMOOTH) return (hstep(p1, t) >> 11) <= th;
+  if (th == ~0ULL) return true;
+  const double thr = __longlong_as_double(static_cast<long long>(th));
+  const double rr = smooth_finish(v, hstep(p1, t), hstep(p2, t));
+  if (fabs(rr - thr) <= kGuard * thr) ++uncert;
+  return rr <= thr;
+}
+
 // Per-warp body of labor_mark: IPT words of 32 consecutive positions starting
 // at tile-relative offset r0. Records come either from smem (STAGED) or
 // straight from the global record array (tiles spanning > kRecs records).
+// Lane j keeps word j's ballot and record; one coalesced store at the end.
 template <int IPT, bool SMOOTH, bool STAGED>
 __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v, uint64_t p1,
                                           uint64_t p2, uint64_t x0, uint32_t r0, uint32_t rend,
@@ -265,6 +279,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
                                           const uint32_t* s_nxt, const uint32_t* const* s_row,
                                           const unsigned long long* s_th,
                                           unsigned long long& uncert) {
+  static_assert(IPT <= 32, "one word per lane");
   const uint32_t lane = lane_id();
   auto nxt_of = [&](uint32_t c) -> uint32_t {  // tile-relative start of record c+1
     if (STAGED) return s_nxt[c];
@@ -272,47 +287,61 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
     const uint64_t pr = __ldg(&a.act[a0 + c + 1].pre);
     return static_cast<uint32_t>(min(pr - x0, static_cast<uint64_t>(0xffffffffu)));
   };
-  uint32_t li[IPT];
-  uint32_t tv[IPT];
-  uint32_t c = cur;
-  uint32_t nxt = nxt_of(c);
+  auto row_of = [&](uint32_t c) -> const uint32_t* {
+    return STAGED ? s_row[c] : a.indices + (__ldg(&a.act[a0 + c].a) + x0);
+  };
+  auto th_of = [&](uint32_t c) -> uint64_t {
+    return STAGED ? s_th[c] : __ldg(&a.act[a0 + c].b);
+  };
+  uint32_t my_word = 0, my_rec = 0;
+  const uint32_t nxt0 = nxt_of(cur);
+  if (nxt0 >= r0 + 32 * IPT && r0 + 32 * IPT <= rend) {
+    // fast path: the whole span lies inside record `cur`
+    const uint32_t* row = row_of(cur) + r0 + lane;
+    const uint64_t th = th_of(cur);
+    uint32_t tv[IPT];
 #pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    const uint32_t r = r0 + j * 32 + lane;
-    while (r >= nxt) {  // forward walk, only at record boundaries
-      ++c;
-      nxt = nxt_of(c);
+    for (int j = 0; j < IPT; ++j) tv[j] = __ldg(row + j * 32);
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const bool keep = keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert);
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (lane == j) my_word = bal;
+      if (keep) set_bit(a.bits, tv[j]);
     }
-    li[j] = c;
-    const uint32_t* row =
-        STAGED ? s_row[c] : a.indices + (a.act[a0 + c].a + x0);  // row + r = neighbour
-    tv[j] = (r < rend) ? __ldg(row + r) : 0u;
-  }
+    my_rec = a0 + cur;
+  } else {
+    uint32_t li[IPT];
+    uint32_t tv[IPT];
+    uint32_t c = cur;
+    uint32_t nxt = nxt0;
 #pragma unroll
-  for (int j = 0; j < IPT; ++j) {
-    const uint32_t rw = r0 + j * 32;
-    const uint32_t r = rw + lane;
-    bool keep = false;
-    if (r < rend) {
-      const uint64_t th = STAGED ? s_th[li[j]] : __ldg(&a.act[a0 + li[j]].b);
-      if (th == ~0ULL) {
-        keep = true;
-      } else if (!SMOOTH) {
-        keep = (hstep(p1, tv[j]) >> 11) <= th;
-      } else {
-        const double thr = __longlong_as_double(static_cast<long long>(th));
-        const double rr = smooth_finish(v, hstep(p1, tv[j]), hstep(p2, tv[j]));
-        keep = rr <= thr;
-        if (fabs(rr - thr) <= kGuard * thr) ++uncert;
+    for (int j = 0; j < IPT; ++j) {
+      const uint32_t r = r0 + j * 32 + lane;
+      while (r >= nxt) {  // forward walk, only at record boundaries
+        ++c;
+        nxt = nxt_of(c);
       }
+      li[j] = c;
+      tv[j] = (r < rend) ? __ldg(row_of(c) + r) : 0u;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0 && rw < rend) {
-      const uint64_t wi = (x0 + rw) >> 5;
-      a.keep_words[wi] = bal;
-      a.word_rec[wi] = a0 + li[j];  // record of the word's first position
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const uint32_t r = r0 + j * 32 + lane;
+      const bool keep = (r < rend) && keep_rule<SMOOTH>(v, p1, p2, tv[j], th_of(li[j]), uncert);
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      const uint32_t wrec = __shfl_sync(0xffffffffu, li[j], 0);
+      if (lane == j) {
+        my_word = bal;
+        my_rec = a0 + wrec;
+      }
+      if (keep) set_bit(a.bits, tv[j]);
     }
-    if (keep) set_bit(a.bits, tv[j]);
+  }
+  if (lane < IPT && r0 + lane * 32 < rend) {
+    const uint64_t wi = ((x0 + r0) >> 5) + lane;
+    a.keep_words[wi] = my_word;
+    a.word_rec[wi] = my_rec;  // record of the word's first position
   }
 }
 
