@@ -137,6 +137,8 @@ void ob_sched_advance(ob_sched* s) {
   }
 }
 
+double ob_normal_from_bits(uint64_t bits) { return normal_from_bits(bits); }
+
 /* samplers.hpp:53-126 VariateSource */
 typedef struct {
   uint64_t z1, z2;
@@ -187,6 +189,14 @@ static double vsrc_finish(const vsrc* v, uint64_t b1, uint64_t b2) {
 /* samplers.hpp:102-104 */
 static double vsrc_tail1(const vsrc* v, const vpfx* p, uint64_t a) {
   return vsrc_finish(v, hstep(p->h1, a), v->smoothed ? hstep(p->h2, a) : 0);
+}
+
+/* Variate of neighbour t as labor_block_stream draws it (samplers.cpp:112-129). */
+double ob_labor_variate(const ob_sched* sched, int layer, uint32_t t) {
+  const vsrc v = vsrc_from(sched);
+  const uint64_t ids[2] = {2, (uint64_t)layer};
+  const vpfx p = vsrc_prefix(&v, ids, 2);
+  return vsrc_tail1(&v, &p, t);
 }
 
 /* ------------------------------------------------------------- sorting --- */

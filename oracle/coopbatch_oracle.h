@@ -33,6 +33,8 @@ double ob_hash_uniform(uint64_t seed, const uint64_t* ids, int n_ids);
 /* rng.cpp:7-52 */
 double ob_phi(double x);
 double ob_inverse_phi(double p);
+double ob_normal_from_bits(uint64_t bits);
+double ob_labor_variate(const ob_sched* sched, int layer, uint32_t t);
 /* rng.cpp:69-86 */
 void ob_sched_make(uint64_t kappa, uint64_t root_seed, ob_sched* out);
 void ob_sched_advance(ob_sched* s);

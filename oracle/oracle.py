@@ -97,6 +97,10 @@ def lib(impl: str = "restated") -> C.CDLL:
         L.ob_phi.argtypes = [_f64]
         L.ob_inverse_phi.restype = _f64
         L.ob_inverse_phi.argtypes = [_f64]
+        L.ob_normal_from_bits.restype = _f64
+        L.ob_normal_from_bits.argtypes = [_u64]
+        L.ob_labor_variate.restype = _f64
+        L.ob_labor_variate.argtypes = [C.POINTER(Sched), C.c_int, _u32]
         L.ob_sched_make.argtypes = [_u64, _u64, C.POINTER(Sched)]
         L.ob_sched_advance.argtypes = [C.POINTER(Sched)]
         L.ob_rmat.argtypes = [_u64, _u64, _u64, C.POINTER(C.POINTER(_u64)),
@@ -547,3 +551,32 @@ def reference_step(rg: RefGraph, fs: RefFeatureStore, mode: int, owner, parts: i
                         kind, fanout, C.byref(sched), C.byref(ts), C.byref(tg),
                         C.byref(rows)), rg.L)
     return ts.value, tg.value, rows.value
+
+
+def dependent_experiment_restated(g: CSR, kappa: int, batch: int, steps: int, capacity: int,
+                                  kind: int, fanout: int, L: int, dim: int, bps: int,
+                                  seed: int) -> dict:
+    """run_dependent_experiment (cache.cpp:137-208), smoothed mode, composed from
+    the restated pieces: Fisher-Yates order (hash(seed,{8,i})), SeedSchedule,
+    expand, stack_fingerprint, access_order, LRU."""
+    n = g.n
+    b = min(batch, n)
+    order = np.arange(n, dtype=np.uint32)
+    for i in range(n, 1, -1):
+        j = int(lib().ob_hash_uniform(seed, _ptr(np.array([8, i], np.uint64)), 2) * i)
+        order[i - 1], order[min(j, i - 1)] = order[min(j, i - 1)], order[i - 1]
+    spe = max(1, n // b)
+    sched = make_sched(kappa, seed)
+    lru = Lru(capacity)
+    fp, sl, by = [], [], []
+    for step in range(steps):
+        slot = (step % spe) * b
+        st = expand(g, order[slot:slot + b], L, kind, fanout, sched)
+        sched = advance(sched)
+        fp.append(stack_fingerprint(st))
+        inputs = access_order(st[-1]["src"], hash_bits(seed, [step, 0xACCE55]))
+        miss = sum(lru.access(int(v)) for v in inputs)
+        sl.append(len(inputs))
+        by.append(miss * dim * bps)
+    return {"fingerprint": np.array(fp, np.uint64), "s_l": np.array(sl, np.uint64),
+            "bytes": np.array(by, np.uint64)}

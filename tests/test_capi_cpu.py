@@ -1,0 +1,86 @@
+"""CPU: the C-ABI boundary and the host-side mirror, without a GPU.
+
+* libcoopbatch_b200.so loads and exports every entry point declared in
+  include/coopbatch_cuda.h (no compute calls);
+* the .so was built for sm_100a (cubin present);
+* the host mirror's schedule / hash / seed-draw helpers equal the oracle's
+  restatement of rng.cpp / cli.cpp.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2310_12403_b200 import _lib
+    L = _lib.load()
+    syms = _lib.header_symbols()
+    assert len(syms) >= 30
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+    assert b"sm_100a" in L.cb_version()
+
+
+def test_library_is_sm100a():
+    from paper_2310_12403_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_no_device_is_a_clean_error():
+    """Without a GPU the product fails loudly (status + message), never falls back."""
+    from paper_2310_12403_b200 import _lib
+    L = _lib.load()
+    n = ctypes.c_int(-1)
+    rc = L.cb_device_count(ctypes.byref(n))
+    if rc == 0 and n.value > 0:
+        pytest.skip("a GPU is visible")
+    import paper_2310_12403_b200 as cb
+    with pytest.raises((cb.CudaError, cb.InputError)):
+        cb.Graph.generate_rmat(1 << 10, 1 << 12, 1)
+
+
+def test_schedule_and_hash_mirror():
+    import paper_2310_12403_b200 as cb
+    for kappa in (1, 2, 7, cb.KAPPA_INFINITY):
+        a = cb.SeedSchedule.make(kappa, 1234)
+        b = O.make_sched(kappa, 1234)
+        for _ in range(30):
+            assert (a.kappa, a.z1, a.z2, a.iteration) == (b.kappa, b.z1, b.z2, b.iteration)
+            a, b = cb.schedule_advance(a), O.advance(b)
+    for ids in ([1], [2, 3, 4], [8, 1 << 40, 0]):
+        assert cb.hash_bits(99, ids) == O.hash_bits(99, ids)
+        assert cb.mix64(ids[-1]) == O.lib().ob_mix64(ids[-1])
+
+
+def test_seed_draws_mirror():
+    from paper_2310_12403_b200.seeds import coop_seeds, draw_from_pool
+    owner = O.partition_random(5000, 4, 7)
+    members = O.part_members(owner, 4)
+    for step in range(3):
+        a = coop_seeds(members, 64, 7, step)
+        b = O.draw_coop_seeds(owner, 4, 64, 7, step)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    pool = np.arange(100, dtype=np.uint32)
+    assert np.array_equal(draw_from_pool(pool, 100, 3, 5), O.draw_from_pool(pool, 100, 3, 5))
+    with pytest.raises(ValueError):
+        draw_from_pool(pool, 101, 3, 5)
+
+
+def test_header_matches_loader_table():
+    from paper_2310_12403_b200 import _lib
+    assert set(_lib._SIGS) == set(_lib.header_symbols())
+
+
+def test_build_artifacts_in_tree():
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    assert os.path.exists(os.path.join(root, "paper_2310_12403_b200", "libcoopbatch_b200.so"))
+    assert os.path.exists(os.path.join(root, "oracle", "liboracle.so"))
