@@ -153,6 +153,41 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
 int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_device,
                    const cb_sched* sched, int what);
 
+/* ---- multi-process cooperative step (one rank = one part) ----
+ * The library runs each part's kernels; the caller moves ids/rows between
+ * ranks (NCCL all-to-allv). This is build_exchange (coop.cpp:25-64) and
+ * all_to_all_forward (coop.cpp:145-159) split at the rank boundary.
+ * All pointers named d_* are device pointers on the plan's device. */
+int cb_plan_create_dist(const cb_graph* g, uint32_t world, int num_layers, int kind,
+                        const uint32_t* fanouts, uint64_t max_seeds, cb_plan** out);
+/* Sample block `layer` for frontier d_dst[n_dst]; returns |src| (sorted
+ * unique sampled ids, device list via cb_plan_layer_src). Synchronous. */
+int cb_plan_sample_layer(cb_plan* plan, int layer, const uint32_t* d_dst, uint64_t n_dst,
+                         const cb_sched* sched, uint64_t* n_src);
+int cb_plan_layer_src(cb_plan* plan, int layer, uint32_t** d_src);
+/* Stable partition of d_ids by d_owner[id] (bucket-major, input order inside
+ * a bucket); d_perm[k] = input index of d_out[k]; counts[parts] on host. */
+int cb_bucket_by_owner(cb_plan* plan, const uint32_t* d_ids, uint64_t n, const uint32_t* d_owner,
+                       uint32_t parts, uint32_t* d_out, uint32_t* d_perm, uint64_t* counts);
+/* Owner side: sorted unique of the received ids -> d_next (next layer's
+ * seeds), and d_rank[i] = row of d_recv[i] in d_next. */
+int cb_merge_owned(cb_plan* plan, int layer, const uint32_t* d_recv, uint64_t n_recv,
+                   uint32_t* d_next, uint64_t cap_next, uint64_t* n_next, uint32_t* d_rank);
+/* d_out[d_perm[k]] = d_in[k] (u32 values / feature rows of row_bytes). */
+int cb_scatter_u32(cb_plan* plan, const uint32_t* d_in, const uint32_t* d_perm, uint64_t n,
+                   uint32_t* d_out);
+int cb_scatter_rows(cb_plan* plan, const void* d_in, const uint32_t* d_perm, uint64_t n,
+                    uint64_t row_bytes, void* d_out);
+/* The feature rows of one part only (its members in ascending id order). */
+int cb_features_synth_shard(const cb_graph* g, const cb_partition* pm, uint32_t part,
+                            uint32_t dim, int dtype, uint64_t seed, cb_features** out);
+/* d_out[i] = row of vertex d_ids[i] (owned by the table's part). */
+int cb_gather_rows(const cb_features* f, const uint32_t* d_ids, uint64_t n, void* d_out,
+                   void* stream);
+
+/* Synchronous copy between any host/device pointers (cudaMemcpyDefault). */
+int cb_memcpy(void* dst, const void* src, uint64_t bytes, int device);
+
 /* One eager batch (+ gather when f != NULL) with a CUDA event after every
  * launch: ms[i] = device time of launch i, in enqueue order. */
 int cb_plan_profile(cb_plan* plan, int mode, const uint32_t* seeds_flat,

@@ -57,6 +57,17 @@ _SIGS = {
     "cb_rows_device": (C.c_int, [_P, _u32, _PP, C.POINTER(_u64)]),
     "cb_plan_capture": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched)]),
     "cb_plan_replay": (C.c_int, [_P, _P, C.c_int, C.POINTER(Sched), C.c_int]),
+    "cb_plan_create_dist": (C.c_int, [_P, _u32, C.c_int, C.c_int, _P, _u64, _PP]),
+    "cb_plan_sample_layer": (C.c_int, [_P, C.c_int, _P, _u64, C.POINTER(Sched),
+                                       C.POINTER(_u64)]),
+    "cb_plan_layer_src": (C.c_int, [_P, C.c_int, _PP]),
+    "cb_bucket_by_owner": (C.c_int, [_P, _P, _u64, _P, _u32, _P, _P, _P]),
+    "cb_merge_owned": (C.c_int, [_P, C.c_int, _P, _u64, _P, _u64, C.POINTER(_u64), _P]),
+    "cb_scatter_u32": (C.c_int, [_P, _P, _P, _u64, _P]),
+    "cb_scatter_rows": (C.c_int, [_P, _P, _P, _u64, _u64, _P]),
+    "cb_features_synth_shard": (C.c_int, [_P, _P, _u32, _u32, C.c_int, _u64, _PP]),
+    "cb_gather_rows": (C.c_int, [_P, _P, _u64, _P, _P]),
+    "cb_memcpy": (C.c_int, [_P, _P, _u64, C.c_int]),
     "cb_plan_profile": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched), _P, _P, C.c_int,
                                   C.POINTER(C.c_int)]),
     "cb_plan_launch_count": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_u64)]),

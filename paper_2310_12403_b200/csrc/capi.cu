@@ -19,6 +19,7 @@
 #include "cb_internal.h"
 #include "exchange.h"
 #include "gather.h"
+#include "dist.h"
 
 using namespace cb;
 using cbdev::Variates;
@@ -106,6 +107,7 @@ struct cb_features {
   Arena mem;
   void* table = nullptr;
   uint32_t* row_map = nullptr;  // nullptr = identity (P = 1)
+  uint64_t shard_rows = 0;      // rows actually held (sharded tables)
 };
 
 namespace {
@@ -145,6 +147,8 @@ struct cb_plan {
   uint64_t seeds_cap = 0;
   int mode = -1;          // mode of the last batch
   int dirty_mode = -1;    // mode whose final bitmap still holds bits (-1: clean)
+  uint32_t dist_world = 0;  // >0: one part of a multi-process cooperative step
+  unsigned long long* scratch = nullptr;  // small device counters (dist ops)
   bool smooth = false;    // kernels of the last enqueue used smoothed variates
   std::vector<cudaEvent_t>* prof = nullptr;  // per-launch events (cb_plan_profile)
   bool cap_smooth = false;
@@ -169,6 +173,7 @@ struct cb_plan {
 
   LayerMeta* meta_at(uint32_t p, int l) { return meta + p * (L + 1) + l; }
   bool coop_active() const { return mode == CB_MODE_COOP && P > 1; }
+  bool own_dst() const { return coop_active() || dist_world > 0; }
 };
 
 namespace {
@@ -227,7 +232,8 @@ void plan_alloc(cb_plan* pl) {
         w.loc_row.push_back(pl->mem.alloc<uint32_t>(b.cap_src));
       }
       // next layer's frontier: indep -> this src; coop -> owner set
-      const uint64_t next = (P > 1) ? std::min(n, sat_mul(P, b.cap_src)) : b.cap_src;
+      const uint64_t mult = std::max<uint64_t>(P, pl->dist_world);
+      const uint64_t next = (mult > 1) ? std::min(n, sat_mul(mult, b.cap_src)) : b.cap_src;
       cd = std::max(next, b.cap_src);
     }
     w.cap_final = cd;
@@ -260,6 +266,7 @@ void plan_alloc(cb_plan* pl) {
   pl->var = pl->mem.alloc<Variates>(1);
   pl->seeds_cap = static_cast<uint64_t>(P) * std::max<uint64_t>(pl->max_seeds, 1);
   pl->seeds = pl->mem.alloc<uint32_t>(pl->seeds_cap);
+  pl->scratch = pl->mem.alloc<unsigned long long>(8);
   pl->have_batch = false;
   pl->dirty_mode = -1;
   CB_CUDA(cudaDeviceSynchronize());
@@ -1100,7 +1107,7 @@ int cb_download_block(cb_plan* plan, uint32_t part, int layer, uint32_t* dst, ui
     PeWork& w = plan->pe[part];
     const uint32_t* d_dst;
     if (layer == 0) d_dst = plan->seeds + plan->seeds_off[part];
-    else if (!plan->coop_active()) d_dst = w.L[layer - 1].src;
+    else if (!plan->own_dst()) d_dst = w.L[layer - 1].src;
     else d_dst = w.L[layer].dst;
     const LayerBufs& b = w.L[layer];
     if (dst && m.n_dst) CB_CUDA(cudaMemcpy(dst, d_dst, m.n_dst * 4, cudaMemcpyDeviceToHost));
@@ -1237,6 +1244,185 @@ int cb_plan_profile(cb_plan* plan, int mode, const uint32_t* seeds_flat,
       CB_CUDA(cudaEventElapsedTime(&ms[k], ev[i - 1], ev[i]));
     *n = k;
     for (auto e : ev) cudaEventDestroy(e);
+  });
+}
+
+int cb_plan_create_dist(const cb_graph* g, uint32_t world, int num_layers, int kind,
+                        const uint32_t* fanouts, uint64_t max_seeds, cb_plan** out) {
+  return guard([&] {
+    require(g != nullptr && out != nullptr, "null argument");
+    require(world >= 1 && world <= kDistMaxParts, "world size must be in [1, 64]");
+    require(num_layers >= 1, "coop_sample: num_layers must be >= 1");
+    require(num_layers <= 8, "at most 8 layers");
+    require(kind == CB_FULL || kind == CB_NS || kind == CB_LABOR0,
+            "sample_block: unknown sampler kind");
+    DeviceGuard dg(g->g.device);
+    auto pl = std::make_unique<cb_plan>();
+    pl->device = g->g.device;
+    pl->g = g;
+    pl->P = 1;
+    pl->dist_world = world;
+    pl->L = num_layers;
+    pl->kind = kind;
+    for (int l = 0; l < num_layers; ++l) {
+      const uint32_t k = fanouts ? fanouts[l] : 1;
+      if (kind != CB_FULL) require(k >= 1, "fanout must be >= 1");
+      pl->fanouts.push_back(k);
+    }
+    pl->max_seeds = std::max<uint64_t>(max_seeds, 1);
+    CB_CUDA(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
+    plan_alloc(pl.get());
+    pl->mode = CB_MODE_COOP;
+    *out = pl.release();
+  });
+}
+
+int cb_plan_sample_layer(cb_plan* plan, int layer, const uint32_t* d_dst, uint64_t n_dst,
+                         const cb_sched* sched, uint64_t* n_src) {
+  return guard([&] {
+    require(plan != nullptr && sched != nullptr && n_src != nullptr, "null argument");
+    require(plan->P == 1, "per-layer sampling needs a single-part plan");
+    require(layer >= 0 && layer < plan->L, "layer index out of range");
+    require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
+    DeviceGuard dg(plan->device);
+    PeWork& w = plan->pe[0];
+    LayerBufs& b = w.L[layer];
+    uint32_t* D = (layer == 0) ? plan->seeds : b.dst;
+    const uint64_t cap = (layer == 0) ? plan->max_seeds : b.cap_dst;
+    if (n_dst > cap)
+      throw Error(kOverflow, "frontier of layer " + std::to_string(layer) +
+                                 " exceeds the plan capacity (" + std::to_string(cap) + ")");
+    cudaStream_t st = plan->stream;
+    if (n_dst)
+      CB_CUDA(cudaMemcpyAsync(D, d_dst, n_dst * 4, cudaMemcpyDeviceToDevice, st));
+    if (layer == 0) {
+      const Variates v = make_variates(sched);
+      CB_CUDA(cudaMemcpyAsync(plan->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+      plan->seeds_off.assign({0, n_dst});
+      plan->mode = CB_MODE_COOP;
+    }
+    const bool smooth = sched->kappa != cbdev::kKappaInf && sched->kappa >= 2;
+    launch_batch_begin(w.sync, nullptr, nullptr, nullptr, 0, 0, st);
+    const RelabelArgs none{};
+    enqueue_layer(plan, w, 0, layer, D, cap, n_dst, w.bm[0], none, 0, smooth,
+                  extract_args(w, w.bm[0], nullptr, b.src, b.cap_src,
+                               &plan->meta_at(0, layer)->n_src, nullptr, 3 * layer + 2,
+                               8 * layer + 4));
+    launch_relabel(relabel_args(w.bm[0], b, D, plan->meta_at(0, layer)),
+                   std::max(b.cap_edges, b.cap_dst), st);
+    launch_clear(w.bm[0], b.src, &plan->meta_at(0, layer)->n_src, st);
+    check_overflow(plan);
+    *n_src = host_meta(plan, 0, layer).n_src;
+    plan->have_batch = true;
+    plan->dirty_mode = -1;
+  });
+}
+
+int cb_plan_layer_src(cb_plan* plan, int layer, uint32_t** d_src) {
+  return guard([&] {
+    require(plan != nullptr && d_src != nullptr, "null argument");
+    require(layer >= 0 && layer < plan->L, "layer index out of range");
+    *d_src = plan->pe[0].L[layer].src;
+  });
+}
+
+int cb_bucket_by_owner(cb_plan* plan, const uint32_t* d_ids, uint64_t n, const uint32_t* d_owner,
+                       uint32_t parts, uint32_t* d_out, uint32_t* d_perm, uint64_t* counts) {
+  return guard([&] {
+    require(plan != nullptr && counts != nullptr, "null argument");
+    DeviceGuard dg(plan->device);
+    bucket_by_owner(d_ids, n, d_owner, parts, d_out, d_perm, counts, plan->stream);
+  });
+}
+
+int cb_merge_owned(cb_plan* plan, int layer, const uint32_t* d_recv, uint64_t n_recv,
+                   uint32_t* d_next, uint64_t cap_next, uint64_t* n_next, uint32_t* d_rank) {
+  return guard([&] {
+    require(plan != nullptr && n_next != nullptr, "null argument");
+    require(layer >= 0 && layer < plan->L, "layer index out of range");
+    DeviceGuard dg(plan->device);
+    PeWork& w = plan->pe[0];
+    cudaStream_t st = plan->stream;
+    unsigned long long* cnt = plan->scratch;
+    launch_batch_begin(w.sync, nullptr, nullptr, nullptr, 0, 0, st);
+    mark_ids(d_recv, n_recv, w.bm[1].bits, st);
+    launch_extract(extract_args(w, w.bm[1], nullptr, d_next, cap_next, cnt, nullptr,
+                                3 * plan->L + layer, 8 * layer + 5),
+                   st);
+    CB_CUDA(cudaMemcpyAsync(cnt + 1, &n_recv, 8, cudaMemcpyHostToDevice, st));
+    launch_rank(w.bm[1], d_recv, cnt + 1, d_rank, st);
+    launch_clear(w.bm[1], d_next, cnt, st);
+    check_overflow(plan);
+    unsigned long long h = 0;
+    CB_CUDA(cudaMemcpy(&h, cnt, 8, cudaMemcpyDeviceToHost));
+    *n_next = h;
+  });
+}
+
+int cb_scatter_u32(cb_plan* plan, const uint32_t* d_in, const uint32_t* d_perm, uint64_t n,
+                   uint32_t* d_out) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    DeviceGuard dg(plan->device);
+    scatter_u32(d_in, d_perm, n, d_out, plan->stream);
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int cb_scatter_rows(cb_plan* plan, const void* d_in, const uint32_t* d_perm, uint64_t n,
+                    uint64_t row_bytes, void* d_out) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    DeviceGuard dg(plan->device);
+    scatter_rows(d_in, d_perm, n, row_bytes, d_out, plan->stream);
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+int cb_features_synth_shard(const cb_graph* g, const cb_partition* pm, uint32_t part,
+                            uint32_t dim, int dtype, uint64_t seed, cb_features** out) {
+  return guard([&] {
+    require(g != nullptr && pm != nullptr && out != nullptr, "null argument");
+    require(part < pm->parts, "part index out of range");
+    require(dim >= 1, "feature dim must be >= 1");
+    require(dtype == CB_F64 || dtype == CB_F32 || dtype == CB_F16, "unknown dtype");
+    DeviceGuard dg(g->g.device);
+    auto f = std::make_unique<cb_features>();
+    f->device = g->g.device;
+    f->dim = dim;
+    f->dtype = dtype;
+    const uint64_t es = dtype == CB_F64 ? 8 : (dtype == CB_F32 ? 4 : 2);
+    f->row_bytes = es * dim;
+    const uint64_t r0 = pm->shard_off[part], r1 = pm->shard_off[part + 1];
+    f->n_rows = g->g.n;  // addressable by global row id of owned vertices
+    f->shard_rows = r1 - r0;
+    unsigned char* shard = f->mem.alloc<unsigned char>((r1 - r0) * f->row_bytes);
+    f->table = shard - r0 * f->row_bytes;  // virtual base: row_map[v] indexes it
+    f->row_map = f->mem.alloc<uint32_t>(g->g.n);
+    CB_CUDA(cudaMemcpy(f->row_map, pm->row_map, g->g.n * 4, cudaMemcpyDeviceToDevice));
+    launch_synth(seed, dim, dtype, r1 - r0, pm->members + r0, 0, shard, nullptr);
+    CB_CUDA(cudaDeviceSynchronize());
+    *out = f.release();
+  });
+}
+
+int cb_gather_rows(const cb_features* f, const uint32_t* d_ids, uint64_t n, void* d_out,
+                   void* stream) {
+  return guard([&] {
+    require(f != nullptr, "null features");
+    DeviceGuard dg(f->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    launch_gather(f->table, vec_bytes_for(f->row_bytes), f->row_bytes, d_ids, nullptr, n,
+                  f->row_map, d_out, st);
+    CB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int cb_memcpy(void* dst, const void* src, uint64_t bytes, int device) {
+  return guard([&] {
+    if (!bytes) return;
+    DeviceGuard dg(device);
+    CB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
   });
 }
 

@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(256) gather_kernel(
     const V* __restrict__ table, const uint32_t* __restrict__ ids,
     const unsigned long long* __restrict__ count, uint64_t cap_rows,
     const uint32_t* __restrict__ row_map, uint32_t vpr, V* __restrict__ out) {
-  const uint64_t n = min(static_cast<uint64_t>(*count), cap_rows);
+  // count == nullptr: cap_rows is the row count itself
+  const uint64_t n = count ? min(static_cast<uint64_t>(*count), cap_rows) : cap_rows;
   const uint64_t total = n * vpr;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;

@@ -1,0 +1,230 @@
+"""Multi-process cooperative minibatching: one process per GPU, one part per
+rank (Alg. 1; coop.cpp:68-106 with the in-memory exchange of
+build_exchange, coop.cpp:25-64, replaced by all-to-allv between ranks).
+
+Per layer l on rank p:
+  1. engine.sample_layer(l, D_p)   -> sorted unique src list S~_p (device)
+  2. engine.bucket(S~_p)           -> ids bucketed by owner, perm, counts
+  3. all_to_all(counts); all_to_all(ids)        [torch.distributed: NCCL]
+  4. engine.merge(l, received)     -> D_p^{l+1} (sorted unique) + row of
+                                      every received id in it
+  5. all_to_all(rows back)         -> src_location[p][j] = (owner, row)
+Feature loading (coop.cpp:457-467): the owner gathers the rows requested by
+the last layer's ids from its shard and returns them in request order; the
+requester scatters them to src order (all_to_all_forward).
+
+The engine does the per-part compute. ``CudaEngine`` runs the sm_100a
+kernels through the C-ABI; the CPU tests run the same orchestration with an
+oracle-backed engine over the gloo backend.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .coopbatch import (FeatureStore, Graph, PartitionMap, SamplerConfig, SeedSchedule,
+                        _check, _DT)
+
+
+@dataclass
+class DistExchange:
+    """This rank's row of an ExchangeRecord (coop.hpp:25-37)."""
+    layer: int
+    send_counts: list[int]         # send_counts[p][*] for this rank p
+    owner_row_count: int           # owner_row_counts[p]
+    loc_part: np.ndarray           # src_location[p][*].part
+    loc_row: np.ndarray            # src_location[p][*].row
+
+
+@dataclass
+class DistSample:
+    blocks: list[dict] = field(default_factory=list)
+    exchanges: list[DistExchange] = field(default_factory=list)
+    owner_set: np.ndarray | None = None
+
+
+def _i32(t: torch.Tensor) -> torch.Tensor:
+    return t.view(torch.int32) if t.dtype != torch.int32 else t
+
+
+class DistCoop:
+    def __init__(self, engine, group=None):
+        self.e = engine
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self._last = None
+
+    def _a2a(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits):
+        dist.all_to_all_single(out, inp, output_split_sizes=list(out_splits),
+                               input_split_sizes=list(in_splits), group=self.group)
+
+    def _exchange_counts(self, counts) -> list[int]:
+        send = torch.tensor(counts, dtype=torch.int64, device=self.e.comm_device)
+        recv = torch.empty(self.world, dtype=torch.int64, device=self.e.comm_device)
+        dist.all_to_all_single(recv, send, group=self.group)
+        return recv.tolist()
+
+    def sample(self, seeds: np.ndarray, num_layers: int, schedule: SeedSchedule,
+               keep_blocks: bool = True) -> DistSample:
+        out = DistSample()
+        D = self.e.to_device(np.ascontiguousarray(seeds, dtype=np.uint32))
+        n_d = len(seeds)
+        for l in range(num_layers):
+            src, n_src = self.e.sample_layer(l, D, n_d, schedule)
+            bucketed, perm, counts = self.e.bucket(src, n_src)
+            rcounts = self._exchange_counts(counts)
+            recv = self.e.empty_ids(sum(rcounts))
+            self._a2a(_i32(recv), _i32(bucketed), rcounts, counts)
+            D, n_d, ranks = self.e.merge(l, recv, sum(rcounts))
+            back = self.e.empty_ids(sum(counts))
+            self._a2a(_i32(back), _i32(ranks), counts, rcounts)
+            loc_row = self.e.scatter(back, perm, n_src)
+            part = np.repeat(np.arange(self.world, dtype=np.uint32), counts)
+            loc_part = np.zeros(n_src, np.uint32)
+            loc_part[self.e.to_host(perm, n_src)] = part
+            out.exchanges.append(DistExchange(l, counts, n_d, loc_part,
+                                              self.e.to_host(loc_row, n_src).astype(np.uint64)))
+            if keep_blocks:
+                out.blocks.append(self.e.block(l))
+            self._last = (recv, sum(rcounts), rcounts, perm, counts, n_src)
+        out.owner_set = self.e.to_host(D, n_d)
+        return out
+
+    def load_inputs(self) -> np.ndarray:
+        """Rows of this rank's input vertices (src of the last block), in src
+        order: owner-side gather of the requested ids, all-to-allv back,
+        requester-side scatter (all_to_all_forward, coop.cpp:145-159)."""
+        recv, n_recv, rcounts, perm, counts, n_src = self._last
+        rb = self.e.row_bytes
+        rows = self.e.gather_rows(recv, n_recv)              # owner side, request order
+        back = torch.empty(sum(counts) * rb, dtype=torch.uint8, device=self.e.comm_device)
+        self._a2a(back, rows, [c * rb for c in counts], [c * rb for c in rcounts])
+        return self.e.scatter_rows(back, perm, n_src)
+
+
+class CudaEngine:
+    """Per-part compute through libcoopbatch_b200 (sm_100a kernels)."""
+
+    def __init__(self, g: Graph, pm: PartitionMap, rank: int, num_layers: int,
+                 cfg: SamplerConfig, max_seeds: int, store: FeatureStore | None = None,
+                 comm_device: str | None = None):
+        self.L = _lib.load()
+        self.g, self.rank, self.world = g, rank, pm.num_parts
+        self.device = torch.device(f"cuda:{g.device}")
+        # ids/rows cross ranks on this device (NCCL); "cpu" stages them for gloo
+        self.comm_device = torch.device(comm_device) if comm_device else self.device
+        fo = np.asarray(cfg.layer_fanouts(num_layers), dtype=np.uint32)
+        h = C.c_void_p()
+        _check(self.L.cb_plan_create_dist(g._h, pm.num_parts, num_layers, int(cfg.kind),
+                                          fo.ctypes.data_as(C.c_void_p), max_seeds,
+                                          C.byref(h)))
+        self._h = h
+        self.owner = torch.from_numpy(pm.owner.view(np.int32)).to(self.device)
+        self.store = store
+        self.row_bytes = store.row_bytes if store is not None else 0
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self.L.cb_plan_destroy(self._h)
+            self._h = None
+
+    # -- helpers --------------------------------------------------------------
+    def _dev(self, t: torch.Tensor) -> torch.Tensor:
+        return t if t.device == self.device else t.to(self.device)
+
+    def _comm(self, t: torch.Tensor) -> torch.Tensor:
+        return t if t.device == self.comm_device else t.to(self.comm_device)
+
+    def to_device(self, a: np.ndarray) -> torch.Tensor:
+        return torch.from_numpy(a.view(np.int32)).to(self.device)
+
+    def to_host(self, t: torch.Tensor, n: int) -> np.ndarray:
+        return t[:n].cpu().numpy().view(np.uint32).copy()
+
+    def empty_ids(self, n: int) -> torch.Tensor:
+        return torch.empty(max(n, 1), dtype=torch.int32, device=self.comm_device)[:n]
+
+    # -- engine interface -----------------------------------------------------
+    def sample_layer(self, l, D, n_d, schedule: SeedSchedule):
+        D = self._dev(D)
+        n_src = C.c_uint64()
+        s = schedule._c()
+        _check(self.L.cb_plan_sample_layer(self._h, l, C.c_void_p(D.data_ptr()), n_d,
+                                           C.byref(s), C.byref(n_src)))
+        ptr = C.c_void_p()
+        _check(self.L.cb_plan_layer_src(self._h, l, C.byref(ptr)))
+        src = torch.empty(max(n_src.value, 1), dtype=torch.int32, device=self.device)
+        _check(self.L.cb_memcpy(C.c_void_p(src.data_ptr()), ptr, n_src.value * 4,
+                                self.g.device))
+        return src[: n_src.value], n_src.value
+
+    def bucket(self, src, n):
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        perm = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        counts = np.zeros(self.world, np.uint64)
+        _check(self.L.cb_bucket_by_owner(self._h, C.c_void_p(src.data_ptr()), n,
+                                         C.c_void_p(self.owner.data_ptr()), self.world,
+                                         C.c_void_p(out.data_ptr()),
+                                         C.c_void_p(perm.data_ptr()),
+                                         counts.ctypes.data_as(C.c_void_p)))
+        return self._comm(out[:n]), perm[:n], [int(c) for c in counts]
+
+    def merge(self, l, recv, n_recv):
+        recv = self._dev(recv)
+        nxt = torch.empty(max(n_recv, 1), dtype=torch.int32, device=self.device)
+        rank = torch.empty(max(n_recv, 1), dtype=torch.int32, device=self.device)
+        n_next = C.c_uint64()
+        _check(self.L.cb_merge_owned(self._h, l, C.c_void_p(recv.data_ptr()), n_recv,
+                                     C.c_void_p(nxt.data_ptr()), max(n_recv, 1),
+                                     C.byref(n_next), C.c_void_p(rank.data_ptr())))
+        return nxt[: n_next.value], n_next.value, self._comm(rank[:n_recv])
+
+    def scatter(self, vals, perm, n):
+        vals = self._dev(vals)
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        _check(self.L.cb_scatter_u32(self._h, C.c_void_p(vals.data_ptr()),
+                                     C.c_void_p(perm.data_ptr()), n,
+                                     C.c_void_p(out.data_ptr())))
+        return out[:n]
+
+    def block(self, l) -> dict:
+        sz = np.zeros(6, np.uint64)
+        _check(self.L.cb_layer_sizes(self._h, 0, l, sz.ctypes.data_as(C.c_void_p)))
+        nd, ns, ne = int(sz[0]), int(sz[1]), int(sz[2])
+        dst, src = np.zeros(nd, np.uint32), np.zeros(ns, np.uint32)
+        edges, dpos = np.zeros((ne, 2), np.uint32), np.zeros(nd, np.uint32)
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        _check(self.L.cb_download_block(self._h, 0, l, p(dst), p(src), p(edges), p(dpos)))
+        return {"layer": l, "dst": dst, "src": src, "edges": edges, "dst_pos": dpos}
+
+    def gather_rows(self, ids, n):
+        ids = self._dev(ids)
+        out = torch.empty(max(n, 1) * self.row_bytes, dtype=torch.uint8, device=self.device)
+        _check(self.L.cb_gather_rows(self.store._h, C.c_void_p(ids.data_ptr()), n,
+                                     C.c_void_p(out.data_ptr()), None))
+        return self._comm(out[: n * self.row_bytes])
+
+    def scatter_rows(self, rows, perm, n) -> np.ndarray:
+        rows = self._dev(rows)
+        out = torch.empty(max(n, 1) * self.row_bytes, dtype=torch.uint8, device=self.device)
+        _check(self.L.cb_scatter_rows(self._h, C.c_void_p(rows.data_ptr()),
+                                      C.c_void_p(perm.data_ptr()), n, self.row_bytes,
+                                      C.c_void_p(out.data_ptr())))
+        dt = _DT[self.store.dtype][1]
+        return out[: n * self.row_bytes].cpu().numpy().view(dt).reshape(n, self.store.dim)
+
+
+def synth_shard(g: Graph, pm: PartitionMap, part: int, dim: int, seed: int,
+                dtype: str = "f32") -> FeatureStore:
+    """Feature rows of one part only (FeatureStore::synth restricted to the
+    part's members, coop.cpp:359-376)."""
+    h = C.c_void_p()
+    _check(_lib.load().cb_features_synth_shard(g._h, pm._h, part, dim, _DT[dtype][0], seed,
+                                               C.byref(h)))
+    return FeatureStore(g, h, dim, dtype, pm)
