@@ -136,7 +136,11 @@ class CudaEngine:
 
     # -- helpers --------------------------------------------------------------
     def _dev(self, t: torch.Tensor) -> torch.Tensor:
-        return t if t.device == self.device else t.to(self.device)
+        """Device copy of a torch tensor, complete before the library's own
+        (non-blocking) plan stream reads it."""
+        t = t if t.device == self.device else t.to(self.device)
+        torch.cuda.current_stream(self.device).synchronize()
+        return t
 
     def _comm(self, t: torch.Tensor) -> torch.Tensor:
         return t if t.device == self.comm_device else t.to(self.comm_device)
@@ -152,7 +156,7 @@ class CudaEngine:
 
     # -- engine interface -----------------------------------------------------
     def sample_layer(self, l, D, n_d, schedule: SeedSchedule):
-        D = self._dev(D)
+        D = self._dev(D)  # also orders torch-side writes before the plan stream
         n_src = C.c_uint64()
         s = schedule._c()
         _check(self.L.cb_plan_sample_layer(self._h, l, C.c_void_p(D.data_ptr()), n_d,
@@ -165,6 +169,7 @@ class CudaEngine:
         return src[: n_src.value], n_src.value
 
     def bucket(self, src, n):
+        torch.cuda.current_stream(self.device).synchronize()
         out = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         perm = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
         counts = np.zeros(self.world, np.uint64)
