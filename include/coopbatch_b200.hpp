@@ -1,0 +1,264 @@
+// coopbatch_b200.hpp — header-only C++17 drop-in for the reference's sampler /
+// minibatch API (/root/reference/proj/include/coopbatch/{graph,rng,samplers,
+// partition,coop}.hpp) over the C-ABI of libcoopbatch_b200.so.
+//
+// Same names, argument meaning, value-type results and exception behaviour
+// (InputError for contract violations, common.hpp:12-15); the work runs in
+// the sm_100a kernels. Link with -lcoopbatch_b200 (paper_2310_12403_b200/).
+#pragma once
+
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "coopbatch_cuda.h"
+
+namespace coopbatch_b200 {
+
+using VertexId = std::uint32_t;
+
+struct InputError : std::invalid_argument {  // common.hpp:12-15
+  using std::invalid_argument::invalid_argument;
+};
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == CB_OK) return;
+  const std::string msg = cb_last_error();
+  if (rc == CB_INPUT) throw InputError(msg);
+  throw DeviceError(msg);
+}
+
+enum class SamplerKind { kFull = CB_FULL, kNs = CB_NS, kLabor0 = CB_LABOR0 };
+
+struct SamplerConfig {  // samplers.hpp:17-23 (+ per-layer fanouts extension)
+  SamplerKind kind = SamplerKind::kNs;
+  std::uint32_t fanout = 10;
+  std::vector<std::uint32_t> fanouts;  // empty -> fanout at every layer
+
+  std::vector<std::uint32_t> per_layer(int L) const {
+    if (!fanouts.empty()) {
+      if (static_cast<int>(fanouts.size()) != L)
+        throw InputError("fanouts must list one fanout per layer");
+      return fanouts;
+    }
+    return std::vector<std::uint32_t>(L, fanout);
+  }
+};
+
+inline constexpr std::uint64_t kKappaInfinity = std::numeric_limits<std::uint64_t>::max();
+
+struct SeedSchedule {  // rng.hpp:93-111 (value type; make/advance as rng.cpp:69-86)
+  std::uint64_t kappa = 1, z1 = 0, z2 = 0, iteration = 0;
+  cb_sched c() const { return {kappa, z1, z2, iteration}; }
+};
+
+struct BipartiteBlock {  // samplers.hpp:30-38
+  std::vector<VertexId> dst_vertices;
+  std::vector<VertexId> src_vertices;
+  std::vector<std::pair<std::uint32_t, std::uint32_t>> edges;
+  std::vector<std::uint32_t> dst_pos_in_src;
+  int layer = 0;
+  std::uint64_t num_edges() const { return edges.size(); }
+};
+
+struct LayerStack {  // samplers.hpp:42-49
+  std::vector<BipartiteBlock> blocks;
+  const std::vector<VertexId>& input_vertices() const { return blocks.back().src_vertices; }
+};
+
+struct RemoteRef {  // coop.hpp:14-17
+  std::uint32_t part = 0;
+  std::uint64_t row = 0;
+};
+
+struct ExchangeRecord {  // coop.hpp:25-37
+  int layer = 0;
+  std::vector<std::vector<std::uint64_t>> send_counts;
+  std::vector<std::vector<RemoteRef>> src_location;
+  std::vector<std::uint64_t> owner_row_counts;
+  std::uint32_t num_parts() const { return static_cast<std::uint32_t>(send_counts.size()); }
+  std::uint64_t communicated(std::uint32_t p) const {
+    std::uint64_t t = 0;
+    for (std::uint32_t q = 0; q < num_parts(); ++q)
+      if (q != p) t += send_counts[p][q];
+    return t;
+  }
+};
+
+struct CoopSampleResult {  // coop.hpp:39-43
+  std::vector<LayerStack> stacks;
+  std::vector<ExchangeRecord> exchanges;
+  std::vector<std::vector<VertexId>> owner_sets;
+};
+
+// ---- device handles ---------------------------------------------------------
+class Graph {  // graph.hpp:21-53, resident in HBM
+ public:
+  static Graph from_csr(const std::vector<std::uint64_t>& indptr,
+                        const std::vector<VertexId>& indices, int device = 0) {
+    cb_graph* g = nullptr;
+    check(cb_graph_create_from_csr(indptr.data(), indices.data(), indptr.size() - 1,
+                                   indices.size(), device, &g));
+    return Graph(g);
+  }
+  static Graph generate_rmat(std::uint64_t n, std::uint64_t m, std::uint64_t seed,
+                             int device = 0) {
+    cb_graph* g = nullptr;
+    check(cb_graph_generate_rmat(n, m, seed, device, &g));
+    return Graph(g);
+  }
+  std::uint64_t num_vertices() const {
+    std::uint64_t n = 0;
+    check(cb_graph_info(h_.get(), &n, nullptr, nullptr));
+    return n;
+  }
+  cb_graph* get() const { return h_.get(); }
+
+ private:
+  explicit Graph(cb_graph* g) : h_(g, cb_graph_destroy) {}
+  std::shared_ptr<cb_graph> h_;
+};
+
+class PartitionMap {  // partition.hpp:12-17
+ public:
+  static PartitionMap random(const Graph& g, std::uint32_t parts, std::uint64_t seed) {
+    cb_partition* p = nullptr;
+    check(cb_partition_random(g.get(), parts, seed, &p));
+    return PartitionMap(p, parts);
+  }
+  static PartitionMap from_owner(const Graph& g, const std::vector<std::uint32_t>& owner,
+                                 std::uint32_t parts) {
+    if (owner.size() != g.num_vertices())
+      throw InputError("partition: owner array does not cover all vertices");
+    cb_partition* p = nullptr;
+    check(cb_partition_create(g.get(), owner.data(), parts, &p));
+    return PartitionMap(p, parts);
+  }
+  std::uint32_t num_parts() const { return parts_; }
+  cb_partition* get() const { return h_.get(); }
+
+ private:
+  PartitionMap(cb_partition* p, std::uint32_t parts) : h_(p, cb_partition_destroy), parts_(parts) {}
+  std::shared_ptr<cb_partition> h_;
+  std::uint32_t parts_;
+};
+
+namespace detail {
+
+inline BipartiteBlock download_block(cb_plan* pl, std::uint32_t p, int l) {
+  std::uint64_t sz[6];
+  check(cb_layer_sizes(pl, p, l, sz));
+  BipartiteBlock b;
+  b.layer = l;
+  b.dst_vertices.resize(sz[0]);
+  b.src_vertices.resize(sz[1]);
+  std::vector<std::uint32_t> e(2 * sz[2]);
+  b.dst_pos_in_src.resize(sz[0]);
+  check(cb_download_block(pl, p, l, b.dst_vertices.data(), b.src_vertices.data(), e.data(),
+                          b.dst_pos_in_src.data()));
+  b.edges.resize(sz[2]);
+  for (std::uint64_t i = 0; i < sz[2]; ++i) b.edges[i] = {e[2 * i], e[2 * i + 1]};
+  return b;
+}
+
+struct PlanDeleter {
+  void operator()(cb_plan* p) const { cb_plan_destroy(p); }
+};
+using PlanPtr = std::unique_ptr<cb_plan, PlanDeleter>;
+
+inline PlanPtr make_plan(const Graph& g, const PartitionMap* pm, int L, const SamplerConfig& cfg,
+                         std::uint64_t max_seeds) {
+  if (L < 1) throw InputError("expand: num_layers must be >= 1");
+  const auto fo = cfg.per_layer(L);
+  cb_plan* pl = nullptr;
+  check(cb_plan_create(g.get(), pm ? pm->get() : nullptr, L, static_cast<int>(cfg.kind),
+                       fo.data(), max_seeds ? max_seeds : 1, &pl));
+  return PlanPtr(pl);
+}
+
+}  // namespace detail
+
+// samplers.cpp:340-354
+inline LayerStack expand(const Graph& g, const std::vector<VertexId>& seeds, int num_layers,
+                         const SamplerConfig& cfg, const SeedSchedule& schedule) {
+  auto pl = detail::make_plan(g, nullptr, num_layers, cfg, seeds.size());
+  const std::uint64_t off[2] = {0, seeds.size()};
+  const cb_sched s = schedule.c();
+  check(cb_sample_sync(pl.get(), CB_MODE_INDEP, seeds.data(), off, &s));
+  LayerStack st;
+  for (int l = 0; l < num_layers; ++l) st.blocks.push_back(detail::download_block(pl.get(), 0, l));
+  return st;
+}
+
+// coop.cpp:108-119
+inline std::vector<LayerStack> indep_sample(const Graph& g,
+                                            const std::vector<std::vector<VertexId>>& per_pe,
+                                            int num_layers, const SamplerConfig& cfg,
+                                            const SeedSchedule& schedule) {
+  std::vector<LayerStack> out;
+  for (const auto& s : per_pe) out.push_back(expand(g, s, num_layers, cfg, schedule));
+  return out;
+}
+
+// coop.cpp:68-106
+inline CoopSampleResult coop_sample(const Graph& g, const PartitionMap& pm,
+                                    const std::vector<std::vector<VertexId>>& per_pe,
+                                    int num_layers, const SamplerConfig& cfg,
+                                    const SeedSchedule& schedule) {
+  const std::uint32_t P = pm.num_parts();
+  if (per_pe.size() != P)
+    throw InputError("coop_sample: seed lists must match the partition count");
+  std::uint64_t maxb = 1;
+  std::vector<VertexId> flat;
+  std::vector<std::uint64_t> off{0};
+  for (const auto& s : per_pe) {
+    flat.insert(flat.end(), s.begin(), s.end());
+    off.push_back(flat.size());
+    maxb = std::max<std::uint64_t>(maxb, s.size());
+  }
+  auto pl = detail::make_plan(g, &pm, num_layers, cfg, maxb);
+  const cb_sched s = schedule.c();
+  check(cb_sample_sync(pl.get(), CB_MODE_COOP, flat.data(), off.data(), &s));
+  CoopSampleResult r;
+  r.stacks.resize(P);
+  for (std::uint32_t p = 0; p < P; ++p)
+    for (int l = 0; l < num_layers; ++l)
+      r.stacks[p].blocks.push_back(detail::download_block(pl.get(), p, l));
+  for (int l = 0; l < num_layers; ++l) {
+    ExchangeRecord e;
+    e.layer = l;
+    std::vector<std::uint64_t> sc(P * P), orc(P);
+    std::uint64_t tot = 0;
+    for (std::uint32_t p = 0; p < P; ++p) tot += r.stacks[p].blocks[l].src_vertices.size();
+    std::vector<std::uint32_t> lp(tot);
+    std::vector<std::uint64_t> lr(tot);
+    check(cb_download_exchange(pl.get(), l, sc.data(), orc.data(), lp.data(), lr.data()));
+    e.send_counts.assign(P, std::vector<std::uint64_t>(P));
+    for (std::uint32_t p = 0; p < P; ++p)
+      for (std::uint32_t q = 0; q < P; ++q) e.send_counts[p][q] = sc[p * P + q];
+    e.owner_row_counts = orc;
+    std::uint64_t o = 0;
+    e.src_location.resize(P);
+    for (std::uint32_t p = 0; p < P; ++p)
+      for (std::size_t j = 0; j < r.stacks[p].blocks[l].src_vertices.size(); ++j, ++o)
+        e.src_location[p].push_back({lp[o], lr[o]});
+    r.exchanges.push_back(std::move(e));
+  }
+  r.owner_sets.resize(P);
+  for (std::uint32_t p = 0; p < P; ++p) {
+    std::uint64_t n = 0;
+    check(cb_owner_set_size(pl.get(), p, &n));
+    r.owner_sets[p].resize(n);
+    if (n) check(cb_download_owner_set(pl.get(), p, r.owner_sets[p].data()));
+  }
+  return r;
+}
+
+}  // namespace coopbatch_b200
