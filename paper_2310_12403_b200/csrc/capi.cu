@@ -160,6 +160,7 @@ struct cb_plan {
   // CUDA graphs of one batch (sample) and its gather, replayed per step
   cudaGraphExec_t exec_sample = nullptr;
   cudaGraphExec_t exec_gather = nullptr;
+  cudaGraphExec_t exec_all = nullptr;  // sample + gather in one graph
   int cap_mode = -1;
   std::vector<uint64_t> cap_off;
   uint64_t cap_launches_sample = 0, cap_launches_gather = 0;
@@ -167,7 +168,8 @@ struct cb_plan {
   void drop_graphs() {
     if (exec_sample) cudaGraphExecDestroy(exec_sample);
     if (exec_gather) cudaGraphExecDestroy(exec_gather);
-    exec_sample = exec_gather = nullptr;
+    if (exec_all) cudaGraphExecDestroy(exec_all);
+    exec_sample = exec_gather = exec_all = nullptr;
   }
   ~cb_plan() { drop_graphs(); }
 
@@ -1012,6 +1014,12 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
       CB_CUDA(cudaGraphInstantiate(&plan->exec_gather, graph, 0));
       CB_CUDA(cudaGraphDestroy(graph));
       plan->cap_launches_gather = plan->launches;
+      CB_CUDA(cudaStreamBeginCapture(plan->stream, cudaStreamCaptureModeThreadLocal));
+      enqueue_batch(plan, mode, plan->seeds, seeds_off, &dummy, true);
+      enqueue_gather(plan, f);
+      CB_CUDA(cudaStreamEndCapture(plan->stream, &graph));
+      CB_CUDA(cudaGraphInstantiate(&plan->exec_all, graph, 0));
+      CB_CUDA(cudaGraphDestroy(graph));
     }
     plan->cap_mode = mode;
     plan->cap_smooth = plan->smooth;
@@ -1055,13 +1063,15 @@ int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_devic
                              plan->pe[p].bm[0].words_padded, st);
         }
       }
-      CB_CUDA(cudaGraphLaunch(plan->exec_sample, st));
+      const bool all = (what & 2) && plan->exec_all;
+      CB_CUDA(cudaGraphLaunch(all ? plan->exec_all : plan->exec_sample, st));
       plan->dirty_mode = plan->cap_mode;
       plan->mode = plan->cap_mode;
       plan->seeds_off = plan->cap_off;
       plan->have_batch = true;
-      plan->have_rows = false;
-      plan->launches = plan->cap_launches_sample;
+      plan->have_rows = all;
+      plan->launches = plan->cap_launches_sample + (all ? plan->cap_launches_gather : 0);
+      if (all) return;
     }
     if (what & 2) {
       require(plan->exec_gather != nullptr, "no captured gather");

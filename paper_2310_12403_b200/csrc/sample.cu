@@ -44,17 +44,9 @@ __device__ __forceinline__ uint32_t bm_rank(const uint32_t* bits, const uint32_t
 
 // Reset a ticket counter once every CTA of the launch is done with it, so no
 // per-batch memset of the tickets is needed.
-__device__ __forceinline__ void retire_ticket(unsigned* ticket, unsigned* exit_ctr,
-                                              unsigned ncta) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // every ticket atomic of this CTA has returned, i.e. is performed
-    if (atomicAdd(exit_ctr, 1u) == ncta - 1) {
-      atomicExch(ticket, 0u);
-      atomicExch(exit_ctr, 0u);
-    }
-  }
-}
+// Tickets are zeroed by batch_begin_kernel at the start of every batch /
+// per-layer op (stream order), so kernels need no exit bookkeeping.
+__device__ __forceinline__ void retire_ticket(unsigned*, unsigned*, unsigned) {}
 
 __device__ void relabel_range(const RelabelArgs& r, uint64_t tid, uint64_t stride) {
   const uint64_t ne = min(static_cast<uint64_t>(r.meta->n_edges), r.cap_edges);
@@ -70,13 +62,17 @@ __device__ void relabel_range(const RelabelArgs& r, uint64_t tid, uint64_t strid
 // ------------------------------------------------------------ batch begin --
 // Clears the previous batch's last bitmap (its final id list), bumps the
 // look-back epoch, resets the overflow flag. One launch per batch.
-__global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, uint32_t* clear_bits,
+__global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, unsigned* tickets,
+                                   int n_tickets, uint32_t* clear_bits,
                                    const uint32_t* __restrict__ clear_list,
                                    const unsigned long long* clear_count, uint64_t cap,
                                    uint64_t nwords) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *epoch = *epoch + 1;
-    *overflow = 0;
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      *epoch = *epoch + 1;
+      *overflow = 0;
+    }
+    for (int i = threadIdx.x; i < n_tickets; i += blockDim.x) tickets[i] = 0u;
   }
   if (!clear_bits) return;
   const uint64_t n = min(static_cast<uint64_t>(*clear_count), cap);
@@ -413,8 +409,8 @@ __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
   }
 }
 
-constexpr int kEmitWPT = 8;                    // keep words per thread
-constexpr int kEmitTileWords = kNT * kEmitWPT;  // 2048 words = 65536 positions
+constexpr int kEmitWPT = 1;                    // keep words per thread
+constexpr int kEmitTileWords = kNT * kEmitWPT;  // 256 words = 8192 positions
 
 // Ordered compaction of the keep words. The tile's kept items are spread
 // over all threads (item q -> its word by binary search over the per-word
@@ -692,8 +688,9 @@ void launch_batch_begin(const Sync& s, uint32_t* clear_bits, const uint32_t* cle
                         const unsigned long long* clear_count, uint64_t clear_cap,
                         uint64_t nwords, cudaStream_t st) {
   const int grid = grid_for(clear_cap, 256, 4);
-  batch_begin_kernel<<<grid, 256, 0, st>>>(s.epoch, s.overflow, clear_bits, clear_list,
-                                           clear_count, clear_cap, nwords);
+  batch_begin_kernel<<<grid, 256, 0, st>>>(s.epoch, s.overflow, s.tickets, Sync::kMaxTickets,
+                                           clear_bits, clear_list, clear_count, clear_cap,
+                                           nwords);
   CB_LAUNCH("batch_begin");
 }
 
