@@ -194,6 +194,11 @@ int cb_plan_profile(cb_plan* plan, int mode, const uint32_t* seeds_flat,
                     const uint64_t* seeds_off, const cb_sched* sched, const cb_features* f,
                     float* ms, int max_n, int* n);
 
+/* Replay the captured batch once through its profiling twin (event-record
+ * nodes between launches): ms[i] = in-graph device time of launch i. */
+int cb_plan_graph_profile(cb_plan* plan, const uint32_t* d_seeds, const cb_sched* sched,
+                          float* ms, int max_n, int* n);
+
 /* Number of kernels one cb_sample/cb_gather call enqueues (for reporting). */
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n);
 

@@ -381,6 +381,16 @@ class Plan:
                                            C.byref(n)))
         return ms[: n.value].tolist()
 
+    def graph_profile(self, seeds_ptr: int | None, schedule: SeedSchedule) -> list[float]:
+        """In-graph per-launch device times (ms) of one replay of the captured batch."""
+        ms = np.zeros(256, np.float32)
+        n = C.c_int()
+        s = schedule._c()
+        _check(_lib.load().cb_plan_graph_profile(self._h, C.c_void_p(seeds_ptr) if seeds_ptr
+                                                 else None, C.byref(s), _ptr(ms), 256,
+                                                 C.byref(n)))
+        return ms[: n.value].tolist()
+
     def launch_count(self, mode: int, with_gather: bool) -> int:
         n = C.c_uint64()
         _check(_lib.load().cb_plan_launch_count(self._h, mode, int(with_gather), C.byref(n)))

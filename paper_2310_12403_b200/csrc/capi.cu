@@ -151,6 +151,9 @@ struct cb_plan {
   unsigned long long* scratch = nullptr;  // small device counters (dist ops)
   bool smooth = false;    // kernels of the last enqueue used smoothed variates
   std::vector<cudaEvent_t>* prof = nullptr;  // per-launch events (cb_plan_profile)
+  bool prof_external = false;                 // record as graph event nodes
+  std::vector<cudaEvent_t> graph_events;      // of exec_prof
+  cudaGraphExec_t exec_prof = nullptr;
   bool cap_smooth = false;
   bool have_batch = false;
   bool have_rows = false;
@@ -169,7 +172,10 @@ struct cb_plan {
     if (exec_sample) cudaGraphExecDestroy(exec_sample);
     if (exec_gather) cudaGraphExecDestroy(exec_gather);
     if (exec_all) cudaGraphExecDestroy(exec_all);
-    exec_sample = exec_gather = exec_all = nullptr;
+    if (exec_prof) cudaGraphExecDestroy(exec_prof);
+    for (auto e : graph_events) cudaEventDestroy(e);
+    graph_events.clear();
+    exec_sample = exec_gather = exec_all = exec_prof = nullptr;
   }
   ~cb_plan() { drop_graphs(); }
 
@@ -343,7 +349,10 @@ void prof_mark(cb_plan* pl) {
   if (!pl->prof) return;
   cudaEvent_t e;
   CB_CUDA(cudaEventCreate(&e));
-  CB_CUDA(cudaEventRecord(e, pl->stream));
+  if (pl->prof_external)
+    CB_CUDA(cudaEventRecordWithFlags(e, pl->stream, cudaEventRecordExternal));
+  else
+    CB_CUDA(cudaEventRecord(e, pl->stream));
   pl->prof->push_back(e);
 }
 
@@ -1021,6 +1030,20 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
       CB_CUDA(cudaGraphInstantiate(&plan->exec_all, graph, 0));
       CB_CUDA(cudaGraphDestroy(graph));
     }
+    // profiling twin: same launches with external event-record nodes between
+    {
+      plan->prof = &plan->graph_events;
+      plan->prof_external = true;
+      CB_CUDA(cudaStreamBeginCapture(plan->stream, cudaStreamCaptureModeThreadLocal));
+      prof_mark(plan);
+      enqueue_batch(plan, mode, plan->seeds, seeds_off, &dummy, true);
+      if (f) enqueue_gather(plan, f);
+      CB_CUDA(cudaStreamEndCapture(plan->stream, &graph));
+      plan->prof = nullptr;
+      plan->prof_external = false;
+      CB_CUDA(cudaGraphInstantiate(&plan->exec_prof, graph, 0));
+      CB_CUDA(cudaGraphDestroy(graph));
+    }
     plan->cap_mode = mode;
     plan->cap_smooth = plan->smooth;
     plan->cap_off.assign(seeds_off, seeds_off + plan->P + 1);
@@ -1433,6 +1456,38 @@ int cb_memcpy(void* dst, const void* src, uint64_t bytes, int device) {
     if (!bytes) return;
     DeviceGuard dg(device);
     CB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+  });
+}
+
+int cb_plan_graph_profile(cb_plan* plan, const uint32_t* d_seeds, const cb_sched* sched,
+                          float* ms, int max_n, int* n) {
+  return guard([&] {
+    require(plan != nullptr && sched != nullptr && ms != nullptr && n != nullptr,
+            "null argument");
+    require(plan->exec_prof != nullptr, "no captured batch (call cb_plan_capture)");
+    DeviceGuard dg(plan->device);
+    cudaStream_t st = plan->stream;
+    const uint64_t total = plan->cap_off[plan->P];
+    if (d_seeds && total)
+      CB_CUDA(cudaMemcpyAsync(plan->seeds, d_seeds, total * 4, cudaMemcpyDefault, st));
+    const Variates v = make_variates(sched);
+    CB_CUDA(cudaMemcpyAsync(plan->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+    if (plan->dirty_mode >= 0 && plan->dirty_mode != plan->cap_mode)
+      for (uint32_t p = 0; p < plan->P; ++p) {
+        const Dirty d = dirty_of(plan, p, plan->dirty_mode);
+        launch_batch_begin(plan->pe[p].sync, d.bits, d.list, d.count, d.cap,
+                           plan->pe[p].bm[0].words_padded, st);
+      }
+    CB_CUDA(cudaGraphLaunch(plan->exec_prof, st));
+    CB_CUDA(cudaStreamSynchronize(st));
+    plan->dirty_mode = plan->cap_mode;
+    plan->have_batch = true;
+    plan->have_rows = true;
+    int k = 0;
+    const auto& ev = plan->graph_events;
+    for (size_t i = 1; i < ev.size() && k < max_n; ++i, ++k)
+      CB_CUDA(cudaEventElapsedTime(&ms[k], ev[i - 1], ev[i]));
+    *n = k;
   });
 }
 
