@@ -261,6 +261,21 @@ __device__ inline unsigned long long tile_prefix(unsigned long long* status, uns
   return *s_bcast;
 }
 
+// Tile cursor for ordered (look-back) kernels: the first tile of each CTA is
+// its role index (the first wave is co-resident: grids are capped at the
+// kernel's resident capacity, as in CUB's blockIdx-ordered scans); later
+// tiles come from a ticket counter offset by the CTA count, so a CTA waits
+// only on tiles held by running CTAs. No atomic at all when one wave covers
+// every tile.
+__device__ __forceinline__ unsigned next_tile_after(unsigned* ticket, unsigned* s_tile,
+                                                    unsigned ncta, unsigned long long ntiles) {
+  if (ncta >= ntiles) return 0xffffffffu;
+  __syncthreads();
+  if (threadIdx.x == 0) *s_tile = atomicAdd(ticket, 1u) + ncta;
+  __syncthreads();
+  return *s_tile;
+}
+
 // Ticket in ticket order (deadlock-free look-back with persistent CTAs).
 __device__ __forceinline__ unsigned next_tile(unsigned* ticket, unsigned* s_tile) {
   __syncthreads();

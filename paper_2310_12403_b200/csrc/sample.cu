@@ -19,6 +19,9 @@
 //                 the next frontier; standalone only after the last layer)
 // No host synchronisation: all counts live in device LayerMeta; every kernel
 // is a persistent ticketed loop bounded by those counts.
+#include <mutex>
+#include <unordered_map>
+
 #include "cb_internal.h"
 
 namespace cb {
@@ -109,8 +112,8 @@ __global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelAr
   const bool smooth = v.smoothed != 0;
   const uint64_t z1p = hstep(hstep(hinit(v.z1), 1ULL), static_cast<uint64_t>(a.layer));
   const uint32_t k = a.k;
-  for (unsigned tile = next_tile(a.ticket, &s_tile); tile < ntiles;
-       tile = next_tile(a.ticket, &s_tile)) {
+  for (unsigned tile = blockIdx.x; tile < ntiles;
+       tile = next_tile_after(a.ticket, &s_tile, gridDim.x, ntiles)) {
     const uint64_t i0 = static_cast<uint64_t>(tile) * TILE + threadIdx.x * IPT;
     unsigned long long q[IPT], o[IPT];
     uint32_t vv[IPT];
@@ -409,14 +412,19 @@ __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
   }
 }
 
-constexpr int kEmitWPT = 1;                    // keep words per thread
-constexpr int kEmitTileWords = kNT * kEmitWPT;  // 256 words = 8192 positions
+// Emit tiles: 256 keep words (8K positions) per tile for small layers, 2048
+// (64K positions) once a layer has > 64K words, so the look-back front never
+// walks more than a few thousand tiles.
+constexpr int kEmitWPT = 8;                     // max keep words per thread
+constexpr int kEmitTileWords = kNT * kEmitWPT;  // max words per tile
+constexpr uint64_t kEmitBigLayerWords = 64 * 1024;
 
 // Ordered compaction of the keep words. The tile's kept items are spread
 // over all threads (item q -> its word by binary search over the per-word
 // output bases in smem), so every kept edge is an independent chain:
 // word_rec -> record -> neighbour id -> store.
-__device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned ncta) {
+__device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned role,
+                                                unsigned ncta) {
   __shared__ unsigned long long s_scan[kNT / 32 + 1];
   __shared__ uint32_t s_wbase[kEmitTileWords + 1];
   __shared__ uint32_t s_word[kEmitTileWords];
@@ -425,17 +433,18 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned nct
   LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
   const uint64_t nwords = (total + 31) / 32;
-  const uint64_t ntiles = (nwords + kEmitTileWords - 1) / kEmitTileWords;
+  const int wpt = nwords > kEmitBigLayerWords ? kEmitWPT : 1;
+  const uint32_t tw = kNT * wpt;  // words per tile
+  const uint64_t ntiles = (nwords + tw - 1) / tw;
   const unsigned ep = inv_epoch(a.epoch, a.slot);
-  for (unsigned tile = next_tile(a.ticket, &s_tile); tile < ntiles;
-       tile = next_tile(a.ticket, &s_tile)) {
-    const uint64_t wt = static_cast<uint64_t>(tile) * kEmitTileWords;
-    const uint32_t l0 = threadIdx.x * kEmitWPT;
+  for (unsigned tile = role; tile < ntiles; tile = next_tile_after(a.ticket, &s_tile, ncta, ntiles)) {
+    const uint64_t wt = static_cast<uint64_t>(tile) * tw;
+    const uint32_t l0 = threadIdx.x * wpt;
     uint32_t wv[kEmitWPT];
     unsigned long long c = 0;
 #pragma unroll
     for (int j = 0; j < kEmitWPT; ++j) {
-      wv[j] = (wt + l0 + j < nwords) ? a.keep_words[wt + l0 + j] : 0u;
+      wv[j] = (j < wpt && wt + l0 + j < nwords) ? a.keep_words[wt + l0 + j] : 0u;
       c += __popc(wv[j]);
     }
     unsigned long long tot;
@@ -443,9 +452,11 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned nct
     uint32_t run = static_cast<uint32_t>(ex);
 #pragma unroll
     for (int j = 0; j < kEmitWPT; ++j) {
-      s_word[l0 + j] = wv[j];
-      s_wbase[l0 + j] = run;
-      run += __popc(wv[j]);
+      if (j < wpt) {
+        s_word[l0 + j] = wv[j];
+        s_wbase[l0 + j] = run;
+        run += __popc(wv[j]);
+      }
     }
     const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
     // (tile_prefix ends with __syncthreads: s_word / s_wbase are visible)
@@ -461,7 +472,7 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned nct
         x[u] = 0;
         ri[u] = 0;
         if (ok[u]) {
-          uint32_t lo = 0, hi = kEmitTileWords - 1;
+          uint32_t lo = 0, hi = tw - 1;
           while (lo < hi) {
             const uint32_t mid = (lo + hi + 1) >> 1;
             if (s_wbase[mid] <= q) lo = mid;
@@ -596,15 +607,15 @@ __global__ void __launch_bounds__(kNT) ns_emit_kernel(
 // Sorted unique list = set bits in id order; wprefix[w] = rank of word w.
 constexpr int kWPT = 2;  // words per thread (one 8-byte load)
 static_assert(kNT * kWPT == kExtractTileWords, "extract tile");
-__device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned ncta) {
+__device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned role,
+                                             unsigned ncta) {
   __shared__ unsigned long long s_scan[kNT / 32 + 1];
   __shared__ unsigned long long s_b;
   __shared__ unsigned s_tile;
   constexpr int TILE = kNT * kWPT;
   const uint64_t ntiles = a.words_padded / TILE;
   const unsigned ep = inv_epoch(a.epoch, a.slot);
-  for (unsigned tile = next_tile(a.ticket, &s_tile); tile < ntiles;
-       tile = next_tile(a.ticket, &s_tile)) {
+  for (unsigned tile = role; tile < ntiles; tile = next_tile_after(a.ticket, &s_tile, ncta, ntiles)) {
     const uint64_t w0 = static_cast<uint64_t>(tile) * TILE + threadIdx.x * kWPT;
     const uint2 wv2 = *reinterpret_cast<const uint2*>(a.bits + w0);
     if (a.zero_bits) *reinterpret_cast<uint2*>(a.zero_bits + w0) = make_uint2(0u, 0u);
@@ -637,14 +648,14 @@ __device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned ncta
 }
 
 __global__ void __launch_bounds__(kNT) extract_kernel(ExtractArgs a) {
-  extract_body(a, gridDim.x);
+  extract_body(a, blockIdx.x, gridDim.x);
 }
 
 // Extract (dedup of the layer) and the ordered LABOR edge emission only
 // depend on labor_mark, not on each other: one launch, CTAs split by role.
 __global__ void __launch_bounds__(kNT) post_kernel(ExtractArgs e, LaborArgs a, unsigned n_ext) {
-  if (blockIdx.x < n_ext) extract_body(e, n_ext);
-  else labor_emit_body(a, gridDim.x - n_ext);
+  if (blockIdx.x < n_ext) extract_body(e, blockIdx.x, n_ext);
+  else labor_emit_body(a, blockIdx.x - n_ext, gridDim.x - n_ext);
 }
 
 // ---------------------------------------------------------------- relabel --
@@ -678,6 +689,21 @@ constexpr int kLaborIPT = kLaborTile / kNT;
 
 }  // namespace
 
+// Resident CTAs per SM of a kernel at kNT threads (cached per function).
+template <typename K>
+int resident_per_sm(K kernel, size_t smem = 0) {
+  static std::unordered_map<const void*, int> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(reinterpret_cast<const void*>(kernel));
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  CB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kNT, smem));
+  n = std::max(1, n);
+  cache.emplace(reinterpret_cast<const void*>(kernel), n);
+  return n;
+}
+
 int grid_for(uint64_t work_items, int per_block, int max_per_sm) {
   const uint64_t blocks = (work_items + per_block - 1) / per_block;
   const uint64_t cap = static_cast<uint64_t>(kNumSMs) * max_per_sm;
@@ -696,8 +722,9 @@ void launch_batch_begin(const Sync& s, uint32_t* clear_bits, const uint32_t* cle
 
 void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_dst,
                      uint64_t relabel_work, cudaStream_t st) {
-  const int grid = std::max(grid_for(cap_dst, kNT * kFrontierIPT, 8),
-                            r.edges ? grid_for(relabel_work, kNT * 4, 8) : 1);
+  const int occ = resident_per_sm(frontier_kernel<kFrontierIPT>);
+  const int grid = std::max(grid_for(cap_dst, kNT * kFrontierIPT, occ),
+                            r.edges ? grid_for(relabel_work, kNT * 4, occ) : 1);
   frontier_kernel<kFrontierIPT><<<grid, kNT, 0, st>>>(a, r);
   CB_LAUNCH("frontier");
 }
@@ -712,8 +739,12 @@ void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStrea
 void launch_labor_post(const LaborArgs& a, uint64_t max_tiles, const ExtractArgs& e,
                        cudaStream_t st) {
   const uint64_t words = (max_tiles * kLaborTile + 31) / 32;
-  const int g_emit = grid_for(words, kEmitTileWords, 4);
-  const int g_ext = grid_for(e.words_padded, kNT * kWPT, 4);
+  const int occ = resident_per_sm(post_kernel);
+  // both roles share the resident capacity: extract gets what its tiles need
+  // (up to half), emit the rest
+  const int cap = occ * kNumSMs;
+  const int g_ext = std::min(grid_for(e.words_padded, kNT * kWPT, occ), cap / 2);
+  const int g_emit = std::min(grid_for(words, kEmitTileWords, occ), cap - g_ext);
   post_kernel<<<g_emit + g_ext, kNT, 0, st>>>(e, a, static_cast<unsigned>(g_ext));
   CB_LAUNCH("post");
 }
@@ -731,7 +762,7 @@ void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix
 }
 
 void launch_extract(const ExtractArgs& a, cudaStream_t st) {
-  const int grid = grid_for(a.words_padded, kNT * kWPT, 8);
+  const int grid = grid_for(a.words_padded, kNT * kWPT, resident_per_sm(extract_kernel));
   extract_kernel<<<grid, kNT, 0, st>>>(a);
   CB_LAUNCH("extract");
 }
