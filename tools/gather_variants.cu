@@ -1,0 +1,136 @@
+// Gather-kernel variant sweep at the c2 bench shape (not part of the
+// product): 55K random rows x 400 B out of a 2.45M-row fp32 table, L2 flushed
+// before every launch, CUDA-event timed inside a graph.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gv tools/gather_variants.cu
+#include <cstdio>
+#include <algorithm>
+#include <vector>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
+
+__global__ void read_k(const uint4* __restrict__ p, unsigned long long n, unsigned* sink) {
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  for (unsigned long long i = blockIdx.x * 1ull * blockDim.x + threadIdx.x; i < n;
+       i += 1ull * gridDim.x * blockDim.x) {
+    const uint4 v = p[i];
+    acc.x ^= v.x;
+  }
+  if (acc.x == 0x12345678u) *sink = acc.x;
+}
+
+__device__ __forceinline__ uint4 ldnc(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+// V1: flattened (row, vec) index, UNROLL loads in flight (current product)
+template <int U>
+__global__ void g_flat(const uint4* __restrict__ t, const unsigned* __restrict__ ids, unsigned n,
+                       unsigned vpr, uint4* __restrict__ out) {
+  const unsigned long long total = 1ull * n * vpr, stride = 1ull * gridDim.x * blockDim.x;
+  for (unsigned long long i = blockIdx.x * 1ull * blockDim.x + threadIdx.x; i < total; i += stride * U) {
+    uint4 b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned long long x = i + u * stride;
+      if (x < total) {
+        const unsigned r = (unsigned)(x / vpr), c = (unsigned)(x - 1ull * r * vpr);
+        b[u] = ldnc(t + 1ull * ids[r] * vpr + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned long long x = i + u * stride;
+      if (x < total) __stcs(out + x, b[u]);
+    }
+  }
+}
+
+// V2: one warp per R rows: ids loaded once per warp (coalesced), lanes cover
+// the row's vectors; R rows in flight per warp.
+template <int R>
+__global__ void g_warp(const uint4* __restrict__ t, const unsigned* __restrict__ ids, unsigned n,
+                       unsigned vpr, uint4* __restrict__ out) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned long long warp = (blockIdx.x * 1ull * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nw = (1ull * gridDim.x * blockDim.x) >> 5;
+  for (unsigned long long r0 = warp * R; r0 < n; r0 += nw * R) {
+    const unsigned myid = (lane < R && r0 + lane < n) ? ids[r0 + lane] : 0u;
+    uint4 b[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const unsigned v = __shfl_sync(0xffffffffu, myid, k);
+      if (r0 + k < n && lane < vpr) b[k] = ldnc(t + 1ull * v * vpr + lane);
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (r0 + k < n && lane < vpr) __stcs(out + (r0 + k) * vpr + lane, b[k]);
+  }
+}
+
+int main() {
+  const unsigned nrows = 2449029, vpr = 25, n = 54874;
+  uint4 *table, *out;
+  unsigned* ids;
+  CK(cudaMalloc(&table, 1ull * nrows * vpr * 16));
+  CK(cudaMalloc(&out, 1ull * n * vpr * 16));
+  CK(cudaMalloc(&ids, n * 4));
+  std::vector<unsigned> h(n);
+  unsigned long long x = 12345;
+  for (unsigned i = 0; i < n; ++i) {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    h[i] = (unsigned)(x % nrows);
+  }
+  std::sort(h.begin(), h.end());
+  CK(cudaMemcpy(ids, h.data(), n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemset(table, 1, 1ull * nrows * vpr * 16));
+  void* flush;
+  CK(cudaMalloc(&flush, 512u << 20));
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const double bytes = 2.0 * n * vpr * 16 + n * 4.0;
+  void* clean;
+  CK(cudaMalloc(&clean, 256u << 20));
+  unsigned* sink;
+  CK(cudaMalloc(&sink, 4));
+  bool readflush = false;
+  auto run = [&](const char* name, auto launch) {
+    float best = 1e9f, sum = 0;
+    for (int r = 0; r < 30; ++r) {
+      cudaMemsetAsync(flush, r, 512u << 20, st);
+      if (readflush) read_k<<<148 * 8, 256, 0, st>>>((const uint4*)clean, (256u << 20) / 16, sink);
+      cudaEventRecord(a, st);
+      launch();
+      cudaEventRecord(b, st);
+      cudaStreamSynchronize(st);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (r >= 5) { sum += ms; if (ms < best) best = ms; }
+    }
+    const float avg = sum / 25;
+    printf("%-34s avg %6.2f us  best %6.2f us  %6.0f GB/s (avg)\n", name, avg * 1e3, best * 1e3,
+           bytes / (avg * 1e-3) / 1e9);
+  };
+  for (int rf = 0; rf < 2; ++rf)
+  for (int g : {148 * 4, 148 * 16}) {
+    readflush = rf;
+    printf("-- flush: %s\n", rf ? "write 512MB + read 256MB" : "write 512MB");
+    char nm[64];
+    snprintf(nm, 64, "flat U=4 grid=%d", g);
+    run(nm, [&] { g_flat<4><<<g, 256, 0, st>>>(table, ids, n, vpr, out); });
+    snprintf(nm, 64, "flat U=8 grid=%d", g);
+    run(nm, [&] { g_flat<8><<<g, 256, 0, st>>>(table, ids, n, vpr, out); });
+    snprintf(nm, 64, "warp R=4 grid=%d", g);
+    run(nm, [&] { g_warp<4><<<g, 256, 0, st>>>(table, ids, n, vpr, out); });
+    snprintf(nm, 64, "warp R=8 grid=%d", g);
+    run(nm, [&] { g_warp<8><<<g, 256, 0, st>>>(table, ids, n, vpr, out); });
+  }
+  // large-batch reference point: 16x more rows (P=8 coop-like 880K rows)
+  return 0;
+}
