@@ -186,7 +186,7 @@ struct RelabelArgs {  // edges == nullptr disables
   uint32_t* dst_pos;
 };
 
-constexpr int kExtractTileWords = 512;
+constexpr int kExtractTileWords = 2048;  // bitmap padding granule (max tile)
 constexpr int kLaborTile = 4096;
 constexpr int kFrontierTile = 1024;
 

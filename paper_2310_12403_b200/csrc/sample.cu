@@ -605,29 +605,52 @@ __global__ void __launch_bounds__(kNT) ns_emit_kernel(
 
 // ---------------------------------------------------------------- extract --
 // Sorted unique list = set bits in id order; wprefix[w] = rank of word w.
-constexpr int kWPT = 2;  // words per thread (one 8-byte load)
-static_assert(kNT * kWPT == kExtractTileWords, "extract tile");
+// Words per thread: 2 for small bitmaps (more tiles, short per-thread
+// serial bit loops), 8 (two 16 B loads) once the bitmap exceeds 256K words,
+// so the look-back chain stays ~ <2K tiles even at 10^8 vertices.
+constexpr int kWPTSmall = 2;
+constexpr int kWPTBig = 8;
+static_assert(kNT * kWPTBig == kExtractTileWords, "extract tile");
+constexpr uint64_t kExtractBigWords = 256 * 1024;
+
 __device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned role,
                                              unsigned ncta) {
   __shared__ unsigned long long s_scan[kNT / 32 + 1];
   __shared__ unsigned long long s_b;
   __shared__ unsigned s_tile;
-  constexpr int TILE = kNT * kWPT;
-  const uint64_t ntiles = a.words_padded / TILE;
+  const int wpt = a.words_padded > kExtractBigWords ? kWPTBig : kWPTSmall;
+  const uint32_t tw = kNT * wpt;
+  const uint64_t ntiles = a.words_padded / tw;
   const unsigned ep = inv_epoch(a.epoch, a.slot);
   for (unsigned tile = role; tile < ntiles; tile = next_tile_after(a.ticket, &s_tile, ncta, ntiles)) {
-    const uint64_t w0 = static_cast<uint64_t>(tile) * TILE + threadIdx.x * kWPT;
-    const uint2 wv2 = *reinterpret_cast<const uint2*>(a.bits + w0);
-    if (a.zero_bits) *reinterpret_cast<uint2*>(a.zero_bits + w0) = make_uint2(0u, 0u);
-    const uint32_t wv[kWPT] = {wv2.x, wv2.y};
-    unsigned long long c = __popc(wv[0]) + __popc(wv[1]);
+    const uint64_t w0 = static_cast<uint64_t>(tile) * tw + threadIdx.x * wpt;
+    uint32_t wv[kWPTBig];
+    if (wpt == kWPTBig) {
+      const uint4 x = *reinterpret_cast<const uint4*>(a.bits + w0);
+      const uint4 y = *reinterpret_cast<const uint4*>(a.bits + w0 + 4);
+      wv[0] = x.x; wv[1] = x.y; wv[2] = x.z; wv[3] = x.w;
+      wv[4] = y.x; wv[5] = y.y; wv[6] = y.z; wv[7] = y.w;
+      if (a.zero_bits) {
+        *reinterpret_cast<uint4*>(a.zero_bits + w0) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(a.zero_bits + w0 + 4) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    } else {
+      const uint2 x = *reinterpret_cast<const uint2*>(a.bits + w0);
+      wv[0] = x.x; wv[1] = x.y;
+#pragma unroll
+      for (int j = 2; j < kWPTBig; ++j) wv[j] = 0u;
+      if (a.zero_bits) *reinterpret_cast<uint2*>(a.zero_bits + w0) = make_uint2(0u, 0u);
+    }
+    unsigned long long c = 0;
+#pragma unroll
+    for (int j = 0; j < kWPTBig; ++j) c += __popc(wv[j]);
     unsigned long long tot;
     const unsigned long long ex = block_exclusive_scan<kNT>(c, s_scan, tot);
     const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
     unsigned long long pos = gb + ex;
-    uint32_t pw[kWPT];
+    uint32_t pw[kWPTBig];
 #pragma unroll
-    for (int j = 0; j < kWPT; ++j) {
+    for (int j = 0; j < kWPTBig; ++j) {
       pw[j] = static_cast<uint32_t>(pos);
       uint32_t x = wv[j];
       while (x) {
@@ -637,7 +660,12 @@ __device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned role
         ++pos;
       }
     }
-    *reinterpret_cast<uint2*>(a.wprefix + w0) = make_uint2(pw[0], pw[1]);
+    if (wpt == kWPTBig) {
+      *reinterpret_cast<uint4*>(a.wprefix + w0) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+      *reinterpret_cast<uint4*>(a.wprefix + w0 + 4) = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+    } else {
+      *reinterpret_cast<uint2*>(a.wprefix + w0) = make_uint2(pw[0], pw[1]);
+    }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       *a.count_out = gb + tot;
       if (a.count_out2) *a.count_out2 = gb + tot;
@@ -743,7 +771,9 @@ void launch_labor_post(const LaborArgs& a, uint64_t max_tiles, const ExtractArgs
   // both roles share the resident capacity: extract gets what its tiles need
   // (up to half), emit the rest
   const int cap = occ * kNumSMs;
-  const int g_ext = std::min(grid_for(e.words_padded, kNT * kWPT, occ), cap / 2);
+  const int g_ext = std::min(
+      grid_for(e.words_padded, kNT * (e.words_padded > kExtractBigWords ? kWPTBig : kWPTSmall), occ),
+      cap / 2);
   const int g_emit = std::min(grid_for(words, kEmitTileWords, occ), cap - g_ext);
   post_kernel<<<g_emit + g_ext, kNT, 0, st>>>(e, a, static_cast<unsigned>(g_ext));
   CB_LAUNCH("post");
@@ -762,7 +792,9 @@ void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix
 }
 
 void launch_extract(const ExtractArgs& a, cudaStream_t st) {
-  const int grid = grid_for(a.words_padded, kNT * kWPT, resident_per_sm(extract_kernel));
+  const int grid = grid_for(a.words_padded,
+                            kNT * (a.words_padded > kExtractBigWords ? kWPTBig : kWPTSmall),
+                            resident_per_sm(extract_kernel));
   extract_kernel<<<grid, kNT, 0, st>>>(a);
   CB_LAUNCH("extract");
 }
