@@ -191,7 +191,9 @@ void make_bitmap(Arena& a, Bitmap& b, uint64_t n) {
   b.words_padded = ceil_div(std::max<uint64_t>(b.words, 1), kExtractTileWords) * kExtractTileWords;
   b.bits = a.alloc<uint32_t>(b.words_padded);
   b.wprefix = a.alloc<uint32_t>(b.words_padded);
+  b.summ = a.alloc<uint32_t>(b.words_padded / 32);
   CB_CUDA(cudaMemset(b.bits, 0, b.words_padded * sizeof(uint32_t)));
+  CB_CUDA(cudaMemset(b.summ, 0, b.words_padded / 32 * sizeof(uint32_t)));
 }
 
 // Capacity plan (host): upper bounds sized from the seeds and fanouts; any
@@ -360,6 +362,7 @@ void prof_mark(cb_plan* pl) {
 // (with its device count) that names every set word.
 struct Dirty {
   uint32_t* bits = nullptr;
+  uint32_t* summ = nullptr;
   const uint32_t* list = nullptr;
   const unsigned long long* count = nullptr;
   uint64_t cap = 0;
@@ -372,11 +375,13 @@ Dirty dirty_of(cb_plan* pl, uint32_t p, int mode) {
   const int L = pl->L;
   if (mode == CB_MODE_COOP && pl->P > 1) {
     d.bits = w.bm[1].bits;
+    d.summ = w.bm[1].summ;
     d.list = w.owner_final;
     d.count = &pl->meta_at(p, L)->n_dst;
     d.cap = w.cap_final;
   } else {
     d.bits = w.bm[(L - 1) & 1].bits;
+    d.summ = w.bm[(L - 1) & 1].summ;
     d.list = w.L[L - 1].src;
     d.count = &pl->meta_at(p, L - 1)->n_src;
     d.cap = w.L[L - 1].cap_src;
@@ -384,13 +389,15 @@ Dirty dirty_of(cb_plan* pl, uint32_t p, int mode) {
   return d;
 }
 
-ExtractArgs extract_args(PeWork& w, const Bitmap& bm, uint32_t* zero_bits, uint32_t* out,
+ExtractArgs extract_args(PeWork& w, const Bitmap& bm, const Bitmap* zero_bm, uint32_t* out,
                          uint64_t cap, unsigned long long* c1, unsigned long long* c2,
                          int ticket, int slot) {
   ExtractArgs e{};
   e.bits = bm.bits;
+  e.summ = bm.summ;
   e.wprefix = bm.wprefix;
-  e.zero_bits = zero_bits;
+  e.zero_bits = zero_bm ? zero_bm->bits : nullptr;
+  e.zero_summ = zero_bm ? zero_bm->summ : nullptr;
   e.words_padded = bm.words_padded;
   e.out = out;
   e.cap_out = cap;
@@ -437,6 +444,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   fa.layer = l;
   fa.var = pl->var;
   fa.set_bits = set_bm.bits;
+  fa.set_summ = set_bm.summ;
   fa.act = b.act;
   fa.tile_first = b.tile_first;
   fa.out_prefix = b.out_prefix;
@@ -463,6 +471,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   la.layer = l;
   la.var = pl->var;
   la.bits = set_bm.bits;
+  la.summ = set_bm.summ;
   la.edges = b.edges;
   la.slots = b.slots;
   la.keep_words = w.sync.keep_words;
@@ -515,7 +524,7 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
   const int dm = capturing ? mode : pl->dirty_mode;
   for (uint32_t p = 0; p < P; ++p) {
     const Dirty d = dirty_of(pl, p, dm);
-    launch_batch_begin(pl->pe[p].sync, d.bits, d.list, d.count, d.cap,
+    launch_batch_begin(pl->pe[p].sync, d.bits, d.summ, d.list, d.count, d.cap,
                        pl->pe[p].bm[0].words_padded, st);
     ++launches;
     prof_mark(pl);
@@ -538,7 +547,7 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
         launches += enqueue_layer(
             pl, w, p, l, D, cap_dst, l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[l & 1], fused,
             fused_work, smooth,
-            extract_args(w, w.bm[l & 1], w.bm[(l + 1) & 1].bits, w.L[l].src, w.L[l].cap_src,
+            extract_args(w, w.bm[l & 1], &w.bm[(l + 1) & 1], w.L[l].src, w.L[l].cap_src,
                          &pl->meta_at(p, l)->n_src, &pl->meta_at(p, l + 1)->n_dst, 3 * l + 2,
                          8 * l + 4));
       }
@@ -558,7 +567,7 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
         launches += enqueue_layer(
             pl, w, p, l, D, w.L[l].cap_dst, l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[0], none,
             0, smooth,
-            extract_args(w, w.bm[0], w.bm[1].bits, w.L[l].src, w.L[l].cap_src,
+            extract_args(w, w.bm[0], &w.bm[1], w.L[l].src, w.L[l].cap_src,
                          &pl->meta_at(p, l)->n_src, nullptr, 3 * l + 2, 8 * l + 4));
         launch_relabel(relabel_args(w.bm[0], w.L[l], D, pl->meta_at(p, l)),
                        std::max(w.L[l].cap_edges, w.L[l].cap_dst), st);
@@ -571,7 +580,9 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
         pp.src[p] = w.L[l].src;
         pp.count[p] = &pl->meta_at(p, l)->n_src;
         pp.clear_bits[p] = w.bm[0].bits;
+        pp.clear_summ[p] = w.bm[0].summ;
         pp.xbits[p] = w.bm[1].bits;
+        pp.xsumm[p] = w.bm[1].summ;
         pp.xprefix[p] = w.bm[1].wprefix;
         pp.loc_part[p] = w.loc_part[l];
         pp.loc_row[p] = w.loc_row[l];
@@ -1082,7 +1093,7 @@ int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_devic
       if (plan->dirty_mode >= 0 && plan->dirty_mode != plan->cap_mode) {
         for (uint32_t p = 0; p < plan->P; ++p) {
           const Dirty d = dirty_of(plan, p, plan->dirty_mode);
-          launch_batch_begin(plan->pe[p].sync, d.bits, d.list, d.count, d.cap,
+          launch_batch_begin(plan->pe[p].sync, d.bits, d.summ, d.list, d.count, d.cap,
                              plan->pe[p].bm[0].words_padded, st);
         }
       }
@@ -1335,7 +1346,7 @@ int cb_plan_sample_layer(cb_plan* plan, int layer, const uint32_t* d_dst, uint64
       plan->mode = CB_MODE_COOP;
     }
     const bool smooth = sched->kappa != cbdev::kKappaInf && sched->kappa >= 2;
-    launch_batch_begin(w.sync, nullptr, nullptr, nullptr, 0, 0, st);
+    launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);
     const RelabelArgs none{};
     enqueue_layer(plan, w, 0, layer, D, cap, n_dst, w.bm[0], none, 0, smooth,
                   extract_args(w, w.bm[0], nullptr, b.src, b.cap_src,
@@ -1377,8 +1388,8 @@ int cb_merge_owned(cb_plan* plan, int layer, const uint32_t* d_recv, uint64_t n_
     PeWork& w = plan->pe[0];
     cudaStream_t st = plan->stream;
     unsigned long long* cnt = plan->scratch;
-    launch_batch_begin(w.sync, nullptr, nullptr, nullptr, 0, 0, st);
-    mark_ids(d_recv, n_recv, w.bm[1].bits, st);
+    launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);
+    mark_ids(d_recv, n_recv, w.bm[1].bits, w.bm[1].summ, st);
     launch_extract(extract_args(w, w.bm[1], nullptr, d_next, cap_next, cnt, nullptr,
                                 3 * plan->L + layer, 8 * layer + 5),
                    st);
@@ -1475,7 +1486,7 @@ int cb_plan_graph_profile(cb_plan* plan, const uint32_t* d_seeds, const cb_sched
     if (plan->dirty_mode >= 0 && plan->dirty_mode != plan->cap_mode)
       for (uint32_t p = 0; p < plan->P; ++p) {
         const Dirty d = dirty_of(plan, p, plan->dirty_mode);
-        launch_batch_begin(plan->pe[p].sync, d.bits, d.list, d.count, d.cap,
+        launch_batch_begin(plan->pe[p].sync, d.bits, d.summ, d.list, d.count, d.cap,
                            plan->pe[p].bm[0].words_padded, st);
       }
     CB_CUDA(cudaGraphLaunch(plan->exec_prof, st));

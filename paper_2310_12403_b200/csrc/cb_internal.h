@@ -91,9 +91,13 @@ struct Sync {
 };
 
 // Bitmap dedup structure over the vertex id space.
+// Two levels: bits (1 per vertex) and summ (1 per data word, set by the
+// setter that turns a word non-zero), so extraction of large sparse bitmaps
+// visits only non-empty words.
 struct Bitmap {
   uint32_t* bits = nullptr;     // [words_padded]
   uint32_t* wprefix = nullptr;  // [words_padded] rank of first bit of word
+  uint32_t* summ = nullptr;     // [words_padded / 32]
   uint64_t words = 0, words_padded = 0;
 };
 
@@ -122,6 +126,7 @@ struct FrontierArgs {
   int layer;
   const cbdev::Variates* var;
   uint32_t* set_bits;
+  uint32_t* set_summ;
   ActRec* act;
   uint32_t* tile_first;
   uint64_t* out_prefix;
@@ -146,6 +151,7 @@ struct LaborArgs {
   int layer;
   const cbdev::Variates* var;
   uint32_t* bits;
+  uint32_t* summ;
   uint2* edges;
   uint32_t* slots;
   uint32_t* keep_words;  // 1 bit per scan position (labor_mark -> labor_emit)
@@ -161,8 +167,10 @@ struct LaborArgs {
 
 struct ExtractArgs {
   const uint32_t* bits;
+  const uint32_t* summ;
   uint32_t* wprefix;
   uint32_t* zero_bits;  // optional: bitmap zeroed word-for-word on the way
+  uint32_t* zero_summ;
   uint64_t words_padded;
   uint32_t* out;
   uint64_t cap_out;
@@ -192,7 +200,8 @@ constexpr int kFrontierTile = 1024;
 
 // ----------------------------------------------------- kernel launchers ----
 // sample.cu
-void launch_batch_begin(const Sync& s, uint32_t* clear_bits, const uint32_t* clear_list,
+void launch_batch_begin(const Sync& s, uint32_t* clear_bits, uint32_t* clear_summ,
+                        const uint32_t* clear_list,
                         const unsigned long long* clear_count, uint64_t clear_cap,
                         uint64_t nwords, cudaStream_t st);
 void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_dst,

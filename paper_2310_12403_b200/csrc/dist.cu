@@ -92,12 +92,14 @@ __global__ void scatter_rows_kernel(const V* __restrict__ in, const uint32_t* __
   }
 }
 
-__global__ void mark_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t* bits) {
+__global__ void mark_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32_t* bits,
+                            uint32_t* summ) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
        k += stride) {
     const uint32_t v = ids[k];
-    atomicOr(&bits[v >> 5], 1u << (v & 31u));
+    if (atomicOr(&bits[v >> 5], 1u << (v & 31u)) == 0u)
+      atomicOr(&summ[v >> 10], 1u << ((v >> 5) & 31u));
   }
 }
 
@@ -178,9 +180,10 @@ void scatter_rows(const void* in, const uint32_t* perm, uint64_t n, uint64_t row
   CB_LAUNCH("scatter_rows");
 }
 
-void mark_ids(const uint32_t* ids, uint64_t n, uint32_t* bits, cudaStream_t st) {
+void mark_ids(const uint32_t* ids, uint64_t n, uint32_t* bits, uint32_t* summ,
+              cudaStream_t st) {
   if (!n) return;
-  mark_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(ids, n, bits);
+  mark_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(ids, n, bits, summ);
   CB_LAUNCH("mark");
 }
 

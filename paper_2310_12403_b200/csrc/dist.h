@@ -18,6 +18,7 @@ void scatter_u32(const uint32_t* in, const uint32_t* perm, uint64_t n, uint32_t*
                  cudaStream_t st);
 void scatter_rows(const void* in, const uint32_t* perm, uint64_t n, uint64_t row_bytes,
                   void* out, cudaStream_t st);
-void mark_ids(const uint32_t* ids, uint64_t n, uint32_t* bits, cudaStream_t st);
+void mark_ids(const uint32_t* ids, uint64_t n, uint32_t* bits, uint32_t* summ,
+              cudaStream_t st);
 
 }  // namespace cb

@@ -25,14 +25,19 @@ __global__ void route_kernel(PartPtrs pp, const uint32_t* __restrict__ owner, ui
   const uint64_t n = *pp.count[p];
   const uint32_t* src = pp.src[p];
   uint32_t* clear = pp.clear_bits[p];
+  uint32_t* clear_s = pp.clear_summ[p];
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
        j += stride) {
     const uint32_t v = src[j];
     const uint32_t q = owner[v];
-    atomicOr(&pp.xbits[q][v >> 5], 1u << (v & 31u));
+    if (atomicOr(&pp.xbits[q][v >> 5], 1u << (v & 31u)) == 0u)
+      atomicOr(&pp.xsumm[q][v >> 10], 1u << ((v >> 5) & 31u));
     atomicAdd(&hist[q], 1ULL);
-    if (clear) clear[v >> 5] = 0u;
+    if (clear) {
+      clear[v >> 5] = 0u;
+      clear_s[v >> 10] = 0u;
+    }
   }
   __syncthreads();
   for (uint32_t q = threadIdx.x; q < P; q += blockDim.x)

@@ -12,7 +12,9 @@ struct PartPtrs {
   const uint32_t* src[kMaxParts];              // sender's sorted src list
   const unsigned long long* count[kMaxParts];  // its length (device)
   uint32_t* clear_bits[kMaxParts];             // sender's sampling bitmap
+  uint32_t* clear_summ[kMaxParts];
   uint32_t* xbits[kMaxParts];                  // owner's exchange bitmap
+  uint32_t* xsumm[kMaxParts];
   uint32_t* xprefix[kMaxParts];                // owner's exchange word ranks
   uint32_t* loc_part[kMaxParts];
   uint32_t* loc_row[kMaxParts];

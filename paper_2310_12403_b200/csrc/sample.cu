@@ -35,8 +35,9 @@ __device__ __forceinline__ unsigned inv_epoch(const unsigned* ep, int slot) {
   return ((*ep & 0x3ffffu) << 6) | static_cast<unsigned>(slot);
 }
 
-__device__ __forceinline__ void set_bit(uint32_t* bits, uint32_t v) {
-  atomicOr(&bits[v >> 5], 1u << (v & 31u));
+__device__ __forceinline__ void set_bit(uint32_t* bits, uint32_t* summ, uint32_t v) {
+  if (atomicOr(&bits[v >> 5], 1u << (v & 31u)) == 0u)
+    atomicOr(&summ[v >> 10], 1u << ((v >> 5) & 31u));
 }
 
 __device__ __forceinline__ uint32_t bm_rank(const uint32_t* bits, const uint32_t* wprefix,
@@ -66,7 +67,7 @@ __device__ void relabel_range(const RelabelArgs& r, uint64_t tid, uint64_t strid
 // Clears the previous batch's last bitmap (its final id list), bumps the
 // look-back epoch, resets the overflow flag. One launch per batch.
 __global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, unsigned* tickets,
-                                   int n_tickets, uint32_t* clear_bits,
+                                   int n_tickets, uint32_t* clear_bits, uint32_t* clear_summ,
                                    const uint32_t* __restrict__ clear_list,
                                    const unsigned long long* clear_count, uint64_t cap,
                                    uint64_t nwords) {
@@ -83,7 +84,10 @@ __global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, unsigned
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += stride) {
     const uint32_t w = clear_list[i] >> 5;
-    if (w < nwords) clear_bits[w] = 0u;
+    if (w < nwords) {
+      clear_bits[w] = 0u;
+      clear_summ[w >> 5] = 0u;
+    }
   }
 }
 
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelAr
         vv[j] = vx;
         rs[j] = a.indptr[vx];
         const uint64_t d = a.indptr[vx + 1] - rs[j];
-        set_bit(a.set_bits, vx);
+        set_bit(a.set_bits, a.set_summ, vx);
         if (is_ns) {
           q[j] = d > k ? d - k : 0;
           o[j] = d < k ? d : k;
@@ -306,7 +310,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
       const bool keep = keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert);
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == j) my_word = bal;
-      if (keep) set_bit(a.bits, tv[j]);
+      if (keep) set_bit(a.bits, a.summ, tv[j]);
     }
     my_rec = a0 + cur;
   } else {
@@ -334,7 +338,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
         my_word = bal;
         my_rec = a0 + wrec;
       }
-      if (keep) set_bit(a.bits, tv[j]);
+      if (keep) set_bit(a.bits, a.summ, tv[j]);
     }
   }
   if (lane < IPT && r0 + lane * 32 < rend) {
@@ -572,7 +576,7 @@ __global__ void __launch_bounds__(kNT) ns_emit_kernel(
     const uint32_t* __restrict__ D, const LayerMeta* meta,
     const uint64_t* __restrict__ out_prefix, const uint64_t* __restrict__ indptr,
     const uint32_t* __restrict__ indices, uint32_t k, const uint32_t* __restrict__ slots,
-    uint32_t* bits, uint2* edges, uint64_t cap_edges) {
+    uint32_t* bits, uint32_t* summ, uint2* edges, uint64_t cap_edges) {
   __shared__ uint64_t s_op[kEmitDst + 1];
   __shared__ uint64_t s_rs[kEmitDst];
   __shared__ uint32_t s_d[kEmitDst];
@@ -598,7 +602,7 @@ __global__ void __launch_bounds__(kNT) ns_emit_kernel(
       const uint64_t pos = (s_d[li] <= k) ? q : slots[x];
       const uint32_t t = __ldg(indices + s_rs[li] + pos);
       edges[x] = make_uint2(t, static_cast<uint32_t>(d0 + li));
-      set_bit(bits, t);
+      set_bit(bits, summ, t);
     }
   }
 }
@@ -613,7 +617,7 @@ constexpr int kWPTBig = 8;
 static_assert(kNT * kWPTBig == kExtractTileWords, "extract tile");
 constexpr uint64_t kExtractBigWords = 256 * 1024;
 
-__device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned role,
+__device__ __forceinline__ void extract_flat(const ExtractArgs& a, unsigned role,
                                              unsigned ncta) {
   __shared__ unsigned long long s_scan[kNT / 32 + 1];
   __shared__ unsigned long long s_b;
@@ -641,6 +645,8 @@ __device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned role
       for (int j = 2; j < kWPTBig; ++j) wv[j] = 0u;
       if (a.zero_bits) *reinterpret_cast<uint2*>(a.zero_bits + w0) = make_uint2(0u, 0u);
     }
+    if (a.zero_summ && threadIdx.x < tw / 32)
+      a.zero_summ[static_cast<uint64_t>(tile) * (tw / 32) + threadIdx.x] = 0u;
     unsigned long long c = 0;
 #pragma unroll
     for (int j = 0; j < kWPTBig; ++j) c += __popc(wv[j]);
@@ -672,6 +678,75 @@ __device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned role
       if (gb + tot > a.cap_out) atomicExch(a.overflow, 1u);
     }
   }
+}
+
+// Summary-driven extraction for large bitmaps: a tile is kNT summary words
+// (8K data words); threads visit only data words whose summary bit is set,
+// so the cost follows the frontier, not n. The zeroing of the previous
+// layer's bitmap likewise walks its own summary.
+__device__ __forceinline__ void extract_summ(const ExtractArgs& a, unsigned role,
+                                             unsigned ncta) {
+  __shared__ unsigned long long s_scan[kNT / 32 + 1];
+  __shared__ unsigned long long s_b;
+  __shared__ unsigned s_tile;
+  const uint64_t swords = a.words_padded / 32;
+  const uint64_t ntiles = (swords + kNT - 1) / kNT;
+  const unsigned ep = inv_epoch(a.epoch, a.slot);
+  for (unsigned tile = role; tile < ntiles; tile = next_tile_after(a.ticket, &s_tile, ncta, ntiles)) {
+    const uint64_t sw = static_cast<uint64_t>(tile) * kNT + threadIdx.x;
+    const uint32_t sm = sw < swords ? a.summ[sw] : 0u;
+    if (a.zero_summ && sw < swords) {
+      uint32_t z = a.zero_summ[sw];
+      while (z) {
+        const int j = __ffs(z) - 1;
+        z &= z - 1;
+        a.zero_bits[sw * 32 + j] = 0u;
+      }
+      a.zero_summ[sw] = 0u;
+    }
+    unsigned long long c = 0;
+    {
+      uint32_t m = sm;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        c += __popc(a.bits[sw * 32 + j]);
+      }
+    }
+    unsigned long long tot;
+    const unsigned long long ex = block_exclusive_scan<kNT>(c, s_scan, tot);
+    const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
+    unsigned long long pos = gb + ex;
+    uint32_t m = sm;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint64_t w = sw * 32 + j;
+      uint32_t x = a.bits[w];
+      a.wprefix[w] = static_cast<uint32_t>(pos);
+      while (x) {
+        const int bit = __ffs(x) - 1;
+        x &= x - 1;
+        if (pos < a.cap_out) a.out[pos] = static_cast<uint32_t>(w * 32 + bit);
+        ++pos;
+      }
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+      *a.count_out = gb + tot;
+      if (a.count_out2) *a.count_out2 = gb + tot;
+      if (gb + tot > a.cap_out) atomicExch(a.overflow, 1u);
+    }
+  }
+}
+
+__device__ __forceinline__ bool extract_uses_summary(const ExtractArgs& a) {
+  return a.words_padded > kExtractBigWords;
+}
+
+__device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned role,
+                                             unsigned ncta) {
+  if (extract_uses_summary(a)) extract_summ(a, role, ncta);
+  else extract_flat(a, role, ncta);
   retire_ticket(a.ticket, a.exit_ctr, ncta);
 }
 
@@ -703,19 +778,27 @@ __global__ void rank_kernel(const uint32_t* __restrict__ bits,
     out[i] = bm_rank(bits, wprefix, ids[i]);
 }
 
-__global__ void clear_kernel(uint32_t* bits, const uint32_t* __restrict__ list,
+__global__ void clear_kernel(uint32_t* bits, uint32_t* summ, const uint32_t* __restrict__ list,
                              const unsigned long long* count) {
   const uint64_t n = *count;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += stride)
-    bits[list[i] >> 5] = 0u;
+       i += stride) {
+    const uint32_t v = list[i];
+    bits[v >> 5] = 0u;
+    summ[v >> 10] = 0u;
+  }
 }
 
 constexpr int kFrontierIPT = 4;
 constexpr int kLaborIPT = kLaborTile / kNT;
 
 }  // namespace
+
+uint64_t extract_tiles(uint64_t words_padded) {
+  if (words_padded > kExtractBigWords) return (words_padded / 32 + kNT - 1) / kNT;
+  return words_padded / (kNT * kWPTSmall);
+}
 
 // Resident CTAs per SM of a kernel at kNT threads (cached per function).
 template <typename K>
@@ -738,13 +821,13 @@ int grid_for(uint64_t work_items, int per_block, int max_per_sm) {
   return static_cast<int>(std::max<uint64_t>(1, std::min(blocks, cap)));
 }
 
-void launch_batch_begin(const Sync& s, uint32_t* clear_bits, const uint32_t* clear_list,
-                        const unsigned long long* clear_count, uint64_t clear_cap,
-                        uint64_t nwords, cudaStream_t st) {
+void launch_batch_begin(const Sync& s, uint32_t* clear_bits, uint32_t* clear_summ,
+                        const uint32_t* clear_list, const unsigned long long* clear_count,
+                        uint64_t clear_cap, uint64_t nwords, cudaStream_t st) {
   const int grid = grid_for(clear_cap, 256, 4);
   batch_begin_kernel<<<grid, 256, 0, st>>>(s.epoch, s.overflow, s.tickets, Sync::kMaxTickets,
-                                           clear_bits, clear_list, clear_count, clear_cap,
-                                           nwords);
+                                           clear_bits, clear_summ, clear_list, clear_count,
+                                           clear_cap, nwords);
   CB_LAUNCH("batch_begin");
 }
 
@@ -771,9 +854,7 @@ void launch_labor_post(const LaborArgs& a, uint64_t max_tiles, const ExtractArgs
   // both roles share the resident capacity: extract gets what its tiles need
   // (up to half), emit the rest
   const int cap = occ * kNumSMs;
-  const int g_ext = std::min(
-      grid_for(e.words_padded, kNT * (e.words_padded > kExtractBigWords ? kWPTBig : kWPTSmall), occ),
-      cap / 2);
+  const int g_ext = std::min(grid_for(extract_tiles(e.words_padded), 1, occ), cap / 2);
   const int g_emit = std::min(grid_for(words, kEmitTileWords, occ), cap - g_ext);
   post_kernel<<<g_emit + g_ext, kNT, 0, st>>>(e, a, static_cast<unsigned>(g_ext));
   CB_LAUNCH("post");
@@ -787,14 +868,12 @@ void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix
   CB_LAUNCH("ns_reservoir");
   const int grid = grid_for(cap_dst, kEmitDst, 8);
   ns_emit_kernel<<<grid, kNT, 0, st>>>(D, a.meta, out_prefix, indptr, indices, a.k, a.slots,
-                                       a.bits, a.edges, a.cap_edges);
+                                       a.bits, a.summ, a.edges, a.cap_edges);
   CB_LAUNCH("ns_emit");
 }
 
 void launch_extract(const ExtractArgs& a, cudaStream_t st) {
-  const int grid = grid_for(a.words_padded,
-                            kNT * (a.words_padded > kExtractBigWords ? kWPTBig : kWPTSmall),
-                            resident_per_sm(extract_kernel));
+  const int grid = grid_for(extract_tiles(a.words_padded), 1, resident_per_sm(extract_kernel));
   extract_kernel<<<grid, kNT, 0, st>>>(a);
   CB_LAUNCH("extract");
 }
@@ -813,7 +892,7 @@ void launch_rank(const Bitmap& bm, const uint32_t* ids, const unsigned long long
 
 void launch_clear(Bitmap& bm, const uint32_t* list, const unsigned long long* count,
                   cudaStream_t st) {
-  clear_kernel<<<kNumSMs * 4, 256, 0, st>>>(bm.bits, list, count);
+  clear_kernel<<<kNumSMs * 4, 256, 0, st>>>(bm.bits, bm.summ, list, count);
   CB_LAUNCH("clear");
 }
 

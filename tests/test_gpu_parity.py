@@ -302,3 +302,34 @@ def test_graph_replay_matches_eager(c1, kappa):
         assert_stack_eq(got, want, f"replay step {step}")
         rows = plan.rows(0, store)
         assert np.array_equal(rows, O.feature_rows(3, 32, "f32", want[-1]["src"]))
+
+
+@pytest.mark.parametrize("kind,okind", KINDS[1:])
+def test_expand_parity_large_sparse_bitmap(gpu, kind, okind):
+    """n = 2^24 > 8.4M vertices: the dedup runs in summary-bitmap mode (only
+    non-empty words visited). Checked against the oracle on the downloaded CSR."""
+    n, m = 1 << 24, 1 << 25
+    g = cb.Graph.generate_rmat(n, m, 77)
+    ip, ix = g.download()
+    ref = O.CSR(ip, ix)
+    pool = np.arange(n, dtype=np.uint32)
+    for step in range(2):
+        seeds = O.draw_from_pool(pool, 2048, 77, step)
+        sched = cb.SeedSchedule.make(1, 100 + step)
+        got = cb.expand(g, seeds, 3, cb.SamplerConfig(kind, 10), sched)
+        want = O.expand(ref, seeds, 3, okind, 10, osched(sched))
+        assert_stack_eq(got, want, f"{kind.name} step={step}")
+
+
+def test_coop_parity_large_sparse_bitmap(gpu):
+    n, m, P = 1 << 24, 1 << 25, 4
+    g = cb.Graph.generate_rmat(n, m, 78)
+    ip, ix = g.download()
+    ref = O.CSR(ip, ix)
+    pm = cb.partition_random(g, P, 3)
+    owner = O.partition_random(n, P, 3)
+    seeds = O.draw_coop_seeds(owner, P, 512, 3, 0)
+    sched = cb.SeedSchedule.plain(5)
+    res = cb.coop_sample(g, pm, seeds, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), sched)
+    exp = O.coop_sample(ref, owner, P, seeds, 3, O.LABOR0, 10, osched(sched))
+    coop_eq(res, exp, P, 3, "large coop")
