@@ -191,9 +191,11 @@ void make_bitmap(Arena& a, Bitmap& b, uint64_t n) {
   b.words_padded = ceil_div(std::max<uint64_t>(b.words, 1), kExtractTileWords) * kExtractTileWords;
   b.bits = a.alloc<uint32_t>(b.words_padded);
   b.wprefix = a.alloc<uint32_t>(b.words_padded);
-  b.summ = a.alloc<uint32_t>(b.words_padded / 32);
   CB_CUDA(cudaMemset(b.bits, 0, b.words_padded * sizeof(uint32_t)));
-  CB_CUDA(cudaMemset(b.summ, 0, b.words_padded / 32 * sizeof(uint32_t)));
+  if (b.words_padded > kExtractBigWords) {  // summary only where extract uses it
+    b.summ = a.alloc<uint32_t>(b.words_padded / 32);
+    CB_CUDA(cudaMemset(b.summ, 0, b.words_padded / 32 * sizeof(uint32_t)));
+  }
 }
 
 // Capacity plan (host): upper bounds sized from the seeds and fanouts; any

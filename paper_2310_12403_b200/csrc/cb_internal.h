@@ -195,6 +195,7 @@ struct RelabelArgs {  // edges == nullptr disables
 };
 
 constexpr int kExtractTileWords = 2048;  // bitmap padding granule (max tile)
+constexpr uint64_t kExtractBigWords = 256 * 1024;  // summary-mode threshold
 constexpr int kLaborTile = 4096;
 constexpr int kFrontierTile = 1024;
 

@@ -98,8 +98,8 @@ __global__ void mark_kernel(const uint32_t* __restrict__ ids, uint64_t n, uint32
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
        k += stride) {
     const uint32_t v = ids[k];
-    if (atomicOr(&bits[v >> 5], 1u << (v & 31u)) == 0u)
-      atomicOr(&summ[v >> 10], 1u << ((v >> 5) & 31u));
+    atomicOr(&bits[v >> 5], 1u << (v & 31u));
+    if (summ) atomicOr(&summ[v >> 10], 1u << ((v >> 5) & 31u));
   }
 }
 

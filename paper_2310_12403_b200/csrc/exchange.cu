@@ -31,12 +31,12 @@ __global__ void route_kernel(PartPtrs pp, const uint32_t* __restrict__ owner, ui
        j += stride) {
     const uint32_t v = src[j];
     const uint32_t q = owner[v];
-    if (atomicOr(&pp.xbits[q][v >> 5], 1u << (v & 31u)) == 0u)
-      atomicOr(&pp.xsumm[q][v >> 10], 1u << ((v >> 5) & 31u));
+    atomicOr(&pp.xbits[q][v >> 5], 1u << (v & 31u));
+    if (pp.xsumm[q]) atomicOr(&pp.xsumm[q][v >> 10], 1u << ((v >> 5) & 31u));
     atomicAdd(&hist[q], 1ULL);
     if (clear) {
       clear[v >> 5] = 0u;
-      clear_s[v >> 10] = 0u;
+      if (clear_s) clear_s[v >> 10] = 0u;
     }
   }
   __syncthreads();

@@ -35,9 +35,11 @@ __device__ __forceinline__ unsigned inv_epoch(const unsigned* ep, int slot) {
   return ((*ep & 0x3ffffu) << 6) | static_cast<unsigned>(slot);
 }
 
+// summ == nullptr for bitmaps small enough to be extracted flat; otherwise
+// the summary bit of the word is OR-ed too (both fire-and-forget REDs).
 __device__ __forceinline__ void set_bit(uint32_t* bits, uint32_t* summ, uint32_t v) {
-  if (atomicOr(&bits[v >> 5], 1u << (v & 31u)) == 0u)
-    atomicOr(&summ[v >> 10], 1u << ((v >> 5) & 31u));
+  atomicOr(&bits[v >> 5], 1u << (v & 31u));
+  if (summ) atomicOr(&summ[v >> 10], 1u << ((v >> 5) & 31u));
 }
 
 __device__ __forceinline__ uint32_t bm_rank(const uint32_t* bits, const uint32_t* wprefix,
@@ -86,7 +88,7 @@ __global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, unsigned
     const uint32_t w = clear_list[i] >> 5;
     if (w < nwords) {
       clear_bits[w] = 0u;
-      clear_summ[w >> 5] = 0u;
+      if (clear_summ) clear_summ[w >> 5] = 0u;
     }
   }
 }
@@ -615,7 +617,6 @@ __global__ void __launch_bounds__(kNT) ns_emit_kernel(
 constexpr int kWPTSmall = 2;
 constexpr int kWPTBig = 8;
 static_assert(kNT * kWPTBig == kExtractTileWords, "extract tile");
-constexpr uint64_t kExtractBigWords = 256 * 1024;
 
 __device__ __forceinline__ void extract_flat(const ExtractArgs& a, unsigned role,
                                              unsigned ncta) {
@@ -786,7 +787,7 @@ __global__ void clear_kernel(uint32_t* bits, uint32_t* summ, const uint32_t* __r
        i += stride) {
     const uint32_t v = list[i];
     bits[v >> 5] = 0u;
-    summ[v >> 10] = 0u;
+    if (summ) summ[v >> 10] = 0u;
   }
 }
 
