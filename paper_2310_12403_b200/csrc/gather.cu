@@ -13,84 +13,20 @@
 
 #include "cb_internal.h"
 #include "gather.h"
+#include "gather_body.cuh"
 
 namespace cb {
 using namespace cbdev;
 
 namespace {
 
-template <typename V>
-__device__ __forceinline__ V ld_stream(const V* p);
-template <>
-__device__ __forceinline__ uint4 ld_stream<uint4>(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-template <>
-__device__ __forceinline__ uint2 ld_stream<uint2>(const uint2* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
-               : "=r"(r.x), "=r"(r.y)
-               : "l"(p));
-  return r;
-}
-template <>
-__device__ __forceinline__ uint32_t ld_stream<uint32_t>(const uint32_t* p) {
-  uint32_t r;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
-  return r;
-}
-template <>
-__device__ __forceinline__ unsigned short ld_stream<unsigned short>(const unsigned short* p) {
-  unsigned short r;
-  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
-  return r;
-}
-
-template <typename V>
-__device__ __forceinline__ void st_stream(V* p, V v) {
-  __stcs(p, v);
-}
-template <>
-__device__ __forceinline__ void st_stream<unsigned short>(unsigned short* p, unsigned short v) {
-  asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"(v));
-}
-
-// out[j] = table[row(ids[j])], j < count. Flattened (row, vector) index space
-// so every lane moves a full vector even when row_bytes/16 is not a multiple
-// of 32. row(v) = row_map ? row_map[v] : v.
 template <typename V, int UNROLL>
 __global__ void __launch_bounds__(256) gather_kernel(
     const V* __restrict__ table, const uint32_t* __restrict__ ids,
     const unsigned long long* __restrict__ count, uint64_t cap_rows,
     const uint32_t* __restrict__ row_map, uint32_t vpr, V* __restrict__ out) {
-  // count == nullptr: cap_rows is the row count itself
-  const uint64_t n = count ? min(static_cast<uint64_t>(*count), cap_rows) : cap_rows;
-  const uint64_t total = n * vpr;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  for (; idx < total; idx += stride * UNROLL) {
-    V buf[UNROLL];
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      const uint64_t x = idx + u * stride;
-      if (x < total) {
-        const uint64_t r = x / vpr;
-        const uint64_t c = x - r * vpr;
-        const uint32_t v = __ldg(ids + r);
-        const uint64_t row = row_map ? __ldg(row_map + v) : v;
-        buf[u] = ld_stream(table + row * vpr + c);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      const uint64_t x = idx + u * stride;
-      if (x < total) st_stream(out + x, buf[u]);
-    }
-  }
+  gbody::gather_body<V, UNROLL>(table, ids, count, cap_rows, row_map, vpr, out, blockIdx.x,
+                                gridDim.x);
 }
 
 // value[v, j] = 2*U(hash(seed,{9,v,j})) - 1 (exact in f64), one rounding to

@@ -23,6 +23,7 @@
 #include <unordered_map>
 
 #include "cb_internal.h"
+#include "gather_body.cuh"
 
 namespace cb {
 using namespace cbdev;
@@ -68,12 +69,14 @@ __device__ void relabel_range(const RelabelArgs& r, uint64_t tid, uint64_t strid
 // ------------------------------------------------------------ batch begin --
 // Clears the previous batch's last bitmap (its final id list), bumps the
 // look-back epoch, resets the overflow flag. One launch per batch.
-__global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, unsigned* tickets,
-                                   int n_tickets, uint32_t* clear_bits, uint32_t* clear_summ,
-                                   const uint32_t* __restrict__ clear_list,
-                                   const unsigned long long* clear_count, uint64_t cap,
-                                   uint64_t nwords) {
-  if (blockIdx.x == 0) {
+__device__ __forceinline__ void batch_begin_body(unsigned* epoch, unsigned* overflow,
+                                                 unsigned* tickets, int n_tickets,
+                                                 uint32_t* clear_bits, uint32_t* clear_summ,
+                                                 const uint32_t* __restrict__ clear_list,
+                                                 const unsigned long long* clear_count,
+                                                 uint64_t cap, uint64_t nwords, unsigned role,
+                                                 unsigned ncta) {
+  if (role == 0) {
     if (threadIdx.x == 0) {
       *epoch = *epoch + 1;
       *overflow = 0;
@@ -82,8 +85,8 @@ __global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, unsigned
   }
   if (!clear_bits) return;
   const uint64_t n = min(static_cast<uint64_t>(*clear_count), cap);
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+  const uint64_t stride = static_cast<uint64_t>(ncta) * blockDim.x;
+  for (uint64_t i = role * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += stride) {
     const uint32_t w = clear_list[i] >> 5;
     if (w < nwords) {
@@ -93,21 +96,31 @@ __global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, unsigned
   }
 }
 
+__global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, unsigned* tickets,
+                                   int n_tickets, uint32_t* clear_bits, uint32_t* clear_summ,
+                                   const uint32_t* __restrict__ clear_list,
+                                   const unsigned long long* clear_count, uint64_t cap,
+                                   uint64_t nwords) {
+  batch_begin_body(epoch, overflow, tickets, n_tickets, clear_bits, clear_summ, clear_list,
+                   clear_count, cap, nwords, blockIdx.x, gridDim.x);
+}
+
 // ---------------------------------------------------------------- frontier --
 // kind: 0 FULL, 1 NS, 2 LABOR0 (samplers.hpp:15). Per dst: scan work q
 // (LABOR/FULL: d; NS: reservoir positions max(d-k,0)), active flag q>0 and,
 // for NS, the output count min(d,k).
 template <int IPT>
-__global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelArgs r) {
+__device__ __forceinline__ void frontier_body(const FrontierArgs& a, const RelabelArgs& r,
+                                              unsigned role, unsigned ncta) {
   __shared__ unsigned long long s_scan[3][kNT / 32 + 1];
   __shared__ unsigned long long s_bc[3];
   __shared__ unsigned s_tile;
   if (r.edges) {  // relabel of the previous layer (independent work)
-    relabel_range(r, blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
-                  static_cast<uint64_t>(gridDim.x) * blockDim.x);
+    relabel_range(r, role * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
+                  static_cast<uint64_t>(ncta) * blockDim.x);
   }
   LayerMeta* meta = a.meta;
-  if (a.n_dst_param != ~0ULL && blockIdx.x == 0 && threadIdx.x == 0)
+  if (a.n_dst_param != ~0ULL && role == 0 && threadIdx.x == 0)
     meta->n_dst = a.n_dst_param;
   const uint64_t n = (a.n_dst_param != ~0ULL) ? a.n_dst_param : meta->n_dst;
   constexpr int TILE = kNT * IPT;
@@ -118,8 +131,8 @@ __global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelAr
   const bool smooth = v.smoothed != 0;
   const uint64_t z1p = hstep(hstep(hinit(v.z1), 1ULL), static_cast<uint64_t>(a.layer));
   const uint32_t k = a.k;
-  for (unsigned tile = blockIdx.x; tile < ntiles;
-       tile = next_tile_after(a.ticket, &s_tile, gridDim.x, ntiles)) {
+  for (unsigned tile = role; tile < ntiles;
+       tile = next_tile_after(a.ticket, &s_tile, ncta, ntiles)) {
     const uint64_t i0 = static_cast<uint64_t>(tile) * TILE + threadIdx.x * IPT;
     unsigned long long q[IPT], o[IPT];
     uint32_t vv[IPT];
@@ -215,7 +228,7 @@ __global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelAr
       }
     }
   }
-  if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (n == 0 && role == 0 && threadIdx.x == 0) {
     ActRec sent{};
     a.act[0] = sent;
     a.tile_first[0] = 0;
@@ -226,6 +239,11 @@ __global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelAr
     if (is_ns) a.out_prefix[0] = 0;
   }
   retire_ticket(a.ticket, a.exit_ctr, gridDim.x);
+}
+
+template <int IPT>
+__global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelArgs r) {
+  frontier_body<IPT>(a, r, blockIdx.x, gridDim.x);
 }
 
 // Largest record index in [lo, hi] whose scan prefix is <= x.
@@ -351,7 +369,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
 }
 
 template <int IPT, bool SMOOTH>
-__global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
+__device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, unsigned ncta) {
   constexpr int TILE = kNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
   constexpr uint32_t WSPAN = 32 * IPT;  // contiguous positions owned by one warp
@@ -370,7 +388,7 @@ __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
   const uint64_t p2 = SMOOTH ? hstep(hstep(hinit(v.z2), 2ULL), static_cast<uint64_t>(a.layer)) : 0;
   const uint32_t warp = threadIdx.x >> 5;
   unsigned long long uncert = 0;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (uint64_t tile = role; tile < ntiles; tile += ncta) {
     const uint64_t x0 = tile * TILE;
     const uint32_t rend = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), total - x0));
     uint32_t a0, a1;
@@ -416,6 +434,11 @@ __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
     uncert = warp_sum(uncert);
     if (lane_id() == 0 && uncert) atomicAdd(&meta->uncertified, uncert);
   }
+}
+
+template <int IPT, bool SMOOTH>
+__global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
+  mark_body<IPT, SMOOTH>(a, blockIdx.x, gridDim.x);
 }
 
 // Emit tiles: 256 keep words (8K positions) per tile for small layers, 2048
@@ -794,6 +817,43 @@ __global__ void clear_kernel(uint32_t* bits, uint32_t* summ, const uint32_t* __r
 constexpr int kFrontierIPT = 4;
 constexpr int kLaborIPT = kLaborTile / kNT;
 
+// Software grid barrier for the cooperative fused kernel (all CTAs are
+// co-resident: cudaLaunchCooperativeKernel). `target` = barrier index x grid.
+__device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (ld_acquire_u32(ctr) < target) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <bool SMOOTH>
+__global__ void __launch_bounds__(kNT, 2) fused_batch_kernel(const __grid_constant__ FusedParams p) {
+  const unsigned G = gridDim.x, b = blockIdx.x;
+  unsigned k = 0;
+  batch_begin_body(p.epoch, p.overflow, p.tickets, Sync::kMaxTickets, p.clear_bits,
+                   p.clear_summ, p.clear_list, p.clear_count, p.clear_cap, p.clear_nwords, b, G);
+  grid_sync(p.barrier, ++k * G);
+  for (int l = 0; l < p.L; ++l) {
+    const FusedLayer& fl = p.layer[l];
+    frontier_body<kFrontierIPT>(fl.f, fl.relabel_prev, b, G);
+    grid_sync(p.barrier, ++k * G);
+    mark_body<kLaborIPT, SMOOTH>(fl.la, b, G);
+    grid_sync(p.barrier, ++k * G);
+    if (b < p.n_ext) extract_body(fl.ex, b, p.n_ext);
+    else labor_emit_body(fl.la, b - p.n_ext, G - p.n_ext);
+    grid_sync(p.barrier, ++k * G);
+  }
+  relabel_range(p.relabel_last, b * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
+                static_cast<uint64_t>(G) * blockDim.x);
+  if (p.table)
+    gbody::gather_any(p.table, p.vec_bytes, p.vpr, p.gather_ids, p.gather_count, p.cap_rows,
+                      p.row_map, p.rows_out, b, G);
+}
+
 }  // namespace
 
 uint64_t extract_tiles(uint64_t words_padded) {
@@ -883,6 +943,19 @@ void launch_relabel(const RelabelArgs& r, uint64_t work, cudaStream_t st) {
   const int grid = grid_for(work, 256 * 4, 8);
   relabel_kernel<<<grid, 256, 0, st>>>(r);
   CB_LAUNCH("relabel");
+}
+
+void launch_fused(FusedParams& p, bool smooth, cudaStream_t st) {
+  void* args[] = {&p};
+  auto* k = smooth ? fused_batch_kernel<true> : fused_batch_kernel<false>;
+  const int occ = resident_per_sm(k);
+  const int grid = occ * kNumSMs;
+  const uint64_t ext_tiles = p.L > 0 ? extract_tiles(p.layer[0].ex.words_padded) : 1;
+  p.n_ext = static_cast<unsigned>(std::max<uint64_t>(
+      1, std::min<uint64_t>(ext_tiles, static_cast<uint64_t>(grid / 2))));
+  CB_CUDA(cudaMemsetAsync(p.barrier, 0, sizeof(unsigned), st));
+  CB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(kNT),
+                                      args, 0, st));
 }
 
 void launch_rank(const Bitmap& bm, const uint32_t* ids, const unsigned long long* count,
