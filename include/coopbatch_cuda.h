@@ -199,6 +199,9 @@ int cb_plan_profile(cb_plan* plan, int mode, const uint32_t* seeds_flat,
 int cb_plan_graph_profile(cb_plan* plan, const uint32_t* d_seeds, const cb_sched* sched,
                           float* ms, int max_n, int* n);
 
+/* Debug: globaltimer stamps of the last batch (plan created with CB_TRACE=1). */
+int cb_plan_trace(cb_plan* plan, uint64_t* out, uint64_t n);
+
 /* Number of kernels one cb_sample/cb_gather call enqueues (for reporting). */
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n);
 

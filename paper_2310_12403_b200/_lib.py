@@ -72,6 +72,7 @@ _SIGS = {
                                   C.POINTER(C.c_int)]),
     "cb_plan_graph_profile": (C.c_int, [_P, _P, C.POINTER(Sched), _P, C.c_int,
                                         C.POINTER(C.c_int)]),
+    "cb_plan_trace": (C.c_int, [_P, _P, _u64]),
     "cb_plan_launch_count": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_u64)]),
 }
 

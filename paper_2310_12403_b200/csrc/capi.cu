@@ -151,7 +151,9 @@ struct cb_plan {
   uint32_t dist_world = 0;  // >0: one part of a multi-process cooperative step
   unsigned long long* scratch = nullptr;  // small device counters (dist ops)
   bool smooth = false;    // kernels of the last enqueue used smoothed variates
-  bool use_fused = true;  // single cooperative launch for indep LABOR/FULL batches
+  bool trace_on = false;   // globaltimer stamps per CTA (debug, CB_TRACE=1)
+  unsigned long long* trace = nullptr;  // [kTraceSlots]
+  bool use_fused = false;  // single cooperative launch (slower on B200 at b=1024: see DESIGN)
   std::vector<cudaEvent_t>* prof = nullptr;  // per-launch events (cb_plan_profile)
   bool prof_external = false;                 // record as graph event nodes
   std::vector<cudaEvent_t> graph_events;      // of exec_prof
@@ -282,6 +284,10 @@ void plan_alloc(cb_plan* pl) {
   pl->seeds_cap = static_cast<uint64_t>(P) * std::max<uint64_t>(pl->max_seeds, 1);
   pl->seeds = pl->mem.alloc<uint32_t>(pl->seeds_cap);
   pl->scratch = pl->mem.alloc<unsigned long long>(8);
+  if (pl->trace_on) {
+    pl->trace = pl->mem.alloc<unsigned long long>(kTraceSlots);
+    CB_CUDA(cudaMemset(pl->trace, 0, kTraceSlots * 8));
+  }
   pl->have_batch = false;
   pl->dirty_mode = -1;
   CB_CUDA(cudaDeviceSynchronize());
@@ -457,6 +463,7 @@ FrontierArgs frontier_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint
   fa.epoch = w.sync.epoch;
   fa.slot = 8 * l;
   fa.overflow = w.sync.overflow;
+  fa.trace = pl->trace ? pl->trace + (3 * l) * kTraceKernel : nullptr;
   return fa;
 }
 
@@ -486,6 +493,7 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
   la.epoch = w.sync.epoch;
   la.slot = 8 * l + 3;
   la.overflow = w.sync.overflow;
+  la.trace = pl->trace ? pl->trace + (3 * l + 1) * kTraceKernel : nullptr;
   return la;
 }
 
@@ -1000,6 +1008,7 @@ int cb_plan_create(const cb_graph* g, const cb_partition* pm, int num_layers, in
     }
     pl->max_seeds = std::max<uint64_t>(max_seeds_per_part, 1);
     if (const char* e = std::getenv("CB_FUSED")) pl->use_fused = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CB_TRACE")) pl->trace_on = std::atoi(e) != 0;
     CB_CUDA(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
     plan_alloc(pl.get());
     *out = pl.release();
@@ -1575,6 +1584,17 @@ int cb_plan_graph_profile(cb_plan* plan, const uint32_t* d_seeds, const cb_sched
     for (size_t i = 1; i < ev.size() && k < max_n; ++i, ++k)
       CB_CUDA(cudaEventElapsedTime(&ms[k], ev[i - 1], ev[i]));
     *n = k;
+  });
+}
+
+int cb_plan_trace(cb_plan* plan, uint64_t* out, uint64_t n) {
+  return guard([&] {
+    require(plan != nullptr && out != nullptr, "null argument");
+    require(plan->trace != nullptr, "tracing off (set CB_TRACE=1 before creating the plan)");
+    DeviceGuard dg(plan->device);
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    CB_CUDA(cudaMemcpy(out, plan->trace, std::min<uint64_t>(n, kTraceSlots) * 8,
+                       cudaMemcpyDeviceToHost));
   });
 }
 

@@ -130,6 +130,16 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// trace[cta*8 + k] = time stamp k of this CTA (first writer per slot wins)
+__device__ __forceinline__ void tstamp(unsigned long long* trace, unsigned cta, int k) {
+  if (trace && cta < 64 && threadIdx.x == 0) trace[cta * 8 + k] = gtimer();
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;

@@ -117,7 +117,14 @@ struct ActRec {
   uint32_t d;              // degree
 };
 
+// Debug tracing (CB_TRACE=1): per kernel, per CTA (<= kTraceCtas) up to 8
+// %globaltimer stamps at fixed points.
+constexpr int kTraceCtas = 64;
+constexpr int kTraceKernel = kTraceCtas * 8;
+constexpr int kTraceSlots = 32 * kTraceKernel;
+
 struct FrontierArgs {
+  unsigned long long* trace;
   const uint32_t* D;
   LayerMeta* meta;
   unsigned long long n_dst_param;  // ~0 = read meta->n_dst
@@ -142,6 +149,7 @@ struct FrontierArgs {
 };
 
 struct LaborArgs {
+  unsigned long long* trace;
   LayerMeta* meta;
   const ActRec* act;
   const uint32_t* tile_first;

@@ -115,10 +115,12 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
   __shared__ unsigned long long s_scan[3][kNT / 32 + 1];
   __shared__ unsigned long long s_bc[3];
   __shared__ unsigned s_tile;
+  tstamp(a.trace, role, 0);
   if (r.edges) {  // relabel of the previous layer (independent work)
     relabel_range(r, role * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
                   static_cast<uint64_t>(ncta) * blockDim.x);
   }
+  tstamp(a.trace, role, 1);
   LayerMeta* meta = a.meta;
   if (a.n_dst_param != ~0ULL && role == 0 && threadIdx.x == 0)
     meta->n_dst = a.n_dst_param;
@@ -161,6 +163,7 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
       as += (q[j] > 0);
       os += o[j];
     }
+    if (tile == role) tstamp(a.trace, role, 2);
     unsigned long long tq, ta, to = 0;
     unsigned long long eq = block_exclusive_scan<kNT>(qs, s_scan[0], tq);
     unsigned long long ea = block_exclusive_scan<kNT>(as, s_scan[1], ta);
@@ -172,6 +175,7 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
         tile_prefix<4>(a.st_b, tile, ta, inv_epoch(a.epoch, a.slot + 1), &s_bc[1]);
     unsigned long long bo = 0;
     if (is_ns) bo = tile_prefix<4>(a.st_c, tile, to, inv_epoch(a.epoch, a.slot + 2), &s_bc[2]);
+    if (tile == role) tstamp(a.trace, role, 3);
     eq += bq;
     ea += ba;
     eo += bo;
@@ -228,6 +232,7 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
       }
     }
   }
+  tstamp(a.trace, role, 4);
   if (n == 0 && role == 0 && threadIdx.x == 0) {
     ActRec sent{};
     a.act[0] = sent;
@@ -388,6 +393,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   const uint64_t p2 = SMOOTH ? hstep(hstep(hinit(v.z2), 2ULL), static_cast<uint64_t>(a.layer)) : 0;
   const uint32_t warp = threadIdx.x >> 5;
   unsigned long long uncert = 0;
+  tstamp(a.trace, role, 0);
   for (uint64_t tile = role; tile < ntiles; tile += ncta) {
     const uint64_t x0 = tile * TILE;
     const uint32_t rend = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), total - x0));
@@ -434,6 +440,8 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
     uncert = warp_sum(uncert);
     if (lane_id() == 0 && uncert) atomicAdd(&meta->uncertified, uncert);
   }
+  __syncthreads();
+  tstamp(a.trace, role, 1);
 }
 
 template <int IPT, bool SMOOTH>

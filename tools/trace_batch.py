@@ -1,0 +1,33 @@
+"""Debug: globaltimer stamps of one c2 batch (CB_TRACE=1). Prints per kernel
+the stamp offsets (us) relative to the first stamp of the batch."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+os.environ["CB_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2310_12403_b200 as cb  # noqa: E402
+from paper_2310_12403_b200 import _lib  # noqa: E402
+from paper_2310_12403_b200.seeds import draw_from_pool  # noqa: E402
+
+g = cb.Graph.generate_rmat(2449029, 61859140, 42)
+plan = cb.Plan(g, None, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), 1024)
+pool = np.arange(g.num_vertices, dtype=np.uint32)
+s = cb.SeedSchedule.make(1, 1234)
+for step in range(4):
+    seeds = draw_from_pool(pool, 1024, 1234, cb.hash_bits(step, [0]))
+    plan.sample([seeds], s, cb.MODE_INDEP)
+    s = cb.schedule_advance(s)
+buf = np.zeros(32 * 64 * 8, np.uint64)
+assert _lib.load().cb_plan_trace(plan._h, buf.ctypes.data_as(C.c_void_p), len(buf)) == 0
+t = buf.reshape(32, 64, 8).astype(np.int64)
+t0 = t[t > 0].min()
+names = {0: "frontier0", 1: "mark0", 3: "frontier1", 4: "mark1", 6: "frontier2", 7: "mark2"}
+for k, nm in names.items():
+    for cta in range(0, 64, 8):
+        row = t[k, cta]
+        if row[0] == 0:
+            continue
+        print(nm, cta, [round((x - t0) / 1000, 2) if x else None for x in row[:5]])
