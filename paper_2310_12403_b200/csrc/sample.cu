@@ -138,20 +138,24 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
     const uint64_t i0 = static_cast<uint64_t>(tile) * TILE + threadIdx.x * IPT;
     unsigned long long q[IPT], o[IPT];
     uint32_t vv[IPT];
-    uint64_t rs[IPT];
+    uint64_t rs[IPT], re[IPT];
     unsigned long long qs = 0, as = 0, os = 0;
+    // batched loads: all ids, then all indptr pairs, then the bitmap REDs (the
+    // atomics may alias, so interleaving them would serialise the loads)
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) vv[j] = (i0 + j < n) ? __ldg(a.D + i0 + j) : 0u;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      rs[j] = (i0 + j < n) ? __ldg(a.indptr + vv[j]) : 0;
+      re[j] = (i0 + j < n) ? __ldg(a.indptr + vv[j] + 1) : 0;
+    }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const uint64_t i = i0 + j;
       q[j] = o[j] = 0;
-      vv[j] = 0;
-      rs[j] = 0;
       if (i < n) {
-        const uint32_t vx = a.D[i];
-        vv[j] = vx;
-        rs[j] = a.indptr[vx];
-        const uint64_t d = a.indptr[vx + 1] - rs[j];
-        set_bit(a.set_bits, a.set_summ, vx);
+        const uint64_t d = re[j] - rs[j];
+        set_bit(a.set_bits, a.set_summ, vv[j]);
         if (is_ns) {
           q[j] = d > k ? d - k : 0;
           o[j] = d < k ? d : k;
