@@ -70,6 +70,19 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel: str, dim: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per launch from
+    the committed `ncu --set full` capture of this workload (profiles/), or
+    None when no capture of this shape is committed."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        e = d[kernel]
+        return e["dram_bytes"] if e.get("dim") == dim else None
+    except Exception:
+        return None
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -198,6 +211,53 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------ concavity evidence --
+def concavity_evidence(cb, g, scfg, L, b, row_bytes, dev, parts=(1, 2, 4, 8)):
+    """The paper's work comparison at equal global batch (acceptance.cpp:
+    270-300): P parts of b seeds (cli.cpp:210-214 draws), cooperative
+    (coop_sample: per-owner input sets |S^L_p| after the exchange) vs
+    independent (the same global batch split round-robin, indep_sample).
+    All P parts run on this one GPU (the reference's simulated PEs)."""
+    import torch
+
+    from paper_2310_12403_b200.seeds import coop_seeds
+    out = []
+    sched = cb.SeedSchedule.make(1, RUN_SEED)
+    for P in parts:
+        pm = cb.partition_random(g, P, RUN_SEED)
+        seeds = coop_seeds(pm.members(), b, RUN_SEED, 0)
+        plan = cb.Plan(g, pm, L, scfg, b)
+        plan.sample(seeds, sched, cb.MODE_COOP)
+        st = torch.cuda.ExternalStream(plan.stream, device=torch.device(f"cuda:{dev}"))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        plan.sample(seeds, sched, cb.MODE_COOP, sync=False)
+        e1.record(st)
+        plan.synchronize()
+        coop_ms = e0.elapsed_time(e1)
+        c_s3 = sum(len(plan.owner_set(p)) for p in range(P))
+        c_work = sum(plan.layer_sizes(p, l)["n_edges"] for p in range(P) for l in range(L))
+        c_comm = sum(plan.exchange(l).total_communicated() for l in range(L))
+        union = np.concatenate(seeds)
+        chunks = [union[i::P] for i in range(P)]
+        ip = cb.Plan(g, None, L, scfg, max(len(c) for c in chunks))
+        i_s3 = i_work = 0
+        for c in chunks:
+            ip.sample([c], sched, cb.MODE_INDEP)
+            i_s3 += ip.layer_sizes(0, L - 1)["n_src"]
+            i_work += sum(ip.layer_sizes(0, l)["n_edges"] for l in range(L))
+        gb = P * b
+        out.append({"P": P, "global_batch": gb,
+                    "coop": {"input_vertices_per_seed": c_s3 / gb, "edges_per_seed": c_work / gb,
+                             "feature_bytes_per_seed": c_s3 * row_bytes / gb,
+                             "ids_exchanged_per_seed": c_comm / gb,
+                             "step_ms_one_gpu_eager": round(coop_ms, 4)},
+                    "indep": {"input_vertices_per_seed": i_s3 / gb, "edges_per_seed": i_work / gb,
+                              "feature_bytes_per_seed": i_s3 * row_bytes / gb}})
+        del plan, ip, pm
+    return out
+
+
 # -------------------------------------------------------------- our arm ----
 def run_ours(args, cfg):
     import torch
@@ -281,7 +341,7 @@ def run_ours(args, cfg):
     for i in range(K):
         flush_l2()
         gev[i][0].record(stream)
-        plan.replay(None, None, True, 2)
+        plan.gather(store)  # one gather_kernel launch on the plan stream
         gev[i][1].record(stream)
     torch.cuda.synchronize()
     gath_ms = [e[0].elapsed_time(e[1]) for e in gev]
@@ -333,12 +393,13 @@ def run_ours(args, cfg):
                    "cuda_graphs": True},
         "feature_gbps": feat_gbps,
         "stage_ms": {"sample_dedup": float(np.mean(samp_ms)), "gather": float(np.mean(gath_ms)),
-                     "note": "gather timed alone (own graph launch); sample = step - gather"},
+                     "note": "gather timed alone (one launch, events on its stream); sample = step - gather"},
         "e2e": {"value": seeds_total / e2e_s, "unit": "seeds/s",
                 "h2d_bytes_per_step": b * 4 + 40, "d2h_bytes_per_step": 64},
         "roofline": {"bound": "hbm", "kernel": "gather_kernel<uint4,4>",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic("gather_kernel", cfg["dim"]),
                      "bytes_per_launch": gather_bytes},
         "gpu_launches": launches_per_step * K,
         "kernel_ms_graph": [round(x, 4) for x in prof_ms],
@@ -347,6 +408,8 @@ def run_ours(args, cfg):
                      "feature_bytes_per_step": rows_last * row_bytes},
         "clocks": clocks.summary(),
     }
+    if world == 1 and not args.no_evidence:
+        line["evidence"]["concavity"] = concavity_evidence(cb, g, scfg, L, b, row_bytes, dev)
     if world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import oracle as O
@@ -369,6 +432,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-evidence", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

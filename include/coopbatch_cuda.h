@@ -92,6 +92,11 @@ int cb_partition_random(const cb_graph* g, uint32_t parts, uint64_t seed, cb_par
 int cb_partition_create(const cb_graph* g, const uint32_t* owner, uint32_t parts,
                         cb_partition** out);
 int cb_partition_download(const cb_partition* pm, uint32_t* owner);
+/* part_members (partition.hpp:33-36, src/partition.cpp:99-105): the vertices of
+ * all parts concatenated part-major, ascending within a part (members[n]);
+ * shard_off[parts+1] = start of each part. This order is the feature shard
+ * layout (row of v = its index here). Either pointer may be NULL. */
+int cb_partition_members(const cb_partition* pm, uint32_t* members, uint64_t* shard_off);
 void cb_partition_destroy(cb_partition* pm);
 
 /* ---- feature tables (row-sharded by owner when pm != NULL) ---- */

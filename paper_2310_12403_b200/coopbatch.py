@@ -195,6 +195,13 @@ class PartitionMap:
         _check(_lib.load().cb_partition_download(self._h, _ptr(o)))
         return o
 
+    def members(self) -> list[np.ndarray]:
+        """part_members (partition.cpp:99-105): ascending members of each part."""
+        m = np.zeros(self._g.num_vertices, np.uint32)
+        off = np.zeros(self.num_parts + 1, np.uint64)
+        _check(_lib.load().cb_partition_members(self._h, _ptr(m), _ptr(off)))
+        return [m[int(off[q]):int(off[q + 1])] for q in range(self.num_parts)]
+
     def __del__(self):
         if getattr(self, "_h", None):
             _lib.load().cb_partition_destroy(self._h)

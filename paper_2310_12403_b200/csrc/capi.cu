@@ -857,6 +857,9 @@ static void finish_partition(cb_partition* pm) {
   CB_CUDA(cudaMemcpy(ids, iota.data(), n * 4, cudaMemcpyHostToDevice));
   uint32_t* keys = pm->mem.alloc<uint32_t>(n);
   CB_CUDA(cudaMemcpy(keys, pm->owner, n * 4, cudaMemcpyDeviceToDevice));
+  // the copies above run on the legacy stream (D2D and staged pageable H2D
+  // return before completion); st is non-blocking, so order them explicitly
+  CB_CUDA(cudaDeviceSynchronize());
   int bits = 1;
   while ((1u << bits) < pm->parts) ++bits;
   cub::DoubleBuffer<uint32_t> kb(keys, keys2), vb(ids, pm->members);
@@ -923,6 +926,16 @@ int cb_partition_download(const cb_partition* pm, uint32_t* owner) {
     require(pm != nullptr && owner != nullptr, "null argument");
     DeviceGuard dg(pm->device);
     CB_CUDA(cudaMemcpy(owner, pm->owner, pm->n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int cb_partition_members(const cb_partition* pm, uint32_t* members, uint64_t* shard_off) {
+  return guard([&] {
+    require(pm != nullptr, "null partition");
+    DeviceGuard dg(pm->device);
+    if (members) CB_CUDA(cudaMemcpy(members, pm->members, pm->n * 4, cudaMemcpyDeviceToHost));
+    if (shard_off)
+      for (uint32_t q = 0; q <= pm->parts; ++q) shard_off[q] = pm->shard_off[q];
   });
 }
 

@@ -53,7 +53,10 @@ __device__ __forceinline__ void st_stream<unsigned short>(unsigned short* p, uns
 
 // out[j] = table[row(ids[j])], j < count. Flattened (row, vector) index space
 // so every lane moves a full vector even when row_bytes/16 is not a multiple
-// of 32. row(v) = row_map ? row_map[v] : v.
+// of 32. row(v) = row_map ? row_map[v] : v. Index math is 32-bit whenever the
+// flattened space fits (division by vpr = multiply-high + correction), and
+// each thread issues all its id loads before any table load so the UNROLL
+// table reads are in flight together.
 template <typename V, int UNROLL>
 __device__ __forceinline__ void gather_body(const V* __restrict__ table,
                                             const uint32_t* __restrict__ ids,
@@ -65,6 +68,42 @@ __device__ __forceinline__ void gather_body(const V* __restrict__ table,
   const uint64_t n = count ? min(static_cast<uint64_t>(*count), cap_rows) : cap_rows;
   const uint64_t total = n * vpr;
   const uint64_t stride = static_cast<uint64_t>(ncta) * blockDim.x;
+  if (total + stride * UNROLL < (1ULL << 32)) {
+    const uint32_t tot32 = static_cast<uint32_t>(total), s32 = static_cast<uint32_t>(stride);
+    const uint32_t magic = 0xffffffffu / vpr;
+    for (uint32_t idx = role * blockDim.x + threadIdx.x; idx < tot32; idx += s32 * UNROLL) {
+      uint32_t r[UNROLL], c[UNROLL];
+      V buf[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const uint32_t x = idx + u * s32;
+        uint32_t q = __umulhi(x, magic);
+        uint32_t rem = x - q * vpr;
+        while (rem >= vpr) {
+          ++q;
+          rem -= vpr;
+        }
+        r[u] = x < tot32 ? q : 0u;
+        c[u] = rem;
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) r[u] = __ldg(ids + r[u]);
+      if (row_map) {
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) r[u] = __ldg(row_map + r[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (idx + u * s32 < tot32)
+          buf[u] = ld_stream(table + static_cast<uint64_t>(r[u]) * vpr + c[u]);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const uint32_t x = idx + u * s32;
+        if (x < tot32) st_stream(out + x, buf[u]);
+      }
+    }
+    return;
+  }
   uint64_t idx = role * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   for (; idx < total; idx += stride * UNROLL) {
     V buf[UNROLL];

@@ -181,6 +181,19 @@ def coop_eq(res: cb.CoopSampleResult, exp: dict, P: int, L: int, where=""):
             assert np.array_equal(a.loc_row[p], b["loc_row"][p]), f"{where} loc_row {l},{p}"
 
 
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+def test_partition_members(c1, P):
+    """partition.cpp:99-105 part_members: the shard layout of the feature
+    tables (non-power-of-two part counts included)."""
+    g, ref = c1
+    for _ in range(3):  # the member sort once raced the owner copy
+        pm = cb.partition_random(g, P, 11 + P)
+        owner = O.partition_random(ref.n, P, 11 + P)
+        assert np.array_equal(pm.owner, owner)
+        for got, want in zip(pm.members(), O.part_members(owner, P)):
+            assert np.array_equal(got, want)
+
+
 @pytest.mark.parametrize("P", [1, 2, 4, 8])
 @pytest.mark.parametrize("kind,okind", KINDS[1:])
 def test_coop_parity_c1(c1, P, kind, okind):
