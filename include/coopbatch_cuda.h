@@ -30,6 +30,11 @@
  *   cb_download_block         <- BipartiteBlock fields (samplers.hpp:30-38)
  *   cb_download_exchange      <- ExchangeRecord fields (coop.hpp:25-37)
  *   cb_download_owner_set     <- CoopSampleResult::owner_sets (coop.hpp:39-43)
+ *   cb_cache_*                <- LruCache / feature_load_sim (cache.hpp:17-42,
+ *                                80-83; src/cache.cpp:8-32, 74-119)
+ *   cb_stack_fingerprint,     <- stack_fingerprint / run_dependent_experiment
+ *   cb_shuffled_order            order (src/cache.cpp:123-162)
+ *   cb_partition_members      <- part_members (partition.hpp:33-36)
  *   cb_last_error             <- the what() of coopbatch::InputError etc.
  *                                (include/coopbatch/common.hpp:12-31)
  */
@@ -209,6 +214,48 @@ int cb_plan_trace(cb_plan* plan, uint64_t* out, uint64_t n);
 
 /* Number of kernels one cb_sample/cb_gather call enqueues (for reporting). */
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n);
+
+/* ---- per-GPU feature cache (LruCache, cache.hpp:17-42; cache.cpp:8-32) ----
+ * Exact LRU semantics evaluated one id set at a time on the device: the ids
+ * of a step (sorted unique, e.g. input_vertices()) are accessed in
+ * access_order(ids, order_key) (cache.cpp:74-84), optionally only those with
+ * owner == part (feature_load_sim's cooperative filter, cache.cpp:105).
+ * row_bytes > 0 gives the cache HBM row storage: with a backing table and
+ * d_rows_out, rows of the kept ids are produced in kept (ascending id) order,
+ * hits read from the cache, misses from the table (HBM or host tier). */
+typedef struct cb_cache cb_cache;
+int cb_cache_create(int device, uint64_t n_keys, uint64_t capacity, uint64_t row_bytes,
+                    cb_cache** out);
+void cb_cache_destroy(cb_cache* c);
+/* LruCache::access over an arbitrary host trace: miss[i] = 1 on a miss. */
+int cb_cache_access_trace(cb_cache* c, const uint32_t* keys, uint64_t n, uint8_t* miss);
+int cb_cache_access_ids(cb_cache* c, const uint32_t* d_ids, uint64_t n, uint64_t order_key,
+                        const cb_partition* pm, uint32_t part, const cb_features* backing,
+                        void* d_rows_out, uint64_t* kept, void* stream);
+/* Host id list (uploaded, then as cb_cache_access_ids without rows). */
+int cb_cache_access_host_ids(cb_cache* c, const uint32_t* ids, uint64_t n, uint64_t order_key,
+                             const cb_partition* pm, uint32_t part, uint64_t* kept);
+/* Same, over the input vertices of part `part` of the plan's last batch.
+ * backing != NULL and d_rows_out == NULL: the rows land in the plan's row
+ * buffer (cb_download_rows), which needs pm == NULL. */
+int cb_cache_access_plan(cb_cache* c, cb_plan* plan, uint32_t part, uint64_t order_key,
+                         const cb_partition* pm, uint32_t owner_part,
+                         const cb_features* backing, void* d_rows_out, uint64_t* kept);
+int cb_cache_stats(const cb_cache* c, uint64_t* hits, uint64_t* misses, uint64_t* size);
+int cb_cache_reset_counters(cb_cache* c);
+/* LruCache::resident(): resident keys, most recent first. */
+int cb_cache_resident(cb_cache* c, uint32_t* out, uint64_t cap_out, uint64_t* n);
+int cb_cache_storage(const cb_cache* c, const void** d_rows);
+
+/* stack_fingerprint (cache.cpp:123-133) of part `part` of the last batch. */
+int cb_stack_fingerprint(cb_plan* plan, uint32_t part, uint64_t* out);
+/* run_dependent_experiment's fixed training order (cache.cpp:155-162). */
+int cb_shuffled_order(uint64_t n, uint64_t seed, uint32_t* out);
+/* Feature storage tier: 1 = pinned host memory mapped into the device
+ * (the paper's storage channel), 0 = HBM. */
+int cb_features_set_tier(cb_features* f, int host);
+/* Device pointer + count of the input vertices of part `part`. */
+int cb_plan_input_ids(cb_plan* plan, uint32_t part, const uint32_t** d_ids, uint64_t* n);
 
 #ifdef __cplusplus
 }

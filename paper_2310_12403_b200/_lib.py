@@ -75,6 +75,22 @@ _SIGS = {
                                         C.POINTER(C.c_int)]),
     "cb_plan_trace": (C.c_int, [_P, _P, _u64]),
     "cb_plan_launch_count": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_u64)]),
+    "cb_cache_create": (C.c_int, [C.c_int, _u64, _u64, _u64, _PP]),
+    "cb_cache_destroy": (None, [_P]),
+    "cb_cache_access_trace": (C.c_int, [_P, _P, _u64, _P]),
+    "cb_cache_access_ids": (C.c_int, [_P, _P, _u64, _u64, _P, _u32, _P, _P,
+                                      C.POINTER(_u64), _P]),
+    "cb_cache_access_plan": (C.c_int, [_P, _P, _u32, _u64, _P, _u32, _P, _P,
+                                       C.POINTER(_u64)]),
+    "cb_cache_access_host_ids": (C.c_int, [_P, _P, _u64, _u64, _P, _u32, C.POINTER(_u64)]),
+    "cb_cache_stats": (C.c_int, [_P, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
+    "cb_cache_reset_counters": (C.c_int, [_P]),
+    "cb_cache_resident": (C.c_int, [_P, _P, _u64, C.POINTER(_u64)]),
+    "cb_cache_storage": (C.c_int, [_P, _PP]),
+    "cb_stack_fingerprint": (C.c_int, [_P, _u32, C.POINTER(_u64)]),
+    "cb_shuffled_order": (C.c_int, [_u64, _u64, _P]),
+    "cb_features_set_tier": (C.c_int, [_P, C.c_int]),
+    "cb_plan_input_ids": (C.c_int, [_P, _u32, _PP, C.POINTER(_u64)]),
 }
 
 _lib = None

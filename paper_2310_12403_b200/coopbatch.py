@@ -244,6 +244,12 @@ class FeatureStore:
                                              seed, C.byref(h)))
         return cls(g, h, dim, dtype, pm)
 
+    def set_tier(self, host: bool):
+        """Move the table to pinned host memory mapped into the device (the
+        paper's storage channel: every row read crosses the host link) or back
+        to HBM. Rows and their layout are unchanged."""
+        _check(_lib.load().cb_features_set_tier(self._h, int(bool(host))))
+
     def __del__(self):
         if getattr(self, "_h", None):
             _lib.load().cb_features_destroy(self._h)

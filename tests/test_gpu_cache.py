@@ -1,0 +1,137 @@
+"""GPU: the device LRU feature cache (csrc/cache.cu) against the reference's
+LruCache (cache.cpp:8-32, compiled in oracle/_ref) and its restatement, key by
+key; feature_load_sim (cache.cpp:88-119) and run_dependent_experiment
+(cache.cpp:137-208) against the compiled reference, step by step
+(fingerprints, |S^L|, miss bytes, steady miss rate); rows served through the
+cache (hits from HBM slots, misses from the table / host tier) equal the
+oracle's rows."""
+import numpy as np
+import pytest
+
+import paper_2310_12403_b200 as cb
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_lru(cap):
+    return O.Lru(cap, impl="reference" if O.available("reference") else "restated")
+
+
+@pytest.mark.parametrize("cap,n,length,seed", [(1, 50, 400, 1), (7, 40, 3000, 2),
+                                               (100, 300, 20000, 3), (500, 300, 5000, 4),
+                                               (2000, 100000, 60000, 5)])
+def test_lru_trace_matches_reference(gpu, cap, n, length, seed):
+    rng = np.random.default_rng(seed)
+    # skewed keys: many repeats, long distinct runs, and re-references
+    keys = (rng.zipf(1.3, length) % n).astype(np.uint32)
+    c = cb.LruCache(cap, n)
+    got = c.access_trace(keys)
+    r = ref_lru(cap)
+    want = np.array([r.access(int(k)) for k in keys], np.uint8)
+    assert np.array_equal(got, want)
+    assert c.misses() == int(want.sum()) and c.hits() == length - int(want.sum())
+    # resident set, most recent first
+    seen, res = set(), []
+    for k in keys[::-1]:
+        if int(k) not in seen:
+            seen.add(int(k))
+            res.append(int(k))
+    assert c.resident().tolist() == res[:cap]
+    assert c.size() == min(cap, len(seen))
+
+
+def test_lru_time_compaction(gpu):
+    """Enough accesses to wrap the time bitmap several times."""
+    n, cap = 64, 20
+    rng = np.random.default_rng(9)
+    c = cb.LruCache(cap, n)
+    r = ref_lru(cap)
+    for _ in range(30):
+        keys = rng.permutation(n)[: rng.integers(1, n)].astype(np.uint32)
+        got = c.access_trace(keys)
+        want = np.array([r.access(int(k)) for k in keys], np.uint8)
+        assert np.array_equal(got, want)
+
+
+def test_lru_capacity_zero_rejected(gpu):
+    with pytest.raises(cb.InputError):
+        cb.LruCache(0, 10)
+
+
+@pytest.fixture(scope="module")
+def small(gpu):
+    n, m, seed = 1 << 12, 1 << 15, 77
+    return cb.Graph.generate_rmat(n, m, seed), O.rmat(n, m, seed)
+
+
+@pytest.mark.parametrize("coop", [False, True])
+def test_feature_load_sim_matches_restated(small, coop):
+    g, ref = small
+    P, L, b = 4, 2, 64
+    pm = cb.partition_random(g, P, 3)
+    owner = O.partition_random(ref.n, P, 3)
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, 5)
+    steps, sched = [], cb.SeedSchedule.make(1, 5)
+    for s in range(6):
+        seeds = O.draw_coop_seeds(owner, P, b, 5, s)
+        steps.append([cb.expand(g, seeds[p], L, cfg, sched) for p in range(P)])
+        sched = cb.schedule_advance(sched)
+    caches = [cb.LruCache(150, ref.n) for _ in range(P)]
+    stats = cb.feature_load_sim(steps, caches, pm if coop else None, 16, 4)
+    for p in range(P):
+        lru = ref_lru(150)
+        acc = miss = 0
+        for si, step in enumerate(steps, start=1):
+            for v in O.access_order(step[p].input_vertices(), O.hash_bits(si, [p])):
+                if coop and owner[v] != p:
+                    continue
+                acc += 1
+                miss += lru.access(int(v))
+        assert (stats[p].accesses, stats[p].misses) == (acc, miss), p
+        assert stats[p].bytes == miss * 16 * 4
+
+
+@pytest.mark.parametrize("mode,kappa", [(cb.BatchMode.kSmoothed, 4), (cb.BatchMode.kNested, 4),
+                                        (cb.BatchMode.kIndependent, 1),
+                                        (cb.BatchMode.kSmoothed, cb.KAPPA_INFINITY)])
+def test_dependent_experiment_matches_reference(small, mode, kappa):
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    g, ref = small
+    steps, cap, b, L, dim, bps, seed = 24, 600, 128, 2, 32, 2, 11
+    got = cb.run_dependent_experiment(g, cb.MinibatchSchedule(mode, kappa, b), steps, cap,
+                                      cb.SamplerConfig(cb.SamplerKind.kLabor0, 5), L, dim, bps,
+                                      seed)
+    want = O.dependent_experiment(ref, int(mode), kappa, b, steps, cap, O.LABOR0, 5, L, dim,
+                                  bps, seed)
+    assert [r.fingerprint for r in got.rows] == want["fingerprint"].tolist()
+    assert [r.s_l for r in got.rows] == want["s_l"].tolist()
+    assert [r.bytes for r in got.rows] == want["bytes"].tolist()
+    assert got.steady_miss_rate == pytest.approx(want["steady"], abs=0, rel=0)
+
+
+@pytest.mark.parametrize("host_tier", [False, True])
+def test_cached_rows_match_oracle(small, host_tier):
+    """Rows through the cache (hits from HBM slots, misses from the table)
+    equal FeatureStore::load_rows at every step, with evictions."""
+    g, ref = small
+    dim, fseed = 24, 13
+    store = cb.FeatureStore.synth(g, dim, fseed, "f32")
+    if host_tier:
+        store.set_tier(True)
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, 5)
+    sizes = []
+
+    def check(step, plan):
+        ids = plan.block(0, 1).src_vertices
+        sizes.append(len(ids))
+        assert np.array_equal(plan.rows(0, store), O.feature_rows(fseed, dim, "f32", ids)), step
+
+    res = cb.run_dependent_experiment(g, cb.MinibatchSchedule(cb.BatchMode.kSmoothed, 4, 96), 16,
+                                      300, cfg, 2, dim, 4, 3, fingerprints=False, store=store,
+                                      on_step=check)
+    assert len(sizes) == 16 and max(sizes) > 300  # more rows than slots: evictions happen
+    assert 0.0 < res.steady_miss_rate < 1.0
+    if host_tier:
+        store.set_tier(False)
