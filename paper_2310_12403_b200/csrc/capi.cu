@@ -80,6 +80,16 @@ uint64_t sat_mul(uint64_t a, uint64_t b) {
 
 }  // namespace
 
+namespace cb {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CB_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+}  // namespace cb
+
 // ------------------------------------------------------------------ handles --
 struct cb_graph {
   DeviceGraph g;
@@ -282,7 +292,6 @@ void plan_alloc(cb_plan* pl) {
     w.sync.overflow = pl->mem.alloc<unsigned>(1);
     w.sync.barrier = pl->mem.alloc<unsigned>(1);
     w.sync.keep_words = pl->mem.alloc<uint32_t>(max_tiles * kLaborTile / 32 + 1);
-    w.sync.word_rec = pl->mem.alloc<uint32_t>(max_tiles * kLaborTile / 32 + 1);
     w.sync.status_a = pl->mem.alloc<unsigned long long>(max_tiles);
     w.sync.status_b = pl->mem.alloc<unsigned long long>(max_tiles);
     w.sync.status_c = pl->mem.alloc<unsigned long long>(max_tiles);
@@ -291,6 +300,12 @@ void plan_alloc(cb_plan* pl) {
     CB_CUDA(cudaMemset(w.sync.status_b, 0, max_tiles * 8));
     CB_CUDA(cudaMemset(w.sync.status_c, 0, max_tiles * 8));
   }
+  // kept-edge stage: parts run one after another on the plan stream, so one
+  // buffer (the largest scan space) serves all of them
+  uint64_t stage_tiles = 0;
+  for (const PeWork& w : pl->pe) stage_tiles = std::max(stage_tiles, w.sync.max_tiles);
+  uint2* stage = pl->mem.alloc<uint2>(stage_tiles * kLaborTile + 32);
+  for (PeWork& w : pl->pe) w.sync.stage = stage;
   pl->meta = pl->mem.alloc<LayerMeta>(static_cast<uint64_t>(P) * (L + 1));
   CB_CUDA(cudaMemset(pl->meta, 0, sizeof(LayerMeta) * P * (L + 1)));
   pl->send_counts = pl->mem.alloc<unsigned long long>(static_cast<uint64_t>(L) * P * P);
@@ -499,7 +514,7 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
   la.edges = b.edges;
   la.slots = b.slots;
   la.keep_words = w.sync.keep_words;
-  la.word_rec = w.sync.word_rec;
+  la.stage = w.sync.stage;
   la.cap_edges = b.cap_edges;
   la.ticket = w.sync.tickets + 3 * l + 1;
   la.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l + 1;

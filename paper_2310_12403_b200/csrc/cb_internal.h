@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "cb_device.cuh"
@@ -40,6 +41,26 @@ inline void cuda_check(cudaError_t e, const char* what) {
 
 inline void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(kInput, msg);
+}
+
+// Kernel launch with programmatic stream serialisation (PDL), so the next
+// kernel's launch and prologue overlap this one's tail; every kernel launched
+// this way starts with cbdev::pdl_begin(). CB_PDL=0 disables it.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, unsigned block, cudaStream_t st,
+              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
 }
 
 // ---------------------------------------------------------------- graph ----
@@ -86,7 +107,7 @@ struct Sync {
   unsigned* overflow = nullptr;               // [1]
   unsigned* barrier = nullptr;                // [1] fused-kernel grid barrier
   uint32_t* keep_words = nullptr;             // [max_tiles*kLaborTile/32]
-  uint32_t* word_rec = nullptr;               // [max_tiles*kLaborTile/32]
+  uint2* stage = nullptr;                     // [max_tiles*kLaborTile] kept edges by position
   uint64_t max_tiles = 0;
   static constexpr int kMaxTickets = 256;
 };
@@ -164,7 +185,7 @@ struct LaborArgs {
   uint2* edges;
   uint32_t* slots;
   uint32_t* keep_words;  // 1 bit per scan position (labor_mark -> labor_emit)
-  uint32_t* word_rec;    // record holding the first position of each keep word
+  uint2* stage;          // (t, dst index) of each kept scan position
   uint64_t cap_edges;
   unsigned* ticket;
   unsigned* exit_ctr;

@@ -18,6 +18,7 @@ namespace {
 
 __global__ void route_kernel(PartPtrs pp, const uint32_t* __restrict__ owner, uint32_t P,
                              unsigned long long* send_counts) {
+  pdl_begin();
   __shared__ unsigned long long hist[kMaxParts];
   const uint32_t p = blockIdx.y;
   for (uint32_t q = threadIdx.x; q < P; q += blockDim.x) hist[q] = 0;
@@ -45,6 +46,7 @@ __global__ void route_kernel(PartPtrs pp, const uint32_t* __restrict__ owner, ui
 }
 
 __global__ void locate_kernel(PartPtrs pp, const uint32_t* __restrict__ owner) {
+  pdl_begin();
   const uint32_t p = blockIdx.y;
   const uint64_t n = *pp.count[p];
   const uint32_t* src = pp.src[p];
@@ -64,14 +66,14 @@ __global__ void locate_kernel(PartPtrs pp, const uint32_t* __restrict__ owner) {
 void launch_route(const PartPtrs& pp, const uint32_t* owner, uint32_t P,
                   unsigned long long* send_counts, uint64_t max_src, cudaStream_t st) {
   dim3 grid(static_cast<unsigned>(grid_for(max_src, 256, 8) / P + 1), P);
-  route_kernel<<<grid, 256, 0, st>>>(pp, owner, P, send_counts);
+  launch_k(route_kernel, grid, 256, st, pp, owner, P, send_counts);
   CB_LAUNCH("route");
 }
 
 void launch_locate(const PartPtrs& pp, const uint32_t* owner, uint32_t P, uint64_t max_src,
                    cudaStream_t st) {
   dim3 grid(static_cast<unsigned>(grid_for(max_src, 256, 8) / P + 1), P);
-  locate_kernel<<<grid, 256, 0, st>>>(pp, owner);
+  launch_k(locate_kernel, grid, 256, st, pp, owner);
   CB_LAUNCH("locate");
 }
 

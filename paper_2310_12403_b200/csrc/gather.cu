@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(256) gather_kernel(
     const V* __restrict__ table, const uint32_t* __restrict__ ids,
     const unsigned long long* __restrict__ count, uint64_t cap_rows,
     const uint32_t* __restrict__ row_map, uint32_t vpr, V* __restrict__ out) {
+  pdl_begin();
   gbody::gather_body<V, UNROLL>(table, ids, count, cap_rows, row_map, vpr, out, blockIdx.x,
                                 gridDim.x);
 }
@@ -58,22 +59,22 @@ void launch_gather(const void* table, int vec_bytes, uint64_t row_bytes, const u
   const int grid = kNumSMs * 8;
   switch (vec_bytes) {
     case 16:
-      gather_kernel<uint4, 4><<<grid, 256, 0, st>>>(static_cast<const uint4*>(table), ids,
+      launch_k(gather_kernel<uint4, 4>, grid, 256, st, static_cast<const uint4*>(table), ids,
                                                    count, cap_rows, row_map, vpr,
                                                    static_cast<uint4*>(out));
       break;
     case 8:
-      gather_kernel<uint2, 4><<<grid, 256, 0, st>>>(static_cast<const uint2*>(table), ids,
+      launch_k(gather_kernel<uint2, 4>, grid, 256, st, static_cast<const uint2*>(table), ids,
                                                    count, cap_rows, row_map, vpr,
                                                    static_cast<uint2*>(out));
       break;
     case 4:
-      gather_kernel<uint32_t, 4><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(table),
+      launch_k(gather_kernel<uint32_t, 4>, grid, 256, st, static_cast<const uint32_t*>(table),
                                                        ids, count, cap_rows, row_map, vpr,
                                                        static_cast<uint32_t*>(out));
       break;
     default:
-      gather_kernel<unsigned short, 4><<<grid, 256, 0, st>>>(
+      launch_k(gather_kernel<unsigned short, 4>, grid, 256, st, 
           static_cast<const unsigned short*>(table), ids, count, cap_rows, row_map, vpr,
           static_cast<unsigned short*>(out));
   }

@@ -101,6 +101,7 @@ __global__ void batch_begin_kernel(unsigned* epoch, unsigned* overflow, unsigned
                                    const uint32_t* __restrict__ clear_list,
                                    const unsigned long long* clear_count, uint64_t cap,
                                    uint64_t nwords) {
+  pdl_begin();
   batch_begin_body(epoch, overflow, tickets, n_tickets, clear_bits, clear_summ, clear_list,
                    clear_count, cap, nwords, blockIdx.x, gridDim.x);
 }
@@ -252,6 +253,7 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
 
 template <int IPT>
 __global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelArgs r) {
+  pdl_begin();
   frontier_body<IPT>(a, r, blockIdx.x, gridDim.x);
 }
 
@@ -303,13 +305,15 @@ __device__ __forceinline__ bool keep_rule(const Variates& v, uint64_t p1, uint64
 // Per-warp body of labor_mark: IPT words of 32 consecutive positions starting
 // at tile-relative offset r0. Records come either from smem (STAGED) or
 // straight from the global record array (tiles spanning > kRecs records).
-// Lane j keeps word j's ballot and record; one coalesced store at the end.
+// Lane j keeps word j's ballot; one coalesced store at the end. Every kept
+// position also leaves its finished edge (t, dst index) in the stage array,
+// so the ordered emission is one load per edge.
 template <int IPT, bool SMOOTH, bool STAGED>
 __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v, uint64_t p1,
                                           uint64_t p2, uint64_t x0, uint32_t r0, uint32_t rend,
                                           uint32_t a0, uint32_t a1, uint32_t cur,
                                           const uint32_t* s_nxt, const uint32_t* const* s_row,
-                                          const unsigned long long* s_th,
+                                          const unsigned long long* s_th, const uint32_t* s_di,
                                           unsigned long long& uncert) {
   static_assert(IPT <= 32, "one word per lane");
   const uint32_t lane = lane_id();
@@ -325,12 +329,17 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
   auto th_of = [&](uint32_t c) -> uint64_t {
     return STAGED ? s_th[c] : __ldg(&a.act[a0 + c].b);
   };
-  uint32_t my_word = 0, my_rec = 0;
+  auto di_of = [&](uint32_t c) -> uint32_t {
+    return STAGED ? s_di[c] : __ldg(&a.act[a0 + c].di);
+  };
+  uint2* stage = a.stage + x0 + r0;
+  uint32_t my_word = 0;
   const uint32_t nxt0 = nxt_of(cur);
   if (nxt0 >= r0 + 32 * IPT && r0 + 32 * IPT <= rend) {
     // fast path: the whole span lies inside record `cur`
     const uint32_t* row = row_of(cur) + r0 + lane;
     const uint64_t th = th_of(cur);
+    const uint32_t di = di_of(cur);
     uint32_t tv[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) tv[j] = __ldg(row + j * 32);
@@ -339,9 +348,11 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
       const bool keep = keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert);
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == j) my_word = bal;
-      if (keep) set_bit(a.bits, a.summ, tv[j]);
+      if (keep) {
+        set_bit(a.bits, a.summ, tv[j]);
+        stage[j * 32 + lane] = make_uint2(tv[j], di);
+      }
     }
-    my_rec = a0 + cur;
   } else {
     uint32_t li[IPT];
     uint32_t tv[IPT];
@@ -362,19 +373,14 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
       const uint32_t r = r0 + j * 32 + lane;
       const bool keep = (r < rend) && keep_rule<SMOOTH>(v, p1, p2, tv[j], th_of(li[j]), uncert);
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      const uint32_t wrec = __shfl_sync(0xffffffffu, li[j], 0);
-      if (lane == j) {
-        my_word = bal;
-        my_rec = a0 + wrec;
+      if (lane == j) my_word = bal;
+      if (keep) {
+        set_bit(a.bits, a.summ, tv[j]);
+        stage[j * 32 + lane] = make_uint2(tv[j], di_of(li[j]));
       }
-      if (keep) set_bit(a.bits, a.summ, tv[j]);
     }
   }
-  if (lane < IPT && r0 + lane * 32 < rend) {
-    const uint64_t wi = ((x0 + r0) >> 5) + lane;
-    a.keep_words[wi] = my_word;
-    a.word_rec[wi] = my_rec;  // record of the word's first position
-  }
+  if (lane < IPT && r0 + lane * 32 < rend) a.keep_words[((x0 + r0) >> 5) + lane] = my_word;
 }
 
 template <int IPT, bool SMOOTH>
@@ -387,6 +393,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   __shared__ uint32_t s_nxt[kRecs];     // tile-relative start of the next record
   __shared__ const uint32_t* s_row[kRecs];
   __shared__ unsigned long long s_th[kRecs];
+  __shared__ uint32_t s_di[kRecs];
   LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
   const uint64_t n_act = meta->n_active;
@@ -412,6 +419,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
         s_pre[i] = rec.pre > x0 ? static_cast<uint32_t>(rec.pre - x0) : 0u;
         s_row[i] = a.indices + (rec.a + x0);
         s_th[i] = rec.b;
+        s_di[i] = rec.di;
         const uint64_t nx = (i + 1 < nd) ? a.act[a0 + i + 1].pre : ~0ULL;
         s_nxt[i] = static_cast<uint32_t>(min(nx - x0, static_cast<uint64_t>(0xffffffffu)));
       }
@@ -433,11 +441,11 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
         if (step == 1) break;
       }
       mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, s_nxt, s_row, s_th,
-                                   uncert);
+                                   s_di, uncert);
     } else {
       const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
       mark_span<IPT, SMOOTH, false>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, s_nxt, s_row,
-                                    s_th, uncert);
+                                    s_th, s_di, uncert);
     }
   }
   if (SMOOTH) {
@@ -450,6 +458,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
 
 template <int IPT, bool SMOOTH>
 __global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
+  pdl_begin();
   mark_body<IPT, SMOOTH>(a, blockIdx.x, gridDim.x);
 }
 
@@ -462,8 +471,8 @@ constexpr uint64_t kEmitBigLayerWords = 64 * 1024;
 
 // Ordered compaction of the keep words. The tile's kept items are spread
 // over all threads (item q -> its word by binary search over the per-word
-// output bases in smem), so every kept edge is an independent chain:
-// word_rec -> record -> neighbour id -> store.
+// output bases in smem); the edge itself was staged by labor_mark at its scan
+// position, so each kept edge is one load and one store.
 __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned role,
                                                 unsigned ncta) {
   __shared__ unsigned long long s_scan[kNT / 32 + 1];
@@ -501,18 +510,13 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned rol
     }
     const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
     // (tile_prefix ends with __syncthreads: s_word / s_wbase are visible)
-    constexpr int B = 4;  // kept items per thread in flight
+    constexpr int B = 8;  // kept items per thread in flight
     for (uint32_t q0 = threadIdx.x; q0 < tot; q0 += kNT * B) {
-      uint64_t x[B];
-      uint32_t ri[B];
-      bool ok[B];
+      uint2 e[B];
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         const uint32_t q = q0 + u * kNT;
-        ok[u] = q < tot;
-        x[u] = 0;
-        ri[u] = 0;
-        if (ok[u]) {
+        if (q < tot) {
           uint32_t lo = 0, hi = tw - 1;
           while (lo < hi) {
             const uint32_t mid = (lo + hi + 1) >> 1;
@@ -521,27 +525,13 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned rol
           }
           uint32_t word = s_word[lo];
           for (uint32_t r = q - s_wbase[lo]; r > 0; --r) word &= word - 1;
-          x[u] = (wt + lo) * 32 + (__ffs(word) - 1);
-          ri[u] = __ldg(&a.word_rec[wt + lo]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < B; ++u)
-        if (ok[u])
-          while (__ldg(&a.act[ri[u] + 1].pre) <= x[u]) ++ri[u];
-      uint32_t t[B], di[B];
-#pragma unroll
-      for (int u = 0; u < B; ++u) {
-        if (ok[u]) {
-          const ActRec rec = a.act[ri[u]];
-          di[u] = rec.di;
-          t[u] = __ldg(a.indices + rec.a + x[u]);
+          e[u] = __ldg(&a.stage[(wt + lo) * 32 + (__ffs(word) - 1)]);
         }
       }
 #pragma unroll
       for (int u = 0; u < B; ++u) {
         const unsigned long long pos = gb + q0 + u * kNT;
-        if (ok[u] && pos < a.cap_edges) a.edges[pos] = make_uint2(t[u], di[u]);
+        if (q0 + u * kNT < tot && pos < a.cap_edges) a.edges[pos] = e[u];
       }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
@@ -558,6 +548,7 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned rol
 // position is an independent atomicMax, so hub rows split across CTAs.
 template <int IPT, bool SMOOTH>
 __global__ void __launch_bounds__(kNT) ns_reservoir_kernel(LaborArgs a) {
+  pdl_begin();
   constexpr int TILE = kNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
   LayerMeta* meta = a.meta;
@@ -614,6 +605,7 @@ __global__ void __launch_bounds__(kNT) ns_emit_kernel(
     const uint64_t* __restrict__ out_prefix, const uint64_t* __restrict__ indptr,
     const uint32_t* __restrict__ indices, uint32_t k, const uint32_t* __restrict__ slots,
     uint32_t* bits, uint32_t* summ, uint2* edges, uint64_t cap_edges) {
+  pdl_begin();
   __shared__ uint64_t s_op[kEmitDst + 1];
   __shared__ uint64_t s_rs[kEmitDst];
   __shared__ uint32_t s_d[kEmitDst];
@@ -787,18 +779,21 @@ __device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned role
 }
 
 __global__ void __launch_bounds__(kNT) extract_kernel(ExtractArgs a) {
+  pdl_begin();
   extract_body(a, blockIdx.x, gridDim.x);
 }
 
 // Extract (dedup of the layer) and the ordered LABOR edge emission only
 // depend on labor_mark, not on each other: one launch, CTAs split by role.
 __global__ void __launch_bounds__(kNT) post_kernel(ExtractArgs e, LaborArgs a, unsigned n_ext) {
+  pdl_begin();
   if (blockIdx.x < n_ext) extract_body(e, blockIdx.x, n_ext);
   else labor_emit_body(a, blockIdx.x - n_ext, gridDim.x - n_ext);
 }
 
 // ---------------------------------------------------------------- relabel --
 __global__ void relabel_kernel(RelabelArgs r) {
+  pdl_begin();
   relabel_range(r, blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
                 static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
@@ -807,6 +802,7 @@ __global__ void rank_kernel(const uint32_t* __restrict__ bits,
                             const uint32_t* __restrict__ wprefix,
                             const uint32_t* __restrict__ ids,
                             const unsigned long long* count, uint32_t* out) {
+  pdl_begin();
   const uint64_t n = *count;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -816,6 +812,7 @@ __global__ void rank_kernel(const uint32_t* __restrict__ bits,
 
 __global__ void clear_kernel(uint32_t* bits, uint32_t* summ, const uint32_t* __restrict__ list,
                              const unsigned long long* count) {
+  pdl_begin();
   const uint64_t n = *count;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -898,7 +895,7 @@ void launch_batch_begin(const Sync& s, uint32_t* clear_bits, uint32_t* clear_sum
                         const uint32_t* clear_list, const unsigned long long* clear_count,
                         uint64_t clear_cap, uint64_t nwords, cudaStream_t st) {
   const int grid = grid_for(clear_cap, 256, 4);
-  batch_begin_kernel<<<grid, 256, 0, st>>>(s.epoch, s.overflow, s.tickets, Sync::kMaxTickets,
+  launch_k(batch_begin_kernel, grid, 256, st, s.epoch, s.overflow, s.tickets, Sync::kMaxTickets,
                                            clear_bits, clear_summ, clear_list, clear_count,
                                            clear_cap, nwords);
   CB_LAUNCH("batch_begin");
@@ -909,14 +906,14 @@ void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_d
   const int occ = resident_per_sm(frontier_kernel<kFrontierIPT>);
   const int grid = std::max(grid_for(cap_dst, kNT * kFrontierIPT, occ),
                             r.edges ? grid_for(relabel_work, kNT * 4, occ) : 1);
-  frontier_kernel<kFrontierIPT><<<grid, kNT, 0, st>>>(a, r);
+  launch_k(frontier_kernel<kFrontierIPT>, grid, kNT, st, a, r);
   CB_LAUNCH("frontier");
 }
 
 void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStream_t st) {
   const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, 3);
-  if (smooth && a.kind != 0) labor_mark_kernel<kLaborIPT, true><<<grid, kNT, 0, st>>>(a);
-  else labor_mark_kernel<kLaborIPT, false><<<grid, kNT, 0, st>>>(a);
+  if (smooth && a.kind != 0) launch_k(labor_mark_kernel<kLaborIPT, true>, grid, kNT, st, a);
+  else launch_k(labor_mark_kernel<kLaborIPT, false>, grid, kNT, st, a);
   CB_LAUNCH("labor_mark");
 }
 
@@ -929,31 +926,31 @@ void launch_labor_post(const LaborArgs& a, uint64_t max_tiles, const ExtractArgs
   const int cap = occ * kNumSMs;
   const int g_ext = std::min(grid_for(extract_tiles(e.words_padded), 1, occ), cap / 2);
   const int g_emit = std::min(grid_for(words, kEmitTileWords, occ), cap - g_ext);
-  post_kernel<<<g_emit + g_ext, kNT, 0, st>>>(e, a, static_cast<unsigned>(g_ext));
+  launch_k(post_kernel, g_emit + g_ext, kNT, st, e, a, static_cast<unsigned>(g_ext));
   CB_LAUNCH("post");
 }
 
 void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix,
                const uint64_t* indptr, const uint32_t* indices, uint64_t cap_dst, bool smooth,
                cudaStream_t st) {
-  if (smooth) ns_reservoir_kernel<kLaborIPT, true><<<kNumSMs * 8, kNT, 0, st>>>(a);
-  else ns_reservoir_kernel<kLaborIPT, false><<<kNumSMs * 8, kNT, 0, st>>>(a);
+  if (smooth) launch_k(ns_reservoir_kernel<kLaborIPT, true>, kNumSMs * 8, kNT, st, a);
+  else launch_k(ns_reservoir_kernel<kLaborIPT, false>, kNumSMs * 8, kNT, st, a);
   CB_LAUNCH("ns_reservoir");
   const int grid = grid_for(cap_dst, kEmitDst, 8);
-  ns_emit_kernel<<<grid, kNT, 0, st>>>(D, a.meta, out_prefix, indptr, indices, a.k, a.slots,
+  launch_k(ns_emit_kernel, grid, kNT, st, D, a.meta, out_prefix, indptr, indices, a.k, a.slots,
                                        a.bits, a.summ, a.edges, a.cap_edges);
   CB_LAUNCH("ns_emit");
 }
 
 void launch_extract(const ExtractArgs& a, cudaStream_t st) {
   const int grid = grid_for(extract_tiles(a.words_padded), 1, resident_per_sm(extract_kernel));
-  extract_kernel<<<grid, kNT, 0, st>>>(a);
+  launch_k(extract_kernel, grid, kNT, st, a);
   CB_LAUNCH("extract");
 }
 
 void launch_relabel(const RelabelArgs& r, uint64_t work, cudaStream_t st) {
   const int grid = grid_for(work, 256 * 4, 8);
-  relabel_kernel<<<grid, 256, 0, st>>>(r);
+  launch_k(relabel_kernel, grid, 256, st, r);
   CB_LAUNCH("relabel");
 }
 
@@ -972,13 +969,13 @@ void launch_fused(FusedParams& p, bool smooth, cudaStream_t st) {
 
 void launch_rank(const Bitmap& bm, const uint32_t* ids, const unsigned long long* count,
                  uint32_t* rank_out, cudaStream_t st) {
-  rank_kernel<<<kNumSMs * 4, 256, 0, st>>>(bm.bits, bm.wprefix, ids, count, rank_out);
+  launch_k(rank_kernel, kNumSMs * 4, 256, st, bm.bits, bm.wprefix, ids, count, rank_out);
   CB_LAUNCH("rank");
 }
 
 void launch_clear(Bitmap& bm, const uint32_t* list, const unsigned long long* count,
                   cudaStream_t st) {
-  clear_kernel<<<kNumSMs * 4, 256, 0, st>>>(bm.bits, bm.summ, list, count);
+  launch_k(clear_kernel, kNumSMs * 4, 256, st, bm.bits, bm.summ, list, count);
   CB_LAUNCH("clear");
 }
 
