@@ -213,11 +213,14 @@ __device__ __forceinline__ unsigned long long mkstat(unsigned epoch, unsigned lo
 // exclusive prefix of the tile in tile order. Warp 0 looks back over W*32
 // predecessors per step (lane l reads tiles base - l*W - j), so the
 // inclusive-prefix front advances W*32 tiles per L2 round trip.
+// tile_prefix_async: the same look-back run by warp `warp` only, result in
+// *s_bcast, no barrier (several independent scans of one tile can look back
+// concurrently in different warps; the caller syncs once).
 template <int W = 4>
-__device__ inline unsigned long long tile_prefix(unsigned long long* status, unsigned tile,
-                                                 unsigned long long agg, unsigned epoch,
-                                                 unsigned long long* s_bcast) {
-  if (threadIdx.x < 32) {
+__device__ inline void tile_prefix_async(unsigned long long* status, unsigned tile,
+                                         unsigned long long agg, unsigned epoch,
+                                         unsigned long long* s_bcast, unsigned warp) {
+  if ((threadIdx.x >> 5) == warp) {
     const unsigned long long want = static_cast<unsigned long long>(epoch & 0xffffffu);
     if (tile == 0) {
       if (lane_id() == 0) {
@@ -276,6 +279,13 @@ __device__ inline unsigned long long tile_prefix(unsigned long long* status, uns
       }
     }
   }
+}
+
+template <int W = 4>
+__device__ inline unsigned long long tile_prefix(unsigned long long* status, unsigned tile,
+                                                 unsigned long long agg, unsigned epoch,
+                                                 unsigned long long* s_bcast) {
+  tile_prefix_async<W>(status, tile, agg, epoch, s_bcast, 0);
   __syncthreads();
   return *s_bcast;
 }

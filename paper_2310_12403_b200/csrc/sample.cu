@@ -31,6 +31,9 @@ using namespace cbdev;
 namespace {
 
 constexpr int kNT = 256;
+// labor_mark residency: 4 CTAs/SM so one CTA's staging barrier overlaps
+// another's hashing
+constexpr int kMarkCtasPerSM = 4;
 
 __device__ __forceinline__ unsigned inv_epoch(const unsigned* ep, int slot) {
   return ((*ep & 0x3ffffu) << 6) | static_cast<unsigned>(slot);
@@ -174,12 +177,14 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
     unsigned long long ea = block_exclusive_scan<kNT>(as, s_scan[1], ta);
     unsigned long long eo = 0;
     if (is_ns) eo = block_exclusive_scan<kNT>(os, s_scan[2], to);
-    const unsigned long long bq =
-        tile_prefix<4>(a.st_a, tile, tq, inv_epoch(a.epoch, a.slot), &s_bc[0]);
-    const unsigned long long ba =
-        tile_prefix<4>(a.st_b, tile, ta, inv_epoch(a.epoch, a.slot + 1), &s_bc[1]);
-    unsigned long long bo = 0;
-    if (is_ns) bo = tile_prefix<4>(a.st_c, tile, to, inv_epoch(a.epoch, a.slot + 2), &s_bc[2]);
+    // the (two or three) look-backs run concurrently in warps 0, 1, 2
+    tile_prefix_async<4>(a.st_a, tile, tq, inv_epoch(a.epoch, a.slot), &s_bc[0], 0);
+    tile_prefix_async<4>(a.st_b, tile, ta, inv_epoch(a.epoch, a.slot + 1), &s_bc[1], 1);
+    if (is_ns)
+      tile_prefix_async<4>(a.st_c, tile, to, inv_epoch(a.epoch, a.slot + 2), &s_bc[2], 2);
+    __syncthreads();
+    const unsigned long long bq = s_bc[0], ba = s_bc[1];
+    const unsigned long long bo = is_ns ? s_bc[2] : 0ULL;
     if (tile == role) tstamp(a.trace, role, 3);
     eq += bq;
     ea += ba;
@@ -457,7 +462,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
 }
 
 template <int IPT, bool SMOOTH>
-__global__ void __launch_bounds__(kNT, 3) labor_mark_kernel(LaborArgs a) {
+__global__ void __launch_bounds__(kNT, kMarkCtasPerSM) labor_mark_kernel(LaborArgs a) {
   pdl_begin();
   mark_body<IPT, SMOOTH>(a, blockIdx.x, gridDim.x);
 }
@@ -911,7 +916,7 @@ void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_d
 }
 
 void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStream_t st) {
-  const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, 3);
+  const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, kMarkCtasPerSM);
   if (smooth && a.kind != 0) launch_k(labor_mark_kernel<kLaborIPT, true>, grid, kNT, st, a);
   else launch_k(labor_mark_kernel<kLaborIPT, false>, grid, kNT, st, a);
   CB_LAUNCH("labor_mark");
