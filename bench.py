@@ -21,6 +21,7 @@ e2e    : wall clock through the public API with host (pinned) seeds: H2D of
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import subprocess
@@ -299,6 +300,105 @@ def kappa_evidence(cb, dev, steps_epochs=2, kappas=(1, 4, 16, 64, 256, None)):
     return out
 
 
+# ------------------------------------------------- our arm, N>1 cooperative --
+def run_ours_coop(args, cfg):
+    """One process per GPU, one part per rank: the cooperative step of
+    coop.cpp:68-106 with the per-layer owner exchange (build_exchange,
+    coop.cpp:25-64) and the feature fetch (all_to_all_forward, coop.cpp:
+    145-159) as torch.distributed all-to-allv over NCCL; per-part compute is
+    libcoopbatch_b200 (dist.CudaEngine). Each rank draws b seeds from the
+    vertices it owns (cli.cpp:210-214). Weak scaling: b seeds per GPU."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_12403_b200 as cb
+    from paper_2310_12403_b200 import _lib
+    from paper_2310_12403_b200.dist import CudaEngine, DistCoop, synth_shard
+    from paper_2310_12403_b200.seeds import draw_from_pool
+
+    rank, world, local = dist_env()
+    backend = args.dist_backend
+    dev = local if backend == "nccl" else 0
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+    else:
+        dist.init_process_group("gloo")
+    kind = {"labor0": cb.SamplerKind.kLabor0, "ns": cb.SamplerKind.kNs,
+            "full": cb.SamplerKind.kFull}[cfg["kind"]]
+    L, b = len(cfg["fanouts"]), cfg["batch"]
+    t0 = time.time()
+    g = cb.Graph.generate_rmat(cfg["n"], cfg["m"], GRAPH_SEED, device=dev)
+    gen_s = time.time() - t0
+    pm = cb.partition_random(g, world, RUN_SEED)
+    mine = pm.members()[rank]
+    store = synth_shard(g, pm, rank, cfg["dim"], FEAT_SEED, cfg["dtype"])
+    scfg = cb.SamplerConfig(kind, fanouts=cfg["fanouts"])
+    eng = CudaEngine(g, pm, rank, L, scfg, max_seeds=b, store=store,
+                     comm_device=None if backend == "nccl" else "cpu")
+    dc = DistCoop(eng)
+    W, K = args.warmup, args.steps
+    seeds_host = [draw_from_pool(mine, b, RUN_SEED, cb.hash_bits(s, [rank])) for s in range(W + K)]
+    seeds_dev = [eng.to_device(s) for s in seeds_host]
+    scheds = [cb.SeedSchedule.make(1, RUN_SEED)]
+    for _ in range(W + K):
+        scheds.append(cb.schedule_advance(scheds[-1]))
+
+    def step(i, seeds):
+        dc.sample(seeds, L, scheds[i], keep_blocks=False, records=False)
+        return dc.load_inputs(to_host=False)
+
+    for i in range(W):
+        step(i, seeds_dev[i])
+    lc = C.c_uint64()
+
+    def timed(seeds_of):
+        dist.barrier()
+        torch.cuda.synchronize()
+        _lib.load().cb_kernel_launches(C.byref(lc))
+        l0 = lc.value
+        t = time.perf_counter()
+        n_rows = 0
+        for i in range(W, W + K):
+            rows = step(i, seeds_of(i))
+            n_rows += rows.numel()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        _lib.load().cb_kernel_launches(C.byref(lc))
+        dist.barrier()
+        m = torch.tensor([dt], dtype=torch.float64)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        return float(m.item()), n_rows, lc.value - l0
+
+    clocks = ClockSampler(dev)
+    with clocks:
+        dt, row_bytes_total, launches = timed(lambda i: seeds_dev[i])
+    # e2e: host seeds (H2D inside), rows end on the device, one D2H of the
+    # owned-set size per step (the batch result the trainer reads)
+    e2e_dt, _, _ = timed(lambda i: seeds_host[i])
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    seeds_total = K * b * world
+    line = {
+        "metric": METRIC, "value": seeds_total / dt, "unit": "seeds/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (hash-keyed R-MAT, hashed features)",
+        "config": {"workload": cfg["workload"], "mode": f"cooperative (P={world}, one part per "
+                   f"GPU, {backend} all-to-allv per layer + feature all-to-allv)",
+                   "timing": "wall clock between barriers + device sync, max over ranks "
+                             "(host-orchestrated exchange)",
+                   "graph": {"vertices": cfg["n"], "edges": cfg["m"], "gen_s": round(gen_s, 2)}},
+        "feature_gbps": row_bytes_total / dt / 1e9,
+        "e2e": {"value": seeds_total / e2e_dt, "unit": "seeds/s", "h2d_bytes_per_step": b * 4,
+                "d2h_bytes_per_step": 8 * (1 + 2 * L)},
+        "gpu_launches": launches, "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 # -------------------------------------------------------------- our arm ----
 def run_ours(args, cfg):
     import torch
@@ -475,15 +575,22 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-evidence", action="store_true")
+    ap.add_argument("--mode", choices=["coop", "indep"], default="coop",
+                    help="N>1: cooperative minibatching (one part per GPU) or independent")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: ranks share cuda:0 with CPU-staged exchanges (testing)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    rank, world, _ = dist_env()
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif world > 1 and args.mode == "coop":
+        run_ours_coop(args, cfg)
+        return
     else:
         run_ours(args, cfg)
-    rank, world, _ = dist_env()
     if world > 1 and args.impl == "ours":
         import torch.distributed as dist
         dist.destroy_process_group()

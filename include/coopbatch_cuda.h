@@ -254,6 +254,9 @@ int cb_shuffled_order(uint64_t n, uint64_t seed, uint32_t* out);
 /* Feature storage tier: 1 = pinned host memory mapped into the device
  * (the paper's storage channel), 0 = HBM. */
 int cb_features_set_tier(cb_features* f, int host);
+/* Kernels of this library enqueued eagerly by this process so far (CUDA
+ * graph replays excluded; for reporting launch counts). */
+int cb_kernel_launches(uint64_t* n);
 /* Device pointer + count of the input vertices of part `part`. */
 int cb_plan_input_ids(cb_plan* plan, uint32_t part, const uint32_t** d_ids, uint64_t* n);
 

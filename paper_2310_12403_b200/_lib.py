@@ -90,6 +90,7 @@ _SIGS = {
     "cb_stack_fingerprint": (C.c_int, [_P, _u32, C.POINTER(_u64)]),
     "cb_shuffled_order": (C.c_int, [_u64, _u64, _P]),
     "cb_features_set_tier": (C.c_int, [_P, C.c_int]),
+    "cb_kernel_launches": (C.c_int, [C.POINTER(_u64)]),
     "cb_plan_input_ids": (C.c_int, [_P, _u32, _PP, C.POINTER(_u64)]),
 }
 

@@ -81,6 +81,7 @@ uint64_t sat_mul(uint64_t a, uint64_t b) {
 }  // namespace
 
 namespace cb {
+std::atomic<unsigned long long> g_kernel_launches{0};
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("CB_PDL");
@@ -1871,6 +1872,13 @@ int cb_features_set_tier(cb_features* f, int host) {
       f->table = f->hbm_table;
       f->hbm_table = nullptr;
     }
+  });
+}
+
+int cb_kernel_launches(uint64_t* n) {
+  return guard([&] {
+    require(n != nullptr, "null argument");
+    *n = g_kernel_launches.load();
   });
 }
 

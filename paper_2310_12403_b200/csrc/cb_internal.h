@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <atomic>
 #include <utility>
 #include <vector>
 
@@ -47,6 +48,8 @@ inline void require(bool ok, const std::string& msg) {
 // kernel's launch and prologue overlap this one's tail; every kernel launched
 // this way starts with cbdev::pdl_begin(). CB_PDL=0 disables it.
 bool pdl_enabled();
+// Kernels this process enqueued eagerly (graph replays not included).
+extern std::atomic<unsigned long long> g_kernel_launches;
 template <typename... KArgs, typename... Args>
 void launch_k(void (*kernel)(KArgs...), dim3 grid, unsigned block, cudaStream_t st,
               Args&&... args) {
@@ -61,6 +64,7 @@ void launch_k(void (*kernel)(KArgs...), dim3 grid, unsigned block, cudaStream_t 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 // ---------------------------------------------------------------- graph ----

@@ -119,6 +119,7 @@ void bucket_by_owner(const uint32_t* ids, uint64_t n, const uint32_t* owner, uin
   bucket_count_kernel<<<static_cast<unsigned>(ntiles), kBT, 0, st>>>(ids, n, owner, P,
                                                                      d_counts);
   CB_LAUNCH("bucket_count");
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   std::vector<uint32_t> h(ntiles * P);
   CB_CUDA(cudaMemcpyAsync(h.data(), d_counts, ntiles * P * 4, cudaMemcpyDeviceToHost, st));
   CB_CUDA(cudaStreamSynchronize(st));
@@ -139,6 +140,7 @@ void bucket_by_owner(const uint32_t* ids, uint64_t n, const uint32_t* owner, uin
   bucket_scatter_kernel<<<static_cast<unsigned>(ntiles), kBT, 0, st>>>(ids, n, owner, P, d_off,
                                                                        out, perm);
   CB_LAUNCH("bucket_scatter");
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   CB_CUDA(cudaFreeAsync(d_counts, st));
   CB_CUDA(cudaFreeAsync(d_off, st));
   CB_CUDA(cudaStreamSynchronize(st));
@@ -149,6 +151,7 @@ void scatter_u32(const uint32_t* in, const uint32_t* perm, uint64_t n, uint32_t*
   if (!n) return;
   scatter_u32_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(in, perm, n, out);
   CB_LAUNCH("scatter_u32");
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void scatter_rows(const void* in, const uint32_t* perm, uint64_t n, uint64_t row_bytes,
@@ -178,6 +181,7 @@ void scatter_rows(const void* in, const uint32_t* perm, uint64_t n, uint64_t row
           static_cast<unsigned short*>(out));
   }
   CB_LAUNCH("scatter_rows");
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void mark_ids(const uint32_t* ids, uint64_t n, uint32_t* bits, uint32_t* summ,
@@ -185,6 +189,7 @@ void mark_ids(const uint32_t* ids, uint64_t n, uint32_t* bits, uint32_t* summ,
   if (!n) return;
   mark_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(ids, n, bits, summ);
   CB_LAUNCH("mark");
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 }  // namespace cb

@@ -70,11 +70,17 @@ class DistCoop:
         dist.all_to_all_single(recv, send, group=self.group)
         return recv.tolist()
 
-    def sample(self, seeds: np.ndarray, num_layers: int, schedule: SeedSchedule,
-               keep_blocks: bool = True) -> DistSample:
+    def sample(self, seeds, num_layers: int, schedule: SeedSchedule,
+               keep_blocks: bool = True, records: bool = True) -> DistSample:
+        """One cooperative step. `seeds` is a host array or a device tensor
+        (int32 view of u32 ids). records=False keeps the exchange on the
+        device only (no host ExchangeRecord / owner set), for timing."""
         out = DistSample()
-        D = self.e.to_device(np.ascontiguousarray(seeds, dtype=np.uint32))
-        n_d = len(seeds)
+        if isinstance(seeds, torch.Tensor):
+            D, n_d = seeds, seeds.numel()
+        else:
+            D = self.e.to_device(np.ascontiguousarray(seeds, dtype=np.uint32))
+            n_d = len(seeds)
         for l in range(num_layers):
             src, n_src = self.e.sample_layer(l, D, n_d, schedule)
             bucketed, perm, counts = self.e.bucket(src, n_src)
@@ -85,27 +91,31 @@ class DistCoop:
             back = self.e.empty_ids(sum(counts))
             self._a2a(_i32(back), _i32(ranks), counts, rcounts)
             loc_row = self.e.scatter(back, perm, n_src)
-            part = np.repeat(np.arange(self.world, dtype=np.uint32), counts)
-            loc_part = np.zeros(n_src, np.uint32)
-            loc_part[self.e.to_host(perm, n_src)] = part
-            out.exchanges.append(DistExchange(l, counts, n_d, loc_part,
-                                              self.e.to_host(loc_row, n_src).astype(np.uint64)))
+            if records:
+                part = np.repeat(np.arange(self.world, dtype=np.uint32), counts)
+                loc_part = np.zeros(n_src, np.uint32)
+                loc_part[self.e.to_host(perm, n_src)] = part
+                out.exchanges.append(DistExchange(
+                    l, counts, n_d, loc_part, self.e.to_host(loc_row, n_src).astype(np.uint64)))
             if keep_blocks:
                 out.blocks.append(self.e.block(l))
             self._last = (recv, sum(rcounts), rcounts, perm, counts, n_src)
-        out.owner_set = self.e.to_host(D, n_d)
+        self.n_owned = n_d
+        if records:
+            out.owner_set = self.e.to_host(D, n_d)
         return out
 
-    def load_inputs(self) -> np.ndarray:
+    def load_inputs(self, to_host: bool = True):
         """Rows of this rank's input vertices (src of the last block), in src
         order: owner-side gather of the requested ids, all-to-allv back,
-        requester-side scatter (all_to_all_forward, coop.cpp:145-159)."""
+        requester-side scatter (all_to_all_forward, coop.cpp:145-159).
+        to_host=False returns the device tensor (bytes) instead."""
         recv, n_recv, rcounts, perm, counts, n_src = self._last
         rb = self.e.row_bytes
         rows = self.e.gather_rows(recv, n_recv)              # owner side, request order
         back = torch.empty(sum(counts) * rb, dtype=torch.uint8, device=self.e.comm_device)
         self._a2a(back, rows, [c * rb for c in counts], [c * rb for c in rcounts])
-        return self.e.scatter_rows(back, perm, n_src)
+        return self.e.scatter_rows(back, perm, n_src, to_host=to_host)
 
 
 class CudaEngine:
@@ -215,12 +225,14 @@ class CudaEngine:
                                      C.c_void_p(out.data_ptr()), None))
         return self._comm(out[: n * self.row_bytes])
 
-    def scatter_rows(self, rows, perm, n) -> np.ndarray:
+    def scatter_rows(self, rows, perm, n, to_host: bool = True):
         rows = self._dev(rows)
         out = torch.empty(max(n, 1) * self.row_bytes, dtype=torch.uint8, device=self.device)
         _check(self.L.cb_scatter_rows(self._h, C.c_void_p(rows.data_ptr()),
                                       C.c_void_p(perm.data_ptr()), n, self.row_bytes,
                                       C.c_void_p(out.data_ptr())))
+        if not to_host:
+            return out[: n * self.row_bytes]
         dt = _DT[self.store.dtype][1]
         return out[: n * self.row_bytes].cpu().numpy().view(dt).reshape(n, self.store.dim)
 

@@ -76,7 +76,7 @@ class OracleEngine:
         rows = O.feature_rows(self.feat_seed, self.dim, self.dtype, self.to_host(ids, n))
         return torch.from_numpy(rows.view(np.uint8).reshape(-1).copy())
 
-    def scatter_rows(self, rows, perm, n):
+    def scatter_rows(self, rows, perm, n, to_host=True):
         dt = O.DTYPES[self.dtype][1]
         r = rows.numpy().view(dt).reshape(-1, self.dim)
         out = np.zeros((n, self.dim), dt)
