@@ -188,6 +188,7 @@ struct cb_plan {
   bool have_rows = false;
   uint64_t batches = 0;
   uint64_t launches = 0;  // kernels enqueued by the last cb_sample (+ cb_gather)
+  double* vtab = nullptr;  // smoothed LABOR r_t table [n] (nullptr: per position)
   std::vector<uint64_t> seeds_off;
   // CUDA graphs of one batch (sample) and its gather, replayed per step
   cudaGraphExec_t exec_sample = nullptr;
@@ -307,6 +308,8 @@ void plan_alloc(cb_plan* pl) {
   for (const PeWork& w : pl->pe) stage_tiles = std::max(stage_tiles, w.sync.max_tiles);
   uint2* stage = pl->mem.alloc<uint2>(stage_tiles * kLaborTile + 32);
   for (PeWork& w : pl->pe) w.sync.stage = stage;
+  // smoothed LABOR variate table (shared by the parts like the stage)
+  pl->vtab = (pl->kind == CB_LABOR0 && n <= kVtabMaxVerts) ? pl->mem.alloc<double>(n) : nullptr;
   pl->meta = pl->mem.alloc<LayerMeta>(static_cast<uint64_t>(P) * (L + 1));
   CB_CUDA(cudaMemset(pl->meta, 0, sizeof(LayerMeta) * P * (L + 1)));
   pl->send_counts = pl->mem.alloc<unsigned long long>(static_cast<uint64_t>(L) * P * P);
@@ -516,6 +519,8 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
   la.slots = b.slots;
   la.keep_words = w.sync.keep_words;
   la.stage = w.sync.stage;
+  la.vtab = pl->vtab;
+  la.n_vert = pl->g->g.n;
   la.cap_edges = b.cap_edges;
   la.ticket = w.sync.tickets + 3 * l + 1;
   la.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l + 1;
@@ -550,7 +555,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   prof_mark(pl);
   launch_labor_post(la, w.sync.max_tiles, ex, st);  // emit || extract
   prof_mark(pl);
-  return 3;
+  return (smooth && pl->kind == CB_LABOR0 && pl->vtab) ? 4 : 3;  // (+ variate table)
 }
 
 // The per-batch launch sequence. d_seeds: P seed lists back to back (device).

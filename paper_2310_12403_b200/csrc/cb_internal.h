@@ -190,6 +190,8 @@ struct LaborArgs {
   uint32_t* slots;
   uint32_t* keep_words;  // 1 bit per scan position (labor_mark -> labor_emit)
   uint2* stage;          // (t, dst index) of each kept scan position
+  double* vtab;          // smoothed r_t per vertex (nullptr: evaluate per position)
+  uint64_t n_vert;
   uint64_t cap_edges;
   unsigned* ticket;
   unsigned* exit_ctr;
@@ -267,6 +269,7 @@ struct FusedParams {
 constexpr int kExtractTileWords = 2048;  // bitmap padding granule (max tile)
 constexpr uint64_t kExtractBigWords = 256 * 1024;  // summary-mode threshold
 constexpr int kLaborTile = 4096;
+constexpr uint64_t kVtabMaxVerts = 1ULL << 26;  // smoothed variate table cap (512 MiB)
 constexpr int kFrontierTile = 1024;
 
 // ----------------------------------------------------- kernel launchers ----

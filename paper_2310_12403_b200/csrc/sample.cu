@@ -296,13 +296,34 @@ __device__ __forceinline__ void tile_records(const ActRec* act, const uint32_t* 
 //                grouped by dst, CSR order inside a dst (the reference order)
 // Keep decision for neighbour t under threshold th (frontier ActRec.b). Plain
 // stream: th = ~0 (keep all) needs no special case since (h>>11) < 2^53.
+// The layer's smoothed variate table r_t = finish(hash(z1,{2,l,t}),
+// hash(z2,{2,l,t})) for every vertex, built when the scan space is at least
+// twice the vertex count (each r_t then serves >= 2 positions on average).
+__device__ __forceinline__ bool vtab_used(const LaborArgs& a, uint64_t scan_total) {
+  return a.vtab != nullptr && scan_total >= 2 * a.n_vert;
+}
+
+__global__ void __launch_bounds__(kNT) vtab_kernel(LaborArgs a) {
+  pdl_begin();
+  if (!vtab_used(a, a.meta->scan_total)) return;
+  const Variates v = *a.var;
+  const uint64_t p1 = hstep(hstep(hinit(v.z1), 2ULL), static_cast<uint64_t>(a.layer));
+  const uint64_t p2 = hstep(hstep(hinit(v.z2), 2ULL), static_cast<uint64_t>(a.layer));
+  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < a.n_vert;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    a.vtab[t] = smooth_finish(v, hstep(p1, t), hstep(p2, t));
+}
+
+// Smoothed stream: r_t from the layer's variate table when one was built
+// (samplers.cpp:114-129 memoises r_t per t the same way), else evaluated.
 template <bool SMOOTH>
 __device__ __forceinline__ bool keep_rule(const Variates& v, uint64_t p1, uint64_t p2,
-                                          uint32_t t, uint64_t th, unsigned long long& uncert) {
+                                          uint32_t t, uint64_t th, unsigned long long& uncert,
+                                          const double* vtab) {
   if (!SMOOTH) return (hstep(p1, t) >> 11) <= th;
   if (th == ~0ULL) return true;
   const double thr = __longlong_as_double(static_cast<long long>(th));
-  const double rr = smooth_finish(v, hstep(p1, t), hstep(p2, t));
+  const double rr = vtab ? __ldg(vtab + t) : smooth_finish(v, hstep(p1, t), hstep(p2, t));
   if (fabs(rr - thr) <= kGuard * thr) ++uncert;
   return rr <= thr;
 }
@@ -319,7 +340,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
                                           uint32_t a0, uint32_t a1, uint32_t cur,
                                           const uint32_t* s_nxt, const uint32_t* const* s_row,
                                           const unsigned long long* s_th, const uint32_t* s_di,
-                                          unsigned long long& uncert) {
+                                          unsigned long long& uncert, const double* vtab) {
   static_assert(IPT <= 32, "one word per lane");
   const uint32_t lane = lane_id();
   auto nxt_of = [&](uint32_t c) -> uint32_t {  // tile-relative start of record c+1
@@ -350,7 +371,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
     for (int j = 0; j < IPT; ++j) tv[j] = __ldg(row + j * 32);
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
-      const bool keep = keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert);
+      const bool keep = keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab);
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == j) my_word = bal;
       if (keep) {
@@ -376,7 +397,8 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const uint32_t r = r0 + j * 32 + lane;
-      const bool keep = (r < rend) && keep_rule<SMOOTH>(v, p1, p2, tv[j], th_of(li[j]), uncert);
+      const bool keep =
+          (r < rend) && keep_rule<SMOOTH>(v, p1, p2, tv[j], th_of(li[j]), uncert, vtab);
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == j) my_word = bal;
       if (keep) {
@@ -407,6 +429,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   // prefix({kStreamLabor, layer}) under z1 (and z2 when smoothed)
   const uint64_t p1 = hstep(hstep(hinit(v.z1), 2ULL), static_cast<uint64_t>(a.layer));
   const uint64_t p2 = SMOOTH ? hstep(hstep(hinit(v.z2), 2ULL), static_cast<uint64_t>(a.layer)) : 0;
+  const double* vtab = (SMOOTH && vtab_used(a, total)) ? a.vtab : nullptr;
   const uint32_t warp = threadIdx.x >> 5;
   unsigned long long uncert = 0;
   tstamp(a.trace, role, 0);
@@ -446,11 +469,11 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
         if (step == 1) break;
       }
       mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, s_nxt, s_row, s_th,
-                                   s_di, uncert);
+                                   s_di, uncert, vtab);
     } else {
       const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
       mark_span<IPT, SMOOTH, false>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, s_nxt, s_row,
-                                    s_th, s_di, uncert);
+                                    s_th, s_di, uncert, vtab);
     }
   }
   if (SMOOTH) {
@@ -916,6 +939,10 @@ void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_d
 }
 
 void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStream_t st) {
+  if (smooth && a.kind != 0 && a.vtab) {
+    launch_k(vtab_kernel, grid_for(a.n_vert, kNT, 8), kNT, st, a);
+    CB_LAUNCH("vtab");
+  }
   const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, kMarkCtasPerSM);
   if (smooth && a.kind != 0) launch_k(labor_mark_kernel<kLaborIPT, true>, grid, kNT, st, a);
   else launch_k(labor_mark_kernel<kLaborIPT, false>, grid, kNT, st, a);

@@ -181,6 +181,24 @@ def coop_eq(res: cb.CoopSampleResult, exp: dict, P: int, L: int, where=""):
             assert np.array_equal(a.loc_row[p], b["loc_row"][p]), f"{where} loc_row {l},{p}"
 
 
+@pytest.mark.parametrize("kappa", [4, 64])
+def test_smoothed_variate_table_c1(c1, kappa):
+    """Smoothed LABOR where the scan space exceeds 2|V| (the per-vertex
+    variate table path, samplers.cpp:114-129 memoisation) and where it does
+    not (per-position evaluation): both bit-exact vs the oracle."""
+    g, ref = c1
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, 10)
+    sched = cb.schedule_advance(cb.SeedSchedule.make(kappa, 5))
+    rng = np.random.default_rng(kappa)
+    seeds = rng.choice(ref.n, 2000, replace=False).astype(np.uint32)
+    pl = cb.Plan(g, None, 3, cfg, len(seeds))
+    pl.sample([seeds], sched, cb.MODE_INDEP)
+    scans = [pl.layer_sizes(0, l)["scan_total"] for l in range(3)]
+    assert min(scans) < 2 * ref.n <= max(scans), scans  # both paths exercised
+    want = O.expand(ref, seeds, 3, O.LABOR0, 10, osched(sched))
+    assert_stack_eq(pl.stack(0), want, f"kappa={kappa}")
+
+
 @pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
 def test_partition_members(c1, P):
     """partition.cpp:99-105 part_members: the shard layout of the feature
