@@ -537,10 +537,11 @@ def run_ours(args, cfg):
                      "note": "gather timed alone (one launch, events on its stream); sample = step - gather"},
         "e2e": {"value": seeds_total / e2e_s, "unit": "seeds/s",
                 "h2d_bytes_per_step": b * 4 + 40, "d2h_bytes_per_step": 64},
-        "roofline": {"bound": "hbm", "kernel": "gather_kernel<uint4,4>",
+        "roofline": {"bound": "hbm",
+                     "kernel": "gather_kernel<V,4> (16/8/4/2-byte vectors by row size)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic("gather_kernel", cfg["dim"]),
+                     "traffic": ncu_traffic("gather", cfg["dim"]),
                      "bytes_per_launch": gather_bytes},
         "gpu_launches": launches_per_step * K,
         "kernel_ms_graph": [round(x, 4) for x in prof_ms],

@@ -81,12 +81,12 @@ def main():
         starts = [i for i, d in enumerate(data) if "batch_begin" in d["Kernel Name"]]
         segs = [data[a:b] for a, b in zip(starts, starts[1:] + [len(data)])]
         # an indep P=1 batch: begin, L x (frontier, mark, post), relabel, gather
-        full = [sg for sg in segs if any("gather_kernel<uint4" in d["Kernel Name"] for d in sg)
+        full = [sg for sg in segs if any("gather" in d["Kernel Name"] for d in sg)
                 and sum("frontier" in d["Kernel Name"] for d in sg) == 3
                 and sum("relabel" in d["Kernel Name"] for d in sg) == 1]
         step = full[-1] if full else data[last:]
         # keep the batch and its own gather only
-        gi = max(i for i, d in enumerate(step) if "gather_kernel" in d["Kernel Name"]) \
+        gi = max(i for i, d in enumerate(step) if "gather" in d["Kernel Name"]) \
             if full else len(step) - 1
         step = step[:gi + 1]
         tot = sum(float(d["Metric Value"].replace(",", "")) for d in step)
@@ -103,8 +103,8 @@ def main():
             for k in KEYS:
                 if k in m:
                     md.append(f"- {k}: {m[k][0]} {m[k][1]}")
-            if "gather_kernel" in m["kernel"]:
-                traffic["gather_kernel"] = {
+            if "gather" in m["kernel"]:
+                traffic["gather"] = {
                     "dram_bytes": to_bytes(m["dram__bytes_read.sum"]) +
                     to_bytes(m["dram__bytes_write.sum"]), "dim": dim, "source": f"{tag}/{rep}"}
         shutil.copy(os.path.join(src, rep), os.path.join(dst, f"{tag}_{rep}"))
