@@ -259,6 +259,70 @@ def concavity_evidence(cb, g, scfg, L, b, row_bytes, dev, parts=(1, 2, 4, 8)):
     return out
 
 
+# ---------------------------------------------------------- scale evidence --
+def scale_evidence(cb, dev, steps=20, parts=(1, 8)):
+    """north_star's target workload on one B200: config 4 (papers100M-shaped
+    R-MAT, 111M V / 1.6B E, 128 fp16 rows), independent P=1 throughput with
+    the same timing as the headline (CUDA graphs, L2 flushed, events), the
+    gather's roofline, and cooperative vs independent per-seed work at P=8
+    (simulated parts on this GPU)."""
+    import torch
+
+    c = CONFIGS["c4"]
+    t0 = time.time()
+    g = cb.Graph.generate_rmat(c["n"], c["m"], GRAPH_SEED, device=dev)
+    gen_s = time.time() - t0
+    store = cb.FeatureStore.synth(g, c["dim"], FEAT_SEED, c["dtype"])
+    scfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, fanouts=c["fanouts"])
+    L, b = len(c["fanouts"]), c["batch"]
+    plan = cb.Plan(g, None, L, scfg, b)
+    pool = np.arange(c["n"], dtype=np.uint32)
+    from paper_2310_12403_b200.seeds import draw_from_pool
+    seeds = [draw_from_pool(pool, b, RUN_SEED, cb.hash_bits(s, [0])) for s in range(steps + 3)]
+    scheds = [cb.SeedSchedule.make(1, RUN_SEED)]
+    for _ in range(steps + 3):
+        scheds.append(cb.schedule_advance(scheds[-1]))
+    plan.sample([seeds[0]], scheds[0], cb.MODE_INDEP, sync=True)
+    plan.capture(np.array([0, b], np.uint64), scheds[0], cb.MODE_INDEP, store)
+    st = torch.cuda.ExternalStream(plan.stream, device=torch.device(f"cuda:{dev}"))
+    d = torch.from_numpy(np.stack(seeds).view(np.int32)).to(f"cuda:{dev}")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    clean = torch.empty(64 << 20, dtype=torch.int32, device=f"cuda:{dev}")
+
+    def flush_l2():  # same as the headline: 512 MiB write, then 256 MiB read
+        with torch.cuda.stream(st):
+            flush.zero_()
+            clean.sum()
+    ms, gms = [], []
+    for i in range(steps + 3):
+        flush_l2()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record(st)
+        plan.replay(d.data_ptr() + i * b * 4, scheds[i], True, 3)
+        e[1].record(st)
+        flush_l2()
+        e[2].record(st)
+        plan.gather(store)
+        e[3].record(st)
+        plan.synchronize()
+        if i >= 3:
+            ms.append(e[0].elapsed_time(e[1]))
+            gms.append(e[2].elapsed_time(e[3]))
+    rows = plan.layer_sizes(0, L - 1)["n_src"]
+    gbytes = rows * (2 * store.row_bytes + 4)
+    peak, _ = peaks()
+    out = {"workload": c["workload"], "graph_gen_s": round(gen_s, 2),
+           "seeds_per_s": b / (np.mean(ms) / 1e3), "ms_per_step": float(np.mean(ms)),
+           "gather": {"ms": float(np.mean(gms)), "rows": rows,
+                      "achieved_gbs": gbytes / (np.mean(gms) / 1e3) / 1e9,
+                      "frac": gbytes / (np.mean(gms) / 1e3) / 1e9 / peak},
+           "per_layer": [plan.layer_sizes(0, l) for l in range(L)]}
+    del plan, store
+    out["concavity"] = concavity_evidence(cb, g, scfg, L, b, c["dim"] * 2, dev, parts=parts)
+    del g
+    return out
+
+
 # ---------------------------------------------------------- kappa evidence --
 def kappa_evidence(cb, dev, steps_epochs=2, kappas=(1, 4, 16, 64, 256, None)):
     """Config 3's kappa sweep (acceptance.cpp:362-390 at full scale): the
@@ -553,6 +617,7 @@ def run_ours(args, cfg):
     if world == 1 and not args.no_evidence:
         line["evidence"]["concavity"] = concavity_evidence(cb, g, scfg, L, b, row_bytes, dev)
         line["evidence"]["kappa"] = kappa_evidence(cb, dev)
+        line["evidence"]["papers100m"] = scale_evidence(cb, dev)
     if world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import oracle as O
