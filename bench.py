@@ -398,19 +398,28 @@ def run_ours_coop(args, cfg):
     mine = pm.members()[rank]
     store = synth_shard(g, pm, rank, cfg["dim"], FEAT_SEED, cfg["dtype"])
     scfg = cb.SamplerConfig(kind, fanouts=cfg["fanouts"])
-    eng = CudaEngine(g, pm, rank, L, scfg, max_seeds=b, store=store,
-                     comm_device=None if backend == "nccl" else "cpu")
-    dc = DistCoop(eng)
     W, K = args.warmup, args.steps
     seeds_host = [draw_from_pool(mine, b, RUN_SEED, cb.hash_bits(s, [rank])) for s in range(W + K)]
-    seeds_dev = [eng.to_device(s) for s in seeds_host]
+    seeds_dev = [torch.from_numpy(s.view(np.int32)).to(f"cuda:{dev}") for s in seeds_host]
     scheds = [cb.SeedSchedule.make(1, RUN_SEED)]
     for _ in range(W + K):
         scheds.append(cb.schedule_advance(scheds[-1]))
+    if args.exchange == "px":
+        from paper_2310_12403_b200.dist import PeerCoop
+        pc = PeerCoop(g, pm, rank, L, scfg, max_seeds=b, store=store)
 
-    def step(i, seeds):
-        dc.sample(seeds, L, scheds[i], keep_blocks=False, records=False)
-        return dc.load_inputs(to_host=False)
+        def step(i, seeds):
+            pc.sample(seeds, scheds[i])
+            pc.load_inputs()
+            return 0  # row bytes read from the device after the timed loop
+    else:
+        eng = CudaEngine(g, pm, rank, L, scfg, max_seeds=b, store=store,
+                         comm_device=None if backend == "nccl" else "cpu")
+        dc = DistCoop(eng)
+
+        def step(i, seeds):
+            dc.sample(seeds, L, scheds[i], keep_blocks=False, records=False)
+            return dc.load_inputs(to_host=False).numel()
 
     for i in range(W):
         step(i, seeds_dev[i])
@@ -424,8 +433,9 @@ def run_ours_coop(args, cfg):
         t = time.perf_counter()
         n_rows = 0
         for i in range(W, W + K):
-            rows = step(i, seeds_of(i))
-            n_rows += rows.numel()
+            n_rows += step(i, seeds_of(i))
+        if args.exchange == "px":
+            pc.finish()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
         _lib.load().cb_kernel_launches(C.byref(lc))
@@ -437,6 +447,10 @@ def run_ours_coop(args, cfg):
     clocks = ClockSampler(dev)
     with clocks:
         dt, row_bytes_total, launches = timed(lambda i: seeds_dev[i])
+    if args.exchange == "px":  # the last step's rows, times K
+        nr = C.c_uint64()
+        _lib.load().cb_px_sizes(pc._h, L - 1, C.byref(nr), None)
+        row_bytes_total = nr.value * store.row_bytes * K
     # e2e: host seeds (H2D inside), rows end on the device, one D2H of the
     # owned-set size per step (the batch result the trainer reads)
     e2e_dt, _, _ = timed(lambda i: seeds_host[i])
@@ -449,8 +463,12 @@ def run_ours_coop(args, cfg):
         "steps": K, "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (hash-keyed R-MAT, hashed features)",
-        "config": {"workload": cfg["workload"], "mode": f"cooperative (P={world}, one part per "
-                   f"GPU, {backend} all-to-allv per layer + feature all-to-allv)",
+        "config": {"workload": cfg["workload"],
+                   "mode": f"cooperative (P={world}, one part per GPU; " + (
+                       "peer-memory exchange: ids OR-ed into owners' bitmaps over CUDA IPC, "
+                       f"ranks read back, rows pulled from owners' shards; {backend} phase "
+                       "barriers)" if args.exchange == "px" else
+                       f"{backend} all-to-allv per layer + feature all-to-allv)"),
                    "timing": "wall clock between barriers + device sync, max over ranks "
                              "(host-orchestrated exchange)",
                    "graph": {"vertices": cfg["n"], "edges": cfg["m"], "gen_s": round(gen_s, 2)}},
@@ -643,6 +661,8 @@ def main():
     ap.add_argument("--no-evidence", action="store_true")
     ap.add_argument("--mode", choices=["coop", "indep"], default="coop",
                     help="N>1: cooperative minibatching (one part per GPU) or independent")
+    ap.add_argument("--exchange", choices=["px", "a2a"], default="px",
+                    help="N>1 coop: peer-memory exchange (cb_px_*) or all-to-allv (DistCoop)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: ranks share cuda:0 with CPU-staged exchanges (testing)")
     args = ap.parse_args()

@@ -35,6 +35,8 @@
  *   cb_stack_fingerprint,     <- stack_fingerprint / run_dependent_experiment
  *   cb_shuffled_order            order (src/cache.cpp:123-162)
  *   cb_partition_members      <- part_members (partition.hpp:33-36)
+ *   cb_px_*                   <- coop_sample + build_exchange + all_to_all_forward
+ *                                across processes (coop.cpp:25-106, 145-159)
  *   cb_last_error             <- the what() of coopbatch::InputError etc.
  *                                (include/coopbatch/common.hpp:12-31)
  */
@@ -259,6 +261,34 @@ int cb_features_set_tier(cb_features* f, int host);
 int cb_kernel_launches(uint64_t* n);
 /* Device pointer + count of the input vertices of part `part`. */
 int cb_plan_input_ids(cb_plan* plan, uint32_t part, const uint32_t** d_ids, uint64_t* n);
+
+/* ---- multi-process peer exchange (one part per rank, CUDA IPC) ----
+ * coop_sample (coop.cpp:68-106) with build_exchange (coop.cpp:25-64) done in
+ * peer memory: requesters OR their src ids straight into the owners'
+ * exchange bitmaps over NVLink, owners extract their sorted sets in place,
+ * requesters read their ranks back from the owners' bitmaps; input rows are
+ * pulled from the owners' shards (all_to_all_forward, coop.cpp:145-159).
+ * No counts cross ranks and nothing syncs with the host: between
+ * cb_px_layer -> cb_px_owner -> cb_px_locate of a layer the caller puts a
+ * cross-rank barrier ordered on cb_plan_stream (an NCCL all-reduce on that
+ * stream, or a host barrier after a stream sync). Handles are 64 bytes. */
+int cb_px_setup(cb_plan* plan, const cb_partition* pm, uint32_t rank, void* handle_out);
+int cb_px_connect(cb_plan* plan, uint32_t peer, const void* handle);
+int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seeds,
+                const cb_sched* sched);
+int cb_px_owner(cb_plan* plan, int layer);
+int cb_px_locate(cb_plan* plan, int layer);
+int cb_px_finish(cb_plan* plan);
+int cb_px_sizes(cb_plan* plan, int layer, uint64_t* n_src, uint64_t* n_owned);
+/* This rank's send_counts row, src_location, and its owned set after layer l. */
+int cb_px_download(cb_plan* plan, int layer, uint64_t* send_row, uint32_t* loc_part,
+                   uint32_t* loc_row, uint32_t* owned);
+int cb_features_export(const cb_features* f, void* handle_out, uint64_t* shard_r0);
+int cb_px_connect_features(cb_plan* plan, uint32_t peer, const void* handle, uint64_t shard_r0,
+                           const cb_features* local);
+/* Input rows of this rank's last layer into the plan's row buffer
+ * (cb_download_rows / cb_rows_device), requester-aligned. */
+int cb_px_gather(cb_plan* plan, const cb_features* local);
 
 #ifdef __cplusplus
 }

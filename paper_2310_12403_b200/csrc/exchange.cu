@@ -61,7 +61,129 @@ __global__ void locate_kernel(PartPtrs pp, const uint32_t* __restrict__ owner) {
   }
 }
 
+// ---- peer exchange kernels ----
+__global__ void px_route_kernel(const uint32_t* __restrict__ src,
+                                const unsigned long long* __restrict__ count, uint64_t cap,
+                                const uint32_t* __restrict__ owner, PxPeers peers,
+                                unsigned long long* send_row) {
+  pdl_begin();
+  __shared__ unsigned long long hist[kMaxParts];
+  for (uint32_t q = threadIdx.x; q < kMaxParts; q += blockDim.x) hist[q] = 0;
+  __syncthreads();
+  const uint64_t n = min(static_cast<uint64_t>(*count), cap);
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t v = src[j];
+    const uint32_t q = owner[v];
+    atomicOr(&peers.bits[q][v >> 5], 1u << (v & 31u));
+    if (peers.summ[q]) atomicOr(&peers.summ[q][v >> 10], 1u << ((v >> 5) & 31u));
+    atomicAdd(&hist[q], 1ULL);
+  }
+  // the owner reads these bits after a cross-rank barrier
+  __threadfence_system();
+  __syncthreads();
+  for (uint32_t q = threadIdx.x; q < kMaxParts; q += blockDim.x)
+    if (hist[q]) atomicAdd(&send_row[q], hist[q]);
+}
+
+__global__ void px_locate_kernel(const uint32_t* __restrict__ src,
+                                 const unsigned long long* __restrict__ count, uint64_t cap,
+                                 const uint32_t* __restrict__ owner, PxPeers peers,
+                                 uint32_t* loc_part, uint32_t* loc_row) {
+  pdl_begin();
+  const uint64_t n = min(static_cast<uint64_t>(*count), cap);
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t v = src[j];
+    const uint32_t q = owner[v];
+    const uint32_t w = v >> 5;
+    loc_part[j] = q;
+    loc_row[j] = peers.pre[q][w] + __popc(peers.bits[q][w] & ((1u << (v & 31u)) - 1u));
+  }
+}
+
+template <typename V>
+__global__ void px_gather_kernel(const unsigned char* const* __restrict__ bases,
+                                 const uint32_t* __restrict__ owner,
+                                 const uint32_t* __restrict__ row_map, uint32_t vpr,
+                                 uint64_t row_bytes, const uint32_t* __restrict__ ids,
+                                 const unsigned long long* __restrict__ count, uint64_t cap,
+                                 V* __restrict__ out) {
+  pdl_begin();
+  const uint64_t n = min(static_cast<uint64_t>(*count), cap);
+  const uint64_t total = n * vpr;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  constexpr int U = 4;
+  for (uint64_t x0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x0 < total;
+       x0 += stride * U) {
+    V buf[U];
+    const V* srcp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t x = x0 + u * stride;
+      srcp[u] = nullptr;
+      if (x < total) {
+        const uint64_t r = x / vpr, c = x - r * vpr;
+        const uint32_t v = __ldg(ids + r);
+        srcp[u] = reinterpret_cast<const V*>(bases[__ldg(owner + v)] +
+                                             static_cast<uint64_t>(__ldg(row_map + v)) *
+                                                 row_bytes) + c;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (srcp[u]) buf[u] = *srcp[u];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (srcp[u]) __stcs(out + x0 + u * stride, buf[u]);
+  }
+}
+
 }  // namespace
+
+void launch_px_route(const uint32_t* src, const unsigned long long* count, uint64_t cap,
+                     const uint32_t* owner, const PxPeers& peers, unsigned long long* send_row,
+                     cudaStream_t st) {
+  launch_k(px_route_kernel, grid_for(cap, 256, 8), 256, st, src, count, cap, owner, peers,
+           send_row);
+  CB_LAUNCH("px_route");
+}
+
+void launch_px_locate(const uint32_t* src, const unsigned long long* count, uint64_t cap,
+                      const uint32_t* owner, const PxPeers& peers, uint32_t* loc_part,
+                      uint32_t* loc_row, cudaStream_t st) {
+  launch_k(px_locate_kernel, grid_for(cap, 256, 8), 256, st, src, count, cap, owner, peers,
+           loc_part, loc_row);
+  CB_LAUNCH("px_locate");
+}
+
+void launch_px_gather(const unsigned char* const* d_bases, const uint32_t* owner,
+                      const uint32_t* row_map, uint64_t row_bytes, const uint32_t* ids,
+                      const unsigned long long* count, uint64_t cap, void* out,
+                      cudaStream_t st) {
+  int vb = 16;
+  while (row_bytes % vb) vb >>= 1;
+  const uint32_t vpr = static_cast<uint32_t>(row_bytes / vb);
+  const unsigned grid = kNumSMs * 8;
+  switch (vb) {
+    case 16:
+      launch_k(px_gather_kernel<uint4>, grid, 256, st, d_bases, owner, row_map, vpr, row_bytes,
+               ids, count, cap, static_cast<uint4*>(out));
+      break;
+    case 8:
+      launch_k(px_gather_kernel<uint2>, grid, 256, st, d_bases, owner, row_map, vpr, row_bytes,
+               ids, count, cap, static_cast<uint2*>(out));
+      break;
+    case 4:
+      launch_k(px_gather_kernel<uint32_t>, grid, 256, st, d_bases, owner, row_map, vpr,
+               row_bytes, ids, count, cap, static_cast<uint32_t*>(out));
+      break;
+    default:
+      launch_k(px_gather_kernel<unsigned short>, grid, 256, st, d_bases, owner, row_map, vpr,
+               row_bytes, ids, count, cap, static_cast<unsigned short*>(out));
+  }
+  CB_LAUNCH("px_gather");
+}
 
 void launch_route(const PartPtrs& pp, const uint32_t* owner, uint32_t P,
                   unsigned long long* send_counts, uint64_t max_src, cudaStream_t st) {

@@ -20,6 +20,33 @@ struct PartPtrs {
   uint32_t* loc_row[kMaxParts];
 };
 
+// ---- multi-process peer exchange (one part per rank, CUDA IPC peer memory) ----
+// Pointers into every rank's exchange region for one layer slot (entry q =
+// rank q's bitmap, IPC-mapped; q == self is local memory).
+struct PxPeers {
+  uint32_t* bits[kMaxParts];
+  uint32_t* summ[kMaxParts];  // nullptr: flat bitmaps
+  const uint32_t* pre[kMaxParts];
+};
+
+// Requester side of build_exchange (coop.cpp:35-51): OR every src id into its
+// owner's exchange bitmap over peer memory; send_row[q] += ids sent to q.
+void launch_px_route(const uint32_t* src, const unsigned long long* count, uint64_t cap,
+                     const uint32_t* owner, const PxPeers& peers, unsigned long long* send_row,
+                     cudaStream_t st);
+// src_location (coop.cpp:53-62): (owner, rank of v in the owner's sorted set)
+// read from the owner's exchange bitmap and word ranks over peer memory.
+void launch_px_locate(const uint32_t* src, const unsigned long long* count, uint64_t cap,
+                      const uint32_t* owner, const PxPeers& peers, uint32_t* loc_part,
+                      uint32_t* loc_row, cudaStream_t st);
+// all_to_all_forward (coop.cpp:145-159) as one-sided reads: row of input
+// vertex v from its owner's shard, bases[q] = rank q's shard (virtual base
+// indexed by the global shard-major row) -> out[j] requester-aligned.
+void launch_px_gather(const unsigned char* const* d_bases, const uint32_t* owner,
+                      const uint32_t* row_map, uint64_t row_bytes, const uint32_t* ids,
+                      const unsigned long long* count, uint64_t cap, void* out,
+                      cudaStream_t st);
+
 void launch_route(const PartPtrs& pp, const uint32_t* owner, uint32_t P,
                   unsigned long long* send_counts, uint64_t max_src, cudaStream_t st);
 void launch_locate(const PartPtrs& pp, const uint32_t* owner, uint32_t P, uint64_t max_src,

@@ -245,3 +245,126 @@ def synth_shard(g: Graph, pm: PartitionMap, part: int, dim: int, seed: int,
     _check(_lib.load().cb_features_synth_shard(g._h, pm._h, part, dim, _DT[dtype][0], seed,
                                                C.byref(h)))
     return FeatureStore(g, h, dim, dtype, pm)
+
+
+class PeerCoop:
+    """One part per rank with the exchange done in peer memory (cb_px_*,
+    csrc/exchange.cu): each rank's src ids are OR-ed straight into their
+    owners' exchange bitmaps over NVLink (CUDA IPC mappings), owners extract
+    their sorted sets in place, requesters read their ranks back from the
+    owners' bitmaps, and input rows are pulled from the owners' shards
+    requester-aligned. No counts cross ranks and the host never waits: the
+    only cross-rank operation is a barrier between the three phases of a
+    layer -- an NCCL all-reduce of one element ordered on the plan stream (or,
+    over gloo, a stream sync plus a host barrier)."""
+
+    HANDLE = 64
+
+    def __init__(self, g: Graph, pm: PartitionMap, rank: int, num_layers: int,
+                 cfg: SamplerConfig, max_seeds: int, store: FeatureStore | None = None,
+                 group=None):
+        self.L = _lib.load()
+        self.g, self.pm, self.rank, self.group = g, pm, rank, group
+        self.world = dist.get_world_size(group)
+        if pm.num_parts != self.world:
+            raise ValueError("PeerCoop: partition part count must equal the world size")
+        self.num_layers, self.store = num_layers, store
+        self.device = torch.device(f"cuda:{g.device}")
+        fo = np.asarray(cfg.layer_fanouts(num_layers), dtype=np.uint32)
+        h = C.c_void_p()
+        _check(self.L.cb_plan_create_dist(g._h, self.world, num_layers, int(cfg.kind),
+                                          fo.ctypes.data_as(C.c_void_p), max_seeds,
+                                          C.byref(h)))
+        self._h = h
+        buf = (C.c_ubyte * self.HANDLE)()
+        _check(self.L.cb_px_setup(h, pm._h, rank, buf))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(buf), group=group)
+        for q in range(self.world):
+            if q != rank:
+                hq = (C.c_ubyte * self.HANDLE).from_buffer_copy(handles[q])
+                _check(self.L.cb_px_connect(h, q, hq))
+        if store is not None:
+            fb, r0 = (C.c_ubyte * self.HANDLE)(), C.c_uint64()
+            _check(self.L.cb_features_export(store._h, fb, C.byref(r0)))
+            fh = [None] * self.world
+            dist.all_gather_object(fh, (bytes(fb), r0.value), group=group)
+            for q in range(self.world):
+                hq = (C.c_ubyte * self.HANDLE).from_buffer_copy(fh[q][0])
+                _check(self.L.cb_px_connect_features(h, q, hq, fh[q][1], store._h))
+        self.stream = torch.cuda.ExternalStream(self.L.cb_plan_stream(h), device=self.device)
+        self._nccl = dist.get_backend(group) == "nccl"
+        self._tok = torch.zeros(1, device=self.device if self._nccl else "cpu")
+        dist.barrier(group=group)  # every mapping is open before anyone writes
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self.L.cb_plan_destroy(self._h)
+            self._h = None
+
+    def barrier(self):
+        if self._nccl:
+            with torch.cuda.stream(self.stream):
+                dist.all_reduce(self._tok, group=self.group)
+        else:
+            _check(self.L.cb_synchronize(self._h))
+            dist.barrier(group=self.group)
+
+    def sample(self, seeds, schedule: SeedSchedule):
+        """One cooperative step for this rank's seeds (host u32 array or a
+        device tensor), all phases stream-ordered on the plan stream."""
+        if isinstance(seeds, torch.Tensor):
+            ptr, n = seeds.data_ptr(), seeds.numel()
+        else:
+            self._seeds = np.ascontiguousarray(seeds, dtype=np.uint32)
+            ptr, n = self._seeds.ctypes.data, len(self._seeds)
+        s = schedule._c()
+        for l in range(self.num_layers):
+            _check(self.L.cb_px_layer(self._h, l, C.c_void_p(ptr) if l == 0 else None,
+                                      n if l == 0 else 0, C.byref(s)))
+            self.barrier()
+            _check(self.L.cb_px_owner(self._h, l))
+            self.barrier()
+            _check(self.L.cb_px_locate(self._h, l))
+
+    def load_inputs(self):
+        """all_to_all_forward: rows of the input vertices pulled from the
+        owners' shards into the plan's row buffer (shards are static, so no
+        barrier is needed)."""
+        _check(self.L.cb_px_gather(self._h, self.store._h))
+
+    def finish(self):
+        _check(self.L.cb_px_finish(self._h))
+
+    # -- results (host) --------------------------------------------------------
+    def result(self) -> DistSample:
+        self.finish()
+        out = DistSample()
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        for l in range(self.num_layers):
+            sz = np.zeros(6, np.uint64)
+            _check(self.L.cb_layer_sizes(self._h, 0, l, p(sz)))
+            nd, ns, ne = int(sz[0]), int(sz[1]), int(sz[2])
+            dst, src = np.zeros(nd, np.uint32), np.zeros(ns, np.uint32)
+            edges, dpos = np.zeros((ne, 2), np.uint32), np.zeros(nd, np.uint32)
+            _check(self.L.cb_download_block(self._h, 0, l, p(dst), p(src), p(edges), p(dpos)))
+            out.blocks.append({"layer": l, "dst": dst, "src": src, "edges": edges,
+                               "dst_pos": dpos})
+            n_src, n_own = C.c_uint64(), C.c_uint64()
+            _check(self.L.cb_px_sizes(self._h, l, C.byref(n_src), C.byref(n_own)))
+            send = np.zeros(self.world, np.uint64)
+            lp, lr = np.zeros(n_src.value, np.uint32), np.zeros(n_src.value, np.uint32)
+            own = np.zeros(n_own.value, np.uint32)
+            _check(self.L.cb_px_download(self._h, l, p(send), p(lp), p(lr), p(own)))
+            out.exchanges.append(DistExchange(l, [int(x) for x in send], n_own.value, lp,
+                                              lr.astype(np.uint64)))
+            out.owner_set = own
+        return out
+
+    def rows(self) -> np.ndarray:
+        n = C.c_uint64()
+        _check(self.L.cb_px_sizes(self._h, self.num_layers - 1, C.byref(n), None))
+        dt = _DT[self.store.dtype][1]
+        out = np.zeros((n.value, self.store.dim), dtype=dt)
+        _check(self.L.cb_download_rows(self._h, 0, out.ctypes.data_as(C.c_void_p)))
+        return out
