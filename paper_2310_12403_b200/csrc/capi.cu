@@ -207,7 +207,6 @@ struct cb_plan {
   bool smooth = false;    // kernels of the last enqueue used smoothed variates
   bool trace_on = false;   // globaltimer stamps per CTA (debug, CB_TRACE=1)
   unsigned long long* trace = nullptr;  // [kTraceSlots]
-  bool use_fused = false;  // single cooperative launch (slower on B200 at b=1024: see DESIGN)
   std::vector<cudaEvent_t>* prof = nullptr;  // per-launch events (cb_plan_profile)
   bool prof_external = false;                 // record as graph event nodes
   std::vector<cudaEvent_t> graph_events;      // of exec_prof
@@ -322,7 +321,6 @@ void plan_alloc(cb_plan* pl) {
     w.sync.tickets = pl->mem.alloc<unsigned>(2 * Sync::kMaxTickets);
     CB_CUDA(cudaMemset(w.sync.tickets, 0, 2 * Sync::kMaxTickets * sizeof(unsigned)));
     w.sync.overflow = pl->mem.alloc<unsigned>(1);
-    w.sync.barrier = pl->mem.alloc<unsigned>(1);
     w.sync.keep_words = pl->mem.alloc<uint32_t>(max_tiles * kLaborTile / 32 + 1);
     w.sync.status_a = pl->mem.alloc<unsigned long long>(max_tiles);
     w.sync.status_b = pl->mem.alloc<unsigned long long>(max_tiles);
@@ -590,8 +588,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
 
 // The per-batch launch sequence. d_seeds: P seed lists back to back (device).
 void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_t* off,
-                   const cb_sched* sched, bool capturing = false,
-                   const cb_features* fuse_gather = nullptr, bool* gathered = nullptr) {
+                   const cb_sched* sched, bool capturing = false) {
   const uint32_t P = pl->P;
   const int L = pl->L;
   cudaStream_t st = pl->stream;
@@ -614,62 +611,7 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
   pl->smooth = smooth;
   // during capture the graph must clear what a batch of its own mode leaves
   const int dm = capturing ? mode : pl->dirty_mode;
-  if (gathered) *gathered = false;
   const RelabelArgs none{};
-  const bool fused = !coop && pl->kind != CB_NS && pl->use_fused && !pl->prof;
-  if (fused) {
-    // one cooperative persistent launch per part: every phase of every layer
-    for (uint32_t p = 0; p < P; ++p) {
-      PeWork& w = pl->pe[p];
-      FusedParams fp{};
-      fp.L = L;
-      const Dirty d = dirty_of(pl, p, dm);
-      fp.epoch = w.sync.epoch;
-      fp.overflow = w.sync.overflow;
-      fp.tickets = w.sync.tickets;
-      fp.clear_bits = d.bits;
-      fp.clear_summ = d.summ;
-      fp.clear_list = d.list;
-      fp.clear_count = d.count;
-      fp.clear_cap = d.cap;
-      fp.clear_nwords = w.bm[0].words_padded;
-      for (int l = 0; l < L; ++l) {
-        const uint32_t* D = (l == 0) ? d_seeds + off[p] : w.L[l - 1].src;
-        FusedLayer& fl = fp.layer[l];
-        fl.f = frontier_args(pl, w, p, l, D, l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[l & 1]);
-        fl.relabel_prev = none;
-        if (l > 0) {
-          const uint32_t* Dp = (l == 1) ? d_seeds + off[p] : w.L[l - 2].src;
-          fl.relabel_prev = relabel_args(w.bm[(l - 1) & 1], w.L[l - 1], Dp, pl->meta_at(p, l - 1));
-        }
-        fl.la = labor_args(pl, w, p, l, D, w.bm[l & 1]);
-        fl.ex = extract_args(w, w.bm[l & 1], &w.bm[(l + 1) & 1], w.L[l].src, w.L[l].cap_src,
-                             &pl->meta_at(p, l)->n_src, &pl->meta_at(p, l + 1)->n_dst, 3 * l + 2,
-                             8 * l + 4);
-      }
-      const uint32_t* Dl = (L == 1) ? d_seeds + off[p] : w.L[L - 2].src;
-      fp.relabel_last = relabel_args(w.bm[(L - 1) & 1], w.L[L - 1], Dl, pl->meta_at(p, L - 1));
-      if (fuse_gather) {
-        fp.table = fuse_gather->table;
-        fp.row_map = fuse_gather->row_map;
-        fp.vec_bytes = vec_bytes_for(fuse_gather->row_bytes);
-        fp.vpr = static_cast<uint32_t>(fuse_gather->row_bytes / fp.vec_bytes);
-        fp.rows_out = w.rows;
-        fp.cap_rows = w.cap_rows;
-        fp.gather_ids = w.L[L - 1].src;
-        fp.gather_count = &pl->meta_at(p, L - 1)->n_src;
-      }
-      fp.barrier = w.sync.barrier;
-      launch_fused(fp, smooth, st);
-      ++launches;
-    }
-    if (gathered) *gathered = fuse_gather != nullptr;
-    pl->launches = launches;
-    pl->have_batch = true;
-    pl->have_rows = fuse_gather != nullptr;
-    pl->dirty_mode = mode;
-    return;
-  }
   for (uint32_t p = 0; p < P; ++p) {
     const Dirty d = dirty_of(pl, p, dm);
     launch_batch_begin(pl->pe[p].sync, d.bits, d.summ, d.list, d.count, d.cap,
@@ -1085,7 +1027,6 @@ int cb_plan_create(const cb_graph* g, const cb_partition* pm, int num_layers, in
       pl->fanouts.push_back(k);
     }
     pl->max_seeds = std::max<uint64_t>(max_seeds_per_part, 1);
-    if (const char* e = std::getenv("CB_FUSED")) pl->use_fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("CB_TRACE")) pl->trace_on = std::atoi(e) != 0;
     CB_CUDA(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
     plan_alloc(pl.get());
@@ -1197,9 +1138,8 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
       CB_CUDA(cudaGraphDestroy(graph));
       plan->cap_launches_gather = plan->launches;
       CB_CUDA(cudaStreamBeginCapture(plan->stream, cudaStreamCaptureModeThreadLocal));
-      bool g_done = false;
-      enqueue_batch(plan, mode, plan->seeds, seeds_off, &dummy, true, f, &g_done);
-      if (!g_done) enqueue_gather(plan, f);
+      enqueue_batch(plan, mode, plan->seeds, seeds_off, &dummy, true);
+      enqueue_gather(plan, f);
       CB_CUDA(cudaStreamEndCapture(plan->stream, &graph));
       CB_CUDA(cudaGraphInstantiate(&plan->exec_all, graph, 0));
       CB_CUDA(cudaGraphDestroy(graph));
@@ -1680,10 +1620,6 @@ int cb_plan_trace(cb_plan* plan, uint64_t* out, uint64_t n) {
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n) {
   return guard([&] {
     require(plan != nullptr && n != nullptr, "null argument");
-    if (plan->use_fused && plan->kind != CB_NS && !(mode == CB_MODE_COOP && plan->P > 1)) {
-      *n = plan->P;  // one cooperative persistent launch per part (gather fused)
-      return;
-    }
     const uint64_t samp = (plan->kind == CB_NS) ? 4 : 3;  // incl. extract
     const uint64_t P = plan->P;
     const uint64_t L = plan->L;

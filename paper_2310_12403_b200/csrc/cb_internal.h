@@ -109,7 +109,6 @@ struct Sync {
   unsigned long long* status_b = nullptr;     // [max_tiles]
   unsigned long long* status_c = nullptr;     // [max_tiles]
   unsigned* overflow = nullptr;               // [1]
-  unsigned* barrier = nullptr;                // [1] fused-kernel grid barrier
   uint32_t* keep_words = nullptr;             // [max_tiles*kLaborTile/32]
   uint2* stage = nullptr;                     // [max_tiles*kLaborTile] kept edges by position
   uint64_t max_tiles = 0;
@@ -230,42 +229,6 @@ struct RelabelArgs {  // edges == nullptr disables
   uint32_t* dst_pos;
 };
 
-// Persistent single-launch batch (indep / one part, LABOR-0 or FULL): every
-// phase of every layer in one cooperative kernel, grid barriers between.
-constexpr int kMaxFusedLayers = 8;
-struct FusedLayer {
-  FrontierArgs f;
-  RelabelArgs relabel_prev;  // relabel of layer l-1 (fused into this frontier)
-  LaborArgs la;
-  ExtractArgs ex;
-};
-struct FusedParams {
-  int L;
-  // batch begin
-  unsigned* epoch;
-  unsigned* overflow;
-  unsigned* tickets;
-  uint32_t* clear_bits;
-  uint32_t* clear_summ;
-  const uint32_t* clear_list;
-  const unsigned long long* clear_count;
-  uint64_t clear_cap;
-  uint64_t clear_nwords;
-  FusedLayer layer[kMaxFusedLayers];
-  RelabelArgs relabel_last;
-  // gather (table == nullptr: none)
-  const void* table;
-  const uint32_t* row_map;
-  int vec_bytes;
-  uint32_t vpr;
-  void* rows_out;
-  uint64_t cap_rows;
-  const uint32_t* gather_ids;
-  const unsigned long long* gather_count;
-  unsigned* barrier;   // zeroed before every launch
-  unsigned n_ext;      // CTAs doing extract in the post phases
-};
-
 constexpr int kExtractTileWords = 2048;  // bitmap padding granule (max tile)
 constexpr uint64_t kExtractBigWords = 256 * 1024;  // summary-mode threshold
 constexpr int kLaborTile = 4096;
@@ -288,7 +251,6 @@ void launch_extract(const ExtractArgs& a, cudaStream_t st);
 void launch_labor_post(const LaborArgs& a, uint64_t max_tiles, const ExtractArgs& e,
                        cudaStream_t st);
 void launch_relabel(const RelabelArgs& r, uint64_t work, cudaStream_t st);
-void launch_fused(FusedParams& p, bool smooth, cudaStream_t st);
 void launch_clear(Bitmap& bm, const uint32_t* list, const unsigned long long* count,
                   cudaStream_t st);
 void launch_rank(const Bitmap& bm, const uint32_t* ids, const unsigned long long* count,

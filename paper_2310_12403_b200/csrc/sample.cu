@@ -31,6 +31,7 @@ using namespace cbdev;
 namespace {
 
 constexpr int kNT = 256;
+constexpr uint32_t kTileExact = 0x80000000u;
 // labor_mark residency: 4 CTAs/SM so one CTA's staging barrier overlaps
 // another's hashing
 constexpr int kMarkCtasPerSM = 4;
@@ -218,7 +219,11 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
           // scan tiles whose first position falls inside this record
           const uint64_t t_first = (eq + kLaborTile - 1) / kLaborTile;
           const uint64_t t_last = (eq + q[j] - 1) / kLaborTile;
-          for (uint64_t t = t_first; t <= t_last; ++t) a.tile_first[t] = static_cast<uint32_t>(ea);
+          // bit 31: the record starts exactly at the tile start (so the
+          // previous tile ends with record ea-1: no load to find it)
+          for (uint64_t t = t_first; t <= t_last; ++t)
+            a.tile_first[t] = static_cast<uint32_t>(ea) |
+                              ((t == t_first && eq == t * kLaborTile) ? kTileExact : 0u);
           ++ea;
         }
         if (is_ns) a.out_prefix[i] = eo;
@@ -231,7 +236,7 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
       ActRec sent{};
       sent.pre = tot;
       a.act[nact] = sent;
-      a.tile_first[(tot + kLaborTile - 1) / kLaborTile] = static_cast<uint32_t>(nact);
+      a.tile_first[(tot + kLaborTile - 1) / kLaborTile] = static_cast<uint32_t>(nact) | kTileExact;
       meta->scan_total = tot;
       meta->n_active = nact;
       meta->uncertified = 0;
@@ -246,7 +251,7 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
   if (n == 0 && role == 0 && threadIdx.x == 0) {
     ActRec sent{};
     a.act[0] = sent;
-    a.tile_first[0] = 0;
+    a.tile_first[0] = kTileExact;
     meta->scan_total = 0;
     meta->n_active = 0;
     meta->uncertified = 0;
@@ -274,12 +279,17 @@ __device__ __forceinline__ uint32_t rec_search(const ActRec* __restrict__ act, u
 }
 
 // Record range [a0, a1] overlapping scan tile [x0, x1).
-__device__ __forceinline__ void tile_records(const ActRec* act, const uint32_t* tile_first,
-                                             uint64_t n_act, uint64_t tile, uint64_t x1,
-                                             uint32_t& a0, uint32_t& a1) {
-  a0 = __ldg(&tile_first[tile]);
-  const uint32_t ae = __ldg(&tile_first[tile + 1]);
-  a1 = (ae < n_act && __ldg(&act[ae].pre) < x1) ? ae : ae - 1;
+// tile_first[t] = first record overlapping scan tile t, bit 31 set when that
+// record starts exactly at the tile start (frontier_body).
+__device__ __forceinline__ void tile_decode(uint32_t tf0, uint32_t tf1, uint32_t& a0,
+                                            uint32_t& a1) {
+  a0 = tf0 & ~kTileExact;
+  a1 = (tf1 & ~kTileExact) - ((tf1 & kTileExact) ? 1u : 0u);
+}
+__device__ __forceinline__ void tile_records(const ActRec*, const uint32_t* tile_first, uint64_t,
+                                             uint64_t tile, uint64_t, uint32_t& a0,
+                                             uint32_t& a1) {
+  tile_decode(__ldg(&tile_first[tile]), __ldg(&tile_first[tile + 1]), a0, a1);
 }
 
 // ------------------------------------------------------------- LABOR/FULL --
@@ -338,25 +348,27 @@ template <int IPT, bool SMOOTH, bool STAGED>
 __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v, uint64_t p1,
                                           uint64_t p2, uint64_t x0, uint32_t r0, uint32_t rend,
                                           uint32_t a0, uint32_t a1, uint32_t cur,
-                                          const uint32_t* s_nxt, const uint32_t* const* s_row,
-                                          const unsigned long long* s_th, const uint32_t* s_di,
+                                          const ActRec* s_act, uint32_t nd,
                                           unsigned long long& uncert, const double* vtab) {
   static_assert(IPT <= 32, "one word per lane");
   const uint32_t lane = lane_id();
   auto nxt_of = [&](uint32_t c) -> uint32_t {  // tile-relative start of record c+1
-    if (STAGED) return s_nxt[c];
+    if (STAGED)
+      return (c + 1 < nd) ? static_cast<uint32_t>(min(static_cast<uint64_t>(s_act[c + 1].pre) - x0,
+                                                      static_cast<uint64_t>(0xffffffffu)))
+                          : 0xffffffffu;
     if (a0 + c + 1 > a1) return 0xffffffffu;
     const uint64_t pr = __ldg(&a.act[a0 + c + 1].pre);
     return static_cast<uint32_t>(min(pr - x0, static_cast<uint64_t>(0xffffffffu)));
   };
   auto row_of = [&](uint32_t c) -> const uint32_t* {
-    return STAGED ? s_row[c] : a.indices + (__ldg(&a.act[a0 + c].a) + x0);
+    return a.indices + ((STAGED ? s_act[c].a : __ldg(&a.act[a0 + c].a)) + x0);
   };
   auto th_of = [&](uint32_t c) -> uint64_t {
-    return STAGED ? s_th[c] : __ldg(&a.act[a0 + c].b);
+    return STAGED ? s_act[c].b : __ldg(&a.act[a0 + c].b);
   };
   auto di_of = [&](uint32_t c) -> uint32_t {
-    return STAGED ? s_di[c] : __ldg(&a.act[a0 + c].di);
+    return STAGED ? s_act[c].di : __ldg(&a.act[a0 + c].di);
   };
   uint2* stage = a.stage + x0 + r0;
   uint32_t my_word = 0;
@@ -410,17 +422,25 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
   if (lane < IPT && r0 + lane * 32 < rend) a.keep_words[((x0 + r0) >> 5) + lane] = my_word;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+
+// labor_mark: tiles of kNT*IPT scan positions (grid-stride), one 32*IPT span
+// per warp. A tile's records (when <= kRecs) are staged raw in shared memory
+// by cp.async, double-buffered: the records of tile k+1 stream in while tile
+// k is hashed, and tile_first of tile k+2 is already in registers, so the
+// per-tile barrier no longer waits on a chain of global loads.
 template <int IPT, bool SMOOTH>
 __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, unsigned ncta) {
   constexpr int TILE = kNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
   constexpr uint32_t WSPAN = 32 * IPT;  // contiguous positions owned by one warp
   constexpr int kRecs = 512;            // records staged in smem (else global path)
-  __shared__ uint32_t s_pre[kRecs];     // tile-relative record starts (clamped at 0)
-  __shared__ uint32_t s_nxt[kRecs];     // tile-relative start of the next record
-  __shared__ const uint32_t* s_row[kRecs];
-  __shared__ unsigned long long s_th[kRecs];
-  __shared__ uint32_t s_di[kRecs];
+  __shared__ __align__(16) ActRec s_act[2][kRecs];
   LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
   const uint64_t n_act = meta->n_active;
@@ -432,50 +452,70 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   const double* vtab = (SMOOTH && vtab_used(a, total)) ? a.vtab : nullptr;
   const uint32_t warp = threadIdx.x >> 5;
   unsigned long long uncert = 0;
+  (void)n_act;
   tstamp(a.trace, role, 0);
-  for (uint64_t tile = role; tile < ntiles; tile += ncta) {
+  auto stage = [&](uint32_t a0, uint32_t a1, int buf) {
+    const uint32_t nd = a1 - a0 + 1;
+    if (nd <= static_cast<uint32_t>(kRecs)) {
+      const char* src = reinterpret_cast<const char*>(a.act + a0);
+      char* dst = reinterpret_cast<char*>(s_act[buf]);
+      for (uint32_t i = threadIdx.x; i < 2 * nd; i += kNT) cp_async16(dst + 16 * i, src + 16 * i);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  uint32_t a0c = 0, a1c = 0, tfa = 0, tfb = 0;
+  if (role < ntiles) {
+    tile_records(a.act, a.tile_first, 0, role, 0, a0c, a1c);
+    stage(a0c, a1c, 0);
+  }
+  if (role + ncta < ntiles) {
+    tfa = __ldg(&a.tile_first[role + ncta]);
+    tfb = __ldg(&a.tile_first[role + ncta + 1]);
+  }
+  int buf = 0;
+  for (uint64_t tile = role; tile < ntiles; tile += ncta, buf ^= 1) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // this tile's records are staged; the other buffer is free
+    uint32_t a0n = 0, a1n = 0;
+    if (tile + ncta < ntiles) {
+      tile_decode(tfa, tfb, a0n, a1n);
+      stage(a0n, a1n, buf ^ 1);
+      if (tile + 2 * ncta < ntiles) {
+        tfa = __ldg(&a.tile_first[tile + 2 * ncta]);
+        tfb = __ldg(&a.tile_first[tile + 2 * ncta + 1]);
+      }
+    }
     const uint64_t x0 = tile * TILE;
     const uint32_t rend = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), total - x0));
-    uint32_t a0, a1;
-    tile_records(a.act, a.tile_first, n_act, tile, x0 + rend, a0, a1);
+    const uint32_t a0 = a0c, a1 = a1c;
     const uint32_t nd = a1 - a0 + 1;
-    const bool staged = nd <= kRecs;
-    __syncthreads();  // previous tile done with the staging buffers
-    if (staged) {
-      for (uint32_t i = threadIdx.x; i < nd; i += kNT) {
-        const ActRec rec = a.act[a0 + i];
-        s_pre[i] = rec.pre > x0 ? static_cast<uint32_t>(rec.pre - x0) : 0u;
-        s_row[i] = a.indices + (rec.a + x0);
-        s_th[i] = rec.b;
-        s_di[i] = rec.di;
-        const uint64_t nx = (i + 1 < nd) ? a.act[a0 + i + 1].pre : ~0ULL;
-        s_nxt[i] = static_cast<uint32_t>(min(nx - x0, static_cast<uint64_t>(0xffffffffu)));
-      }
-      __syncthreads();
-    }
+    a0c = a0n;
+    a1c = a1n;
     const uint32_t r0 = warp * WSPAN;
     if (r0 >= rend) continue;
-    if (staged) {
-      // record of the warp's first position: 32-ary search over s_pre
+    if (nd <= static_cast<uint32_t>(kRecs)) {
+      const ActRec* sa = s_act[buf];
+      // record of the warp's first position: 32-ary search over the starts
       uint32_t lo = 0, hi = nd - 1;
       while (lo < hi) {
         const uint32_t step = (hi - lo + 32) / 32;
         const uint32_t cand = lo + lane_id() * step;
-        const bool le = cand <= hi && s_pre[cand] <= r0;
+        const bool le = cand <= hi && sa[cand].pre <= x0 + r0;
         const unsigned m = __ballot_sync(0xffffffffu, le);
         const uint32_t best = lo + (31 - __clz(m)) * step;
         lo = best;
         hi = min(hi, best + step - 1);
         if (step == 1) break;
       }
-      mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, s_nxt, s_row, s_th,
-                                   s_di, uncert, vtab);
+      mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, sa, nd, uncert,
+                                   vtab);
     } else {
       const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
-      mark_span<IPT, SMOOTH, false>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, s_nxt, s_row,
-                                    s_th, s_di, uncert, vtab);
+      mark_span<IPT, SMOOTH, false>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, nullptr, 0,
+                                    uncert, vtab);
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   if (SMOOTH) {
     uncert = warp_sum(uncert);
     if (lane_id() == 0 && uncert) atomicAdd(&meta->uncertified, uncert);
@@ -854,43 +894,6 @@ __global__ void clear_kernel(uint32_t* bits, uint32_t* summ, const uint32_t* __r
 constexpr int kFrontierIPT = 4;
 constexpr int kLaborIPT = kLaborTile / kNT;
 
-// Software grid barrier for the cooperative fused kernel (all CTAs are
-// co-resident: cudaLaunchCooperativeKernel). `target` = barrier index x grid.
-__device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    while (ld_acquire_u32(ctr) < target) __nanosleep(20);
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-template <bool SMOOTH>
-__global__ void __launch_bounds__(kNT, 2) fused_batch_kernel(const __grid_constant__ FusedParams p) {
-  const unsigned G = gridDim.x, b = blockIdx.x;
-  unsigned k = 0;
-  batch_begin_body(p.epoch, p.overflow, p.tickets, Sync::kMaxTickets, p.clear_bits,
-                   p.clear_summ, p.clear_list, p.clear_count, p.clear_cap, p.clear_nwords, b, G);
-  grid_sync(p.barrier, ++k * G);
-  for (int l = 0; l < p.L; ++l) {
-    const FusedLayer& fl = p.layer[l];
-    frontier_body<kFrontierIPT>(fl.f, fl.relabel_prev, b, G);
-    grid_sync(p.barrier, ++k * G);
-    mark_body<kLaborIPT, SMOOTH>(fl.la, b, G);
-    grid_sync(p.barrier, ++k * G);
-    if (b < p.n_ext) extract_body(fl.ex, b, p.n_ext);
-    else labor_emit_body(fl.la, b - p.n_ext, G - p.n_ext);
-    grid_sync(p.barrier, ++k * G);
-  }
-  relabel_range(p.relabel_last, b * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
-                static_cast<uint64_t>(G) * blockDim.x);
-  if (p.table)
-    gbody::gather_any(p.table, p.vec_bytes, p.vpr, p.gather_ids, p.gather_count, p.cap_rows,
-                      p.row_map, p.rows_out, b, G);
-}
-
 }  // namespace
 
 uint64_t extract_tiles(uint64_t words_padded) {
@@ -984,19 +987,6 @@ void launch_relabel(const RelabelArgs& r, uint64_t work, cudaStream_t st) {
   const int grid = grid_for(work, 256 * 4, 8);
   launch_k(relabel_kernel, grid, 256, st, r);
   CB_LAUNCH("relabel");
-}
-
-void launch_fused(FusedParams& p, bool smooth, cudaStream_t st) {
-  void* args[] = {&p};
-  auto* k = smooth ? fused_batch_kernel<true> : fused_batch_kernel<false>;
-  const int occ = resident_per_sm(k);
-  const int grid = occ * kNumSMs;
-  const uint64_t ext_tiles = p.L > 0 ? extract_tiles(p.layer[0].ex.words_padded) : 1;
-  p.n_ext = static_cast<unsigned>(std::max<uint64_t>(
-      1, std::min<uint64_t>(ext_tiles, static_cast<uint64_t>(grid / 2))));
-  CB_CUDA(cudaMemsetAsync(p.barrier, 0, sizeof(unsigned), st));
-  CB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(kNT),
-                                      args, 0, st));
 }
 
 void launch_rank(const Bitmap& bm, const uint32_t* ids, const unsigned long long* count,
