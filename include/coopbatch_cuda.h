@@ -256,6 +256,11 @@ int cb_shuffled_order(uint64_t n, uint64_t seed, uint32_t* out);
 /* Feature storage tier: 1 = pinned host memory mapped into the device
  * (the paper's storage channel), 0 = HBM. */
 int cb_features_set_tier(cb_features* f, int host);
+/* Asynchronous D2H (on cb_plan_stream) of the batch's per-part, per-layer
+ * counts (n_dst, scan_total, n_active, n_edges, n_src, uncertified, 2 pad;
+ * u64 each, P x (L+1) records) into host_dst (pinned for true asynchrony).
+ * host_dst == NULL: only *bytes is set. */
+int cb_plan_meta_async(cb_plan* plan, void* host_dst, uint64_t* bytes);
 /* Kernels of this library enqueued eagerly by this process so far (CUDA
  * graph replays excluded; for reporting launch counts). */
 int cb_kernel_launches(uint64_t* n);

@@ -83,9 +83,12 @@ class LruCache:
         self._h, self.n_keys, self._cap = h, n_keys, capacity
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.load().cb_cache_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib.load().cb_cache_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: the loader may be gone
+            pass
 
     def capacity(self) -> int:
         return self._cap

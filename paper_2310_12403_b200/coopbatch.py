@@ -176,9 +176,12 @@ class Graph:
         return indptr, indices
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.load().cb_graph_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib.load().cb_graph_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: the loader may be gone
+            pass
 
 
 class PartitionMap:
@@ -203,9 +206,12 @@ class PartitionMap:
         return [m[int(off[q]):int(off[q + 1])] for q in range(self.num_parts)]
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.load().cb_partition_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib.load().cb_partition_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: the loader may be gone
+            pass
 
 
 def partition_random(g: Graph, parts: int, seed: int) -> PartitionMap:
@@ -251,9 +257,12 @@ class FeatureStore:
         _check(_lib.load().cb_features_set_tier(self._h, int(bool(host))))
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.load().cb_features_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib.load().cb_features_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: the loader may be gone
+            pass
 
 
 # ---------------------------------------------------------------- results ---
@@ -328,9 +337,12 @@ class Plan:
         self.P = pm.num_parts if pm else 1
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.load().cb_plan_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib.load().cb_plan_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: the loader may be gone
+            pass
 
     @property
     def stream(self) -> int:

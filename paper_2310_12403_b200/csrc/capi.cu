@@ -1847,6 +1847,17 @@ int cb_features_set_tier(cb_features* f, int host) {
   });
 }
 
+int cb_plan_meta_async(cb_plan* plan, void* host_dst, uint64_t* bytes) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    const uint64_t nb = sizeof(LayerMeta) * plan->P * (plan->L + 1);
+    if (bytes) *bytes = nb;
+    if (!host_dst) return;
+    DeviceGuard dg(plan->device);
+    CB_CUDA(cudaMemcpyAsync(host_dst, plan->meta, nb, cudaMemcpyDeviceToHost, plan->stream));
+  });
+}
+
 int cb_kernel_launches(uint64_t* n) {
   return guard([&] {
     require(n != nullptr, "null argument");

@@ -140,9 +140,12 @@ class CudaEngine:
         self.row_bytes = store.row_bytes if store is not None else 0
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            self.L.cb_plan_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                self.L.cb_plan_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: the loader may be gone
+            pass
 
     # -- helpers --------------------------------------------------------------
     def _dev(self, t: torch.Tensor) -> torch.Tensor:
@@ -298,9 +301,12 @@ class PeerCoop:
         dist.barrier(group=group)  # every mapping is open before anyone writes
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            self.L.cb_plan_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                self.L.cb_plan_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: the loader may be gone
+            pass
 
     def barrier(self):
         if self._nccl:
