@@ -88,6 +88,12 @@ int cb_device_count(int* out);
 /* ---- graph (CSR resident in HBM) ---- */
 int cb_graph_create_from_csr(const uint64_t* indptr, const uint32_t* indices, uint64_t n,
                              uint64_t m, int device, cb_graph** out);
+/* CBCS binary CSR (graph.hpp:78-80; load_csr / save_csr, src/graph.cpp:196-265):
+ * CB_IO when the file cannot be opened/written, CB_FORMAT for a bad magic,
+ * version or truncation, CB_INPUT when validate_csr fails. Weights in a file
+ * are validated and dropped (unweighted sampling). */
+int cb_graph_load_cbcs(const char* path, int device, cb_graph** out);
+int cb_graph_save_cbcs(const cb_graph* g, const char* path);
 int cb_graph_generate_rmat(uint64_t n, uint64_t m, uint64_t seed, int device,
                            cb_graph** out);
 int cb_graph_info(const cb_graph* g, uint64_t* n, uint64_t* m, uint64_t* max_degree);

@@ -168,6 +168,9 @@ def lib(impl: str = "restated") -> C.CDLL:
         L.rf_step.argtypes = [_P, _P, C.c_int, _P, _u32, _P, _P, C.c_int, C.c_int, _u32,
                               C.POINTER(Sched), C.POINTER(_f64), C.POINTER(_f64),
                               C.POINTER(_u64)]
+        L.rf_save_csr.argtypes = [_P, C.c_char_p]
+        L.rf_load_csr.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64),
+                                  C.POINTER(C.POINTER(_u64)), C.POINTER(C.POINTER(_u32))]
         L.rf_lru_new.restype = _P
         L.rf_lru_new.argtypes = [_u64]
         L.rf_lru_access.argtypes = [_P, _u32]
@@ -299,6 +302,25 @@ class RefGraph:
         if getattr(self, "h", None):
             self.L.rf_graph_free(self.h)
             self.h = None
+
+
+def save_csr_reference(g: CSR, path: str):
+    """The reference's save_csr (graph.cpp:216-229) on this CSR."""
+    rg = RefGraph(g)
+    _check(rg.L.rf_save_csr(rg.h, str(path).encode()), rg.L)
+
+
+def load_csr_reference(path: str) -> CSR:
+    """The reference's load_csr (graph.cpp:231-252), incl. validate_csr."""
+    L = lib("reference")
+    n, m = C.c_uint64(), C.c_uint64()
+    ip, ix = C.POINTER(_u64)(), C.POINTER(_u32)()
+    _check(L.rf_load_csr(str(path).encode(), C.byref(n), C.byref(m), C.byref(ip), C.byref(ix)), L)
+    indptr = np.ctypeslib.as_array(ip, (n.value + 1,)).copy()
+    indices = np.ctypeslib.as_array(ix, (max(m.value, 1),))[: m.value].copy()
+    L.rf_free(C.cast(ip, _P))
+    L.rf_free(C.cast(ix, _P))
+    return CSR(indptr, indices)
 
 
 def partition_random(n: int, parts: int, seed: int, impl: str = "restated") -> np.ndarray:

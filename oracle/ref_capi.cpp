@@ -135,6 +135,23 @@ void* rf_graph_new(const uint64_t* indptr, const uint32_t* indices, uint64_t n,
 }
 void rf_graph_free(void* g) { delete static_cast<Graph*>(g); }
 
+/* graph.cpp:216-252 — the reference's own CBCS writer / reader. */
+int rf_save_csr(void* g, const char* path) {
+  return guard([&] { save_csr(*static_cast<Graph*>(g), path); });
+}
+int rf_load_csr(const char* path, uint64_t* n, uint64_t* m, uint64_t** indptr,
+                uint32_t** indices) {
+  return guard([&] {
+    const Graph g = load_csr(path);
+    *n = g.num_vertices;
+    *m = g.indices.size();
+    *indptr = static_cast<uint64_t*>(std::malloc((g.num_vertices + 1) * 8));
+    *indices = static_cast<uint32_t*>(std::malloc(g.indices.size() * 4 + 4));
+    std::memcpy(*indptr, g.indptr.data(), (g.num_vertices + 1) * 8);
+    std::memcpy(*indices, g.indices.data(), g.indices.size() * 4);
+  });
+}
+
 int rf_validate_csr(void* g) {
   return guard([&] { validate_csr(*static_cast<Graph*>(g)); });
 }

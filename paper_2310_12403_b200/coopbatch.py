@@ -169,6 +169,17 @@ class Graph:
     def num_edges(self) -> int:
         return self._m
 
+    @classmethod
+    def load_csr(cls, path: str, device: int = 0) -> "Graph":
+        """load_csr (graph.cpp:231-252): a CBCS file straight into HBM."""
+        h = C.c_void_p()
+        _check(_lib.load().cb_graph_load_cbcs(str(path).encode(), device, C.byref(h)))
+        return cls(h, device)
+
+    def save_csr(self, path: str):
+        """save_csr (graph.cpp:216-229)."""
+        _check(_lib.load().cb_graph_save_cbcs(self._h, str(path).encode()))
+
     def download(self):
         indptr = np.zeros(self.num_vertices + 1, np.uint64)
         indices = np.zeros(self._m, np.uint32)

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -799,6 +800,71 @@ int cb_graph_create_from_csr(const uint64_t* indptr, const uint32_t* indices, ui
     for (uint64_t v = 0; v < n; ++v) md = std::max(md, indptr[v + 1] - indptr[v]);
     h->g.max_degree = md;
     *out = h.release();
+  });
+}
+
+// CBCS binary CSR (graph.hpp:78-80, graph.cpp:196-265): "CBCS", u32 version 1,
+// u64 n, u64 m, u64 indptr[n+1], u32 indices[m], u8 flags, f32 weights[m] if
+// flags & 1. Little-endian. Weights are validated (> 0) and not kept: the
+// device path samples unweighted (LABOR-0 / NS / FULL).
+int cb_graph_load_cbcs(const char* path, int device, cb_graph** out) {
+  return guard([&] {
+    require(path != nullptr && out != nullptr, "null argument");
+    FILE* f = std::fopen(path, "rb");
+    if (!f) throw Error(kIo, std::string("cannot open: ") + path);
+    std::unique_ptr<FILE, int (*)(FILE*)> guard_f(f, &std::fclose);
+    auto rd = [&](void* dst, size_t bytes, const char* what) {
+      if (bytes && std::fread(dst, 1, bytes, f) != bytes)
+        throw Error(kFormat, std::string("csr file truncated reading ") + what);
+    };
+    char magic[4];
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "CBCS", 4) != 0)
+      throw Error(kFormat, std::string("not a CBCS file: ") + path);
+    uint32_t version = 0;
+    rd(&version, 4, "version");
+    if (version != 1) throw Error(kFormat, "unsupported CBCS version " + std::to_string(version));
+    uint64_t n = 0, m = 0;
+    rd(&n, 8, "num_vertices");
+    rd(&m, 8, "num_edges");
+    std::vector<uint64_t> indptr(n + 1);
+    std::vector<uint32_t> indices(m);
+    rd(indptr.data(), (n + 1) * 8, "indptr");
+    rd(indices.data(), m * 4, "indices");
+    uint8_t flags = 0;
+    rd(&flags, 1, "flags");
+    if (flags & 1) {
+      std::vector<float> w(m);
+      rd(w.data(), m * 4, "weights");
+      for (float x : w) require(x > 0.0f, "csr: weights must be > 0");
+    }
+    const int rc = cb_graph_create_from_csr(indptr.data(), indices.data(), n, m, device, out);
+    if (rc != CB_OK) throw Error(static_cast<Status>(rc), g_err);
+  });
+}
+
+int cb_graph_save_cbcs(const cb_graph* g, const char* path) {
+  return guard([&] {
+    require(g != nullptr && path != nullptr, "null argument");
+    std::vector<uint64_t> indptr(g->g.n + 1);
+    std::vector<uint32_t> indices(g->g.m);
+    {
+      DeviceGuard dg(g->g.device);
+      CB_CUDA(cudaMemcpy(indptr.data(), g->g.indptr, (g->g.n + 1) * 8, cudaMemcpyDeviceToHost));
+      if (g->g.m)
+        CB_CUDA(cudaMemcpy(indices.data(), g->g.indices, g->g.m * 4, cudaMemcpyDeviceToHost));
+    }
+    FILE* f = std::fopen(path, "wb");
+    if (!f) throw Error(kIo, std::string("cannot open for write: ") + path);
+    std::unique_ptr<FILE, int (*)(FILE*)> guard_f(f, &std::fclose);
+    const uint32_t version = 1;
+    const uint64_t n = g->g.n, m = g->g.m;
+    const uint8_t flags = 0;
+    bool ok = std::fwrite("CBCS", 1, 4, f) == 4 && std::fwrite(&version, 4, 1, f) == 1 &&
+              std::fwrite(&n, 8, 1, f) == 1 && std::fwrite(&m, 8, 1, f) == 1 &&
+              std::fwrite(indptr.data(), 8, n + 1, f) == n + 1 &&
+              (m == 0 || std::fwrite(indices.data(), 4, m, f) == m) &&
+              std::fwrite(&flags, 1, 1, f) == 1;
+    if (!ok) throw Error(kIo, std::string("write failed: ") + path);
   });
 }
 

@@ -84,3 +84,43 @@ def test_build_artifacts_in_tree():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     assert os.path.exists(os.path.join(root, "paper_2310_12403_b200", "libcoopbatch_b200.so"))
     assert os.path.exists(os.path.join(root, "oracle", "liboracle.so"))
+
+
+def test_cbcs_errors_before_any_device_work(tmp_path):
+    """load_csr's error taxonomy (graph.cpp:231-284) through the C-ABI:
+    IoError / FormatError / InputError map to CB_IO / CB_FORMAT / CB_INPUT,
+    decided on the host before any device allocation."""
+    import struct
+
+    import paper_2310_12403_b200 as cb
+    with pytest.raises(OSError) as e:
+        cb.Graph.load_csr(str(tmp_path / "missing.cbcs"))
+    assert "cannot open" in str(e.value)
+    bad = tmp_path / "bad.cbcs"
+    bad.write_bytes(b"XXXX" + b"\0" * 32)
+    with pytest.raises(cb.FormatError):
+        cb.Graph.load_csr(str(bad))
+    trunc = tmp_path / "trunc.cbcs"
+    trunc.write_bytes(b"CBCS" + struct.pack("<IQQ", 1, 3, 2) + struct.pack("<QQ", 0, 1))
+    with pytest.raises(cb.FormatError, match="truncated"):
+        cb.Graph.load_csr(str(trunc))
+    ver = tmp_path / "ver.cbcs"
+    ver.write_bytes(b"CBCS" + struct.pack("<I", 7))
+    with pytest.raises(cb.FormatError, match="version"):
+        cb.Graph.load_csr(str(ver))
+    inv = tmp_path / "inv.cbcs"  # indices out of range -> validate_csr InputError
+    inv.write_bytes(b"CBCS" + struct.pack("<IQQ", 1, 2, 1) + struct.pack("<QQQ", 0, 1, 1)
+                    + struct.pack("<I", 5) + b"\0")
+    with pytest.raises(cb.InputError, match="out of range"):
+        cb.Graph.load_csr(str(inv))
+
+
+def test_reference_cbcs_roundtrip_oracle(tmp_path):
+    """The compiled reference's save_csr/load_csr (the fixture writer the GPU
+    test reads back) round-trips a graph."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    g = O.rmat(500, 3000, 4)
+    O.save_csr_reference(g, tmp_path / "g.cbcs")
+    h = O.load_csr_reference(tmp_path / "g.cbcs")
+    assert np.array_equal(h.indptr, g.indptr) and np.array_equal(h.indices, g.indices)
