@@ -21,7 +21,7 @@ using namespace cbdev;
 namespace {
 
 template <typename V, int UNROLL>
-__global__ void __launch_bounds__(256) gather_kernel(
+__global__ void __launch_bounds__(256, 8) gather_kernel(
     const V* __restrict__ table, const uint32_t* __restrict__ ids,
     const unsigned long long* __restrict__ count, uint64_t cap_rows,
     const uint32_t* __restrict__ row_map, uint32_t vpr, V* __restrict__ out) {

@@ -64,14 +64,16 @@ __device__ __forceinline__ void gather_body(const V* __restrict__ table,
                                             uint64_t cap_rows, const uint32_t* __restrict__ row_map,
                                             uint32_t vpr, V* __restrict__ out, unsigned role,
                                             unsigned ncta) {
-  // count == nullptr: cap_rows is the row count itself
-  const uint64_t n = count ? min(static_cast<uint64_t>(*count), cap_rows) : cap_rows;
-  const uint64_t total = n * vpr;
   const uint64_t stride = static_cast<uint64_t>(ncta) * blockDim.x;
-  if (total + stride * UNROLL < (1ULL << 32)) {
-    const uint32_t tot32 = static_cast<uint32_t>(total), s32 = static_cast<uint32_t>(stride);
+  if (cap_rows * vpr + stride * UNROLL < (1ULL << 32)) {
+    // the row count (written by the previous kernel) is loaded together with
+    // the first ids, which are read speculatively within the capacity
+    const unsigned long long cnt = count ? __ldg(count) : cap_rows;
+    const uint32_t s32 = static_cast<uint32_t>(stride);
     const uint32_t magic = 0xffffffffu / vpr;
-    for (uint32_t idx = role * blockDim.x + threadIdx.x; idx < tot32; idx += s32 * UNROLL) {
+    const uint32_t last = static_cast<uint32_t>(cap_rows ? cap_rows - 1 : 0);
+    uint32_t tot32 = 0xffffffffu;
+    for (uint32_t idx = role * blockDim.x + threadIdx.x;; idx += s32 * UNROLL) {
       uint32_t r[UNROLL], c[UNROLL];
       V buf[UNROLL];
 #pragma unroll
@@ -83,14 +85,18 @@ __device__ __forceinline__ void gather_body(const V* __restrict__ table,
           ++q;
           rem -= vpr;
         }
-        r[u] = x < tot32 ? q : 0u;
+        r[u] = min(q, last);
         c[u] = rem;
       }
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) r[u] = __ldg(ids + r[u]);
+      if (tot32 == 0xffffffffu)
+        tot32 = static_cast<uint32_t>(min(static_cast<uint64_t>(cnt), cap_rows) * vpr);
+      if (idx >= tot32) break;
       if (row_map) {
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) r[u] = __ldg(row_map + r[u]);
+        for (int u = 0; u < UNROLL; ++u)
+          if (idx + u * s32 < tot32) r[u] = __ldg(row_map + r[u]);
       }
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u)
@@ -104,6 +110,8 @@ __device__ __forceinline__ void gather_body(const V* __restrict__ table,
     }
     return;
   }
+  const uint64_t n = count ? min(static_cast<uint64_t>(*count), cap_rows) : cap_rows;
+  const uint64_t total = n * vpr;
   uint64_t idx = role * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   for (; idx < total; idx += stride * UNROLL) {
     V buf[UNROLL];

@@ -103,6 +103,36 @@ __global__ void __launch_bounds__(256) g_flat32(const uint4* __restrict__ t, con
   }
 }
 
+template <int U>
+__global__ void __launch_bounds__(256, 8) g_flat32_lb8(const uint4* __restrict__ t, const unsigned* __restrict__ ids,
+                                                unsigned n, unsigned vpr, unsigned magic,
+                                                uint4* __restrict__ out) {
+  const unsigned total = n * vpr, stride = gridDim.x * blockDim.x;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride * U) {
+    unsigned r[U], c[U], v[U];
+    uint4 b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned x = i + u * stride;
+      unsigned q = __umulhi(x, magic);
+      unsigned rem = x - q * vpr;
+      if (rem >= vpr) { ++q; rem -= vpr; }
+      r[u] = x < total ? q : 0u;
+      c[u] = rem;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldg(ids + r[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i + u * stride < total) b[u] = ldnc(t + 1ull * v[u] * vpr + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned x = i + u * stride;
+      if (x < total) __stcs(out + x, b[u]);
+    }
+  }
+}
+
 int main() {
   const unsigned nrows = 2449029, vpr = 25, n = 54874;
   uint4 *table, *out;
@@ -149,13 +179,19 @@ int main() {
     printf("%-34s avg %6.2f us  best %6.2f us  %6.0f GB/s (avg)\n", name, avg * 1e3, best * 1e3,
            bytes / (avg * 1e-3) / 1e9);
   };
-  for (int rf = 0; rf < 2; ++rf)
+  for (int rf = 1; rf < 2; ++rf)
   for (int g : {148 * 4, 148 * 8}) {
     readflush = rf;
     printf("-- flush: %s\n", rf ? "write 512MB + read 256MB" : "write 512MB");
     char nm[64];
     const unsigned magic = (unsigned)((1ull << 32) / vpr);
-    for (int gg : {148 * 5, 148 * 6, 148 * 8}) {
+    for (int gg : {148 * 8, 148 * 16}) {
+      snprintf(nm, 64, "flat32lb8 U=4 grid=%d", gg);
+      run(nm, [&] { g_flat32_lb8<4><<<gg, 256, 0, st>>>(table, ids, n, vpr, magic, out); });
+      snprintf(nm, 64, "flat32lb8 U=2 grid=%d", gg);
+      run(nm, [&] { g_flat32_lb8<2><<<gg, 256, 0, st>>>(table, ids, n, vpr, magic, out); });
+    }
+    for (int gg : {148 * 5, 148 * 8}) {
       snprintf(nm, 64, "flat32 U=4 grid=%d", gg);
       run(nm, [&] { g_flat32<4><<<gg, 256, 0, st>>>(table, ids, n, vpr, magic, out); });
       snprintf(nm, 64, "flat32 U=8 grid=%d", gg);
