@@ -543,6 +543,48 @@ def coop_sample(g: Graph, pm: PartitionMap, per_pe_seeds, num_layers: int,
                             [pl.owner_set(p) for p in range(pl.P)])
 
 
+@dataclass
+class LayerMetrics:  # coop.hpp:157-162
+    s_l: int = 0            # |S^l_p| (block destinations)
+    s_tilde_l: int = 0      # |S~^{l+1}_p| (block sources)
+    e_l: int = 0            # |E^l_p|
+    comm_vertices: int = 0  # ids this part sent away at this layer
+
+
+@dataclass
+class PeMetrics:  # coop.hpp:164-168
+    layers: list[LayerMetrics] = field(default_factory=list)
+    feat_bytes: int = 0
+    input_rows: int = 0
+
+
+def step_metrics(plan: Plan, mode: int, row_bytes: int) -> list[PeMetrics]:
+    """The per-PE metrics coop_train_step / indep_train_step report
+    (block_metrics, coop.cpp:428-434; comm_vertices = ExchangeRecord::
+    communicated, coop.cpp:543-546; feat_bytes / input_rows from the rows each
+    part loads: its owner set when cooperative, coop.cpp:456-460, its input
+    vertices when independent, coop.cpp:579-581), read from the device counts
+    of the plan's last batch."""
+    out = []
+    coop = mode == MODE_COOP and plan.P > 1
+    ex = [plan.exchange(l) for l in range(plan.L)] if coop else None
+    for p in range(plan.P):
+        pm_ = PeMetrics()
+        for l in range(plan.L):
+            sz = plan.layer_sizes(p, l)
+            pm_.layers.append(LayerMetrics(sz["n_dst"], sz["n_src"], sz["n_edges"],
+                                           ex[l].communicated(p) if coop else 0))
+        n = C.c_uint64()
+        if coop:
+            _check(_lib.load().cb_owner_set_size(plan._h, p, C.byref(n)))
+            pm_.input_rows = n.value
+        else:
+            pm_.input_rows = pm_.layers[-1].s_tilde_l
+        pm_.feat_bytes = pm_.input_rows * row_bytes
+        out.append(pm_)
+    return out
+
+
 def load_inputs(g: Graph, pm: PartitionMap | None, per_pe_seeds, num_layers: int,
                 cfg: SamplerConfig, schedule: SeedSchedule, store: FeatureStore,
                 mode: int = MODE_COOP) -> list[np.ndarray]:

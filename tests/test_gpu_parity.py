@@ -246,6 +246,30 @@ def test_coop_parity_c1(c1, P, kind, okind):
         coop_eq(res, exp, P, 3, f"P={P} {kind.name} step={step}")
 
 
+def test_step_metrics_match_reference_definitions(c1):
+    """LayerMetrics / PeMetrics (coop.hpp:157-168) as coop_train_step fills
+    them (coop.cpp:456-460, 541-546), from the oracle's coop_sample."""
+    g, ref = c1
+    P = 4
+    pm = cb.partition_random(g, P, 23)
+    owner = O.partition_random(ref.n, P, 23)
+    seeds = O.draw_coop_seeds(owner, P, 100, 23, 0)
+    sched = cb.SeedSchedule.plain(9)
+    plan = cb.Plan(g, pm, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), 100)
+    plan.sample(seeds, sched, cb.MODE_COOP)
+    got = cb.step_metrics(plan, cb.MODE_COOP, 400)
+    exp = O.coop_sample(ref, owner, P, seeds, 3, O.LABOR0, 10, osched(sched))
+    for p in range(P):
+        for l in range(3):
+            b = exp["stacks"][p][l]
+            sc = exp["exchanges"][l]["send_counts"][p]
+            want = (len(b["dst"]), len(b["src"]), len(b["edges"]), int(sc.sum() - sc[p]))
+            m = got[p].layers[l]
+            assert (m.s_l, m.s_tilde_l, m.e_l, m.comm_vertices) == want, (p, l)
+        assert got[p].input_rows == len(exp["owner_sets"][p])
+        assert got[p].feat_bytes == 400 * len(exp["owner_sets"][p])
+
+
 def test_coop_union_property(c1):
     """test_coop.cpp:128-157: cooperative input set == single-part union batch."""
     g, ref = c1
