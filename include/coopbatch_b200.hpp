@@ -35,12 +35,15 @@ inline void check(int rc) {
   throw DeviceError(msg);
 }
 
-enum class SamplerKind { kFull = CB_FULL, kNs = CB_NS, kLabor0 = CB_LABOR0 };
+enum class SamplerKind { kFull = CB_FULL, kNs = CB_NS, kLabor0 = CB_LABOR0, kRw = CB_RW };
 
 struct SamplerConfig {  // samplers.hpp:17-23 (+ per-layer fanouts extension)
   SamplerKind kind = SamplerKind::kNs;
   std::uint32_t fanout = 10;
   std::vector<std::uint32_t> fanouts;  // empty -> fanout at every layer
+  std::uint32_t rw_length = 3;  // o
+  double rw_restart = 0.5;      // p
+  std::uint32_t rw_walks = 100; // a
 
   std::vector<std::uint32_t> per_layer(int L) const {
     if (!fanouts.empty()) {
@@ -180,7 +183,10 @@ inline PlanPtr make_plan(const Graph& g, const PartitionMap* pm, int L, const Sa
   cb_plan* pl = nullptr;
   check(cb_plan_create(g.get(), pm ? pm->get() : nullptr, L, static_cast<int>(cfg.kind),
                        fo.data(), max_seeds ? max_seeds : 1, &pl));
-  return PlanPtr(pl);
+  PlanPtr plan(pl);
+  if (cfg.kind == SamplerKind::kRw)
+    check(cb_plan_set_rw(pl, cfg.rw_length, cfg.rw_restart, cfg.rw_walks));
+  return plan;
 }
 
 }  // namespace detail

@@ -63,7 +63,7 @@ enum {
 };
 
 /* SamplerKind order of samplers.hpp:15 */
-enum { CB_FULL = 0, CB_NS = 1, CB_LABOR0 = 2 };
+enum { CB_FULL = 0, CB_NS = 1, CB_LABOR0 = 2, CB_RW = 3 };
 enum { CB_MODE_COOP = 0, CB_MODE_INDEP = 1 };
 enum { CB_F64 = 0, CB_F32 = 1, CB_F16 = 2 };
 
@@ -262,6 +262,10 @@ int cb_shuffled_order(uint64_t n, uint64_t seed, uint32_t* out);
 /* Feature storage tier: 1 = pinned host memory mapped into the device
  * (the paper's storage channel), 0 = HBM. */
 int cb_features_set_tier(cb_features* f, int host);
+/* SamplerConfig's random-walk parameters (samplers.hpp:19-22) of a CB_RW
+ * plan: rw_length o >= 1, rw_restart p in [0,1), rw_walks a >= 1, with
+ * a*o <= 512 visits per dst on the device. Defaults 3 / 0.5 / 100. */
+int cb_plan_set_rw(cb_plan* plan, uint32_t rw_length, double rw_restart, uint32_t rw_walks);
 /* Asynchronous D2H (on cb_plan_stream) of the batch's per-part, per-layer
  * counts (n_dst, scan_total, n_active, n_edges, n_src, uncertified, 2 pad;
  * u64 each, P x (L+1) records) into host_dst (pinned for true asynchrony).

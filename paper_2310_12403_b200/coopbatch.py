@@ -80,6 +80,7 @@ class SamplerKind(enum.IntEnum):  # samplers.hpp:15
     kFull = 0
     kNs = 1
     kLabor0 = 2
+    kRw = 3
 
 
 @dataclass
@@ -87,6 +88,9 @@ class SamplerConfig:  # samplers.hpp:17-23 (+ per-layer fanouts extension)
     kind: SamplerKind = SamplerKind.kNs
     fanout: int = 10
     fanouts: list[int] | None = None  # fanouts[l] applies at block l
+    rw_length: int = 3      # o (samplers.hpp:20-22)
+    rw_restart: float = 0.5  # p
+    rw_walks: int = 100     # a
 
     def layer_fanouts(self, num_layers: int) -> list[int]:
         if self.fanouts:
@@ -345,6 +349,8 @@ class Plan:
                                           int(cfg.kind), _ptr(fo), max_seeds_per_part,
                                           C.byref(h)))
         self._h = h
+        if cfg.kind == SamplerKind.kRw:
+            _check(_lib.load().cb_plan_set_rw(h, cfg.rw_length, cfg.rw_restart, cfg.rw_walks))
         self.P = pm.num_parts if pm else 1
 
     def __del__(self):
@@ -484,7 +490,7 @@ _plan_cache: dict = {}
 
 def _plan_for(g: Graph, pm, num_layers: int, cfg: SamplerConfig, n_seeds: int) -> Plan:
     key = (id(g), id(pm) if pm else None, num_layers, int(cfg.kind),
-           tuple(cfg.layer_fanouts(num_layers)))
+           tuple(cfg.layer_fanouts(num_layers)), cfg.rw_length, cfg.rw_restart, cfg.rw_walks)
     pl = _plan_cache.get(key)
     if pl is None or pl.max_seeds < n_seeds or pl.g is not g or pl.pm is not pm:
         pl = Plan(g, pm, num_layers, cfg, max(n_seeds, 1))
@@ -513,6 +519,15 @@ def sample_ns(g: Graph, seeds, k: int, epoch_seed: int) -> BipartiteBlock:
     if k == 0:
         raise InputError("sample_ns: fanout must be >= 1")
     return expand(g, seeds, 1, SamplerConfig(SamplerKind.kNs, k),
+                  SeedSchedule.plain(epoch_seed)).blocks[0]
+
+
+def sample_rw(g: Graph, seeds, cfg: SamplerConfig, epoch_seed: int) -> BipartiteBlock:
+    """samplers.cpp:314-321 (layer 0): random walks with restart, top-k visits."""
+    if cfg.rw_length < 1 or cfg.rw_walks < 1:
+        raise InputError("sample_rw: rw_length and rw_walks must be >= 1")
+    return expand(g, seeds, 1, SamplerConfig(SamplerKind.kRw, cfg.fanout, None, cfg.rw_length,
+                                             cfg.rw_restart, cfg.rw_walks),
                   SeedSchedule.plain(epoch_seed)).blocks[0]
 
 

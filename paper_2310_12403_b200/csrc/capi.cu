@@ -218,6 +218,8 @@ struct cb_plan {
   uint64_t batches = 0;
   uint64_t launches = 0;  // kernels enqueued by the last cb_sample (+ cb_gather)
   double* vtab = nullptr;  // smoothed LABOR r_t table [n] (nullptr: per position)
+  uint32_t rw_length = 3, rw_walks = 100;  // samplers.hpp:19-22 defaults
+  double rw_restart = 0.5;
   std::unique_ptr<PxState> px;  // multi-process peer exchange (dist plans)
   std::vector<uint64_t> seeds_off;
   // CUDA graphs of one batch (sample) and its gather, replayed per step
@@ -280,11 +282,12 @@ void plan_alloc(cb_plan* pl) {
       const uint64_t sum_deg = (l == 0) ? sat_mul(cd, maxdeg) : std::min(m, sat_mul(cd, maxdeg));
       uint64_t est;
       if (pl->kind == CB_FULL) est = sum_deg;
-      else if (pl->kind == CB_NS) est = sat_mul(cd, k);
+      else if (pl->kind == CB_NS || pl->kind == CB_RW) est = sat_mul(cd, k);
       else est = sat_mul(cd, 2 * k) + 4096;
       if (pl->kind != CB_FULL) est = static_cast<uint64_t>(std::ceil(est * pl->grow));
       uint64_t cap_e = std::max<uint64_t>(1, std::min(est, sum_deg));
-      if (pl->kind == CB_NS) cap_e = std::min(cap_e, sat_mul(cd, k));
+      if (pl->kind == CB_NS || pl->kind == CB_RW) cap_e = std::min(cap_e, sat_mul(cd, k));
+      if (pl->kind == CB_RW) cap_e = std::max<uint64_t>(sat_mul(cd, k), 1);
       LayerBufs& b = w.L[l];
       b.cap_dst = cd;
       b.cap_edges = std::max<uint64_t>(cap_e, 1);
@@ -292,8 +295,9 @@ void plan_alloc(cb_plan* pl) {
       if (l == 0) b.dst = nullptr;  // seeds live in pl->seeds
       else b.dst = pl->mem.alloc<uint32_t>(cd);
       b.act = pl->mem.alloc<ActRec>(cd + 1);
-      b.out_prefix = pl->kind == CB_NS ? pl->mem.alloc<uint64_t>(cd + 1) : nullptr;
-      b.slots = pl->kind == CB_NS ? pl->mem.alloc<uint32_t>(b.cap_edges) : nullptr;
+      const bool nsrw = pl->kind == CB_NS || pl->kind == CB_RW;
+      b.out_prefix = nsrw ? pl->mem.alloc<uint64_t>(cd + 1) : nullptr;
+      b.slots = nsrw ? pl->mem.alloc<uint32_t>(b.cap_edges) : nullptr;
       b.edges = pl->mem.alloc<uint2>(b.cap_edges);
       b.src = pl->mem.alloc<uint32_t>(b.cap_src);
       b.dst_pos = pl->mem.alloc<uint32_t>(cd);
@@ -575,6 +579,35 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   const LaborArgs la = labor_args(pl, w, p, l, D, set_bm);
   if (pl->kind == CB_NS) {
     launch_ns(la, D, b.out_prefix, g.indptr, g.indices, cap_dst, smooth, st);
+    prof_mark(pl);
+    launch_extract(ex, st);
+    prof_mark(pl);
+    return 4;
+  }
+  if (pl->kind == CB_RW) {
+    RwArgs ra{};
+    ra.D = D;
+    ra.meta = la.meta;
+    ra.indptr = g.indptr;
+    ra.indices = g.indices;
+    ra.layer = l;
+    ra.k = pl->fanouts[l];
+    ra.walks = pl->rw_walks;
+    ra.length = pl->rw_length;
+    ra.restart = pl->rw_restart;
+    ra.var = pl->var;
+    ra.bits = set_bm.bits;
+    ra.summ = set_bm.summ;
+    ra.slots = b.slots;
+    ra.cnt = b.out_prefix;
+    ra.edges = b.edges;
+    ra.cap_edges = b.cap_edges;
+    ra.status = w.sync.status_c;
+    ra.epoch = w.sync.epoch;
+    ra.slot = 8 * l + 6;
+    ra.ticket = w.sync.tickets + 3 * l + 1;
+    ra.overflow = w.sync.overflow;
+    launch_rw(ra, cap_dst, smooth, st);
     prof_mark(pl);
     launch_extract(ex, st);
     prof_mark(pl);
@@ -1073,7 +1106,7 @@ int cb_plan_create(const cb_graph* g, const cb_partition* pm, int num_layers, in
     require(g != nullptr, "null graph");
     require(num_layers >= 1, "expand: num_layers must be >= 1");
     require(num_layers <= 8, "at most 8 layers");
-    require(kind == CB_FULL || kind == CB_NS || kind == CB_LABOR0,
+    require(kind == CB_FULL || kind == CB_NS || kind == CB_LABOR0 || kind == CB_RW,
             "sample_block: unknown sampler kind");
     require(fanouts != nullptr || kind == CB_FULL, "null fanouts");
     require(pm == nullptr || pm->n == g->g.n, "partition does not cover the graph");
@@ -1467,7 +1500,7 @@ int cb_plan_create_dist(const cb_graph* g, uint32_t world, int num_layers, int k
     require(world >= 1 && world <= kDistMaxParts, "world size must be in [1, 64]");
     require(num_layers >= 1, "coop_sample: num_layers must be >= 1");
     require(num_layers <= 8, "at most 8 layers");
-    require(kind == CB_FULL || kind == CB_NS || kind == CB_LABOR0,
+    require(kind == CB_FULL || kind == CB_NS || kind == CB_LABOR0 || kind == CB_RW,
             "sample_block: unknown sampler kind");
     DeviceGuard dg(g->g.device);
     auto pl = std::make_unique<cb_plan>();
@@ -1686,7 +1719,7 @@ int cb_plan_trace(cb_plan* plan, uint64_t* out, uint64_t n) {
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n) {
   return guard([&] {
     require(plan != nullptr && n != nullptr, "null argument");
-    const uint64_t samp = (plan->kind == CB_NS) ? 4 : 3;  // incl. extract
+    const uint64_t samp = (plan->kind == CB_NS || plan->kind == CB_RW) ? 4 : 3;  // incl. extract
     const uint64_t P = plan->P;
     const uint64_t L = plan->L;
     uint64_t k;
@@ -1910,6 +1943,20 @@ int cb_features_set_tier(cb_features* f, int host) {
       f->table = f->hbm_table;
       f->hbm_table = nullptr;
     }
+  });
+}
+
+int cb_plan_set_rw(cb_plan* plan, uint32_t rw_length, double rw_restart, uint32_t rw_walks) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require(rw_length >= 1 && rw_walks >= 1, "sample_rw: rw_length and rw_walks must be >= 1");
+    require(rw_restart >= 0.0 && rw_restart < 1.0, "sample_rw: rw_restart must be in [0, 1)");
+    require(static_cast<uint64_t>(rw_length) * rw_walks <= kRwMaxVisits,
+            "rw_walks * rw_length must be <= 512 on the device");
+    plan->rw_length = rw_length;
+    plan->rw_restart = rw_restart;
+    plan->rw_walks = rw_walks;
+    plan->drop_graphs();
   });
 }
 

@@ -200,6 +200,31 @@ struct LaborArgs {
   unsigned* overflow;
 };
 
+// Random walks with restart (samplers.cpp:202-285 rw_block), one warp per dst.
+struct RwArgs {
+  const uint32_t* D;
+  LayerMeta* meta;
+  const uint64_t* indptr;
+  const uint32_t* indices;
+  int layer;
+  uint32_t k;            // fanout: top-k visited vertices per dst
+  uint32_t walks, length;
+  double restart;        // p
+  const cbdev::Variates* var;
+  uint32_t* bits;
+  uint32_t* summ;
+  uint32_t* slots;       // [cap_dst * k] ranked picks per dst
+  uint64_t* cnt;         // [cap_dst] picks per dst
+  uint2* edges;
+  uint64_t cap_edges;
+  unsigned long long* status;
+  const unsigned* epoch;
+  int slot;
+  unsigned* ticket;
+  unsigned* overflow;
+};
+constexpr uint32_t kRwMaxVisits = 512;  // rw_walks * rw_length per dst on the device
+
 struct ExtractArgs {
   const uint32_t* bits;
   const uint32_t* summ;
@@ -248,6 +273,7 @@ void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix
                const uint64_t* indptr, const uint32_t* indices, uint64_t cap_dst, bool smooth,
                cudaStream_t st);
 void launch_extract(const ExtractArgs& a, cudaStream_t st);
+void launch_rw(const RwArgs& a, uint64_t cap_dst, bool smooth, cudaStream_t st);
 void launch_labor_post(const LaborArgs& a, uint64_t max_tiles, const ExtractArgs& e,
                        cudaStream_t st);
 void launch_relabel(const RelabelArgs& r, uint64_t work, cudaStream_t st);

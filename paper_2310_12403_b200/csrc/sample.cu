@@ -704,6 +704,185 @@ __global__ void __launch_bounds__(kNT) ns_emit_kernel(
   }
 }
 
+// -------------------------------------------------------------------- RW --
+// rw_block (samplers.cpp:202-285): per dst s, rw_walks walks of rw_length
+// steps; step j of walk w draws u = U(hash(hash(prefix{3, layer, s}, w), j))
+// (smoothed when kappa says so); after the first step a restart coin takes the
+// [0,p) slice and the remainder is rescaled; the next vertex is
+// indices[beg + (u64)(u*d)]; visits of s itself are not counted; the k most
+// visited vertices (ties: smaller id) become the dst's edges, in rank order.
+// One warp per dst: lane-strided walks, the visits sorted in shared memory,
+// top-k by warp arg-max rounds.
+constexpr int kRwWarps = kNT / 32;
+
+template <bool SMOOTH>
+__global__ void __launch_bounds__(kNT) rw_walk_kernel(RwArgs a) {
+  pdl_begin();
+  constexpr uint32_t kDead = 0xfffffffeu, kNone = 0xffffffffu;
+  __shared__ uint32_t s_vis[kRwWarps][kRwMaxVisits];  // visit of (step, walk); then ids
+  __shared__ uint32_t s_key[kRwWarps][kRwMaxVisits];  // sorted visited ids
+  __shared__ uint16_t s_cc[kRwWarps][kRwMaxVisits];   // visit count per candidate
+  const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
+  uint32_t* vis = s_vis[wib];
+  uint32_t* key = s_key[wib];
+  uint16_t* cc = s_cc[wib];
+  const uint64_t n = a.meta->n_dst;
+  const Variates v = *a.var;
+  const uint64_t z1p = hstep(hstep(hinit(v.z1), 3ULL), static_cast<uint64_t>(a.layer));
+  const uint64_t z2p = SMOOTH ? hstep(hstep(hinit(v.z2), 3ULL), static_cast<uint64_t>(a.layer))
+                              : 0ULL;
+  const uint32_t nv = a.walks * a.length;
+  const double p = a.restart;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kRwWarps;
+  for (uint64_t di = static_cast<uint64_t>(blockIdx.x) * kRwWarps + wib; di < n; di += nw) {
+    const uint32_t s = a.D[di];
+    const uint64_t h1 = hstep(z1p, s), h2 = SMOOTH ? hstep(z2p, s) : 0ULL;
+    // round-major walks (samplers.cpp:228-260); the walk's current vertex is
+    // its previous visit, kDead once it hit a dead end
+    for (uint32_t j = 0; j < a.length; ++j) {
+      for (uint32_t w = lane; w < a.walks; w += 32) {
+        const uint32_t cur = (j == 0) ? s : vis[(j - 1) * a.walks + w];
+        uint32_t out = kDead;
+        if (cur != kDead) {
+          const uint64_t b1 = hstep(hstep(h1, w), j);
+          double u = SMOOTH ? smooth_finish(v, b1, hstep(hstep(h2, w), j)) : ufb(b1);
+          uint32_t from = cur;
+          if (j > 0 && p > 0.0) {
+            if (u < p) {
+              from = s;
+              u = __ddiv_rn(u, p);
+            } else {
+              u = __ddiv_rn(__dsub_rn(u, p), __dsub_rn(1.0, p));
+            }
+          }
+          const uint64_t beg = __ldg(a.indptr + from);
+          const uint64_t d = __ldg(a.indptr + from + 1) - beg;
+          if (d != 0) {
+            uint64_t idx = __double2ull_rz(__dmul_rn(u, static_cast<double>(d)));
+            if (idx >= d) idx = d - 1;
+            out = __ldg(a.indices + beg + idx);
+          }
+        }
+        vis[j * a.walks + w] = out;
+      }
+      __syncwarp();
+    }
+    // counted visits: every next != s (samplers.cpp:258)
+    for (uint32_t i = lane; i < kRwMaxVisits; i += 32) {
+      const uint32_t x = i < nv ? vis[i] : kNone;
+      key[i] = (x == s || x == kDead) ? kNone : x;
+    }
+    __syncwarp();
+    // bitonic sort (ascending), whole warp
+    for (uint32_t size = 2; size <= kRwMaxVisits; size <<= 1) {
+      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+        for (uint32_t t = lane; t < kRwMaxVisits / 2; t += 32) {
+          const uint32_t i = 2 * t - (t & (stride - 1));
+          const uint32_t jj = i + stride;
+          const bool up = ((i & size) == 0);
+          const uint32_t x = key[i], y = key[jj];
+          if ((x > y) == up) {
+            key[i] = y;
+            key[jj] = x;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    // distinct ids with their visit counts, compacted (ids -> vis, counts -> cc)
+    uint32_t ncand = 0;
+    for (uint32_t base = 0; base < kRwMaxVisits; base += 32) {
+      const uint32_t i = base + lane;
+      const uint32_t x = key[i];
+      const bool start = x != kNone && (i == 0 || key[i - 1] != x);
+      uint32_t c = 0;
+      if (start) {
+        uint32_t e = i + 1;
+        while (e < kRwMaxVisits && key[e] == x) ++e;
+        c = e - i;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, start);
+      if (start) {
+        const uint32_t pos = ncand + __popc(m & lanemask_lt());
+        vis[pos] = x;
+        cc[pos] = static_cast<uint16_t>(c);
+      }
+      ncand += __popc(m);
+    }
+    __syncwarp();
+    // top-k by (count desc, id asc) (samplers.cpp:271-281), rank order
+    const uint32_t take = min(a.k, ncand);
+    for (uint32_t r = 0; r < take; ++r) {
+      uint32_t bc = 0, bid = kNone, bpos = kNone;
+      for (uint32_t q = lane; q < ncand; q += 32) {
+        const uint32_t c = cc[q], id = vis[q];
+        if (c > bc || (c == bc && c > 0 && id < bid)) {
+          bc = c;
+          bid = id;
+          bpos = q;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        const uint32_t oid = __shfl_xor_sync(0xffffffffu, bid, o);
+        const uint32_t op = __shfl_xor_sync(0xffffffffu, bpos, o);
+        if (oc > bc || (oc == bc && oid < bid)) {
+          bc = oc;
+          bid = oid;
+          bpos = op;
+        }
+      }
+      if (lane == 0) {
+        a.slots[di * a.k + r] = bid;
+        cc[bpos] = 0;  // taken
+        set_bit(a.bits, a.summ, bid);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) a.cnt[di] = take;
+    __syncwarp();
+  }
+}
+
+// Edges of the RW picks in dst order (ordered compaction of the per-dst
+// counts, decoupled look-back), rank order inside a dst.
+__global__ void __launch_bounds__(kNT) rw_emit_kernel(RwArgs a) {
+  pdl_begin();
+  __shared__ unsigned long long s_scan[kNT / 32 + 1];
+  __shared__ unsigned long long s_b;
+  __shared__ unsigned s_tile;
+  constexpr int IPT = 4;
+  constexpr int TILE = kNT * IPT;
+  const uint64_t n = a.meta->n_dst;
+  const uint64_t ntiles = (n + TILE - 1) / TILE;
+  const unsigned ep = inv_epoch(a.epoch, a.slot);
+  for (unsigned tile = blockIdx.x; tile < ntiles;
+       tile = next_tile_after(a.ticket, &s_tile, gridDim.x, ntiles)) {
+    const uint64_t i0 = static_cast<uint64_t>(tile) * TILE + threadIdx.x * IPT;
+    uint64_t c[IPT];
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      c[j] = (i0 + j < n) ? a.cnt[i0 + j] : 0;
+      sum += c[j];
+    }
+    unsigned long long tot;
+    const unsigned long long ex = block_exclusive_scan<kNT>(sum, s_scan, tot);
+    const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
+    unsigned long long pos = gb + ex;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j)
+      for (uint64_t r = 0; r < c[j]; ++r, ++pos)
+        if (pos < a.cap_edges)
+          a.edges[pos] = make_uint2(a.slots[(i0 + j) * a.k + r], static_cast<uint32_t>(i0 + j));
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+      a.meta->n_edges = gb + tot;
+      if (gb + tot > a.cap_edges) atomicExch(a.overflow, 1u);
+    }
+  }
+  if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) a.meta->n_edges = 0;
+}
+
 // ---------------------------------------------------------------- extract --
 // Sorted unique list = set bits in id order; wprefix[w] = rank of word w.
 // Words per thread: 2 for small bitmaps (more tiles, short per-thread
@@ -975,6 +1154,16 @@ void launch_ns(const LaborArgs& a, const uint32_t* D, const uint64_t* out_prefix
   launch_k(ns_emit_kernel, grid, kNT, st, D, a.meta, out_prefix, indptr, indices, a.k, a.slots,
                                        a.bits, a.summ, a.edges, a.cap_edges);
   CB_LAUNCH("ns_emit");
+}
+
+void launch_rw(const RwArgs& a, uint64_t cap_dst, bool smooth, cudaStream_t st) {
+  const int grid = grid_for(cap_dst, kRwWarps, 4);
+  if (smooth) launch_k(rw_walk_kernel<true>, grid, kNT, st, a);
+  else launch_k(rw_walk_kernel<false>, grid, kNT, st, a);
+  CB_LAUNCH("rw_walk");
+  launch_k(rw_emit_kernel, grid_for(cap_dst, kNT * 4, resident_per_sm(rw_emit_kernel)), kNT, st,
+           a);
+  CB_LAUNCH("rw_emit");
 }
 
 void launch_extract(const ExtractArgs& a, cudaStream_t st) {

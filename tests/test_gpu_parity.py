@@ -406,3 +406,37 @@ def test_coop_parity_large_sparse_bitmap(gpu):
     res = cb.coop_sample(g, pm, seeds, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), sched)
     exp = O.coop_sample(ref, owner, P, seeds, 3, O.LABOR0, 10, osched(sched))
     coop_eq(res, exp, P, 3, "large coop")
+
+
+@pytest.mark.parametrize("kappa", [1, 4])
+def test_rw_sampler_matches_compiled_reference(powerlaw, kappa):
+    """rw_block (samplers.cpp:202-285): random walks with restart, top-k by
+    visit count (ties to the smaller id), through expand, vs the compiled
+    reference with its default rw parameters (3 steps, p = 0.5, 100 walks)."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    g, ref = powerlaw
+    rng = np.random.default_rng(kappa)
+    for trial in range(2):
+        seeds = np.sort(rng.choice(ref.n, 150, replace=False)).astype(np.uint32)
+        sched = cb.schedule_advance(cb.SeedSchedule.make(kappa, 40 + trial))
+        got = cb.expand(g, seeds, 2, cb.SamplerConfig(cb.SamplerKind.kRw, 4), sched)
+        want = O.expand(ref, seeds, 2, 3, 4, osched(sched), impl="reference")
+        assert_stack_eq(got, want, f"RW kappa={kappa} trial={trial}")
+
+
+def test_rw_sampler_c1_and_params(c1):
+    """RW on the R-MAT config-1 graph (dead ends, hubs) and non-default
+    parameters vs the compiled reference's sample_rw."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    g, ref = c1
+    rng = np.random.default_rng(5)
+    seeds = np.sort(rng.choice(ref.n, 300, replace=False)).astype(np.uint32)
+    sched = cb.SeedSchedule.plain(77)
+    got = cb.expand(g, seeds, 3, cb.SamplerConfig(cb.SamplerKind.kRw, 10), sched)
+    want = O.expand(ref, seeds, 3, 3, 10, osched(sched), impl="reference")
+    assert_stack_eq(got, want, "RW c1")
+    with pytest.raises(cb.InputError):
+        cb.expand(g, seeds, 1, cb.SamplerConfig(cb.SamplerKind.kRw, 5, rw_walks=300, rw_length=3),
+                  sched)
