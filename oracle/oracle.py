@@ -168,6 +168,7 @@ def lib(impl: str = "restated") -> C.CDLL:
         L.rf_step.argtypes = [_P, _P, C.c_int, _P, _u32, _P, _P, C.c_int, C.c_int, _u32,
                               C.POINTER(Sched), C.POINTER(_f64), C.POINTER(_f64),
                               C.POINTER(_u64)]
+        L.rf_edge_pred_seeds.argtypes = [_P, _P, _u64, _u64, _P, C.POINTER(_u64)]
         L.rf_save_csr.argtypes = [_P, C.c_char_p]
         L.rf_load_csr.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64),
                                   C.POINTER(C.POINTER(_u64)), C.POINTER(C.POINTER(_u32))]
@@ -302,6 +303,17 @@ class RefGraph:
         if getattr(self, "h", None):
             self.L.rf_graph_free(self.h)
             self.h = None
+
+
+def edge_pred_seeds_reference(g: CSR, edges, epoch_seed: int) -> np.ndarray:
+    """The reference's edge_pred_seeds (samplers.cpp:356-393)."""
+    rg = RefGraph(g)
+    uv = np.ascontiguousarray(edges, dtype=np.uint32).reshape(-1, 2)
+    out = np.zeros(3 * len(uv) + 1, np.uint32)
+    n = C.c_uint64()
+    _check(rg.L.rf_edge_pred_seeds(rg.h, _ptr(uv), len(uv), epoch_seed, _ptr(out),
+                                   C.byref(n)), rg.L)
+    return out[: n.value]
 
 
 def save_csr_reference(g: CSR, path: str):

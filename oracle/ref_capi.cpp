@@ -135,6 +135,18 @@ void* rf_graph_new(const uint64_t* indptr, const uint32_t* indices, uint64_t n,
 }
 void rf_graph_free(void* g) { delete static_cast<Graph*>(g); }
 
+/* samplers.cpp:356-393 edge_pred_seeds; out needs 3 * n_edges slots. */
+int rf_edge_pred_seeds(void* g, const uint32_t* uv, uint64_t n_edges, uint64_t epoch_seed,
+                       uint32_t* out, uint64_t* n_out) {
+  return guard([&] {
+    std::vector<std::pair<VertexId, VertexId>> batch(n_edges);
+    for (uint64_t i = 0; i < n_edges; ++i) batch[i] = {uv[2 * i], uv[2 * i + 1]};
+    const auto s = edge_pred_seeds(*static_cast<Graph*>(g), batch, epoch_seed);
+    std::memcpy(out, s.data(), s.size() * 4);
+    *n_out = s.size();
+  });
+}
+
 /* graph.cpp:216-252 — the reference's own CBCS writer / reader. */
 int rf_save_csr(void* g, const char* path) {
   return guard([&] { save_csr(*static_cast<Graph*>(g), path); });

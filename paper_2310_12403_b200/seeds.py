@@ -51,3 +51,42 @@ def coop_seeds(members: list[np.ndarray], b: int, seed: int, step: int) -> list[
     """Per-part seeds of one cooperative step (cli.cpp:210-214)."""
     return [draw_from_pool(members[p], b, seed, hash_bits(step, [p]))
             for p in range(len(members))]
+
+
+def edge_pred_seeds(indptr: np.ndarray, indices: np.ndarray, edge_batch, epoch_seed: int,
+                    num_vertices: int | None = None) -> np.ndarray:
+    """samplers.cpp:356-393: seeds of an edge-prediction minibatch. For each
+    (u, v): both endpoints (first occurrence order), then one negative endpoint
+    w drawn uniformly with hash_uniform(seed, {kStreamEdgeNeg=6, u, v, attempt})
+    that is neither the shared endpoint (u or v by the coin hash_uniform(seed,
+    {kStreamEdgeCoin=5, u, v}) < 0.5) nor one of its in-neighbours; 100
+    attempts, else InputError. Host-side input generation like
+    draw_from_pool (the graph's CSR arrays come from Graph.download())."""
+    from .coopbatch import InputError, hash_uniform
+    n = len(indptr) - 1 if num_vertices is None else num_vertices
+    out, seen = [], set()
+
+    def push(x):
+        if x not in seen:
+            seen.add(x)
+            out.append(x)
+    for u, v in np.asarray(edge_batch, dtype=np.uint64).reshape(-1, 2):
+        u, v = int(u), int(v)
+        if u >= n or v >= n:
+            raise InputError("vertex id out of range")
+        push(u)
+        push(v)
+        shared = u if hash_uniform(epoch_seed, [5, u, v]) < 0.5 else v
+        blocked = set(indices[indptr[shared]:indptr[shared + 1]].tolist())
+        blocked.add(shared)
+        for attempt in range(100):
+            r = hash_uniform(epoch_seed, [6, u, v, attempt])
+            w = min(int(r * float(n)), n - 1)
+            if w in blocked:
+                continue
+            push(w)
+            break
+        else:
+            raise InputError("edge_pred_seeds: no negative endpoint found for vertex "
+                             f"{shared} after 100 attempts")
+    return np.asarray(out, dtype=np.uint32)

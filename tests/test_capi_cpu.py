@@ -124,3 +124,20 @@ def test_reference_cbcs_roundtrip_oracle(tmp_path):
     O.save_csr_reference(g, tmp_path / "g.cbcs")
     h = O.load_csr_reference(tmp_path / "g.cbcs")
     assert np.array_equal(h.indptr, g.indptr) and np.array_equal(h.indices, g.indices)
+
+
+def test_edge_pred_seeds_match_reference():
+    """edge_pred_seeds (samplers.cpp:356-393): host seed generation of an
+    edge-prediction batch equals the compiled reference."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    from paper_2310_12403_b200.seeds import edge_pred_seeds
+    g = O.rmat(2000, 16000, 8)
+    rng = np.random.default_rng(3)
+    src = rng.integers(0, g.n, 64)
+    pos = np.array([(int(g.indices[g.indptr[v]]), v) if g.indptr[v + 1] > g.indptr[v]
+                    else (v, (v + 1) % g.n) for v in src], dtype=np.uint32)
+    for seed in (1, 99):
+        got = edge_pred_seeds(g.indptr, g.indices, pos, seed)
+        want = O.edge_pred_seeds_reference(g, pos, seed)
+        assert np.array_equal(got, want)
