@@ -105,6 +105,10 @@ int cb_partition_random(const cb_graph* g, uint32_t parts, uint64_t seed, cb_par
 int cb_partition_create(const cb_graph* g, const uint32_t* owner, uint32_t parts,
                         cb_partition** out);
 int cb_partition_download(const cb_partition* pm, uint32_t* owner);
+/* cross_edge_ratio (partition.hpp:29-31, src/partition.cpp:79-89): edges whose
+ * endpoints have different owners, and their fraction of all edges. */
+int cb_cross_edge_ratio(const cb_graph* g, const cb_partition* pm, uint64_t* cross,
+                        double* ratio);
 /* part_members (partition.hpp:33-36, src/partition.cpp:99-105): the vertices of
  * all parts concatenated part-major, ascending within a part (members[n]);
  * shard_off[parts+1] = start of each part. This order is the feature shard

@@ -168,6 +168,7 @@ def lib(impl: str = "restated") -> C.CDLL:
         L.rf_step.argtypes = [_P, _P, C.c_int, _P, _u32, _P, _P, C.c_int, C.c_int, _u32,
                               C.POINTER(Sched), C.POINTER(_f64), C.POINTER(_f64),
                               C.POINTER(_u64)]
+        L.rf_cross_edge_ratio.argtypes = [_P, _P, _u32, C.POINTER(_f64)]
         L.rf_edge_pred_seeds.argtypes = [_P, _P, _u64, _u64, _P, C.POINTER(_u64)]
         L.rf_save_csr.argtypes = [_P, C.c_char_p]
         L.rf_load_csr.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64),
@@ -303,6 +304,14 @@ class RefGraph:
         if getattr(self, "h", None):
             self.L.rf_graph_free(self.h)
             self.h = None
+
+
+def cross_edge_ratio_reference(g: CSR, owner: np.ndarray, parts: int) -> float:
+    rg = RefGraph(g)
+    out = C.c_double()
+    own = np.ascontiguousarray(owner, dtype=np.uint32)
+    _check(rg.L.rf_cross_edge_ratio(rg.h, _ptr(own), parts, C.byref(out)), rg.L)
+    return out.value
 
 
 def edge_pred_seeds_reference(g: CSR, edges, epoch_seed: int) -> np.ndarray:

@@ -135,6 +135,17 @@ void* rf_graph_new(const uint64_t* indptr, const uint32_t* indices, uint64_t n,
 }
 void rf_graph_free(void* g) { delete static_cast<Graph*>(g); }
 
+/* partition.cpp:79-89 */
+int rf_cross_edge_ratio(void* g, const uint32_t* owner, uint32_t parts, double* out) {
+  return guard([&] {
+    const Graph& gr = *static_cast<Graph*>(g);
+    PartitionMap pm;
+    pm.num_parts = parts;
+    pm.owner.assign(owner, owner + gr.num_vertices);
+    *out = cross_edge_ratio(gr, pm);
+  });
+}
+
 /* samplers.cpp:356-393 edge_pred_seeds; out needs 3 * n_edges slots. */
 int rf_edge_pred_seeds(void* g, const uint32_t* uv, uint64_t n_edges, uint64_t epoch_seed,
                        uint32_t* out, uint64_t* n_out) {

@@ -38,6 +38,7 @@ _SIGS = {
     "cb_partition_create": (C.c_int, [_P, _P, _u32, _PP]),
     "cb_partition_download": (C.c_int, [_P, _P]),
     "cb_partition_members": (C.c_int, [_P, _P, _P]),
+    "cb_cross_edge_ratio": (C.c_int, [_P, _P, C.POINTER(_u64), C.POINTER(C.c_double)]),
     "cb_partition_destroy": (None, [_P]),
     "cb_features_synth": (C.c_int, [_P, _P, _u32, C.c_int, _u64, _PP]),
     "cb_features_info": (C.c_int, [_P, C.POINTER(_u32), C.POINTER(C.c_int), C.POINTER(_u64)]),

@@ -236,6 +236,13 @@ def partition_random(g: Graph, parts: int, seed: int) -> PartitionMap:
     return PartitionMap(g, h, parts)
 
 
+def cross_edge_ratio(g: Graph, pm: PartitionMap) -> float:
+    """partition.cpp:79-89 — fraction of edges whose endpoints have different owners."""
+    r = C.c_double()
+    _check(_lib.load().cb_cross_edge_ratio(g._h, pm._h, None, C.byref(r)))
+    return r.value
+
+
 def partition_from_owner(g: Graph, owner, parts: int) -> PartitionMap:
     owner = np.ascontiguousarray(owner, dtype=np.uint32)
     if len(owner) != g.num_vertices:

@@ -1035,6 +1035,18 @@ int cb_partition_download(const cb_partition* pm, uint32_t* owner) {
   });
 }
 
+int cb_cross_edge_ratio(const cb_graph* g, const cb_partition* pm, uint64_t* cross,
+                        double* ratio) {
+  return guard([&] {
+    require(g != nullptr && pm != nullptr, "null argument");
+    require(pm->n == g->g.n, "partition: owner array does not cover all vertices");
+    DeviceGuard dg(g->g.device);
+    const uint64_t c = cross_edges(g->g, pm->owner, nullptr);
+    if (cross) *cross = c;
+    if (ratio) *ratio = g->g.m ? static_cast<double>(c) / static_cast<double>(g->g.m) : 0.0;
+  });
+}
+
 int cb_partition_members(const cb_partition* pm, uint32_t* members, uint64_t* shard_off) {
   return guard([&] {
     require(pm != nullptr, "null partition");

@@ -20,6 +20,7 @@ int vec_bytes_for(uint64_t row_bytes);
 void graph_generate_rmat(DeviceGraph& g, uint64_t n, uint64_t m, uint64_t seed,
                          cudaStream_t st);
 void graph_max_degree(DeviceGraph& g, cudaStream_t st);
+uint64_t cross_edges(const DeviceGraph& g, const uint32_t* owner, cudaStream_t st);
 void partition_random_device(uint64_t n, uint32_t parts, uint64_t seed, uint32_t* owner,
                              cudaStream_t st);
 

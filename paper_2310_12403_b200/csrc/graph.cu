@@ -123,6 +123,40 @@ __global__ void max_degree_kernel(const uint64_t* indptr, uint64_t n,
   if ((threadIdx.x & 31) == 0) atomicMax(out, best);
 }
 
+// cross_edge_ratio (partition.cpp:79-89): edges whose endpoints have different
+// owners. Each thread takes 32 consecutive edges, finds the destination of
+// the first by binary search over indptr, then walks forward.
+__global__ void cross_edges_kernel(const uint64_t* __restrict__ indptr,
+                                   const uint32_t* __restrict__ indices, uint64_t n, uint64_t m,
+                                   const uint32_t* __restrict__ owner,
+                                   unsigned long long* out) {
+  constexpr uint64_t kChunk = 32;
+  unsigned long long cross = 0;
+  const uint64_t nchunks = (m + kChunk - 1) / kChunk;
+  for (uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; c < nchunks;
+       c += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t e0 = c * kChunk, e1 = min(m, e0 + kChunk);
+    uint64_t lo = 0, hi = n;  // largest s with indptr[s] <= e0
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (indptr[mid] <= e0) lo = mid;
+      else hi = mid;
+    }
+    uint64_t s = lo, end = indptr[s + 1];
+    uint32_t os = owner[s];
+    for (uint64_t e = e0; e < e1; ++e) {
+      while (e >= end) {
+        ++s;
+        end = indptr[s + 1];
+        os = owner[s];
+      }
+      cross += owner[indices[e]] != os;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) cross += __shfl_xor_sync(0xffffffffu, cross, o);
+  if ((threadIdx.x & 31) == 0 && cross) atomicAdd(out, cross);
+}
+
 __global__ void partition_kernel(uint64_t n, uint32_t parts, uint64_t pfx, uint32_t* owner) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < n;
@@ -144,6 +178,21 @@ int scale_of(uint64_t n) {
 }
 
 }  // namespace
+
+uint64_t cross_edges(const DeviceGraph& g, const uint32_t* owner, cudaStream_t st) {
+  unsigned long long* d = nullptr;
+  CB_CUDA(cudaMalloc(&d, 8));
+  CB_CUDA(cudaMemsetAsync(d, 0, 8, st));
+  const uint64_t chunks = (g.m + 31) / 32;
+  const int grid = static_cast<int>(std::max<uint64_t>(
+      1, std::min<uint64_t>((chunks + 255) / 256, static_cast<uint64_t>(kNumSMs) * 8)));
+  if (g.m) cross_edges_kernel<<<grid, 256, 0, st>>>(g.indptr, g.indices, g.n, g.m, owner, d);
+  unsigned long long h = 0;
+  CB_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st));
+  CB_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d);
+  return h;
+}
 
 void graph_generate_rmat(DeviceGraph& g, uint64_t n, uint64_t m, uint64_t seed,
                          cudaStream_t st) {

@@ -270,6 +270,19 @@ def test_step_metrics_match_reference_definitions(c1):
         assert got[p].feat_bytes == 400 * len(exp["owner_sets"][p])
 
 
+@pytest.mark.parametrize("P", [2, 8])
+def test_cross_edge_ratio_matches_reference(c1, P):
+    """cross_edge_ratio (partition.cpp:79-89); random ownership cuts ~(P-1)/P
+    of the edges (acceptance c6)."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    g, ref = c1
+    pm = cb.partition_random(g, P, 4)
+    got = cb.cross_edge_ratio(g, pm)
+    assert got == O.cross_edge_ratio_reference(ref, pm.owner, P)
+    assert abs(got - (P - 1) / P) < 0.01
+
+
 def test_coop_union_property(c1):
     """test_coop.cpp:128-157: cooperative input set == single-part union batch."""
     g, ref = c1
