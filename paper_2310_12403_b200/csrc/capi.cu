@@ -615,7 +615,9 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   }
   launch_labor(la, w.sync.max_tiles, smooth, st);  // labor_mark
   prof_mark(pl);
-  launch_labor_post(la, w.sync.max_tiles, ex, st);  // emit || extract
+  ExtractArgs ext = ex;
+  ext.trace = pl->trace ? pl->trace + (3 * l + 2) * kTraceKernel : nullptr;
+  launch_labor_post(la, w.sync.max_tiles, ext, st);  // emit || extract
   prof_mark(pl);
   return (smooth && pl->kind == CB_LABOR0 && pl->vtab) ? 4 : 3;  // (+ variate table)
 }

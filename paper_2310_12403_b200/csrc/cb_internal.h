@@ -226,6 +226,7 @@ struct RwArgs {
 constexpr uint32_t kRwMaxVisits = 512;  // rw_walks * rw_length per dst on the device
 
 struct ExtractArgs {
+  unsigned long long* trace;  // debug stamps (CB_TRACE), nullptr = off
   const uint32_t* bits;
   const uint32_t* summ;
   uint32_t* wprefix;

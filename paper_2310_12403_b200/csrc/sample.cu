@@ -542,7 +542,9 @@ constexpr uint64_t kEmitBigLayerWords = 64 * 1024;
 // output bases in smem); the edge itself was staged by labor_mark at its scan
 // position, so each kept edge is one load and one store.
 __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned role,
-                                                unsigned ncta) {
+                                                unsigned ncta,
+                                                unsigned long long* trace_in = nullptr) {
+  unsigned long long* trace = role < 32 ? trace_in : nullptr;
   __shared__ unsigned long long s_scan[kNT / 32 + 1];
   __shared__ uint32_t s_wbase[kEmitTileWords + 1];
   __shared__ uint32_t s_word[kEmitTileWords];
@@ -555,6 +557,7 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned rol
   const uint32_t tw = kNT * wpt;  // words per tile
   const uint64_t ntiles = (nwords + tw - 1) / tw;
   const unsigned ep = inv_epoch(a.epoch, a.slot);
+  tstamp(trace, 32 + role, 0);
   for (unsigned tile = role; tile < ntiles; tile = next_tile_after(a.ticket, &s_tile, ncta, ntiles)) {
     const uint64_t wt = static_cast<uint64_t>(tile) * tw;
     const uint32_t l0 = threadIdx.x * wpt;
@@ -565,8 +568,10 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned rol
       wv[j] = (j < wpt && wt + l0 + j < nwords) ? a.keep_words[wt + l0 + j] : 0u;
       c += __popc(wv[j]);
     }
+    if (tile == role) tstamp(trace, 32 + role, 1);
     unsigned long long tot;
     const unsigned long long ex = block_exclusive_scan<kNT>(c, s_scan, tot);
+    if (tile == role) tstamp(trace, 32 + role, 2);
     uint32_t run = static_cast<uint32_t>(ex);
 #pragma unroll
     for (int j = 0; j < kEmitWPT; ++j) {
@@ -577,6 +582,7 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned rol
       }
     }
     const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
+    if (tile == role) tstamp(trace, 32 + role, 3);
     // (tile_prefix ends with __syncthreads: s_word / s_wbase are visible)
     constexpr int B = 8;  // kept items per thread in flight
     for (uint32_t q0 = threadIdx.x; q0 < tot; q0 += kNT * B) {
@@ -607,6 +613,7 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned rol
       if (gb + tot > a.cap_edges) atomicExch(a.overflow, 1u);
     }
   }
+  tstamp(trace, 32 + role, 4);
   retire_ticket(a.ticket, a.exit_ctr, ncta);
 }
 
@@ -901,6 +908,8 @@ __device__ __forceinline__ void extract_flat(const ExtractArgs& a, unsigned role
   const uint32_t tw = kNT * wpt;
   const uint64_t ntiles = a.words_padded / tw;
   const unsigned ep = inv_epoch(a.epoch, a.slot);
+  unsigned long long* tr = role < 32 ? a.trace : nullptr;
+  tstamp(tr, role, 0);
   for (unsigned tile = role; tile < ntiles; tile = next_tile_after(a.ticket, &s_tile, ncta, ntiles)) {
     const uint64_t w0 = static_cast<uint64_t>(tile) * tw + threadIdx.x * wpt;
     uint32_t wv[kWPTBig];
@@ -925,9 +934,12 @@ __device__ __forceinline__ void extract_flat(const ExtractArgs& a, unsigned role
     unsigned long long c = 0;
 #pragma unroll
     for (int j = 0; j < kWPTBig; ++j) c += __popc(wv[j]);
+    if (tile == role) tstamp(tr, role, 1);
     unsigned long long tot;
     const unsigned long long ex = block_exclusive_scan<kNT>(c, s_scan, tot);
+    if (tile == role) tstamp(tr, role, 2);
     const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
+    if (tile == role) tstamp(tr, role, 3);
     unsigned long long pos = gb + ex;
     uint32_t pw[kWPTBig];
 #pragma unroll
@@ -953,6 +965,7 @@ __device__ __forceinline__ void extract_flat(const ExtractArgs& a, unsigned role
       if (gb + tot > a.cap_out) atomicExch(a.overflow, 1u);
     }
   }
+  tstamp(tr, role, 4);
 }
 
 // Summary-driven extraction for large bitmaps: a tile is kNT summary words
@@ -1035,7 +1048,7 @@ __global__ void __launch_bounds__(kNT) extract_kernel(ExtractArgs a) {
 __global__ void __launch_bounds__(kNT) post_kernel(ExtractArgs e, LaborArgs a, unsigned n_ext) {
   pdl_begin();
   if (blockIdx.x < n_ext) extract_body(e, blockIdx.x, n_ext);
-  else labor_emit_body(a, blockIdx.x - n_ext, gridDim.x - n_ext);
+  else labor_emit_body(a, blockIdx.x - n_ext, gridDim.x - n_ext, e.trace);
 }
 
 // ---------------------------------------------------------------- relabel --

@@ -24,9 +24,12 @@ buf = np.zeros(32 * 64 * 8, np.uint64)
 assert _lib.load().cb_plan_trace(plan._h, buf.ctypes.data_as(C.c_void_p), len(buf)) == 0
 t = buf.reshape(32, 64, 8).astype(np.int64)
 t0 = t[t > 0].min()
-names = {0: "frontier0", 1: "mark0", 3: "frontier1", 4: "mark1", 6: "frontier2", 7: "mark2"}
+names = {0: "frontier0", 1: "mark0", 2: "post0", 3: "frontier1", 4: "mark1", 5: "post1",
+         6: "frontier2", 7: "mark2", 8: "post2"}
 for k, nm in names.items():
-    for cta in range(0, 64, 8):
+    # post: CTAs 0-31 = extract roles, 32-63 = emit roles
+    for cta in (list(range(0, 64, 8)) if not nm.startswith("post") else
+                [0, 1, 2, 8, 16, 31, 32, 33, 34, 40, 48, 63]):
         row = t[k, cta]
         if row[0] == 0:
             continue
