@@ -323,6 +323,52 @@ def scale_evidence(cb, dev, steps=20, parts=(1, 8)):
     return out
 
 
+# ------------------------------------------------------ c5 batch sweep ------
+def batch_sweep_evidence(cb, dev, batches=(1024, 4096, 16384, 65536), steps=10):
+    """Config 5's batch sweep on one B200: mag240M-shaped R-MAT (244M V /
+    1.73B E), 2-layer LABOR-0 fanout 25/15. The 768-dim fp16 table (375 GB)
+    does not fit one GPU, so this sweep times sampling + dedup only and
+    reports the feature bytes the batch would fetch (rows x 1536 B)."""
+    import torch
+
+    c = CONFIGS["c5"]
+    t0 = time.time()
+    g = cb.Graph.generate_rmat(c["n"], c["m"], GRAPH_SEED, device=dev)
+    gen_s = time.time() - t0
+    scfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, fanouts=c["fanouts"])
+    L = len(c["fanouts"])
+    rng = np.random.default_rng(RUN_SEED)
+    out = {"workload": c["workload"] + " (sampling + dedup only)", "graph_gen_s": round(gen_s, 2),
+           "sweep": []}
+    for b in batches:
+        plan = cb.Plan(g, None, L, scfg, b)
+        seeds = [np.sort(rng.choice(c["n"], b, replace=False)).astype(np.uint32)
+                 for _ in range(steps + 2)]
+        sched = cb.SeedSchedule.make(1, RUN_SEED)
+        plan.sample([seeds[0]], sched, cb.MODE_INDEP, sync=True)
+        plan.capture(np.array([0, b], np.uint64), sched, cb.MODE_INDEP, None)
+        st = torch.cuda.ExternalStream(plan.stream, device=torch.device(f"cuda:{dev}"))
+        d = torch.from_numpy(np.stack(seeds).view(np.int32)).to(f"cuda:{dev}")
+        ms, rows = [], []
+        for i in range(steps + 2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            plan.replay(d.data_ptr() + i * b * 4, sched, True, 1)
+            e1.record(st)
+            plan.synchronize()
+            sched = cb.schedule_advance(sched)
+            if i >= 2:
+                ms.append(e0.elapsed_time(e1))
+                rows.append(plan.layer_sizes(0, L - 1)["n_src"])
+        out["sweep"].append({"batch": b, "ms_per_batch": float(np.mean(ms)),
+                             "seeds_per_s": b / (float(np.mean(ms)) / 1e3),
+                             "input_vertices_per_seed": float(np.mean(rows)) / b,
+                             "feature_bytes_per_seed": float(np.mean(rows)) * 1536 / b})
+        del plan, d
+    del g
+    return out
+
+
 # ---------------------------------------------------------- kappa evidence --
 def kappa_evidence(cb, dev, steps_epochs=2, kappas=(1, 4, 16, 64, 256, None)):
     """Config 3's kappa sweep (acceptance.cpp:362-390 at full scale): the
@@ -688,6 +734,7 @@ def run_ours(args, cfg):
         line["evidence"]["concavity"] = concavity_evidence(cb, g, scfg, L, b, row_bytes, dev)
         line["evidence"]["kappa"] = kappa_evidence(cb, dev)
         line["evidence"]["papers100m"] = scale_evidence(cb, dev)
+        line["evidence"]["mag240m_batch_sweep"] = batch_sweep_evidence(cb, dev)
     if world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import oracle as O

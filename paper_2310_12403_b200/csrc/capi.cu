@@ -279,7 +279,13 @@ void plan_alloc(cb_plan* pl) {
     uint64_t max_tiles = 2;
     for (int l = 0; l < L; ++l) {
       const uint64_t k = pl->fanouts[l];
-      const uint64_t sum_deg = (l == 0) ? sat_mul(cd, maxdeg) : std::min(m, sat_mul(cd, maxdeg));
+      // scan space: layer-0 seeds may repeat, so its bound is m * grow (an
+      // overflow is flagged on the device and retried with grow * 2); later
+      // frontiers are unique vertex sets, so m bounds them
+      const uint64_t m_grow = sat_mul(std::max<uint64_t>(m, 1),
+                                      static_cast<uint64_t>(std::ceil(pl->grow)));
+      const uint64_t sum_deg =
+          std::min((l == 0) ? m_grow : m, sat_mul(cd, maxdeg));
       uint64_t est;
       if (pl->kind == CB_FULL) est = sum_deg;
       else if (pl->kind == CB_NS || pl->kind == CB_RW) est = sat_mul(cd, k);
@@ -521,6 +527,7 @@ FrontierArgs frontier_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint
   fa.out_prefix = b.out_prefix;
   fa.slots = b.slots;
   fa.cap_edges = b.cap_edges;
+  fa.cap_tiles = w.sync.max_tiles - 1;
   fa.ticket = w.sync.tickets + 3 * l;
   fa.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l;
   fa.st_a = w.sync.status_a;

@@ -164,6 +164,7 @@ struct FrontierArgs {
   uint64_t* out_prefix;
   uint32_t* slots;
   uint64_t cap_edges;
+  uint64_t cap_tiles;  // scan tiles the plan holds (tile_first has cap_tiles + 1)
   unsigned* ticket;
   unsigned* exit_ctr;
   unsigned long long *st_a, *st_b, *st_c;

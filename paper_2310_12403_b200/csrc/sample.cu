@@ -218,7 +218,10 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
           a.act[ea] = rec;
           // scan tiles whose first position falls inside this record
           const uint64_t t_first = (eq + kLaborTile - 1) / kLaborTile;
-          const uint64_t t_last = (eq + q[j] - 1) / kLaborTile;
+          // (clamped to the scan capacity: an overflowing layer is flagged
+          // below and sampled empty, then retried with a larger plan)
+          const uint64_t t_last =
+              min(static_cast<uint64_t>((eq + q[j] - 1) / kLaborTile), a.cap_tiles);
           // bit 31: the record starts exactly at the tile start (so the
           // previous tile ends with record ea-1: no load to find it)
           for (uint64_t t = t_first; t <= t_last; ++t)
@@ -232,7 +235,11 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
       eo += o[j];
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
-      const uint64_t tot = bq + tq, nact = ba + ta;
+      uint64_t tot = bq + tq, nact = ba + ta;
+      if ((tot + kLaborTile - 1) / kLaborTile > a.cap_tiles) {  // scan space overflow
+        atomicExch(a.overflow, 1u);
+        tot = nact = 0;
+      }
       ActRec sent{};
       sent.pre = tot;
       a.act[nact] = sent;

@@ -453,3 +453,21 @@ def test_rw_sampler_c1_and_params(c1):
     with pytest.raises(cb.InputError):
         cb.expand(g, seeds, 1, cb.SamplerConfig(cb.SamplerKind.kRw, 5, rw_walks=300, rw_length=3),
                   sched)
+
+
+def test_repeated_seeds_beyond_edge_count(powerlaw):
+    """Seeds may repeat (check_seeds, samplers.cpp:11-13 only bounds-checks):
+    a layer-0 scan space larger than |E| overflows the first capacity plan on
+    the device and is retried with a larger one; the result equals the
+    oracle's."""
+    g, ref = powerlaw
+    deg = np.diff(ref.indptr.astype(np.int64))
+    hubs = np.argsort(deg)[::-1][:3].astype(np.uint32)
+    reps = int(3 * ref.m / max(1, int(deg[hubs].sum()))) + 1
+    seeds = np.tile(hubs, reps)
+    assert int(deg[seeds].sum()) > 2 * ref.m
+    sched = cb.SeedSchedule.plain(3)
+    for kind, okind in KINDS[1:]:
+        got = cb.expand(g, seeds, 2, cb.SamplerConfig(kind, 4), sched)
+        want = O.expand(ref, seeds, 2, okind, 4, osched(sched))
+        assert_stack_eq(got, want, f"repeated {kind.name}")
