@@ -35,6 +35,8 @@
  *   cb_stack_fingerprint,     <- stack_fingerprint / run_dependent_experiment
  *   cb_shuffled_order            order (src/cache.cpp:123-162)
  *   cb_partition_members      <- part_members (partition.hpp:33-36)
+ *   cb_gcn_*, cb_train_step   <- GcnModel, gcn_forward/backward, coop_train_step,
+ *                                indep_train_step (coop.hpp:105-185)
  *   cb_px_*                   <- coop_sample + build_exchange + all_to_all_forward
  *                                across processes (coop.cpp:25-106, 145-159)
  *   cb_last_error             <- the what() of coopbatch::InputError etc.
@@ -308,6 +310,24 @@ int cb_px_connect_features(cb_plan* plan, uint32_t peer, const void* handle, uin
 /* Input rows of this rank's last layer into the plan's row buffer
  * (cb_download_rows / cb_rows_device), requester-aligned. */
 int cb_px_gather(cb_plan* plan, const cb_features* local);
+
+/* ---- GCN training step (coop.hpp:105-185; coop.cpp:161-357, 394-610) ----
+ * GcnModel on the device: weights[l] (rows x cols, f64 row-major) is used at
+ * block l; hidden layers use tanh, block 0 the identity (logits). */
+typedef struct cb_model cb_model;
+/* GcnModel::init (coop.cpp:334-357) */
+int cb_gcn_model_init(int device, uint32_t in_dim, uint32_t hidden, uint32_t classes,
+                      int num_layers, uint64_t seed, cb_model** out);
+/* Read (upload = 0) or write (upload = 1) the weights of one layer. */
+int cb_gcn_model_weights(cb_model* m, int layer, double* host, int upload, uint64_t* rows,
+                         uint64_t* cols);
+void cb_gcn_model_destroy(cb_model* m);
+/* coop_train_step (mode COOP, P > 1) / indep_train_step over the plan's last
+ * batch with an f64 FeatureStore (labels = hash(seed,{10,v}) mod classes):
+ * mean loss over all seeds and the part-summed weight gradients, layer 0
+ * first, each rows x cols (grad_w may be NULL). */
+int cb_train_step(cb_plan* plan, const cb_features* store, uint32_t classes, cb_model* model,
+                  double* loss, double* grad_w);
 
 #ifdef __cplusplus
 }

@@ -168,6 +168,8 @@ def lib(impl: str = "restated") -> C.CDLL:
         L.rf_step.argtypes = [_P, _P, C.c_int, _P, _u32, _P, _P, C.c_int, C.c_int, _u32,
                               C.POINTER(Sched), C.POINTER(_f64), C.POINTER(_f64),
                               C.POINTER(_u64)]
+        L.rf_train_step.argtypes = [_P, _P, C.c_int, _P, _u32, _P, _P, C.c_int, C.c_int, _u32,
+                                    C.POINTER(Sched), _u32, _u64, C.POINTER(_f64), _P]
         L.rf_cross_edge_ratio.argtypes = [_P, _P, _u32, C.POINTER(_f64)]
         L.rf_edge_pred_seeds.argtypes = [_P, _P, _u64, _u64, _P, C.POINTER(_u64)]
         L.rf_save_csr.argtypes = [_P, C.c_char_p]
@@ -304,6 +306,27 @@ class RefGraph:
         if getattr(self, "h", None):
             self.L.rf_graph_free(self.h)
             self.h = None
+
+
+def train_step_reference(g: CSR, mode: int, owner, parts: int, per_pe_seeds, L: int, kind: int,
+                         fanout: int, sched: Sched, dim: int, classes: int, feat_seed: int,
+                         hidden: int, model_seed: int, grad_sizes):
+    """The compiled reference's coop_train_step (mode 0) / indep_train_step
+    (mode 1) with FeatureStore::synth(n, dim, classes, feat_seed) and
+    GcnModel::init(dim, hidden, classes, L, model_seed)."""
+    rg = RefGraph(g)
+    fs = RefFeatureStore(g.n, dim, feat_seed, classes)
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(s, np.uint32) for s in per_pe_seeds]),
+                                dtype=np.uint32)
+    off = np.zeros(parts + 1, np.uint64)
+    off[1:] = np.cumsum([len(s) for s in per_pe_seeds])
+    own = None if owner is None else np.ascontiguousarray(owner, dtype=np.uint32)
+    gw = np.zeros(int(sum(grad_sizes)), np.float64)
+    loss = C.c_double()
+    _check(rg.L.rf_train_step(rg.h, fs.h, mode, _ptr(own), parts, _ptr(flat), _ptr(off), L, kind,
+                              fanout, C.byref(sched), hidden, model_seed, C.byref(loss),
+                              _ptr(gw)), rg.L)
+    return loss.value, gw
 
 
 def cross_edge_ratio_reference(g: CSR, owner: np.ndarray, parts: int) -> float:

@@ -135,6 +135,37 @@ void* rf_graph_new(const uint64_t* indptr, const uint32_t* indices, uint64_t n,
 }
 void rf_graph_free(void* g) { delete static_cast<Graph*>(g); }
 
+/* coop_train_step / indep_train_step (coop.cpp:438-610) with GcnModel::init
+ * (in_dim = store dim); grad_w: layers concatenated, each rows x cols. */
+int rf_train_step(void* g, void* fs, int mode, const uint32_t* owner, uint32_t parts,
+                  const uint32_t* seeds_flat, const uint64_t* seeds_off, int L, int kind,
+                  uint32_t fanout, const ob_sched* sched, uint32_t hidden, uint64_t model_seed,
+                  double* loss, double* grad_w) {
+  return guard([&] {
+    const Graph& gr = *static_cast<Graph*>(g);
+    const FeatureStore& store = *static_cast<FeatureStore*>(fs);
+    std::vector<std::vector<VertexId>> seeds(parts);
+    for (uint32_t p = 0; p < parts; ++p)
+      seeds[p].assign(seeds_flat + seeds_off[p], seeds_flat + seeds_off[p + 1]);
+    const GcnModel model = GcnModel::init(store.dim, hidden, store.num_classes, L, model_seed);
+    TrainStepResult r;
+    if (mode == 0) {
+      PartitionMap pm;
+      pm.num_parts = parts;
+      pm.owner.assign(owner, owner + gr.num_vertices);
+      r = coop_train_step(gr, pm, seeds, L, to_cfg(kind, fanout), to_sched(sched), model, store);
+    } else {
+      r = indep_train_step(gr, seeds, L, to_cfg(kind, fanout), to_sched(sched), model, store);
+    }
+    *loss = r.loss;
+    std::size_t off = 0;
+    for (const auto& w : r.grad_w) {
+      std::memcpy(grad_w + off, w.data.data(), w.data.size() * sizeof(double));
+      off += w.data.size();
+    }
+  });
+}
+
 /* partition.cpp:79-89 */
 int rf_cross_edge_ratio(void* g, const uint32_t* owner, uint32_t parts, double* out) {
   return guard([&] {

@@ -12,3 +12,4 @@ from .cache import (  # noqa: F401
     BatchMode, CacheOutcome, CacheStats, DependentExperimentResult, DependentStepRow, LruCache,
     MinibatchSchedule, feature_load_sim, lru_access, nested_batches, run_dependent_experiment,
     shuffled_order, stack_fingerprint)
+from .train import GcnModel, TrainStepResult, coop_train_step, indep_train_step  # noqa: F401,E402

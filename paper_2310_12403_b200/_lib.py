@@ -94,6 +94,11 @@ _SIGS = {
     "cb_shuffled_order": (C.c_int, [_u64, _u64, _P]),
     "cb_features_set_tier": (C.c_int, [_P, C.c_int]),
     "cb_kernel_launches": (C.c_int, [C.POINTER(_u64)]),
+    "cb_gcn_model_init": (C.c_int, [C.c_int, _u32, _u32, _u32, C.c_int, _u64, _PP]),
+    "cb_gcn_model_weights": (C.c_int, [_P, C.c_int, _P, C.c_int, C.POINTER(_u64),
+                                       C.POINTER(_u64)]),
+    "cb_gcn_model_destroy": (None, [_P]),
+    "cb_train_step": (C.c_int, [_P, _P, _u32, _P, C.POINTER(C.c_double), _P]),
     "cb_plan_set_rw": (C.c_int, [_P, _u32, C.c_double, _u32]),
     "cb_plan_meta_async": (C.c_int, [_P, _P, C.POINTER(_u64)]),
     "cb_px_setup": (C.c_int, [_P, _P, _u32, _P]),
