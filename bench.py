@@ -758,7 +758,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-evidence", action="store_true")
-    ap.add_argument("--inflight", type=int, default=4,
+    ap.add_argument("--inflight", type=int, default=8,
                     help="independent minibatches in flight per GPU (streams); 1 = one at a time")
     ap.add_argument("--mode", choices=["coop", "indep"], default="coop",
                     help="N>1: cooperative minibatching (one part per GPU) or independent")

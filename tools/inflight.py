@@ -21,7 +21,7 @@ d = torch.from_numpy(seeds.view(np.int32)).cuda()
 sch = [cb.SeedSchedule.make(1, 1234)]
 for _ in range(K):
     sch.append(cb.schedule_advance(sch[-1]))
-for S in (1, 2, 3, 4, 6, 8):
+for S in (1, 2, 4, 6, 8, 12):
     plans = []
     for s in range(S):
         p = cb.Plan(g, None, 3, cfg, b)
