@@ -135,3 +135,21 @@ def test_cached_rows_match_oracle(small, host_tier):
     assert 0.0 < res.steady_miss_rate < 1.0
     if host_tier:
         store.set_tier(False)
+
+
+def test_nested_batches(small):
+    """nested_batches (cache.cpp:34-66): kappa b-sized slices of a super
+    batch under one epoch seed, each contained layerwise in the super batch's
+    expansion and equal to the oracle's expand of that slice."""
+    g, ref = small
+    rng = np.random.default_rng(2)
+    sup = rng.choice(ref.n, 4 * 50, replace=False).astype(np.uint32)
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, 5)
+    stacks = cb.nested_batches(g, sup, 4, 50, 2, cfg, 123)
+    assert len(stacks) == 4
+    for i, st in enumerate(stacks):
+        want = O.expand(ref, sup[i * 50:(i + 1) * 50], 2, O.LABOR0, 5, O.plain_sched(123))
+        for l in range(2):
+            assert np.array_equal(st.blocks[l].src_vertices, want[l]["src"])
+    with pytest.raises(cb.InputError):
+        cb.nested_batches(g, sup[:199], 4, 50, 2, cfg, 123)
