@@ -21,6 +21,29 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
   return x ^ (x >> 31);
 }
+// 64-bit x * C (mod 2^64) as one 32x32->64 multiply plus two multiply-adds
+// into the high word (the compiler's form needs a fourth add).
+__device__ __forceinline__ uint64_t mul64c(uint64_t x, uint64_t c) {
+  const uint32_t xl = static_cast<uint32_t>(x), xh = static_cast<uint32_t>(x >> 32);
+  const uint32_t cl = static_cast<uint32_t>(c), ch = static_cast<uint32_t>(c >> 32);
+  uint32_t lo, hi;
+  asm("{\n\t.reg .u32 ph;\n\t"
+      "mul.lo.u32 %0, %2, %4;\n\t"
+      "mul.hi.u32 ph, %2, %4;\n\t"
+      "mad.lo.u32 ph, %3, %4, ph;\n\t"
+      "mad.lo.u32 %1, %2, %5, ph;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(xl), "r"(xh), "r"(cl), "r"(ch));
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+// mix64 on the device with the cheaper multiplies (bit-identical)
+__device__ __forceinline__ uint64_t mix64_dev(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = mul64c(x ^ (x >> 30), 0xbf58476d1ce4e5b9ULL);
+  x = mul64c(x ^ (x >> 27), 0x94d049bb133111ebULL);
+  return x ^ (x >> 31);
+}
+
 __host__ __device__ __forceinline__ uint64_t hinit(uint64_t seed) { return mix64(seed ^ kSalt); }
 __host__ __device__ __forceinline__ uint64_t hstep(uint64_t h, uint64_t id) { return mix64(h ^ id); }
 // rng.hpp:42-44; (bits>>11) < 2^53 converts exactly, the 2^-53 scale is exact.

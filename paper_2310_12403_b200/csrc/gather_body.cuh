@@ -1,5 +1,4 @@
-// Row gather body shared by the standalone gather kernel (gather.cu) and the
-// fused batch kernel (sample.cu): out[j] = table[row(ids[j])], flattened
+// Row gather body of the gather kernel (gather.cu): out[j] = table[row(ids[j])], flattened
 // (row, vector) index space, 16/8/4/2-byte vectors, non-coherent
 // L1-no-allocate loads, streaming stores, UNROLL loads in flight per thread.
 #pragma once
@@ -134,31 +133,6 @@ __device__ __forceinline__ void gather_body(const V* __restrict__ table,
   }
 }
 
-
-// Dispatch on the vector width (bytes) of the row.
-__device__ __forceinline__ void gather_any(const void* table, int vec_bytes, uint32_t vpr,
-                                           const uint32_t* ids, const unsigned long long* count,
-                                           uint64_t cap_rows, const uint32_t* row_map,
-                                           void* out, unsigned role, unsigned ncta) {
-  switch (vec_bytes) {
-    case 16:
-      gather_body<uint4, 4>(static_cast<const uint4*>(table), ids, count, cap_rows, row_map, vpr,
-                            static_cast<uint4*>(out), role, ncta);
-      break;
-    case 8:
-      gather_body<uint2, 4>(static_cast<const uint2*>(table), ids, count, cap_rows, row_map, vpr,
-                            static_cast<uint2*>(out), role, ncta);
-      break;
-    case 4:
-      gather_body<uint32_t, 4>(static_cast<const uint32_t*>(table), ids, count, cap_rows,
-                               row_map, vpr, static_cast<uint32_t*>(out), role, ncta);
-      break;
-    default:
-      gather_body<unsigned short, 4>(static_cast<const unsigned short*>(table), ids, count,
-                                     cap_rows, row_map, vpr, static_cast<unsigned short*>(out),
-                                     role, ncta);
-  }
-}
 
 }  // namespace gbody
 }  // namespace cb

@@ -337,7 +337,7 @@ template <bool SMOOTH>
 __device__ __forceinline__ bool keep_rule(const Variates& v, uint64_t p1, uint64_t p2,
                                           uint32_t t, uint64_t th, unsigned long long& uncert,
                                           const double* vtab) {
-  if (!SMOOTH) return (hstep(p1, t) >> 11) <= th;
+  if (!SMOOTH) return (mix64_dev(p1 ^ t) >> 11) <= th;
   if (th == ~0ULL) return true;
   const double thr = __longlong_as_double(static_cast<long long>(th));
   const double rr = vtab ? __ldg(vtab + t) : smooth_finish(v, hstep(p1, t), hstep(p2, t));
