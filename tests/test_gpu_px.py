@@ -49,3 +49,55 @@ def _px_worker(rank, world, kind, fanouts, kappa, steps):
 ])
 def test_peer_coop(gpu, world, kind, fanouts, kappa, steps):
     spawn(world, _px_worker, (kind, fanouts, kappa, steps), timeout=600)
+
+
+def _px_nccl_worker():
+    import os
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_12403_b200 as cb
+    from oracle import oracle as O
+    from paper_2310_12403_b200.dist import PeerCoop, synth_shard
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        n, m, gseed = 1 << 13, 1 << 16, 5
+        g = cb.Graph.generate_rmat(n, m, gseed)
+        ref = O.rmat(n, m, gseed)
+        pm = cb.partition_random(g, 1, 2)
+        store = synth_shard(g, pm, 0, 16, 3, "f32")
+        pc = PeerCoop(g, pm, 0, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), 512, store)
+        seeds = O.draw_coop_seeds(pm.owner, 1, 256, 2, 0)
+        sched = cb.SeedSchedule.plain(4)
+        pc.sample(torch.from_numpy(seeds[0].view(np.int32)).cuda(), sched)  # device seeds
+        pc.load_inputs()
+        res, rows = pc.result(), pc.rows()
+        exp = O.coop_sample(ref, pm.owner, 1, seeds, 3, O.LABOR0, 10,
+                            O.Sched(sched.kappa, sched.z1, sched.z2, sched.iteration))
+        from tests.dist_harness import check_rank
+        check_rank(res, rows, exp, 0, 1, 3, 3, 16, "f32")
+    finally:
+        dist.destroy_process_group()
+    del os
+
+
+def test_peer_coop_nccl_single_rank(gpu):
+    """The NCCL code paths of PeerCoop (handle all-gather over NCCL, the
+    phase barrier as an NCCL all-reduce ordered on the plan stream, device
+    seeds) at world size 1, the only NCCL world one GPU allows."""
+    import torch
+
+    from tests.dist_harness import free_port
+    ctx = torch.multiprocessing.get_context("spawn")
+    import os
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(free_port())
+    p = ctx.Process(target=_px_nccl_worker)
+    p.start()
+    p.join(300)
+    assert p.exitcode == 0
