@@ -846,6 +846,7 @@ __global__ void __launch_bounds__(kNT) rw_walk_kernel(RwArgs a) {
           bpos = op;
         }
       }
+      __syncwarp();  // every lane's reads of cc[] precede the write below
       if (lane == 0) {
         a.slots[di * a.k + r] = bid;
         cc[bpos] = 0;  // taken
