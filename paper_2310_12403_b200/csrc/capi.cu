@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/coopbatch_cuda.h"
 #include "cb_internal.h"
 #include "exchange.h"
@@ -32,6 +34,12 @@ using cbdev::Variates;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range per host-side stage (nsys / ncu --nvtx); free without a tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 template <typename F>
 int guard(F&& f) {
@@ -580,6 +588,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
                        uint64_t cap_dst, uint64_t n_dst_param, Bitmap& set_bm,
                        const RelabelArgs& fused, uint64_t fused_work, bool smooth,
                        const ExtractArgs& ex) {
+  NvtxRange nvtx_("cb.layer");
   const DeviceGraph& g = pl->g->g;
   const LayerBufs& b = w.L[l];
   cudaStream_t st = pl->stream;
@@ -794,6 +803,7 @@ void prepare_rows(cb_plan* pl, const cb_features* f) {
 }
 
 void enqueue_gather(cb_plan* pl, const cb_features* f) {
+  NvtxRange nvtx_("cb.gather");
   const int vb = vec_bytes_for(f->row_bytes);
   for (uint32_t p = 0; p < pl->P; ++p) {
     PeWork& w = pl->pe[p];
@@ -1178,6 +1188,7 @@ void* cb_plan_stream(const cb_plan* plan) { return plan ? plan->stream : nullptr
 
 int cb_sample(cb_plan* plan, int mode, const uint32_t* seeds_flat, const uint64_t* seeds_off,
               const cb_sched* sched) {
+  NvtxRange nvtx_("cb.sample");
   return guard([&] {
     require(plan != nullptr && seeds_off != nullptr, "null argument");
     DeviceGuard dg(plan->device);
@@ -1187,6 +1198,7 @@ int cb_sample(cb_plan* plan, int mode, const uint32_t* seeds_flat, const uint64_
 
 int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
                    const uint64_t* seeds_off, const cb_sched* sched) {
+  NvtxRange nvtx_("cb.sample_sync");
   return guard([&] {
     require(plan != nullptr && seeds_off != nullptr, "null argument");
     DeviceGuard dg(plan->device);
@@ -1289,6 +1301,7 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
 
 int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_device,
                    const cb_sched* sched, int what) {
+  NvtxRange nvtx_("cb.replay");
   return guard([&] {
     require(plan != nullptr, "null plan");
     require(plan->exec_sample != nullptr, "no captured batch (call cb_plan_capture)");
@@ -1790,6 +1803,7 @@ int cb_cache_access_trace(cb_cache* c, const uint32_t* keys, uint64_t n, uint8_t
 int cb_cache_access_ids(cb_cache* c, const uint32_t* d_ids, uint64_t n, uint64_t order_key,
                         const cb_partition* pm, uint32_t part, const cb_features* backing,
                         void* d_rows_out, uint64_t* kept, void* stream) {
+  NvtxRange nvtx_("cb.cache_access");
   return guard([&] {
     require(c != nullptr, "null cache");
     require(pm == nullptr || part < pm->parts, "part index out of range");
@@ -1814,6 +1828,7 @@ int cb_cache_access_ids(cb_cache* c, const uint32_t* d_ids, uint64_t n, uint64_t
 int cb_cache_access_plan(cb_cache* c, cb_plan* plan, uint32_t part, uint64_t order_key,
                          const cb_partition* pm, uint32_t owner_part,
                          const cb_features* backing, void* d_rows_out, uint64_t* kept) {
+  NvtxRange nvtx_("cb.cache_access_plan");
   return guard([&] {
     require(c != nullptr && plan != nullptr, "null argument");
     require_batch(plan, part, plan->L - 1);
@@ -2104,6 +2119,7 @@ int cb_px_connect(cb_plan* plan, uint32_t q, const void* handle) {
 
 int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seeds,
                 const cb_sched* sched) {
+  NvtxRange nvtx_("cb.px_layer");
   return guard([&] {
     require(plan != nullptr && sched != nullptr, "null argument");
     require(layer >= 0 && layer < plan->L, "layer index out of range");
@@ -2148,6 +2164,7 @@ int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seed
 }
 
 int cb_px_owner(cb_plan* plan, int layer) {
+  NvtxRange nvtx_("cb.px_owner");
   return guard([&] {
     require(plan != nullptr, "null plan");
     require(layer >= 0 && layer < plan->L, "layer index out of range");
@@ -2167,6 +2184,7 @@ int cb_px_owner(cb_plan* plan, int layer) {
 }
 
 int cb_px_locate(cb_plan* plan, int layer) {
+  NvtxRange nvtx_("cb.px_locate");
   return guard([&] {
     require(plan != nullptr, "null plan");
     require(layer >= 0 && layer < plan->L, "layer index out of range");
@@ -2264,6 +2282,7 @@ int cb_px_connect_features(cb_plan* plan, uint32_t q, const void* handle, uint64
 }
 
 int cb_px_gather(cb_plan* plan, const cb_features* local) {
+  NvtxRange nvtx_("cb.px_gather");
   return guard([&] {
     require(plan != nullptr && local != nullptr, "null argument");
     require(plan->have_batch, "no sampled batch in this plan");
@@ -2422,6 +2441,7 @@ void cb_gcn_model_destroy(cb_model* m) {
 
 int cb_train_step(cb_plan* pl, const cb_features* f, uint32_t classes, cb_model* m,
                   double* loss_out, double* grad_w_out) {
+  NvtxRange nvtx_("cb.train_step");
   return guard([&] {
     require(pl != nullptr && f != nullptr && m != nullptr && loss_out != nullptr,
             "null argument");
