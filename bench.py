@@ -58,6 +58,7 @@ CONFIGS = {
                dtype="f16"),
 }
 GRAPH_SEED = 42
+CSV_ROWS: dict = {}  # per-step report rows for --csv-dir (reports.py)
 FEAT_SEED = 7
 RUN_SEED = 1234
 
@@ -236,6 +237,8 @@ def concavity_evidence(cb, g, scfg, L, b, row_bytes, dev, parts=(1, 2, 4, 8)):
         e1.record(st)
         plan.synchronize()
         coop_ms = e0.elapsed_time(e1)
+        CSV_ROWS.setdefault("run", []).append(
+            (f"coop_P{P}", cb.step_metrics(plan, cb.MODE_COOP, row_bytes)))
         c_s3 = sum(len(plan.owner_set(p)) for p in range(P))
         c_work = sum(plan.layer_sizes(p, l)["n_edges"] for p in range(P) for l in range(L))
         c_comm = sum(plan.exchange(l).total_communicated() for l in range(L))
@@ -360,6 +363,9 @@ def batch_sweep_evidence(cb, dev, batches=(1024, 4096, 16384, 65536), steps=10):
             if i >= 2:
                 ms.append(e0.elapsed_time(e1))
                 rows.append(plan.layer_sizes(0, L - 1)["n_src"])
+        CSV_ROWS.setdefault("curve", []).append(
+            (b, float(np.mean(rows)), float(np.std(rows) / np.sqrt(len(rows))),
+             float(np.mean(rows)) / b))
         out["sweep"].append({"batch": b, "ms_per_batch": float(np.mean(ms)),
                              "seeds_per_s": b / (float(np.mean(ms)) / 1e3),
                              "input_vertices_per_seed": float(np.mean(rows)) / b,
@@ -399,6 +405,8 @@ def kappa_evidence(cb, dev, steps_epochs=2, kappas=(1, 4, 16, 64, 256, None)):
                                         fingerprints=False, store=store)
         wall = time.perf_counter() - tt
         steady = r.rows[r.warmup_steps:]
+        CSV_ROWS.setdefault("cache", []).append(
+            (kappa, [(x.step, x.miss_rate, x.s_l, x.bytes) for x in r.rows]))
         out["sweep"].append({
             "kappa": "inf" if kappa is None else kappa,
             "steady_miss_rate": r.steady_miss_rate,
@@ -746,6 +754,29 @@ def run_ours(args, cfg):
         except Exception as e:  # report, never fake
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line), flush=True)
+    if args.csv_dir:
+        write_reports(args, cfg)
+
+
+def write_reports(args, cfg):
+    """The reference CLI's CSV reports (reports.py) of the evidence runs."""
+    from paper_2310_12403_b200 import reports as R
+    os.makedirs(args.csv_dir, exist_ok=True)
+    base = {"config": args.config, "layers": len(cfg["fanouts"]),
+            "fanout": "/".join(map(str, cfg["fanouts"])), "batch": cfg["batch"],
+            "sampler": cfg["kind"], "graph_seed": GRAPH_SEED, "run_seed": RUN_SEED}
+    for kappa, rows in CSV_ROWS.get("cache", []):
+        R.write_csv(os.path.join(args.csv_dir, f"cache_c3_kappa{kappa or 'inf'}.csv"),
+                    {**base, "config": "c3", "kappa": kappa or "inf", "mode": "smoothed"},
+                    R.CACHE_COLUMNS, rows)
+    if CSV_ROWS.get("curve"):
+        R.write_csv(os.path.join(args.csv_dir, "curve_c5.csv"), {**base, "config": "c5"},
+                    R.CURVE_COLUMNS, CSV_ROWS["curve"])
+    run = []
+    for tag, metrics in CSV_ROWS.get("run", []):
+        run.extend(R.run_rows(0, tag, metrics))
+    if run:
+        R.write_csv(os.path.join(args.csv_dir, "run_concavity.csv"), base, R.RUN_COLUMNS, run)
 
 
 def main():
@@ -758,6 +789,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-evidence", action="store_true")
+    ap.add_argument("--csv-dir", default="", help="also write the evidence as CLI-format CSVs")
     ap.add_argument("--inflight", type=int, default=8,
                     help="independent minibatches in flight per GPU (streams); 1 = one at a time")
     ap.add_argument("--mode", choices=["coop", "indep"], default="coop",

@@ -141,3 +141,14 @@ def test_edge_pred_seeds_match_reference():
         got = edge_pred_seeds(g.indptr, g.indices, pos, seed)
         want = O.edge_pred_seeds_reference(g, pos, seed)
         assert np.array_equal(got, want)
+
+
+def test_csv_report_format(tmp_path):
+    """reports.py: `# key=value` header, column line, atomic write (cli.cpp:74-99)."""
+    from paper_2310_12403_b200 import reports as R
+    p = tmp_path / "cache.csv"
+    R.write_csv(str(p), {"kappa": 4, "mode": "smoothed"}, R.CACHE_COLUMNS,
+                [(0, 0.5, 10, 1280), (1, 0.25, 12, 768)])
+    lines = p.read_text().splitlines()
+    assert lines[:3] == ["# kappa=4", "# mode=smoothed", "step,miss_rate,s_l,bytes"]
+    assert lines[3] == "0,0.5,10,1280" and not (tmp_path / "cache.csv.tmp").exists()
