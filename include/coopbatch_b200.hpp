@@ -117,6 +117,13 @@ class Graph {  // graph.hpp:21-53, resident in HBM
     check(cb_graph_generate_rmat(n, m, seed, device, &g));
     return Graph(g);
   }
+  // load_csr / save_csr (graph.cpp:216-252): CBCS straight into / out of HBM
+  static Graph load_csr(const std::string& path, int device = 0) {
+    cb_graph* g = nullptr;
+    check(cb_graph_load_cbcs(path.c_str(), device, &g));
+    return Graph(g);
+  }
+  void save_csr(const std::string& path) const { check(cb_graph_save_cbcs(h_.get(), path.c_str())); }
   std::uint64_t num_vertices() const {
     std::uint64_t n = 0;
     check(cb_graph_info(h_.get(), &n, nullptr, nullptr));
@@ -265,6 +272,154 @@ inline CoopSampleResult coop_sample(const Graph& g, const PartitionMap& pm,
     if (n) check(cb_download_owner_set(pl.get(), p, r.owner_sets[p].data()));
   }
   return r;
+}
+
+// ---- features, cache, training step ----------------------------------------
+enum class Dtype { kF64 = CB_F64, kF32 = CB_F32, kF16 = CB_F16 };
+
+class FeatureStore {  // coop.hpp:140-155, synthetic rows in HBM (sharded by pm)
+ public:
+  static FeatureStore synth(const Graph& g, std::uint32_t dim, std::uint64_t seed,
+                            Dtype dtype = Dtype::kF64, const PartitionMap* pm = nullptr) {
+    cb_features* f = nullptr;
+    check(cb_features_synth(g.get(), pm ? pm->get() : nullptr, dim, static_cast<int>(dtype), seed,
+                            &f));
+    return FeatureStore(f);
+  }
+  cb_features* get() const { return h_.get(); }
+
+ private:
+  explicit FeatureStore(cb_features* f) : h_(f, cb_features_destroy) {}
+  std::shared_ptr<cb_features> h_;
+};
+
+enum class CacheOutcome { kHit, kMiss };
+
+class LruCache {  // cache.hpp:17-42 (exact LRU, evaluated on the device)
+ public:
+  LruCache(std::uint64_t capacity, std::uint64_t n_keys, int device = 0) {
+    if (capacity == 0) throw InputError("LruCache: capacity must be >= 1");
+    cb_cache* c = nullptr;
+    check(cb_cache_create(device, n_keys, capacity, 0, &c));
+    h_.reset(c, cb_cache_destroy);
+  }
+  CacheOutcome access(VertexId key) {
+    std::uint8_t miss = 0;
+    check(cb_cache_access_trace(h_.get(), &key, 1, &miss));
+    return miss ? CacheOutcome::kMiss : CacheOutcome::kHit;
+  }
+  // LruCache::access over a whole trace, in order (one device batch per run
+  // of distinct keys)
+  std::vector<CacheOutcome> access_all(const std::vector<VertexId>& keys) {
+    std::vector<std::uint8_t> miss(keys.size());
+    check(cb_cache_access_trace(h_.get(), keys.data(), keys.size(), miss.data()));
+    std::vector<CacheOutcome> out(keys.size());
+    for (std::size_t i = 0; i < keys.size(); ++i)
+      out[i] = miss[i] ? CacheOutcome::kMiss : CacheOutcome::kHit;
+    return out;
+  }
+  std::uint64_t hits() const { return stat(0); }
+  std::uint64_t misses() const { return stat(1); }
+  std::uint64_t size() const { return stat(2); }
+  std::vector<VertexId> resident() const {
+    std::uint64_t n = 0;
+    check(cb_cache_resident(h_.get(), nullptr, 0, &n));
+    std::vector<VertexId> out(n);
+    check(cb_cache_resident(h_.get(), out.data(), n, &n));
+    return out;
+  }
+
+ private:
+  std::uint64_t stat(int i) const {
+    std::uint64_t v[3];
+    check(cb_cache_stats(h_.get(), &v[0], &v[1], &v[2]));
+    return v[i];
+  }
+  std::shared_ptr<cb_cache> h_;
+};
+
+class GcnModel {  // coop.hpp:126-135
+ public:
+  static GcnModel init(std::uint32_t in_dim, std::uint32_t hidden, std::uint32_t num_classes,
+                       int num_layers, std::uint64_t seed, int device = 0) {
+    cb_model* m = nullptr;
+    check(cb_gcn_model_init(device, in_dim, hidden, num_classes, num_layers, seed, &m));
+    return GcnModel(m, num_layers, num_classes);
+  }
+  int num_layers() const { return L_; }
+  std::uint32_t num_classes() const { return C_; }
+  cb_model* get() const { return h_.get(); }
+
+ private:
+  GcnModel(cb_model* m, int L, std::uint32_t C) : h_(m, cb_gcn_model_destroy), L_(L), C_(C) {}
+  std::shared_ptr<cb_model> h_;
+  int L_;
+  std::uint32_t C_;
+};
+
+struct DenseMatrix {  // coop.hpp:95-103 (row-major)
+  std::uint64_t rows = 0, cols = 0;
+  std::vector<double> data;
+};
+
+struct TrainStepResult {  // coop.hpp:175-179 (metrics: see the Python mirror)
+  double loss = 0.0;
+  std::vector<DenseMatrix> grad_w;
+};
+
+namespace detail {
+inline TrainStepResult train(cb_plan* pl, const FeatureStore& store, const GcnModel& model) {
+  TrainStepResult r;
+  std::uint64_t total = 0;
+  for (int l = 0; l < model.num_layers(); ++l) {
+    DenseMatrix d;
+    check(cb_gcn_model_weights(model.get(), l, nullptr, 0, &d.rows, &d.cols));
+    total += d.rows * d.cols;
+    r.grad_w.push_back(d);
+  }
+  std::vector<double> gw(total);
+  check(cb_train_step(pl, store.get(), model.num_classes(), model.get(), &r.loss, gw.data()));
+  std::uint64_t o = 0;
+  for (auto& d : r.grad_w) {
+    d.data.assign(gw.begin() + o, gw.begin() + o + d.rows * d.cols);
+    o += d.rows * d.cols;
+  }
+  return r;
+}
+}  // namespace detail
+
+// coop.cpp:438-556 (store: f64, sharded by pm)
+inline TrainStepResult coop_train_step(const Graph& g, const PartitionMap& pm,
+                                       const std::vector<std::vector<VertexId>>& per_pe,
+                                       int num_layers, const SamplerConfig& cfg,
+                                       const SeedSchedule& schedule, const GcnModel& model,
+                                       const FeatureStore& store) {
+  if (per_pe.size() != pm.num_parts())
+    throw InputError("coop_sample: seed lists must match the partition count");
+  std::uint64_t maxb = 1;
+  std::vector<VertexId> flat;
+  std::vector<std::uint64_t> off{0};
+  for (const auto& s : per_pe) {
+    flat.insert(flat.end(), s.begin(), s.end());
+    off.push_back(flat.size());
+    maxb = std::max<std::uint64_t>(maxb, s.size());
+  }
+  auto pl = detail::make_plan(g, &pm, num_layers, cfg, maxb);
+  const cb_sched s = schedule.c();
+  check(cb_sample_sync(pl.get(), CB_MODE_COOP, flat.data(), off.data(), &s));
+  return detail::train(pl.get(), store, model);
+}
+
+// coop.cpp:560-610, one part (P = 1) per call of the reference's parts loop
+inline TrainStepResult indep_train_step(const Graph& g, const std::vector<VertexId>& seeds,
+                                        int num_layers, const SamplerConfig& cfg,
+                                        const SeedSchedule& schedule, const GcnModel& model,
+                                        const FeatureStore& store) {
+  auto pl = detail::make_plan(g, nullptr, num_layers, cfg, seeds.size());
+  const std::uint64_t off[2] = {0, seeds.size()};
+  const cb_sched s = schedule.c();
+  check(cb_sample_sync(pl.get(), CB_MODE_INDEP, seeds.data(), off, &s));
+  return detail::train(pl.get(), store, model);
 }
 
 }  // namespace coopbatch_b200

@@ -23,7 +23,18 @@ void rf_stack_free(ob_stack*);
 void rf_coop_free(ob_coop*);
 void rf_sched_make(uint64_t, uint64_t, ob_sched*);
 void rf_free(void*);
+void* rf_lru_new(uint64_t);
+int rf_lru_access(void*, uint32_t);
+void rf_lru_free(void*);
+void* rf_features_new(uint64_t, uint32_t, uint32_t, uint64_t);
+void rf_features_free(void*);
+int rf_train_step(void*, void*, int, const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
+                  int, int, uint32_t, const ob_sched*, uint32_t, uint64_t, double*, double*);
+int rf_save_csr(void*, const char*);
 }
+
+#include <cmath>
+#include <string>
 
 namespace cb = coopbatch_b200;
 
@@ -136,6 +147,67 @@ int main() {
     threw = true;
   }
   CHECK(threw);
+
+  // LruCache == reference LruCache, access by access (cache.cpp:12-27)
+  {
+    cb::LruCache c(7, n);
+    void* r = rf_lru_new(7);
+    std::vector<uint32_t> keys;
+    uint64_t x = 1;
+    for (int i = 0; i < 3000; ++i) {
+      x = x * 6364136223846793005ULL + 1442695040888963407ULL;
+      keys.push_back(static_cast<uint32_t>((x >> 33) % 23));
+    }
+    const auto got_m = c.access_all(keys);
+    uint64_t misses = 0;
+    for (std::size_t i = 0; i < keys.size(); ++i) {
+      const int miss = rf_lru_access(r, keys[i]);
+      misses += miss;
+      CHECK((got_m[i] == cb::CacheOutcome::kMiss) == (miss != 0));
+    }
+    CHECK(c.misses() == misses && c.hits() == keys.size() - misses && c.size() == 7);
+    rf_lru_free(r);
+  }
+
+  // coop_train_step == reference coop_train_step (coop.cpp:438-556)
+  {
+    const uint32_t dim = 6, classes = 4, hidden = 5;
+    auto store = cb::FeatureStore::synth(g, dim, 1, cb::Dtype::kF64, &pm);
+    auto model = cb::GcnModel::init(dim, hidden, classes, 2, 2);
+    cb::SamplerConfig tc;
+    tc.kind = cb::SamplerKind::kLabor0;
+    tc.fanout = 4;
+    const auto tr = cb::coop_train_step(g, pm, per_pe, 2, tc, {1, 31, 31, 0}, model, store);
+    void* rfs = rf_features_new(n, dim, classes, 1);
+    double loss = 0;
+    std::vector<double> gw(hidden * classes + dim * hidden);
+    ob_sched ts{1, 31, 31, 0};
+    CHECK(rf_train_step(rg, rfs, 0, owner.data(), 4, flat.data(), off.data(), 2, CB_LABOR0, 4,
+                        &ts, hidden, 2, &loss, gw.data()) == 0);
+    CHECK(std::fabs(tr.loss - loss) <= 1e-12 * std::fabs(loss));
+    std::size_t o = 0;
+    double err = 0, mag = 0;
+    for (const auto& d : tr.grad_w)
+      for (double v : d.data) {
+        err = std::fmax(err, std::fabs(v - gw[o]));
+        mag = std::fmax(mag, std::fabs(gw[o]));
+        ++o;
+      }
+    CHECK(o == gw.size() && err <= 1e-12 * mag);
+    rf_features_free(rfs);
+  }
+
+  // CBCS written by the reference loads into HBM (graph.cpp:216-252)
+  {
+    const std::string path = "/tmp/cb_test_shim.cbcs";
+    CHECK(rf_save_csr(rg, path.c_str()) == 0);
+    auto h = cb::Graph::load_csr(path);
+    CHECK(h.num_vertices() == n);
+    const auto a = cb::expand(h, seeds, 2, cfg, {1, 5, 5, 0});
+    const auto b = cb::expand(g, seeds, 2, cfg, {1, 5, 5, 0});
+    for (int l = 0; l < 2; ++l) CHECK(a.blocks[l].edges == b.blocks[l].edges);
+    std::remove(path.c_str());
+  }
 
   rf_graph_free(rg);
   rf_free(ip);
