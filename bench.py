@@ -770,7 +770,10 @@ def write_reports(args, cfg):
                     {**base, "config": "c3", "kappa": kappa or "inf", "mode": "smoothed"},
                     R.CACHE_COLUMNS, rows)
     if CSV_ROWS.get("curve"):
-        R.write_csv(os.path.join(args.csv_dir, "curve_c5.csv"), {**base, "config": "c5"},
+        c5 = CONFIGS["c5"]
+        R.write_csv(os.path.join(args.csv_dir, "curve_c5.csv"),
+                    {**base, "config": "c5", "layers": len(c5["fanouts"]),
+                     "fanout": "/".join(map(str, c5["fanouts"])), "batch": "sweep"},
                     R.CURVE_COLUMNS, CSV_ROWS["curve"])
     run = []
     for tag, metrics in CSV_ROWS.get("run", []):
