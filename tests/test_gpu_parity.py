@@ -366,6 +366,34 @@ def test_gather_matches_reference_forward(powerlaw):
     assert np.array_equal(got, out)
 
 
+def test_coop_graph_replay_matches_oracle(c1):
+    """A captured cooperative batch (P = 4: sampling, route / extract / locate
+    rendezvous per layer, fused gather) replayed with new seeds and keys."""
+    g, ref = c1
+    P, b = 4, 128
+    pm = cb.partition_random(g, P, 12)
+    owner = O.partition_random(ref.n, P, 12)
+    store = cb.FeatureStore.synth(g, 16, 2, "f32", pm)
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, 10)
+    plan = cb.Plan(g, pm, 3, cfg, b)
+    sched = cb.SeedSchedule.make(1, 21)
+    seeds0 = O.draw_coop_seeds(owner, P, b, 12, 0)
+    plan.sample(seeds0, sched, cb.MODE_COOP)
+    plan.capture(np.arange(P + 1, dtype=np.uint64) * b, sched, cb.MODE_COOP, store)
+    for step in range(1, 3):
+        sched = cb.schedule_advance(sched)
+        seeds = O.draw_coop_seeds(owner, P, b, 12, step)
+        flat = np.ascontiguousarray(np.concatenate(seeds), dtype=np.uint32)
+        plan.replay(flat.ctypes.data, sched, False, 3)
+        plan.synchronize()
+        exp = O.coop_sample(ref, owner, P, seeds, 3, O.LABOR0, 10, osched(sched))
+        for p in range(P):
+            assert_stack_eq(plan.stack(p), exp["stacks"][p], f"coop replay {step} part {p}")
+            assert np.array_equal(plan.owner_set(p), exp["owner_sets"][p])
+            rows = plan.rows(p, store)
+            assert np.array_equal(rows, O.feature_rows(2, 16, "f32", exp["stacks"][p][-1]["src"]))
+
+
 @pytest.mark.parametrize("kappa", [1, 4])
 def test_graph_replay_matches_eager(c1, kappa):
     """cb_plan_capture/cb_plan_replay (the bench path) == eager batches."""
