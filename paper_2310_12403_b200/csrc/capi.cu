@@ -6,90 +6,9 @@
 // stream; counts stay on the device (LayerMeta) so a batch never waits on the
 // host. Contract violations raise cb::Error(kInput) -> CB_INPUT, mirroring
 // coopbatch::InputError (common.hpp:12-15).
-#include <cub/cub.cuh>
-#include <thrust/iterator/transform_iterator.h>
+#include "capi_internal.h"
 
-#include <algorithm>
-#include <cmath>
-#include <cstdlib>
-#include <cstdio>
-#include <cstring>
-#include <memory>
-#include <string>
-#include <vector>
-
-#include <nvtx3/nvToolsExt.h>
-
-#include "../../include/coopbatch_cuda.h"
-#include "cb_internal.h"
-#include "exchange.h"
-#include "gather.h"
-#include "dist.h"
-#include "cache.h"
-#include "train.h"
-
-using namespace cb;
-using cbdev::Variates;
-
-namespace {
-
-thread_local std::string g_err;
-
-// NVTX range per host-side stage (nsys / ncu --nvtx); free without a tool.
-struct NvtxRange {
-  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
-  ~NvtxRange() { nvtxRangePop(); }
-};
-
-template <typename F>
-int guard(F&& f) {
-  try {
-    f();
-    return CB_OK;
-  } catch (const Error& e) {
-    g_err = e.what();
-    return e.code;
-  } catch (const std::bad_alloc& e) {
-    g_err = std::string("host allocation failed: ") + e.what();
-    return CB_INTERNAL;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return CB_INTERNAL;
-  }
-}
-
-struct Arena {
-  std::vector<void*> ptrs;
-  template <typename T>
-  T* alloc(uint64_t count) {
-    void* p = nullptr;
-    CB_CUDA(cudaMalloc(&p, std::max<uint64_t>(count, 1) * sizeof(T) + 64));
-    ptrs.push_back(p);
-    return static_cast<T*>(p);
-  }
-  void release() {
-    for (void* p : ptrs) cudaFree(p);
-    ptrs.clear();
-  }
-  ~Arena() { release(); }
-};
-
-struct DeviceGuard {
-  int prev = 0;
-  explicit DeviceGuard(int dev) {
-    CB_CUDA(cudaGetDevice(&prev));
-    if (prev != dev) CB_CUDA(cudaSetDevice(dev));
-  }
-  ~DeviceGuard() { cudaSetDevice(prev); }
-};
-
-uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
-uint64_t sat_mul(uint64_t a, uint64_t b) {
-  if (a != 0 && b > UINT64_MAX / a) return UINT64_MAX;
-  return a * b;
-}
-
-}  // namespace
+thread_local std::string cb::capi::g_err;
 
 namespace cb {
 std::atomic<unsigned long long> g_kernel_launches{0};
@@ -102,162 +21,8 @@ bool pdl_enabled() {
 }
 }  // namespace cb
 
-// ------------------------------------------------------------------ handles --
-struct cb_graph {
-  DeviceGraph g;
-  ~cb_graph() {
-    if (g.indptr) cudaFree(g.indptr);
-    if (g.indices) cudaFree(g.indices);
-  }
-};
-
-struct cb_partition {
-  int device = 0;
-  uint64_t n = 0;
-  uint32_t parts = 1;
-  Arena mem;
-  uint32_t* owner = nullptr;    // [n]
-  uint32_t* row_map = nullptr;  // [n] global table row of v (shard-major)
-  uint32_t* members = nullptr;  // [n] vertex of each global row
-  std::vector<uint64_t> shard_off;  // [parts+1]
-};
-
-struct cb_features {
-  int device = 0;
-  uint32_t dim = 0;
-  int dtype = CB_F32;
-  uint64_t seed = 0;            // FeatureStore::synth seed (values and labels)
-  uint64_t row_bytes = 0;
-  uint64_t n_rows = 0;
-  Arena mem;
-  void* table = nullptr;
-  uint32_t* row_map = nullptr;  // nullptr = identity (P = 1)
-  uint64_t shard_rows = 0;      // rows actually held (sharded tables)
-  uint64_t shard_r0 = 0;        // first global row of the shard
-  void* host_base = nullptr;    // pinned mapped host copy (host tier) or nullptr
-  void* hbm_table = nullptr;    // the HBM table while the host tier is active
-  ~cb_features() {
-    if (host_base) cudaFreeHost(host_base);
-  }
-};
-
-struct cb_cache {
-  std::unique_ptr<DeviceLru> lru;
-  cudaStream_t stream = nullptr;
-  ~cb_cache() {
-    if (stream) cudaStreamDestroy(stream);
-  }
-};
-
-namespace {
-
-struct PeWork {
-  std::vector<LayerBufs> L;
-  Bitmap bm[2];
-  Sync sync;
-  std::vector<uint32_t*> loc_part, loc_row;  // [layer] cap_src
-  uint32_t* owner_final = nullptr;            // coop: S^L_p
-  uint64_t cap_final = 0;
-  void* rows = nullptr;
-  uint64_t cap_rows = 0;
-  uint64_t rows_row_bytes = 0;
-};
-
-// Multi-process peer exchange state (one part per rank): this rank's
-// IPC-exportable exchange region (2 layer slots of bitmap + summary + word
-// ranks) and every rank's mapping of it.
-struct PxState {
-  uint32_t rank = 0, world = 0;
-  const uint32_t* owner = nullptr;  // pm->owner (device)
-  void* region = nullptr;           // local cudaMalloc, exported
-  uint64_t region_bytes = 0;
-  Bitmap slot[2];                   // local views of the region
-  PxPeers peers[2];                 // per slot, every rank's pointers
-  std::vector<void*> opened;        // IPC mappings to close
-  unsigned long long* send = nullptr;  // [L * world] this rank's send_counts rows
-  uint64_t layer_ctr = 0;           // slot of a layer = ctr & 1 (alternates across batches)
-  std::vector<int> slot_of;         // [L]
-  // features: virtual bases of every rank's shard (device array) + mappings
-  const unsigned char** d_fbase = nullptr;
-  std::vector<const unsigned char*> fbase;
-  std::vector<void*> fopened;
-  uint64_t frow_bytes = 0;
-  ~PxState() {
-    for (void* p : opened) cudaIpcCloseMemHandle(p);
-    for (void* p : fopened) cudaIpcCloseMemHandle(p);
-    if (region) cudaFree(region);
-    if (send) cudaFree(send);
-    if (d_fbase) cudaFree(d_fbase);
-  }
-};
-
-}  // namespace
-
-struct cb_plan {
-  int device = 0;
-  const cb_graph* g = nullptr;
-  const cb_partition* pm = nullptr;
-  uint32_t P = 1;
-  int L = 1;
-  int kind = CB_LABOR0;
-  std::vector<uint32_t> fanouts;
-  uint64_t max_seeds = 0;
-  double grow = 1.0;
-  cudaStream_t stream = nullptr;
-  Arena mem;       // capacity-dependent buffers
-  Arena rows_mem;  // gathered rows
-  std::vector<PeWork> pe;
-  LayerMeta* meta = nullptr;                // [P*(L+1)]
-  unsigned long long* send_counts = nullptr;  // [L*P*P]
-  Variates* var = nullptr;
-  uint32_t* seeds = nullptr;
-  uint64_t seeds_cap = 0;
-  int mode = -1;          // mode of the last batch
-  int dirty_mode = -1;    // mode whose final bitmap still holds bits (-1: clean)
-  uint32_t dist_world = 0;  // >0: one part of a multi-process cooperative step
-  unsigned long long* scratch = nullptr;  // small device counters (dist ops)
-  bool smooth = false;    // kernels of the last enqueue used smoothed variates
-  bool trace_on = false;   // globaltimer stamps per CTA (debug, CB_TRACE=1)
-  unsigned long long* trace = nullptr;  // [kTraceSlots]
-  std::vector<cudaEvent_t>* prof = nullptr;  // per-launch events (cb_plan_profile)
-  bool prof_external = false;                 // record as graph event nodes
-  std::vector<cudaEvent_t> graph_events;      // of exec_prof
-  cudaGraphExec_t exec_prof = nullptr;
-  bool cap_smooth = false;
-  bool have_batch = false;
-  bool have_rows = false;
-  uint64_t batches = 0;
-  uint64_t launches = 0;  // kernels enqueued by the last cb_sample (+ cb_gather)
-  double* vtab = nullptr;  // smoothed LABOR r_t table [n] (nullptr: per position)
-  uint32_t rw_length = 3, rw_walks = 100;  // samplers.hpp:19-22 defaults
-  double rw_restart = 0.5;
-  std::unique_ptr<PxState> px;  // multi-process peer exchange (dist plans)
-  std::vector<uint64_t> seeds_off;
-  // CUDA graphs of one batch (sample) and its gather, replayed per step
-  cudaGraphExec_t exec_sample = nullptr;
-  cudaGraphExec_t exec_gather = nullptr;
-  cudaGraphExec_t exec_all = nullptr;  // sample + gather in one graph
-  int cap_mode = -1;
-  std::vector<uint64_t> cap_off;
-  uint64_t cap_launches_sample = 0, cap_launches_gather = 0;
-
-  void drop_graphs() {
-    if (exec_sample) cudaGraphExecDestroy(exec_sample);
-    if (exec_gather) cudaGraphExecDestroy(exec_gather);
-    if (exec_all) cudaGraphExecDestroy(exec_all);
-    if (exec_prof) cudaGraphExecDestroy(exec_prof);
-    for (auto e : graph_events) cudaEventDestroy(e);
-    graph_events.clear();
-    exec_sample = exec_gather = exec_all = exec_prof = nullptr;
-  }
-  ~cb_plan() { drop_graphs(); }
-
-  LayerMeta* meta_at(uint32_t p, int l) { return meta + p * (L + 1) + l; }
-  bool coop_active() const { return mode == CB_MODE_COOP && P > 1; }
-  bool own_dst() const { return coop_active() || dist_world > 0; }
-};
-
-namespace {
+namespace cb {
+namespace capi {
 
 void make_bitmap(Arena& a, Bitmap& b, uint64_t n) {
   b.words = ceil_div(n, 32);
@@ -816,7 +581,8 @@ void enqueue_gather(cb_plan* pl, const cb_features* f) {
   pl->have_rows = true;
 }
 
-}  // namespace
+}  // namespace capi
+}  // namespace cb
 
 // ===================================================================== C-ABI ==
 extern "C" {
@@ -1766,851 +1532,6 @@ int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_
       k = P * (1 + L * samp + 1);
     if (with_gather) k += P;
     *n = k;
-  });
-}
-
-// ------------------------------------------------------------- LRU cache --
-int cb_cache_create(int device, uint64_t n_keys, uint64_t capacity, uint64_t row_bytes,
-                    cb_cache** out) {
-  return guard([&] {
-    require(out != nullptr, "null argument");
-    require(capacity >= 1, "LruCache: capacity must be >= 1");
-    DeviceGuard dg(device);
-    auto c = std::make_unique<cb_cache>();
-    c->lru = std::make_unique<DeviceLru>(device, n_keys, capacity, row_bytes);
-    CB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    *out = c.release();
-  });
-}
-
-void cb_cache_destroy(cb_cache* c) {
-  if (!c) return;
-  int prev = 0;
-  cudaGetDevice(&prev);
-  cudaSetDevice(c->lru->device());
-  delete c;
-  cudaSetDevice(prev);
-}
-
-int cb_cache_access_trace(cb_cache* c, const uint32_t* keys, uint64_t n, uint8_t* miss) {
-  return guard([&] {
-    require(c != nullptr && (n == 0 || (keys != nullptr && miss != nullptr)), "null argument");
-    DeviceGuard dg(c->lru->device());
-    c->lru->access_trace(keys, n, miss, c->stream);
-  });
-}
-
-int cb_cache_access_ids(cb_cache* c, const uint32_t* d_ids, uint64_t n, uint64_t order_key,
-                        const cb_partition* pm, uint32_t part, const cb_features* backing,
-                        void* d_rows_out, uint64_t* kept, void* stream) {
-  NvtxRange nvtx_("cb.cache_access");
-  return guard([&] {
-    require(c != nullptr, "null cache");
-    require(pm == nullptr || part < pm->parts, "part index out of range");
-    require(d_rows_out == nullptr || backing != nullptr, "rows requested without a table");
-    require(backing == nullptr || c->lru->row_bytes() == 0 ||
-                backing->row_bytes == c->lru->row_bytes(),
-            "cache row size does not match the feature table");
-    DeviceGuard dg(c->lru->device());
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
-    CacheGatherSrc src;
-    if (backing && d_rows_out) {
-      src.table = backing->table;
-      src.row_map = backing->row_map;
-      src.rows_out = d_rows_out;
-    }
-    const uint64_t k = c->lru->access_ids(d_ids, n, order_key, pm ? pm->owner : nullptr,
-                                          part, src, st);
-    if (kept) *kept = k;
-  });
-}
-
-int cb_cache_access_plan(cb_cache* c, cb_plan* plan, uint32_t part, uint64_t order_key,
-                         const cb_partition* pm, uint32_t owner_part,
-                         const cb_features* backing, void* d_rows_out, uint64_t* kept) {
-  NvtxRange nvtx_("cb.cache_access_plan");
-  return guard([&] {
-    require(c != nullptr && plan != nullptr, "null argument");
-    require_batch(plan, part, plan->L - 1);
-    DeviceGuard dg(plan->device);
-    check_overflow(plan);
-    const uint64_t n = host_meta(plan, part, plan->L - 1).n_src;
-    CB_CUDA(cudaStreamSynchronize(plan->stream));
-    const uint32_t* ids = plan->pe[part].L[plan->L - 1].src;
-    if (backing && !d_rows_out) {  // rows land in the plan's own row buffer
-      require(pm == nullptr, "plan row buffer holds all input rows: no owner filter");
-      prepare_rows(plan, backing);
-      d_rows_out = plan->pe[part].rows;
-      plan->have_rows = true;
-    }
-    CacheGatherSrc src;
-    if (backing && d_rows_out) {
-      require(c->lru->row_bytes() == 0 || backing->row_bytes == c->lru->row_bytes(),
-              "cache row size does not match the feature table");
-      src.table = backing->table;
-      src.row_map = backing->row_map;
-      src.rows_out = d_rows_out;
-    }
-    const uint64_t k = c->lru->access_ids(ids, n, order_key, pm ? pm->owner : nullptr,
-                                          owner_part, src, plan->stream);
-    if (kept) *kept = k;
-  });
-}
-
-int cb_cache_access_host_ids(cb_cache* c, const uint32_t* ids, uint64_t n, uint64_t order_key,
-                             const cb_partition* pm, uint32_t part, uint64_t* kept) {
-  return guard([&] {
-    require(c != nullptr && (n == 0 || ids != nullptr), "null argument");
-    require(pm == nullptr || part < pm->parts, "part index out of range");
-    DeviceGuard dg(c->lru->device());
-    uint32_t* d = nullptr;
-    CB_CUDA(cudaMalloc(&d, n * 4 + 16));
-    uint64_t k = 0;
-    try {
-      CB_CUDA(cudaMemcpy(d, ids, n * 4, cudaMemcpyHostToDevice));
-      k = c->lru->access_ids(d, n, order_key, pm ? pm->owner : nullptr, part, CacheGatherSrc{},
-                             c->stream);
-    } catch (...) {
-      cudaFree(d);
-      throw;
-    }
-    cudaFree(d);
-    if (kept) *kept = k;
-  });
-}
-
-int cb_cache_stats(const cb_cache* c, uint64_t* hits, uint64_t* misses, uint64_t* size) {
-  return guard([&] {
-    require(c != nullptr, "null cache");
-    if (hits) *hits = c->lru->hits();
-    if (misses) *misses = c->lru->misses();
-    if (size) *size = c->lru->size();
-  });
-}
-
-int cb_cache_reset_counters(cb_cache* c) {
-  return guard([&] {
-    require(c != nullptr, "null cache");
-    c->lru->reset_counters();
-  });
-}
-
-int cb_cache_resident(cb_cache* c, uint32_t* out, uint64_t cap_out, uint64_t* n) {
-  return guard([&] {
-    require(c != nullptr && n != nullptr, "null argument");
-    DeviceGuard dg(c->lru->device());
-    std::vector<uint32_t> r;
-    c->lru->resident(r);
-    require(out == nullptr || cap_out >= r.size(), "output buffer too small");
-    if (out) std::memcpy(out, r.data(), r.size() * 4);
-    *n = r.size();
-  });
-}
-
-int cb_cache_storage(const cb_cache* c, const void** d_rows) {
-  return guard([&] {
-    require(c != nullptr && d_rows != nullptr, "null argument");
-    *d_rows = c->lru->storage();
-  });
-}
-
-// stack_fingerprint (cache.cpp:123-133): sequential mix64 fold over the
-// downloaded blocks of part p, computed on the host.
-int cb_stack_fingerprint(cb_plan* plan, uint32_t part, uint64_t* out) {
-  return guard([&] {
-    require(plan != nullptr && out != nullptr, "null argument");
-    require_batch(plan, part, 0);
-    uint64_t h = 0x9e3779b97f4a7c15ULL;
-    for (int l = 0; l < plan->L; ++l) {
-      uint64_t sz[6];
-      if (cb_layer_sizes(plan, part, l, sz) != CB_OK) throw Error(kCuda, g_err);
-      std::vector<uint32_t> dst(sz[0]), src(sz[1]), edges(2 * sz[2]);
-      if (cb_download_block(plan, part, l, dst.data(), src.data(), edges.data(), nullptr) !=
-          CB_OK)
-        throw Error(kCuda, g_err);
-      h = cbdev::mix64(h ^ static_cast<uint64_t>(l));
-      for (uint32_t v : dst) h = cbdev::mix64(h ^ v);
-      for (uint32_t v : src) h = cbdev::mix64(h ^ (0x100000000ULL | v));
-      for (uint64_t e = 0; e < sz[2]; ++e)
-        h = cbdev::mix64(h ^ ((static_cast<uint64_t>(edges[2 * e]) << 32) | edges[2 * e + 1]));
-    }
-    *out = h;
-  });
-}
-
-// Fixed training order of run_dependent_experiment (cache.cpp:155-162):
-// Fisher-Yates with j = (u64)(hash_uniform(seed, {kStreamSeedDraw, i}) * i).
-int cb_shuffled_order(uint64_t n, uint64_t seed, uint32_t* out) {
-  return guard([&] {
-    require(out != nullptr || n == 0, "null argument");
-    for (uint64_t v = 0; v < n; ++v) out[v] = static_cast<uint32_t>(v);
-    const uint64_t pfx = cbdev::hstep(cbdev::hinit(seed), 8ULL);
-    for (uint64_t i = n; i > 1; --i) {
-      const double u = cbdev::ufb(cbdev::hstep(pfx, i));
-      const uint64_t j = static_cast<uint64_t>(u * static_cast<double>(i));
-      std::swap(out[i - 1], out[std::min(j, i - 1)]);
-    }
-  });
-}
-
-// Storage tier of a feature table: 1 = pinned host memory mapped into the
-// device address space (rows then cross the host link on every miss),
-// 0 = HBM. The row layout is unchanged.
-int cb_features_set_tier(cb_features* f, int host) {
-  return guard([&] {
-    require(f != nullptr, "null features");
-    DeviceGuard dg(f->device);
-    require(f->shard_rows == 0, "host tier of a single-part shard table is not supported");
-    const uint64_t rows = f->n_rows;
-    const uint64_t bytes = rows * f->row_bytes;
-    const bool on_host = f->host_base != nullptr;
-    if (static_cast<bool>(host) == on_host) return;
-    CB_CUDA(cudaDeviceSynchronize());
-    if (host) {
-      void* h = nullptr;
-      CB_CUDA(cudaHostAlloc(&h, bytes + 64, cudaHostAllocMapped | cudaHostAllocPortable));
-      CB_CUDA(cudaMemcpy(h, f->table, bytes, cudaMemcpyDeviceToHost));
-      void* d = nullptr;
-      CB_CUDA(cudaHostGetDevicePointer(&d, h, 0));
-      f->hbm_table = f->table;
-      f->host_base = h;
-      f->table = d;
-    } else {
-      CB_CUDA(cudaMemcpy(f->hbm_table, f->host_base, bytes, cudaMemcpyHostToDevice));
-      CB_CUDA(cudaFreeHost(f->host_base));
-      f->host_base = nullptr;
-      f->table = f->hbm_table;
-      f->hbm_table = nullptr;
-    }
-  });
-}
-
-int cb_plan_set_rw(cb_plan* plan, uint32_t rw_length, double rw_restart, uint32_t rw_walks) {
-  return guard([&] {
-    require(plan != nullptr, "null plan");
-    require(rw_length >= 1 && rw_walks >= 1, "sample_rw: rw_length and rw_walks must be >= 1");
-    require(rw_restart >= 0.0 && rw_restart < 1.0, "sample_rw: rw_restart must be in [0, 1)");
-    require(static_cast<uint64_t>(rw_length) * rw_walks <= kRwMaxVisits,
-            "rw_walks * rw_length must be <= 512 on the device");
-    plan->rw_length = rw_length;
-    plan->rw_restart = rw_restart;
-    plan->rw_walks = rw_walks;
-    plan->drop_graphs();
-  });
-}
-
-int cb_plan_meta_async(cb_plan* plan, void* host_dst, uint64_t* bytes) {
-  return guard([&] {
-    require(plan != nullptr, "null plan");
-    const uint64_t nb = sizeof(LayerMeta) * plan->P * (plan->L + 1);
-    if (bytes) *bytes = nb;
-    if (!host_dst) return;
-    DeviceGuard dg(plan->device);
-    CB_CUDA(cudaMemcpyAsync(host_dst, plan->meta, nb, cudaMemcpyDeviceToHost, plan->stream));
-  });
-}
-
-int cb_kernel_launches(uint64_t* n) {
-  return guard([&] {
-    require(n != nullptr, "null argument");
-    *n = g_kernel_launches.load();
-  });
-}
-
-int cb_plan_input_ids(cb_plan* plan, uint32_t part, const uint32_t** d_ids, uint64_t* n) {
-  return guard([&] {
-    require(plan != nullptr && d_ids != nullptr && n != nullptr, "null argument");
-    require_batch(plan, part, plan->L - 1);
-    DeviceGuard dg(plan->device);
-    check_overflow(plan);
-    *n = host_meta(plan, part, plan->L - 1).n_src;
-    *d_ids = plan->pe[part].L[plan->L - 1].src;
-  });
-}
-
-// ------------------------------------------------ multi-process peer exchange --
-// One part per rank (cb_plan_create_dist). Per layer l, with a cross-rank
-// barrier (the caller's: an NCCL all-reduce on cb_plan_stream, or a host
-// barrier) between the three calls:
-//   cb_px_layer(l)  : sample layer l, then OR every src id into its owner's
-//                     exchange bitmap over peer memory (build_exchange,
-//                     coop.cpp:35-51) -- no counts, no host sync
-//   cb_px_owner(l)  : the owner's sorted unique set S^{l+1}_q + word ranks
-//                     (coop.cpp:44-51), next layer's frontier
-//   cb_px_locate(l) : src_location from the owners' bitmaps (coop.cpp:53-62)
-// and cb_px_gather pulls the input rows from the owners' shards
-// (all_to_all_forward, coop.cpp:145-159). Everything is stream-ordered on the
-// plan stream.
-namespace {
-
-PxState& px_of(cb_plan* pl) {
-  require(pl->px != nullptr, "peer exchange not set up (cb_px_setup)");
-  return *pl->px;
-}
-
-}  // namespace
-
-int cb_px_setup(cb_plan* plan, const cb_partition* pm, uint32_t rank, void* handle_out) {
-  return guard([&] {
-    require(plan != nullptr && pm != nullptr && handle_out != nullptr, "null argument");
-    require(plan->dist_world > 0, "peer exchange needs a dist plan (cb_plan_create_dist)");
-    require(pm->parts == plan->dist_world, "partition part count != world size");
-    require(plan->dist_world <= static_cast<uint32_t>(kMaxParts), "peer exchange: world <= 16");
-    require(rank < plan->dist_world, "rank out of range");
-    DeviceGuard dg(plan->device);
-    auto px = std::make_unique<PxState>();
-    px->rank = rank;
-    px->world = plan->dist_world;
-    px->owner = pm->owner;
-    const uint64_t n = plan->g->g.n;
-    const uint64_t words = ceil_div(n, 32);
-    const uint64_t wp = ceil_div(std::max<uint64_t>(words, 1), kExtractTileWords) * kExtractTileWords;
-    const bool summ = wp > kExtractBigWords;
-    const uint64_t per = (2 * wp + (summ ? wp / 32 : 0)) * 4;
-    px->region_bytes = 2 * per;
-    CB_CUDA(cudaMalloc(&px->region, px->region_bytes));
-    CB_CUDA(cudaMemset(px->region, 0, px->region_bytes));
-    for (int s = 0; s < 2; ++s) {
-      uint32_t* base = reinterpret_cast<uint32_t*>(static_cast<char*>(px->region) + s * per);
-      Bitmap& b = px->slot[s];
-      b.words = words;
-      b.words_padded = wp;
-      b.bits = base;
-      b.wprefix = base + wp;
-      b.summ = summ ? base + 2 * wp : nullptr;
-      px->peers[s] = PxPeers{};
-      px->peers[s].bits[rank] = b.bits;
-      px->peers[s].summ[rank] = b.summ;
-      px->peers[s].pre[rank] = b.wprefix;
-    }
-    CB_CUDA(cudaMalloc(&px->send, plan->L * px->world * 8 + 8));
-    CB_CUDA(cudaMemset(px->send, 0, plan->L * px->world * 8 + 8));
-    CB_CUDA(cudaMalloc(&px->d_fbase, kMaxParts * sizeof(void*)));
-    px->fbase.assign(kMaxParts, nullptr);
-    px->slot_of.assign(plan->L, 0);
-    cudaIpcMemHandle_t h;
-    CB_CUDA(cudaIpcGetMemHandle(&h, px->region));
-    std::memcpy(handle_out, &h, sizeof(h));
-    plan->px = std::move(px);
-  });
-}
-
-int cb_px_connect(cb_plan* plan, uint32_t q, const void* handle) {
-  return guard([&] {
-    require(plan != nullptr && handle != nullptr, "null argument");
-    PxState& px = px_of(plan);
-    require(q < px.world && q != px.rank, "peer rank out of range (or self)");
-    DeviceGuard dg(plan->device);
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, handle, sizeof(h));
-    void* p = nullptr;
-    CB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-    px.opened.push_back(p);
-    const uint64_t per = px.region_bytes / 2;
-    for (int s = 0; s < 2; ++s) {
-      uint32_t* base = reinterpret_cast<uint32_t*>(static_cast<char*>(p) + s * per);
-      const uint64_t wp = px.slot[s].words_padded;
-      px.peers[s].bits[q] = base;
-      px.peers[s].pre[q] = base + wp;
-      px.peers[s].summ[q] = px.slot[s].summ ? base + 2 * wp : nullptr;
-    }
-  });
-}
-
-int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seeds,
-                const cb_sched* sched) {
-  NvtxRange nvtx_("cb.px_layer");
-  return guard([&] {
-    require(plan != nullptr && sched != nullptr, "null argument");
-    require(layer >= 0 && layer < plan->L, "layer index out of range");
-    require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
-    PxState& px = px_of(plan);
-    DeviceGuard dg(plan->device);
-    PeWork& w = plan->pe[0];
-    LayerBufs& b = w.L[layer];
-    cudaStream_t st = plan->stream;
-    uint32_t* D = (layer == 0) ? plan->seeds : b.dst;
-    const uint64_t cap = (layer == 0) ? plan->max_seeds : b.cap_dst;
-    if (layer == 0) {
-      require(seeds != nullptr || n_seeds == 0, "null seeds");
-      require(n_seeds <= plan->max_seeds, "more seeds than the plan's max_seeds_per_part");
-      if (n_seeds)
-        CB_CUDA(cudaMemcpyAsync(D, seeds, n_seeds * 4, cudaMemcpyDefault, st));
-      const Variates v = make_variates(sched);
-      CB_CUDA(cudaMemcpyAsync(plan->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
-      CB_CUDA(cudaMemsetAsync(px.send, 0, plan->L * px.world * 8, st));
-      plan->seeds_off.assign({0, n_seeds});
-      plan->mode = CB_MODE_COOP;
-    }
-    const bool smooth = sched->kappa != cbdev::kKappaInf && sched->kappa >= 2;
-    const int s = static_cast<int>(px.layer_ctr++ & 1);
-    px.slot_of[layer] = s;
-    launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);
-    const RelabelArgs none{};
-    enqueue_layer(plan, w, 0, layer, D, cap, layer == 0 ? n_seeds : ~0ULL, w.bm[0], none, 0,
-                  smooth,
-                  extract_args(w, w.bm[0], nullptr, b.src, b.cap_src,
-                               &plan->meta_at(0, layer)->n_src, nullptr, 3 * layer + 2,
-                               8 * layer + 4));
-    launch_relabel(relabel_args(w.bm[0], b, D, plan->meta_at(0, layer)),
-                   std::max(b.cap_edges, b.cap_dst), st);
-    launch_clear(w.bm[0], b.src, &plan->meta_at(0, layer)->n_src, st);
-    launch_px_route(b.src, &plan->meta_at(0, layer)->n_src, b.cap_src, px.owner, px.peers[s],
-                    px.send + static_cast<uint64_t>(layer) * px.world, st);
-    plan->have_batch = true;
-    plan->have_rows = false;
-    plan->dirty_mode = -1;
-  });
-}
-
-int cb_px_owner(cb_plan* plan, int layer) {
-  NvtxRange nvtx_("cb.px_owner");
-  return guard([&] {
-    require(plan != nullptr, "null plan");
-    require(layer >= 0 && layer < plan->L, "layer index out of range");
-    PxState& px = px_of(plan);
-    DeviceGuard dg(plan->device);
-    PeWork& w = plan->pe[0];
-    const int s = px.slot_of[layer];
-    uint32_t* next = (layer + 1 < plan->L) ? w.L[layer + 1].dst : w.owner_final;
-    const uint64_t cap = (layer + 1 < plan->L) ? w.L[layer + 1].cap_dst : w.cap_final;
-    // the other slot was last read by the previous layer's locates, which
-    // every rank finished before the barrier that precedes this call
-    launch_extract(extract_args(w, px.slot[s], &px.slot[s ^ 1], next, cap,
-                                &plan->meta_at(0, layer + 1)->n_dst, nullptr,
-                                3 * plan->L + layer, 8 * layer + 5),
-                   plan->stream);
-  });
-}
-
-int cb_px_locate(cb_plan* plan, int layer) {
-  NvtxRange nvtx_("cb.px_locate");
-  return guard([&] {
-    require(plan != nullptr, "null plan");
-    require(layer >= 0 && layer < plan->L, "layer index out of range");
-    PxState& px = px_of(plan);
-    DeviceGuard dg(plan->device);
-    PeWork& w = plan->pe[0];
-    LayerBufs& b = w.L[layer];
-    launch_px_locate(b.src, &plan->meta_at(0, layer)->n_src, b.cap_src, px.owner,
-                     px.peers[px.slot_of[layer]], w.loc_part[layer], w.loc_row[layer],
-                     plan->stream);
-  });
-}
-
-int cb_px_finish(cb_plan* plan) {
-  return guard([&] {
-    require(plan != nullptr, "null plan");
-    DeviceGuard dg(plan->device);
-    check_overflow(plan);
-  });
-}
-
-int cb_px_sizes(cb_plan* plan, int layer, uint64_t* n_src, uint64_t* n_owned) {
-  return guard([&] {
-    require(plan != nullptr, "null plan");
-    require(layer >= 0 && layer < plan->L, "layer index out of range");
-    DeviceGuard dg(plan->device);
-    CB_CUDA(cudaStreamSynchronize(plan->stream));
-    if (n_src) *n_src = host_meta(plan, 0, layer).n_src;
-    if (n_owned) *n_owned = host_meta(plan, 0, layer + 1).n_dst;
-  });
-}
-
-int cb_px_download(cb_plan* plan, int layer, uint64_t* send_row, uint32_t* loc_part,
-                   uint32_t* loc_row, uint32_t* owned) {
-  return guard([&] {
-    require(plan != nullptr, "null plan");
-    require(layer >= 0 && layer < plan->L, "layer index out of range");
-    PxState& px = px_of(plan);
-    DeviceGuard dg(plan->device);
-    check_overflow(plan);
-    PeWork& w = plan->pe[0];
-    const uint64_t n = host_meta(plan, 0, layer).n_src;
-    const uint64_t no = host_meta(plan, 0, layer + 1).n_dst;
-    if (send_row) {
-      std::vector<unsigned long long> h(px.world);
-      CB_CUDA(cudaMemcpy(h.data(), px.send + static_cast<uint64_t>(layer) * px.world,
-                         px.world * 8, cudaMemcpyDeviceToHost));
-      for (uint32_t q = 0; q < px.world; ++q) send_row[q] = h[q];
-    }
-    if (loc_part && n) CB_CUDA(cudaMemcpy(loc_part, w.loc_part[layer], n * 4, cudaMemcpyDeviceToHost));
-    if (loc_row && n) CB_CUDA(cudaMemcpy(loc_row, w.loc_row[layer], n * 4, cudaMemcpyDeviceToHost));
-    if (owned && no) {
-      const uint32_t* d = (layer + 1 < plan->L) ? w.L[layer + 1].dst : w.owner_final;
-      CB_CUDA(cudaMemcpy(owned, d, no * 4, cudaMemcpyDeviceToHost));
-    }
-  });
-}
-
-int cb_features_export(const cb_features* f, void* handle_out, uint64_t* shard_r0) {
-  return guard([&] {
-    require(f != nullptr && handle_out != nullptr, "null argument");
-    require(f->shard_rows > 0, "export needs a single-part shard table (cb_features_synth_shard)");
-    require(f->host_base == nullptr, "export of a host-tier table is not supported");
-    DeviceGuard dg(f->device);
-    void* base = static_cast<unsigned char*>(f->table) + f->shard_r0 * f->row_bytes;
-    cudaIpcMemHandle_t h;
-    CB_CUDA(cudaIpcGetMemHandle(&h, base));
-    std::memcpy(handle_out, &h, sizeof(h));
-    if (shard_r0) *shard_r0 = f->shard_r0;
-  });
-}
-
-int cb_px_connect_features(cb_plan* plan, uint32_t q, const void* handle, uint64_t shard_r0,
-                           const cb_features* local) {
-  return guard([&] {
-    require(plan != nullptr && local != nullptr, "null argument");
-    PxState& px = px_of(plan);
-    require(q < px.world, "peer rank out of range");
-    DeviceGuard dg(plan->device);
-    px.frow_bytes = local->row_bytes;
-    if (q == px.rank) {
-      px.fbase[q] = static_cast<const unsigned char*>(local->table);
-    } else {
-      require(handle != nullptr, "null handle");
-      cudaIpcMemHandle_t h;
-      std::memcpy(&h, handle, sizeof(h));
-      void* p = nullptr;
-      CB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-      px.fopened.push_back(p);
-      px.fbase[q] = static_cast<const unsigned char*>(p) - shard_r0 * local->row_bytes;
-    }
-    CB_CUDA(cudaMemcpy(px.d_fbase, px.fbase.data(), kMaxParts * sizeof(void*),
-                       cudaMemcpyHostToDevice));
-  });
-}
-
-int cb_px_gather(cb_plan* plan, const cb_features* local) {
-  NvtxRange nvtx_("cb.px_gather");
-  return guard([&] {
-    require(plan != nullptr && local != nullptr, "null argument");
-    require(plan->have_batch, "no sampled batch in this plan");
-    PxState& px = px_of(plan);
-    for (uint32_t q = 0; q < px.world; ++q)
-      require(px.fbase[q] != nullptr, "feature shard of a rank not connected");
-    DeviceGuard dg(plan->device);
-    prepare_rows(plan, local);
-    PeWork& w = plan->pe[0];
-    const int L = plan->L;
-    launch_px_gather(px.d_fbase, px.owner, local->row_map, local->row_bytes, w.L[L - 1].src,
-                     &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, plan->stream);
-    plan->have_rows = true;
-  });
-}
-
-}  // extern "C"
-
-// ------------------------------------------------- GCN training step (f1) --
-// GcnModel (coop.hpp:105-135) on the device and coop_train_step /
-// indep_train_step (coop.cpp:438-610) over the plan's last batch: the
-// forward pass mean-aggregates each block's sampled in-neighbours, applies
-// W and tanh (identity at block 0), moves hidden rows to the requesters with
-// the batch's exchange records (all_to_all_forward), takes the softmax
-// cross-entropy of the seeds, and runs the backward pass with the owner-side
-// gradient sums (all_to_all_reverse_sum). FP64 in the reference's
-// accumulation order (train.cu).
-struct cb_model {
-  int device = 0;
-  int L = 0;
-  bool tanh_hidden = true;
-  std::vector<uint32_t> rows, cols;
-  std::vector<double*> w;
-  ~cb_model() {
-    for (double* p : w) if (p) cudaFree(p);
-  }
-};
-
-namespace {
-
-struct TmpArena {
-  std::vector<void*> ptrs;
-  template <typename T>
-  T* get(uint64_t n) {
-    void* p = nullptr;
-    CB_CUDA(cudaMalloc(&p, std::max<uint64_t>(n, 1) * sizeof(T) + 16));
-    ptrs.push_back(p);
-    return static_cast<T*>(p);
-  }
-  ~TmpArena() {
-    for (void* p : ptrs) cudaFree(p);
-  }
-};
-
-struct U32ToU64 {
-  __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
-};
-
-// out[0..n] = exclusive prefix of the u32 counts (out[n] = total)
-void scan_counts(const uint32_t* cnt, uint64_t n, uint64_t* out, TmpArena& A, cudaStream_t st) {
-  auto it = thrust::make_transform_iterator(cnt, U32ToU64{});
-  size_t bytes = 0;
-  CB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, out, static_cast<int64_t>(n + 1), st));
-  void* tmp = A.get<unsigned char>(bytes);
-  CB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, it, out, static_cast<int64_t>(n + 1), st));
-}
-
-__global__ void src_hist_kernel(const uint2* __restrict__ edges, uint64_t n, uint32_t* cnt,
-                                uint32_t* key, uint32_t* val) {
-  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < n;
-       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    atomicAdd(&cnt[edges[e].x], 1u);
-    key[e] = edges[e].x;
-    val[e] = static_cast<uint32_t>(e);
-  }
-}
-
-__global__ void owner_key_kernel(const uint32_t* __restrict__ part, const uint32_t* __restrict__ row,
-                                 uint64_t n, const uint64_t* __restrict__ owner_base,
-                                 uint64_t g0, uint32_t* cnt, uint64_t* key, uint64_t* val) {
-  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
-       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t k = owner_base[part[j]] + row[j];
-    atomicAdd(&cnt[k], 1u);
-    key[g0 + j] = k;
-    val[g0 + j] = g0 + j;
-  }
-}
-
-int grid_of_n(uint64_t n) {
-  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 16)));
-}
-
-}  // namespace
-
-extern "C" {
-
-int cb_gcn_model_init(int device, uint32_t in_dim, uint32_t hidden, uint32_t classes,
-                      int num_layers, uint64_t seed, cb_model** out) {
-  return guard([&] {
-    require(out != nullptr, "null argument");
-    require(num_layers >= 1, "GcnModel: num_layers must be >= 1");
-    require(in_dim >= 1 && hidden >= 1 && classes >= 1, "GcnModel: dims must be >= 1");
-    DeviceGuard dg(device);
-    auto m = std::make_unique<cb_model>();
-    m->device = device;
-    m->L = num_layers;
-    for (int l = 0; l < num_layers; ++l) {
-      // GcnModel::init (coop.cpp:334-357): weights[l] is used at block l
-      const uint32_t rows = (l == num_layers - 1) ? in_dim : hidden;
-      const uint32_t cols = (l == 0) ? classes : hidden;
-      std::vector<double> w(static_cast<uint64_t>(rows) * cols);
-      const double scale = 1.0 / std::sqrt(static_cast<double>(rows));
-      const uint64_t pfx = cbdev::hstep(cbdev::hstep(cbdev::hinit(seed), 11ULL),
-                                        static_cast<uint64_t>(l));
-      for (uint64_t i = 0; i < rows; ++i)
-        for (uint64_t j = 0; j < cols; ++j) {
-          const double u = cbdev::ufb(cbdev::hstep(cbdev::hstep(pfx, i), j));
-          volatile double t = 2.0 * u;  // no contraction: (2u - 1) * scale as two roundings
-          w[i * cols + j] = (t - 1.0) * scale;
-        }
-      double* d = nullptr;
-      CB_CUDA(cudaMalloc(&d, w.size() * 8));
-      CB_CUDA(cudaMemcpy(d, w.data(), w.size() * 8, cudaMemcpyHostToDevice));
-      m->rows.push_back(rows);
-      m->cols.push_back(cols);
-      m->w.push_back(d);
-    }
-    *out = m.release();
-  });
-}
-
-int cb_gcn_model_weights(cb_model* m, int layer, double* host, int upload, uint64_t* rows,
-                         uint64_t* cols) {
-  return guard([&] {
-    require(m != nullptr, "null model");
-    require(layer >= 0 && layer < m->L, "layer index out of range");
-    DeviceGuard dg(m->device);
-    const uint64_t n = static_cast<uint64_t>(m->rows[layer]) * m->cols[layer];
-    if (rows) *rows = m->rows[layer];
-    if (cols) *cols = m->cols[layer];
-    if (!host) return;
-    if (upload) CB_CUDA(cudaMemcpy(m->w[layer], host, n * 8, cudaMemcpyHostToDevice));
-    else CB_CUDA(cudaMemcpy(host, m->w[layer], n * 8, cudaMemcpyDeviceToHost));
-  });
-}
-
-void cb_gcn_model_destroy(cb_model* m) {
-  if (!m) return;
-  int prev = 0;
-  cudaGetDevice(&prev);
-  cudaSetDevice(m->device);
-  delete m;
-  cudaSetDevice(prev);
-}
-
-int cb_train_step(cb_plan* pl, const cb_features* f, uint32_t classes, cb_model* m,
-                  double* loss_out, double* grad_w_out) {
-  NvtxRange nvtx_("cb.train_step");
-  return guard([&] {
-    require(pl != nullptr && f != nullptr && m != nullptr && loss_out != nullptr,
-            "null argument");
-    require(pl->have_batch, "no sampled batch in this plan");
-    require(f->dtype == CB_F64, "train step: the feature table must be f64 (FeatureStore)");
-    require(m->L == pl->L, "train step: model depth does not match layer count");
-    require(m->rows[pl->L - 1] == f->dim, "train step: model input dim does not match store");
-    require(classes >= 1 && m->cols[0] == classes, "train step: class count mismatch");
-    DeviceGuard dg(pl->device);
-    check_overflow(pl);
-    const uint32_t P = pl->P;
-    const int L = pl->L;
-    const bool coop = pl->coop_active();
-    cudaStream_t st = pl->stream;
-    TmpArena A;
-    // counts of the batch (one host read)
-    std::vector<std::vector<LayerMeta>> M(P, std::vector<LayerMeta>(L + 1));
-    for (uint32_t p = 0; p < P; ++p)
-      CB_CUDA(cudaMemcpy(M[p].data(), pl->meta_at(p, 0), sizeof(LayerMeta) * (L + 1),
-                         cudaMemcpyDeviceToHost));
-    uint64_t total_seeds = 0;
-    for (uint32_t p = 0; p < P; ++p) total_seeds += M[p][0].n_dst;
-    require(total_seeds > 0, coop ? "coop_train_step: no seeds" : "indep_train_step: no seeds");
-    auto dst_of = [&](uint32_t p, int l) -> const uint32_t* {
-      if (l == 0) return pl->seeds + pl->seeds_off[p];
-      return pl->own_dst() ? pl->pe[p].L[l].dst : pl->pe[p].L[l - 1].src;
-    };
-    // input rows of every part, requester-aligned (load_rows + all_to_all_forward)
-    prepare_rows(pl, f);
-    enqueue_gather(pl, f);
-    std::vector<std::vector<double*>> hin(L, std::vector<double*>(P)), agg(L, std::vector<double*>(P)),
-        out(L, std::vector<double*>(P));
-    std::vector<std::vector<uint32_t*>> deg(L, std::vector<uint32_t*>(P));
-    for (int l = L - 1; l >= 0; --l) {
-      const uint32_t din = m->rows[l], dout = m->cols[l];
-      const bool act = (l > 0) && m->tanh_hidden;
-      for (uint32_t p = 0; p < P; ++p) {
-        const LayerBufs& b = pl->pe[p].L[l];
-        const uint64_t nd = M[p][l].n_dst, ne = M[p][l].n_edges;
-        if (l == L - 1) hin[l][p] = static_cast<double*>(pl->pe[p].rows);
-        else if (!coop) hin[l][p] = out[l + 1][p];
-        deg[l][p] = A.get<uint32_t>(nd);
-        CB_CUDA(cudaMemsetAsync(deg[l][p], 0, std::max<uint64_t>(nd, 1) * 4, st));
-        launch_in_degrees(b.edges, ne, deg[l][p], st);
-        uint64_t* off = A.get<uint64_t>(nd + 1);
-        scan_counts(deg[l][p], nd, off, A, st);
-        agg[l][p] = A.get<double>(nd * din);
-        launch_aggregate(b.edges, deg[l][p], off, b.dst_pos, nd, hin[l][p], din, agg[l][p], st);
-        out[l][p] = A.get<double>(nd * dout);
-        launch_dense(agg[l][p], nd, din, m->w[l], dout, act, out[l][p], st);
-      }
-      if (coop && l > 0) {  // all_to_all_forward of block l's outputs to block l-1's sources
-        const double** owners = A.get<const double*>(P);
-        std::vector<const double*> h(out[l].begin(), out[l].end());
-        CB_CUDA(cudaMemcpyAsync(owners, h.data(), P * sizeof(void*), cudaMemcpyHostToDevice, st));
-        CB_CUDA(cudaStreamSynchronize(st));
-        for (uint32_t p = 0; p < P; ++p) {
-          const uint64_t ns = M[p][l - 1].n_src;
-          hin[l - 1][p] = A.get<double>(ns * dout);
-          launch_row_forward(owners, pl->pe[p].loc_part[l - 1], pl->pe[p].loc_row[l - 1], ns,
-                             dout, hin[l - 1][p], st);
-        }
-      }
-    }
-    // loss on the seeds, gradient rows scaled by the global mean
-    const double scale = 1.0 / static_cast<double>(total_seeds);
-    const uint32_t C = classes;
-    std::vector<std::vector<double*>> grad(L + 1, std::vector<double*>(P, nullptr));
-    double loss_sum = 0.0;
-    for (uint32_t p = 0; p < P; ++p) {
-      const uint64_t n0 = M[p][0].n_dst;
-      double* rl = A.get<double>(n0);
-      grad[0][p] = A.get<double>(n0 * C);
-      launch_softmax_ce(out[0][p], n0, C, dst_of(p, 0), f->seed, scale, rl, grad[0][p], st);
-      std::vector<double> h(n0);
-      if (n0) CB_CUDA(cudaMemcpyAsync(h.data(), rl, n0 * 8, cudaMemcpyDeviceToHost, st));
-      CB_CUDA(cudaStreamSynchronize(st));
-      for (double x : h) loss_sum += x;
-    }
-    *loss_out = loss_sum * scale;
-    // backward with owner-side gradient accumulation between layers
-    uint64_t gw_off = 0;
-    for (int l = 0; l < L; ++l) {
-      const uint32_t din = m->rows[l], dout = m->cols[l];
-      const bool act = (l > 0) && m->tanh_hidden;
-      const uint64_t nw = static_cast<uint64_t>(din) * dout;
-      double* gw = A.get<double>(nw);
-      CB_CUDA(cudaMemsetAsync(gw, 0, nw * 8, st));
-      double* gwp = A.get<double>(nw);
-      uint64_t req_total = 0;
-      std::vector<uint64_t> req_off(P + 1, 0);
-      for (uint32_t p = 0; p < P; ++p) req_off[p + 1] = req_off[p] + M[p][l].n_src;
-      req_total = req_off[P];
-      double* gh_all = A.get<double>(req_total * din);
-      for (uint32_t p = 0; p < P; ++p) {
-        const LayerBufs& b = pl->pe[p].L[l];
-        const uint64_t nd = M[p][l].n_dst, ne = M[p][l].n_edges, ns = M[p][l].n_src;
-        double* dp = grad[l][p];
-        if (act) launch_tanh_grad(out[l][p], nd * dout, dp, st);
-        launch_grad_w(agg[l][p], dp, nd, din, dout, gwp, st);
-        launch_add(gw, gwp, nw, st);  // parts in order (the simulated all-reduce)
-        double* dagg = A.get<double>(nd * din);
-        launch_grad_agg(dp, m->w[l], nd, din, dout, dagg, st);
-        // sources' edges in edge order (stable CSC) + the isolated dst of each source
-        uint32_t* cnt = A.get<uint32_t>(ns);
-        CB_CUDA(cudaMemsetAsync(cnt, 0, std::max<uint64_t>(ns, 1) * 4, st));
-        uint32_t* key = A.get<uint32_t>(ne);
-        uint32_t* val = A.get<uint32_t>(ne);
-        uint32_t* key2 = A.get<uint32_t>(ne);
-        uint32_t* val2 = A.get<uint32_t>(ne);
-        if (ne) src_hist_kernel<<<grid_of_n(ne), 256, 0, st>>>(b.edges, ne, cnt, key, val);
-        CB_LAUNCH("src_hist");
-        uint64_t* soff = A.get<uint64_t>(ns + 1);
-        scan_counts(cnt, ns, soff, A, st);
-        cub::DoubleBuffer<uint32_t> kb(key, key2), vb(val, val2);
-        size_t bytes = 0;
-        CB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, static_cast<int64_t>(ne), 0,
-                                                32, st));
-        void* tmp = A.get<unsigned char>(bytes);
-        CB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int64_t>(ne), 0, 32,
-                                                st));
-        int64_t* iso = A.get<int64_t>(ns);
-        CB_CUDA(cudaMemsetAsync(iso, 0xff, std::max<uint64_t>(ns, 1) * 8, st));
-        launch_iso_dst(deg[l][p], b.dst_pos, nd, iso, st);
-        launch_grad_h_in(b.edges, vb.Current(), soff, deg[l][p], iso, ns, dagg, din,
-                         gh_all + req_off[p] * din, st);
-      }
-      if (grad_w_out)
-        CB_CUDA(cudaMemcpyAsync(grad_w_out + gw_off, gw, nw * 8, cudaMemcpyDeviceToHost, st));
-      gw_off += nw;
-      if (l + 1 < L) {
-        if (!coop) {
-          for (uint32_t p = 0; p < P; ++p) grad[l + 1][p] = gh_all + req_off[p] * din;
-        } else {  // all_to_all_reverse_sum over the exchange of layer l
-          std::vector<uint64_t> obase(P + 1, 0);
-          for (uint32_t q = 0; q < P; ++q) obase[q + 1] = obase[q] + M[q][l + 1].n_dst;
-          const uint64_t no = obase[P];
-          uint64_t* d_obase = A.get<uint64_t>(P + 1);
-          CB_CUDA(cudaMemcpyAsync(d_obase, obase.data(), (P + 1) * 8, cudaMemcpyHostToDevice, st));
-          uint32_t* cnt = A.get<uint32_t>(no);
-          CB_CUDA(cudaMemsetAsync(cnt, 0, std::max<uint64_t>(no, 1) * 4, st));
-          uint64_t* key = A.get<uint64_t>(req_total);
-          uint64_t* val = A.get<uint64_t>(req_total);
-          uint64_t* key2 = A.get<uint64_t>(req_total);
-          uint64_t* val2 = A.get<uint64_t>(req_total);
-          for (uint32_t p = 0; p < P; ++p) {
-            const uint64_t ns = M[p][l].n_src;
-            if (ns)
-              owner_key_kernel<<<grid_of_n(ns), 256, 0, st>>>(
-                  pl->pe[p].loc_part[l], pl->pe[p].loc_row[l], ns, d_obase, req_off[p], cnt, key,
-                  val);
-            CB_LAUNCH("owner_key");
-          }
-          uint64_t* ooff = A.get<uint64_t>(no + 1);
-          scan_counts(cnt, no, ooff, A, st);
-          cub::DoubleBuffer<uint64_t> kb(key, key2), vb(val, val2);
-          size_t bytes = 0;
-          CB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb,
-                                                  static_cast<int64_t>(req_total), 0, 64, st));
-          void* tmp = A.get<unsigned char>(bytes);
-          CB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb,
-                                                  static_cast<int64_t>(req_total), 0, 64, st));
-          double* oall = A.get<double>(no * din);
-          launch_reverse_sum(ooff, vb.Current(), no, gh_all, din, oall, st);
-          for (uint32_t q = 0; q < P; ++q) grad[l + 1][q] = oall + obase[q] * din;
-        }
-      }
-    }
-    CB_CUDA(cudaStreamSynchronize(st));
   });
 }
 

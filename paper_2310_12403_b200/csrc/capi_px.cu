@@ -1,0 +1,277 @@
+// C-ABI: multi-process peer exchange (cb_px_*), one part per rank over CUDA IPC.
+#include "capi_internal.h"
+
+extern "C" {
+
+// ------------------------------------------------ multi-process peer exchange --
+// One part per rank (cb_plan_create_dist). Per layer l, with a cross-rank
+// barrier (the caller's: an NCCL all-reduce on cb_plan_stream, or a host
+// barrier) between the three calls:
+//   cb_px_layer(l)  : sample layer l, then OR every src id into its owner's
+//                     exchange bitmap over peer memory (build_exchange,
+//                     coop.cpp:35-51) -- no counts, no host sync
+//   cb_px_owner(l)  : the owner's sorted unique set S^{l+1}_q + word ranks
+//                     (coop.cpp:44-51), next layer's frontier
+//   cb_px_locate(l) : src_location from the owners' bitmaps (coop.cpp:53-62)
+// and cb_px_gather pulls the input rows from the owners' shards
+// (all_to_all_forward, coop.cpp:145-159). Everything is stream-ordered on the
+// plan stream.
+namespace {
+
+PxState& px_of(cb_plan* pl) {
+  require(pl->px != nullptr, "peer exchange not set up (cb_px_setup)");
+  return *pl->px;
+}
+
+}  // namespace
+
+int cb_px_setup(cb_plan* plan, const cb_partition* pm, uint32_t rank, void* handle_out) {
+  return guard([&] {
+    require(plan != nullptr && pm != nullptr && handle_out != nullptr, "null argument");
+    require(plan->dist_world > 0, "peer exchange needs a dist plan (cb_plan_create_dist)");
+    require(pm->parts == plan->dist_world, "partition part count != world size");
+    require(plan->dist_world <= static_cast<uint32_t>(kMaxParts), "peer exchange: world <= 16");
+    require(rank < plan->dist_world, "rank out of range");
+    DeviceGuard dg(plan->device);
+    auto px = std::make_unique<PxState>();
+    px->rank = rank;
+    px->world = plan->dist_world;
+    px->owner = pm->owner;
+    const uint64_t n = plan->g->g.n;
+    const uint64_t words = ceil_div(n, 32);
+    const uint64_t wp = ceil_div(std::max<uint64_t>(words, 1), kExtractTileWords) * kExtractTileWords;
+    const bool summ = wp > kExtractBigWords;
+    const uint64_t per = (2 * wp + (summ ? wp / 32 : 0)) * 4;
+    px->region_bytes = 2 * per;
+    CB_CUDA(cudaMalloc(&px->region, px->region_bytes));
+    CB_CUDA(cudaMemset(px->region, 0, px->region_bytes));
+    for (int s = 0; s < 2; ++s) {
+      uint32_t* base = reinterpret_cast<uint32_t*>(static_cast<char*>(px->region) + s * per);
+      Bitmap& b = px->slot[s];
+      b.words = words;
+      b.words_padded = wp;
+      b.bits = base;
+      b.wprefix = base + wp;
+      b.summ = summ ? base + 2 * wp : nullptr;
+      px->peers[s] = PxPeers{};
+      px->peers[s].bits[rank] = b.bits;
+      px->peers[s].summ[rank] = b.summ;
+      px->peers[s].pre[rank] = b.wprefix;
+    }
+    CB_CUDA(cudaMalloc(&px->send, plan->L * px->world * 8 + 8));
+    CB_CUDA(cudaMemset(px->send, 0, plan->L * px->world * 8 + 8));
+    CB_CUDA(cudaMalloc(&px->d_fbase, kMaxParts * sizeof(void*)));
+    px->fbase.assign(kMaxParts, nullptr);
+    px->slot_of.assign(plan->L, 0);
+    cudaIpcMemHandle_t h;
+    CB_CUDA(cudaIpcGetMemHandle(&h, px->region));
+    std::memcpy(handle_out, &h, sizeof(h));
+    plan->px = std::move(px);
+  });
+}
+
+int cb_px_connect(cb_plan* plan, uint32_t q, const void* handle) {
+  return guard([&] {
+    require(plan != nullptr && handle != nullptr, "null argument");
+    PxState& px = px_of(plan);
+    require(q < px.world && q != px.rank, "peer rank out of range (or self)");
+    DeviceGuard dg(plan->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    CB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    px.opened.push_back(p);
+    const uint64_t per = px.region_bytes / 2;
+    for (int s = 0; s < 2; ++s) {
+      uint32_t* base = reinterpret_cast<uint32_t*>(static_cast<char*>(p) + s * per);
+      const uint64_t wp = px.slot[s].words_padded;
+      px.peers[s].bits[q] = base;
+      px.peers[s].pre[q] = base + wp;
+      px.peers[s].summ[q] = px.slot[s].summ ? base + 2 * wp : nullptr;
+    }
+  });
+}
+
+int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seeds,
+                const cb_sched* sched) {
+  NvtxRange nvtx_("cb.px_layer");
+  return guard([&] {
+    require(plan != nullptr && sched != nullptr, "null argument");
+    require(layer >= 0 && layer < plan->L, "layer index out of range");
+    require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
+    PxState& px = px_of(plan);
+    DeviceGuard dg(plan->device);
+    PeWork& w = plan->pe[0];
+    LayerBufs& b = w.L[layer];
+    cudaStream_t st = plan->stream;
+    uint32_t* D = (layer == 0) ? plan->seeds : b.dst;
+    const uint64_t cap = (layer == 0) ? plan->max_seeds : b.cap_dst;
+    if (layer == 0) {
+      require(seeds != nullptr || n_seeds == 0, "null seeds");
+      require(n_seeds <= plan->max_seeds, "more seeds than the plan's max_seeds_per_part");
+      if (n_seeds)
+        CB_CUDA(cudaMemcpyAsync(D, seeds, n_seeds * 4, cudaMemcpyDefault, st));
+      const Variates v = make_variates(sched);
+      CB_CUDA(cudaMemcpyAsync(plan->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+      CB_CUDA(cudaMemsetAsync(px.send, 0, plan->L * px.world * 8, st));
+      plan->seeds_off.assign({0, n_seeds});
+      plan->mode = CB_MODE_COOP;
+    }
+    const bool smooth = sched->kappa != cbdev::kKappaInf && sched->kappa >= 2;
+    const int s = static_cast<int>(px.layer_ctr++ & 1);
+    px.slot_of[layer] = s;
+    launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);
+    const RelabelArgs none{};
+    enqueue_layer(plan, w, 0, layer, D, cap, layer == 0 ? n_seeds : ~0ULL, w.bm[0], none, 0,
+                  smooth,
+                  extract_args(w, w.bm[0], nullptr, b.src, b.cap_src,
+                               &plan->meta_at(0, layer)->n_src, nullptr, 3 * layer + 2,
+                               8 * layer + 4));
+    launch_relabel(relabel_args(w.bm[0], b, D, plan->meta_at(0, layer)),
+                   std::max(b.cap_edges, b.cap_dst), st);
+    launch_clear(w.bm[0], b.src, &plan->meta_at(0, layer)->n_src, st);
+    launch_px_route(b.src, &plan->meta_at(0, layer)->n_src, b.cap_src, px.owner, px.peers[s],
+                    px.send + static_cast<uint64_t>(layer) * px.world, st);
+    plan->have_batch = true;
+    plan->have_rows = false;
+    plan->dirty_mode = -1;
+  });
+}
+
+int cb_px_owner(cb_plan* plan, int layer) {
+  NvtxRange nvtx_("cb.px_owner");
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require(layer >= 0 && layer < plan->L, "layer index out of range");
+    PxState& px = px_of(plan);
+    DeviceGuard dg(plan->device);
+    PeWork& w = plan->pe[0];
+    const int s = px.slot_of[layer];
+    uint32_t* next = (layer + 1 < plan->L) ? w.L[layer + 1].dst : w.owner_final;
+    const uint64_t cap = (layer + 1 < plan->L) ? w.L[layer + 1].cap_dst : w.cap_final;
+    // the other slot was last read by the previous layer's locates, which
+    // every rank finished before the barrier that precedes this call
+    launch_extract(extract_args(w, px.slot[s], &px.slot[s ^ 1], next, cap,
+                                &plan->meta_at(0, layer + 1)->n_dst, nullptr,
+                                3 * plan->L + layer, 8 * layer + 5),
+                   plan->stream);
+  });
+}
+
+int cb_px_locate(cb_plan* plan, int layer) {
+  NvtxRange nvtx_("cb.px_locate");
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require(layer >= 0 && layer < plan->L, "layer index out of range");
+    PxState& px = px_of(plan);
+    DeviceGuard dg(plan->device);
+    PeWork& w = plan->pe[0];
+    LayerBufs& b = w.L[layer];
+    launch_px_locate(b.src, &plan->meta_at(0, layer)->n_src, b.cap_src, px.owner,
+                     px.peers[px.slot_of[layer]], w.loc_part[layer], w.loc_row[layer],
+                     plan->stream);
+  });
+}
+
+int cb_px_finish(cb_plan* plan) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    DeviceGuard dg(plan->device);
+    check_overflow(plan);
+  });
+}
+
+int cb_px_sizes(cb_plan* plan, int layer, uint64_t* n_src, uint64_t* n_owned) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require(layer >= 0 && layer < plan->L, "layer index out of range");
+    DeviceGuard dg(plan->device);
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    if (n_src) *n_src = host_meta(plan, 0, layer).n_src;
+    if (n_owned) *n_owned = host_meta(plan, 0, layer + 1).n_dst;
+  });
+}
+
+int cb_px_download(cb_plan* plan, int layer, uint64_t* send_row, uint32_t* loc_part,
+                   uint32_t* loc_row, uint32_t* owned) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require(layer >= 0 && layer < plan->L, "layer index out of range");
+    PxState& px = px_of(plan);
+    DeviceGuard dg(plan->device);
+    check_overflow(plan);
+    PeWork& w = plan->pe[0];
+    const uint64_t n = host_meta(plan, 0, layer).n_src;
+    const uint64_t no = host_meta(plan, 0, layer + 1).n_dst;
+    if (send_row) {
+      std::vector<unsigned long long> h(px.world);
+      CB_CUDA(cudaMemcpy(h.data(), px.send + static_cast<uint64_t>(layer) * px.world,
+                         px.world * 8, cudaMemcpyDeviceToHost));
+      for (uint32_t q = 0; q < px.world; ++q) send_row[q] = h[q];
+    }
+    if (loc_part && n) CB_CUDA(cudaMemcpy(loc_part, w.loc_part[layer], n * 4, cudaMemcpyDeviceToHost));
+    if (loc_row && n) CB_CUDA(cudaMemcpy(loc_row, w.loc_row[layer], n * 4, cudaMemcpyDeviceToHost));
+    if (owned && no) {
+      const uint32_t* d = (layer + 1 < plan->L) ? w.L[layer + 1].dst : w.owner_final;
+      CB_CUDA(cudaMemcpy(owned, d, no * 4, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int cb_features_export(const cb_features* f, void* handle_out, uint64_t* shard_r0) {
+  return guard([&] {
+    require(f != nullptr && handle_out != nullptr, "null argument");
+    require(f->shard_rows > 0, "export needs a single-part shard table (cb_features_synth_shard)");
+    require(f->host_base == nullptr, "export of a host-tier table is not supported");
+    DeviceGuard dg(f->device);
+    void* base = static_cast<unsigned char*>(f->table) + f->shard_r0 * f->row_bytes;
+    cudaIpcMemHandle_t h;
+    CB_CUDA(cudaIpcGetMemHandle(&h, base));
+    std::memcpy(handle_out, &h, sizeof(h));
+    if (shard_r0) *shard_r0 = f->shard_r0;
+  });
+}
+
+int cb_px_connect_features(cb_plan* plan, uint32_t q, const void* handle, uint64_t shard_r0,
+                           const cb_features* local) {
+  return guard([&] {
+    require(plan != nullptr && local != nullptr, "null argument");
+    PxState& px = px_of(plan);
+    require(q < px.world, "peer rank out of range");
+    DeviceGuard dg(plan->device);
+    px.frow_bytes = local->row_bytes;
+    if (q == px.rank) {
+      px.fbase[q] = static_cast<const unsigned char*>(local->table);
+    } else {
+      require(handle != nullptr, "null handle");
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handle, sizeof(h));
+      void* p = nullptr;
+      CB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      px.fopened.push_back(p);
+      px.fbase[q] = static_cast<const unsigned char*>(p) - shard_r0 * local->row_bytes;
+    }
+    CB_CUDA(cudaMemcpy(px.d_fbase, px.fbase.data(), kMaxParts * sizeof(void*),
+                       cudaMemcpyHostToDevice));
+  });
+}
+
+int cb_px_gather(cb_plan* plan, const cb_features* local) {
+  NvtxRange nvtx_("cb.px_gather");
+  return guard([&] {
+    require(plan != nullptr && local != nullptr, "null argument");
+    require(plan->have_batch, "no sampled batch in this plan");
+    PxState& px = px_of(plan);
+    for (uint32_t q = 0; q < px.world; ++q)
+      require(px.fbase[q] != nullptr, "feature shard of a rank not connected");
+    DeviceGuard dg(plan->device);
+    prepare_rows(plan, local);
+    PeWork& w = plan->pe[0];
+    const int L = plan->L;
+    launch_px_gather(px.d_fbase, px.owner, local->row_map, local->row_bytes, w.L[L - 1].src,
+                     &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, plan->stream);
+    plan->have_rows = true;
+  });
+}
+
+}  // extern "C"
