@@ -121,10 +121,33 @@ void plan_alloc(cb_plan* pl) {
   // buffer (the largest scan space) serves all of them
   uint64_t stage_tiles = 0;
   for (const PeWork& w : pl->pe) stage_tiles = std::max(stage_tiles, w.sync.max_tiles);
-  uint2* stage = pl->mem.alloc<uint2>(stage_tiles * kLaborTile + 32);
-  for (PeWork& w : pl->pe) w.sync.stage = stage;
-  // smoothed LABOR variate table (shared by the parts like the stage)
-  pl->vtab = (pl->kind == CB_LABOR0 && n <= kVtabMaxVerts) ? pl->mem.alloc<double>(n) : nullptr;
+  const bool tab = pl->kind == CB_LABOR0 && n <= kVtabMaxVerts;
+  // parts run concurrently (own stage + variate table each) when that fits a
+  // modest budget; otherwise one after another on the plan stream, sharing them
+  const uint64_t per_part = stage_tiles * kLaborTile * 8 + (tab ? n * 8 : 0);
+  pl->part_concurrent = P > 1 && sat_mul(per_part, P) <= (8ULL << 30);
+  if (pl->part_concurrent && pl->part_st.size() != P) {
+    for (uint32_t p = 0; p < P; ++p) {
+      cudaStream_t s;
+      cudaEvent_t e;
+      CB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      CB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      pl->part_st.push_back(s);
+      pl->ev_join.push_back(e);
+    }
+    CB_CUDA(cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming));
+  }
+  uint2* stage = nullptr;
+  double* vt = nullptr;
+  for (PeWork& w : pl->pe) {
+    if (!stage || pl->part_concurrent) {
+      stage = pl->mem.alloc<uint2>(stage_tiles * kLaborTile + 32);
+      vt = tab ? pl->mem.alloc<double>(n) : nullptr;
+    }
+    w.sync.stage = stage;
+    w.sync.vtab = vt;
+  }
+  pl->vtab = vt;
   pl->meta = pl->mem.alloc<LayerMeta>(static_cast<uint64_t>(P) * (L + 1));
   CB_CUDA(cudaMemset(pl->meta, 0, sizeof(LayerMeta) * P * (L + 1)));
   pl->send_counts = pl->mem.alloc<unsigned long long>(static_cast<uint64_t>(L) * P * P);
@@ -335,7 +358,7 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
   la.slots = b.slots;
   la.keep_words = w.sync.keep_words;
   la.stage = w.sync.stage;
-  la.vtab = pl->vtab;
+  la.vtab = w.sync.vtab;
   la.n_vert = pl->g->g.n;
   la.cap_edges = b.cap_edges;
   la.ticket = w.sync.tickets + 3 * l + 1;
@@ -352,11 +375,11 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
 uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* D,
                        uint64_t cap_dst, uint64_t n_dst_param, Bitmap& set_bm,
                        const RelabelArgs& fused, uint64_t fused_work, bool smooth,
-                       const ExtractArgs& ex) {
+                       const ExtractArgs& ex, cudaStream_t stream) {
   NvtxRange nvtx_("cb.layer");
   const DeviceGraph& g = pl->g->g;
   const LayerBufs& b = w.L[l];
-  cudaStream_t st = pl->stream;
+  cudaStream_t st = stream ? stream : pl->stream;
   launch_frontier(frontier_args(pl, w, p, l, D, n_dst_param, set_bm), fused, cap_dst,
                   fused_work, st);
   prof_mark(pl);
@@ -440,7 +463,24 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
     prof_mark(pl);
   }
 
+  // parts on their own streams (fork after the batch_begin launches, join
+  // before anything that reads another part's results)
+  const bool conc = pl->part_concurrent && !pl->prof && P > 1;
+  auto pst = [&](uint32_t p) { return conc ? pl->part_st[p] : st; };
+  auto fork = [&]() {
+    if (!conc) return;
+    CB_CUDA(cudaEventRecord(pl->ev_fork, st));
+    for (uint32_t p = 0; p < P; ++p) CB_CUDA(cudaStreamWaitEvent(pl->part_st[p], pl->ev_fork, 0));
+  };
+  auto join = [&]() {
+    if (!conc) return;
+    for (uint32_t p = 0; p < P; ++p) {
+      CB_CUDA(cudaEventRecord(pl->ev_join[p], pl->part_st[p]));
+      CB_CUDA(cudaStreamWaitEvent(st, pl->ev_join[p], 0));
+    }
+  };
   if (!coop) {
+    fork();
     for (uint32_t p = 0; p < P; ++p) {
       PeWork& w = pl->pe[p];
       for (int l = 0; l < L; ++l) {
@@ -458,18 +498,21 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
             fused_work, smooth,
             extract_args(w, w.bm[l & 1], &w.bm[(l + 1) & 1], w.L[l].src, w.L[l].cap_src,
                          &pl->meta_at(p, l)->n_src, &pl->meta_at(p, l + 1)->n_dst, 3 * l + 2,
-                         8 * l + 4));
+                         8 * l + 4),
+            pst(p));
       }
       const uint32_t* Dl = (L == 1) ? d_seeds + off[p] : w.L[L - 2].src;
       launch_relabel(relabel_args(w.bm[(L - 1) & 1], w.L[L - 1], Dl, pl->meta_at(p, L - 1)),
-                     std::max(w.L[L - 1].cap_edges, w.L[L - 1].cap_dst), st);
+                     std::max(w.L[L - 1].cap_edges, w.L[L - 1].cap_dst), pst(p));
       ++launches;
       prof_mark(pl);
     }
+    join();
   } else {
     CB_CUDA(cudaMemsetAsync(pl->send_counts, 0, sizeof(unsigned long long) * L * P * P, st));
     for (int l = 0; l < L; ++l) {
       uint64_t max_src = 1;
+      fork();
       for (uint32_t p = 0; p < P; ++p) {
         PeWork& w = pl->pe[p];
         const uint32_t* D = (l == 0) ? d_seeds + off[p] : w.L[l].dst;
@@ -477,12 +520,14 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
             pl, w, p, l, D, w.L[l].cap_dst, l == 0 ? off[p + 1] - off[p] : ~0ULL, w.bm[0], none,
             0, smooth,
             extract_args(w, w.bm[0], &w.bm[1], w.L[l].src, w.L[l].cap_src,
-                         &pl->meta_at(p, l)->n_src, nullptr, 3 * l + 2, 8 * l + 4));
+                         &pl->meta_at(p, l)->n_src, nullptr, 3 * l + 2, 8 * l + 4),
+            pst(p));
         launch_relabel(relabel_args(w.bm[0], w.L[l], D, pl->meta_at(p, l)),
-                       std::max(w.L[l].cap_edges, w.L[l].cap_dst), st);
+                       std::max(w.L[l].cap_edges, w.L[l].cap_dst), pst(p));
         launches += 1;
         max_src = std::max(max_src, w.L[l].cap_src);
       }
+      join();
       PartPtrs pp{};
       for (uint32_t p = 0; p < P; ++p) {
         PeWork& w = pl->pe[p];
@@ -570,14 +615,25 @@ void prepare_rows(cb_plan* pl, const cb_features* f) {
 void enqueue_gather(cb_plan* pl, const cb_features* f) {
   NvtxRange nvtx_("cb.gather");
   const int vb = vec_bytes_for(f->row_bytes);
+  const bool conc = pl->part_concurrent && !pl->prof && pl->P > 1;
+  if (conc) {  // the parts' gathers are independent: one stream each
+    CB_CUDA(cudaEventRecord(pl->ev_fork, pl->stream));
+    for (uint32_t p = 0; p < pl->P; ++p)
+      CB_CUDA(cudaStreamWaitEvent(pl->part_st[p], pl->ev_fork, 0));
+  }
   for (uint32_t p = 0; p < pl->P; ++p) {
     PeWork& w = pl->pe[p];
     const LayerBufs& b = w.L[pl->L - 1];
     launch_gather(f->table, vb, f->row_bytes, b.src, &pl->meta_at(p, pl->L - 1)->n_src,
-                  w.cap_rows, f->row_map, w.rows, pl->stream);
+                  w.cap_rows, f->row_map, w.rows, conc ? pl->part_st[p] : pl->stream);
     pl->launches += 1;
     prof_mark(pl);
   }
+  if (conc)
+    for (uint32_t p = 0; p < pl->P; ++p) {
+      CB_CUDA(cudaEventRecord(pl->ev_join[p], pl->part_st[p]));
+      CB_CUDA(cudaStreamWaitEvent(pl->stream, pl->ev_join[p], 0));
+    }
   pl->have_rows = true;
 }
 

@@ -244,7 +244,18 @@ struct cb_plan {
     graph_events.clear();
     exec_sample = exec_gather = exec_all = exec_prof = nullptr;
   }
-  ~cb_plan() { drop_graphs(); }
+  // parts of a multi-part plan run concurrently, one stream each, joined
+  // before every cross-part step (part_st empty: one after another)
+  std::vector<cudaStream_t> part_st;
+  cudaEvent_t ev_fork = nullptr;
+  std::vector<cudaEvent_t> ev_join;
+  bool part_concurrent = false;
+  ~cb_plan() {
+    drop_graphs();
+    for (cudaStream_t s : part_st) cudaStreamDestroy(s);
+    for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+  }
 
   LayerMeta* meta_at(uint32_t p, int l) { return meta + p * (L + 1) + l; }
   bool coop_active() const { return mode == CB_MODE_COOP && P > 1; }
@@ -264,7 +275,7 @@ RelabelArgs relabel_args(const Bitmap& bm, const LayerBufs& b, const uint32_t* D
 uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* D,
                        uint64_t cap_dst, uint64_t n_dst_param, Bitmap& set_bm,
                        const RelabelArgs& fused, uint64_t fused_work, bool smooth,
-                       const ExtractArgs& ex);
+                       const ExtractArgs& ex, cudaStream_t stream = nullptr);
 void check_overflow(cb_plan* pl);
 const LayerMeta host_meta(cb_plan* pl, uint32_t p, int l);
 void require_batch(const cb_plan* pl, uint32_t p, int l);

@@ -111,6 +111,7 @@ struct Sync {
   unsigned* overflow = nullptr;               // [1]
   uint32_t* keep_words = nullptr;             // [max_tiles*kLaborTile/32]
   uint2* stage = nullptr;                     // [max_tiles*kLaborTile] kept edges by position
+  double* vtab = nullptr;                     // smoothed LABOR r_t table [n] (nullptr: none)
   uint64_t max_tiles = 0;
   static constexpr int kMaxTickets = 256;
 };
