@@ -259,7 +259,7 @@ struct RelabelArgs {  // edges == nullptr disables
 
 constexpr int kExtractTileWords = 2048;  // bitmap padding granule (max tile)
 constexpr uint64_t kExtractBigWords = 256 * 1024;  // summary-mode threshold
-constexpr int kLaborTile = 4096;
+constexpr int kLaborTile = 2048;
 constexpr uint64_t kVtabMaxVerts = 1ULL << 26;  // smoothed variate table cap (512 MiB)
 constexpr int kFrontierTile = 1024;
 
