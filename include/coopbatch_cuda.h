@@ -128,6 +128,10 @@ void cb_features_destroy(cb_features* f);
 /* fanouts[l] applies at block l (seeds outward); pm may be NULL for P = 1. */
 int cb_plan_create(const cb_graph* g, const cb_partition* pm, int num_layers, int kind,
                    const uint32_t* fanouts, uint64_t max_seeds_per_part, cb_plan** out);
+/* A plan of `parts` independent parts without a partition (indep mode only):
+ * the trial batches of work_curve / indep_sample at equal global batch. */
+int cb_plan_create_parts(const cb_graph* g, uint32_t parts, int num_layers, int kind,
+                         const uint32_t* fanouts, uint64_t max_seeds_per_part, cb_plan** out);
 void cb_plan_destroy(cb_plan* plan);
 int cb_plan_num_parts(const cb_plan* plan, uint32_t* parts);
 /* The CUDA stream every kernel of this plan runs on (cudaStream_t). */
@@ -141,6 +145,13 @@ int cb_sample(cb_plan* plan, int mode, const uint32_t* seeds_flat, const uint64_
               const cb_sched* sched);
 int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
                    const uint64_t* seeds_off, const cb_sched* sched);
+/* P independent expansions in one batch, part p under its own schedule
+ * scheds[p] (indep mode; all schedules plain or all smoothed). This is the
+ * trial loop of work_curve (analysis.cpp:78-124: a fresh plain stream
+ * hash_bits(seed, {tag, 9}) per trial) with the trials as concurrent parts.
+ * Waits, and retries with larger buffers on overflow like cb_sample_sync. */
+int cb_sample_multi(cb_plan* plan, const uint32_t* seeds_flat, const uint64_t* seeds_off,
+                    const cb_sched* scheds);
 /* Same, seeds already in device memory (seeds_off on host). */
 int cb_sample_device(cb_plan* plan, int mode, const uint32_t* d_seeds_flat,
                      const uint64_t* seeds_off, const cb_sched* sched);

@@ -172,6 +172,9 @@ def lib(impl: str = "restated") -> C.CDLL:
                                     C.POINTER(Sched), _u32, _u64, C.POINTER(_f64), _P]
         L.rf_cross_edge_ratio.argtypes = [_P, _P, _u32, C.POINTER(_f64)]
         L.rf_edge_pred_seeds.argtypes = [_P, _P, _u64, _u64, _P, C.POINTER(_u64)]
+        L.rf_work_curve.argtypes = [_P, C.c_int, _u32, _P, _u64, _u32, C.c_int, _u64,
+                                    C.c_int, _P]
+        L.rf_concavity_check.argtypes = [_P, _P, _P, _u64, _P, _P, _P, C.POINTER(C.c_int)]
         L.rf_save_csr.argtypes = [_P, C.c_char_p]
         L.rf_load_csr.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64),
                                   C.POINTER(C.POINTER(_u64)), C.POINTER(C.POINTER(_u32))]
@@ -346,6 +349,34 @@ def edge_pred_seeds_reference(g: CSR, edges, epoch_seed: int) -> np.ndarray:
     _check(rg.L.rf_edge_pred_seeds(rg.h, _ptr(uv), len(uv), epoch_seed, _ptr(out),
                                    C.byref(n)), rg.L)
     return out[: n.value]
+
+
+def work_curve_reference(g: CSR, kind: int, fanout: int, sizes, trials: int, num_layers: int,
+                         seed: int, edge_mode: bool = False) -> np.ndarray:
+    """The reference's work_curve (analysis.cpp:78-124): rows of (mean_sl,
+    se_sl, work_per_seed, se_work) per batch size."""
+    rg = RefGraph(g)
+    sz = np.ascontiguousarray(sizes, dtype=np.uint64)
+    out = np.zeros((len(sz), 4), np.float64)
+    _check(rg.L.rf_work_curve(rg.h, kind, fanout, _ptr(sz), len(sz), trials, num_layers, seed,
+                              int(edge_mode), _ptr(out)), rg.L)
+    return out
+
+
+def concavity_check_reference(sizes, mean, se):
+    """The reference's concavity_check (analysis.cpp:126-151): (second_diff,
+    threshold, violation) per interior point and the overall pass flag."""
+    L = lib("reference")
+    sz = np.ascontiguousarray(sizes, dtype=np.uint64)
+    mu = np.ascontiguousarray(mean, dtype=np.float64)
+    sd = np.ascontiguousarray(se, dtype=np.float64)
+    n = len(sz)
+    d2, thr = np.zeros(max(n - 2, 1)), np.zeros(max(n - 2, 1))
+    vio = np.zeros(max(n - 2, 1), np.int32)
+    ok = C.c_int()
+    _check(L.rf_concavity_check(_ptr(sz), _ptr(mu), _ptr(sd), n, _ptr(d2), _ptr(thr), _ptr(vio),
+                                C.byref(ok)), L)
+    return d2[: n - 2], thr[: n - 2], vio[: n - 2].astype(bool), bool(ok.value)
 
 
 def save_csr_reference(g: CSR, path: str):

@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "coopbatch/analysis.hpp"
 #include "coopbatch/cache.hpp"
 #include "coopbatch/coop.hpp"
 #include "coopbatch/graph.hpp"
@@ -186,6 +187,40 @@ int rf_edge_pred_seeds(void* g, const uint32_t* uv, uint64_t n_edges, uint64_t e
     const auto s = edge_pred_seeds(*static_cast<Graph*>(g), batch, epoch_seed);
     std::memcpy(out, s.data(), s.size() * 4);
     *n_out = s.size();
+  });
+}
+
+/* analysis.cpp:78-124 work_curve; out[4 * i ..] = mean_sl, se_sl,
+ * work_per_seed, se_work of batch size i. edge_mode selects SeedMode::kEdge. */
+int rf_work_curve(void* g, int kind, uint32_t fanout, const uint64_t* sizes, uint64_t n_sizes,
+                  uint32_t trials, int L, uint64_t seed, int edge_mode, double* out) {
+  return guard([&] {
+    const WorkCurve c = work_curve(*static_cast<Graph*>(g), to_cfg(kind, fanout),
+                                   {sizes, n_sizes}, trials, L, seed,
+                                   edge_mode ? SeedMode::kEdge : SeedMode::kNode);
+    for (uint64_t i = 0; i < n_sizes; ++i) {
+      out[4 * i] = c.points[i].mean_sl;
+      out[4 * i + 1] = c.points[i].se_sl;
+      out[4 * i + 2] = c.points[i].work_per_seed;
+      out[4 * i + 3] = c.points[i].se_work;
+    }
+  });
+}
+
+/* analysis.cpp:126-151 concavity_check over (batch, mean, se) points;
+ * entry i-1 of the outputs belongs to interior point i. */
+int rf_concavity_check(const uint64_t* sizes, const double* mean, const double* se, uint64_t n,
+                       double* second_diff, double* threshold, int* violation, int* pass) {
+  return guard([&] {
+    WorkCurve c;
+    for (uint64_t i = 0; i < n; ++i) c.points.push_back({sizes[i], mean[i], se[i], 0.0, 0.0});
+    const ConcavityReport r = concavity_check(c);
+    for (size_t i = 0; i < r.entries.size(); ++i) {
+      second_diff[i] = r.entries[i].second_diff;
+      threshold[i] = r.entries[i].threshold;
+      violation[i] = r.entries[i].violation ? 1 : 0;
+    }
+    *pass = r.pass ? 1 : 0;
   });
 }
 

@@ -13,3 +13,6 @@ from .cache import (  # noqa: F401
     MinibatchSchedule, feature_load_sim, lru_access, nested_batches, run_dependent_experiment,
     shuffled_order, stack_fingerprint)
 from .train import GcnModel, TrainStepResult, coop_train_step, indep_train_step  # noqa: F401,E402
+from .analysis import (  # noqa: F401,E402
+    ConcavityEntry, ConcavityReport, SeedMode, WorkCurve, WorkCurvePoint, concavity_check,
+    work_curve)

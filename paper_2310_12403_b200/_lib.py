@@ -44,11 +44,13 @@ _SIGS = {
     "cb_features_info": (C.c_int, [_P, C.POINTER(_u32), C.POINTER(C.c_int), C.POINTER(_u64)]),
     "cb_features_destroy": (None, [_P]),
     "cb_plan_create": (C.c_int, [_P, _P, C.c_int, C.c_int, _P, _u64, _PP]),
+    "cb_plan_create_parts": (C.c_int, [_P, _u32, C.c_int, C.c_int, _P, _u64, _PP]),
     "cb_plan_destroy": (None, [_P]),
     "cb_plan_num_parts": (C.c_int, [_P, C.POINTER(_u32)]),
     "cb_plan_stream": (C.c_void_p, [_P]),
     "cb_sample": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched)]),
     "cb_sample_sync": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched)]),
+    "cb_sample_multi": (C.c_int, [_P, _P, _P, C.POINTER(Sched)]),
     "cb_sample_device": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched)]),
     "cb_gather": (C.c_int, [_P, _P]),
     "cb_synchronize": (C.c_int, [_P]),

@@ -347,18 +347,24 @@ class Plan:
     combination; reusable across batches."""
 
     def __init__(self, g: Graph, pm: PartitionMap | None, num_layers: int,
-                 cfg: SamplerConfig, max_seeds_per_part: int):
+                 cfg: SamplerConfig, max_seeds_per_part: int, parts: int | None = None):
+        """parts (with pm None): that many independent parts without a
+        partition (indep mode only; cb_plan_create_parts)."""
         self.g, self.pm, self.L, self.cfg = g, pm, num_layers, cfg
         self.max_seeds = max_seeds_per_part
         fo = np.asarray(cfg.layer_fanouts(num_layers), dtype=np.uint32)
         h = C.c_void_p()
-        _check(_lib.load().cb_plan_create(g._h, pm._h if pm else None, num_layers,
-                                          int(cfg.kind), _ptr(fo), max_seeds_per_part,
-                                          C.byref(h)))
+        if pm is None and parts is not None:
+            _check(_lib.load().cb_plan_create_parts(g._h, parts, num_layers, int(cfg.kind),
+                                                    _ptr(fo), max_seeds_per_part, C.byref(h)))
+        else:
+            _check(_lib.load().cb_plan_create(g._h, pm._h if pm else None, num_layers,
+                                              int(cfg.kind), _ptr(fo), max_seeds_per_part,
+                                              C.byref(h)))
         self._h = h
         if cfg.kind == SamplerKind.kRw:
             _check(_lib.load().cb_plan_set_rw(h, cfg.rw_length, cfg.rw_restart, cfg.rw_walks))
-        self.P = pm.num_parts if pm else 1
+        self.P = pm.num_parts if pm else (parts or 1)
 
     def __del__(self):
         try:
@@ -389,6 +395,15 @@ class Plan:
         s = schedule._c()
         f = _lib.load().cb_sample_sync if sync else _lib.load().cb_sample
         _check(f(self._h, mode, _ptr(flat), _ptr(off), C.byref(s)))
+
+    def sample_multi(self, per_pe_seeds, schedules: list[SeedSchedule]):
+        """Independent expansions, part p under schedules[p] (cb_sample_multi)."""
+        if len(per_pe_seeds) != self.P or len(schedules) != self.P:
+            raise InputError("sample_multi: one seed list and one schedule per part")
+        flat, off = self._flat(per_pe_seeds)
+        self._keep = (flat, off)
+        sc = (Sched * self.P)(*[s._c() for s in schedules])
+        _check(_lib.load().cb_sample_multi(self._h, _ptr(flat), _ptr(off), sc))
 
     def sample_device(self, d_seeds_ptr: int, offsets, schedule: SeedSchedule,
                       mode: int = MODE_COOP):

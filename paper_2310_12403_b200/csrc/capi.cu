@@ -151,7 +151,7 @@ void plan_alloc(cb_plan* pl) {
   pl->meta = pl->mem.alloc<LayerMeta>(static_cast<uint64_t>(P) * (L + 1));
   CB_CUDA(cudaMemset(pl->meta, 0, sizeof(LayerMeta) * P * (L + 1)));
   pl->send_counts = pl->mem.alloc<unsigned long long>(static_cast<uint64_t>(L) * P * P);
-  pl->var = pl->mem.alloc<Variates>(1);
+  pl->var = pl->mem.alloc<Variates>(P);  // one per part (per-part schedules)
   pl->seeds_cap = static_cast<uint64_t>(P) * std::max<uint64_t>(pl->max_seeds, 1);
   pl->seeds = pl->mem.alloc<uint32_t>(pl->seeds_cap);
   pl->scratch = pl->mem.alloc<unsigned long long>(8);
@@ -188,6 +188,15 @@ Variates make_variates(const cb_sched* s) {
   return v;
 }
 
+// The same variates for every part (the reference's single schedule), or one
+// schedule per part (cb_sample_multi).
+void upload_variates(cb_plan* pl, const cb_sched* s, uint32_t n_sched, cudaStream_t st) {
+  std::vector<Variates> v(pl->P);
+  for (uint32_t p = 0; p < pl->P; ++p) v[p] = make_variates(s + (n_sched > 1 ? p : 0));
+  CB_CUDA(cudaMemcpyAsync(pl->var, v.data(), sizeof(Variates) * pl->P, cudaMemcpyHostToDevice,
+                          st));  // pageable source: staged before the call returns
+}
+
 void check_seeds_host(const cb_plan* pl, const uint32_t* flat, const uint64_t* off) {
   const uint64_t n = pl->g->g.n;
   for (uint32_t p = 0; p < pl->P; ++p) {
@@ -198,6 +207,12 @@ void check_seeds_host(const cb_plan* pl, const uint32_t* flat, const uint64_t* o
       require(flat[i] < n, "vertex id " + std::to_string(flat[i]) + " out of range [0, " +
                                std::to_string(n) + ")");
   }
+}
+
+void require_mode(const cb_plan* pl, int mode) {
+  require(mode == CB_MODE_COOP || mode == CB_MODE_INDEP, "unknown sampling mode");
+  require(mode != CB_MODE_COOP || pl->P == 1 || pl->pm != nullptr,
+          "cooperative sampling needs a partition (plan created without one)");
 }
 
 void check_ownership_host(const cb_plan* pl, const uint32_t* flat, const uint64_t* off) {
@@ -318,7 +333,7 @@ FrontierArgs frontier_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint
   fa.kind = pl->kind;
   fa.k = pl->fanouts[l];
   fa.layer = l;
-  fa.var = pl->var;
+  fa.var = pl->var + p;
   fa.set_bits = set_bm.bits;
   fa.set_summ = set_bm.summ;
   fa.act = b.act;
@@ -351,7 +366,7 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
   la.kind = pl->kind;
   la.k = pl->fanouts[l];
   la.layer = l;
-  la.var = pl->var;
+  la.var = pl->var + p;
   la.bits = set_bm.bits;
   la.summ = set_bm.summ;
   la.edges = b.edges;
@@ -402,7 +417,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
     ra.walks = pl->rw_walks;
     ra.length = pl->rw_length;
     ra.restart = pl->rw_restart;
-    ra.var = pl->var;
+    ra.var = pl->var + p;
     ra.bits = set_bm.bits;
     ra.summ = set_bm.summ;
     ra.slots = b.slots;
@@ -431,15 +446,12 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
 
 // The per-batch launch sequence. d_seeds: P seed lists back to back (device).
 void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_t* off,
-                   const cb_sched* sched, bool capturing = false) {
+                   const cb_sched* sched, bool capturing = false, uint32_t n_sched = 1) {
   const uint32_t P = pl->P;
   const int L = pl->L;
   cudaStream_t st = pl->stream;
   uint64_t launches = 0;
-  if (!capturing) {
-    const Variates v = make_variates(sched);
-    CB_CUDA(cudaMemcpyAsync(pl->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
-  }
+  if (!capturing) upload_variates(pl, sched, n_sched, st);
   pl->mode = mode;
   pl->seeds_off.assign(off, off + P + 1);
   if (!capturing && ++pl->batches % (1u << 17) == 0) {  // epoch wrap (18-bit epochs)
@@ -574,16 +586,24 @@ void check_overflow(cb_plan* pl) {
 }
 
 void sample_host(cb_plan* pl, int mode, const uint32_t* flat, const uint64_t* off,
-                 const cb_sched* sched) {
+                 const cb_sched* sched, uint32_t n_sched = 1) {
   require(mode == CB_MODE_COOP || mode == CB_MODE_INDEP, "unknown sampling mode");
   require(sched != nullptr, "null schedule");
-  require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
+  for (uint32_t i = 0; i < n_sched; ++i) {
+    require(sched[i].kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
+    const auto smoothed = [](const cb_sched& x) {
+      return x.kappa != cbdev::kKappaInf && x.kappa >= 2;
+    };
+    require(smoothed(sched[i]) == smoothed(sched[0]),
+            "per-part schedules must agree on smoothing (kappa in {1, inf} vs 2..)");
+  }
   check_seeds_host(pl, flat, off);
+  require_mode(pl, mode);
   if (mode == CB_MODE_COOP) check_ownership_host(pl, flat, off);
   const uint64_t total = off[pl->P];
   if (total)
     CB_CUDA(cudaMemcpyAsync(pl->seeds, flat, total * 4, cudaMemcpyHostToDevice, pl->stream));
-  enqueue_batch(pl, mode, pl->seeds, off, sched);
+  enqueue_batch(pl, mode, pl->seeds, off, sched, false, n_sched);
 }
 
 const LayerMeta host_meta(cb_plan* pl, uint32_t p, int l) {
@@ -955,10 +975,12 @@ void cb_features_destroy(cb_features* f) {
   cudaSetDevice(prev);
 }
 
-int cb_plan_create(const cb_graph* g, const cb_partition* pm, int num_layers, int kind,
-                   const uint32_t* fanouts, uint64_t max_seeds_per_part, cb_plan** out) {
+namespace {
+int plan_create(const cb_graph* g, const cb_partition* pm, uint32_t parts, int num_layers,
+                int kind, const uint32_t* fanouts, uint64_t max_seeds_per_part, cb_plan** out) {
   return guard([&] {
-    require(g != nullptr, "null graph");
+    require(g != nullptr && out != nullptr, "null argument");
+    require(parts >= 1 && parts <= 64, "part count must be in [1, 64]");
     require(num_layers >= 1, "expand: num_layers must be >= 1");
     require(num_layers <= 8, "at most 8 layers");
     require(kind == CB_FULL || kind == CB_NS || kind == CB_LABOR0 || kind == CB_RW,
@@ -970,7 +992,7 @@ int cb_plan_create(const cb_graph* g, const cb_partition* pm, int num_layers, in
     pl->device = g->g.device;
     pl->g = g;
     pl->pm = pm;
-    pl->P = pm ? pm->parts : 1;
+    pl->P = pm ? pm->parts : parts;
     pl->L = num_layers;
     pl->kind = kind;
     for (int l = 0; l < num_layers; ++l) {
@@ -986,6 +1008,17 @@ int cb_plan_create(const cb_graph* g, const cb_partition* pm, int num_layers, in
     plan_alloc(pl.get());
     *out = pl.release();
   });
+}
+}  // namespace
+
+int cb_plan_create(const cb_graph* g, const cb_partition* pm, int num_layers, int kind,
+                   const uint32_t* fanouts, uint64_t max_seeds_per_part, cb_plan** out) {
+  return plan_create(g, pm, 1, num_layers, kind, fanouts, max_seeds_per_part, out);
+}
+
+int cb_plan_create_parts(const cb_graph* g, uint32_t parts, int num_layers, int kind,
+                         const uint32_t* fanouts, uint64_t max_seeds_per_part, cb_plan** out) {
+  return plan_create(g, nullptr, parts, num_layers, kind, fanouts, max_seeds_per_part, out);
 }
 
 void cb_plan_destroy(cb_plan* plan) {
@@ -1038,11 +1071,31 @@ int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
   });
 }
 
+int cb_sample_multi(cb_plan* plan, const uint32_t* seeds_flat, const uint64_t* seeds_off,
+                    const cb_sched* scheds) {
+  NvtxRange nvtx_("cb.sample_multi");
+  return guard([&] {
+    require(plan != nullptr && seeds_off != nullptr && scheds != nullptr, "null argument");
+    DeviceGuard dg(plan->device);
+    for (int attempt = 0;; ++attempt) {
+      sample_host(plan, CB_MODE_INDEP, seeds_flat, seeds_off, scheds, plan->P);
+      try {
+        check_overflow(plan);
+        return;
+      } catch (const Error& e) {
+        if (e.code != kOverflow || attempt >= 12) throw;
+        plan->grow *= 2.0;
+        plan_alloc(plan);
+      }
+    }
+  });
+}
+
 int cb_sample_device(cb_plan* plan, int mode, const uint32_t* d_seeds_flat,
                      const uint64_t* seeds_off, const cb_sched* sched) {
   return guard([&] {
     require(plan != nullptr && seeds_off != nullptr && sched != nullptr, "null argument");
-    require(mode == CB_MODE_COOP || mode == CB_MODE_INDEP, "unknown sampling mode");
+    require_mode(plan, mode);
     for (uint32_t p = 0; p < plan->P; ++p)
       require(seeds_off[p + 1] - seeds_off[p] <= plan->max_seeds,
               "more seeds than the plan's max_seeds_per_part");
@@ -1066,7 +1119,7 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
   return guard([&] {
     require(plan != nullptr && seeds_off != nullptr && sched != nullptr, "null argument");
     require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
-    require(mode == CB_MODE_COOP || mode == CB_MODE_INDEP, "unknown sampling mode");
+    require_mode(plan, mode);
     for (uint32_t p = 0; p < plan->P; ++p)
       require(seeds_off[p + 1] - seeds_off[p] <= plan->max_seeds,
               "more seeds than the plan's max_seeds_per_part");
@@ -1141,8 +1194,7 @@ int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_devic
                                 seeds_on_device ? cudaMemcpyDeviceToDevice
                                                 : cudaMemcpyHostToDevice,
                                 st));
-      const Variates v = make_variates(sched);
-      CB_CUDA(cudaMemcpyAsync(plan->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+      upload_variates(plan, sched, 1, st);
       if (++plan->batches % (1u << 17) == 0) {
         for (auto& w : plan->pe) {
           CB_CUDA(cudaMemsetAsync(w.sync.status_a, 0, w.sync.max_tiles * 8, st));
@@ -1400,8 +1452,7 @@ int cb_plan_sample_layer(cb_plan* plan, int layer, const uint32_t* d_dst, uint64
     if (n_dst)
       CB_CUDA(cudaMemcpyAsync(D, d_dst, n_dst * 4, cudaMemcpyDeviceToDevice, st));
     if (layer == 0) {
-      const Variates v = make_variates(sched);
-      CB_CUDA(cudaMemcpyAsync(plan->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+      upload_variates(plan, sched, 1, st);
       plan->seeds_off.assign({0, n_dst});
       plan->mode = CB_MODE_COOP;
     }
@@ -1543,8 +1594,7 @@ int cb_plan_graph_profile(cb_plan* plan, const uint32_t* d_seeds, const cb_sched
     const uint64_t total = plan->cap_off[plan->P];
     if (d_seeds && total)
       CB_CUDA(cudaMemcpyAsync(plan->seeds, d_seeds, total * 4, cudaMemcpyDefault, st));
-    const Variates v = make_variates(sched);
-    CB_CUDA(cudaMemcpyAsync(plan->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+    upload_variates(plan, sched, 1, st);
     if (plan->dirty_mode >= 0 && plan->dirty_mode != plan->cap_mode)
       for (uint32_t p = 0; p < plan->P; ++p) {
         const Dirty d = dirty_of(plan, p, plan->dirty_mode);

@@ -267,6 +267,7 @@ namespace cb {
 namespace capi {
 // capi.cu helpers shared with the other C-ABI translation units
 Variates make_variates(const cb_sched* s);
+void upload_variates(cb_plan* pl, const cb_sched* s, uint32_t n_sched, cudaStream_t st);
 ExtractArgs extract_args(PeWork& w, const Bitmap& bm, const Bitmap* zero_bm, uint32_t* out,
                          uint64_t cap, unsigned long long* c1, unsigned long long* c2,
                          int ticket, int slot);

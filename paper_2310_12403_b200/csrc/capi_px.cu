@@ -111,8 +111,7 @@ int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seed
       require(n_seeds <= plan->max_seeds, "more seeds than the plan's max_seeds_per_part");
       if (n_seeds)
         CB_CUDA(cudaMemcpyAsync(D, seeds, n_seeds * 4, cudaMemcpyDefault, st));
-      const Variates v = make_variates(sched);
-      CB_CUDA(cudaMemcpyAsync(plan->var, &v, sizeof(Variates), cudaMemcpyHostToDevice, st));
+      upload_variates(plan, sched, 1, st);
       CB_CUDA(cudaMemsetAsync(px.send, 0, plan->L * px.world * 8, st));
       plan->seeds_off.assign({0, n_seeds});
       plan->mode = CB_MODE_COOP;

@@ -21,30 +21,33 @@ def _mix64(x: np.ndarray) -> np.ndarray:
         return x ^ (x >> _M(31))
 
 
+def first_distinct(prefix: int, space: int, count: int) -> np.ndarray:
+    """The first `count` distinct values of the stream
+    v_a = min(floor(U(mix64(prefix ^ a)) * space), space - 1), a = 0, 1, ...,
+    in stream order: the rejection loops of draw_from_pool (cli.cpp:121-139),
+    draw_seeds and draw_edges (analysis.cpp:15-54), vectorised."""
+    if count == 0:
+        return np.zeros(0, np.uint64)
+    vals = np.zeros(0, np.uint64)
+    attempt, chunk = 0, max(2 * count, 64)
+    while True:
+        att = np.arange(attempt, attempt + chunk, dtype=np.uint64)
+        u = (_mix64(_M(prefix) ^ att) >> _M(11)).astype(np.float64) * 2.0 ** -53
+        v = np.minimum((u * float(space)).astype(np.uint64), _M(space - 1))
+        vals = np.concatenate([vals, v])
+        attempt += chunk
+        uniq, first = np.unique(vals, return_index=True)
+        if len(uniq) >= count:
+            first.sort()
+            return vals[first[:count]]
+        chunk *= 2
+
+
 def draw_from_pool(pool: np.ndarray, count: int, seed: int, tag: int) -> np.ndarray:
     pool = np.asarray(pool, dtype=np.uint32)
-    n = len(pool)
-    if count > n:
+    if count > len(pool):
         raise ValueError("not enough vertices in pool to draw batch")
-    pfx = hash_bits(seed, [8, tag])
-    used = np.zeros(n, dtype=bool)
-    out = np.empty(count, dtype=np.uint32)
-    got, attempt = 0, 0
-    while got < count:
-        chunk = max(2 * (count - got), 64)
-        att = np.arange(attempt, attempt + chunk, dtype=np.uint64)
-        h = _mix64(_M(pfx) ^ att)
-        u = (h >> _M(11)).astype(np.float64) * 2.0 ** -53
-        idx = np.minimum((u * float(n)).astype(np.uint64), n - 1).astype(np.int64)
-        for i in idx:  # sequential rejection of repeats, in attempt order
-            if not used[i]:
-                used[i] = True
-                out[got] = pool[i]
-                got += 1
-                if got == count:
-                    break
-        attempt += chunk
-    return out
+    return pool[first_distinct(hash_bits(seed, [8, tag]), len(pool), count).astype(np.int64)]
 
 
 def coop_seeds(members: list[np.ndarray], b: int, seed: int, step: int) -> list[np.ndarray]:

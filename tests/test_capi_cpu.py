@@ -152,3 +152,47 @@ def test_csv_report_format(tmp_path):
     lines = p.read_text().splitlines()
     assert lines[:3] == ["# kappa=4", "# mode=smoothed", "step,miss_rate,s_l,bytes"]
     assert lines[3] == "0,0.5,10,1280" and not (tmp_path / "cache.csv.tmp").exists()
+
+
+def test_first_distinct_equals_sequential_rejection():
+    """seeds.first_distinct (vectorised) == the reference's sequential
+    rejection loop (cli.cpp:121-139, analysis.cpp:15-31) restated here."""
+    from paper_2310_12403_b200.coopbatch import hash_bits, hash_uniform
+    from paper_2310_12403_b200.seeds import first_distinct
+    for space, count, seed, tag in [(100, 10, 5, 7), (12, 12, 1, 3), (5000, 1024, 4, 99),
+                                    (1, 1, 0, 0), (50, 0, 2, 2)]:
+        want, seen, a = [], set(), 0
+        while len(want) < count:
+            u = hash_uniform(seed, [8, tag, a])
+            a += 1
+            v = min(int(u * float(space)), space - 1)
+            if v not in seen:
+                seen.add(v)
+                want.append(v)
+        got = first_distinct(hash_bits(seed, [8, tag]), space, count)
+        assert got.tolist() == want
+
+
+def test_concavity_check_matches_reference():
+    """analysis.concavity_check == the compiled reference's (analysis.cpp:126-151)."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    from paper_2310_12403_b200.analysis import (WorkCurve, WorkCurvePoint,
+                                                concavity_check)
+    from paper_2310_12403_b200.coopbatch import InputError
+    rng = np.random.default_rng(0)
+    cases = [([64, 128, 256, 512], [640.0, 1280, 2560, 5120], [0.0] * 4),
+             ([64, 128, 256, 512], [0.001 * b * b for b in (64, 128, 256, 512)], [0.0] * 4)]
+    for _ in range(20):
+        b = np.cumsum(rng.integers(1, 100, 6)).tolist()
+        cases.append((b, np.sqrt(np.array(b, float) * 50).tolist(), rng.random(6).tolist()))
+    for sizes, mean, se in cases:
+        c = WorkCurve(3, [WorkCurvePoint(s, m, e) for s, m, e in zip(sizes, mean, se)])
+        rep = concavity_check(c)
+        d2, thr, vio, ok = O.concavity_check_reference(sizes, mean, se)
+        assert rep.passed == ok
+        assert [e.second_diff for e in rep.entries] == d2.tolist()
+        assert [e.threshold for e in rep.entries] == thr.tolist()
+        assert [e.violation for e in rep.entries] == vio.tolist()
+    with pytest.raises(InputError):
+        concavity_check(WorkCurve(3, [WorkCurvePoint(1), WorkCurvePoint(2)]))
