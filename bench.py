@@ -27,6 +27,7 @@ import os
 import subprocess
 import sys
 import threading
+import math
 import time
 
 import numpy as np
@@ -378,6 +379,58 @@ def batch_sweep_evidence(cb, dev, batches=(1024, 4096, 16384, 65536), steps=10):
                              "input_vertices_per_seed": float(np.mean(rows)) / b,
                              "feature_bytes_per_seed": float(np.mean(rows)) * 1536 / b})
         del plan, d
+    del g
+    return out
+
+
+# ------------------------------------------------------ work curves (f4) ---
+def work_curve_evidence(cb, dev, cpu: bool, trials=50, layers=3, seed=49):
+    """Acceptance criteria 2-3 (acceptance.cpp:137-192): E|S^3| against batch
+    size 64..8192 for NS / LABOR-0 / RW (defaults k=10, o=3, p=0.5, a=100),
+    50 trials per size, on the c1 R-MAT (2^16 V / 2^20 E, avg degree 16; the
+    acceptance graph is a 100K-vertex degree-16 power-law graph). The trials
+    of a size run as the parts of one plan (cb_sample_multi). Checks: work per
+    seed nonincreasing within +1 pooled s.e., concavity_check passes. With
+    `cpu`, the compiled reference's work_curve runs on the same CSR (all host
+    threads) for LABOR-0 as the CPU baseline and the curves are compared."""
+    import os
+    c = CONFIGS["c1"]
+    g = cb.Graph.generate_rmat(c["n"], c["m"], GRAPH_SEED, device=dev)
+    sizes = [64 << i for i in range(8)]
+    out = {"graph": "c1 R-MAT 2^16 V / 2^20 E", "sizes": sizes, "trials": trials,
+           "layers": layers, "samplers": {}}
+    for name, kind in (("ns", cb.SamplerKind.kNs), ("labor0", cb.SamplerKind.kLabor0),
+                       ("rw", cb.SamplerKind.kRw)):
+        cfg = cb.SamplerConfig(kind)
+        cb.work_curve(g, cfg, sizes[:1], 2, layers, seed)  # warm-up
+        t0 = time.time()
+        curve = cb.work_curve(g, cfg, sizes, trials, layers, seed)
+        dt = time.time() - t0
+        mono = all(b.work_per_seed <= a.work_per_seed + math.sqrt(a.se_work ** 2 + b.se_work ** 2)
+                   for a, b in zip(curve.points, curve.points[1:]))
+        out["samplers"][name] = {
+            "seconds": round(dt, 3),
+            "work_per_seed": [round(p.work_per_seed, 4) for p in curve.points],
+            "nonincreasing": mono, "concave": cb.concavity_check(curve).passed}
+        for p in curve.points:
+            CSV_ROWS.setdefault("work_curve", []).append(
+                (name, p.batch_size, p.mean_sl, p.se_sl, p.work_per_seed, p.se_work))
+        if cpu and name == "labor0":
+            try:
+                from oracle import oracle as O
+                indptr, indices = g.download()
+                os.environ.setdefault("COOPBATCH_THREADS", str(os.cpu_count() or 1))
+                t0 = time.time()
+                ref = O.work_curve_reference(O.CSR(indptr, indices), O.LABOR0, cfg.fanout, sizes,
+                                             trials, layers, seed)
+                rt = time.time() - t0
+                got = np.array([[p.mean_sl, p.se_sl, p.work_per_seed, p.se_work]
+                                for p in curve.points])
+                out["samplers"][name]["cpu_baseline"] = {
+                    "kind": "reference", "seconds": round(rt, 3), "cores": os.cpu_count(),
+                    "equal_to_gpu": bool(np.array_equal(ref, got))}
+            except Exception as e:  # noqa: BLE001 - evidence only
+                out["samplers"][name]["cpu_baseline"] = {"unavailable": str(e)[:200]}
     del g
     return out
 
@@ -750,6 +803,7 @@ def run_ours(args, cfg):
         line["evidence"]["kappa"] = kappa_evidence(cb, dev)
         line["evidence"]["papers100m"] = scale_evidence(cb, dev)
         line["evidence"]["mag240m_batch_sweep"] = batch_sweep_evidence(cb, dev)
+        line["evidence"]["work_curves"] = work_curve_evidence(cb, dev, not args.no_cpu_baseline)
     if world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import oracle as O

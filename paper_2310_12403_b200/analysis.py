@@ -96,7 +96,7 @@ def _mean_se(xs: list[float]) -> tuple[float, float]:
 
 def work_curve(g: Graph, cfg: SamplerConfig, batch_sizes, trials: int, num_layers: int,
                seed: int, mode: SeedMode = SeedMode.kNode,
-               trials_per_launch: int = 16) -> WorkCurve:
+               trials_per_launch: int = 8) -> WorkCurve:
     """analysis.cpp:78-124 on the GPU: mean and standard error of |S^L| over
     `trials` batches per batch size."""
     if trials == 0:
@@ -104,32 +104,36 @@ def work_curve(g: Graph, cfg: SamplerConfig, batch_sizes, trials: int, num_layer
     sizes = [int(b) for b in batch_sizes]
     curve = WorkCurve(layer=num_layers)
     csr = g.download() if mode == SeedMode.kEdge else None
+    seeds: list[list[np.ndarray]] = []
     for bi, b in enumerate(sizes):
         if bi > 0 and b <= sizes[bi - 1]:
             raise InputError("work_curve: batch sizes must be strictly increasing")
-        seeds, scheds = [], []
+        row = []
         for t in range(trials):
             tag = hash_bits(seed, [b, t])
             if mode == SeedMode.kNode:
-                s = draw_seeds(g.num_vertices, b, seed, tag)
+                row.append(draw_seeds(g.num_vertices, b, seed, tag))
             else:
                 edges = draw_edges(csr[0], csr[1], b, seed, tag)
-                s = edge_pred_seeds(csr[0], csr[1], edges, hash_bits(seed, [tag, 7]),
-                                    g.num_vertices)
-            seeds.append(s)
-            z = hash_bits(seed, [tag, 9])
-            scheds.append(SeedSchedule(1, z, z, 0))
-        G = max(1, min(trials, trials_per_launch))
-        plan = Plan(g, None, num_layers, cfg, max(1, max(len(s) for s in seeds)), parts=G)
+                row.append(edge_pred_seeds(csr[0], csr[1], edges, hash_bits(seed, [tag, 7]),
+                                           g.num_vertices))
+        seeds.append(row)
+    # one plan for the whole curve: G trials per launch, sized for the largest
+    G = max(1, min(trials, trials_per_launch))
+    plan = Plan(g, None, num_layers, cfg, max(1, max(len(s) for r in seeds for s in r)),
+                parts=G)
+    empty, idle = np.zeros(0, np.uint32), SeedSchedule.plain(0)
+    for b, row in zip(sizes, seeds):
         sl: list[float] = []
         for c0 in range(0, trials, G):
-            cs, cz = seeds[c0:c0 + G], scheds[c0:c0 + G]
+            cs = row[c0:c0 + G]
+            cz = [SeedSchedule(1, z, z, 0)
+                  for z in (hash_bits(seed, [hash_bits(seed, [b, t]), 9])
+                            for t in range(c0, c0 + len(cs)))]
             n = len(cs)
-            cs = cs + [np.zeros(0, np.uint32)] * (G - n)
-            cz = cz + [SeedSchedule.plain(0)] * (G - n)
-            plan.sample_multi(cs, cz)
-            sl += [float(plan.layer_sizes(p, num_layers - 1)["n_src"]) for p in range(n)]
-        del plan
+            plan.sample_multi(cs + [empty] * (G - n), cz + [idle] * (G - n))
+            meta = plan.all_layer_sizes()
+            sl += [float(meta[p, num_layers - 1, 4]) for p in range(n)]
         mean, se = _mean_se(sl)
         curve.points.append(WorkCurvePoint(b, mean, se, mean / b, se / b))
     return curve

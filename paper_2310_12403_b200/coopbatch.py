@@ -460,6 +460,17 @@ class Plan:
         _check(_lib.load().cb_plan_launch_count(self._h, mode, int(with_gather), C.byref(n)))
         return n.value
 
+    def all_layer_sizes(self) -> np.ndarray:
+        """All parts' per-layer counts in one read: [P, L+1, 8] u64 records
+        (n_dst, scan_total, n_active, n_edges, n_src, uncertified, pad, pad)."""
+        L = _lib.load()
+        nb = C.c_uint64()
+        _check(L.cb_plan_meta_async(self._h, None, C.byref(nb)))
+        out = np.zeros(nb.value // 8, np.uint64)
+        _check(L.cb_plan_meta_async(self._h, _ptr(out), None))
+        self.synchronize()
+        return out.reshape(self.P, self.L + 1, 8)
+
     def layer_sizes(self, p: int, l: int) -> dict:
         s = np.zeros(6, np.uint64)
         _check(_lib.load().cb_layer_sizes(self._h, p, l, _ptr(s)))

@@ -204,8 +204,9 @@ void check_seeds_host(const cb_plan* pl, const uint32_t* flat, const uint64_t* o
     require(off[p + 1] - off[p] <= pl->max_seeds,
             "part " + std::to_string(p) + " has more seeds than the plan's max_seeds_per_part");
     for (uint64_t i = off[p]; i < off[p + 1]; ++i)
-      require(flat[i] < n, "vertex id " + std::to_string(flat[i]) + " out of range [0, " +
-                               std::to_string(n) + ")");
+      if (flat[i] >= n)
+        throw Error(kInput, "vertex id " + std::to_string(flat[i]) + " out of range [0, " +
+                                std::to_string(n) + ")");
   }
 }
 
@@ -240,8 +241,9 @@ void check_ownership_host(const cb_plan* pl, const uint32_t* flat, const uint64_
   cudaFree(d_cnt);
   for (uint32_t p = 0; p < pl->P; ++p)
     for (uint64_t i = off[p]; i < off[p + 1]; ++i)
-      require(owners[i] == p, "coop_sample: seed " + std::to_string(flat[i]) +
-                                  " is not owned by part " + std::to_string(p));
+      if (owners[i] != p)
+        throw Error(kInput, "coop_sample: seed " + std::to_string(flat[i]) +
+                                " is not owned by part " + std::to_string(p));
 }
 
 void prof_mark(cb_plan* pl) {
@@ -679,8 +681,8 @@ int cb_graph_create_from_csr(const uint64_t* indptr, const uint32_t* indices, ui
     require(indptr[0] == 0, "csr: indptr[0] != 0");
     require(indptr[n] == m, "csr: indptr[n] != num edges");
     for (uint64_t v = 0; v < n; ++v)
-      require(indptr[v] <= indptr[v + 1],
-              "csr: indptr not nondecreasing at " + std::to_string(v));
+      if (indptr[v] > indptr[v + 1])
+        throw Error(kInput, "csr: indptr not nondecreasing at " + std::to_string(v));
     for (uint64_t e = 0; e < m; ++e) require(indices[e] < n, "csr: index out of range");
     DeviceGuard dg(device);
     auto h = std::make_unique<cb_graph>();

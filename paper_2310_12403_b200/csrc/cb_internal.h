@@ -40,6 +40,11 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define CB_CUDA(x) ::cb::cuda_check((x), #x)
 #define CB_LAUNCH(what) ::cb::cuda_check(cudaGetLastError(), what)
 
+inline void require(bool ok, const char* msg) {
+  if (!ok) throw Error(kInput, msg);
+}
+// Callers in per-element loops test first and build the message only on
+// failure (a std::string per element cost ~70 ns/seed on the host).
 inline void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(kInput, msg);
 }
