@@ -10,7 +10,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcoopbatch_b200.so")
+# CB_LIB_PATH: an alternative in-tree build (A/B experiments under tools/)
+LIB_PATH = os.environ.get("CB_LIB_PATH") or os.path.join(HERE, "libcoopbatch_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "coopbatch_cuda.h")
 
 

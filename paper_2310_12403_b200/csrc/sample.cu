@@ -333,6 +333,13 @@ __global__ void __launch_bounds__(kNT) vtab_kernel(LaborArgs a) {
 
 // Smoothed stream: r_t from the layer's variate table when one was built
 // (samplers.cpp:114-129 memoises r_t per t the same way), else evaluated.
+// Plain stream: (mix64(p1 ^ t) >> 11) <= th  <=>  mix64(p1 ^ t) <= T with
+// T = th * 2^11 + 2^11 - 1 (th < 2^53; th >= 2^53 keeps every position), so
+// the per-position test is one 64-bit compare without the shift.
+__device__ __forceinline__ uint64_t plain_bound(uint64_t th) {
+  return th >= (1ULL << 53) ? ~0ULL : ((th << 11) | 0x7ffULL);
+}
+
 template <bool SMOOTH>
 __device__ __forceinline__ bool keep_rule(const Variates& v, uint64_t p1, uint64_t p2,
                                           uint32_t t, uint64_t th, unsigned long long& uncert,
@@ -384,13 +391,15 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
     // fast path: the whole span lies inside record `cur`
     const uint32_t* row = row_of(cur) + r0 + lane;
     const uint64_t th = th_of(cur);
+    const uint64_t T = plain_bound(th);
     const uint32_t di = di_of(cur);
     uint32_t tv[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) tv[j] = __ldg(row + j * 32);
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
-      const bool keep = keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab);
+      const bool keep = SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab)
+                               : mix64_dev(p1 ^ tv[j]) <= T;
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == j) my_word = bal;
       if (keep) {
@@ -417,7 +426,9 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
     for (int j = 0; j < IPT; ++j) {
       const uint32_t r = r0 + j * 32 + lane;
       const bool keep =
-          (r < rend) && keep_rule<SMOOTH>(v, p1, p2, tv[j], th_of(li[j]), uncert, vtab);
+          (r < rend) &&
+          (SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th_of(li[j]), uncert, vtab)
+                  : mix64_dev(p1 ^ tv[j]) <= plain_bound(th_of(li[j])));
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == j) my_word = bal;
       if (keep) {
