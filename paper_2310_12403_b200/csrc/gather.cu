@@ -20,8 +20,15 @@ using namespace cbdev;
 
 namespace {
 
+// 8 CTAs of 256 per SM (32 registers). 16-byte rows keep 3 vectors in
+// flight per thread: UNROLL 4 spilled 56 B to the stack under the 32-register
+// bound (gather 14.8 -> 14.0 us at c2, 14.7 -> 13.6 us at c4; tools/ab.sh).
+constexpr int kGatherCtasPerSM = 8;
+template <typename V>
+constexpr int gather_unroll() { return sizeof(V) == 16 ? 3 : 4; }
+
 template <typename V, int UNROLL>
-__global__ void __launch_bounds__(256, 8) gather_kernel(
+__global__ void __launch_bounds__(256, kGatherCtasPerSM) gather_kernel(
     const V* __restrict__ table, const uint32_t* __restrict__ ids,
     const unsigned long long* __restrict__ count, uint64_t cap_rows,
     const uint32_t* __restrict__ row_map, uint32_t vpr, V* __restrict__ out) {
@@ -56,25 +63,25 @@ void launch_gather(const void* table, int vec_bytes, uint64_t row_bytes, const u
                    const unsigned long long* count, uint64_t cap_rows, const uint32_t* row_map,
                    void* out, cudaStream_t st) {
   const uint32_t vpr = static_cast<uint32_t>(row_bytes / vec_bytes);
-  const int grid = kNumSMs * 8;
+  const int grid = kNumSMs * kGatherCtasPerSM;
   switch (vec_bytes) {
     case 16:
-      launch_k(gather_kernel<uint4, 4>, grid, 256, st, static_cast<const uint4*>(table), ids,
+      launch_k(gather_kernel<uint4, gather_unroll<uint4>()>, grid, 256, st, static_cast<const uint4*>(table), ids,
                                                    count, cap_rows, row_map, vpr,
                                                    static_cast<uint4*>(out));
       break;
     case 8:
-      launch_k(gather_kernel<uint2, 4>, grid, 256, st, static_cast<const uint2*>(table), ids,
+      launch_k(gather_kernel<uint2, gather_unroll<uint2>()>, grid, 256, st, static_cast<const uint2*>(table), ids,
                                                    count, cap_rows, row_map, vpr,
                                                    static_cast<uint2*>(out));
       break;
     case 4:
-      launch_k(gather_kernel<uint32_t, 4>, grid, 256, st, static_cast<const uint32_t*>(table),
+      launch_k(gather_kernel<uint32_t, gather_unroll<uint32_t>()>, grid, 256, st, static_cast<const uint32_t*>(table),
                                                        ids, count, cap_rows, row_map, vpr,
                                                        static_cast<uint32_t*>(out));
       break;
     default:
-      launch_k(gather_kernel<unsigned short, 4>, grid, 256, st, 
+      launch_k(gather_kernel<unsigned short, gather_unroll<unsigned short>()>, grid, 256, st, 
           static_cast<const unsigned short*>(table), ids, count, cap_rows, row_map, vpr,
           static_cast<unsigned short*>(out));
   }

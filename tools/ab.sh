@@ -7,6 +7,6 @@ for r in $(seq 1 $ROUNDS); do
   for v in "$@"; do
     n=$(basename $v)
     if [ "$v" = "-" ]; then n=tree; lib=""; else lib=$(pwd)/$v/libcoopbatch_b200.so; fi
-    CB_LIB_PATH=$lib timeout 300 python bench.py --no-cpu-baseline --no-evidence > $OUT/${n}_$r.json 2> $OUT/${n}_$r.err
+    CB_LIB_PATH=$lib timeout 600 python bench.py --no-cpu-baseline --no-evidence ${BENCH_ARGS:-} > $OUT/${n}_$r.json 2> $OUT/${n}_$r.err
   done
 done
