@@ -393,6 +393,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
     const uint64_t th = th_of(cur);
     const uint64_t T = plain_bound(th);
     const uint32_t di = di_of(cur);
+    uint2* const st_lane = stage + lane;  // kept position j -> st_lane[32 j]
     uint32_t tv[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) tv[j] = __ldg(row + j * 32);
@@ -404,7 +405,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
       if (lane == j) my_word = bal;
       if (keep) {
         set_bit(a.bits, a.summ, tv[j]);
-        stage[j * 32 + lane] = make_uint2(tv[j], di);
+        st_lane[j * 32] = make_uint2(tv[j], di);
       }
     }
   } else {
