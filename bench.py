@@ -786,7 +786,7 @@ def run_ours(args, cfg):
                 "h2d_bytes_per_step": b * 4 + 40, "d2h_bytes_per_step": int(mb.value),
                 "device_ms": e2e_ms},
         "roofline": {"bound": "hbm",
-                     "kernel": "gather_kernel<V,4> (16/8/4/2-byte vectors by row size)",
+                     "kernel": "gather_kernel<V,U> (16/8/4/2-byte vectors by row size; U = 3 for 16-byte, else 4)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic("gather", cfg["dim"]),
