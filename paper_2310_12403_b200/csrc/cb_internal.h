@@ -264,7 +264,14 @@ struct RelabelArgs {  // edges == nullptr disables
 
 constexpr int kExtractTileWords = 2048;  // bitmap padding granule (max tile)
 constexpr uint64_t kExtractBigWords = 256 * 1024;  // summary-mode threshold
-constexpr int kLaborTile = 2048;
+#ifndef CB_MARK_NT
+#define CB_MARK_NT 128
+#endif
+#ifndef CB_MARK_IPT
+#define CB_MARK_IPT 8
+#endif
+constexpr int kMarkNT = CB_MARK_NT;                // labor_mark block size
+constexpr int kLaborTile = kMarkNT * CB_MARK_IPT;  // scan positions per mark tile
 constexpr uint64_t kVtabMaxVerts = 1ULL << 26;  // smoothed variate table cap (512 MiB)
 constexpr int kFrontierTile = 1024;
 

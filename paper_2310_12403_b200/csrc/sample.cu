@@ -34,7 +34,10 @@ constexpr int kNT = 256;
 constexpr uint32_t kTileExact = 0x80000000u;
 // labor_mark residency: 4 CTAs/SM so one CTA's staging barrier overlaps
 // another's hashing
-constexpr int kMarkCtasPerSM = 4;
+#ifndef CB_MARK_CTAS
+#define CB_MARK_CTAS (1024 / CB_MARK_NT)
+#endif
+constexpr int kMarkCtasPerSM = CB_MARK_CTAS;
 
 __device__ __forceinline__ unsigned inv_epoch(const unsigned* ep, int slot) {
   return ((*ep & 0x3ffffu) << 6) | static_cast<unsigned>(slot);
@@ -455,10 +458,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // per-tile barrier no longer waits on a chain of global loads.
 template <int IPT, bool SMOOTH>
 __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, unsigned ncta) {
-  constexpr int TILE = kNT * IPT;
+  constexpr int TILE = kMarkNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
   constexpr uint32_t WSPAN = 32 * IPT;  // contiguous positions owned by one warp
-  constexpr int kRecs = 512;            // records staged in smem (else global path)
+  constexpr int kRecs = kLaborTile / 4;  // records staged in smem (else global path)
   __shared__ __align__(16) ActRec s_act[2][kRecs];
   LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
@@ -478,7 +481,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
     if (nd <= static_cast<uint32_t>(kRecs)) {
       const char* src = reinterpret_cast<const char*>(a.act + a0);
       char* dst = reinterpret_cast<char*>(s_act[buf]);
-      for (uint32_t i = threadIdx.x; i < 2 * nd; i += kNT) cp_async16(dst + 16 * i, src + 16 * i);
+      for (uint32_t i = threadIdx.x; i < 2 * nd; i += kMarkNT) cp_async16(dst + 16 * i, src + 16 * i);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -544,7 +547,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
 }
 
 template <int IPT, bool SMOOTH>
-__global__ void __launch_bounds__(kNT, kMarkCtasPerSM) labor_mark_kernel(LaborArgs a) {
+__global__ void __launch_bounds__(kMarkNT, kMarkCtasPerSM) labor_mark_kernel(LaborArgs a) {
   pdl_begin();
   mark_body<IPT, SMOOTH>(a, blockIdx.x, gridDim.x);
 }
@@ -1104,7 +1107,8 @@ __global__ void clear_kernel(uint32_t* bits, uint32_t* summ, const uint32_t* __r
 }
 
 constexpr int kFrontierIPT = 4;
-constexpr int kLaborIPT = kLaborTile / kNT;
+constexpr int kLaborIPT = kLaborTile / kNT;      // NS reservoir tiles
+constexpr int kMarkIPT = kLaborTile / kMarkNT;   // labor_mark
 
 }  // namespace
 
@@ -1159,8 +1163,8 @@ void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStrea
     CB_LAUNCH("vtab");
   }
   const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, kMarkCtasPerSM);
-  if (smooth && a.kind != 0) launch_k(labor_mark_kernel<kLaborIPT, true>, grid, kNT, st, a);
-  else launch_k(labor_mark_kernel<kLaborIPT, false>, grid, kNT, st, a);
+  if (smooth && a.kind != 0) launch_k(labor_mark_kernel<kMarkIPT, true>, grid, kMarkNT, st, a);
+  else launch_k(labor_mark_kernel<kMarkIPT, false>, grid, kMarkNT, st, a);
   CB_LAUNCH("labor_mark");
 }
 
