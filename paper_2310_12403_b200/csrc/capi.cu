@@ -12,10 +12,13 @@ thread_local std::string cb::capi::g_err;
 
 namespace cb {
 std::atomic<unsigned long long> g_kernel_launches{0};
+// Off by default: with 8 batches in flight the early-launched (waiting) CTAs
+// of the next kernel take SM slots from the other batches' kernels
+// (65.4 vs 67.4 us/step at c2, latency 148 vs 150 us). CB_PDL=1 enables it.
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("CB_PDL");
-    return !(e && std::atoi(e) == 0);
+    return e && std::atoi(e) != 0;
   }();
   return on;
 }
