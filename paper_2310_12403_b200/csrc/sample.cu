@@ -461,7 +461,10 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   constexpr int TILE = kMarkNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
   constexpr uint32_t WSPAN = 32 * IPT;  // contiguous positions owned by one warp
-  constexpr int kRecs = kLaborTile / 4;  // records staged in smem (else global path)
+#ifndef CB_MARK_RECS
+#define CB_MARK_RECS (kLaborTile / 4)
+#endif
+  constexpr int kRecs = CB_MARK_RECS;  // records staged in smem (else global path)
   __shared__ __align__(16) ActRec s_act[2][kRecs];
   LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
