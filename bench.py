@@ -383,6 +383,28 @@ def batch_sweep_evidence(cb, dev, batches=(1024, 4096, 16384, 65536), steps=10):
     return out
 
 
+def mark_roofline(prof_ms, prof_sizes, L, scfg, peak):
+    """The largest sampling launch: labor_mark of the last layer, from the
+    profiling replay of the captured batch (event nodes between launches, L2
+    flushed before the replay). Algorithmic bytes per launch: 4 B per scanned
+    position (the neighbour id), 4 B per 32 positions (keep word), 8 B per kept
+    edge (staged pair). The kernel is bound by the SplitMix64 issue rate, not
+    by HBM: hbm_frac says how far from the byte roofline it runs."""
+    import math as _m
+    if int(scfg.kind) != 2 or len(prof_ms) != 3 * L + 3:
+        return None
+    i = 3 * (L - 1) + 2
+    s = prof_sizes[L - 1]
+    nbytes = 4 * s["scan_total"] + 4 * _m.ceil(s["scan_total"] / 32) + 8 * s["n_edges"]
+    t = prof_ms[i] / 1e3
+    return {"kernel": "labor_mark_kernel (last layer)", "bound": "issue (SplitMix64 per position)",
+            "ms": prof_ms[i], "positions": s["scan_total"], "kept": s["n_edges"],
+            "positions_per_s": s["scan_total"] / t, "bytes_per_launch": nbytes,
+            "achieved": nbytes / t / 1e9, "peak": peak, "unit": "GB/s",
+            "hbm_frac": nbytes / t / 1e9 / peak,
+            "share_of_batch": prof_ms[i] / sum(prof_ms)}
+
+
 # ------------------------------------------------------ work curves (f4) ---
 def work_curve_evidence(cb, dev, cpu: bool, trials=50, layers=3, seed=49):
     """Acceptance criteria 2-3 (acceptance.cpp:137-192): E|S^3| against batch
@@ -752,6 +774,7 @@ def run_ours(args, cfg):
     # per-launch breakdown inside the CUDA graph (event-record nodes), L2 flushed
     flush_l2()
     prof_ms = plan.graph_profile(step_ptr(W), scheds[W])
+    prof_sizes = [plan.layer_sizes(0, l) for l in range(L)]
     if rank != 0:
         return
     seeds_total = K * b * world
@@ -791,6 +814,7 @@ def run_ours(args, cfg):
                      "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic("gather", cfg["dim"]),
                      "bytes_per_launch": gather_bytes},
+        "roofline_sampling": mark_roofline(prof_ms, prof_sizes, L, scfg, peaks()[0]),
         "gpu_launches": launches_per_step * K,
         "kernel_ms_graph": [round(x, 4) for x in prof_ms],
         "evidence": {"per_layer": sizes,
