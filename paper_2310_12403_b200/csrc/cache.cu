@@ -505,32 +505,22 @@ void DeviceLru::access_ordered(const uint32_t* d_keys, uint64_t B, uint8_t* d_mi
 
 void DeviceLru::access_trace(const uint32_t* keys, uint64_t n, uint8_t* miss, cudaStream_t st) {
   for (uint64_t i = 0; i < n; ++i) require(keys[i] < n_, "LruCache: key outside the key space");
-  uint32_t* d_keys = nullptr;
-  uint8_t* d_miss = nullptr;
-  CB_CUDA(cudaMalloc(&d_keys, n * 4 + 16));
-  CB_CUDA(cudaMalloc(&d_miss, n + 16));
+  DevBuf b_keys(n * 4 + 16), b_miss(n + 16);
+  uint32_t* d_keys = b_keys.as<uint32_t>();
+  uint8_t* d_miss = b_miss.as<uint8_t>();
   CB_CUDA(cudaMemcpy(d_keys, keys, n * 4, cudaMemcpyHostToDevice));
-  std::vector<uint32_t> seen_at;  // run-local dedup: key -> run stamp
   std::vector<uint8_t> in_run;
   in_run.assign(n_, 0);
   uint64_t start = 0;
-  try {
-    while (start < n) {
-      uint64_t end = start;
-      while (end < n && !in_run[keys[end]]) in_run[keys[end++]] = 1;
-      run_batch(d_keys + start, nullptr, end - start, d_miss + start, nullptr, st);
-      for (uint64_t i = start; i < end; ++i) in_run[keys[i]] = 0;
-      start = end;
-    }
-    CB_CUDA(cudaMemcpyAsync(miss, d_miss, n, cudaMemcpyDeviceToHost, st));
-    CB_CUDA(cudaStreamSynchronize(st));
-  } catch (...) {
-    cudaFree(d_keys);
-    cudaFree(d_miss);
-    throw;
+  while (start < n) {
+    uint64_t end = start;
+    while (end < n && !in_run[keys[end]]) in_run[keys[end++]] = 1;
+    run_batch(d_keys + start, nullptr, end - start, d_miss + start, nullptr, st);
+    for (uint64_t i = start; i < end; ++i) in_run[keys[i]] = 0;
+    start = end;
   }
-  cudaFree(d_keys);
-  cudaFree(d_miss);
+  CB_CUDA(cudaMemcpyAsync(miss, d_miss, n, cudaMemcpyDeviceToHost, st));
+  CB_CUDA(cudaStreamSynchronize(st));
 }
 
 uint64_t DeviceLru::size() const { return std::min(cap_, distinct_); }

@@ -226,22 +226,17 @@ void check_ownership_host(const cb_plan* pl, const uint32_t* flat, const uint64_
   std::vector<uint32_t> owners(total);
   std::vector<uint32_t> seeds(flat, flat + total);
   // gather owner[seed] on the device: tiny (one value per seed)
-  uint32_t* d_ids = nullptr;
-  uint32_t* d_out = nullptr;
-  CB_CUDA(cudaMalloc(&d_ids, total * 4 + 4));
-  CB_CUDA(cudaMalloc(&d_out, total * 4 + 4));
+  DevBuf b_ids(total * 4 + 4), b_out(total * 4 + 4), b_cnt(8);
+  uint32_t* d_ids = b_ids.as<uint32_t>();
+  uint32_t* d_out = b_out.as<uint32_t>();
   CB_CUDA(cudaMemcpy(d_ids, seeds.data(), total * 4, cudaMemcpyHostToDevice));
   // reuse the feature gather kernel with a 4-byte "row" = owner[v]
-  unsigned long long* d_cnt = nullptr;
-  CB_CUDA(cudaMalloc(&d_cnt, 8));
+  unsigned long long* d_cnt = b_cnt.as<unsigned long long>();
   const unsigned long long t = total;
   CB_CUDA(cudaMemcpy(d_cnt, &t, 8, cudaMemcpyHostToDevice));
   launch_gather(pl->pm->owner, 4, 4, d_ids, d_cnt, total, nullptr, d_out, pl->stream);
   CB_CUDA(cudaStreamSynchronize(pl->stream));
   CB_CUDA(cudaMemcpy(owners.data(), d_out, total * 4, cudaMemcpyDeviceToHost));
-  cudaFree(d_ids);
-  cudaFree(d_out);
-  cudaFree(d_cnt);
   for (uint32_t p = 0; p < pl->P; ++p)
     for (uint64_t i = off[p]; i < off[p + 1]; ++i)
       if (owners[i] != p)
@@ -838,11 +833,12 @@ static void finish_partition(cb_partition* pm) {
   cub::DoubleBuffer<uint32_t> kb(keys, keys2), vb(ids, pm->members);
   size_t tmp_bytes = 0;
   CB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, (int64_t)n, 0, bits, st));
-  void* tmp = nullptr;
-  CB_CUDA(cudaMalloc(&tmp, tmp_bytes + 16));
-  CB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kb, vb, (int64_t)n, 0, bits, st));
-  CB_CUDA(cudaStreamSynchronize(st));
-  cudaFree(tmp);
+  {
+    DevBuf tmp(tmp_bytes + 16);
+    CB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.as<void>(), tmp_bytes, kb, vb, (int64_t)n, 0,
+                                            bits, st));
+    CB_CUDA(cudaStreamSynchronize(st));
+  }
   std::vector<uint32_t> members(n), sorted_keys(n);
   CB_CUDA(cudaMemcpy(members.data(), vb.Current(), n * 4, cudaMemcpyDeviceToHost));
   CB_CUDA(cudaMemcpy(sorted_keys.data(), kb.Current(), n * 4, cudaMemcpyDeviceToHost));

@@ -98,18 +98,11 @@ int cb_cache_access_host_ids(cb_cache* c, const uint32_t* ids, uint64_t n, uint6
     require(c != nullptr && (n == 0 || ids != nullptr), "null argument");
     require(pm == nullptr || part < pm->parts, "part index out of range");
     DeviceGuard dg(c->lru->device());
-    uint32_t* d = nullptr;
-    CB_CUDA(cudaMalloc(&d, n * 4 + 16));
-    uint64_t k = 0;
-    try {
-      CB_CUDA(cudaMemcpy(d, ids, n * 4, cudaMemcpyHostToDevice));
-      k = c->lru->access_ids(d, n, order_key, pm ? pm->owner : nullptr, part, CacheGatherSrc{},
-                             c->stream);
-    } catch (...) {
-      cudaFree(d);
-      throw;
-    }
-    cudaFree(d);
+    DevBuf buf(n * 4 + 16);
+    uint32_t* d = buf.as<uint32_t>();
+    CB_CUDA(cudaMemcpy(d, ids, n * 4, cudaMemcpyHostToDevice));
+    const uint64_t k = c->lru->access_ids(d, n, order_key, pm ? pm->owner : nullptr, part,
+                                          CacheGatherSrc{}, c->stream);
     if (kept) *kept = k;
   });
 }

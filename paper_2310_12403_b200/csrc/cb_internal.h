@@ -40,6 +40,24 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define CB_CUDA(x) ::cb::cuda_check((x), #x)
 #define CB_LAUNCH(what) ::cb::cuda_check(cudaGetLastError(), what)
 
+// Scoped device allocation, freed on every exit path (exceptions included).
+class DevBuf {
+ public:
+  explicit DevBuf(size_t bytes) { cuda_check(cudaMalloc(&p_, bytes), "cudaMalloc"); }
+  ~DevBuf() {
+    if (p_) cudaFree(p_);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p_);
+  }
+
+ private:
+  void* p_ = nullptr;
+};
+
 inline void require(bool ok, const char* msg) {
   if (!ok) throw Error(kInput, msg);
 }
