@@ -145,6 +145,14 @@ int cb_sample(cb_plan* plan, int mode, const uint32_t* seeds_flat, const uint64_
               const cb_sched* sched);
 int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
                    const uint64_t* seeds_off, const cb_sched* sched);
+/* sample_labor0 / labor_block (samplers.cpp:89-104, 305-312) with the
+ * caller's variate r(t) instead of the hash stream: table[t] for every vertex
+ * t (num_vertices doubles, host or device memory; copied). While a table is
+ * set, every LABOR layer of the plan keeps t -> s iff table[t] <= (double)k /
+ * (double)d_s, the reference's comparison, with no keep-all shortcut for
+ * d_s <= k (a caller variate may exceed 1). NULL restores the schedule's
+ * stream. LABOR-0 plans only; drops captured graphs. */
+int cb_plan_set_variate_table(cb_plan* plan, const double* table, int on_device);
 /* P independent expansions in one batch, part p under its own schedule
  * scheds[p] (indep mode; all schedules plain or all smoothed). This is the
  * trial loop of work_curve (analysis.cpp:78-124: a fresh plain stream

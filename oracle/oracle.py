@@ -152,6 +152,7 @@ def lib(impl: str = "restated") -> C.CDLL:
         L.rf_partition_random.argtypes = [_u64, _u32, _u64, _P]
         L.rf_sample_block.argtypes = [_P, _P, _u64, C.c_int, _u32, C.POINTER(Sched),
                                       C.c_int, C.POINTER(Block)]
+        L.rf_sample_labor0.argtypes = [_P, _P, _u64, _u32, _P, C.c_int, C.POINTER(Block)]
         L.rf_expand.argtypes = [_P, _P, _u64, C.c_int, C.c_int, _P, C.POINTER(Sched),
                                 C.POINTER(Stack)]
         L.rf_coop_sample.argtypes = [_P, _P, _u32, _P, _P, C.c_int, C.c_int, _u32,
@@ -349,6 +350,18 @@ def edge_pred_seeds_reference(g: CSR, edges, epoch_seed: int) -> np.ndarray:
     _check(rg.L.rf_edge_pred_seeds(rg.h, _ptr(uv), len(uv), epoch_seed, _ptr(out),
                                    C.byref(n)), rg.L)
     return out[: n.value]
+
+
+def sample_labor0_reference(g: CSR, seeds, k: int, table, layer: int = 0) -> dict:
+    """The reference's sample_labor0 (samplers.cpp:305-312) with r(t) = table[t]."""
+    rg = RefGraph(g)
+    sd = np.ascontiguousarray(seeds, dtype=np.uint32)
+    tb = np.ascontiguousarray(table, dtype=np.float64)
+    b = Block()
+    _check(rg.L.rf_sample_labor0(rg.h, _ptr(sd), len(sd), k, _ptr(tb), layer, C.byref(b)), rg.L)
+    out = _block(b)
+    rg.L.rf_block_free(C.byref(b))
+    return out
 
 
 def work_curve_reference(g: CSR, kind: int, fanout: int, sizes, trials: int, num_layers: int,

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -281,6 +282,15 @@ int rf_sample_block(void* g, const uint32_t* seeds, uint64_t n_seeds, int kind,
     to_block(sample_block(*static_cast<Graph*>(g), {seeds, n_seeds},
                           to_cfg(kind, fanout), src, layer),
              out);
+  });
+}
+
+/* sample_labor0 (samplers.cpp:305-312) with the variate r(t) = table[t]. */
+int rf_sample_labor0(void* g, const uint32_t* seeds, uint64_t n_seeds, uint32_t k,
+                     const double* table, int layer, ob_block* out) {
+  return guard([&] {
+    const std::function<double(VertexId)> variate = [table](VertexId t) { return table[t]; };
+    to_block(sample_labor0(*static_cast<Graph*>(g), {seeds, n_seeds}, k, variate, layer), out);
   });
 }
 

@@ -555,6 +555,32 @@ def sample_ns(g: Graph, seeds, k: int, epoch_seed: int) -> BipartiteBlock:
                   SeedSchedule.plain(epoch_seed)).blocks[0]
 
 
+def sample_labor0(g: Graph, seeds, k: int, variate, layer: int = 0) -> BipartiteBlock:
+    """samplers.cpp:305-312 (labor_block, samplers.cpp:89-104): LABOR-0 with a
+    caller variate r(t): keep t -> s iff r(t) <= k / d_s. `variate` is a
+    callable VertexId -> float (evaluated once per distinct neighbour of the
+    seeds, on the host) or an array of num_vertices floats. The block is
+    sampled on the GPU from that table (cb_plan_set_variate_table)."""
+    if k < 1:
+        raise InputError("sample_labor0: fanout must be >= 1")
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint32)
+    n = g.num_vertices
+    if callable(variate):
+        table = np.zeros(n, np.float64)
+        for t in sample_full(g, seeds).src_vertices.tolist():
+            table[t] = float(variate(t))
+    else:
+        table = np.ascontiguousarray(variate, dtype=np.float64)
+        if table.shape != (n,):
+            raise InputError("sample_labor0: variate table must hold one value per vertex")
+    pl = Plan(g, None, 1, SamplerConfig(SamplerKind.kLabor0, k), max(len(seeds), 1))
+    _check(_lib.load().cb_plan_set_variate_table(pl._h, _ptr(table), 0))
+    pl.sample([seeds], SeedSchedule.plain(0), MODE_INDEP)
+    b = pl.block(0, 0)
+    b.layer = layer
+    return b
+
+
 def sample_rw(g: Graph, seeds, cfg: SamplerConfig, epoch_seed: int) -> BipartiteBlock:
     """samplers.cpp:314-321 (layer 0): random walks with restart, top-k visits."""
     if cfg.rw_length < 1 or cfg.rw_walks < 1:

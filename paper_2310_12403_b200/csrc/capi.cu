@@ -167,6 +167,12 @@ void plan_alloc(cb_plan* pl) {
   CB_CUDA(cudaDeviceSynchronize());
 }
 
+// The smoothed (FP64 threshold) kernel path: a smoothing schedule, or the
+// caller's variate table of cb_plan_set_variate_table.
+bool smooth_of(const cb_plan* pl, const cb_sched* s) {
+  return pl->ext_vtab != nullptr || (s->kappa != cbdev::kKappaInf && s->kappa >= 2);
+}
+
 Variates make_variates(const cb_sched* s) {
   // VariateSource::from_schedule (samplers.hpp:75-93): cos/sin on the host,
   // exact 1/0 at the endpoints.
@@ -195,7 +201,10 @@ Variates make_variates(const cb_sched* s) {
 // schedule per part (cb_sample_multi).
 void upload_variates(cb_plan* pl, const cb_sched* s, uint32_t n_sched, cudaStream_t st) {
   std::vector<Variates> v(pl->P);
-  for (uint32_t p = 0; p < pl->P; ++p) v[p] = make_variates(s + (n_sched > 1 ? p : 0));
+  for (uint32_t p = 0; p < pl->P; ++p) {
+    v[p] = make_variates(s + (n_sched > 1 ? p : 0));
+    if (pl->ext_vtab) v[p].smoothed = 2;  // caller variate table (sample_labor0)
+  }
   CB_CUDA(cudaMemcpyAsync(pl->var, v.data(), sizeof(Variates) * pl->P, cudaMemcpyHostToDevice,
                           st));  // pageable source: staged before the call returns
 }
@@ -373,8 +382,8 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
   la.slots = b.slots;
   la.keep_words = w.sync.keep_words;
   la.stage = w.sync.stage;
-  la.vtab = w.sync.vtab;
-  la.n_vert = pl->g->g.n;
+  la.vtab = pl->ext_vtab ? pl->ext_vtab : w.sync.vtab;
+  la.n_vert = pl->ext_vtab ? 0 : pl->g->g.n;  // 0: the table is always used, never rebuilt
   la.cap_edges = b.cap_edges;
   la.ticket = w.sync.tickets + 3 * l + 1;
   la.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l + 1;
@@ -462,7 +471,7 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
     }
   }
   const bool coop = (mode == CB_MODE_COOP) && P > 1;
-  const bool smooth = sched->kappa != cbdev::kKappaInf && sched->kappa >= 2;
+  const bool smooth = smooth_of(pl, sched);
   pl->smooth = smooth;
   // during capture the graph must clear what a batch of its own mode leaves
   const int dm = capturing ? mode : pl->dirty_mode;
@@ -1072,6 +1081,27 @@ int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
   });
 }
 
+int cb_plan_set_variate_table(cb_plan* plan, const double* table, int on_device) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require(plan->kind == CB_LABOR0 || table == nullptr,
+            "a variate table applies to LABOR-0 plans only");
+    require(plan->dist_world == 0, "variate tables are not supported on distributed plans");
+    DeviceGuard dg(plan->device);
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    plan->drop_graphs();  // captured batches baked the previous variate mode in
+    if (!table) {
+      if (plan->ext_vtab) cudaFree(plan->ext_vtab);
+      plan->ext_vtab = nullptr;
+      return;
+    }
+    const uint64_t n = plan->g->g.n;
+    if (!plan->ext_vtab) CB_CUDA(cudaMalloc(&plan->ext_vtab, std::max<uint64_t>(n, 1) * 8));
+    CB_CUDA(cudaMemcpy(plan->ext_vtab, table, n * 8,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  });
+}
+
 int cb_sample_multi(cb_plan* plan, const uint32_t* seeds_flat, const uint64_t* seeds_off,
                     const cb_sched* scheds) {
   NvtxRange nvtx_("cb.sample_multi");
@@ -1186,7 +1216,7 @@ int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_devic
     if (what & 1) {
       require(sched != nullptr, "null schedule");
       require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
-      const bool sm = sched->kappa != cbdev::kKappaInf && sched->kappa >= 2;
+      const bool sm = smooth_of(plan, sched);
       require(sm == plan->cap_smooth,
               "schedule smoothing differs from the captured batch (re-capture)");
       const uint64_t total = plan->cap_off[plan->P];
@@ -1457,7 +1487,7 @@ int cb_plan_sample_layer(cb_plan* plan, int layer, const uint32_t* d_dst, uint64
       plan->seeds_off.assign({0, n_dst});
       plan->mode = CB_MODE_COOP;
     }
-    const bool smooth = sched->kappa != cbdev::kKappaInf && sched->kappa >= 2;
+    const bool smooth = smooth_of(plan, sched);
     launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);
     const RelabelArgs none{};
     enqueue_layer(plan, w, 0, layer, D, cap, n_dst, w.bm[0], none, 0, smooth,

@@ -204,6 +204,7 @@ struct cb_plan {
   LayerMeta* meta = nullptr;                // [P*(L+1)]
   unsigned long long* send_counts = nullptr;  // [L*P*P]
   Variates* var = nullptr;
+  double* ext_vtab = nullptr;  // caller variate table r_t (sample_labor0), n entries
   uint32_t* seeds = nullptr;
   uint64_t seeds_cap = 0;
   int mode = -1;          // mode of the last batch
@@ -255,6 +256,7 @@ struct cb_plan {
     for (cudaStream_t s : part_st) cudaStreamDestroy(s);
     for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ext_vtab) cudaFree(ext_vtab);
   }
 
   LayerMeta* meta_at(uint32_t p, int l) { return meta + p * (L + 1) + l; }
@@ -267,6 +269,7 @@ namespace cb {
 namespace capi {
 // capi.cu helpers shared with the other C-ABI translation units
 Variates make_variates(const cb_sched* s);
+bool smooth_of(const cb_plan* pl, const cb_sched* s);
 void upload_variates(cb_plan* pl, const cb_sched* s, uint32_t n_sched, cudaStream_t st);
 ExtractArgs extract_args(PeWork& w, const Bitmap& bm, const Bitmap* zero_bm, uint32_t* out,
                          uint64_t cap, unsigned long long* c1, unsigned long long* c2,

@@ -116,7 +116,7 @@ int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seed
       plan->seeds_off.assign({0, n_seeds});
       plan->mode = CB_MODE_COOP;
     }
-    const bool smooth = sched->kappa != cbdev::kKappaInf && sched->kappa >= 2;
+    const bool smooth = smooth_of(plan, sched);
     const int s = static_cast<int>(px.layer_ctr++ & 1);
     px.slot_of[layer] = s;
     launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);

@@ -210,7 +210,8 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
               for (uint32_t r2 = 0; r2 < k; ++r2) a.slots[eo + r2] = r2;
           } else {
             rec.a = rs[j] - eq;          // indices[rec.a + x] = neighbour at x
-            if (full || d <= k) {
+            // (a caller variate table may hold values > 1: no keep-all shortcut)
+            if (full || (d <= k && v.smoothed != 2)) {
               rec.b = ~0ULL;
             } else {
               const double thr = __ddiv_rn(static_cast<double>(k), static_cast<double>(d));
@@ -1161,7 +1162,7 @@ void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_d
 }
 
 void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStream_t st) {
-  if (smooth && a.kind != 0 && a.vtab) {
+  if (smooth && a.kind != 0 && a.vtab && a.n_vert) {
     launch_k(vtab_kernel, grid_for(a.n_vert, kNT, 8), kNT, st, a);
     CB_LAUNCH("vtab");
   }

@@ -499,3 +499,39 @@ def test_repeated_seeds_beyond_edge_count(powerlaw):
         got = cb.expand(g, seeds, 2, cb.SamplerConfig(kind, 4), sched)
         want = O.expand(ref, seeds, 2, okind, 4, osched(sched))
         assert_stack_eq(got, want, f"repeated {kind.name}")
+
+
+def test_sample_labor0_caller_variate(powerlaw):
+    """sample_labor0 with a caller variate (samplers.cpp:89-104, 305-312): the
+    GPU block from the variate table equals the compiled reference's, with
+    values exactly at k/d (inclusive), above 1 for low-degree dsts (rejected:
+    no keep-all shortcut) and NaN (rejected)."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    g, ref = powerlaw
+    n = ref.n
+    rng = np.random.default_rng(11)
+    table = rng.random(n)
+    deg = np.diff(ref.indptr.astype(np.int64))
+    k = 4
+    seeds = rng.choice(n, 300, replace=False).astype(np.uint32)
+    # exact thresholds: the first neighbour of some dsts gets r = k / d
+    for s in seeds[:40]:
+        d = int(deg[s])
+        if d:
+            table[ref.indices[ref.indptr[s]]] = k / d
+    table[rng.choice(n, 50, replace=False)] = 1.5
+    table[rng.choice(n, 20, replace=False)] = np.nan
+    for layer in (0, 2):
+        got = cb.sample_labor0(g, seeds, k, table, layer)
+        want = O.sample_labor0_reference(ref, seeds, k, table, layer)
+        d = got.as_dict()
+        for key in ("dst", "src", "edges", "dst_pos"):
+            assert np.array_equal(d[key], want[key]), key
+        assert got.layer == layer
+    via_callable = cb.sample_labor0(g, seeds, k, lambda t: table[t])
+    assert np.array_equal(via_callable.edges, got.edges)
+    with pytest.raises(cb.InputError):
+        cb.sample_labor0(g, seeds, 0, table)
+    with pytest.raises(cb.InputError):
+        cb.sample_labor0(g, seeds, k, table[:-1])
