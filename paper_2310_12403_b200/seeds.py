@@ -50,6 +50,20 @@ def draw_from_pool(pool: np.ndarray, count: int, seed: int, tag: int) -> np.ndar
     return pool[first_distinct(hash_bits(seed, [8, tag]), len(pool), count).astype(np.int64)]
 
 
+def draw_batch(num_vertices: int, count: int, seed: int) -> np.ndarray:
+    """acceptance.cpp:71-83: `count` distinct vertices from the stream
+    hash_uniform(seed, {31337, attempt}) (the acceptance harness's global batch)."""
+    return first_distinct(hash_bits(seed, [31337]), num_vertices, count).astype(np.uint32)
+
+
+def split_by_owner(batch, owner: np.ndarray, parts: int) -> list[np.ndarray]:
+    """acceptance.cpp:64-69: a global batch split into per-part seed lists by
+    owner, batch order kept within a part."""
+    b = np.asarray(batch, dtype=np.uint32)
+    own = np.asarray(owner)[b]
+    return [b[own == p] for p in range(parts)]
+
+
 def coop_seeds(members: list[np.ndarray], b: int, seed: int, step: int) -> list[np.ndarray]:
     """Per-part seeds of one cooperative step (cli.cpp:210-214)."""
     return [draw_from_pool(members[p], b, seed, hash_bits(step, [p]))

@@ -196,3 +196,22 @@ def test_concavity_check_matches_reference():
         assert [e.violation for e in rep.entries] == vio.tolist()
     with pytest.raises(InputError):
         concavity_check(WorkCurve(3, [WorkCurvePoint(1), WorkCurvePoint(2)]))
+
+
+def test_draw_batch_and_split_by_owner():
+    """acceptance.cpp:64-83 restated: draw_batch's {31337, attempt} rejection
+    stream and split_by_owner's order-preserving split."""
+    from paper_2310_12403_b200.coopbatch import hash_uniform
+    from paper_2310_12403_b200.seeds import draw_batch, split_by_owner
+    for n, count, seed in [(2000, 128, 17), (10, 10, 3), (5, 1, 0)]:
+        want, seen, a = [], set(), 0
+        while len(want) < count:
+            v = min(int(hash_uniform(seed, [31337, a]) * float(n)), n - 1)
+            a += 1
+            if v not in seen:
+                seen.add(v)
+                want.append(v)
+        assert draw_batch(n, count, seed).tolist() == want
+    owner = np.array([0, 1, 1, 0, 2, 2, 1], np.uint32)
+    parts = split_by_owner([6, 0, 4, 1, 3, 5], owner, 3)
+    assert [p.tolist() for p in parts] == [[0, 3], [6, 1], [4, 5]]
