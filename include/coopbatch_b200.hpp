@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <limits>
 #include <memory>
 #include <stdexcept>
@@ -208,6 +209,45 @@ inline LayerStack expand(const Graph& g, const std::vector<VertexId>& seeds, int
   LayerStack st;
   for (int l = 0; l < num_layers; ++l) st.blocks.push_back(detail::download_block(pl.get(), 0, l));
   return st;
+}
+
+// samplers.cpp:323-338: one block of any sampler at layer `layer` (the layer
+// namespaces the variates), on a 1-layer plan whose block hashes as `layer`
+inline BipartiteBlock sample_block(const Graph& g, const std::vector<VertexId>& seeds,
+                                   const SamplerConfig& cfg, const SeedSchedule& schedule,
+                                   int layer) {
+  if (layer < 0) throw InputError("sample_block: layer must be >= 0");
+  auto pl = detail::make_plan(g, nullptr, 1, cfg, seeds.size());
+  check(cb_plan_set_layer_base(pl.get(), layer));
+  const std::uint64_t off[2] = {0, seeds.size()};
+  const cb_sched s = schedule.c();
+  check(cb_sample_sync(pl.get(), CB_MODE_INDEP, seeds.data(), off, &s));
+  BipartiteBlock b = detail::download_block(pl.get(), 0, 0);
+  b.layer = layer;
+  return b;
+}
+
+// samplers.cpp:89-104, 305-312: LABOR-0 with the caller's variate r(t), keep
+// t -> s iff r(t) <= k / d_s. r is evaluated once per vertex on the host and
+// the block is sampled on the GPU from that table.
+inline BipartiteBlock sample_labor0(const Graph& g, const std::vector<VertexId>& seeds,
+                                    std::uint32_t k,
+                                    const std::function<double(VertexId)>& variate,
+                                    int layer = 0) {
+  if (k == 0) throw InputError("sample_labor0: fanout must be >= 1");
+  std::vector<double> table(g.num_vertices());
+  for (std::uint64_t t = 0; t < table.size(); ++t) table[t] = variate(static_cast<VertexId>(t));
+  SamplerConfig cfg;
+  cfg.kind = SamplerKind::kLabor0;
+  cfg.fanout = k;
+  auto pl = detail::make_plan(g, nullptr, 1, cfg, seeds.size());
+  check(cb_plan_set_variate_table(pl.get(), table.data(), 0));
+  const std::uint64_t off[2] = {0, seeds.size()};
+  const cb_sched s{1, 0, 0, 0};
+  check(cb_sample_sync(pl.get(), CB_MODE_INDEP, seeds.data(), off, &s));
+  BipartiteBlock b = detail::download_block(pl.get(), 0, 0);
+  b.layer = layer;
+  return b;
 }
 
 // coop.cpp:108-119

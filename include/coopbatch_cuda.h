@@ -145,6 +145,10 @@ int cb_sample(cb_plan* plan, int mode, const uint32_t* seeds_flat, const uint64_
               const cb_sched* sched);
 int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
                    const uint64_t* seeds_off, const cb_sched* sched);
+/* Block l of the plan hashes as layer l + base: sample_block(g, seeds, cfg,
+ * src, layer) (samplers.hpp:158-160) at any layer is a 1-layer plan with
+ * base = layer. Drops captured graphs. */
+int cb_plan_set_layer_base(cb_plan* plan, int base);
 /* sample_labor0 / labor_block (samplers.cpp:89-104, 305-312) with the
  * caller's variate r(t) instead of the hash stream: table[t] for every vertex
  * t (num_vertices doubles, host or device memory; copied). While a table is

@@ -53,6 +53,7 @@ _SIGS = {
     "cb_sample_sync": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched)]),
     "cb_sample_multi": (C.c_int, [_P, _P, _P, C.POINTER(Sched)]),
     "cb_plan_set_variate_table": (C.c_int, [_P, _P, C.c_int]),
+    "cb_plan_set_layer_base": (C.c_int, [_P, C.c_int]),
     "cb_sample_device": (C.c_int, [_P, C.c_int, _P, _P, C.POINTER(Sched)]),
     "cb_gather": (C.c_int, [_P, _P]),
     "cb_synchronize": (C.c_int, [_P]),

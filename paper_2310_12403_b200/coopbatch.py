@@ -547,12 +547,31 @@ def expand(g: Graph, seeds, num_layers: int, cfg: SamplerConfig,
     return pl.stack(0)
 
 
-def sample_ns(g: Graph, seeds, k: int, epoch_seed: int) -> BipartiteBlock:
-    """samplers.cpp:298-303 (layer 0)."""
+def sample_block(g: Graph, seeds, cfg: SamplerConfig, schedule: SeedSchedule,
+                 layer: int = 0) -> BipartiteBlock:
+    """samplers.cpp:323-338: one block of any sampler at layer `layer` (the
+    layer namespaces the variates): a 1-layer plan whose block hashes as
+    `layer` (cb_plan_set_layer_base)."""
+    if layer < 0:
+        raise InputError("sample_block: layer must be >= 0")
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint32)
+    pl = Plan(g, None, 1, cfg, max(len(seeds), 1))
+    _check(_lib.load().cb_plan_set_layer_base(pl._h, layer))
+    pl.sample([seeds], schedule, MODE_INDEP)
+    b = pl.block(0, 0)
+    b.layer = layer
+    return b
+
+
+def sample_ns(g: Graph, seeds, k: int, epoch_seed: int, layer: int = 0) -> BipartiteBlock:
+    """samplers.cpp:298-303."""
     if k == 0:
         raise InputError("sample_ns: fanout must be >= 1")
-    return expand(g, seeds, 1, SamplerConfig(SamplerKind.kNs, k),
-                  SeedSchedule.plain(epoch_seed)).blocks[0]
+    if layer == 0:
+        return expand(g, seeds, 1, SamplerConfig(SamplerKind.kNs, k),
+                      SeedSchedule.plain(epoch_seed)).blocks[0]
+    return sample_block(g, seeds, SamplerConfig(SamplerKind.kNs, k),
+                        SeedSchedule.plain(epoch_seed), layer)
 
 
 def sample_labor0(g: Graph, seeds, k: int, variate, layer: int = 0) -> BipartiteBlock:
@@ -581,19 +600,23 @@ def sample_labor0(g: Graph, seeds, k: int, variate, layer: int = 0) -> Bipartite
     return b
 
 
-def sample_rw(g: Graph, seeds, cfg: SamplerConfig, epoch_seed: int) -> BipartiteBlock:
-    """samplers.cpp:314-321 (layer 0): random walks with restart, top-k visits."""
+def sample_rw(g: Graph, seeds, cfg: SamplerConfig, epoch_seed: int,
+              layer: int = 0) -> BipartiteBlock:
+    """samplers.cpp:314-321: random walks with restart, top-k visits."""
     if cfg.rw_length < 1 or cfg.rw_walks < 1:
         raise InputError("sample_rw: rw_length and rw_walks must be >= 1")
-    return expand(g, seeds, 1, SamplerConfig(SamplerKind.kRw, cfg.fanout, None, cfg.rw_length,
-                                             cfg.rw_restart, cfg.rw_walks),
-                  SeedSchedule.plain(epoch_seed)).blocks[0]
+    rcfg = SamplerConfig(SamplerKind.kRw, cfg.fanout, None, cfg.rw_length, cfg.rw_restart,
+                         cfg.rw_walks)
+    if layer == 0:
+        return expand(g, seeds, 1, rcfg, SeedSchedule.plain(epoch_seed)).blocks[0]
+    return sample_block(g, seeds, rcfg, SeedSchedule.plain(epoch_seed), layer)
 
 
-def sample_full(g: Graph, seeds) -> BipartiteBlock:
-    """samplers.cpp:289-296 (layer 0)."""
-    return expand(g, seeds, 1, SamplerConfig(SamplerKind.kFull, 1),
-                  SeedSchedule.plain(0)).blocks[0]
+def sample_full(g: Graph, seeds, layer: int = 0) -> BipartiteBlock:
+    """samplers.cpp:289-296."""
+    b = expand(g, seeds, 1, SamplerConfig(SamplerKind.kFull, 1), SeedSchedule.plain(0)).blocks[0]
+    b.layer = layer
+    return b
 
 
 def indep_sample(g: Graph, per_pe_seeds, num_layers: int, cfg: SamplerConfig,

@@ -341,7 +341,7 @@ FrontierArgs frontier_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint
   fa.indptr = pl->g->g.indptr;
   fa.kind = pl->kind;
   fa.k = pl->fanouts[l];
-  fa.layer = l;
+  fa.layer = l + pl->layer_base;
   fa.var = pl->var + p;
   fa.set_bits = set_bm.bits;
   fa.set_summ = set_bm.summ;
@@ -374,7 +374,7 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
   la.indices = pl->g->g.indices;
   la.kind = pl->kind;
   la.k = pl->fanouts[l];
-  la.layer = l;
+  la.layer = l + pl->layer_base;
   la.var = pl->var + p;
   la.bits = set_bm.bits;
   la.summ = set_bm.summ;
@@ -421,7 +421,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
     ra.meta = la.meta;
     ra.indptr = g.indptr;
     ra.indices = g.indices;
-    ra.layer = l;
+    ra.layer = l + pl->layer_base;
     ra.k = pl->fanouts[l];
     ra.walks = pl->rw_walks;
     ra.length = pl->rw_length;
@@ -1078,6 +1078,17 @@ int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
         plan_alloc(plan);
       }
     }
+  });
+}
+
+int cb_plan_set_layer_base(cb_plan* plan, int base) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require(base >= 0, "layer index must be >= 0");
+    DeviceGuard dg(plan->device);
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    plan->drop_graphs();
+    plan->layer_base = base;
   });
 }
 

@@ -205,6 +205,7 @@ struct cb_plan {
   unsigned long long* send_counts = nullptr;  // [L*P*P]
   Variates* var = nullptr;
   double* ext_vtab = nullptr;  // caller variate table r_t (sample_labor0), n entries
+  int layer_base = 0;          // block l hashes as layer l + layer_base (sample_block at any layer)
   uint32_t* seeds = nullptr;
   uint64_t seeds_cap = 0;
   int mode = -1;          // mode of the last batch

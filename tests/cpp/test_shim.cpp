@@ -31,6 +31,10 @@ void rf_features_free(void*);
 int rf_train_step(void*, void*, int, const uint32_t*, uint32_t, const uint32_t*, const uint64_t*,
                   int, int, uint32_t, const ob_sched*, uint32_t, uint64_t, double*, double*);
 int rf_save_csr(void*, const char*);
+int rf_sample_block(void*, const uint32_t*, uint64_t, int, uint32_t, const ob_sched*, int,
+                    ob_block*);
+int rf_sample_labor0(void*, const uint32_t*, uint64_t, uint32_t, const double*, int, ob_block*);
+void rf_block_free(ob_block*);
 }
 
 #include <cmath>
@@ -207,6 +211,31 @@ int main() {
     const auto b = cb::expand(g, seeds, 2, cfg, {1, 5, 5, 0});
     for (int l = 0; l < 2; ++l) CHECK(a.blocks[l].edges == b.blocks[l].edges);
     std::remove(path.c_str());
+  }
+
+  // sample_block at layers > 0 (samplers.cpp:323-338) and sample_labor0 with a
+  // caller variate (samplers.cpp:305-312) == the reference's
+  for (int kind : {CB_NS, CB_LABOR0})
+    for (int layer : {1, 2}) {
+      ob_sched s;
+      rf_sched_make(1, 77, &s);
+      cb::SamplerConfig cfg;
+      cfg.kind = static_cast<cb::SamplerKind>(kind);
+      cfg.fanout = 3;
+      const auto got = cb::sample_block(g, seeds, cfg, {s.kappa, s.z1, s.z2, s.iteration}, layer);
+      ob_block want{};
+      CHECK(rf_sample_block(rg, seeds.data(), seeds.size(), kind, 3, &s, layer, &want) == 0);
+      CHECK(same_block(got, want) && got.layer == layer);
+      rf_block_free(&want);
+    }
+  {
+    std::vector<double> table(n);
+    for (uint64_t t = 0; t < n; ++t) table[t] = std::fmod(0.6180339887 * double(t * t + 3), 1.0);
+    const auto got = cb::sample_labor0(g, seeds, 3, [&](uint32_t t) { return table[t]; }, 1);
+    ob_block want{};
+    CHECK(rf_sample_labor0(rg, seeds.data(), seeds.size(), 3, table.data(), 1, &want) == 0);
+    CHECK(same_block(got, want) && got.layer == 1);
+    rf_block_free(&want);
   }
 
   rf_graph_free(rg);

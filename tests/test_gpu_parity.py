@@ -535,3 +535,30 @@ def test_sample_labor0_caller_variate(powerlaw):
         cb.sample_labor0(g, seeds, 0, table)
     with pytest.raises(cb.InputError):
         cb.sample_labor0(g, seeds, k, table[:-1])
+
+
+@pytest.mark.parametrize("layer", [0, 1, 3])
+@pytest.mark.parametrize("kappa", [1, 4])
+def test_sample_block_any_layer(powerlaw, layer, kappa):
+    """sample_block (samplers.cpp:323-338) at layers > 0: the layer namespaces
+    the variates (LABOR {2, layer}, NS {1, layer, s}, RW {3, layer, ...}); a
+    1-layer plan with a layer base must equal the reference's block."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    g, ref = powerlaw
+    rng = np.random.default_rng(layer + 7 * kappa)
+    seeds = rng.choice(ref.n, 200, replace=False).astype(np.uint32)
+    sched = cb.SeedSchedule.make(kappa, 99)
+    sched = cb.schedule_advance(cb.schedule_advance(sched))  # mid-group: smoothed for kappa 4
+    for kind, okind, k in [(cb.SamplerKind.kLabor0, O.LABOR0, 5), (cb.SamplerKind.kNs, O.NS, 3),
+                           (cb.SamplerKind.kRw, 3, 4)]:
+        got = cb.sample_block(g, seeds, cb.SamplerConfig(kind, k), sched, layer).as_dict()
+        want = O.sample_block(ref, seeds, okind, k, osched(sched), layer, impl="reference")
+        for key in ("dst", "src", "edges", "dst_pos"):
+            assert np.array_equal(got[key], want[key]), (kind, key)
+        assert got["layer"] == layer
+    if kappa == 1:
+        ns = cb.sample_ns(g, seeds, 3, 1234, layer).as_dict()
+        want = O.sample_block(ref, seeds, O.NS, 3, osched(cb.SeedSchedule.plain(1234)), layer,
+                              impl="reference")
+        assert np.array_equal(ns["edges"], want["edges"])
