@@ -518,16 +518,21 @@ class Plan:
         return out
 
 
+# Plans of the reference-style free functions, most recently used last. A plan
+# keeps its graph (and partition) alive, so the cache is bounded.
 _plan_cache: dict = {}
+_PLAN_CACHE_MAX = 16
 
 
 def _plan_for(g: Graph, pm, num_layers: int, cfg: SamplerConfig, n_seeds: int) -> Plan:
     key = (id(g), id(pm) if pm else None, num_layers, int(cfg.kind),
            tuple(cfg.layer_fanouts(num_layers)), cfg.rw_length, cfg.rw_restart, cfg.rw_walks)
-    pl = _plan_cache.get(key)
+    pl = _plan_cache.pop(key, None)
     if pl is None or pl.max_seeds < n_seeds or pl.g is not g or pl.pm is not pm:
         pl = Plan(g, pm, num_layers, cfg, max(n_seeds, 1))
-        _plan_cache[key] = pl
+    _plan_cache[key] = pl
+    while len(_plan_cache) > _PLAN_CACHE_MAX:
+        _plan_cache.pop(next(iter(_plan_cache)))
     return pl
 
 
