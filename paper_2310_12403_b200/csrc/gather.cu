@@ -24,6 +24,10 @@ namespace {
 // flight per thread: UNROLL 4 spilled 56 B to the stack under the 32-register
 // bound (gather 14.8 -> 14.0 us at c2, 14.7 -> 13.6 us at c4; tools/ab.sh).
 constexpr int kGatherCtasPerSM = 8;
+#ifndef CB_GATHER_GRID_PER_SM
+#define CB_GATHER_GRID_PER_SM 8
+#endif
+constexpr int kGatherGridPerSM = CB_GATHER_GRID_PER_SM;  // CTAs launched per SM
 template <typename V>
 constexpr int gather_unroll() { return sizeof(V) == 16 ? 3 : 4; }
 
@@ -63,7 +67,7 @@ void launch_gather(const void* table, int vec_bytes, uint64_t row_bytes, const u
                    const unsigned long long* count, uint64_t cap_rows, const uint32_t* row_map,
                    void* out, cudaStream_t st) {
   const uint32_t vpr = static_cast<uint32_t>(row_bytes / vec_bytes);
-  const int grid = kNumSMs * kGatherCtasPerSM;
+  const int grid = kNumSMs * kGatherGridPerSM;
   switch (vec_bytes) {
     case 16:
       launch_k(gather_kernel<uint4, gather_unroll<uint4>()>, grid, 256, st, static_cast<const uint4*>(table), ids,
