@@ -41,6 +41,10 @@ constexpr uint32_t kTileExact = 0x80000000u;
 #define CB_MARK_CTAS (768 / CB_MARK_NT)
 #endif
 constexpr int kMarkCtasPerSM = CB_MARK_CTAS;
+#ifndef CB_MARK_MINB
+#define CB_MARK_MINB CB_MARK_CTAS
+#endif
+constexpr int kMarkMinBlocks = CB_MARK_MINB;  // register bound: 64K / (128 * this)
 
 __device__ __forceinline__ unsigned inv_epoch(const unsigned* ep, int slot) {
   return ((*ep & 0x3ffffu) << 6) | static_cast<unsigned>(slot);
@@ -554,7 +558,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
 }
 
 template <int IPT, bool SMOOTH>
-__global__ void __launch_bounds__(kMarkNT, kMarkCtasPerSM) labor_mark_kernel(LaborArgs a) {
+__global__ void __launch_bounds__(kMarkNT, kMarkMinBlocks) labor_mark_kernel(LaborArgs a) {
   pdl_begin();
   mark_body<IPT, SMOOTH>(a, blockIdx.x, gridDim.x);
 }
