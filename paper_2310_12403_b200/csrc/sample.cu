@@ -566,7 +566,10 @@ __global__ void __launch_bounds__(kMarkNT, kMarkMinBlocks) labor_mark_kernel(Lab
 // Emit tiles: 256 keep words (8K positions) per tile for small layers, 2048
 // (64K positions) once a layer has > 64K words, so the look-back front never
 // walks more than a few thousand tiles.
-constexpr int kEmitWPT = 8;                     // max keep words per thread
+#ifndef CB_EMIT_WPT
+#define CB_EMIT_WPT 8
+#endif
+constexpr int kEmitWPT = CB_EMIT_WPT;           // max keep words per thread
 constexpr int kEmitTileWords = kNT * kEmitWPT;  // max words per tile
 constexpr uint64_t kEmitBigLayerWords = 64 * 1024;
 
@@ -929,7 +932,7 @@ __global__ void __launch_bounds__(kNT) rw_emit_kernel(RwArgs a) {
 // Words per thread: 2 for small bitmaps (more tiles, short per-thread
 // serial bit loops), 8 (two 16 B loads) once the bitmap exceeds 256K words,
 // so the look-back chain stays ~ <2K tiles even at 10^8 vertices.
-constexpr int kWPTSmall = 2;
+constexpr int kWPTSmall = 2;  // the flat path loads word pairs
 constexpr int kWPTBig = 8;
 static_assert(kNT * kWPTBig == kExtractTileWords, "extract tile");
 
