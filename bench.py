@@ -770,7 +770,7 @@ def run_ours(args, cfg):
         e2e_s = float(t.item())
     n_src_last = int(meta_h[K - 1].numpy().view(np.uint64).reshape(-1, 8)[L - 1][4])
     assert n_src_last > 0, "e2e batch result read back empty"
-    launches_per_step = plan.launch_count(cb.MODE_INDEP, True)
+    launches_per_step = plan.captured_launches(3)  # the replayed sample + gather graph
     # per-launch breakdown inside the CUDA graph (event-record nodes), L2 flushed
     flush_l2()
     prof_ms = plan.graph_profile(step_ptr(W), scheds[W])

@@ -249,6 +249,10 @@ int cb_plan_graph_profile(cb_plan* plan, const uint32_t* d_seeds, const cb_sched
 /* Debug: globaltimer stamps of the last batch (plan created with CB_TRACE=1). */
 int cb_plan_trace(cb_plan* plan, uint64_t* out, uint64_t n);
 
+/* Kernels in one replay of the captured graphs: what = 1 sample, 2 gather,
+ * 3 sample + gather (there the last layer's relabel of a 1-part plan is fused
+ * into the gather launch, so it is one fewer than 1 + 2). */
+int cb_plan_captured_launches(const cb_plan* plan, int what, uint64_t* n);
 /* Number of kernels one cb_sample/cb_gather call enqueues (for reporting). */
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n);
 

@@ -83,6 +83,7 @@ _SIGS = {
                                         C.POINTER(C.c_int)]),
     "cb_plan_trace": (C.c_int, [_P, _P, _u64]),
     "cb_plan_launch_count": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_u64)]),
+    "cb_plan_captured_launches": (C.c_int, [_P, C.c_int, C.POINTER(_u64)]),
     "cb_cache_create": (C.c_int, [C.c_int, _u64, _u64, _u64, _PP]),
     "cb_cache_destroy": (None, [_P]),
     "cb_cache_access_trace": (C.c_int, [_P, _P, _u64, _P]),

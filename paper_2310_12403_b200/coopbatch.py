@@ -455,6 +455,12 @@ class Plan:
                                                  C.byref(n)))
         return ms[: n.value].tolist()
 
+    def captured_launches(self, what: int = 3) -> int:
+        """Kernels per replay of the captured graph (1 sample, 2 gather, 3 both)."""
+        n = C.c_uint64()
+        _check(_lib.load().cb_plan_captured_launches(self._h, what, C.byref(n)))
+        return n.value
+
     def launch_count(self, mode: int, with_gather: bool) -> int:
         n = C.c_uint64()
         _check(_lib.load().cb_plan_launch_count(self._h, mode, int(with_gather), C.byref(n)))

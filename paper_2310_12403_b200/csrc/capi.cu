@@ -523,10 +523,18 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
             pst(p));
       }
       const uint32_t* Dl = (L == 1) ? d_seeds + off[p] : w.L[L - 2].src;
-      launch_relabel(relabel_args(w.bm[(L - 1) & 1], w.L[L - 1], Dl, pl->meta_at(p, L - 1)),
-                     std::max(w.L[L - 1].cap_edges, w.L[L - 1].cap_dst), pst(p));
-      ++launches;
-      prof_mark(pl);
+      const RelabelArgs last = relabel_args(w.bm[(L - 1) & 1], w.L[L - 1], Dl,
+                                            pl->meta_at(p, L - 1));
+      const uint64_t work = std::max(w.L[L - 1].cap_edges, w.L[L - 1].cap_dst);
+      if (pl->defer_relabel && P == 1) {  // launched by enqueue_gather, fused
+        pl->deferred = last;
+        pl->deferred_work = work;
+        pl->has_deferred = true;
+      } else {
+        launch_relabel(last, work, pst(p));
+        ++launches;
+        prof_mark(pl);
+      }
     }
     join();
   } else {
@@ -653,8 +661,15 @@ void enqueue_gather(cb_plan* pl, const cb_features* f) {
   for (uint32_t p = 0; p < pl->P; ++p) {
     PeWork& w = pl->pe[p];
     const LayerBufs& b = w.L[pl->L - 1];
-    launch_gather(f->table, vb, f->row_bytes, b.src, &pl->meta_at(p, pl->L - 1)->n_src,
-                  w.cap_rows, f->row_map, w.rows, conc ? pl->part_st[p] : pl->stream);
+    if (p == 0 && pl->has_deferred) {
+      launch_relabel_gather(pl->deferred, pl->deferred_work, f->table, vb, f->row_bytes, b.src,
+                            &pl->meta_at(p, pl->L - 1)->n_src, w.cap_rows, f->row_map, w.rows,
+                            conc ? pl->part_st[p] : pl->stream);
+      pl->has_deferred = false;
+    } else {
+      launch_gather(f->table, vb, f->row_bytes, b.src, &pl->meta_at(p, pl->L - 1)->n_src,
+                    w.cap_rows, f->row_map, w.rows, conc ? pl->part_st[p] : pl->stream);
+    }
     pl->launches += 1;
     prof_mark(pl);
   }
@@ -1189,8 +1204,16 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
       CB_CUDA(cudaGraphDestroy(graph));
       plan->cap_launches_gather = plan->launches;
       CB_CUDA(cudaStreamBeginCapture(plan->stream, cudaStreamCaptureModeThreadLocal));
-      enqueue_batch(plan, mode, plan->seeds, seeds_off, &dummy, true);
+      plan->defer_relabel = true;
+      try {
+        enqueue_batch(plan, mode, plan->seeds, seeds_off, &dummy, true);
+      } catch (...) {
+        plan->defer_relabel = false;
+        throw;
+      }
+      plan->defer_relabel = false;
       enqueue_gather(plan, f);
+      plan->cap_launches_all = plan->launches;
       CB_CUDA(cudaStreamEndCapture(plan->stream, &graph));
       CB_CUDA(cudaGraphInstantiate(&plan->exec_all, graph, 0));
       CB_CUDA(cudaGraphDestroy(graph));
@@ -1258,7 +1281,7 @@ int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_devic
       plan->seeds_off = plan->cap_off;
       plan->have_batch = true;
       plan->have_rows = all;
-      plan->launches = plan->cap_launches_sample + (all ? plan->cap_launches_gather : 0);
+      plan->launches = all ? plan->cap_launches_all : plan->cap_launches_sample;
       if (all) return;
     }
     if (what & 2) {
@@ -1664,6 +1687,19 @@ int cb_plan_trace(cb_plan* plan, uint64_t* out, uint64_t n) {
     CB_CUDA(cudaStreamSynchronize(plan->stream));
     CB_CUDA(cudaMemcpy(out, plan->trace, std::min<uint64_t>(n, kTraceSlots) * 8,
                        cudaMemcpyDeviceToHost));
+  });
+}
+
+int cb_plan_captured_launches(const cb_plan* plan, int what, uint64_t* n) {
+  return guard([&] {
+    require(plan != nullptr && n != nullptr, "null argument");
+    require(plan->exec_sample != nullptr, "no captured batch (call cb_plan_capture)");
+    if (what == 1) *n = plan->cap_launches_sample;
+    else if (what == 2) *n = plan->cap_launches_gather;
+    else {
+      require(what == 3 && plan->exec_all != nullptr, "no captured sample + gather graph");
+      *n = plan->cap_launches_all;
+    }
   });
 }
 

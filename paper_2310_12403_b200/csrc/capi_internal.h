@@ -206,6 +206,12 @@ struct cb_plan {
   Variates* var = nullptr;
   double* ext_vtab = nullptr;  // caller variate table r_t (sample_labor0), n entries
   int layer_base = 0;          // block l hashes as layer l + layer_base (sample_block at any layer)
+  // captured sample + gather graph: the last layer's relabel of part 0 is
+  // launched fused with the gather (launch_relabel_gather)
+  bool defer_relabel = false;
+  bool has_deferred = false;
+  cb::RelabelArgs deferred{};
+  uint64_t deferred_work = 0;
   uint32_t* seeds = nullptr;
   uint64_t seeds_cap = 0;
   int mode = -1;          // mode of the last batch
@@ -235,7 +241,7 @@ struct cb_plan {
   cudaGraphExec_t exec_all = nullptr;  // sample + gather in one graph
   int cap_mode = -1;
   std::vector<uint64_t> cap_off;
-  uint64_t cap_launches_sample = 0, cap_launches_gather = 0;
+  uint64_t cap_launches_sample = 0, cap_launches_gather = 0, cap_launches_all = 0;
 
   void drop_graphs() {
     if (exec_sample) cudaGraphExecDestroy(exec_sample);

@@ -11,9 +11,12 @@
 // per thread.
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "cb_internal.h"
 #include "gather.h"
 #include "gather_body.cuh"
+#include "relabel.cuh"
 
 namespace cb {
 using namespace cbdev;
@@ -39,6 +42,25 @@ __global__ void __launch_bounds__(256, kGatherCtasPerSM) gather_kernel(
   pdl_begin();
   gbody::gather_body<V, UNROLL>(table, ids, count, cap_rows, row_map, vpr, out, blockIdx.x,
                                 gridDim.x);
+}
+
+// The last layer's relabel and the feature gather in one launch (they are
+// independent: the gather reads the src list, the relabel rewrites edges and
+// dst_pos): CTAs [0, n_rel) relabel, the rest gather. Used by the captured
+// sample + gather graph, one launch fewer per batch.
+template <typename V, int UNROLL>
+__global__ void __launch_bounds__(256, kGatherCtasPerSM) relabel_gather_kernel(
+    RelabelArgs r, unsigned n_rel, const V* __restrict__ table,
+    const uint32_t* __restrict__ ids, const unsigned long long* __restrict__ count,
+    uint64_t cap_rows, const uint32_t* __restrict__ row_map, uint32_t vpr, V* __restrict__ out) {
+  pdl_begin();
+  if (blockIdx.x < n_rel) {
+    rbody::relabel_range(r, blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
+                         static_cast<uint64_t>(n_rel) * blockDim.x);
+    return;
+  }
+  gbody::gather_body<V, UNROLL>(table, ids, count, cap_rows, row_map, vpr, out,
+                                blockIdx.x - n_rel, gridDim.x - n_rel);
 }
 
 // value[v, j] = 2*U(hash(seed,{9,v,j})) - 1 (exact in f64), one rounding to
@@ -90,6 +112,39 @@ void launch_gather(const void* table, int vec_bytes, uint64_t row_bytes, const u
           static_cast<unsigned short*>(out));
   }
   CB_LAUNCH("gather");
+}
+
+void launch_relabel_gather(const RelabelArgs& r, uint64_t relabel_work, const void* table,
+                           int vec_bytes, uint64_t row_bytes, const uint32_t* ids,
+                           const unsigned long long* count, uint64_t cap_rows,
+                           const uint32_t* row_map, void* out, cudaStream_t st) {
+  const uint32_t vpr = static_cast<uint32_t>(row_bytes / vec_bytes);
+  // one resident wave: up to 2 relabel CTAs per SM, the gather takes the rest
+  const unsigned n_rel = static_cast<unsigned>(
+      std::min<uint64_t>(std::max<uint64_t>((relabel_work + 1023) / 1024, 1), kNumSMs * 2));
+  const int grid = kNumSMs * kGatherGridPerSM;
+  switch (vec_bytes) {
+    case 16:
+      launch_k(relabel_gather_kernel<uint4, gather_unroll<uint4>()>, grid, 256, st, r, n_rel,
+               static_cast<const uint4*>(table), ids, count, cap_rows, row_map, vpr,
+               static_cast<uint4*>(out));
+      break;
+    case 8:
+      launch_k(relabel_gather_kernel<uint2, gather_unroll<uint2>()>, grid, 256, st, r, n_rel,
+               static_cast<const uint2*>(table), ids, count, cap_rows, row_map, vpr,
+               static_cast<uint2*>(out));
+      break;
+    case 4:
+      launch_k(relabel_gather_kernel<uint32_t, gather_unroll<uint32_t>()>, grid, 256, st, r,
+               n_rel, static_cast<const uint32_t*>(table), ids, count, cap_rows, row_map, vpr,
+               static_cast<uint32_t*>(out));
+      break;
+    default:
+      launch_k(relabel_gather_kernel<unsigned short, gather_unroll<unsigned short>()>, grid, 256,
+               st, r, n_rel, static_cast<const unsigned short*>(table), ids, count, cap_rows,
+               row_map, vpr, static_cast<unsigned short*>(out));
+  }
+  CB_LAUNCH("relabel_gather");
 }
 
 void launch_synth(uint64_t seed, uint32_t dim, int dtype, uint64_t n_rows,

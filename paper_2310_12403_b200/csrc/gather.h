@@ -12,6 +12,11 @@ namespace cb {
 void launch_gather(const void* table, int vec_bytes, uint64_t row_bytes, const uint32_t* ids,
                    const unsigned long long* count, uint64_t cap_rows, const uint32_t* row_map,
                    void* out, cudaStream_t st);
+// the last layer's relabel (sample.cu relabel_kernel) fused with the gather
+void launch_relabel_gather(const RelabelArgs& r, uint64_t relabel_work, const void* table,
+                           int vec_bytes, uint64_t row_bytes, const uint32_t* ids,
+                           const unsigned long long* count, uint64_t cap_rows,
+                           const uint32_t* row_map, void* out, cudaStream_t st);
 void launch_synth(uint64_t seed, uint32_t dim, int dtype, uint64_t n_rows,
                   const uint32_t* row_vertex, uint64_t v_base, void* out, cudaStream_t st);
 int vec_bytes_for(uint64_t row_bytes);

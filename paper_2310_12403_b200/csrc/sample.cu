@@ -24,6 +24,7 @@
 
 #include "cb_internal.h"
 #include "gather_body.cuh"
+#include "relabel.cuh"
 
 namespace cb {
 using namespace cbdev;
@@ -57,11 +58,7 @@ __device__ __forceinline__ void set_bit(uint32_t* bits, uint32_t* summ, uint32_t
   if (summ) atomicOr(&summ[v >> 10], 1u << ((v >> 5) & 31u));
 }
 
-__device__ __forceinline__ uint32_t bm_rank(const uint32_t* bits, const uint32_t* wprefix,
-                                            uint32_t v) {
-  const uint32_t w = v >> 5;
-  return wprefix[w] + __popc(bits[w] & ((1u << (v & 31u)) - 1u));
-}
+using rbody::bm_rank;
 
 // Reset a ticket counter once every CTA of the launch is done with it, so no
 // per-batch memset of the tickets is needed.
@@ -69,16 +66,7 @@ __device__ __forceinline__ uint32_t bm_rank(const uint32_t* bits, const uint32_t
 // per-layer op (stream order), so kernels need no exit bookkeeping.
 __device__ __forceinline__ void retire_ticket(unsigned*, unsigned*, unsigned) {}
 
-__device__ void relabel_range(const RelabelArgs& r, uint64_t tid, uint64_t stride) {
-  const uint64_t ne = min(static_cast<uint64_t>(r.meta->n_edges), r.cap_edges);
-  const uint64_t nd = r.meta->n_dst;
-  for (uint64_t e = tid; e < ne; e += stride) {
-    uint2 x = r.edges[e];
-    x.x = bm_rank(r.bits, r.wprefix, x.x);
-    r.edges[e] = x;
-  }
-  for (uint64_t i = tid; i < nd; i += stride) r.dst_pos[i] = bm_rank(r.bits, r.wprefix, r.D[i]);
-}
+using rbody::relabel_range;
 
 // ------------------------------------------------------------ batch begin --
 // Clears the previous batch's last bitmap (its final id list), bumps the

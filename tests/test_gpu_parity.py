@@ -406,6 +406,11 @@ def test_graph_replay_matches_eager(c1, kappa):
     seeds0 = O.draw_from_pool(pool, 512, 5, 0)
     plan.sample([seeds0], sched, cb.MODE_INDEP)
     plan.capture(np.array([0, 512], np.uint64), sched, cb.MODE_INDEP, store)
+    # the sample + gather graph fuses the last relabel into the gather launch
+    per_layer = 4 if kappa == 4 else 3  # + the smoothed variate table
+    assert plan.captured_launches(1) == 1 + 3 * per_layer + 1
+    assert plan.captured_launches(2) == 1
+    assert plan.captured_launches(3) == plan.captured_launches(1)
     for step in range(1, 4):
         sched = cb.schedule_advance(sched)
         seeds = O.draw_from_pool(pool, 512, 5, step)
