@@ -859,7 +859,14 @@ def write_reports(args, cfg):
         R.write_csv(os.path.join(args.csv_dir, "curve_c5.csv"),
                     {**base, "config": "c5", "layers": len(c5["fanouts"]),
                      "fanout": "/".join(map(str, c5["fanouts"])), "batch": "sweep"},
-                    R.CURVE_COLUMNS, CSV_ROWS["curve"])
+                    R.curve_columns(len(c5["fanouts"])), CSV_ROWS["curve"])
+    by_sampler = {}
+    for name, b, mean, se, wps, _sew in CSV_ROWS.get("work_curve", []):
+        by_sampler.setdefault(name, []).append((b, mean, se, wps))
+    for name, rows in by_sampler.items():
+        R.write_csv(os.path.join(args.csv_dir, f"curve_c1_{name}.csv"),
+                    {**base, "config": "c1", "sampler": name, "layers": 3, "trials": 50,
+                     "batch": "64..8192"}, R.curve_columns(3), rows)
     run = []
     for tag, metrics in CSV_ROWS.get("run", []):
         run.extend(R.run_rows(0, tag, metrics))

@@ -2,8 +2,11 @@
 starts with `# key=value` lines of the resolved configuration and is written
 atomically (temp file, then rename). Column sets follow the CLI's:
   run      step,mode,pe,layer,s_l,s_tilde_l,e_l,comm_vertices,feat_bytes,loss (cli.cpp:208)
-  curve    batch_size,mean_sL,se_sL,work_per_seed                         (cli.cpp:184-185)
+  curve    batch_size,mean_s<L>,se_s<L>,work_per_seed                     (cli.cpp:184-188)
   cache    step,miss_rate,s_l,bytes                                       (cli.cpp:256)
+  partition vertex,part                                                   (cli.cpp:153-162)
+Floating-point fields are printed like the CLI's std::ostream defaults (six
+significant digits, %g).
 """
 from __future__ import annotations
 
@@ -11,8 +14,16 @@ import os
 
 RUN_COLUMNS = ["step", "mode", "pe", "layer", "s_l", "s_tilde_l", "e_l", "comm_vertices",
                "feat_bytes", "loss"]
-CURVE_COLUMNS = ["batch_size", "mean_sL", "se_sL", "work_per_seed"]
 CACHE_COLUMNS = ["step", "miss_rate", "s_l", "bytes"]
+PARTITION_COLUMNS = ["vertex", "part"]
+
+
+def curve_columns(layers: int) -> list[str]:
+    """cli.cpp:184-185: the curve header names the layer count."""
+    return ["batch_size", f"mean_s{layers}", f"se_s{layers}", "work_per_seed"]
+
+
+CURVE_COLUMNS = curve_columns(3)
 
 
 def write_csv(path: str, config: dict, columns: list[str], rows) -> None:
@@ -28,8 +39,20 @@ def write_csv(path: str, config: dict, columns: list[str], rows) -> None:
 
 def _fmt(x) -> str:
     if isinstance(x, float):
-        return repr(x)
+        return f"{x:g}"  # std::ostream << double (precision 6)
     return str(x)
+
+
+def curve_rows(curve):
+    """Rows of the `curve` report from analysis.WorkCurve (cli.cpp:186-188)."""
+    for p in curve.points:
+        yield (p.batch_size, p.mean_sl, p.se_sl, p.work_per_seed)
+
+
+def partition_rows(owner):
+    """Rows of the `partition` report: one (vertex, part) per vertex (cli.cpp:158-161)."""
+    for v, p in enumerate(owner.tolist() if hasattr(owner, "tolist") else owner):
+        yield (v, p)
 
 
 def run_rows(step: int, mode: str, metrics, loss: float = 0.0):

@@ -215,3 +215,21 @@ def test_draw_batch_and_split_by_owner():
     owner = np.array([0, 1, 1, 0, 2, 2, 1], np.uint32)
     parts = split_by_owner([6, 0, 4, 1, 3, 5], owner, 3)
     assert [p.tolist() for p in parts] == [[0, 3], [6, 1], [4, 5]]
+
+
+def test_csv_curve_and_partition_formats(tmp_path):
+    """cli.cpp:153-188: curve header names the layer count, doubles print like
+    std::ostream (%g, 6 significant digits), partition rows are vertex,part."""
+    from paper_2310_12403_b200 import reports as R
+    from paper_2310_12403_b200.analysis import WorkCurve, WorkCurvePoint
+    c = WorkCurve(2, [WorkCurvePoint(64, 1234.5678901, 0.0001234567, 19.29012328),
+                      WorkCurvePoint(128, 2e7, 1e-7, 156250.0)])
+    p = tmp_path / "curve.csv"
+    R.write_csv(str(p), {"layers": 2}, R.curve_columns(2), R.curve_rows(c))
+    lines = p.read_text().splitlines()
+    assert lines[1] == "batch_size,mean_s2,se_s2,work_per_seed"
+    assert lines[2] == "64,1234.57,0.000123457,19.2901"
+    assert lines[3] == "128,2e+07,1e-07,156250"
+    q = tmp_path / "part.csv"
+    R.write_csv(str(q), {"parts": 2}, R.PARTITION_COLUMNS, R.partition_rows(np.array([1, 0, 1])))
+    assert q.read_text().splitlines()[1:] == ["vertex,part", "0,1", "1,0", "2,1"]
