@@ -407,6 +407,9 @@ def test_graph_replay_matches_eager(c1, kappa):
     plan.sample([seeds0], sched, cb.MODE_INDEP)
     plan.capture(np.array([0, 512], np.uint64), sched, cb.MODE_INDEP, store)
     # the sample + gather graph fuses the last relabel into the gather launch
+    fresh = cb.Plan(g, None, 3, cfg, 8)
+    with pytest.raises(cb.InputError):  # nothing captured yet
+        fresh.captured_launches(3)
     per_layer = 4 if kappa == 4 else 3  # + the smoothed variate table
     assert plan.captured_launches(1) == 1 + 3 * per_layer + 1
     assert plan.captured_launches(2) == 1
