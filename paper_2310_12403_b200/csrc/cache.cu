@@ -508,7 +508,7 @@ void DeviceLru::access_trace(const uint32_t* keys, uint64_t n, uint8_t* miss, cu
   DevBuf b_keys(n * 4 + 16), b_miss(n + 16);
   uint32_t* d_keys = b_keys.as<uint32_t>();
   uint8_t* d_miss = b_miss.as<uint8_t>();
-  CB_CUDA(cudaMemcpy(d_keys, keys, n * 4, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpyAsync(d_keys, keys, n * 4, cudaMemcpyHostToDevice, st));
   std::vector<uint8_t> in_run;
   in_run.assign(n_, 0);
   uint64_t start = 0;

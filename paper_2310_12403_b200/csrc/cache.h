@@ -54,6 +54,7 @@ class DeviceLru {
   uint64_t size() const;
   void reset_counters() { hits_ = misses_ = 0; }
   uint64_t capacity() const { return cap_; }
+  uint64_t n_keys() const { return n_; }
   uint64_t row_bytes() const { return row_bytes_; }
   const void* storage() const { return rows_; }
   int device() const { return device_; }

@@ -209,12 +209,22 @@ void upload_variates(cb_plan* pl, const cb_sched* s, uint32_t n_sched, cudaStrea
                           st));  // pageable source: staged before the call returns
 }
 
-void check_seeds_host(const cb_plan* pl, const uint32_t* flat, const uint64_t* off) {
-  const uint64_t n = pl->g->g.n;
+// Seed offsets index the plan's seed buffer (P * max_seeds ids): they start
+// at 0, never decrease, and no part exceeds max_seeds.
+void check_offsets(const cb_plan* pl, const uint64_t* off) {
+  require(off[0] == 0, "seed offsets must start at 0");
   for (uint32_t p = 0; p < pl->P; ++p) {
     require(off[p + 1] >= off[p], "seed offsets must be nondecreasing");
-    require(off[p + 1] - off[p] <= pl->max_seeds,
-            "part " + std::to_string(p) + " has more seeds than the plan's max_seeds_per_part");
+    if (off[p + 1] - off[p] > pl->max_seeds)
+      throw Error(kInput, "part " + std::to_string(p) +
+                              " has more seeds than the plan's max_seeds_per_part");
+  }
+}
+
+void check_seeds_host(const cb_plan* pl, const uint32_t* flat, const uint64_t* off) {
+  const uint64_t n = pl->g->g.n;
+  check_offsets(pl, off);
+  for (uint32_t p = 0; p < pl->P; ++p) {
     for (uint64_t i = off[p]; i < off[p + 1]; ++i)
       if (flat[i] >= n)
         throw Error(kInput, "vertex id " + std::to_string(flat[i]) + " out of range [0, " +
@@ -238,11 +248,13 @@ void check_ownership_host(const cb_plan* pl, const uint32_t* flat, const uint64_
   DevBuf b_ids(total * 4 + 4), b_out(total * 4 + 4), b_cnt(8);
   uint32_t* d_ids = b_ids.as<uint32_t>();
   uint32_t* d_out = b_out.as<uint32_t>();
-  CB_CUDA(cudaMemcpy(d_ids, seeds.data(), total * 4, cudaMemcpyHostToDevice));
+  // uploads ordered on the plan stream: a pageable cudaMemcpy runs on the
+  // legacy stream and may return before its DMA lands
+  CB_CUDA(cudaMemcpyAsync(d_ids, seeds.data(), total * 4, cudaMemcpyHostToDevice, pl->stream));
   // reuse the feature gather kernel with a 4-byte "row" = owner[v]
   unsigned long long* d_cnt = b_cnt.as<unsigned long long>();
   const unsigned long long t = total;
-  CB_CUDA(cudaMemcpy(d_cnt, &t, 8, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpyAsync(d_cnt, &t, 8, cudaMemcpyHostToDevice, pl->stream));
   launch_gather(pl->pm->owner, 4, 4, d_ids, d_cnt, total, nullptr, d_out, pl->stream);
   CB_CUDA(cudaStreamSynchronize(pl->stream));
   CB_CUDA(cudaMemcpy(owners.data(), d_out, total * 4, cudaMemcpyDeviceToHost));
@@ -453,6 +465,22 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
   return (smooth && pl->kind == CB_LABOR0 && pl->vtab) ? 4 : 3;  // (+ variate table)
 }
 
+// Look-back status words carry an 18-bit epoch. Every device epoch bump
+// (one batch_begin launch per part, eager, layer-wise or inside a replayed
+// graph) is counted here, and the status arrays are cleared, in stream order,
+// whenever the count crosses a multiple of 2^17, so a stale status can never
+// alias the current epoch.
+void count_epoch_bumps(cb_plan* pl, cudaStream_t st, uint64_t bumps) {
+  const uint64_t before = pl->batches;
+  pl->batches += bumps;
+  if ((before >> 17) == (pl->batches >> 17)) return;
+  for (auto& w : pl->pe) {
+    CB_CUDA(cudaMemsetAsync(w.sync.status_a, 0, w.sync.max_tiles * 8, st));
+    CB_CUDA(cudaMemsetAsync(w.sync.status_b, 0, w.sync.max_tiles * 8, st));
+    CB_CUDA(cudaMemsetAsync(w.sync.status_c, 0, w.sync.max_tiles * 8, st));
+  }
+}
+
 // The per-batch launch sequence. d_seeds: P seed lists back to back (device).
 void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_t* off,
                    const cb_sched* sched, bool capturing = false, uint32_t n_sched = 1) {
@@ -463,13 +491,7 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
   if (!capturing) upload_variates(pl, sched, n_sched, st);
   pl->mode = mode;
   pl->seeds_off.assign(off, off + P + 1);
-  if (!capturing && ++pl->batches % (1u << 17) == 0) {  // epoch wrap (18-bit epochs)
-    for (auto& w : pl->pe) {
-      CB_CUDA(cudaMemsetAsync(w.sync.status_a, 0, w.sync.max_tiles * 8, st));
-      CB_CUDA(cudaMemsetAsync(w.sync.status_b, 0, w.sync.max_tiles * 8, st));
-      CB_CUDA(cudaMemsetAsync(w.sync.status_c, 0, w.sync.max_tiles * 8, st));
-    }
-  }
+  if (!capturing) count_epoch_bumps(pl, st, 1);
   const bool coop = (mode == CB_MODE_COOP) && P > 1;
   const bool smooth = smooth_of(pl, sched);
   pl->smooth = smooth;
@@ -638,6 +660,7 @@ void require_batch(const cb_plan* pl, uint32_t p, int l) {
 
 void prepare_rows(cb_plan* pl, const cb_features* f) {
   require(f->n_rows == pl->g->g.n, "feature table does not match the graph");
+  require_full_table(f);
   for (uint32_t p = 0; p < pl->P; ++p) {
     PeWork& w = pl->pe[p];
     const LayerBufs& b = w.L[pl->L - 1];
@@ -1123,8 +1146,10 @@ int cb_plan_set_variate_table(cb_plan* plan, const double* table, int on_device)
     }
     const uint64_t n = plan->g->g.n;
     if (!plan->ext_vtab) CB_CUDA(cudaMalloc(&plan->ext_vtab, std::max<uint64_t>(n, 1) * 8));
-    CB_CUDA(cudaMemcpy(plan->ext_vtab, table, n * 8,
-                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    CB_CUDA(cudaMemcpyAsync(plan->ext_vtab, table, n * 8,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            plan->stream));
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
   });
 }
 
@@ -1153,9 +1178,7 @@ int cb_sample_device(cb_plan* plan, int mode, const uint32_t* d_seeds_flat,
   return guard([&] {
     require(plan != nullptr && seeds_off != nullptr && sched != nullptr, "null argument");
     require_mode(plan, mode);
-    for (uint32_t p = 0; p < plan->P; ++p)
-      require(seeds_off[p + 1] - seeds_off[p] <= plan->max_seeds,
-              "more seeds than the plan's max_seeds_per_part");
+    check_offsets(plan, seeds_off);
     DeviceGuard dg(plan->device);
     enqueue_batch(plan, mode, d_seeds_flat, seeds_off, sched);
   });
@@ -1177,9 +1200,7 @@ int cb_plan_capture(cb_plan* plan, int mode, const uint64_t* seeds_off, const cb
     require(plan != nullptr && seeds_off != nullptr && sched != nullptr, "null argument");
     require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
     require_mode(plan, mode);
-    for (uint32_t p = 0; p < plan->P; ++p)
-      require(seeds_off[p + 1] - seeds_off[p] <= plan->max_seeds,
-              "more seeds than the plan's max_seeds_per_part");
+    check_offsets(plan, seeds_off);
     DeviceGuard dg(plan->device);
     plan->drop_graphs();
     if (f) prepare_rows(plan, f);
@@ -1260,14 +1281,11 @@ int cb_plan_replay(cb_plan* plan, const uint32_t* seeds_flat, int seeds_on_devic
                                                 : cudaMemcpyHostToDevice,
                                 st));
       upload_variates(plan, sched, 1, st);
-      if (++plan->batches % (1u << 17) == 0) {
-        for (auto& w : plan->pe) {
-          CB_CUDA(cudaMemsetAsync(w.sync.status_a, 0, w.sync.max_tiles * 8, st));
-          CB_CUDA(cudaMemsetAsync(w.sync.status_b, 0, w.sync.max_tiles * 8, st));
-          CB_CUDA(cudaMemsetAsync(w.sync.status_c, 0, w.sync.max_tiles * 8, st));
-        }
-      }
+      // the graph bumps the epoch once; a re-clear of another mode's
+      // leftovers below bumps it once more
+      count_epoch_bumps(plan, st, 1);
       if (plan->dirty_mode >= 0 && plan->dirty_mode != plan->cap_mode) {
+        count_epoch_bumps(plan, st, 1);
         for (uint32_t p = 0; p < plan->P; ++p) {
           const Dirty d = dirty_of(plan, p, plan->dirty_mode);
           launch_batch_begin(plan->pe[p].sync, d.bits, d.summ, d.list, d.count, d.cap,
@@ -1522,6 +1540,7 @@ int cb_plan_sample_layer(cb_plan* plan, int layer, const uint32_t* d_dst, uint64
       plan->mode = CB_MODE_COOP;
     }
     const bool smooth = smooth_of(plan, sched);
+    count_epoch_bumps(plan, st, 1);
     launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);
     const RelabelArgs none{};
     enqueue_layer(plan, w, 0, layer, D, cap, n_dst, w.bm[0], none, 0, smooth,
@@ -1564,6 +1583,7 @@ int cb_merge_owned(cb_plan* plan, int layer, const uint32_t* d_recv, uint64_t n_
     PeWork& w = plan->pe[0];
     cudaStream_t st = plan->stream;
     unsigned long long* cnt = plan->scratch;
+    count_epoch_bumps(plan, st, 1);
     launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);
     mark_ids(d_recv, n_recv, w.bm[1].bits, w.bm[1].summ, st);
     launch_extract(extract_args(w, w.bm[1], nullptr, d_next, cap_next, cnt, nullptr,
@@ -1632,6 +1652,7 @@ int cb_gather_rows(const cb_features* f, const uint32_t* d_ids, uint64_t n, void
                    void* stream) {
   return guard([&] {
     require(f != nullptr, "null features");
+    require_full_table(f);
     DeviceGuard dg(f->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     launch_gather(f->table, vec_bytes_for(f->row_bytes), f->row_bytes, d_ids, nullptr, n,
@@ -1660,12 +1681,15 @@ int cb_plan_graph_profile(cb_plan* plan, const uint32_t* d_seeds, const cb_sched
     if (d_seeds && total)
       CB_CUDA(cudaMemcpyAsync(plan->seeds, d_seeds, total * 4, cudaMemcpyDefault, st));
     upload_variates(plan, sched, 1, st);
-    if (plan->dirty_mode >= 0 && plan->dirty_mode != plan->cap_mode)
+    count_epoch_bumps(plan, st, 1);
+    if (plan->dirty_mode >= 0 && plan->dirty_mode != plan->cap_mode) {
+      count_epoch_bumps(plan, st, 1);
       for (uint32_t p = 0; p < plan->P; ++p) {
         const Dirty d = dirty_of(plan, p, plan->dirty_mode);
         launch_batch_begin(plan->pe[p].sync, d.bits, d.summ, d.list, d.count, d.cap,
                            plan->pe[p].bm[0].words_padded, st);
       }
+    }
     CB_CUDA(cudaGraphLaunch(plan->exec_prof, st));
     CB_CUDA(cudaStreamSynchronize(st));
     plan->dirty_mode = plan->cap_mode;

@@ -43,6 +43,7 @@ int cb_cache_access_ids(cb_cache* c, const uint32_t* d_ids, uint64_t n, uint64_t
     require(c != nullptr, "null cache");
     require(pm == nullptr || part < pm->parts, "part index out of range");
     require(d_rows_out == nullptr || backing != nullptr, "rows requested without a table");
+    if (backing) require_full_table(backing);
     require(backing == nullptr || c->lru->row_bytes() == 0 ||
                 backing->row_bytes == c->lru->row_bytes(),
             "cache row size does not match the feature table");
@@ -79,6 +80,7 @@ int cb_cache_access_plan(cb_cache* c, cb_plan* plan, uint32_t part, uint64_t ord
       plan->have_rows = true;
     }
     CacheGatherSrc src;
+    if (backing) require_full_table(backing);
     if (backing && d_rows_out) {
       require(c->lru->row_bytes() == 0 || backing->row_bytes == c->lru->row_bytes(),
               "cache row size does not match the feature table");
@@ -100,7 +102,17 @@ int cb_cache_access_host_ids(cb_cache* c, const uint32_t* ids, uint64_t n, uint6
     DeviceGuard dg(c->lru->device());
     DevBuf buf(n * 4 + 16);
     uint32_t* d = buf.as<uint32_t>();
-    CB_CUDA(cudaMemcpy(d, ids, n * 4, cudaMemcpyHostToDevice));
+    // the batch-exact LRU assumes distinct keys inside the key space
+    // (LruCache::access would count a repeat as a hit; that is a trace, see
+    // cb_cache_access_trace)
+    {
+      std::vector<uint32_t> sorted(ids, ids + n);
+      std::sort(sorted.begin(), sorted.end());
+      require(n == 0 || sorted.back() < c->lru->n_keys(), "cache access: id outside the key space");
+      require(std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end(),
+              "cache access: ids of one access set must be distinct");
+    }
+    CB_CUDA(cudaMemcpyAsync(d, ids, n * 4, cudaMemcpyHostToDevice, c->stream));
     const uint64_t k = c->lru->access_ids(d, n, order_key, pm ? pm->owner : nullptr, part,
                                           CacheGatherSrc{}, c->stream);
     if (kept) *kept = k;

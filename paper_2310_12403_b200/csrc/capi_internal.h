@@ -228,7 +228,7 @@ struct cb_plan {
   bool cap_smooth = false;
   bool have_batch = false;
   bool have_rows = false;
-  uint64_t batches = 0;
+  uint64_t batches = 0;  // device epoch bumps (count_epoch_bumps)
   uint64_t launches = 0;  // kernels enqueued by the last cb_sample (+ cb_gather)
   double* vtab = nullptr;  // smoothed LABOR r_t table [n] (nullptr: per position)
   uint32_t rw_length = 3, rw_walks = 100;  // samplers.hpp:19-22 defaults
@@ -290,6 +290,14 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
 void check_overflow(cb_plan* pl);
 const LayerMeta host_meta(cb_plan* pl, uint32_t p, int l);
 void require_batch(const cb_plan* pl, uint32_t p, int l);
+void count_epoch_bumps(cb_plan* pl, cudaStream_t st, uint64_t bumps);
+// Arbitrary ids may be gathered only from a table that holds every row: a
+// single-part shard (cb_features_synth_shard) keeps n_rows = n for its
+// row_map but allocates only its own rows.
+inline void require_full_table(const cb_features* f) {
+  require(f->shard_rows == 0,
+          "this gather needs a full feature table (got a single-part shard)");
+}
 void prepare_rows(cb_plan* pl, const cb_features* f);
 void enqueue_gather(cb_plan* pl, const cb_features* f);
 }  // namespace capi

@@ -119,6 +119,7 @@ int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seed
     const bool smooth = smooth_of(plan, sched);
     const int s = static_cast<int>(px.layer_ctr++ & 1);
     px.slot_of[layer] = s;
+    count_epoch_bumps(plan, st, 1);
     launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);
     const RelabelArgs none{};
     enqueue_layer(plan, w, 0, layer, D, cap, layer == 0 ? n_seeds : ~0ULL, w.bm[0], none, 0,

@@ -146,6 +146,7 @@ int cb_train_step(cb_plan* pl, const cb_features* f, uint32_t classes, cb_model*
     require(pl != nullptr && f != nullptr && m != nullptr && loss_out != nullptr,
             "null argument");
     require(pl->have_batch, "no sampled batch in this plan");
+    require_full_table(f);
     require(f->dtype == CB_F64, "train step: the feature table must be f64 (FeatureStore)");
     require(m->L == pl->L, "train step: model depth does not match layer count");
     require(m->rows[pl->L - 1] == f->dim, "train step: model input dim does not match store");

@@ -321,6 +321,9 @@ class PeerCoop:
         device tensor), all phases stream-ordered on the plan stream."""
         if isinstance(seeds, torch.Tensor):
             ptr, n = seeds.data_ptr(), seeds.numel()
+            # the plan stream copies the seeds: order it after their producer
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+            self._seeds = seeds  # keep alive until the copy is enqueued
         else:
             self._seeds = np.ascontiguousarray(seeds, dtype=np.uint32)
             ptr, n = self._seeds.ctypes.data, len(self._seeds)
