@@ -3,20 +3,28 @@
 
 Metric (BASELINE.json): seed vertices/sec of one minibatch step =
 3-layer LABOR-0 sample + dedup/relabel (+ owner exchange) + input-feature
-gather, on the products-shaped R-MAT (config 2) at N GPUs, plus feature GB/s.
+gather, plus feature GB/s. Headline workload: config 4, the
+ogbn-papers100M-shaped R-MAT (111M V / 1.6B E, 128 fp16 rows) that north_star
+targets and that fits one B200 (`--config` picks another BASELINE config).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4]
   python bench.py --impl reference ...   # the reference's own CPU path
 
-One process per GPU (torchrun for N>1). At N>1 each rank runs its own
-minibatches (independent minibatching, no data-path collective; weak
-scaling) — see DESIGN.md §Multi-GPU for the cooperative NCCL path status.
+One process per GPU (torchrun for N>1).
+  N = 1 : independent minibatches of 1024 seeds, S = 8 in flight (one CUDA
+          graph + stream each); `latency_ms_per_step` is one batch at a time
+          with L2 flushed (512 MiB write + 256 MiB read) before every step.
+          `value` is not flushed between steps: the inputs (6.5 GB CSR +
+          28 GB table at c4) are far larger than the 126 MB L2.
+  N > 1 : the cooperative step (one part per GPU, per-layer owner exchange
+          over peer memory, rows pulled from the owners' shards; weak
+          scaling, 1024 seeds per GPU). See DESIGN.md §Multi-GPU.
 
-value  : device time (CUDA events on the plan stream, max over ranks), inputs
-         resident in HBM, L2 flushed (512 MiB write) before every step.
-e2e    : wall clock through the public API with host (pinned) seeds: H2D of
-         the seeds + variate keys, sample + gather, D2H of the batch's layer
-         counts, every step.
+value  : device time (CUDA events, max over ranks), inputs resident in HBM.
+e2e    : through the C-ABI with host buffers: H2D of the seeds + variate keys
+         from pinned memory, sample + gather, and the whole batch result
+         (every layer's blocks and the gathered rows) written to pinned host
+         memory, every step; wall clock.
 """
 from __future__ import annotations
 
@@ -144,37 +152,65 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU baseline --
 def cpu_reference_leg(cfg, csr, budget_s: float, parts_per_step: int | None = None,
-                      max_steps: int | None = None):
-    """Time the reference's own stock path (oracle/_ref: indep_sample + per-part
-    load_rows on the compiled reference) on this host's cores. Returns
-    (seeds/s, cores, sample description, per-step seconds list)."""
+                      max_steps: int | None = None, coop_parts: int = 0):
+    """Time the reference's own stock path on this host's cores (oracle/_ref,
+    the reference compiled from its sources): indep_sample over P parts of
+    `batch` seeds (the reference parallelises over parts, coop.cpp:115-117) +
+    per-part FeatureStore::load_rows; or, with coop_parts = P > 1,
+    coop_sample over P parts + load_rows of the owner sets +
+    all_to_all_forward (coop.cpp:445-467). When the f64 FeatureStore would not
+    fit (c4: 113 GB), rows are computed from FeatureStore::synth's formula
+    instead of copied. Returns (seeds/s, cores, sample
+    description, per-step seconds list)."""
     from oracle import oracle as O
     threads = os.cpu_count() or 1
-    P = parts_per_step or threads
+    coop = coop_parts > 1
+    P = coop_parts if coop else (parts_per_step or threads)
     rg = O.RefGraph(csr)
+    onfly = csr.n * cfg["dim"] * 8 > (8 << 30)
     t0 = time.time()
-    fs = O.RefFeatureStore(csr.n, cfg["dim"], FEAT_SEED)
+    fs = None if onfly else O.RefFeatureStore(csr.n, cfg["dim"], FEAT_SEED)
     synth_s = time.time() - t0
     kind = {"labor0": O.LABOR0, "ns": O.NS, "full": O.FULL}[cfg["kind"]]
-    pool = np.arange(csr.n, dtype=np.uint32)
     sched = O.make_sched(1, RUN_SEED)
     L = len(cfg["fanouts"])
     if len(set(cfg["fanouts"])) != 1:
         raise SystemExit("reference leg: per-layer fanouts need the sample_block loop")
+    if coop:
+        owner = O.partition_random(csr.n, P, RUN_SEED)
+        members = O.part_members(owner, P)
+    else:
+        pool = np.arange(csr.n, dtype=np.uint32)
     steps, seeds_done, spent, per_step = 0, 0, 0.0, []
     while (steps == 0 or spent < budget_s) and (max_steps is None or steps < max_steps):
-        per_pe = [O.draw_from_pool(pool, cfg["batch"], RUN_SEED, O.hash_bits(steps, [p]))
-                  for p in range(P)]
-        ts, tg, rows = O.reference_step(rg, fs, 1, None, P, per_pe, L, kind,
-                                        cfg["fanouts"][0], sched)
+        if coop:
+            per_pe = [O.draw_from_pool(members[p], cfg["batch"], RUN_SEED,
+                                       O.hash_bits(steps, [p])) for p in range(P)]
+        else:
+            per_pe = [O.draw_from_pool(pool, cfg["batch"], RUN_SEED, O.hash_bits(steps, [p]))
+                      for p in range(P)]
+        mode = 0 if coop else 1
+        own = owner if coop else None
+        if onfly:
+            ts, tg, rows = O.reference_step_onfly(rg, FEAT_SEED, cfg["dim"], mode, own, P,
+                                                  per_pe, L, kind, cfg["fanouts"][0], sched)
+        else:
+            ts, tg, rows = O.reference_step(rg, fs, mode, own, P, per_pe, L, kind,
+                                            cfg["fanouts"][0], sched)
         per_step.append(ts + tg)
         spent += ts + tg
-        seeds_done += P * cfg["batch"]
+        seeds_done += sum(len(x) for x in per_pe)
         sched = O.advance(sched)
         steps += 1
-    desc = (f"{steps} step(s) x indep_sample over {P} parts x {cfg['batch']} seeds "
-            f"(reference parallel_for over parts, COOPBATCH_THREADS={threads}) + per-part "
-            f"FeatureStore::load_rows of f64 rows; FeatureStore synth {synth_s:.1f}s excluded")
+    what = (f"coop_sample over {P} parts x {cfg['batch']} seeds + load_rows(owner_sets) + "
+            "all_to_all_forward" if coop else
+            f"indep_sample over {P} parts x {cfg['batch']} seeds + per-part load_rows")
+    rows_how = ("rows computed from FeatureStore::synth's formula with the reference's "
+                "hash (the f64 store would be "
+                f"{csr.n * cfg['dim'] * 8 / 1e9:.0f} GB), parallel over parts"
+                if onfly else f"f64 FeatureStore rows (synth {synth_s:.1f}s excluded)")
+    desc = (f"{steps} step(s) x {what} (reference parallel_for over parts, "
+            f"COOPBATCH_THREADS={threads}); {rows_how}")
     return seeds_done / spent, min(P, threads), desc, per_step
 
 
@@ -187,16 +223,18 @@ def run_reference(args, cfg):
     csr = O.rmat(cfg["n"], cfg["m"], GRAPH_SEED)
     gen_s = time.time() - t0
     threads = os.cpu_count() or 1
-    # probe one single-part batch to size the per-step sample
-    _, _, _, probe = cpu_reference_leg(cfg, csr, 0.0, parts_per_step=1, max_steps=1)
+    coop_parts = world if world > 1 else 0
+    # probe one batch to size the per-step sample
+    _, _, _, probe = cpu_reference_leg(cfg, csr, 0.0, parts_per_step=1, max_steps=1,
+                                       coop_parts=coop_parts)
     per_batch = max(probe[0], 1e-3)
-    budget = 90.0
+    budget = 120.0
     P = int(max(1, min(threads, budget / max(1, args.steps + args.warmup) / per_batch)))
-    from oracle import oracle as O2  # noqa: F401
     value, cores, desc, per_step = cpu_reference_leg(
-        cfg, csr, float("inf"), parts_per_step=P, max_steps=args.warmup + args.steps)
+        cfg, csr, float("inf"), parts_per_step=P, max_steps=args.warmup + args.steps,
+        coop_parts=coop_parts)
     timed = per_step[args.warmup:] or per_step
-    seeds = P * cfg["batch"] * len(timed)
+    seeds = (coop_parts or P) * cfg["batch"] * len(timed)
     v = seeds / sum(timed)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "seeds/s",
@@ -204,8 +242,11 @@ def run_reference(args, cfg):
         "ms_per_step": 1000 * sum(timed) / len(timed), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64 rows / u32 ids",
         "data": "synthetic (hash-keyed R-MAT, hashed features)",
-        "config": {"workload": cfg["workload"], "parts_per_step": P,
-                   "graph_gen_s": round(gen_s, 1)},
+        "config": {"workload": cfg["workload"],
+                   "mode": (f"cooperative (P={world} parts)" if coop_parts else
+                            f"indep ({P} independent minibatches per step)"),
+                   "graph_gen_s": round(gen_s, 1),
+                   "graph_gen": "oracle R-MAT on the host cores (ob_rmat_par)"},
         "cpu_baseline": {"value": v, "unit": "seeds/s", "cores": cores, "kind": "reference",
                          "sample": desc},
         "e2e": {"value": v, "unit": "seeds/s", "h2d_bytes_per_step": 0,
@@ -271,15 +312,14 @@ def concavity_evidence(cb, g, scfg, L, b, row_bytes, dev, parts=(1, 2, 4, 8)):
 
 
 # ---------------------------------------------------------- scale evidence --
-def scale_evidence(cb, dev, steps=20, parts=(1, 8)):
-    """north_star's target workload on one B200: config 4 (papers100M-shaped
-    R-MAT, 111M V / 1.6B E, 128 fp16 rows), independent P=1 throughput with
-    the same timing as the headline (CUDA graphs, L2 flushed, events), the
-    gather's roofline, and cooperative vs independent per-seed work at P=8
-    (simulated parts on this GPU)."""
+def scale_evidence(cb, dev, name="c2", steps=20, parts=(1, 8)):
+    """Another BASELINE config on one B200 (c2 products-shaped when the
+    headline is c4): one batch at a time (CUDA graphs, L2 flushed, events),
+    the gather's roofline, and cooperative vs independent per-seed work at
+    P = 1 and 8 (simulated parts on this GPU)."""
     import torch
 
-    c = CONFIGS["c4"]
+    c = CONFIGS[name]
     t0 = time.time()
     g = cb.Graph.generate_rmat(c["n"], c["m"], GRAPH_SEED, device=dev)
     gen_s = time.time() - t0
@@ -320,6 +360,7 @@ def scale_evidence(cb, dev, steps=20, parts=(1, 8)):
             ms.append(e[0].elapsed_time(e[1]))
             gms.append(e[2].elapsed_time(e[3]))
     rows = plan.layer_sizes(0, L - 1)["n_src"]
+    store_row_bytes = store.row_bytes
     gbytes = rows * (2 * store.row_bytes + 4)
     peak, _ = peaks()
     out = {"workload": c["workload"], "graph_gen_s": round(gen_s, 2),
@@ -329,7 +370,7 @@ def scale_evidence(cb, dev, steps=20, parts=(1, 8)):
                       "frac": gbytes / (np.mean(gms) / 1e3) / 1e9 / peak},
            "per_layer": [plan.layer_sizes(0, l) for l in range(L)]}
     del plan, store
-    out["concavity"] = concavity_evidence(cb, g, scfg, L, b, c["dim"] * 2, dev, parts=parts)
+    out["concavity"] = concavity_evidence(cb, g, scfg, L, b, store_row_bytes, dev, parts=parts)
     del g
     return out
 
@@ -825,7 +866,9 @@ def run_ours(args, cfg):
     if world == 1 and not args.no_evidence:
         line["evidence"]["concavity"] = concavity_evidence(cb, g, scfg, L, b, row_bytes, dev)
         line["evidence"]["kappa"] = kappa_evidence(cb, dev)
-        line["evidence"]["papers100m"] = scale_evidence(cb, dev)
+        other = "c2" if args.config == "c4" else "c4"
+        line["evidence"]["products_c2" if other == "c2" else "papers100m"] = \
+            scale_evidence(cb, dev, other)
         line["evidence"]["mag240m_batch_sweep"] = batch_sweep_evidence(cb, dev)
         line["evidence"]["work_curves"] = work_curve_evidence(cb, dev, not args.no_cpu_baseline)
     if world == 1 and not args.no_cpu_baseline:
@@ -880,7 +923,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-evidence", action="store_true")

@@ -310,13 +310,16 @@ static int rmat_scale(uint64_t n) {
 static inline int rmat_attempt(uint64_t pfx13, int s, uint64_t a, uint64_t n,
                                uint64_t* src, uint64_t* dst) {
   const uint64_t ha = hstep(pfx13, a);
-  uint64_t sr = 0, ds = 0, w = 0;
-  for (int i = 0; i < s; ++i) {
-    if ((i & 3) == 0) w = hstep(ha, (uint64_t)(i >> 2));
-    const uint32_t u = (uint32_t)((w >> (16 * (i & 3))) & 0xffffu);
-    const uint32_t q = (u >= RMAT_T1) + (u >= RMAT_T2) + (u >= RMAT_T3);
-    sr = (sr << 1) | (q >> 1);
-    ds = (ds << 1) | (q & 1u);
+  uint64_t sr = 0, ds = 0;
+  for (int k = 0; 4 * k < s; ++k) { /* levels 4k..4k+3 share hash_bits(seed,{13,a,k}) */
+    const uint64_t w = hstep(ha, (uint64_t)k);
+    const int lv = s - 4 * k < 4 ? s - 4 * k : 4;
+    for (int l = 0; l < lv; ++l) {
+      const uint32_t u = (uint32_t)(w >> (16 * l)) & 0xffffu;
+      const uint32_t q = (u >= RMAT_T1) + (u >= RMAT_T2) + (u >= RMAT_T3);
+      sr = (sr << 1) | (q >> 1);
+      ds = (ds << 1) | (q & 1u);
+    }
   }
   *src = sr;
   *dst = ds;
@@ -425,6 +428,264 @@ int ob_rmat(uint64_t n, uint64_t m_target, uint64_t seed, uint64_t** indptr_out,
   free(ed);
   *indptr_out = indptr;
   *indices_out = indices;
+  return 0;
+}
+
+/* Parallel form of ob_rmat for the large configs (c4: 1.6B edges), same
+ * result bit for bit (tests/test_oracle_golden.py compares the two). The
+ * sequential walk "take the first m attempts whose (src,dst) pair is new" is
+ * split by destination range:
+ *   1. count the valid attempts per (thread range, dst bucket);
+ *   2. scatter attempt indices into their bucket, ascending (stable);
+ *   3. per bucket, a hash set over its pairs marks each pair's first attempt
+ *      (pairs of different buckets never collide: the bucket is part of dst);
+ *   4. the m-th marked attempt in attempt order is the cutoff;
+ *   5. per bucket, the marked attempts up to the cutoff are counted per dst
+ *      and placed in attempt order (build_csr order, graph.cpp:17-48).
+ * Attempts are pure functions of their index: pass 1 recomputes them to
+ * count, pass 2 stores each valid attempt's pair next to its index. Memory:
+ * 13 B per attempt + the CSR. */
+typedef struct {
+  uint64_t pfx13, n, A;
+  int s, bshift;
+  const rmat_perm* pm;
+  uint32_t nb, nt;
+  uint64_t* cnt;        /* [nt][nb] valid attempts, then write cursors */
+  uint32_t* arr;        /* [valid] attempt indices grouped by bucket */
+  uint64_t* pair;       /* [valid] dst << 32 | src of arr[i] */
+  uint64_t* bstart;     /* [nb+1] */
+  uint8_t* surv;        /* [A] first attempt of its pair */
+  uint64_t a_star;      /* last kept attempt */
+  uint64_t* indptr;     /* [n+1] */
+  uint32_t* indices;
+  uint64_t* bkept;      /* [nb] kept edges per bucket */
+  uint64_t* tsurv;      /* [nt] survivors per thread range */
+  volatile uint32_t next;
+  int phase;
+} rmatp_job;
+
+typedef struct {
+  rmatp_job* j;
+  uint32_t tid;
+} rmatp_arg;
+
+static inline int rmatp_pair(const rmatp_job* j, uint64_t a, uint32_t* src, uint32_t* dst,
+                             int need_src) {
+  uint64_t sr, ds;
+  if (!rmat_attempt(j->pfx13, j->s, a, j->n, &sr, &ds) || sr == ds) return 0;
+  *dst = (uint32_t)perm_walk(j->pm, ds, j->n);
+  if (need_src) *src = (uint32_t)perm_walk(j->pm, sr, j->n);
+  return 1;
+}
+
+static void rmatp_bucket(rmatp_job* j, uint32_t b, uint64_t** tab, uint64_t* tcap,
+                         uint64_t** cur, uint64_t* ccap) {
+  const uint64_t lo = j->bstart[b], hi = j->bstart[b + 1];
+  const uint64_t d0 = (uint64_t)b << j->bshift;
+  uint64_t d1 = d0 + (1ULL << j->bshift);
+  if (d1 > j->n) d1 = j->n;
+  if (j->phase == 3) { /* first attempt of each pair */
+    uint64_t cap = 64;
+    while (cap < 2 * (hi - lo) + 2) cap <<= 1;
+    if (cap > *tcap) {
+      free(*tab);
+      *tab = xmalloc(cap * sizeof(uint64_t));
+      *tcap = cap;
+    }
+    uint64_t* t = *tab;
+    memset(t, 0, cap * sizeof(uint64_t));
+    for (uint64_t i = lo; i < hi; ++i) {
+      const uint64_t a = j->arr[i];
+      const uint64_t key = j->pair[i]; /* never 0: no self loops */
+      uint64_t h = ob_mix64(key) & (cap - 1);
+      int dup = 0;
+      while (t[h]) {
+        if (t[h] == key) { dup = 1; break; }
+        h = (h + 1) & (cap - 1);
+      }
+      if (!dup) {
+        t[h] = key;
+        j->surv[a] = 1;
+      }
+    }
+  } else if (j->phase == 5) { /* per-dst counts of the kept attempts */
+    uint64_t k = 0;
+    for (uint64_t i = lo; i < hi; ++i) {
+      const uint64_t a = j->arr[i];
+      if (a > j->a_star || !j->surv[a]) continue;
+      j->indptr[(j->pair[i] >> 32) + 1] += 1;
+      ++k;
+    }
+    j->bkept[b] = k;
+  } else if (j->phase == 6) { /* counts -> offsets within the bucket */
+    uint64_t run = 0;
+    for (uint64_t b2 = 0; b2 < b; ++b2) run += j->bkept[b2];
+    for (uint64_t d = d0; d < d1; ++d) {
+      const uint64_t c = j->indptr[d + 1];
+      j->indptr[d + 1] = run + c;
+      run += c;
+    }
+  } else { /* phase 7: place src ids in attempt order */
+    const uint64_t w = d1 - d0;
+    if (w > *ccap) {
+      free(*cur);
+      *cur = xmalloc(w * sizeof(uint64_t));
+      *ccap = w;
+    }
+    uint64_t* c = *cur;
+    for (uint64_t d = d0; d < d1; ++d) c[d - d0] = j->indptr[d];
+    for (uint64_t i = lo; i < hi; ++i) {
+      const uint64_t a = j->arr[i];
+      if (a > j->a_star || !j->surv[a]) continue;
+      const uint64_t key = j->pair[i];
+      j->indices[c[(key >> 32) - d0]++] = (uint32_t)key;
+    }
+  }
+}
+
+static void* rmatp_worker(void* argp) {
+  rmatp_arg* arg = argp;
+  rmatp_job* j = arg->j;
+  const uint32_t t = arg->tid;
+  const uint64_t lo = j->A * t / j->nt, hi = j->A * (t + 1) / j->nt;
+  if (j->phase == 1 || j->phase == 2) {
+    uint64_t* c = j->cnt + (uint64_t)t * j->nb;
+    for (uint64_t a = lo; a < hi; ++a) {
+      uint32_t sr = 0, ds = 0;
+      if (!rmatp_pair(j, a, &sr, &ds, j->phase == 2)) continue;
+      const uint32_t b = ds >> j->bshift;
+      if (j->phase == 1) {
+        c[b]++;
+      } else {
+        j->pair[c[b]] = ((uint64_t)ds << 32) | sr;
+        j->arr[c[b]++] = (uint32_t)a;
+      }
+    }
+  } else if (j->phase == 4) {
+    uint64_t k = 0;
+    for (uint64_t a = lo; a < hi; ++a) k += j->surv[a];
+    j->tsurv[t] = k;
+  } else {
+    uint64_t* tab = NULL, *cur = NULL;
+    uint64_t tcap = 0, ccap = 0;
+    for (;;) {
+      const uint32_t b = __atomic_fetch_add(&j->next, 1, __ATOMIC_RELAXED);
+      if (b >= j->nb) break;
+      rmatp_bucket(j, b, &tab, &tcap, &cur, &ccap);
+    }
+    free(tab);
+    free(cur);
+  }
+  return NULL;
+}
+
+#include <time.h>
+static void rmatp_run(rmatp_job* j, int phase) {
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  j->phase = phase;
+  j->next = 0;
+  pthread_t th[64];
+  rmatp_arg args[64];
+  for (uint32_t t = 0; t < j->nt; ++t) {
+    args[t].j = j;
+    args[t].tid = t;
+    pthread_create(&th[t], NULL, rmatp_worker, &args[t]);
+  }
+  for (uint32_t t = 0; t < j->nt; ++t) pthread_join(th[t], NULL);
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  if (getenv("OB_RMAT_TIMING"))
+    fprintf(stderr, "rmat phase %d: %.3f s\n", phase,
+            (t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec));
+}
+
+int ob_rmat_par(uint64_t n, uint64_t m_target, uint64_t seed, uint64_t** indptr_out,
+                uint32_t** indices_out) {
+  if (n < 2 || n > 0xFFFFFFFFULL) return fail("rmat: need 2 <= n < 2^32");
+  if (m_target > n * (n - 1)) return fail("rmat: more edges than simple pairs");
+  if (m_target == 0) {
+    *indptr_out = calloc(n + 1, sizeof(uint64_t));
+    *indices_out = xmalloc(4);
+    return *indptr_out ? 0 : fail("rmat: out of memory");
+  }
+  const int s = rmat_scale(n);
+  const rmat_perm pm = perm_make(seed, s);
+  long nt = sysconf(_SC_NPROCESSORS_ONLN);
+  if (nt < 1) nt = 1;
+  if (nt > 64) nt = 64;
+  rmatp_job j;
+  memset(&j, 0, sizeof(j));
+  j.pfx13 = hstep(hinit(seed), 13);
+  j.n = n;
+  j.s = s;
+  j.pm = &pm;
+  j.nt = (uint32_t)nt;
+  j.bshift = s > 9 ? s - 9 : 0; /* <= 512 buckets: few write streams per thread */
+  j.nb = (uint32_t)((n + (1ULL << j.bshift) - 1) >> j.bshift);
+  uint64_t A = m_target + m_target / 4 + 4096;
+  for (int round = 0;; ++round) {
+    if (A >= (1ULL << 32) - 1) return fail("rmat: attempt count exceeds 2^32");
+    j.A = A;
+    j.cnt = calloc((size_t)j.nt * j.nb, sizeof(uint64_t));
+    j.bstart = xmalloc((j.nb + 1) * sizeof(uint64_t));
+    rmatp_run(&j, 1);
+    uint64_t valid = 0;
+    for (uint32_t b = 0; b < j.nb; ++b) {
+      j.bstart[b] = valid;
+      for (uint32_t t = 0; t < j.nt; ++t) {
+        const uint64_t c = j.cnt[(uint64_t)t * j.nb + b];
+        j.cnt[(uint64_t)t * j.nb + b] = valid;
+        valid += c;
+      }
+    }
+    j.bstart[j.nb] = valid;
+    j.arr = xmalloc(valid * sizeof(uint32_t));
+    j.pair = xmalloc(valid * sizeof(uint64_t));
+    rmatp_run(&j, 2);
+    free(j.cnt);
+    j.cnt = NULL;
+    j.surv = calloc(A, 1);
+    if (!j.surv) return fail("rmat: out of memory");
+    rmatp_run(&j, 3);
+    j.tsurv = calloc(j.nt, sizeof(uint64_t));
+    rmatp_run(&j, 4);
+    uint64_t total = 0;
+    for (uint32_t t = 0; t < j.nt; ++t) total += j.tsurv[t];
+    if (total >= m_target) {
+      uint64_t before = 0;
+      uint32_t t = 0;
+      while (before + j.tsurv[t] < m_target) before += j.tsurv[t++];
+      uint64_t a = A * t / j.nt;
+      for (;; ++a)
+        if (j.surv[a] && ++before == m_target) break;
+      j.a_star = a;
+      free(j.tsurv);
+      break;
+    }
+    free(j.tsurv);
+    free(j.arr);
+    free(j.pair);
+    free(j.surv);
+    free(j.bstart);
+    if (round >= 8) return fail("rmat: could not reach the edge target (graph too dense)");
+    uint64_t A2 = A * 2;
+    if (A2 < m_target + (m_target - total) * 4) A2 = m_target + (m_target - total) * 4;
+    A = A2;
+  }
+  j.indptr = calloc(n + 1, sizeof(uint64_t));
+  j.indices = xmalloc(m_target * sizeof(uint32_t));
+  j.bkept = calloc(j.nb, sizeof(uint64_t));
+  if (!j.indptr) return fail("rmat: out of memory");
+  rmatp_run(&j, 5);
+  rmatp_run(&j, 6);
+  rmatp_run(&j, 7);
+  free(j.bkept);
+  free(j.arr);
+  free(j.pair);
+  free(j.surv);
+  free(j.bstart);
+  *indptr_out = j.indptr;
+  *indices_out = j.indices;
   return 0;
 }
 

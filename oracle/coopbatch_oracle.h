@@ -43,6 +43,9 @@ void ob_sched_advance(ob_sched* s);
  * Allocates *indptr (n+1) and *indices (m_target) with malloc. */
 int ob_rmat(uint64_t n, uint64_t m_target, uint64_t seed, uint64_t** indptr,
             uint32_t** indices);
+/* Same graph as ob_rmat, built in parallel by destination bucket (large m). */
+int ob_rmat_par(uint64_t n, uint64_t m_target, uint64_t seed, uint64_t** indptr,
+                uint32_t** indices);
 /* graph.cpp:17-48 (stable counting sort by dst, duplicates kept) */
 int ob_build_csr(const uint32_t* src, const uint32_t* dst, uint64_t m,
                  uint64_t n, uint64_t* indptr, uint32_t* indices);

@@ -105,6 +105,7 @@ def lib(impl: str = "restated") -> C.CDLL:
         L.ob_sched_advance.argtypes = [C.POINTER(Sched)]
         L.ob_rmat.argtypes = [_u64, _u64, _u64, C.POINTER(C.POINTER(_u64)),
                               C.POINTER(C.POINTER(_u32))]
+        L.ob_rmat_par.argtypes = L.ob_rmat.argtypes
         L.ob_build_csr.argtypes = [_P, _P, _u64, _u64, _P, _P]
         L.ob_partition_random.argtypes = [_u64, _u32, _u64, _P]
         L.ob_sample_block.argtypes = [_P, _P, _u64, _P, _u64, C.c_int, _u32,
@@ -169,6 +170,8 @@ def lib(impl: str = "restated") -> C.CDLL:
         L.rf_step.argtypes = [_P, _P, C.c_int, _P, _u32, _P, _P, C.c_int, C.c_int, _u32,
                               C.POINTER(Sched), C.POINTER(_f64), C.POINTER(_f64),
                               C.POINTER(_u64)]
+        L.rf_step_onfly.argtypes = [_P, _u64, _u32, C.c_int, _P, _u32, _P, _P, C.c_int,
+                                    C.c_int, _u32, C.POINTER(Sched), _P, _P, _P]
         L.rf_train_step.argtypes = [_P, _P, C.c_int, _P, _u32, _P, _P, C.c_int, C.c_int, _u32,
                                     C.POINTER(Sched), _u32, _u64, C.POINTER(_f64), _P]
         L.rf_cross_edge_ratio.argtypes = [_P, _P, _u32, C.POINTER(_f64)]
@@ -262,11 +265,16 @@ class CSR:
         return len(self.indices)
 
 
-def rmat(n: int, m: int, seed: int) -> CSR:
+def rmat(n: int, m: int, seed: int, parallel: bool | None = None) -> CSR:
+    """Hash-keyed R-MAT. `parallel` (default: m > 2^22) uses the bucketed
+    multi-threaded form, which builds the same CSR."""
     L = lib("restated")
     ip = C.POINTER(_u64)()
     ix = C.POINTER(_u32)()
-    _check(L.ob_rmat(n, m, seed, C.byref(ip), C.byref(ix)), L)
+    if parallel is None:
+        parallel = m > (1 << 22)
+    fn = L.ob_rmat_par if parallel else L.ob_rmat
+    _check(fn(n, m, seed, C.byref(ip), C.byref(ix)), L)
     g = CSR(_arr(ip, n + 1, np.uint64), _arr(ix, m, np.uint32))
     L.ob_free(C.cast(ip, C.c_void_p))
     L.ob_free(C.cast(ix, C.c_void_p))
@@ -660,6 +668,24 @@ def reference_step(rg: RefGraph, fs: RefFeatureStore, mode: int, owner, parts: i
     _check(rg.L.rf_step(rg.h, fs.h, mode, _ptr(own), parts, _ptr(flat), _ptr(off), num_layers,
                         kind, fanout, C.byref(sched), C.byref(ts), C.byref(tg),
                         C.byref(rows)), rg.L)
+    return ts.value, tg.value, rows.value
+
+
+def reference_step_onfly(rg: RefGraph, feat_seed: int, dim: int, mode: int, owner,
+                         parts: int, per_pe_seeds, num_layers: int, kind: int, fanout: int,
+                         sched: Sched):
+    """reference_step with load_rows replaced by rows computed from
+    FeatureStore::synth's formula (for graphs whose f64 store does not fit);
+    returns (t_sample_s, t_gather_s, rows)."""
+    flat = np.ascontiguousarray(np.concatenate(
+        [np.asarray(s, dtype=np.uint32) for s in per_pe_seeds]), dtype=np.uint32)
+    off = np.zeros(parts + 1, np.uint64)
+    off[1:] = np.cumsum([len(s) for s in per_pe_seeds])
+    own = None if owner is None else np.ascontiguousarray(owner, dtype=np.uint32)
+    ts, tg, rows = C.c_double(), C.c_double(), C.c_uint64()
+    _check(rg.L.rf_step_onfly(rg.h, feat_seed, dim, mode, _ptr(own), parts, _ptr(flat),
+                              _ptr(off), num_layers, kind, fanout, C.byref(sched),
+                              C.byref(ts), C.byref(tg), C.byref(rows)), rg.L)
     return ts.value, tg.value, rows.value
 
 

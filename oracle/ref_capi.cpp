@@ -12,6 +12,7 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <span>
 #include <string>
 #include <vector>
 
@@ -19,6 +20,7 @@
 #include "coopbatch/cache.hpp"
 #include "coopbatch/coop.hpp"
 #include "coopbatch/graph.hpp"
+#include "coopbatch/parallel.hpp"
 #include "coopbatch/partition.hpp"
 #include "coopbatch/rng.hpp"
 #include "coopbatch/samplers.hpp"
@@ -487,6 +489,67 @@ int rf_step(void* g, void* fs, int mode, const uint32_t* owner, uint32_t parts,
       for (uint32_t p = 0; p < parts; ++p)
         rows += store.load_rows(stacks[p].input_vertices()).rows();
       const auto t2 = clk::now();
+      *t_sample = std::chrono::duration<double>(t1 - t0).count();
+      *t_gather = std::chrono::duration<double>(t2 - t1).count();
+    }
+    *rows_out = rows;
+  });
+}
+
+/* The same stock path for graphs whose f64 FeatureStore does not fit host
+ * memory (c4: 111M x 128 x 8 B = 113 GB): sampling is the
+ * reference's own coop_sample / indep_sample, and load_rows is replaced by
+ * computing each requested row from FeatureStore::synth's formula
+ * (coop.cpp:369-371: 2 * hash_uniform(seed, {kStreamFeature, v, j}) - 1) with
+ * the reference's hash, parallel over parts (parallel.hpp). Coop mode then
+ * runs the reference's all_to_all_forward on the owner rows. */
+static std::vector<double> rows_on_the_fly(std::span<const VertexId> ids, uint32_t dim,
+                                           uint64_t seed) {
+  std::vector<double> out(ids.size() * dim);
+  for (std::size_t r = 0; r < ids.size(); ++r)
+    for (uint32_t j = 0; j < dim; ++j)
+      out[r * dim + j] = 2.0 * hash_uniform(seed, {kStreamFeature, ids[r], j}) - 1.0;
+  return out;
+}
+
+int rf_step_onfly(void* g, uint64_t feat_seed, uint32_t dim, int mode, const uint32_t* owner,
+                  uint32_t parts, const uint32_t* seeds_flat, const uint64_t* seeds_off, int L,
+                  int kind, uint32_t fanout, const ob_sched* sched, double* t_sample,
+                  double* t_gather, uint64_t* rows_out) {
+  return guard([&] {
+    using clk = std::chrono::steady_clock;
+    const Graph& gr = *static_cast<Graph*>(g);
+    std::vector<std::vector<VertexId>> seeds(parts);
+    for (uint32_t p = 0; p < parts; ++p)
+      seeds[p].assign(seeds_flat + seeds_off[p], seeds_flat + seeds_off[p + 1]);
+    const SamplerConfig cfg = to_cfg(kind, fanout);
+    const SeedSchedule sc = to_sched(sched);
+    uint64_t rows = 0;
+    std::vector<std::vector<double>> part_rows(parts);
+    if (mode == 0) {
+      PartitionMap pm;
+      pm.num_parts = parts;
+      pm.owner.assign(owner, owner + gr.num_vertices);
+      const auto t0 = clk::now();
+      const CoopSampleResult r = coop_sample(gr, pm, seeds, L, cfg, sc);
+      const auto t1 = clk::now();
+      parallel_for(parts, [&](std::size_t p) {
+        part_rows[p] = rows_on_the_fly(r.owner_sets[p], dim, feat_seed);
+      });
+      const auto fwd = all_to_all_forward(r.exchanges[L - 1], part_rows, dim);
+      const auto t2 = clk::now();
+      for (const auto& f : fwd) rows += f.size() / dim;
+      *t_sample = std::chrono::duration<double>(t1 - t0).count();
+      *t_gather = std::chrono::duration<double>(t2 - t1).count();
+    } else {
+      const auto t0 = clk::now();
+      const auto stacks = indep_sample(gr, seeds, L, cfg, sc);
+      const auto t1 = clk::now();
+      parallel_for(parts, [&](std::size_t p) {
+        part_rows[p] = rows_on_the_fly(stacks[p].input_vertices(), dim, feat_seed);
+      });
+      const auto t2 = clk::now();
+      for (const auto& f : part_rows) rows += f.size() / dim;
       *t_sample = std::chrono::duration<double>(t1 - t0).count();
       *t_gather = std::chrono::duration<double>(t2 - t1).count();
     }

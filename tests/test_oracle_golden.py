@@ -126,3 +126,13 @@ def test_rmat_digest(G):
     for v in range(0, rm.n, 97):
         nb = rm.indices[rm.indptr[v]:rm.indptr[v + 1]]
         assert len(set(nb.tolist())) == len(nb) and v not in nb.tolist()
+
+
+@pytest.mark.parametrize("n,m,seed", [(1 << 12, 1 << 15, 7), (1 << 16, 1 << 20, 42),
+                                      (5000, 3_000_000, 3), (3, 6, 1), (100, 0, 1)])
+def test_rmat_parallel_equals_sequential(n, m, seed):
+    """ob_rmat_par (bucketed, multi-threaded; builds the c4 graph for the
+    reference arm and tests/golden/c4_csr.json) == the sequential ob_rmat."""
+    a = O.rmat(n, m, seed, parallel=False)
+    b = O.rmat(n, m, seed, parallel=True)
+    assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
