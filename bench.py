@@ -863,6 +863,9 @@ def run_ours(args, cfg):
                      "feature_bytes_per_step": rows_last * row_bytes},
         "clocks": clocks.summary(),
     }
+    plans.clear()  # the evidence runs make their own plans
+    streams.clear()
+    plan = p2 = None  # noqa: F841
     if world == 1 and not args.no_evidence:
         line["evidence"]["concavity"] = concavity_evidence(cb, g, scfg, L, b, row_bytes, dev)
         line["evidence"]["kappa"] = kappa_evidence(cb, dev)

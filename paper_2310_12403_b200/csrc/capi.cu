@@ -86,7 +86,12 @@ void plan_alloc(cb_plan* pl) {
       b.edges = pl->mem.alloc<uint2>(b.cap_edges);
       b.src = pl->mem.alloc<uint32_t>(b.cap_src);
       b.dst_pos = pl->mem.alloc<uint32_t>(cd);
-      max_tiles = std::max(max_tiles, ceil_div(sum_deg, kLaborTile) + 2);
+      // the scan space (stage: 8 B per position) is also bounded by a budget
+      // that grows with the retries: sum_deg alone is m at large graphs (c4:
+      // 1.6B positions = 13 GB of stage per plan for a 48M-position layer)
+      const uint64_t scan_cap = std::min(
+          sum_deg, sat_mul(kScanBudget, static_cast<uint64_t>(std::ceil(pl->grow))));
+      max_tiles = std::max(max_tiles, ceil_div(scan_cap, kLaborTile) + 2);
       max_tiles = std::max(max_tiles, ceil_div(cd, kFrontierTile) + 2);
       if (P > 1 || pl->dist_world > 0) {
         w.loc_part.push_back(pl->mem.alloc<uint32_t>(b.cap_src));
