@@ -663,9 +663,9 @@ void require_batch(const cb_plan* pl, uint32_t p, int l) {
   require(l >= 0 && l < pl->L, "layer index out of range");
 }
 
-void prepare_rows(cb_plan* pl, const cb_features* f) {
+void prepare_rows(cb_plan* pl, const cb_features* f, bool any_row) {
   require(f->n_rows == pl->g->g.n, "feature table does not match the graph");
-  require_full_table(f);
+  if (any_row) require_full_table(f);
   for (uint32_t p = 0; p < pl->P; ++p) {
     PeWork& w = pl->pe[p];
     const LayerBufs& b = w.L[pl->L - 1];
@@ -1657,9 +1657,14 @@ int cb_gather_rows(const cb_features* f, const uint32_t* d_ids, uint64_t n, void
                    void* stream) {
   return guard([&] {
     require(f != nullptr, "null features");
-    require_full_table(f);
     DeviceGuard dg(f->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (f->shard_rows) {  // a single-part shard serves only its own rows
+      DevBuf flag(8);
+      require(shard_holds(d_ids, n, f->row_map, f->shard_r0, f->shard_rows,
+                          flag.as<unsigned>(), st),
+              "gather from a shard table: an id is not owned by the shard");
+    }
     launch_gather(f->table, vec_bytes_for(f->row_bytes), f->row_bytes, d_ids, nullptr, n,
                   f->row_map, d_out, st);
     CB_CUDA(cudaStreamSynchronize(st));

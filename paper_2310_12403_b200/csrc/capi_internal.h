@@ -298,7 +298,9 @@ inline void require_full_table(const cb_features* f) {
   require(f->shard_rows == 0,
           "this gather needs a full feature table (got a single-part shard)");
 }
-void prepare_rows(cb_plan* pl, const cb_features* f);
+// Sizes the plan's row buffers for f. any_row: the gather reads f at any
+// vertex (not only this shard's own rows).
+void prepare_rows(cb_plan* pl, const cb_features* f, bool any_row = true);
 void enqueue_gather(cb_plan* pl, const cb_features* f);
 }  // namespace capi
 }  // namespace cb

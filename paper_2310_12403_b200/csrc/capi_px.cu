@@ -265,7 +265,7 @@ int cb_px_gather(cb_plan* plan, const cb_features* local) {
     for (uint32_t q = 0; q < px.world; ++q)
       require(px.fbase[q] != nullptr, "feature shard of a rank not connected");
     DeviceGuard dg(plan->device);
-    prepare_rows(plan, local);
+    prepare_rows(plan, local, false);  // rows come from the owners' shards
     PeWork& w = plan->pe[0];
     const int L = plan->L;
     launch_px_gather(px.d_fbase, px.owner, local->row_map, local->row_bytes, w.L[L - 1].src,

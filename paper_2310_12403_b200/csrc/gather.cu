@@ -121,6 +121,29 @@ void launch_gather(const void* table, int vec_bytes, uint64_t row_bytes, const u
   CB_LAUNCH("gather");
 }
 
+namespace {
+__global__ void shard_check_kernel(const uint32_t* __restrict__ ids, uint64_t n,
+                                   const uint32_t* __restrict__ row_map, uint64_t r0,
+                                   uint64_t rows, unsigned* bad) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    if (static_cast<uint64_t>(row_map[ids[i]]) - r0 >= rows) atomicOr(bad, 1u);
+}
+}  // namespace
+
+bool shard_holds(const uint32_t* ids, uint64_t n, const uint32_t* row_map, uint64_t r0,
+                 uint64_t rows, unsigned* d_flag, cudaStream_t st) {
+  CB_CUDA(cudaMemsetAsync(d_flag, 0, 4, st));
+  if (n) {
+    launch_k(shard_check_kernel, kNumSMs * 4, 256, st, ids, n, row_map, r0, rows, d_flag);
+    CB_LAUNCH("shard_check");
+  }
+  unsigned h = 0;
+  CB_CUDA(cudaMemcpyAsync(&h, d_flag, 4, cudaMemcpyDeviceToHost, st));
+  CB_CUDA(cudaStreamSynchronize(st));
+  return h == 0;
+}
+
 void launch_relabel_gather(const RelabelArgs& r, uint64_t relabel_work, const void* table,
                            int vec_bytes, uint64_t row_bytes, const uint32_t* ids,
                            const unsigned long long* count, uint64_t cap_rows,

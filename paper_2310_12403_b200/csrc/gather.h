@@ -20,6 +20,9 @@ void launch_relabel_gather(const RelabelArgs& r, uint64_t relabel_work, const vo
 void launch_synth(uint64_t seed, uint32_t dim, int dtype, uint64_t n_rows,
                   const uint32_t* row_vertex, uint64_t v_base, void* out, cudaStream_t st);
 int vec_bytes_for(uint64_t row_bytes);
+// true iff every id's row lies in the shard [r0, r0 + rows) (synchronises st)
+bool shard_holds(const uint32_t* ids, uint64_t n, const uint32_t* row_map, uint64_t r0,
+                 uint64_t rows, unsigned* d_flag, cudaStream_t st);
 
 // graph.cu
 void graph_generate_rmat(DeviceGraph& g, uint64_t n, uint64_t m, uint64_t seed,

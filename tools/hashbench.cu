@@ -1,0 +1,121 @@
+// labor_mark keep-test throughput on B200 (not part of the product):
+// keep(t) = mix64(p1 ^ t) <= T for N neighbour ids, two hash formulations:
+//   V0: SplitMix64 as written (64-bit shifts -> SHF/LOP3 on the ALU pipe)
+//   V1: pipe-balanced: the 64-bit add and the first two xor-shifts' shifts are
+//       IMADs with an opaque multiplier (fma pipe), the rest stays on the ALU
+// each from HBM (ids read coalesced) and compute-only (ids from the index).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o hashbench tools/hashbench.cu
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+struct Bal {  // per-launch constants; the multipliers are opaque to ptxas
+  uint32_t p1_lo;
+  uint64_t k0;          // (p1_hi << 32) + golden gamma
+  uint32_t one, m30, m27;  // 1, 2^2, 2^5
+};
+
+// mix64(p1 ^ t) for 32-bit t with the high word of p1 folded into k0.
+__device__ __forceinline__ uint64_t mix64_bal(const Bal& b, uint32_t t) {
+  const uint32_t lo0 = t ^ b.p1_lo;
+  uint64_t z = static_cast<uint64_t>(lo0) * b.one + b.k0;  // IMAD.WIDE.U32
+  uint32_t lo = static_cast<uint32_t>(z), hi = static_cast<uint32_t>(z >> 32);
+  // z ^= z >> 30: funnel = hi * 4 + (lo >> 30), hi >> 30 = umulhi(hi, 4)
+  uint32_t f = hi * b.m30 + __umulhi(lo, b.m30);
+  lo ^= f;
+  hi ^= __umulhi(hi, b.m30);
+  // z *= c1
+  uint64_t w = static_cast<uint64_t>(lo) * 0x1ce4e5b9u;
+  hi = static_cast<uint32_t>(w >> 32) + lo * 0xbf58476du + hi * 0x1ce4e5b9u;
+  lo = static_cast<uint32_t>(w);
+  // z ^= z >> 27
+  f = hi * b.m27 + __umulhi(lo, b.m27);
+  lo ^= f;
+  hi ^= __umulhi(hi, b.m27);
+  // z *= c2
+  w = static_cast<uint64_t>(lo) * 0x133111ebu;
+  hi = static_cast<uint32_t>(w >> 32) + lo * 0x94d049bbu + hi * 0x133111ebu;
+  lo = static_cast<uint32_t>(w);
+  z = (static_cast<uint64_t>(hi) << 32) | lo;
+  return z ^ (z >> 31);
+}
+
+template <int V, bool LOAD>
+__global__ void __launch_bounds__(128, 8) keep_k(const uint32_t* __restrict__ ids, uint64_t n,
+                                                 uint64_t p1, Bal b, uint64_t T,
+                                                 unsigned long long* out) {
+  uint32_t cnt = 0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 8;
+  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * blockDim.x) * 8 + threadIdx.x;
+       base < n; base += stride) {
+    uint32_t tv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      tv[j] = LOAD ? __ldg(ids + base + 32 * j) : static_cast<uint32_t>(base + 32 * j) * 2654435761u;
+    uint32_t km = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t h = V == 0 ? mix64(p1 ^ tv[j]) : mix64_bal(b, tv[j]);
+      km |= (h <= T ? 1u : 0u) << j;
+    }
+    cnt += __popc(km);
+  }
+  if (cnt) atomicAdd(out, cnt);
+}
+
+int main() {
+  const uint64_t N = 48ull << 20;  // ~ c4 layer-3 scan (48M positions), 192 MB
+  std::vector<uint32_t> h(N);
+  uint64_t x = 88172645463325252ULL;
+  for (uint64_t i = 0; i < N; ++i) {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    h[i] = static_cast<uint32_t>(x % 111059956u);
+  }
+  uint32_t* ids;
+  unsigned long long* out;
+  CK(cudaMalloc(&ids, N * 4));
+  CK(cudaMalloc(&out, 8));
+  CK(cudaMemcpy(ids, h.data(), N * 4, cudaMemcpyHostToDevice));
+  void* flush;
+  CK(cudaMalloc(&flush, 512u << 20));
+  const uint64_t p1 = 0x0123456789abcdefULL;
+  Bal b;
+  b.p1_lo = static_cast<uint32_t>(p1);
+  b.k0 = (p1 & 0xffffffff00000000ULL) + 0x9e3779b97f4a7c15ULL;
+  b.one = 1; b.m30 = 4; b.m27 = 32;
+  const uint64_t T = (14ull << 11) | 0x7ff;  // th ~ k/d for a d ~ 5e9/14 hub: rare keeps
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto run = [&](auto kern, const char* name) {
+    unsigned long long res[2];
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(out, 0, 8);
+      cudaMemset(flush, rep, 512u << 20);
+      cudaEventRecord(e0);
+      kern<<<148 * 8, 128>>>(ids, N, p1, b, ~0ull >> 8, out);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      cudaMemcpy(&res[rep], out, 8, cudaMemcpyDeviceToHost);
+      if (rep) printf("%-28s %8.1f us  %.3f Gpos/s  kept %llu\n", name, ms * 1e3, N / (ms * 1e6), res[rep]);
+    }
+  };
+  (void)T;
+  run(keep_k<0, true>, "V0 plain, HBM ids");
+  run(keep_k<1, true>, "V1 balanced, HBM ids");
+  run(keep_k<0, false>, "V0 plain, compute only");
+  run(keep_k<1, false>, "V1 balanced, compute only");
+  return 0;
+}
