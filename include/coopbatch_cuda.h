@@ -93,8 +93,12 @@ int cb_graph_create_from_csr(const uint64_t* indptr, const uint32_t* indices, ui
 /* CBCS binary CSR (graph.hpp:78-80; load_csr / save_csr, src/graph.cpp:196-265):
  * CB_IO when the file cannot be opened/written, CB_FORMAT for a bad magic,
  * version or truncation, CB_INPUT when validate_csr fails. Weights in a file
- * are validated and dropped (unweighted sampling). */
+ * are validated and kept (cb_graph_set_weights). */
 int cb_graph_load_cbcs(const char* path, int device, cb_graph** out);
+/* Edge weights (graph.hpp:25, Graph::weights; one float per edge, > 0, CB_INPUT
+ * otherwise; nullptr drops them). Only the RW sampler reads them:
+ * pick_neighbor's weighted choice, samplers.cpp:139-165. */
+int cb_graph_set_weights(cb_graph* g, const float* weights);
 int cb_graph_save_cbcs(const cb_graph* g, const char* path);
 int cb_graph_generate_rmat(uint64_t n, uint64_t m, uint64_t seed, int device,
                            cb_graph** out);

@@ -145,6 +145,7 @@ def lib(impl: str = "restated") -> C.CDLL:
         L.rf_graph_new.restype = _P
         L.rf_graph_new.argtypes = [_P, _P, _u64, _u64]
         L.rf_graph_free.argtypes = [_P]
+        L.rf_graph_set_weights.argtypes = [_P, _P, _u64]
         L.rf_validate_csr.argtypes = [_P]
         L.rf_generate_powerlaw.argtypes = [_u64, _f64, _f64, _u64,
                                            C.POINTER(C.POINTER(_u64)),
@@ -255,6 +256,7 @@ def hash_bits(seed: int, ids, impl: str = "restated") -> int:
 class CSR:
     indptr: np.ndarray   # u64[n+1]
     indices: np.ndarray  # u32[m]
+    weights: np.ndarray | None = None  # f32[m] (graph.hpp:25), reference-only
 
     @property
     def n(self) -> int:
@@ -313,6 +315,9 @@ class RefGraph:
         self.csr = g
         self.L = lib("reference")
         self.h = self.L.rf_graph_new(_ptr(g.indptr), _ptr(g.indices), g.n, g.m)
+        if getattr(g, "weights", None) is not None:
+            w = np.ascontiguousarray(g.weights, dtype=np.float32)
+            self.L.rf_graph_set_weights(self.h, _ptr(w), len(w))
 
     def __del__(self):
         if getattr(self, "h", None):

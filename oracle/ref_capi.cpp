@@ -138,6 +138,9 @@ void* rf_graph_new(const uint64_t* indptr, const uint32_t* indices, uint64_t n,
   return g;
 }
 void rf_graph_free(void* g) { delete static_cast<Graph*>(g); }
+void rf_graph_set_weights(void* g, const float* w, uint64_t m) {
+  static_cast<Graph*>(g)->weights.assign(w, w + m);
+}
 
 /* coop_train_step / indep_train_step (coop.cpp:438-610) with GcnModel::init
  * (in_dim = store dim); grad_w: layers concatenated, each rows x cols. */

@@ -31,6 +31,7 @@ _SIGS = {
     "cb_graph_create_from_csr": (C.c_int, [_P, _P, _u64, _u64, C.c_int, _PP]),
     "cb_graph_generate_rmat": (C.c_int, [_u64, _u64, _u64, C.c_int, _PP]),
     "cb_graph_load_cbcs": (C.c_int, [C.c_char_p, C.c_int, _PP]),
+    "cb_graph_set_weights": (C.c_int, [_P, _P]),
     "cb_graph_save_cbcs": (C.c_int, [_P, C.c_char_p]),
     "cb_graph_info": (C.c_int, [_P, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
     "cb_graph_download": (C.c_int, [_P, _P, _P]),

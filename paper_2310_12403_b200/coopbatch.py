@@ -152,14 +152,22 @@ class Graph:
         self.num_vertices, self._m, self.max_degree = n.value, m.value, md.value
 
     @classmethod
-    def from_csr(cls, indptr, indices, device: int = 0) -> "Graph":
+    def from_csr(cls, indptr, indices, device: int = 0, weights=None) -> "Graph":
+        """weights: one positive float per edge (graph.hpp:25), read by the RW
+        sampler's weighted neighbour pick."""
         indptr = np.ascontiguousarray(indptr, dtype=np.uint64)
         indices = np.ascontiguousarray(indices, dtype=np.uint32)
         L = _lib.load()
         h = C.c_void_p()
         _check(L.cb_graph_create_from_csr(_ptr(indptr), _ptr(indices), len(indptr) - 1,
                                           len(indices), device, C.byref(h)))
-        return cls(h, device)
+        g = cls(h, device)
+        if weights is not None:
+            w = np.ascontiguousarray(weights, dtype=np.float32)
+            if len(w) != len(indices):
+                raise InputError("weights must have one entry per edge")
+            _check(L.cb_graph_set_weights(g._h, _ptr(w)))
+        return g
 
     @classmethod
     def generate_rmat(cls, num_vertices: int, num_edges: int, seed: int,

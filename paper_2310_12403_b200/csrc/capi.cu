@@ -438,6 +438,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
     ra.meta = la.meta;
     ra.indptr = g.indptr;
     ra.indices = g.indices;
+    ra.weights = g.weights;
     ra.layer = l + pl->layer_base;
     ra.k = pl->fanouts[l];
     ra.walks = pl->rw_walks;
@@ -750,10 +751,29 @@ int cb_graph_create_from_csr(const uint64_t* indptr, const uint32_t* indices, ui
   });
 }
 
+// Edge weights (graph.hpp:25, one per edge, > 0): kept in HBM next to the
+// indices; only the RW sampler reads them (samplers.cpp:139-165).
+int cb_graph_set_weights(cb_graph* g, const float* weights) {
+  return guard([&] {
+    require(g != nullptr, "null graph");
+    DeviceGuard dg(g->g.device);
+    if (!weights) {
+      if (g->weights_mem) g->weights_mem.reset();
+      g->g.weights = nullptr;
+      return;
+    }
+    for (uint64_t e = 0; e < g->g.m; ++e)
+      require(weights[e] > 0.0f, "csr: weights must be > 0");
+    g->weights_mem = std::make_unique<Arena>();
+    g->g.weights = g->weights_mem->alloc<float>(std::max<uint64_t>(g->g.m, 1));
+    if (g->g.m)
+      CB_CUDA(cudaMemcpy(g->g.weights, weights, g->g.m * 4, cudaMemcpyHostToDevice));
+  });
+}
+
 // CBCS binary CSR (graph.hpp:78-80, graph.cpp:196-265): "CBCS", u32 version 1,
 // u64 n, u64 m, u64 indptr[n+1], u32 indices[m], u8 flags, f32 weights[m] if
-// flags & 1. Little-endian. Weights are validated (> 0) and not kept: the
-// device path samples unweighted (LABOR-0 / NS / FULL).
+// flags & 1. Little-endian. Weights (validated > 0) go to HBM with the CSR.
 int cb_graph_load_cbcs(const char* path, int device, cb_graph** out) {
   return guard([&] {
     require(path != nullptr && out != nullptr, "null argument");
@@ -779,13 +799,22 @@ int cb_graph_load_cbcs(const char* path, int device, cb_graph** out) {
     rd(indices.data(), m * 4, "indices");
     uint8_t flags = 0;
     rd(&flags, 1, "flags");
+    std::vector<float> w;
     if (flags & 1) {
-      std::vector<float> w(m);
+      w.resize(m);
       rd(w.data(), m * 4, "weights");
       for (float x : w) require(x > 0.0f, "csr: weights must be > 0");
     }
     const int rc = cb_graph_create_from_csr(indptr.data(), indices.data(), n, m, device, out);
     if (rc != CB_OK) throw Error(static_cast<Status>(rc), g_err);
+    if (flags & 1) {
+      const int rw = cb_graph_set_weights(*out, w.data());
+      if (rw != CB_OK) {
+        cb_graph_destroy(*out);
+        *out = nullptr;
+        throw Error(static_cast<Status>(rw), g_err);
+      }
+    }
   });
 }
 
@@ -794,23 +823,27 @@ int cb_graph_save_cbcs(const cb_graph* g, const char* path) {
     require(g != nullptr && path != nullptr, "null argument");
     std::vector<uint64_t> indptr(g->g.n + 1);
     std::vector<uint32_t> indices(g->g.m);
+    std::vector<float> w(g->g.weights ? g->g.m : 0);
     {
       DeviceGuard dg(g->g.device);
       CB_CUDA(cudaMemcpy(indptr.data(), g->g.indptr, (g->g.n + 1) * 8, cudaMemcpyDeviceToHost));
       if (g->g.m)
         CB_CUDA(cudaMemcpy(indices.data(), g->g.indices, g->g.m * 4, cudaMemcpyDeviceToHost));
+      if (!w.empty())
+        CB_CUDA(cudaMemcpy(w.data(), g->g.weights, g->g.m * 4, cudaMemcpyDeviceToHost));
     }
     FILE* f = std::fopen(path, "wb");
     if (!f) throw Error(kIo, std::string("cannot open for write: ") + path);
     std::unique_ptr<FILE, int (*)(FILE*)> guard_f(f, &std::fclose);
     const uint32_t version = 1;
     const uint64_t n = g->g.n, m = g->g.m;
-    const uint8_t flags = 0;
+    const uint8_t flags = w.empty() ? 0 : 1;
     bool ok = std::fwrite("CBCS", 1, 4, f) == 4 && std::fwrite(&version, 4, 1, f) == 1 &&
               std::fwrite(&n, 8, 1, f) == 1 && std::fwrite(&m, 8, 1, f) == 1 &&
               std::fwrite(indptr.data(), 8, n + 1, f) == n + 1 &&
               (m == 0 || std::fwrite(indices.data(), 4, m, f) == m) &&
-              std::fwrite(&flags, 1, 1, f) == 1;
+              std::fwrite(&flags, 1, 1, f) == 1 &&
+              (w.empty() || std::fwrite(w.data(), 4, m, f) == m);
     if (!ok) throw Error(kIo, std::string("write failed: ") + path);
   });
 }

@@ -97,6 +97,7 @@ using namespace cb::capi;
 // ------------------------------------------------------------------ handles --
 struct cb_graph {
   DeviceGraph g;
+  std::unique_ptr<Arena> weights_mem;  // g.weights (RW on weighted graphs)
   ~cb_graph() {
     if (g.indptr) cudaFree(g.indptr);
     if (g.indices) cudaFree(g.indices);

@@ -96,6 +96,7 @@ struct DeviceGraph {
   uint64_t n = 0, m = 0;
   uint64_t* indptr = nullptr;   // [n+1]
   uint32_t* indices = nullptr;  // [m]
+  float* weights = nullptr;     // [m] or nullptr (graph.hpp:25; RW only)
   uint64_t max_degree = 0;
 };
 
@@ -231,6 +232,7 @@ struct RwArgs {
   LayerMeta* meta;
   const uint64_t* indptr;
   const uint32_t* indices;
+  const float* weights;  // nullptr = unweighted
   int layer;
   uint32_t k;            // fanout: top-k visited vertices per dst
   uint32_t walks, length;

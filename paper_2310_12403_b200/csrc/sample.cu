@@ -788,7 +788,24 @@ __global__ void __launch_bounds__(kNT) rw_walk_kernel(RwArgs a) {
           }
           const uint64_t beg = __ldg(a.indptr + from);
           const uint64_t d = __ldg(a.indptr + from + 1) - beg;
-          if (d != 0) {
+          if (d != 0 && a.weights) {
+            // pick_neighbor (samplers.cpp:139-165): cdf[i] = weights summed in
+            // f64 in CSR order, x = u * cdf.back(), first i with cdf[i] > x
+            double tot = 0.0;
+            for (uint64_t i = 0; i < d; ++i)
+              tot = __dadd_rn(tot, static_cast<double>(__ldg(a.weights + beg + i)));
+            const double x = __dmul_rn(u, tot);
+            double acc = 0.0;
+            uint64_t idx = d - 1;
+            for (uint64_t i = 0; i < d; ++i) {
+              acc = __dadd_rn(acc, static_cast<double>(__ldg(a.weights + beg + i)));
+              if (acc > x) {
+                idx = i;
+                break;
+              }
+            }
+            out = __ldg(a.indices + beg + idx);
+          } else if (d != 0) {
             uint64_t idx = __double2ull_rz(__dmul_rn(u, static_cast<double>(d)));
             if (idx >= d) idx = d - 1;
             out = __ldg(a.indices + beg + idx);

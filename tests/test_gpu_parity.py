@@ -570,3 +570,25 @@ def test_sample_block_any_layer(powerlaw, layer, kappa):
         want = O.sample_block(ref, seeds, O.NS, 3, osched(cb.SeedSchedule.plain(1234)), layer,
                               impl="reference")
         assert np.array_equal(ns["edges"], want["edges"])
+
+
+@pytest.mark.parametrize("kappa", [1, 4])
+def test_rw_weighted_matches_compiled_reference(powerlaw, kappa):
+    """RW on a weighted graph: pick_neighbor's weighted choice (samplers.cpp:
+    139-165, cdf summed in f64 in CSR order, upper_bound of u * total) on the
+    device vs the compiled reference's rw_block with Graph::weights set."""
+    if not O.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    _, ref = powerlaw
+    rng = np.random.default_rng(11 + kappa)
+    w = rng.uniform(0.05, 4.0, ref.m).astype(np.float32)
+    w[::7] = 1.0
+    g = cb.Graph.from_csr(ref.indptr, ref.indices, weights=w)
+    wref = O.CSR(ref.indptr, ref.indices, w)
+    for trial in range(2):
+        seeds = np.sort(rng.choice(ref.n, 120, replace=False)).astype(np.uint32)
+        sched = cb.schedule_advance(cb.SeedSchedule.make(kappa, 90 + trial))
+        cfg = cb.SamplerConfig(cb.SamplerKind.kRw, 5)  # reference defaults o=3, p=.5, a=100
+        got = cb.expand(g, seeds, 2, cfg, sched)
+        want = O.expand(wref, seeds, 2, 3, 5, osched(sched), impl="reference")
+        assert_stack_eq(got, want, f"weighted RW kappa={kappa} trial={trial}")

@@ -50,21 +50,22 @@ __device__ __forceinline__ uint64_t mix64_bal(const Bal& b, uint32_t t) {
   return z ^ (z >> 31);
 }
 
-template <int V, bool LOAD>
-__global__ void __launch_bounds__(128, 8) keep_k(const uint32_t* __restrict__ ids, uint64_t n,
-                                                 uint64_t p1, Bal b, uint64_t T,
-                                                 unsigned long long* out) {
+template <int V, bool LOAD, int NT = 128, int MINB = 8, int IPT = 8>
+__global__ void __launch_bounds__(NT, MINB) keep_k(const uint32_t* __restrict__ ids, uint64_t n,
+                                                   uint64_t p1, Bal b, uint64_t T,
+                                                   unsigned long long* out) {
   uint32_t cnt = 0;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 8;
-  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * blockDim.x) * 8 + threadIdx.x;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * IPT;
+  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + warp * 32) * IPT + lane;
        base < n; base += stride) {
-    uint32_t tv[8];
+    uint32_t tv[IPT];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < IPT; ++j)
       tv[j] = LOAD ? __ldg(ids + base + 32 * j) : static_cast<uint32_t>(base + 32 * j) * 2654435761u;
     uint32_t km = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < IPT; ++j) {
       const uint64_t h = V == 0 ? mix64(p1 ^ tv[j]) : mix64_bal(b, tv[j]);
       km |= (h <= T ? 1u : 0u) << j;
     }
@@ -97,13 +98,13 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  auto run = [&](auto kern, const char* name) {
+  auto run = [&](auto kern, const char* name, int nt = 128, int minb = 8) {
     unsigned long long res[2];
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemset(out, 0, 8);
       cudaMemset(flush, rep, 512u << 20);
       cudaEventRecord(e0);
-      kern<<<148 * 8, 128>>>(ids, N, p1, b, ~0ull >> 8, out);
+      kern<<<148 * minb, nt>>>(ids, N, p1, b, ~0ull >> 8, out);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -117,5 +118,13 @@ int main() {
   run(keep_k<1, true>, "V1 balanced, HBM ids");
   run(keep_k<0, false>, "V0 plain, compute only");
   run(keep_k<1, false>, "V1 balanced, compute only");
+  run(keep_k<0, false, 128, 12>, "V0 compute 128x12", 128, 12);
+  run(keep_k<0, false, 256, 8>, "V0 compute 256x8", 256, 8);
+  run(keep_k<0, false, 128, 8, 16>, "V0 compute IPT16", 128, 8);
+  run(keep_k<0, false, 128, 16, 4>, "V0 compute 128x16 IPT4", 128, 16);
+  run(keep_k<0, true, 128, 12>, "V0 HBM 128x12", 128, 12);
+  run(keep_k<0, true, 256, 8>, "V0 HBM 256x8", 256, 8);
+  run(keep_k<0, true, 128, 8, 16>, "V0 HBM IPT16", 128, 8);
+  run(keep_k<0, true, 128, 16, 4>, "V0 HBM 128x16 IPT4", 128, 16);
   return 0;
 }
