@@ -183,6 +183,17 @@ int cb_synchronize(cb_plan* plan);
 int cb_layer_sizes(cb_plan* plan, uint32_t part, int layer, uint64_t* sizes);
 int cb_download_block(cb_plan* plan, uint32_t part, int layer, uint32_t* dst, uint32_t* src,
                       uint32_t* edges /* 2 per edge */, uint32_t* dst_pos);
+/* The whole batch result of one part in one call, for callers that want it in
+ * host memory (the reference returns LayerStacks and FeatureMatrix rows by
+ * value: samplers.hpp:42-49, coop.hpp:83-91, 151): every layer's dst, src,
+ * edges and dst_pos, plus the gathered rows when the batch has them, written
+ * by one kernel into pinned (cudaHostAlloc'd / registered) host memory, on the
+ * plan stream, without a host round trip. Layout and the truncation header:
+ * csrc/result.cu. cb_plan_result_bytes bounds the size from the plan's
+ * capacities. */
+int cb_plan_result_bytes(const cb_plan* plan, uint32_t part, uint64_t row_bytes,
+                         uint64_t* max_bytes);
+int cb_plan_result_async(cb_plan* plan, uint32_t part, void* host_pinned, uint64_t cap_bytes);
 int cb_owner_set_size(cb_plan* plan, uint32_t part, uint64_t* n);
 int cb_download_owner_set(cb_plan* plan, uint32_t part, uint32_t* ids);
 /* send_counts[P*P] (row = sender), owner_row_counts[P]; loc_* hold part p's

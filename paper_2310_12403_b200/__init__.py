@@ -7,7 +7,8 @@ from .coopbatch import (  # noqa: F401
     PartitionMap,
     Plan, SamplerConfig, SamplerKind, SeedSchedule, coop_sample, expand, hash_bits,
     hash_uniform, indep_sample, load_inputs, mix64, partition_from_owner, partition_random,
-    sample_block, sample_full, sample_labor0, sample_ns, sample_rw, schedule_advance, LayerMetrics, PeMetrics, step_metrics)
+    sample_block, sample_full, sample_labor0, sample_ns, sample_rw, schedule_advance, LayerMetrics, PeMetrics, step_metrics,
+    parse_result)
 from .cache import (  # noqa: F401
     BatchMode, CacheOutcome, CacheStats, DependentExperimentResult, DependentStepRow, LruCache,
     MinibatchSchedule, feature_load_sim, lru_access, nested_batches, run_dependent_experiment,

@@ -525,11 +525,55 @@ class Plan:
         return ExchangeRecord(l, sc, orc, [lp[offs[p]:offs[p + 1]] for p in range(P)],
                               [lr[offs[p]:offs[p + 1]] for p in range(P)])
 
+    def result_bytes(self, p: int = 0, row_bytes: int = 0) -> int:
+        n = C.c_uint64()
+        _check(_lib.load().cb_plan_result_bytes(self._h, p, row_bytes, C.byref(n)))
+        return n.value
+
+    def result_async(self, host_ptr: int, cap: int, p: int = 0):
+        """Part p's blocks (+ gathered rows) into pinned host memory at
+        host_ptr, ordered on the plan stream (parse_result reads it)."""
+        _check(_lib.load().cb_plan_result_async(self._h, p, C.c_void_p(host_ptr), cap))
+
     def rows(self, p: int, store: FeatureStore) -> np.ndarray:
         n = self.layer_sizes(p, self.L - 1)["n_src"]
         out = np.zeros((n, store.dim), dtype=_DT[store.dtype][1])
         _check(_lib.load().cb_download_rows(self._h, p, _ptr(out)))
         return out
+
+
+def parse_result(buf: np.ndarray, dtype=None, dim: int = 0) -> dict:
+    """Reads a cb_plan_result_async buffer (csrc/result.cu layout): the
+    per-layer blocks as dicts (dst, src, edges, dst_pos) and the rows."""
+    b = np.asarray(buf).view(np.uint8)
+    hd = b[:40].view(np.uint64)
+    if int(hd[0]) != 0x3153524243:
+        raise ValueError("not a batch result buffer")
+    L, row_bytes, total, trunc = (int(x) for x in hd[1:5])
+    if trunc:
+        raise ValueError(f"result truncated: {total} bytes needed")
+    cnt = b[40:40 + 24 * L].view(np.uint64).reshape(L, 3)
+    pad = lambda x: (x + 15) & ~15  # noqa: E731
+    off = pad(8 * (5 + 3 * L))
+    out = {"blocks": []}
+
+    def take(nbytes, dt):
+        nonlocal off
+        a = b[off:off + nbytes].view(dt)
+        off += pad(nbytes)
+        return a
+    for l in range(L):
+        nd, ns, ne = (int(x) for x in cnt[l])
+        blk = {"layer": l, "dst": take(4 * nd, np.uint32), "src": take(4 * ns, np.uint32),
+               "edges": take(8 * ne, np.uint32).reshape(ne, 2),
+               "dst_pos": take(4 * nd, np.uint32)}
+        out["blocks"].append(blk)
+    if row_bytes:
+        n = int(cnt[L - 1][1])
+        raw = take(n * row_bytes, np.uint8)
+        out["rows"] = raw.view(dtype).reshape(n, -1) if dtype is not None else raw
+    out["total_bytes"] = total
+    return out
 
 
 # Plans of the reference-style free functions, most recently used last. A plan

@@ -7,6 +7,7 @@
 // host. Contract violations raise cb::Error(kInput) -> CB_INPUT, mirroring
 // coopbatch::InputError (common.hpp:12-15).
 #include "capi_internal.h"
+#include "result.h"
 
 thread_local std::string cb::capi::g_err;
 
@@ -1393,6 +1394,64 @@ int cb_download_block(cb_plan* plan, uint32_t part, int layer, uint32_t* dst, ui
       CB_CUDA(cudaMemcpy(edges, b.edges, m.n_edges * 8, cudaMemcpyDeviceToHost));
     if (dst_pos && m.n_dst)
       CB_CUDA(cudaMemcpy(dst_pos, b.dst_pos, m.n_dst * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+// Result bytes a batch of this plan can need at most (capacities), for
+// sizing the pinned buffer of cb_plan_result_async.
+int cb_plan_result_bytes(const cb_plan* plan, uint32_t part, uint64_t row_bytes,
+                         uint64_t* max_bytes) {
+  return guard([&] {
+    require(plan != nullptr && max_bytes != nullptr, "null argument");
+    require(part < plan->P, "part index out of range");
+    require(plan->L <= kResultMaxLayers, "result: too many layers");
+    auto pad = [](uint64_t b) { return (b + 15) & ~15ULL; };
+    uint64_t t = pad(8ULL * (5 + 3 * plan->L));
+    const PeWork& w = plan->pe[part];
+    for (int l = 0; l < plan->L; ++l) {
+      const LayerBufs& b = w.L[l];
+      const uint64_t cd = l == 0 ? plan->max_seeds : b.cap_dst;
+      t += 2 * pad(cd * 4) + pad(b.cap_src * 4) + pad(b.cap_edges * 8);
+    }
+    t += pad(w.L[plan->L - 1].cap_src * row_bytes);
+    *max_bytes = t;
+  });
+}
+
+// The batch's blocks (and gathered rows, when the batch has them) written
+// into pinned host memory by one kernel on the plan stream; nothing waits.
+// Layout: result.cu. Ordered after the batch; the caller synchronises
+// (cb_synchronize / an event) before reading.
+int cb_plan_result_async(cb_plan* plan, uint32_t part, void* host_pinned, uint64_t cap_bytes) {
+  return guard([&] {
+    require(plan != nullptr && host_pinned != nullptr, "null argument");
+    require_batch(plan, part, 0);
+    require(plan->L <= kResultMaxLayers, "result: too many layers");
+    require(cap_bytes >= 8ULL * (5 + 3 * plan->L), "result buffer smaller than its header");
+    DeviceGuard dg(plan->device);
+    void* dptr = nullptr;
+    require(cudaHostGetDevicePointer(&dptr, host_pinned, 0) == cudaSuccess,
+            "result buffer is not pinned, device-mapped host memory");
+    PeWork& w = plan->pe[part];
+    ResultArgs a{};
+    a.meta = plan->meta_at(part, 0);
+    a.L = plan->L;
+    for (int l = 0; l < plan->L; ++l) {
+      const LayerBufs& b = w.L[l];
+      const uint32_t* d_dst;
+      if (l == 0) d_dst = plan->seeds + plan->seeds_off[part];
+      else if (!plan->own_dst()) d_dst = w.L[l - 1].src;
+      else d_dst = b.dst;
+      a.ptr[l][0] = d_dst;
+      a.ptr[l][1] = b.src;
+      a.ptr[l][2] = b.edges;
+      a.ptr[l][3] = b.dst_pos;
+    }
+    a.rows = plan->have_rows ? w.rows : nullptr;
+    a.row_bytes = plan->have_rows ? w.rows_row_bytes : 0;
+    a.out = static_cast<unsigned char*>(dptr);
+    a.cap = cap_bytes;
+    launch_result(a, plan->stream);
   });
 }
 

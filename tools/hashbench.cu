@@ -74,6 +74,32 @@ __global__ void __launch_bounds__(NT, MINB) keep_k(const uint32_t* __restrict__ 
   if (cnt) atomicAdd(out, cnt);
 }
 
+// software-pipelined: the next span's ids are loaded before this span is hashed
+template <int NT = 128, int MINB = 8, int IPT = 8>
+__global__ void __launch_bounds__(NT, MINB) keep_pipe_k(const uint32_t* __restrict__ ids,
+                                                        uint64_t n, uint64_t p1, Bal b,
+                                                        uint64_t T, unsigned long long* out) {
+  uint32_t cnt = 0;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * IPT;
+  uint64_t base = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + warp * 32) * IPT + lane;
+  uint32_t tv[IPT], nx[IPT];
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) tv[j] = base + 32 * j < n ? __ldg(ids + base + 32 * j) : 0u;
+  for (; base < n; base += stride) {
+    const uint64_t nb = base + stride;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) nx[j] = nb + 32 * j < n ? __ldg(ids + nb + 32 * j) : 0u;
+    uint32_t km = 0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) km |= (mix64(p1 ^ tv[j]) <= T ? 1u : 0u) << j;
+    cnt += __popc(km);
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) tv[j] = nx[j];
+  }
+  if (cnt) atomicAdd(out, cnt);
+}
+
 int main() {
   const uint64_t N = 48ull << 20;  // ~ c4 layer-3 scan (48M positions), 192 MB
   std::vector<uint32_t> h(N);
@@ -122,6 +148,10 @@ int main() {
   run(keep_k<0, false, 256, 8>, "V0 compute 256x8", 256, 8);
   run(keep_k<0, false, 128, 8, 16>, "V0 compute IPT16", 128, 8);
   run(keep_k<0, false, 128, 16, 4>, "V0 compute 128x16 IPT4", 128, 16);
+  run(keep_pipe_k<128, 8, 8>, "pipelined HBM 128x8", 128, 8);
+  run(keep_pipe_k<128, 6, 8>, "pipelined HBM 128x6", 128, 6);
+  run(keep_pipe_k<128, 8, 4>, "pipelined HBM 128x8 IPT4", 128, 8);
+  run(keep_pipe_k<256, 4, 8>, "pipelined HBM 256x4", 256, 4);
   run(keep_k<0, true, 128, 12>, "V0 HBM 128x12", 128, 12);
   run(keep_k<0, true, 256, 8>, "V0 HBM 256x8", 256, 8);
   run(keep_k<0, true, 128, 8, 16>, "V0 HBM IPT16", 128, 8);
