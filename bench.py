@@ -81,17 +81,82 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel: str, dim: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per launch from
-    the committed `ncu --set full` capture of this workload (profiles/), or
-    None when no capture of this shape is committed."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            d = json.load(f)
-        e = d[kernel]
-        return e["dram_bytes"] if e.get("dim") == dim else None
-    except Exception:
-        return None
+def ncu_traffic(cfg_name: str, seeds_step: int) -> dict:
+    """DRAM traffic per launch of the roofline kernels, measured in this run:
+    a child process (`bench.py --probe`) samples the same batch the
+    per-kernel profile uses (step `seeds_step`) eagerly and gathers its rows,
+    under `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` (cold
+    cache, serialised launches). Returns {kernel: bytes} for the last layer's
+    labor_mark and the gather, or {"error": ...}."""
+    import csv
+    import shutil
+    import tempfile
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return {"error": "ncu not found"}
+    with tempfile.TemporaryDirectory() as td:
+        log = os.path.join(td, "traffic.csv")
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,"
+               "gpu__time_duration.sum", "--clock-control", "none", "-k",
+               "regex:labor_mark_kernel|gather_kernel", "--csv", "--log-file", log,
+               sys.executable, os.path.abspath(__file__), "--probe", "--config", cfg_name,
+               "--probe-step", str(seeds_step)]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        except Exception as e:  # noqa: BLE001 - report, never fake
+            return {"error": f"ncu run failed: {e}"[:200]}
+        if r.returncode != 0 or not os.path.exists(log):
+            return {"error": f"ncu rc={r.returncode}: {(r.stderr or r.stdout)[-200:]}"}
+        launches: dict = {}
+        with open(log) as f:
+            rows = [x for x in csv.reader(f)]
+        hi = next(i for i, x in enumerate(rows) if "Metric Name" in x)
+        h = rows[hi]
+        iid, ik, im, iv = (h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"),
+                           h.index("Metric Value"))
+        for x in rows[hi + 1:]:
+            if len(x) <= iv:
+                continue
+            e = launches.setdefault(int(x[iid]), {"kernel": x[ik]})
+            e[x[im]] = float(x[iv].replace(",", ""))
+    order = [launches[k] for k in sorted(launches)]
+    marks = [e for e in order if "labor_mark" in e["kernel"]]
+    gathers = [e for e in order if "gather_kernel" in e["kernel"]]
+    out = {"how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
+                  "--clock-control none (bench.py --probe child, same batch)"}
+    if marks:
+        e = marks[-1]
+        out["labor_mark_last_layer"] = e["dram__bytes_read.sum"] + e["dram__bytes_write.sum"]
+        out["labor_mark_ncu_us"] = e["gpu__time_duration.sum"] / 1e3
+    if gathers:
+        e = gathers[-1]
+        out["gather"] = e["dram__bytes_read.sum"] + e["dram__bytes_write.sum"]
+        out["gather_ncu_us"] = e["gpu__time_duration.sum"] / 1e3
+    return out
+
+
+def run_probe(args, cfg):
+    """--probe: one eager batch (step args.probe_step's seeds and schedule,
+    the batch the per-kernel profile times) + its gather, for ncu_traffic."""
+    import paper_2310_12403_b200 as cb
+    from paper_2310_12403_b200.seeds import draw_from_pool
+    kind = {"labor0": cb.SamplerKind.kLabor0, "ns": cb.SamplerKind.kNs,
+            "full": cb.SamplerKind.kFull}[cfg["kind"]]
+    L, b = len(cfg["fanouts"]), cfg["batch"]
+    g = cb.Graph.generate_rmat(cfg["n"], cfg["m"], GRAPH_SEED, device=0)
+    store = cb.FeatureStore.synth(g, cfg["dim"], FEAT_SEED, cfg["dtype"])
+    scfg = cb.SamplerConfig(kind, fanouts=cfg["fanouts"])
+    i = args.probe_step
+    seeds = draw_from_pool(np.arange(cfg["n"], dtype=np.uint32), b, RUN_SEED,
+                           cb.hash_bits(i, [0]))
+    sched = cb.SeedSchedule.make(1, RUN_SEED)
+    for _ in range(i):
+        sched = cb.schedule_advance(sched)
+    plan = cb.Plan(g, None, L, scfg, b)
+    plan.sample([seeds], sched, cb.MODE_INDEP, sync=True)
+    plan.gather(store)
+    plan.synchronize()
+    print(json.dumps({"probe": [plan.layer_sizes(0, l) for l in range(L)]}))
 
 
 def dist_env():
@@ -424,13 +489,13 @@ def batch_sweep_evidence(cb, dev, batches=(1024, 4096, 16384, 65536), steps=10):
     return out
 
 
-def mark_roofline(prof_ms, prof_sizes, L, scfg, peak):
-    """The largest sampling launch: labor_mark of the last layer, from the
-    profiling replay of the captured batch (event nodes between launches, L2
-    flushed before the replay). Algorithmic bytes per launch: 4 B per scanned
-    position (the neighbour id), 4 B per 32 positions (keep word), 8 B per kept
-    edge (staged pair). The kernel is bound by the SplitMix64 issue rate, not
-    by HBM: hbm_frac says how far from the byte roofline it runs."""
+def mark_roofline(prof_ms, prof_sizes, L, scfg, peak, peak_kind, traffic):
+    """The dominant kernel: labor_mark of the last layer (c4: ~40% of a
+    batch), timed by the in-graph event profile of one batch (mean of the
+    replays, L2 flushed before each). Algorithmic bytes per launch (SURVEY
+    §8(d)): 4 B per scanned position (the neighbour id) + 4 B per 32 positions
+    (keep word) + 8 B per kept edge (staged pair). `traffic` is the same
+    launch's DRAM bytes measured by ncu in this run (ncu_traffic)."""
     import math as _m
     if int(scfg.kind) != 2 or len(prof_ms) != 3 * L + 3:
         return None
@@ -438,11 +503,14 @@ def mark_roofline(prof_ms, prof_sizes, L, scfg, peak):
     s = prof_sizes[L - 1]
     nbytes = 4 * s["scan_total"] + 4 * _m.ceil(s["scan_total"] / 32) + 8 * s["n_edges"]
     t = prof_ms[i] / 1e3
-    return {"kernel": "labor_mark_kernel (last layer)", "bound": "issue (SplitMix64 per position)",
+    return {"bound": "hbm", "kernel": "labor_mark_kernel (last layer)",
+            "achieved": nbytes / t / 1e9, "peak": peak, "peak_kind": peak_kind,
+            "unit": "GB/s", "frac": nbytes / t / 1e9 / peak,
+            "traffic": traffic.get("labor_mark_last_layer"),
+            "bytes_per_launch": nbytes,
+            "per_unit": "4 B per scanned position + 4 B per keep word + 8 B per kept edge",
             "ms": prof_ms[i], "positions": s["scan_total"], "kept": s["n_edges"],
-            "positions_per_s": s["scan_total"] / t, "bytes_per_launch": nbytes,
-            "achieved": nbytes / t / 1e9, "peak": peak, "unit": "GB/s",
-            "hbm_frac": nbytes / t / 1e9 / peak,
+            "positions_per_s": s["scan_total"] / t,
             "share_of_batch": prof_ms[i] / sum(prof_ms)}
 
 
@@ -725,6 +793,17 @@ def run_ours(args, cfg):
         plans.append(p2)
         streams.append(torch.cuda.ExternalStream(p2.stream, device=torch.device(f"cuda:{dev}")))
 
+    # pinned host buffers of cb_plan_result_async (one per in-flight plan),
+    # sized at 4x one warm batch's result
+    plans[0].replay(step_ptr(0), scheds[0], True, 3)
+    tmp = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+    plans[0].result_async(tmp.data_ptr(), tmp.numel())
+    plans[0].synchronize()
+    one = int(tmp.numpy()[:40].view(np.uint64)[3])
+    del tmp
+    res_cap = max(4 * one, 1 << 20)
+    res_bufs = [torch.empty(res_cap, dtype=torch.uint8).pin_memory() for _ in range(S)]
+
     # ---- warmup
     for i in range(W):
         plans[i % S].replay(step_ptr(i), scheds[i], True, 3)
@@ -773,32 +852,22 @@ def run_ours(args, cfg):
         torch.distributed.barrier()
     sizes = [plan.layer_sizes(0, l) for l in range(L)]
     rows_last = sizes[-1]["n_src"]
-    # the roofline kernel (gather) alone, on the last batch, same L2 flushing
-    gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
-    for i in range(K):
-        flush_l2()
-        gev[i][0].record(stream)
-        plan.gather(store)  # one gather_kernel launch on the plan stream
-        gev[i][1].record(stream)
-    torch.cuda.synchronize()
-    gath_ms = [e[0].elapsed_time(e[1]) for e in gev]
-    samp_ms = [s_ - float(np.mean(gath_ms)) for s_ in step_ms]
     if world > 1:
         t = torch.tensor([total_ms], device=f"cuda:{dev}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
 
-    # ---- e2e: pinned host seeds through the public API (H2D inside the
-    # replay), the batch's counts read back asynchronously into pinned host
-    # memory every step, all S streams joined at the end
+    # ---- e2e through the C-ABI with host buffers: every step the seeds (+
+    # variate keys) go H2D from pinned memory inside the replay, and the whole
+    # batch result -- every layer's block and the gathered rows -- is written
+    # into a pinned host buffer by cb_plan_result_async (one kernel, counts
+    # read on the device); all S streams joined at the end, wall clock
     pinned = torch.from_numpy(seeds_host.view(np.int32)).pin_memory()
-    mb = C.c_uint64()
-    _lib_.cb_plan_meta_async(plan._h, None, C.byref(mb))
-    meta_h = torch.empty((K, int(mb.value)), dtype=torch.uint8).pin_memory()
+    res_cap_used = res_cap
 
     def e2e_step(i):
         plans[i % S].replay(pinned.data_ptr() + (W + i) * b * 4, scheds[W + i], False, 3)
-        _lib_.cb_plan_meta_async(plans[i % S]._h, C.c_void_p(meta_h[i].data_ptr()), None)
+        plans[i % S].result_async(res_bufs[i % S].data_ptr(), res_cap_used)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -809,15 +878,56 @@ def run_ours(args, cfg):
         t = torch.tensor([e2e_s], device=f"cuda:{dev}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
-    n_src_last = int(meta_h[K - 1].numpy().view(np.uint64).reshape(-1, 8)[L - 1][4])
-    assert n_src_last > 0, "e2e batch result read back empty"
+    res_bytes = []
+    for j in range(min(S, K)):  # the last result of every slot
+        hd = res_bufs[j].numpy()[:40].view(np.uint64)
+        assert int(hd[4]) == 0, "e2e result buffer truncated"
+        res_bytes.append(int(hd[3]))
+    last = cb.parse_result(res_bufs[(K - 1) % S].numpy())
+    assert last["blocks"][L - 1]["src"].size > 0, "e2e batch result read back empty"
+    # ---- e2e with the result left on the device (only the per-layer counts
+    # read back): the sampler-feeding-a-GPU-trainer case
+    mb = C.c_uint64()
+    _lib_.cb_plan_meta_async(plan._h, None, C.byref(mb))
+    meta_h = torch.empty((K, int(mb.value)), dtype=torch.uint8).pin_memory()
+
+    def e2e_dev_step(i):
+        plans[i % S].replay(pinned.data_ptr() + (W + i) * b * 4, scheds[W + i], False, 3)
+        _lib_.cb_plan_meta_async(plans[i % S]._h, C.c_void_p(meta_h[i].data_ptr()), None)
+    torch.cuda.synchronize()
+    td = time.perf_counter()
+    run_steps(e2e_dev_step)
+    e2e_dev_s = time.perf_counter() - td
+    if world > 1:
+        t = torch.tensor([e2e_dev_s], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_dev_s = float(t.item())
     launches_per_step = plan.captured_launches(3)  # the replayed sample + gather graph
-    # per-launch breakdown inside the CUDA graph (event-record nodes), L2 flushed
-    flush_l2()
-    prof_ms = plan.graph_profile(step_ptr(W), scheds[W])
+    # per-launch device times of one batch (step W's seeds and schedule)
+    # inside the CUDA graph (event-record nodes on the plan stream), L2
+    # flushed before each of R replays, averaged per launch
+    prof_runs = []
+    for _ in range(5):
+        flush_l2()
+        prof_runs.append(plan.graph_profile(step_ptr(W), scheds[W]))
+    prof_ms = [float(x) for x in np.mean(np.array(prof_runs), axis=0)]
     prof_sizes = [plan.layer_sizes(0, l) for l in range(L)]
+    rows_last = prof_sizes[-1]["n_src"]
+    # the gather alone on that batch, events on its stream, L2 flushed before
+    # every launch
+    gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    for i in range(K):
+        flush_l2()
+        gev[i][0].record(stream)
+        plan.gather(store)  # one gather_kernel launch on the plan stream
+        gev[i][1].record(stream)
+    torch.cuda.synchronize()
+    gath_ms = [e[0].elapsed_time(e[1]) for e in gev]
+    samp_ms = [s_ - float(np.mean(gath_ms)) for s_ in step_ms]
     if rank != 0:
         return
+    traffic = ({"error": "skipped (--no-traffic)"} if args.no_traffic else
+               ncu_traffic(args.config, W))
     seeds_total = K * b * world
     value = seeds_total / (total_ms / 1000.0)
     peak, peak_kind = peaks()
@@ -847,15 +957,27 @@ def run_ours(args, cfg):
         "stage_ms": {"sample_dedup": float(np.mean(samp_ms)), "gather": float(np.mean(gath_ms)),
                      "note": "gather timed alone (one launch, events on its stream); sample = step - gather"},
         "e2e": {"value": seeds_total / e2e_s, "unit": "seeds/s",
-                "h2d_bytes_per_step": b * 4 + 40, "d2h_bytes_per_step": int(mb.value),
+                "h2d_bytes_per_step": b * 4 + 40,
+                "d2h_bytes_per_step": int(np.mean(res_bytes)),
+                "result": "every layer's dst/src/edges/dst_pos + the gathered rows, written "
+                          "into pinned host memory by cb_plan_result_async each step",
                 "device_ms": e2e_ms},
-        "roofline": {"bound": "hbm",
-                     "kernel": "gather_kernel<V,U> (16/8/4/2-byte vectors by row size; U = 3 for 16-byte, else 4)",
-                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
-                     "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic("gather", cfg["dim"]),
-                     "bytes_per_launch": gather_bytes},
-        "roofline_sampling": mark_roofline(prof_ms, prof_sizes, L, scfg, peaks()[0]),
+        "e2e_device_result": {"value": seeds_total / e2e_dev_s, "unit": "seeds/s",
+                              "h2d_bytes_per_step": b * 4 + 40,
+                              "d2h_bytes_per_step": int(mb.value),
+                              "result": "left in HBM for a GPU consumer; per-layer counts "
+                                        "read back (cb_plan_meta_async)"},
+        "roofline": mark_roofline(prof_ms, prof_sizes, L, scfg, peak, peak_kind, traffic),
+        "roofline_gather": {
+            "bound": "hbm",
+            "kernel": "gather_kernel<V,U> (16/8/4/2-byte vectors by row size; U = 3 for "
+                      "16-byte, else 4)",
+            "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic.get("gather"),
+            "bytes_per_launch": gather_bytes,
+            "per_unit": "per input row: owner row read + requester row write + 4 B id",
+            "ms": float(np.mean(gath_ms)), "share_of_batch": prof_ms[-1] / sum(prof_ms)},
+        "traffic_probe": traffic,
         "gpu_launches": launches_per_step * K,
         "kernel_ms_graph": [round(x, 4) for x in prof_ms],
         "evidence": {"per_layer": sizes,
@@ -931,6 +1053,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-evidence", action="store_true")
     ap.add_argument("--csv-dir", default="", help="also write the evidence as CLI-format CSVs")
+    ap.add_argument("--probe", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--probe-step", type=int, default=0, help=argparse.SUPPRESS)
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the in-run ncu DRAM-traffic measurement")
     ap.add_argument("--inflight", type=int, default=8,
                     help="independent minibatches in flight per GPU (streams); 1 = one at a time")
     ap.add_argument("--mode", choices=["coop", "indep"], default="coop",
@@ -944,6 +1070,9 @@ def main():
         args.warmup = 3
     cfg = CONFIGS[args.config]
     rank, world, _ = dist_env()
+    if args.probe:
+        run_probe(args, cfg)
+        return
     if args.impl == "reference":
         run_reference(args, cfg)
     elif world > 1 and args.mode == "coop":

@@ -1430,8 +1430,10 @@ int cb_plan_result_async(cb_plan* plan, uint32_t part, void* host_pinned, uint64
     require(cap_bytes >= 8ULL * (5 + 3 * plan->L), "result buffer smaller than its header");
     DeviceGuard dg(plan->device);
     void* dptr = nullptr;
-    require(cudaHostGetDevicePointer(&dptr, host_pinned, 0) == cudaSuccess,
-            "result buffer is not pinned, device-mapped host memory");
+    if (cudaHostGetDevicePointer(&dptr, host_pinned, 0) != cudaSuccess) {
+      cudaGetLastError();  // not sticky: clear it so later launch checks stay clean
+      throw Error(kInput, "result buffer is not pinned, device-mapped host memory");
+    }
     PeWork& w = plan->pe[part];
     ResultArgs a{};
     a.meta = plan->meta_at(part, 0);

@@ -100,6 +100,86 @@ __global__ void __launch_bounds__(NT, MINB) keep_pipe_k(const uint32_t* __restri
   if (cnt) atomicAdd(out, cnt);
 }
 
+// TMA bulk copies: each warp streams its spans through a ring of NS shared
+// stages (cp.async.bulk + mbarrier, issued by lane 0), so the ids arrive
+// without registers or LSU slots held while the previous stages are hashed.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+template <int NT = 128, int MINB = 8, int IPT = 8, int NS = 4>
+__global__ void __launch_bounds__(NT, MINB) keep_tma_k(const uint32_t* __restrict__ ids,
+                                                       uint64_t n, uint64_t p1, Bal b,
+                                                       uint64_t T, unsigned long long* out) {
+  constexpr int W = NT / 32, SPAN = 32 * IPT;
+  __shared__ __align__(128) uint32_t ring[W][NS][SPAN];
+  __shared__ uint64_t bar[W][NS];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t nspan = n / SPAN;  // whole spans only (the bench size is a multiple)
+  const uint64_t first = static_cast<uint64_t>(blockIdx.x) * W + warp;
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * W;
+  if (lane == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[warp][s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < NS; ++s) {
+      const uint64_t sp = first + s * step;
+      if (sp < nspan) bulk_load(ring[warp][s], ids + sp * SPAN, SPAN * 4, &bar[warp][s]);
+    }
+  }
+  __syncwarp();
+  uint32_t cnt = 0;
+  int s = 0;
+  uint32_t phase = 0;
+  for (uint64_t sp = first; sp < nspan; sp += step) {
+    mbar_wait(&bar[warp][s], phase);
+    uint32_t tv[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) tv[j] = ring[warp][s][lane + 32 * j];
+    __syncwarp();
+    if (lane == 0) {
+      const uint64_t nx = sp + NS * step;
+      if (nx < nspan) bulk_load(ring[warp][s], ids + nx * SPAN, SPAN * 4, &bar[warp][s]);
+    }
+    uint32_t km = 0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) km |= (mix64(p1 ^ tv[j]) <= T ? 1u : 0u) << j;
+    cnt += __popc(km);
+    if (++s == NS) {
+      s = 0;
+      phase ^= 1;
+    }
+  }
+  if (cnt) atomicAdd(out, cnt);
+}
+
+__global__ void __launch_bounds__(128, 8) read_k(const uint32_t* __restrict__ ids, uint64_t n,
+                                                 uint64_t, Bal, uint64_t, unsigned long long* out) {
+  uint32_t acc = 0;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * 8;
+  for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + warp * 32) * 8 + lane;
+       base < n; base += stride)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += __ldg(ids + base + 32 * j);
+  if (acc == 0x12345) atomicAdd(out, 1);
+}
+
 int main() {
   const uint64_t N = 48ull << 20;  // ~ c4 layer-3 scan (48M positions), 192 MB
   std::vector<uint32_t> h(N);
@@ -148,6 +228,11 @@ int main() {
   run(keep_k<0, false, 256, 8>, "V0 compute 256x8", 256, 8);
   run(keep_k<0, false, 128, 8, 16>, "V0 compute IPT16", 128, 8);
   run(keep_k<0, false, 128, 16, 4>, "V0 compute 128x16 IPT4", 128, 16);
+  run(read_k, "read only 128x8", 128, 8);
+  run(keep_tma_k<128, 8, 8, 4>, "TMA ring 128x8 NS4", 128, 8);
+  run(keep_tma_k<128, 8, 8, 6>, "TMA ring 128x8 NS6", 128, 8);
+  run(keep_tma_k<128, 6, 8, 8>, "TMA ring 128x6 NS8", 128, 6);
+  run(keep_tma_k<256, 4, 8, 4>, "TMA ring 256x4 NS4", 256, 4);
   run(keep_pipe_k<128, 8, 8>, "pipelined HBM 128x8", 128, 8);
   run(keep_pipe_k<128, 6, 8>, "pipelined HBM 128x6", 128, 6);
   run(keep_pipe_k<128, 8, 4>, "pipelined HBM 128x8 IPT4", 128, 8);
