@@ -77,6 +77,16 @@ typedef struct cb_sched {
   uint64_t iteration;
 } cb_sched;
 
+/* VariateSource (samplers.hpp:61-126) given directly: z1, z2, cos/sin of the
+ * contribution (exact 1/0 at the endpoints), smoothed flag. */
+typedef struct cb_variates {
+  uint64_t z1;
+  uint64_t z2;
+  double cos_c;
+  double sin_c;
+  int smoothed;
+} cb_variates;
+
 typedef struct cb_graph cb_graph;
 typedef struct cb_partition cb_partition;
 typedef struct cb_features cb_features;
@@ -153,6 +163,11 @@ int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
  * src, layer) (samplers.hpp:158-160) at any layer is a 1-layer plan with
  * base = layer. Drops captured graphs. */
 int cb_plan_set_layer_base(cb_plan* plan, int base);
+/* sample_block(..., const VariateSource&, layer) (samplers.hpp:158-160): the
+ * plan's next batches draw from this source instead of the schedule passed to
+ * cb_sample* (whose kappa is then ignored); nullptr
+ * returns to schedule-derived variates. */
+int cb_plan_set_variate_source(cb_plan* plan, const cb_variates* v);
 /* sample_labor0 / labor_block (samplers.cpp:89-104, 305-312) with the
  * caller's variate r(t) instead of the hash stream: table[t] for every vertex
  * t (num_vertices doubles, host or device memory; copied). While a table is
@@ -361,6 +376,10 @@ typedef struct cb_model cb_model;
 int cb_gcn_model_init(int device, uint32_t in_dim, uint32_t hidden, uint32_t classes,
                       int num_layers, uint64_t seed, cb_model** out);
 /* Read (upload = 0) or write (upload = 1) the weights of one layer. */
+/* GcnModel with explicit layer shapes and host weights (coop.hpp:126-135);
+ * weights row-major, layer after layer. */
+int cb_gcn_model_create(int device, int num_layers, const uint32_t* rows, const uint32_t* cols,
+                        int tanh_hidden, const double* weights, cb_model** out);
 int cb_gcn_model_weights(cb_model* m, int layer, double* host, int upload, uint64_t* rows,
                          uint64_t* cols);
 void cb_gcn_model_destroy(cb_model* m);
@@ -370,6 +389,35 @@ void cb_gcn_model_destroy(cb_model* m);
  * first, each rows x cols (grad_w may be NULL). */
 int cb_train_step(cb_plan* plan, const cb_features* store, uint32_t classes, cb_model* model,
                   double* loss, double* grad_w);
+
+/* ---- host-buffer ops for the C++ drop-in (paper_2310_12403_b200/dropin) ----
+ * The reference's signatures take and return host vectors; these run the
+ * device kernels of the path on uploaded operands and copy the result back.
+ * An exchange record is given as P requester lists concatenated: loc_off[P+1],
+ * src_location parts / rows (coop.hpp:25-37), owner_row_counts[P]. */
+/* all_to_all_forward (coop.hpp:66-68, coop.cpp:145-159) */
+int cb_op_forward_rows(int device, uint32_t P, const uint64_t* loc_off, const uint32_t* loc_part,
+                       const uint64_t* loc_row, const uint64_t* owner_row_counts, uint32_t dim,
+                       const double* owner_flat, double* out_flat);
+/* all_to_all_reverse (sum = 0, last writer in (part, index) order) and
+ * all_to_all_reverse_sum (sum = 1, summed in (part, index) order)
+ * (coop.hpp:70-80, coop.cpp:161-194) */
+int cb_op_reverse_rows(int device, uint32_t P, const uint64_t* loc_off, const uint32_t* loc_part,
+                       const uint64_t* loc_row, const uint64_t* owner_row_counts, uint32_t dim,
+                       const double* requester_flat, int sum, double* owner_out_flat);
+/* gcn_forward (out) and, with grad_out, gcn_backward (grad_h_in, grad_w) of one
+ * block (coop.hpp:106-124, coop.cpp:196-331); edges (src_idx, dst_idx) pairs. */
+int cb_op_gcn_block(int device, uint64_t n_src, uint64_t n_dst, uint64_t n_edges,
+                    const uint32_t* edges, const uint32_t* dst_pos, const double* h_in,
+                    uint32_t in_dim, const double* w, uint32_t out_dim, int tanh_act,
+                    const double* grad_out, double* out, double* grad_h_in, double* grad_w);
+/* A feature table from host rows (FeatureStore::values) and its labels. */
+int cb_features_from_host(int device, uint64_t n_rows, uint32_t dim, int dtype, const void* rows,
+                          cb_features** out);
+int cb_features_set_labels(cb_features* f, const uint32_t* labels);
+/* FeatureStore::synth (coop.cpp:359-376) on the device, into host arrays. */
+int cb_synth_host(int device, uint64_t n, uint32_t dim, uint32_t classes, uint64_t seed,
+                  double* values, uint32_t* labels);
 
 #ifdef __cplusplus
 }

@@ -32,6 +32,15 @@ _SIGS = {
     "cb_graph_generate_rmat": (C.c_int, [_u64, _u64, _u64, C.c_int, _PP]),
     "cb_graph_load_cbcs": (C.c_int, [C.c_char_p, C.c_int, _PP]),
     "cb_graph_set_weights": (C.c_int, [_P, _P]),
+    "cb_plan_set_variate_source": (C.c_int, [_P, _P]),
+    "cb_op_forward_rows": (C.c_int, [C.c_int, _u32, _P, _P, _P, _P, _u32, _P, _P]),
+    "cb_op_reverse_rows": (C.c_int, [C.c_int, _u32, _P, _P, _P, _P, _u32, _P, C.c_int, _P]),
+    "cb_op_gcn_block": (C.c_int, [C.c_int, _u64, _u64, _u64, _P, _P, _P, _u32, _P, _u32, C.c_int,
+                                  _P, _P, _P, _P]),
+    "cb_features_from_host": (C.c_int, [C.c_int, _u64, _u32, C.c_int, _P, _PP]),
+    "cb_features_set_labels": (C.c_int, [_P, _P]),
+    "cb_synth_host": (C.c_int, [C.c_int, _u64, _u32, _u32, _u64, _P, _P]),
+    "cb_gcn_model_create": (C.c_int, [C.c_int, C.c_int, _P, _P, C.c_int, _P, _PP]),
     "cb_graph_save_cbcs": (C.c_int, [_P, C.c_char_p]),
     "cb_graph_info": (C.c_int, [_P, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
     "cb_graph_download": (C.c_int, [_P, _P, _P]),

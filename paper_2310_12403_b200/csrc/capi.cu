@@ -176,6 +176,7 @@ void plan_alloc(cb_plan* pl) {
 // The smoothed (FP64 threshold) kernel path: a smoothing schedule, or the
 // caller's variate table of cb_plan_set_variate_table.
 bool smooth_of(const cb_plan* pl, const cb_sched* s) {
+  if (pl->var_source) return pl->ext_vtab != nullptr || pl->var_source->smoothed != 0;
   return pl->ext_vtab != nullptr || (s->kappa != cbdev::kKappaInf && s->kappa >= 2);
 }
 
@@ -208,7 +209,7 @@ Variates make_variates(const cb_sched* s) {
 void upload_variates(cb_plan* pl, const cb_sched* s, uint32_t n_sched, cudaStream_t st) {
   std::vector<Variates> v(pl->P);
   for (uint32_t p = 0; p < pl->P; ++p) {
-    v[p] = make_variates(s + (n_sched > 1 ? p : 0));
+    v[p] = pl->var_source ? *pl->var_source : make_variates(s + (n_sched > 1 ? p : 0));
     if (pl->ext_vtab) v[p].smoothed = 2;  // caller variate table (sample_labor0)
   }
   CB_CUDA(cudaMemcpyAsync(pl->var, v.data(), sizeof(Variates) * pl->P, cudaMemcpyHostToDevice,
@@ -1189,6 +1190,29 @@ int cb_plan_set_variate_table(cb_plan* plan, const double* table, int on_device)
                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                             plan->stream));
     CB_CUDA(cudaStreamSynchronize(plan->stream));
+  });
+}
+
+// An explicit VariateSource (samplers.hpp:61-126: z1, z2, cos/sin of the
+// contribution, smoothed) for the plan's next batches instead of the one
+// SeedSchedule derives; nullptr goes back to the schedule.
+int cb_plan_set_variate_source(cb_plan* plan, const cb_variates* v) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    DeviceGuard dg(plan->device);
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    plan->drop_graphs();  // captured batches baked the previous smoothing mode in
+    if (!v) {
+      plan->var_source.reset();
+      return;
+    }
+    Variates x{};
+    x.z1 = v->z1;
+    x.z2 = v->z2;
+    x.cos_c = v->cos_c;
+    x.sin_c = v->sin_c;
+    x.smoothed = v->smoothed ? 1 : 0;
+    plan->var_source = x;
   });
 }
 

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -129,6 +130,7 @@ struct cb_features {
   uint64_t shard_r0 = 0;        // first global row of the shard
   void* host_base = nullptr;    // pinned mapped host copy (host tier) or nullptr
   void* hbm_table = nullptr;    // the HBM table while the host tier is active
+  uint32_t* labels = nullptr;   // [n_rows] explicit labels (cb_features_set_labels) or null
   ~cb_features() {
     if (host_base) cudaFreeHost(host_base);
   }
@@ -229,6 +231,7 @@ struct cb_plan {
   bool cap_smooth = false;
   bool have_batch = false;
   bool have_rows = false;
+  std::optional<Variates> var_source;  // cb_plan_set_variate_source override
   uint64_t batches = 0;  // device epoch bumps (count_epoch_bumps)
   uint64_t launches = 0;  // kernels enqueued by the last cb_sample (+ cb_gather)
   double* vtab = nullptr;  // smoothed LABOR r_t table [n] (nullptr: per position)

@@ -21,62 +21,8 @@ struct cb_model {
   }
 };
 
-namespace {
-
-struct TmpArena {
-  std::vector<void*> ptrs;
-  template <typename T>
-  T* get(uint64_t n) {
-    void* p = nullptr;
-    CB_CUDA(cudaMalloc(&p, std::max<uint64_t>(n, 1) * sizeof(T) + 16));
-    ptrs.push_back(p);
-    return static_cast<T*>(p);
-  }
-  ~TmpArena() {
-    for (void* p : ptrs) cudaFree(p);
-  }
-};
-
-struct U32ToU64 {
-  __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
-};
-
-// out[0..n] = exclusive prefix of the u32 counts (out[n] = total)
-void scan_counts(const uint32_t* cnt, uint64_t n, uint64_t* out, TmpArena& A, cudaStream_t st) {
-  auto it = thrust::make_transform_iterator(cnt, U32ToU64{});
-  size_t bytes = 0;
-  CB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, out, static_cast<int64_t>(n + 1), st));
-  void* tmp = A.get<unsigned char>(bytes);
-  CB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, it, out, static_cast<int64_t>(n + 1), st));
-}
-
-__global__ void src_hist_kernel(const uint2* __restrict__ edges, uint64_t n, uint32_t* cnt,
-                                uint32_t* key, uint32_t* val) {
-  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < n;
-       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    atomicAdd(&cnt[edges[e].x], 1u);
-    key[e] = edges[e].x;
-    val[e] = static_cast<uint32_t>(e);
-  }
-}
-
-__global__ void owner_key_kernel(const uint32_t* __restrict__ part, const uint32_t* __restrict__ row,
-                                 uint64_t n, const uint64_t* __restrict__ owner_base,
-                                 uint64_t g0, uint32_t* cnt, uint64_t* key, uint64_t* val) {
-  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
-       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t k = owner_base[part[j]] + row[j];
-    atomicAdd(&cnt[k], 1u);
-    key[g0 + j] = k;
-    val[g0 + j] = g0 + j;
-  }
-}
-
-int grid_of_n(uint64_t n) {
-  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 16)));
-}
-
-}  // namespace
+#include "train_util.cuh"
+using namespace cb_train_util;
 
 extern "C" {
 
@@ -110,6 +56,33 @@ int cb_gcn_model_init(int device, uint32_t in_dim, uint32_t hidden, uint32_t cla
       m->rows.push_back(rows);
       m->cols.push_back(cols);
       m->w.push_back(d);
+    }
+    *out = m.release();
+  });
+}
+
+// A model of any layer shapes (GcnModel::weights as given, coop.hpp:126-135),
+// weights uploaded from host row-major matrices back to back.
+int cb_gcn_model_create(int device, int num_layers, const uint32_t* rows, const uint32_t* cols,
+                        int tanh_hidden, const double* weights, cb_model** out) {
+  return guard([&] {
+    require(out != nullptr && rows != nullptr && cols != nullptr, "null argument");
+    require(num_layers >= 1, "GcnModel: num_layers must be >= 1");
+    DeviceGuard dg(device);
+    auto m = std::make_unique<cb_model>();
+    m->device = device;
+    m->L = num_layers;
+    m->tanh_hidden = tanh_hidden != 0;
+    uint64_t o = 0;
+    for (int l = 0; l < num_layers; ++l) {
+      m->rows.push_back(rows[l]);
+      m->cols.push_back(cols[l]);
+      const uint64_t n = static_cast<uint64_t>(rows[l]) * cols[l];
+      double* p = nullptr;
+      CB_CUDA(cudaMalloc(&p, std::max<uint64_t>(n, 1) * 8));
+      m->w.push_back(p);
+      if (weights && n) CB_CUDA(cudaMemcpy(p, weights + o, n * 8, cudaMemcpyHostToDevice));
+      o += n;
     }
     *out = m.release();
   });
@@ -216,7 +189,8 @@ int cb_train_step(cb_plan* pl, const cb_features* f, uint32_t classes, cb_model*
       const uint64_t n0 = M[p][0].n_dst;
       double* rl = A.get<double>(n0);
       grad[0][p] = A.get<double>(n0 * C);
-      launch_softmax_ce(out[0][p], n0, C, dst_of(p, 0), f->seed, scale, rl, grad[0][p], st);
+      launch_softmax_ce(out[0][p], n0, C, dst_of(p, 0), f->seed, f->labels, scale, rl, grad[0][p],
+                        st);
       std::vector<double> h(n0);
       if (n0) CB_CUDA(cudaMemcpyAsync(h.data(), rl, n0 * 8, cudaMemcpyDeviceToHost, st));
       CB_CUDA(cudaStreamSynchronize(st));

@@ -68,7 +68,8 @@ __global__ void dense_kernel(const double* __restrict__ agg, uint64_t rows, uint
 
 __global__ void softmax_ce_kernel(const double* __restrict__ z_all, uint64_t rows, uint32_t C,
                                   const uint32_t* __restrict__ row_vertex, uint64_t label_seed,
-                                  double scale, double* row_loss, double* grad) {
+                                  const uint32_t* __restrict__ labels, double scale,
+                                  double* row_loss, double* grad) {
   const uint64_t pfx = hstep(hinit(label_seed), 10ULL);  // {kStreamLabel, v}
   for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < rows;
        r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -78,7 +79,9 @@ __global__ void softmax_ce_kernel(const double* __restrict__ z_all, uint64_t row
     for (uint32_t j = 1; j < C; ++j) zmax = fmax(zmax, z[j]);
     double denom = 0.0;
     for (uint32_t j = 0; j < C; ++j) denom = __dadd_rn(denom, exp(__dsub_rn(z[j], zmax)));
-    const uint32_t label = static_cast<uint32_t>(hstep(pfx, row_vertex[r]) % C);
+    // FeatureStore::labels (coop.hpp:145): given, or synth's hash(seed,{10,v}) mod C
+    const uint32_t label = labels ? labels[row_vertex[r]]
+                                  : static_cast<uint32_t>(hstep(pfx, row_vertex[r]) % C);
     row_loss[r] = __dsub_rn(log(denom), __dsub_rn(z[label], zmax));
     for (uint32_t j = 0; j < C; ++j) {
       const double p = __ddiv_rn(exp(__dsub_rn(z[j], zmax)), denom);
@@ -207,10 +210,11 @@ void launch_dense(const double* agg, uint64_t rows, uint32_t in_dim, const doubl
   CB_LAUNCH("dense");
 }
 void launch_softmax_ce(const double* logits, uint64_t rows, uint32_t classes,
-                       const uint32_t* row_vertex, uint64_t label_seed, double scale,
+                       const uint32_t* row_vertex, uint64_t label_seed, const uint32_t* labels,
+                       double scale,
                        double* row_loss, double* grad, cudaStream_t st) {
   if (rows) softmax_ce_kernel<<<grid_n(rows), kTB, 0, st>>>(logits, rows, classes, row_vertex,
-                                                           label_seed, scale, row_loss, grad);
+                                                           label_seed, labels, scale, row_loss, grad);
   CB_LAUNCH("softmax_ce");
 }
 void launch_tanh_grad(const double* t, uint64_t n, double* grad, cudaStream_t st) {

@@ -22,8 +22,9 @@ void launch_dense(const double* agg, uint64_t rows, uint32_t in_dim, const doubl
                   uint32_t out_dim, bool tanh_act, double* out, cudaStream_t st);
 // softmax cross-entropy rows (coop.cpp:392-414): per-row loss, scaled gradient
 void launch_softmax_ce(const double* logits, uint64_t rows, uint32_t classes,
-                       const uint32_t* row_vertex, uint64_t label_seed, double scale,
-                       double* row_loss, double* grad, cudaStream_t st);
+                       const uint32_t* row_vertex, uint64_t label_seed,
+                       const uint32_t* labels, double scale, double* row_loss, double* grad,
+                       cudaStream_t st);
 // dpre = grad * (1 - t^2) for tanh layers (in place)
 void launch_tanh_grad(const double* t, uint64_t n, double* grad, cudaStream_t st);
 // grad_w[i][j] = sum_r agg[r][i] * dp[r][j] (rows ascending, zero agg skipped)
