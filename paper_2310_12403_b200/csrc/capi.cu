@@ -743,7 +743,8 @@ int cb_graph_create_from_csr(const uint64_t* indptr, const uint32_t* indices, ui
     h->g.n = n;
     h->g.m = m;
     CB_CUDA(cudaMalloc(&h->g.indptr, (n + 1) * 8));
-    CB_CUDA(cudaMalloc(&h->g.indices, std::max<uint64_t>(m, 1) * 4));
+    // +16 B: labor_mark bulk-copies 16-byte-aligned supersets of id ranges
+    CB_CUDA(cudaMalloc(&h->g.indices, std::max<uint64_t>(m, 1) * 4 + 16));
     CB_CUDA(cudaMemcpy(h->g.indptr, indptr, (n + 1) * 8, cudaMemcpyHostToDevice));
     if (m) CB_CUDA(cudaMemcpy(h->g.indices, indices, m * 4, cudaMemcpyHostToDevice));
     uint64_t md = 0;

@@ -447,11 +447,83 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                : "memory");
 }
 
+// ---- bulk (TMA engine) staging of a single-record tile's neighbour ids ----
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+// one elected thread: expect `bytes` on bar, then the bulk global->shared copy
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n MBW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MBW;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Span of a single-record tile whose ids sit in shared memory: the IPT keep
+// decisions first (a bit mask per lane), then the keep words by ballot only
+// when the warp kept anything (hub records keep ~k/d of their positions), and
+// each kept position's bitmap bit and staged edge.
+template <int IPT, bool SMOOTH>
+__device__ __forceinline__ void mark_span_smem(const LaborArgs& a, const Variates& v,
+                                               uint64_t p1, uint64_t p2, uint64_t x0,
+                                               uint32_t r0, const uint32_t* ids,
+                                               const ActRec& rec, unsigned long long& uncert,
+                                               const double* vtab) {
+  const uint32_t lane = lane_id();
+  const uint64_t th = rec.b;
+  const uint64_t T = plain_bound(th);
+  uint32_t tv[IPT];
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) tv[j] = ids[r0 + lane + 32 * j];
+  uint32_t km = 0;
+#pragma unroll
+  for (int j = 0; j < IPT; ++j) {
+    const bool keep = SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab)
+                             : mix64_dev(p1 ^ tv[j]) <= T;
+    km |= (keep ? 1u : 0u) << j;
+  }
+  uint32_t my_word = 0;
+  if (__any_sync(0xffffffffu, km != 0)) {
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const unsigned bal = __ballot_sync(0xffffffffu, (km >> j) & 1u);
+      if (lane == j) my_word = bal;
+    }
+    if (km) {
+      uint2* st_lane = a.stage + x0 + r0 + lane;
+#pragma unroll
+      for (int j = 0; j < IPT; ++j)
+        if ((km >> j) & 1u) {
+          set_bit(a.bits, a.summ, tv[j]);
+          st_lane[j * 32] = make_uint2(tv[j], rec.di);
+        }
+    }
+  }
+  if (lane < IPT) a.keep_words[((x0 + r0) >> 5) + lane] = my_word;
+}
+
 // labor_mark: tiles of kNT*IPT scan positions (grid-stride), one 32*IPT span
 // per warp. A tile's records (when <= kRecs) are staged raw in shared memory
-// by cp.async, double-buffered: the records of tile k+1 stream in while tile
-// k is hashed, and tile_first of tile k+2 is already in registers, so the
-// per-tile barrier no longer waits on a chain of global loads.
+// by cp.async, triple-buffered: records of tiles k+1 and k+2 are in flight or
+// staged while tile k is hashed. A tile inside one record (hub neighbour
+// lists: most positions at c4) has its ids brought into shared memory by one
+// bulk copy (TMA engine, mbarrier-completed) issued a tile ahead, so the
+// hashing never waits on the id loads; other tiles load ids per lane.
 template <int IPT, bool SMOOTH>
 __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, unsigned ncta) {
   constexpr int TILE = kMarkNT * IPT;
@@ -461,10 +533,12 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
 #define CB_MARK_RECS (kLaborTile / 4)
 #endif
   constexpr int kRecs = CB_MARK_RECS;  // records staged in smem (else global path)
-  __shared__ __align__(16) ActRec s_act[2][kRecs];
+  __shared__ __align__(16) ActRec s_act[3][kRecs];
+  __shared__ __align__(128) uint32_t s_ids[2][TILE + 4];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ uint32_t s_delta[2];
   LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
-  const uint64_t n_act = meta->n_active;
   const uint64_t ntiles = (total + TILE - 1) / TILE;
   const Variates v = *a.var;
   // prefix({kStreamLabor, layer}) under z1 (and z2 when smoothed)
@@ -473,7 +547,6 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   const double* vtab = (SMOOTH && vtab_used(a, total)) ? a.vtab : nullptr;
   const uint32_t warp = threadIdx.x >> 5;
   unsigned long long uncert = 0;
-  (void)n_act;
   tstamp(a.trace, role, 0);
   auto stage = [&](uint32_t a0, uint32_t a1, int buf) {
     const uint32_t nd = a1 - a0 + 1;
@@ -484,57 +557,115 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  uint32_t a0c = 0, a1c = 0, tfa = 0, tfb = 0;
+  // ids of tile t (inside record 0 of records buffer rb) -> s_ids[ib] by one
+  // bulk copy of the 16-byte-aligned superset; the tile's first id sits at
+  // s_ids[ib][s_delta[ib]] (indices carry >= 16 B of tail padding)
+  auto stage_ids = [&](uint64_t t, int rb, int ib) {
+    const uint64_t x0 = t * TILE;
+    const uint32_t rend = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), total - x0));
+    const uint32_t* first = a.indices + (s_act[rb][0].a + x0);
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(first) & ~static_cast<uintptr_t>(15);
+    const uint32_t delta = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(first) - lo) >> 2);
+    const uint32_t bytes = ((rend + delta) * 4u + 15u) & ~15u;
+    s_delta[ib] = delta;
+    bulk_g2s(s_ids[ib], reinterpret_cast<const void*>(lo), bytes, &s_bar[ib]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0]);
+    mbar_init(&s_bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // records of the first two tiles; tile_first of the third. Record ranges
+  // of this tile (c), the next (n) and the one after (m) rotate in registers.
+  uint32_t c0 = 0, c1 = 0, n0 = 0, n1 = 0, m0 = 0, m1 = 0;
+  uint32_t tfa = 0, tfb = 0;
   if (role < ntiles) {
-    tile_records(a.act, a.tile_first, 0, role, 0, a0c, a1c);
-    stage(a0c, a1c, 0);
+    tile_records(a.act, a.tile_first, 0, role, 0, c0, c1);
+    stage(c0, c1, 0);
   }
   if (role + ncta < ntiles) {
-    tfa = __ldg(&a.tile_first[role + ncta]);
-    tfb = __ldg(&a.tile_first[role + ncta + 1]);
+    tile_records(a.act, a.tile_first, 0, role + ncta, 0, n0, n1);
+    stage(n0, n1, 1);
   }
-  int buf = 0;
-  for (uint64_t tile = role; tile < ntiles; tile += ncta, buf ^= 1) {
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();  // this tile's records are staged; the other buffer is free
-    uint32_t a0n = 0, a1n = 0;
-    if (tile + ncta < ntiles) {
-      tile_decode(tfa, tfb, a0n, a1n);
-      stage(a0n, a1n, buf ^ 1);
-      if (tile + 2 * ncta < ntiles) {
-        tfa = __ldg(&a.tile_first[tile + 2 * ncta]);
-        tfb = __ldg(&a.tile_first[tile + 2 * ncta + 1]);
+  if (role + 2 * ncta < ntiles) {
+    tfa = __ldg(&a.tile_first[role + 2 * ncta]);
+    tfb = __ldg(&a.tile_first[role + 2 * ncta + 1]);
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();  // barriers initialised, first records visible
+  uint32_t iphase = 0;  // mbarrier phase bit per id buffer (bit ib)
+  uint32_t ipure = 0;   // id buffer ib holds its tile's ids (bit ib)
+  if (threadIdx.x == 0 && role < ntiles && c0 == c1) stage_ids(role, 0, 0);
+  if (role < ntiles && c0 == c1) ipure |= 1u;
+  int rb = 0, ib = 0;
+  for (uint64_t tile = role; tile < ntiles; tile += ncta) {
+    const int rb1 = rb == 2 ? 0 : rb + 1, rb2 = rb1 == 2 ? 0 : rb1 + 1;
+    // the tile after this one: its ids (single-record tile) one tile ahead
+    const uint64_t t1 = tile + ncta;
+    if (t1 < ntiles && n0 == n1) {
+      if (threadIdx.x == 0) stage_ids(t1, rb1, ib ^ 1);
+      ipure |= 2u >> ib;  // bit (ib ^ 1)
+    } else {
+      ipure &= ~(2u >> ib);
+    }
+    // records of the tile after that (buffer of the tile two back is free:
+    // every warp passed this iteration's trailing barrier of the last one)
+    if (tile + 2 * ncta < ntiles) {
+      tile_decode(tfa, tfb, m0, m1);
+      stage(m0, m1, rb2);
+      if (tile + 3 * ncta < ntiles) {
+        tfa = __ldg(&a.tile_first[tile + 3 * ncta]);
+        tfb = __ldg(&a.tile_first[tile + 3 * ncta + 1]);
       }
+    } else {
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
     const uint64_t x0 = tile * TILE;
     const uint32_t rend = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), total - x0));
-    const uint32_t a0 = a0c, a1 = a1c;
+    const uint32_t a0 = c0, a1 = c1;
     const uint32_t nd = a1 - a0 + 1;
-    a0c = a0n;
-    a1c = a1n;
     const uint32_t r0 = warp * WSPAN;
-    if (r0 >= rend) continue;
-    if (nd <= static_cast<uint32_t>(kRecs)) {
-      const ActRec* sa = s_act[buf];
-      // record of the warp's first position: 32-ary search over the starts
-      uint32_t lo = 0, hi = nd - 1;
-      while (lo < hi) {
-        const uint32_t step = (hi - lo + 32) / 32;
-        const uint32_t cand = lo + lane_id() * step;
-        const bool le = cand <= hi && sa[cand].pre <= x0 + r0;
-        const unsigned m = __ballot_sync(0xffffffffu, le);
-        const uint32_t best = lo + (31 - __clz(m)) * step;
-        lo = best;
-        hi = min(hi, best + step - 1);
-        if (step == 1) break;
-      }
-      mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, sa, nd, uncert,
-                                   vtab);
-    } else {
-      const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
-      mark_span<IPT, SMOOTH, false>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, nullptr, 0,
+    if ((ipure >> ib) & 1u) {
+      mbar_wait(&s_bar[ib], (iphase >> ib) & 1u);
+      iphase ^= 1u << ib;
+      if (r0 + WSPAN <= rend) {
+        mark_span_smem<IPT, SMOOTH>(a, v, p1, p2, x0, r0, s_ids[ib] + s_delta[ib], s_act[rb][0],
                                     uncert, vtab);
+      } else if (r0 < rend) {
+        mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, 0, s_act[rb], nd, uncert,
+                                     vtab);
+      }
+    } else if (r0 < rend) {
+      if (nd <= static_cast<uint32_t>(kRecs)) {
+        const ActRec* sa = s_act[rb];
+        // record of the warp's first position: 32-ary search over the starts
+        uint32_t lo = 0, hi = nd - 1;
+        while (lo < hi) {
+          const uint32_t step = (hi - lo + 32) / 32;
+          const uint32_t cand = lo + lane_id() * step;
+          const bool le = cand <= hi && sa[cand].pre <= x0 + r0;
+          const unsigned m = __ballot_sync(0xffffffffu, le);
+          const uint32_t best = lo + (31 - __clz(m)) * step;
+          lo = best;
+          hi = min(hi, best + step - 1);
+          if (step == 1) break;
+        }
+        mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, sa, nd, uncert,
+                                     vtab);
+      } else {
+        const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
+        mark_span<IPT, SMOOTH, false>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, nullptr, 0,
+                                      uncert, vtab);
+      }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // this tile's buffers are free; the next records are visible
+    rb = rb1;
+    ib ^= 1;
+    c0 = n0;
+    c1 = n1;
+    n0 = m0;
+    n1 = m1;
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   if (SMOOTH) {
