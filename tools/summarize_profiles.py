@@ -63,13 +63,19 @@ def main():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     dst = os.path.join(root, "profiles")
     os.makedirs(dst, exist_ok=True)
-    md = [f"# {tag}: ncu summary of `python bench.py` (config c2, N=1)\n"]
+    md = [f"# {tag}: ncu summary of `python bench.py` (N=1)\n"]
     if os.path.exists(os.path.join(src, "bench.json")):
         b = json.loads(open(os.path.join(src, "bench.json")).read().strip().splitlines()[-1])
         shutil.copy(os.path.join(src, "bench.json"), os.path.join(dst, f"{tag}_bench.json"))
+        md.append(f"workload: {b['config'].get('workload', '?')}\n")
+        rf = b["roofline"]
         md.append(f"bench: value {b['value']:.0f} seeds/s, {b['ms_per_step']*1e3:.1f} us/step, "
-                  f"e2e {b['e2e']['value']:.0f} seeds/s, gather roofline frac "
-                  f"{b['roofline']['frac']:.3f} ({b['roofline']['achieved']:.0f} GB/s)\n")
+                  f"e2e {b['e2e']['value']:.0f} seeds/s; roofline ({rf.get('kernel', '?')}) frac "
+                  f"{rf['frac']:.3f} ({rf['achieved']:.0f} GB/s)")
+        if "roofline_gather" in b:
+            rg = b["roofline_gather"]
+            md.append(f"; gather frac {rg['frac']:.3f} ({rg['achieved']:.0f} GB/s)")
+        md.append("\n")
     lp = os.path.join(src, "launches.csv")
     if os.path.exists(lp):
         data = launches(lp)
