@@ -415,6 +415,14 @@ int cb_op_gcn_block(int device, uint64_t n_src, uint64_t n_dst, uint64_t n_edges
 int cb_features_from_host(int device, uint64_t n_rows, uint32_t dim, int dtype, const void* rows,
                           cb_features** out);
 int cb_features_set_labels(cb_features* f, const uint32_t* labels);
+/* A feature table over the caller's host rows, read in place by the device
+ * (pinned + mapped until cb_features_destroy; the caller keeps the memory
+ * alive and unmodified meanwhile). */
+int cb_features_wrap_host(int device, uint64_t n_rows, uint32_t dim, int dtype, const void* rows,
+                          cb_features** out);
+/* FeatureStore::load_rows (coop.hpp:151, coop.cpp:378-388): host ids -> host
+ * rows, gathered on the device. CB_INPUT for an id >= n_rows. */
+int cb_op_load_rows(const cb_features* f, const uint32_t* ids, uint64_t n, void* out);
 /* FeatureStore::synth (coop.cpp:359-376) on the device, into host arrays. */
 int cb_synth_host(int device, uint64_t n, uint32_t dim, uint32_t classes, uint64_t seed,
                   double* values, uint32_t* labels);

@@ -131,8 +131,10 @@ struct cb_features {
   void* host_base = nullptr;    // pinned mapped host copy (host tier) or nullptr
   void* hbm_table = nullptr;    // the HBM table while the host tier is active
   uint32_t* labels = nullptr;   // [n_rows] explicit labels (cb_features_set_labels) or null
+  void* registered = nullptr;   // caller's host rows mapped in place (cb_features_wrap_host)
   ~cb_features() {
     if (host_base) cudaFreeHost(host_base);
+    if (registered) cudaHostUnregister(registered);
   }
 };
 

@@ -74,6 +74,23 @@ void check_record(uint32_t P, const uint64_t* loc_off, const uint32_t* loc_part,
   }
 }
 
+// (dst, edge index) keys of a block's edges, for a stable grouping by dst
+__global__ void dst_key_kernel(const uint2* __restrict__ e, uint64_t n, uint32_t* key,
+                               uint32_t* val) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    key[i] = e[i].y;
+    val[i] = static_cast<uint32_t>(i);
+  }
+}
+
+__global__ void permute_edges_kernel(const uint2* __restrict__ e, const uint32_t* __restrict__ perm,
+                                     uint64_t n, uint2* out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = e[perm[i]];
+}
+
 __global__ void labels_kernel(uint64_t seed, uint32_t classes, uint64_t v0, uint64_t n,
                               uint32_t* out) {
   const uint64_t pfx = cbdev::hstep(cbdev::hinit(seed), 10ULL);  // {kStreamLabel, v}
@@ -192,7 +209,7 @@ int cb_op_reverse_rows(int device, uint32_t P, const uint64_t* loc_off, const ui
 }
 
 // gcn_forward / gcn_backward of one block (coop.cpp:236-331) on host buffers:
-// edges are (src_idx, dst_idx) pairs grouped by dst in dst order.
+// edges are (src_idx, dst_idx) pairs in any order (the reference accumulates in edge order).
 int cb_op_gcn_block(int device, uint64_t n_src, uint64_t n_dst, uint64_t n_edges,
                     const uint32_t* edges, const uint32_t* dst_pos, const double* h_in,
                     uint32_t in_dim, const double* w, uint32_t out_dim, int tanh_act,
@@ -203,8 +220,8 @@ int cb_op_gcn_block(int device, uint64_t n_src, uint64_t n_dst, uint64_t n_edges
       require(edges[2 * e] < n_src && edges[2 * e + 1] < n_dst, "gcn: edge index out of range");
     for (uint64_t d = 0; d < n_dst; ++d)
       require(dst_pos[d] < n_src, "gcn: dst_pos_in_src out of range");
-    for (uint64_t e = 1; e < n_edges; ++e)
-      require(edges[2 * e + 1] >= edges[2 * e - 1], "gcn: edges must be grouped by dst");
+    bool grouped = true;
+    for (uint64_t e = 1; e < n_edges && grouped; ++e) grouped = edges[2 * e + 1] >= edges[2 * e - 1];
     DeviceGuard dg(device);
     cudaStream_t st = 0;
     TmpArena A;
@@ -219,13 +236,35 @@ int cb_op_gcn_block(int device, uint64_t n_src, uint64_t n_dst, uint64_t n_edges
     if (in_dim * out_dim)
       CB_CUDA(cudaMemcpyAsync(d_w, w, static_cast<uint64_t>(in_dim) * out_dim * 8,
                               cudaMemcpyHostToDevice, st));
+    // The aggregate walks each destination's edges in edge order; a block
+    // whose edges are not grouped by destination is grouped by a stable sort
+    // (the gradient scatter keeps the original order per source).
+    uint2* d_eg = d_e;
+    if (!grouped) {
+      uint32_t* key = A.get<uint32_t>(n_edges);
+      uint32_t* val = A.get<uint32_t>(n_edges);
+      uint32_t* key2 = A.get<uint32_t>(n_edges);
+      uint32_t* val2 = A.get<uint32_t>(n_edges);
+      dst_key_kernel<<<grid_of_n(n_edges), 256, 0, st>>>(d_e, n_edges, key, val);
+      CB_LAUNCH("dst_key");
+      cub::DoubleBuffer<uint32_t> kb(key, key2), vb(val, val2);
+      size_t bytes = 0;
+      CB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb,
+                                              static_cast<int64_t>(n_edges), 0, 32, st));
+      void* tmp = A.get<unsigned char>(bytes);
+      CB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int64_t>(n_edges),
+                                              0, 32, st));
+      d_eg = A.get<uint2>(n_edges);
+      permute_edges_kernel<<<grid_of_n(n_edges), 256, 0, st>>>(d_e, vb.Current(), n_edges, d_eg);
+      CB_LAUNCH("permute_edges");
+    }
     uint32_t* deg = A.get<uint32_t>(n_dst);
     CB_CUDA(cudaMemsetAsync(deg, 0, std::max<uint64_t>(n_dst, 1) * 4, st));
     launch_in_degrees(d_e, n_edges, deg, st);
     uint64_t* off = A.get<uint64_t>(n_dst + 1);
     scan_counts(deg, n_dst, off, A, st);
     double* agg = A.get<double>(n_dst * in_dim);
-    launch_aggregate(d_e, deg, off, d_dp, n_dst, d_h, in_dim, agg, st);
+    launch_aggregate(d_eg, deg, off, d_dp, n_dst, d_h, in_dim, agg, st);
     double* o = A.get<double>(n_dst * out_dim);
     launch_dense(agg, n_dst, in_dim, d_w, out_dim, tanh_act != 0, o, st);
     if (out && n_dst * out_dim)
@@ -307,6 +346,67 @@ int cb_features_set_labels(cb_features* f, const uint32_t* labels) {
     if (!f->labels) f->labels = f->mem.alloc<uint32_t>(std::max<uint64_t>(f->n_rows, 1));
     if (f->n_rows)
       CB_CUDA(cudaMemcpy(f->labels, labels, f->n_rows * 4, cudaMemcpyHostToDevice));
+  });
+}
+
+// The caller's host rows, read in place by the device: the range is pinned
+// and mapped (cudaHostRegister) until cb_features_destroy. For a table that
+// lives in host memory (the reference's FeatureStore::values, coop.hpp:144);
+// the gather reads rows over the host link instead of copying the table.
+int cb_features_wrap_host(int device, uint64_t n_rows, uint32_t dim, int dtype,
+                          const void* rows, cb_features** out) {
+  return guard([&] {
+    require(out != nullptr && (rows != nullptr || n_rows == 0), "null argument");
+    require(dim >= 1, "feature dim must be >= 1");
+    require(dtype == CB_F64 || dtype == CB_F32 || dtype == CB_F16, "unknown dtype");
+    DeviceGuard dg(device);
+    auto f = std::make_unique<cb_features>();
+    f->device = device;
+    f->dim = dim;
+    f->dtype = dtype;
+    const uint64_t es = dtype == CB_F64 ? 8 : (dtype == CB_F32 ? 4 : 2);
+    f->row_bytes = es * dim;
+    f->n_rows = n_rows;
+    require(reinterpret_cast<uintptr_t>(rows) % es == 0, "host rows are not element-aligned");
+    if (n_rows) {
+      void* h = const_cast<void*>(rows);
+      CB_CUDA(cudaHostRegister(h, n_rows * f->row_bytes,
+                               cudaHostRegisterMapped | cudaHostRegisterPortable));
+      f->registered = h;
+      CB_CUDA(cudaHostGetDevicePointer(&f->table, h, 0));
+    } else {
+      f->table = f->mem.alloc<unsigned char>(f->row_bytes);
+    }
+    *out = f.release();
+  });
+}
+
+// FeatureStore::load_rows (coop.hpp:151, coop.cpp:378-388) from host ids into
+// host rows: out[i] = row ids[i]; ids must be < n_rows (the reference reads
+// past its table otherwise).
+int cb_op_load_rows(const cb_features* f, const uint32_t* ids, uint64_t n, void* out) {
+  return guard([&] {
+    require(f != nullptr && ((ids != nullptr && out != nullptr) || n == 0), "null argument");
+    require(f->shard_rows == 0 && f->row_map == nullptr, "load_rows needs a whole, unsharded table");
+    if (!n) return;
+    for (uint64_t i = 0; i < n; ++i)
+      if (ids[i] >= f->n_rows)
+        throw cb::Error(kInput, "load_rows: vertex id " + std::to_string(ids[i]) +
+                                    " out of range [0, " + std::to_string(f->n_rows) + ")");
+    DeviceGuard dg(f->device);
+    cudaStream_t st = nullptr;
+    CB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    DevBuf d_ids(n * 4), d_out(n * f->row_bytes);
+    CB_CUDA(cudaMemcpyAsync(d_ids.as<void>(), ids, n * 4, cudaMemcpyHostToDevice, st));
+    launch_gather(f->table, vec_bytes_for(f->row_bytes), f->row_bytes, d_ids.as<uint32_t>(),
+                  nullptr, n, nullptr, d_out.as<void>(), st);
+    CB_LAUNCH("load_rows");
+    CB_CUDA(cudaMemcpyAsync(out, d_out.as<void>(), n * f->row_bytes, cudaMemcpyDeviceToHost, st));
+    CB_CUDA(cudaStreamSynchronize(st));
   });
 }
 
