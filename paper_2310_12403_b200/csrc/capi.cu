@@ -112,6 +112,7 @@ void plan_alloc(cb_plan* pl) {
     for (int l = 0; l < L; ++l) {
       w.L[l].tile_first = pl->mem.alloc<uint32_t>(max_tiles + 1);
       CB_CUDA(cudaMemset(w.L[l].tile_first, 0, (max_tiles + 1) * 4));
+      w.L[l].tile_list = pl->mem.alloc<uint2>(max_tiles);
     }
     w.sync.epoch = pl->mem.alloc<unsigned>(1);
     w.sync.tickets = pl->mem.alloc<unsigned>(2 * Sync::kMaxTickets);
@@ -370,6 +371,10 @@ FrontierArgs frontier_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint
   fa.slots = b.slots;
   fa.cap_edges = b.cap_edges;
   fa.cap_tiles = w.sync.max_tiles - 1;
+  const bool lists = pl->kind == CB_LABOR0 || pl->kind == CB_FULL;
+  fa.tile_list = lists ? b.tile_list : nullptr;
+  fa.list_ctr = w.sync.tickets + Sync::kListTicket + 2 * l;
+  fa.list_cap = w.sync.max_tiles;
   fa.ticket = w.sync.tickets + 3 * l;
   fa.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l;
   fa.st_a = w.sync.status_a;
@@ -399,6 +404,9 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
   la.summ = set_bm.summ;
   la.edges = b.edges;
   la.slots = b.slots;
+  la.tile_list = (pl->kind == CB_LABOR0 || pl->kind == CB_FULL) ? b.tile_list : nullptr;
+  la.list_ctr = w.sync.tickets + Sync::kListTicket + 2 * l;
+  la.list_cap = w.sync.max_tiles;
   la.keep_words = w.sync.keep_words;
   la.stage = w.sync.stage;
   la.vtab = pl->ext_vtab ? pl->ext_vtab : w.sync.vtab;

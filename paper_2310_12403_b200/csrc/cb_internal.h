@@ -74,12 +74,12 @@ bool pdl_enabled();
 // Kernels this process enqueued eagerly (graph replays not included).
 extern std::atomic<unsigned long long> g_kernel_launches;
 template <typename... KArgs, typename... Args>
-void launch_k(void (*kernel)(KArgs...), dim3 grid, unsigned block, cudaStream_t st,
-              Args&&... args) {
+void launch_ks(void (*kernel)(KArgs...), dim3 grid, unsigned block, size_t smem, cudaStream_t st,
+               Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -88,6 +88,12 @@ void launch_k(void (*kernel)(KArgs...), dim3 grid, unsigned block, cudaStream_t 
   cfg.numAttrs = 1;
   cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, unsigned block, cudaStream_t st,
+              Args&&... args) {
+  launch_ks(kernel, grid, block, 0, st, std::forward<Args>(args)...);
 }
 
 // ---------------------------------------------------------------- graph ----
@@ -116,6 +122,8 @@ struct LayerBufs {
   uint32_t* dst = nullptr;          // D_l        (cap_dst)
   struct ActRec* act = nullptr;     // records of active dsts (cap_dst+1)
   uint32_t* tile_first = nullptr;   // scan tile -> first record (max_tiles+1)
+  uint2* tile_list = nullptr;       // (tile, record) of single-record tiles from the
+                                    // front, tiles with record boundaries from the back
   uint64_t* out_prefix = nullptr;   // NS output prefix (cap_dst+1)
   uint32_t* slots = nullptr;        // NS reservoir slots (cap_edges)
   uint2* edges = nullptr;           // (src_idx, dst_idx) (cap_edges)
@@ -138,6 +146,8 @@ struct Sync {
   double* vtab = nullptr;                     // smoothed LABOR r_t table [n] (nullptr: none)
   uint64_t max_tiles = 0;
   static constexpr int kMaxTickets = 256;
+  // tickets [kListTicket + 2l, +1]: layer l's single-record / mixed tile counts
+  static constexpr int kListTicket = 192;
 };
 
 // Bitmap dedup structure over the vertex id space.
@@ -190,6 +200,9 @@ struct FrontierArgs {
   uint32_t* slots;
   uint64_t cap_edges;
   uint64_t cap_tiles;  // scan tiles the plan holds (tile_first has cap_tiles + 1)
+  uint2* tile_list;    // (LABOR/FULL, may be null) tile lists for labor_mark
+  unsigned* list_ctr;  // [2]: single-record tiles, mixed tiles (zeroed per batch)
+  uint64_t list_cap;
   unsigned* ticket;
   unsigned* exit_ctr;
   unsigned long long *st_a, *st_b, *st_c;
@@ -213,6 +226,9 @@ struct LaborArgs {
   uint32_t* summ;
   uint2* edges;
   uint32_t* slots;
+  const uint2* tile_list;    // the frontier's tile lists (null: every tile in phase B)
+  const unsigned* list_ctr;
+  uint64_t list_cap;
   uint32_t* keep_words;  // 1 bit per scan position (labor_mark -> labor_emit)
   uint2* stage;          // (t, dst index) of each kept scan position
   double* vtab;          // smoothed r_t per vertex (nullptr: evaluate per position)

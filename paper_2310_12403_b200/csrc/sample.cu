@@ -39,7 +39,7 @@ constexpr uint32_t kTileExact = 0x80000000u;
 // batches' kernels to co-reside with a running mark (65.5 -> 64.1 us/step at
 // 8 batches in flight; one mark alone 45 -> 47 us).
 #ifndef CB_MARK_CTAS
-#define CB_MARK_CTAS (768 / CB_MARK_NT)
+#define CB_MARK_CTAS 4  // 4 x ~50 KB of id rings per SM
 #endif
 constexpr int kMarkCtasPerSM = CB_MARK_CTAS;
 #ifndef CB_MARK_MINB
@@ -188,9 +188,18 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
     eq += bq;
     ea += ba;
     eo += bo;
+    // Tiles started inside each record get tile_first; with lists, the
+    // single-record ones (pure) go to the front of labor_mark's tile list
+    // and the record's last started tile, when it holds a record boundary
+    // (mixed), to the back. A hub starts hundreds of tiles: the whole warp
+    // writes each record's tiles, one record after another.
+    const bool lists = a.tile_list != nullptr;
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const uint64_t i = i0 + j;
+      uint64_t tf = 1, tl = 0, pe = 0;  // started tiles [tf, tl]; pure below pe
+      uint32_t rec_idx = 0;
+      bool exact = false;
       if (i < n) {
         if (q[j] > 0) {
           ActRec rec;
@@ -216,22 +225,71 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
           }
           a.act[ea] = rec;
           // scan tiles whose first position falls inside this record
-          const uint64_t t_first = (eq + kLaborTile - 1) / kLaborTile;
           // (clamped to the scan capacity: an overflowing layer is flagged
           // below and sampled empty, then retried with a larger plan)
-          const uint64_t t_last =
-              min(static_cast<uint64_t>((eq + q[j] - 1) / kLaborTile), a.cap_tiles);
+          tf = (eq + kLaborTile - 1) / kLaborTile;
+          tl = min(static_cast<uint64_t>((eq + q[j] - 1) / kLaborTile), a.cap_tiles);
           // bit 31: the record starts exactly at the tile start (so the
           // previous tile ends with record ea-1: no load to find it)
-          for (uint64_t t = t_first; t <= t_last; ++t)
-            a.tile_first[t] = static_cast<uint32_t>(ea) |
-                              ((t == t_first && eq == t * kLaborTile) ? kTileExact : 0u);
+          exact = eq == tf * kLaborTile;
+          // tiles t with (t + 1) * kLaborTile <= end lie inside this record
+          pe = min(tl + 1, static_cast<uint64_t>((eq + q[j]) / kLaborTile));
+          rec_idx = static_cast<uint32_t>(ea);
           ++ea;
         }
         if (is_ns) a.out_prefix[i] = eo;
       }
       eq += q[j];
       eo += o[j];
+      // list slots: one atomic per warp and list for this j
+      const bool any = tf <= tl;
+      const uint32_t np = (lists && any && pe > tf) ? static_cast<uint32_t>(pe - tf) : 0u;
+      const bool mixed = lists && any && tl + 1 > pe;
+      uint32_t bp = 0, bm = 0;
+      if (lists) {
+        uint32_t ip = np;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+          const uint32_t x = __shfl_up_sync(0xffffffffu, ip, o2);
+          if (lane_id() >= static_cast<unsigned>(o2)) ip += x;
+        }
+        const unsigned mm = __ballot_sync(0xffffffffu, mixed);
+        uint32_t base_p = 0, base_m = 0;
+        if (lane_id() == 31) {
+          if (ip) base_p = atomicAdd(&a.list_ctr[0], ip);
+          if (mm) base_m = atomicAdd(&a.list_ctr[1], static_cast<unsigned>(__popc(mm)));
+        }
+        bp = __shfl_sync(0xffffffffu, base_p, 31) + ip - np;
+        bm = __shfl_sync(0xffffffffu, base_m, 31) + __popc(mm & ((1u << lane_id()) - 1u));
+        if (mixed && bm < a.list_cap)
+          a.tile_list[a.list_cap - 1 - bm] = make_uint2(static_cast<uint32_t>(tl), rec_idx);
+      }
+      // a record that starts a few tiles writes them itself; hubs (many
+      // tiles) are written by the whole warp
+      const bool coop = any && tl >= tf + 4;
+      if (any && !coop) {
+        for (uint64_t t = tf; t <= tl; ++t) {
+          a.tile_first[t] = rec_idx | ((t == tf && exact) ? kTileExact : 0u);
+          if (lists && t < pe && bp + (t - tf) < a.list_cap)
+            a.tile_list[bp + (t - tf)] = make_uint2(static_cast<uint32_t>(t), rec_idx);
+        }
+      }
+      unsigned todo = __ballot_sync(0xffffffffu, coop);
+      while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint64_t f = __shfl_sync(0xffffffffu, tf, src);
+        const uint64_t l2 = __shfl_sync(0xffffffffu, tl, src);
+        const uint64_t p2 = __shfl_sync(0xffffffffu, pe, src);
+        const uint32_t r2 = __shfl_sync(0xffffffffu, rec_idx, src);
+        const bool ex = __shfl_sync(0xffffffffu, exact, src);
+        const uint32_t b2 = __shfl_sync(0xffffffffu, bp, src);
+        for (uint64_t t = f + lane_id(); t <= l2; t += 32) {
+          a.tile_first[t] = r2 | ((t == f && ex) ? kTileExact : 0u);
+          if (lists && t < p2 && b2 + (t - f) < a.list_cap)
+            a.tile_list[b2 + (t - f)] = make_uint2(static_cast<uint32_t>(t), r2);
+        }
+      }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       uint64_t tot = bq + tq, nact = ba + ta;
@@ -517,26 +575,198 @@ __device__ __forceinline__ void mark_span_smem(const LaborArgs& a, const Variate
   if (lane < IPT) a.keep_words[((x0 + r0) >> 5) + lane] = my_word;
 }
 
-// labor_mark: tiles of kNT*IPT scan positions (grid-stride), one 32*IPT span
-// per warp. A tile's records (when <= kRecs) are staged raw in shared memory
-// by cp.async, triple-buffered: records of tiles k+1 and k+2 are in flight or
-// staged while tile k is hashed. A tile inside one record (hub neighbour
-// lists: most positions at c4) has its ids brought into shared memory by one
-// bulk copy (TMA engine, mbarrier-completed) issued a tile ahead, so the
-// hashing never waits on the id loads; other tiles load ids per lane.
+// High word of y = z * c2, the last SplitMix64 multiply of mix64(p1 ^ t)
+// (z after the second xor-shift): keep_plain's prefilter input.
+__device__ __forceinline__ uint32_t mix64_yhi(uint64_t p1, uint32_t t) {
+  uint64_t x = (p1 ^ t) + 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = x ^ (x >> 27);
+  const uint32_t zlo = static_cast<uint32_t>(x), zhi = static_cast<uint32_t>(x >> 32);
+  return __umulhi(zlo, 0x133111ebu) + zlo * 0x94d049bbu + zhi * 0x133111ebu;
+}
+
+// acc = 2 * acc + (yhi <= b2): the prefilter pass bit shifted in through
+// the carry of b2 - yhi (one subtract with carry-out, one add with carry-in)
+__device__ __forceinline__ uint32_t shift_in_pass(uint32_t acc, uint32_t b2, uint32_t yhi) {
+  uint32_t r;
+  asm("{\n .reg .u32 t;\n sub.cc.u32 t, %1, %2;\n addc.u32 %0, %3, %3;\n}"
+      : "=r"(r)
+      : "r"(b2), "r"(yhi), "r"(acc));
+  return r;
+}
+
+// Plain-stream keep test with a high-word prefilter. out = y ^ (y >> 31) for
+// y = z * c2 (the last SplitMix64 round), so out's top 31 bits are y's: when
+// (y_hi >> 1) > (T_hi >> 1) the position is rejected without the final
+// xor-shift and the 64-bit compare. Only survivors (about T / 2^64 of the
+// positions: k/d of a hub's) finish the hash. Exact: same result as
+// mix64(p1 ^ t) <= T.
+__device__ __forceinline__ bool keep_plain(uint64_t p1, uint32_t t, uint64_t T) {
+  uint64_t x = (p1 ^ t) + 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = x ^ (x >> 27);
+  const uint32_t zlo = static_cast<uint32_t>(x), zhi = static_cast<uint32_t>(x >> 32);
+  const uint32_t yhi = __umulhi(zlo, 0x133111ebu) + zlo * 0x94d049bbu + zhi * 0x133111ebu;
+  if ((yhi >> 1) > static_cast<uint32_t>(T >> 33)) return false;
+  const uint64_t y = x * 0x94d049bb133111ebULL;
+  return (y ^ (y >> 31)) <= T;
+}
+
+#ifndef CB_MARK_RECS
+#define CB_MARK_RECS (kLaborTile / 4)
+#endif
+constexpr int kMarkRecs = CB_MARK_RECS;
+#ifndef CB_PURE_STAGES
+#define CB_PURE_STAGES 3
+#endif
+constexpr int kPureStages = CB_PURE_STAGES;     // id tiles in flight per warp
+constexpr uint32_t kPureStride = kLaborTile + 8;  // u32 per ring stage (alignment slack)
+
+// labor_mark's dynamic shared memory: phase B (records, ids, tile list) and
+// phase A (per-warp id rings) reuse the same bytes one after the other.
+struct MarkSmemB {
+  ActRec act[3][kMarkRecs];
+  uint32_t ids[2][kLaborTile + 4];
+};
+struct MarkSmemA {
+  uint32_t ring[kMarkNT / 32][kPureStages][kPureStride];
+};
+constexpr size_t mark_smem_bytes(bool smooth) {
+  return smooth ? sizeof(MarkSmemB)
+                : (sizeof(MarkSmemA) > sizeof(MarkSmemB) ? sizeof(MarkSmemA) : sizeof(MarkSmemB));
+}
+
+// Phase A of labor_mark (plain stream): every full scan tile that lies inside
+// ONE record (hub neighbour lists: most positions at c4) is hashed by one warp
+// on its own, from a per-warp ring of kPureStages tiles brought into shared
+// memory by bulk copies (TMA engine, mbarrier-completed) issued kPureStages
+// tiles ahead, with no CTA barrier. Warp gw of W takes candidate tiles
+// gw, gw + W, ...; a batch of 32 candidates is classified at once (lane i:
+// candidate i, its record read when pure). Lane l owns positions l + 32 j of
+// the tile, so the ballot at j is keep word j; warps that kept nothing (the
+// common case for a hub: ~k/d of its positions survive) skip the ballots.
+template <int NS>
+__device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint64_t n_pure,
+                                          unsigned role, unsigned ncta, uint32_t* ring,
+                                          uint64_t* bars) {
+  constexpr uint32_t TILE = kLaborTile;
+  constexpr uint32_t WPC = kMarkNT / 32;
+  const uint32_t lane = lane_id();
+  const uint64_t W = static_cast<uint64_t>(ncta) * WPC;
+  const uint64_t gw = static_cast<uint64_t>(role) * WPC + (threadIdx.x >> 5);
+  if (gw >= n_pure) return;
+  if (lane == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phase = 0;  // parity bit per stage
+  for (uint64_t kb = 0; gw + kb * 32 * W < n_pure; ++kb) {
+    // lane i: list entry gw + (32 kb + i) W = (tile, record)
+    const uint64_t e = gw + (kb * 32 + lane) * W;
+    uint64_t row = 0, T = 0, x0 = 0;
+    uint32_t di = 0;
+    const bool have = e < n_pure;
+    if (have) {
+      const uint2 tr = a.tile_list[e];
+      x0 = static_cast<uint64_t>(tr.x) * TILE;
+      row = __ldg(&a.act[tr.y].a) + x0;
+      T = plain_bound(__ldg(&a.act[tr.y].b));
+      di = __ldg(&a.act[tr.y].di);
+    }
+    const uint32_t mask = __ballot_sync(0xffffffffu, have);
+    uint32_t im = mask;  // tiles of this batch still to issue, in lane order
+    // bulk copy of the tile owned by lane `src` into stage s (lane 0 issues)
+    auto issue = [&](uint32_t src, int s) {
+      const uint64_t r = __shfl_sync(0xffffffffu, row, src);
+      if (lane == 0) {
+        const uint32_t* first = a.indices + r;
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(first) & ~static_cast<uintptr_t>(15);
+        const uint32_t delta = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(first) - lo) >> 2);
+        bulk_g2s(ring + s * kPureStride, reinterpret_cast<const void*>(lo),
+                 ((TILE + delta) * 4u + 15u) & ~15u, &bars[s]);
+      }
+    };
+    int s_issue = 0;
+    for (int q = 0; q < NS && im; ++q) {
+      issue(__ffs(im) - 1, s_issue);
+      im &= im - 1;
+      s_issue = s_issue + 1 == NS ? 0 : s_issue + 1;
+    }
+    uint32_t cm = mask;
+    int s = 0;
+    while (cm) {
+      const uint32_t src = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const uint64_t r = __shfl_sync(0xffffffffu, row, src);
+      const uint64_t Tq = __shfl_sync(0xffffffffu, T, src);
+      const uint64_t xq = __shfl_sync(0xffffffffu, x0, src);
+      const uint32_t dq = __shfl_sync(0xffffffffu, di, src);
+      const uint32_t delta = static_cast<uint32_t>(
+          (reinterpret_cast<uintptr_t>(a.indices + r) & 15u) >> 2);
+      mbar_wait(&bars[s], (phase >> s) & 1u);
+      phase ^= 1u << s;
+      const uint32_t* ids = ring + s * kPureStride + delta + lane;
+      // prefilter pass bits (yhi <= b2 <=> (yhi >> 1) <= (T >> 33)), then the
+      // exact test for the few survivors
+      const uint32_t b2 = static_cast<uint32_t>(Tq >> 32) | 1u;
+      uint32_t cand = 0;  // bit 31 - j: position j passed
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) cand = shift_in_pass(cand, b2, mix64_yhi(p1, ids[32 * j]));
+      uint32_t km = __brev(cand);
+      for (uint32_t kk = km; kk;) {
+        const int j = __ffs(kk) - 1;
+        kk &= kk - 1;
+        if (!keep_plain(p1, ids[32 * j], Tq)) km &= ~(1u << j);
+      }
+      uint32_t my_word = 0;
+      if (__any_sync(0xffffffffu, km != 0)) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const unsigned bal = __ballot_sync(0xffffffffu, (km >> j) & 1u);
+          if (lane == static_cast<uint32_t>(j)) my_word = bal;
+        }
+        uint32_t kk = km;
+        while (kk) {
+          const int j = __ffs(kk) - 1;
+          kk &= kk - 1;
+          const uint32_t v = ids[32 * j];
+          set_bit(a.bits, a.summ, v);
+          a.stage[xq + lane + 32 * j] = make_uint2(v, dq);
+        }
+      }
+      a.keep_words[(xq >> 5) + lane] = my_word;
+      __syncwarp();  // every lane is done with stage s
+      if (im) {
+        issue(__ffs(im) - 1, s);
+        im &= im - 1;
+      }
+      s = s + 1 == NS ? 0 : s + 1;
+    }
+  }
+}
+
+// labor_mark: tiles of kNT*IPT scan positions, one 32*IPT span per warp.
+// Plain stream: phase A (mark_pure) first takes the full single-record tiles;
+// phase B then runs the tiles with record boundaries (or a partial last tile),
+// listed per CTA from its grid-stride candidates. Smoothed stream: every tile
+// in phase B. In phase B a tile's records (when <= kRecs) are staged raw in
+// shared memory by cp.async, triple-buffered: records of the next two tiles
+// are in flight or staged while one is hashed.
 template <int IPT, bool SMOOTH>
 __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, unsigned ncta) {
   constexpr int TILE = kMarkNT * IPT;
   static_assert(TILE == kLaborTile, "tile size shared with frontier");
   constexpr uint32_t WSPAN = 32 * IPT;  // contiguous positions owned by one warp
-#ifndef CB_MARK_RECS
-#define CB_MARK_RECS (kLaborTile / 4)
-#endif
-  constexpr int kRecs = CB_MARK_RECS;  // records staged in smem (else global path)
-  __shared__ __align__(16) ActRec s_act[3][kRecs];
-  __shared__ __align__(128) uint32_t s_ids[2][TILE + 4];
+  constexpr int kRecs = kMarkRecs;  // records staged in smem (else global path)
+  constexpr int WPC = kMarkNT / 32;
+  extern __shared__ __align__(128) unsigned char s_raw[];  // mark_smem_bytes(SMOOTH)
   __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ __align__(8) uint64_t s_rbar[SMOOTH ? 1 : WPC][kPureStages];
   __shared__ uint32_t s_delta[2];
+  MarkSmemB& sb = *reinterpret_cast<MarkSmemB*>(s_raw);
+  auto& s_act = sb.act;
+  auto& s_ids = sb.ids;
   LayerMeta* meta = a.meta;
   const uint64_t total = meta->scan_total;
   const uint64_t ntiles = (total + TILE - 1) / TILE;
@@ -548,6 +778,25 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   const uint32_t warp = threadIdx.x >> 5;
   unsigned long long uncert = 0;
   tstamp(a.trace, role, 0);
+  // ---- phase A (plain stream with the frontier's tile lists): the
+  // single-record tiles, one warp each. Phase B: the tiles with record
+  // boundaries (the back of the list), or every tile without lists.
+  const bool listed = !SMOOTH && a.tile_list != nullptr;
+  uint64_t n_mixed = 0;
+  if (listed) {
+    const uint64_t n_pure = min(static_cast<uint64_t>(a.list_ctr[0]), ntiles);
+    n_mixed = min(static_cast<uint64_t>(a.list_ctr[1]), ntiles - n_pure);
+    MarkSmemA& sa = *reinterpret_cast<MarkSmemA*>(s_raw);
+    mark_pure<kPureStages>(a, p1, n_pure, role, ncta, &sa.ring[warp][0][0], s_rbar[warp]);
+    __syncthreads();  // the ring memory becomes phase B's
+  }
+  const uint64_t nb = listed ? (n_mixed > role ? (n_mixed - role + ncta - 1) / ncta : 0)
+                             : (ntiles > role ? (ntiles - role + ncta - 1) / ncta : 0);
+  // tile of phase-B item i
+  auto tile_at = [&](uint64_t i) -> uint64_t {
+    const uint64_t j = role + i * ncta;
+    return listed ? static_cast<uint64_t>(a.tile_list[a.list_cap - 1 - j].x) : j;
+  };
   auto stage = [&](uint32_t a0, uint32_t a1, int buf) {
     const uint32_t nd = a1 - a0 + 1;
     if (nd <= static_cast<uint32_t>(kRecs)) {
@@ -575,47 +824,49 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
     mbar_init(&s_bar[1]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // records of the first two tiles; tile_first of the third. Record ranges
-  // of this tile (c), the next (n) and the one after (m) rotate in registers.
+  // records of the first two items; tile_first of the third. Record ranges
+  // of this item (c), the next (n) and the one after (m) rotate in registers.
   uint32_t c0 = 0, c1 = 0, n0 = 0, n1 = 0, m0 = 0, m1 = 0;
   uint32_t tfa = 0, tfb = 0;
-  if (role < ntiles) {
-    tile_records(a.act, a.tile_first, 0, role, 0, c0, c1);
+  if (nb > 0) {
+    tile_records(a.act, a.tile_first, 0, tile_at(0), 0, c0, c1);
     stage(c0, c1, 0);
   }
-  if (role + ncta < ntiles) {
-    tile_records(a.act, a.tile_first, 0, role + ncta, 0, n0, n1);
+  if (nb > 1) {
+    tile_records(a.act, a.tile_first, 0, tile_at(1), 0, n0, n1);
     stage(n0, n1, 1);
   }
-  if (role + 2 * ncta < ntiles) {
-    tfa = __ldg(&a.tile_first[role + 2 * ncta]);
-    tfb = __ldg(&a.tile_first[role + 2 * ncta + 1]);
+  if (nb > 2) {
+    const uint64_t t2 = tile_at(2);
+    tfa = __ldg(&a.tile_first[t2]);
+    tfb = __ldg(&a.tile_first[t2 + 1]);
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();  // barriers initialised, first records visible
   uint32_t iphase = 0;  // mbarrier phase bit per id buffer (bit ib)
   uint32_t ipure = 0;   // id buffer ib holds its tile's ids (bit ib)
-  if (threadIdx.x == 0 && role < ntiles && c0 == c1) stage_ids(role, 0, 0);
-  if (role < ntiles && c0 == c1) ipure |= 1u;
+  if (threadIdx.x == 0 && nb > 0 && c0 == c1) stage_ids(tile_at(0), 0, 0);
+  if (nb > 0 && c0 == c1) ipure |= 1u;
   int rb = 0, ib = 0;
-  for (uint64_t tile = role; tile < ntiles; tile += ncta) {
+  for (uint64_t i = 0; i < nb; ++i) {
+    const uint64_t tile = tile_at(i);
     const int rb1 = rb == 2 ? 0 : rb + 1, rb2 = rb1 == 2 ? 0 : rb1 + 1;
-    // the tile after this one: its ids (single-record tile) one tile ahead
-    const uint64_t t1 = tile + ncta;
-    if (t1 < ntiles && n0 == n1) {
-      if (threadIdx.x == 0) stage_ids(t1, rb1, ib ^ 1);
+    // the item after this one: its ids (single-record tile) one item ahead
+    if (i + 1 < nb && n0 == n1) {
+      if (threadIdx.x == 0) stage_ids(tile_at(i + 1), rb1, ib ^ 1);
       ipure |= 2u >> ib;  // bit (ib ^ 1)
     } else {
       ipure &= ~(2u >> ib);
     }
-    // records of the tile after that (buffer of the tile two back is free:
+    // records of the item after that (buffer of the item two back is free:
     // every warp passed this iteration's trailing barrier of the last one)
-    if (tile + 2 * ncta < ntiles) {
+    if (i + 2 < nb) {
       tile_decode(tfa, tfb, m0, m1);
       stage(m0, m1, rb2);
-      if (tile + 3 * ncta < ntiles) {
-        tfa = __ldg(&a.tile_first[tile + 3 * ncta]);
-        tfb = __ldg(&a.tile_first[tile + 3 * ncta + 1]);
+      if (i + 3 < nb) {
+        const uint64_t t3 = tile_at(i + 3);
+        tfa = __ldg(&a.tile_first[t3]);
+        tfb = __ldg(&a.tile_first[t3 + 1]);
       }
     } else {
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -659,7 +910,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
       }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();  // this tile's buffers are free; the next records are visible
+    __syncthreads();  // this item's buffers are free; the next records are visible
     rb = rb1;
     ib ^= 1;
     c0 = n0;
@@ -1313,8 +1564,20 @@ void launch_labor(const LaborArgs& a, uint64_t max_tiles, bool smooth, cudaStrea
     CB_LAUNCH("vtab");
   }
   const int grid = grid_for(max_tiles * kLaborTile, kLaborTile, kMarkCtasPerSM);
-  if (smooth && a.kind != 0) launch_k(labor_mark_kernel<kMarkIPT, true>, grid, kMarkNT, st, a);
-  else launch_k(labor_mark_kernel<kMarkIPT, false>, grid, kMarkNT, st, a);
+  static const bool attrs_set = [] {
+    CB_CUDA(cudaFuncSetAttribute(labor_mark_kernel<kMarkIPT, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(mark_smem_bytes(true))));
+    CB_CUDA(cudaFuncSetAttribute(labor_mark_kernel<kMarkIPT, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(mark_smem_bytes(false))));
+    return true;
+  }();
+  (void)attrs_set;
+  if (smooth && a.kind != 0)
+    launch_ks(labor_mark_kernel<kMarkIPT, true>, grid, kMarkNT, mark_smem_bytes(true), st, a);
+  else
+    launch_ks(labor_mark_kernel<kMarkIPT, false>, grid, kMarkNT, mark_smem_bytes(false), st, a);
   CB_LAUNCH("labor_mark");
 }
 
