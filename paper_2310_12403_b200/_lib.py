@@ -40,6 +40,8 @@ _SIGS = {
     "cb_features_from_host": (C.c_int, [C.c_int, _u64, _u32, C.c_int, _P, _PP]),
     "cb_features_set_labels": (C.c_int, [_P, _P]),
     "cb_synth_host": (C.c_int, [C.c_int, _u64, _u32, _u32, _u64, _P, _P]),
+    "cb_features_wrap_host": (C.c_int, [C.c_int, _u64, _u32, C.c_int, _P, _PP]),
+    "cb_op_load_rows": (C.c_int, [_P, _P, _u64, _P]),
     "cb_gcn_model_create": (C.c_int, [C.c_int, C.c_int, _P, _P, C.c_int, _P, _PP]),
     "cb_graph_save_cbcs": (C.c_int, [_P, C.c_char_p]),
     "cb_graph_info": (C.c_int, [_P, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
