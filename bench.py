@@ -651,11 +651,19 @@ def run_ours_coop(args, cfg):
         scheds.append(cb.schedule_advance(scheds[-1]))
     if args.exchange == "px":
         from paper_2310_12403_b200.dist import PeerCoop
-        pc = PeerCoop(g, pm, rank, L, scfg, max_seeds=b, store=store)
+        pc = PeerCoop(g, pm, rank, L, scfg, max_seeds=b, store=store, barrier="device")
+        # one eager step on every rank (kernel attributes), then the whole step
+        # (L layers, device barriers on IPC flags, row pull) as one CUDA graph
+        pc.sample(seeds_dev[0], scheds[0])
+        pc.load_inputs()
+        pc.finish()
+        pc.capture(b, scheds[0])
+        n_cap = C.c_uint64()
+        from paper_2310_12403_b200.coopbatch import _check
+        _check(_lib.load().cb_plan_captured_launches(pc._h, 4, C.byref(n_cap)))
 
         def step(i, seeds):
-            pc.sample(seeds, scheds[i])
-            pc.load_inputs()
+            pc.step(seeds, scheds[i])
             return 0  # row bytes read from the device after the timed loop
     else:
         eng = CudaEngine(g, pm, rank, L, scfg, max_seeds=b, store=store,
@@ -670,28 +678,37 @@ def run_ours_coop(args, cfg):
         step(i, seeds_dev[i])
     lc = C.c_uint64()
 
-    def timed(seeds_of):
+    def timed(seeds_of, device_clock=False):
         dist.barrier()
         torch.cuda.synchronize()
         _lib.load().cb_kernel_launches(C.byref(lc))
         l0 = lc.value
+        px = args.exchange == "px"
+        if px and device_clock:  # CUDA events on the plan stream (the launching stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(pc.stream)
         t = time.perf_counter()
         n_rows = 0
         for i in range(W, W + K):
             n_rows += step(i, seeds_of(i))
-        if args.exchange == "px":
+        if px and device_clock:
+            e1.record(pc.stream)
+        if px:
             pc.finish()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
+        if px and device_clock:
+            dt = e0.elapsed_time(e1) / 1e3
         _lib.load().cb_kernel_launches(C.byref(lc))
+        launched = lc.value - l0 + (K * n_cap.value if px else 0)
         dist.barrier()
         m = torch.tensor([dt], dtype=torch.float64)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
-        return float(m.item()), n_rows, lc.value - l0
+        return float(m.item()), n_rows, launched
 
     clocks = ClockSampler(dev)
     with clocks:
-        dt, row_bytes_total, launches = timed(lambda i: seeds_dev[i])
+        dt, row_bytes_total, launches = timed(lambda i: seeds_dev[i], device_clock=True)
     if args.exchange == "px":  # the last step's rows, times K
         nr = C.c_uint64()
         _lib.load().cb_px_sizes(pc._h, L - 1, C.byref(nr), None)
@@ -711,11 +728,14 @@ def run_ours_coop(args, cfg):
         "config": {"workload": cfg["workload"],
                    "mode": f"cooperative (P={world}, one part per GPU; " + (
                        "peer-memory exchange: ids OR-ed into owners' bitmaps over CUDA IPC, "
-                       f"ranks read back, rows pulled from owners' shards; {backend} phase "
-                       "barriers)" if args.exchange == "px" else
+                       "ranks read back, rows pulled from owners' shards; device barriers on "
+                       "IPC flags; the whole step is one CUDA graph per rank)"
+                       if args.exchange == "px" else
                        f"{backend} all-to-allv per layer + feature all-to-allv)"),
-                   "timing": "wall clock between barriers + device sync, max over ranks "
-                             "(host-orchestrated exchange)",
+                   "timing": ("CUDA events on the plan stream around K graph replays, max over "
+                              "ranks" if args.exchange == "px" else
+                              "wall clock between barriers + device sync, max over ranks "
+                              "(host-orchestrated exchange)"),
                    "graph": {"vertices": cfg["n"], "edges": cfg["m"], "gen_s": round(gen_s, 2)}},
         "feature_gbps": row_bytes_total / dt / 1e9,
         "e2e": {"value": seeds_total / e2e_dt, "unit": "seeds/s", "h2d_bytes_per_step": b * 4,

@@ -61,7 +61,8 @@ enum {
   CB_CUDA = 4,
   CB_NCCL = 5,
   CB_OVERFLOW = 6,
-  CB_INTERNAL = 7
+  CB_INTERNAL = 7,
+  CB_UNCERTIFIED = 8 /* smoothed decisions inside the guard band left unresolved */
 };
 
 /* SamplerKind order of samplers.hpp:15 */
@@ -281,7 +282,8 @@ int cb_plan_trace(cb_plan* plan, uint64_t* out, uint64_t n);
 
 /* Kernels in one replay of the captured graphs: what = 1 sample, 2 gather,
  * 3 sample + gather (there the last layer's relabel of a 1-part plan is fused
- * into the gather launch, so it is one fewer than 1 + 2). */
+ * into the gather launch, so it is one fewer than 1 + 2), 4 the captured
+ * peer-exchange step (cb_px_capture). */
 int cb_plan_captured_launches(const cb_plan* plan, int what, uint64_t* n);
 /* Number of kernels one cb_sample/cb_gather call enqueues (for reporting). */
 int cb_plan_launch_count(const cb_plan* plan, int mode, int with_gather, uint64_t* n);
@@ -328,6 +330,20 @@ int cb_features_set_tier(cb_features* f, int host);
 /* SamplerConfig's random-walk parameters (samplers.hpp:19-22) of a CB_RW
  * plan: rw_length o >= 1, rw_restart p in [0,1), rw_walks a >= 1, with
  * a*o <= 512 visits per dst on the device. Defaults 3 / 0.5 / 100. */
+/* Smoothed variates (2 <= kappa < inf): the device's Phi / Phi^-1 may differ
+ * from glibc's by an ulp, so a keep / slot decision whose variate lies within
+ * `band` (relative, default 1e-12) of its threshold is recorded. cb_sample_sync
+ * evaluates every recorded decision with the reference's own arithmetic on
+ * the host (VariateSource::finish, samplers.hpp:96-100; rng.cpp:7-52); if any
+ * differs from the device's, the batch is sampled again with the exact values
+ * (repeated until no new in-band decision appears), so the result is the
+ * reference's by construction. Asynchronous paths (cb_sample, replays, cb_px_*)
+ * cannot resolve: with `strict` (default 1) their cb_synchronize / downloads
+ * return CB_UNCERTIFIED when a recorded decision is left. `perturb` != 0 is a
+ * test hook that flips every unresolved in-band device decision. */
+int cb_plan_set_guard(cb_plan* plan, double band, int perturb, int strict);
+/* Of the last cb_sample_sync: decisions resolved on the host, and re-samplings. */
+int cb_plan_resolve_stats(const cb_plan* plan, uint64_t* resolved, uint64_t* reruns);
 int cb_plan_set_rw(cb_plan* plan, uint32_t rw_length, double rw_restart, uint32_t rw_walks);
 /* Asynchronous D2H (on cb_plan_stream) of the batch's per-part, per-layer
  * counts (n_dst, scan_total, n_active, n_edges, n_src, uncertified, 2 pad;
@@ -347,16 +363,37 @@ int cb_plan_input_ids(cb_plan* plan, uint32_t part, const uint32_t** d_ids, uint
  * requesters read their ranks back from the owners' bitmaps; input rows are
  * pulled from the owners' shards (all_to_all_forward, coop.cpp:145-159).
  * No counts cross ranks and nothing syncs with the host: between
- * cb_px_layer -> cb_px_owner -> cb_px_locate of a layer the caller puts a
- * cross-rank barrier ordered on cb_plan_stream (an NCCL all-reduce on that
- * stream, or a host barrier after a stream sync). Handles are 64 bytes. */
+ * cb_px_layer -> cb_px_owner -> cb_px_locate of a layer goes a cross-rank
+ * barrier ordered on cb_plan_stream -- cb_px_barrier (a device barrier on
+ * flags in the IPC region), an NCCL all-reduce on that stream, or a host
+ * barrier after a stream sync. Handles are 64 bytes. */
 int cb_px_setup(cb_plan* plan, const cb_partition* pm, uint32_t rank, void* handle_out);
 int cb_px_connect(cb_plan* plan, uint32_t peer, const void* handle);
 int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seeds,
                 const cb_sched* sched);
 int cb_px_owner(cb_plan* plan, int layer);
 int cb_px_locate(cb_plan* plan, int layer);
+/* Waits for pending work; CB_OVERFLOW on a capacity overflow, CB_CUDA when a
+ * device barrier timed out (CB_PX_BARRIER_TIMEOUT_MS, default 20 s). */
 int cb_px_finish(cb_plan* plan);
+/* Device barrier across the ranks, ordered on cb_plan_stream: a one-warp
+ * kernel stores this rank's arrival (release, system scope) into every peer's
+ * flag array and waits for every peer's (acquire). Every rank must issue the
+ * same number of barriers. */
+int cb_px_barrier(cb_plan* plan);
+/* The whole cooperative step (coop_sample, coop.cpp:92-102: per layer
+ * px_layer -> barrier -> owner -> barrier -> locate; then the row pull of
+ * cb_px_gather when local != NULL) captured as one CUDA graph per rank (two
+ * when L is odd: the exchange slots alternate across steps). Fixed seed count
+ * n_seeds; the schedule fixes only whether variates are smoothed. Every rank
+ * must have run one eager step before (kernel attributes) and must capture
+ * the same step. */
+int cb_px_capture(cb_plan* plan, uint64_t n_seeds, const cb_sched* sched,
+                  const cb_features* local);
+/* One captured step: seeds (host or device) + the schedule's variates are
+ * copied on cb_plan_stream, then the graph is launched. No host sync. */
+int cb_px_replay(cb_plan* plan, const uint32_t* seeds, int seeds_on_device,
+                 const cb_sched* sched);
 int cb_px_sizes(cb_plan* plan, int layer, uint64_t* n_src, uint64_t* n_owned);
 /* This rank's send_counts row, src_location, and its owned set after layer l. */
 int cb_px_download(cb_plan* plan, int layer, uint64_t* send_row, uint32_t* loc_part,

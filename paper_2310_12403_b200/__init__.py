@@ -3,6 +3,7 @@ arXiv 2310.12403, as hand-written sm_100a kernels behind a C-ABI
 (include/coopbatch_cuda.h) with a host mirror of the reference's API."""
 from .coopbatch import (  # noqa: F401
     KAPPA_INFINITY, MODE_COOP, MODE_INDEP, BipartiteBlock, CapacityError, CoopSampleResult,
+    UncertifiedError,
     CudaError, ExchangeRecord, cross_edge_ratio, FeatureStore, FormatError, Graph, InputError, LayerStack,
     PartitionMap,
     Plan, SamplerConfig, SamplerKind, SeedSchedule, coop_sample, expand, hash_bits,

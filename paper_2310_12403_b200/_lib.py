@@ -120,6 +120,8 @@ _SIGS = {
     "cb_gcn_model_destroy": (None, [_P]),
     "cb_train_step": (C.c_int, [_P, _P, _u32, _P, C.POINTER(C.c_double), _P]),
     "cb_plan_set_rw": (C.c_int, [_P, _u32, C.c_double, _u32]),
+    "cb_plan_set_guard": (C.c_int, [_P, C.c_double, C.c_int, C.c_int]),
+    "cb_plan_resolve_stats": (C.c_int, [_P, C.POINTER(_u64), C.POINTER(_u64)]),
     "cb_plan_meta_async": (C.c_int, [_P, _P, C.POINTER(_u64)]),
     "cb_px_setup": (C.c_int, [_P, _P, _u32, _P]),
     "cb_px_connect": (C.c_int, [_P, _u32, _P]),
@@ -127,6 +129,9 @@ _SIGS = {
     "cb_px_owner": (C.c_int, [_P, C.c_int]),
     "cb_px_locate": (C.c_int, [_P, C.c_int]),
     "cb_px_finish": (C.c_int, [_P]),
+    "cb_px_barrier": (C.c_int, [_P]),
+    "cb_px_capture": (C.c_int, [_P, _u64, C.POINTER(Sched), _P]),
+    "cb_px_replay": (C.c_int, [_P, _P, C.c_int, C.POINTER(Sched)]),
     "cb_px_sizes": (C.c_int, [_P, C.c_int, C.POINTER(_u64), C.POINTER(_u64)]),
     "cb_px_download": (C.c_int, [_P, C.c_int, _P, _P, _P, _P]),
     "cb_features_export": (C.c_int, [_P, _P, C.POINTER(_u64)]),

@@ -41,8 +41,13 @@ class CapacityError(RuntimeError):
     """A device capacity bound overflowed (cb_sample_sync retries these)."""
 
 
+class UncertifiedError(RuntimeError):
+    """Smoothed variate decisions inside the guard band were left unresolved
+    (an asynchronous path; cb_sample_sync resolves them on the host)."""
+
+
 _ERRS = {1: InputError, 2: FormatError, 3: OSError, 4: CudaError, 5: CudaError,
-         6: CapacityError, 7: RuntimeError}
+         6: CapacityError, 7: RuntimeError, 8: UncertifiedError}
 
 
 def _check(rc: int):
@@ -440,6 +445,19 @@ class Plan:
 
     def synchronize(self):
         _check(_lib.load().cb_synchronize(self._h))
+
+    def set_guard(self, band: float = 1e-12, perturb: bool = False, strict: bool = True):
+        """Guard band of smoothed decisions (cb_plan_set_guard): in-band decisions
+        are resolved on the host with the reference's arithmetic by the
+        synchronous sample; `perturb` flips unresolved in-band device decisions
+        (a test hook for the re-sampling path)."""
+        _check(_lib.load().cb_plan_set_guard(self._h, band, int(perturb), int(strict)))
+
+    def resolve_stats(self) -> tuple[int, int]:
+        """(decisions resolved on the host, re-samplings) of the last sync sample."""
+        a, b = C.c_uint64(), C.c_uint64()
+        _check(_lib.load().cb_plan_resolve_stats(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def profile(self, per_pe_seeds, schedule: SeedSchedule, mode: int = MODE_COOP,
                 store: FeatureStore | None = None) -> list[float]:

@@ -205,6 +205,24 @@ Variates make_variates(const cb_sched* s) {
   return v;
 }
 
+constexpr uint32_t kResolvePendCap = 1u << 16;
+
+// The resolve buffers of a plan (allocated the first time a smoothed batch
+// runs): the device Resolve struct, the pending list and its count.
+void resolve_alloc(cb_plan* pl) {
+  if (pl->d_rs) return;
+  CB_CUDA(cudaMalloc(&pl->d_rs, sizeof(cbdev::Resolve)));
+  CB_CUDA(cudaMalloc(&pl->rs_pend, sizeof(cbdev::ResolvePend) * kResolvePendCap));
+  CB_CUDA(cudaMalloc(&pl->rs_npend, 8));
+  CB_CUDA(cudaMemset(pl->rs_npend, 0, 8));
+  cbdev::Resolve r{};
+  r.cap_pend = kResolvePendCap;
+  r.pend = pl->rs_pend;
+  r.n_pend = pl->rs_npend;
+  r.perturb = pl->perturb;
+  CB_CUDA(cudaMemcpy(pl->d_rs, &r, sizeof(r), cudaMemcpyHostToDevice));
+}
+
 // The same variates for every part (the reference's single schedule), or one
 // schedule per part (cb_sample_multi).
 void upload_variates(cb_plan* pl, const cb_sched* s, uint32_t n_sched, cudaStream_t st) {
@@ -212,7 +230,15 @@ void upload_variates(cb_plan* pl, const cb_sched* s, uint32_t n_sched, cudaStrea
   for (uint32_t p = 0; p < pl->P; ++p) {
     v[p] = pl->var_source ? *pl->var_source : make_variates(s + (n_sched > 1 ? p : 0));
     if (pl->ext_vtab) v[p].smoothed = 2;  // caller variate table (sample_labor0)
+    v[p].guard = pl->guard;
+    v[p].part = static_cast<int>(p);
   }
+  // in-band decisions are recorded per (part, layer, vertex[, position])
+  if (v[0].smoothed == 1) {
+    resolve_alloc(pl);
+    for (auto& x : v) x.rs = pl->d_rs;
+  }
+  if (pl->rs_npend) CB_CUDA(cudaMemsetAsync(pl->rs_npend, 0, 8, st));
   CB_CUDA(cudaMemcpyAsync(pl->var, v.data(), sizeof(Variates) * pl->P, cudaMemcpyHostToDevice,
                           st));  // pageable source: staged before the call returns
 }
@@ -330,7 +356,6 @@ ExtractArgs extract_args(PeWork& w, const Bitmap& bm, const Bitmap* zero_bm, uin
   e.count_out = c1;
   e.count_out2 = c2;
   e.ticket = w.sync.tickets + ticket;
-  e.exit_ctr = w.sync.tickets + Sync::kMaxTickets + ticket;
   e.status = w.sync.status_a;
   e.epoch = w.sync.epoch;
   e.slot = slot;
@@ -376,7 +401,6 @@ FrontierArgs frontier_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint
   fa.list_ctr = w.sync.tickets + Sync::kListTicket + 2 * l;
   fa.list_cap = w.sync.max_tiles;
   fa.ticket = w.sync.tickets + 3 * l;
-  fa.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l;
   fa.st_a = w.sync.status_a;
   fa.st_b = w.sync.status_b;
   fa.st_c = w.sync.status_c;
@@ -413,7 +437,6 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
   la.n_vert = pl->ext_vtab ? 0 : pl->g->g.n;  // 0: the table is always used, never rebuilt
   la.cap_edges = b.cap_edges;
   la.ticket = w.sync.tickets + 3 * l + 1;
-  la.exit_ctr = w.sync.tickets + Sync::kMaxTickets + 3 * l + 1;
   la.status = w.sync.status_b;  // emit runs concurrently with extract (status_a)
   la.epoch = w.sync.epoch;
   la.slot = 8 * l + 3;
@@ -631,13 +654,149 @@ void enqueue_batch(cb_plan* pl, int mode, const uint32_t* d_seeds, const uint64_
   pl->dirty_mode = mode;
 }
 
-void check_overflow(cb_plan* pl) {
+uint64_t pending_count(cb_plan* pl);
+
+void check_overflow(cb_plan* pl, bool strict_smooth) {
   CB_CUDA(cudaStreamSynchronize(pl->stream));
   for (auto& w : pl->pe) {
     unsigned o = 0;
     CB_CUDA(cudaMemcpy(&o, w.sync.overflow, 4, cudaMemcpyDeviceToHost));
     if (o) throw Error(kOverflow, "capacity bound exceeded on device (retry with larger plan)");
   }
+  // a smoothed decision inside the guard band that no host pass resolved
+  // (asynchronous paths; cb_sample_sync resolves them) fails loudly
+  if (strict_smooth && pl->strict && pending_count(pl) != 0)
+    throw Error(kUncertified,
+                "smoothed variate decisions inside the guard band are unresolved "
+                "(sample with cb_sample_sync to resolve them on the host)");
+}
+
+// ---- host resolution of smoothed decisions inside the guard band ----------
+// The reference's own arithmetic (rng.cpp:7-52, rng.hpp:40-58,
+// samplers.hpp:96-100) on the host: glibc erfc/log/log1p/exp/sqrt, no FMA
+// (-ffp-contract=off), so the value is the reference's bit for bit.
+namespace hostvar {
+
+double phi(double x) { return 0.5 * std::erfc(-x * 0.7071067811865475244); }
+
+double inverse_phi(double p) {
+  static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02,
+                             -2.759285104469687e+02, 1.383577518672690e+02,
+                             -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02,
+                             -1.556989798598866e+02, 6.680131188771972e+01,
+                             -1.328068155288572e+01};
+  static const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01,
+                             -2.400758277161838e+00, -2.549732539343734e+00,
+                             4.374664141464968e+00,  2.938163982698783e+00};
+  static const double d[] = {7.784695709041462e-03, 3.224671290700398e-01,
+                             2.445134137142996e+00, 3.754408661907416e+00};
+  const double plow = 0.02425;
+  double x;
+  if (p < plow) {
+    const double q = std::sqrt(-2.0 * std::log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  } else if (p <= 1.0 - plow) {
+    const double q = p - 0.5;
+    const double r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0);
+  } else {
+    const double q = std::sqrt(-2.0 * std::log1p(-p));
+    x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  }
+  const double e = phi(x) - p;
+  const double u = e * std::sqrt(2.0 * 3.14159265358979323846) * std::exp(0.5 * x * x);
+  return x - u / (1.0 + 0.5 * x * u);
+}
+
+double normal_from_bits(uint64_t bits) {
+  return inverse_phi((static_cast<double>(bits >> 11) + 0.5) * 0x1.0p-53);
+}
+
+// VariateSource::finish (samplers.hpp:96-100), smoothed branch
+double finish(const Variates& v, uint64_t b1, uint64_t b2) {
+  return phi(v.cos_c * normal_from_bits(b1) + v.sin_c * normal_from_bits(b2));
+}
+
+// The exact variate of a recorded decision: LABOR r_t under prefix
+// {kStreamLabor, layer} (samplers.cpp:114-129), NS u_i under
+// {kStreamNs, layer, s} (samplers.cpp:75-81).
+double exact(const Variates& v, uint64_t k1, uint64_t k2) {
+  using cbdev::hinit;
+  using cbdev::hstep;
+  const uint64_t layer = (k1 >> 32) & 0xffffULL;
+  const uint64_t id = k1 & 0xffffffffULL;
+  if (k1 & cbdev::kResolveLabor) {
+    const uint64_t h1 = hstep(hstep(hinit(v.z1), 2ULL), layer);
+    const uint64_t h2 = hstep(hstep(hinit(v.z2), 2ULL), layer);
+    return finish(v, hstep(h1, id), hstep(h2, id));
+  }
+  const uint64_t h1 = hstep(hstep(hstep(hinit(v.z1), 1ULL), layer), id);
+  const uint64_t h2 = hstep(hstep(hstep(hinit(v.z2), 1ULL), layer), id);
+  return finish(v, hstep(h1, k2), hstep(h2, k2));
+}
+
+}  // namespace hostvar
+
+void resolve_upload(cb_plan* pl, const std::map<std::pair<uint64_t, uint64_t>, double>& tab,
+                    cudaStream_t st) {
+  const uint32_t n = static_cast<uint32_t>(tab.size());
+  if (n > pl->rs_cap) {
+    for (void* q : {static_cast<void*>(pl->rs_k1), static_cast<void*>(pl->rs_k2),
+                    static_cast<void*>(pl->rs_val)})
+      if (q) CB_CUDA(cudaFree(q));
+    pl->rs_cap = std::max<uint32_t>(n, 1024);
+    CB_CUDA(cudaMalloc(&pl->rs_k1, 8ULL * pl->rs_cap));
+    CB_CUDA(cudaMalloc(&pl->rs_k2, 8ULL * pl->rs_cap));
+    CB_CUDA(cudaMalloc(&pl->rs_val, 8ULL * pl->rs_cap));
+  }
+  std::vector<uint64_t> k1, k2;
+  std::vector<double> val;
+  for (const auto& [k, x] : tab) {
+    k1.push_back(k.first);
+    k2.push_back(k.second);
+    val.push_back(x);
+  }
+  if (n) {
+    CB_CUDA(cudaMemcpy(pl->rs_k1, k1.data(), 8ULL * n, cudaMemcpyHostToDevice));
+    CB_CUDA(cudaMemcpy(pl->rs_k2, k2.data(), 8ULL * n, cudaMemcpyHostToDevice));
+    CB_CUDA(cudaMemcpy(pl->rs_val, val.data(), 8ULL * n, cudaMemcpyHostToDevice));
+  }
+  cbdev::Resolve r{};
+  r.k1 = pl->rs_k1;
+  r.k2 = pl->rs_k2;
+  r.val = pl->rs_val;
+  r.n = n;
+  r.cap_pend = kResolvePendCap;
+  r.pend = pl->rs_pend;
+  r.n_pend = pl->rs_npend;
+  r.perturb = pl->perturb;
+  CB_CUDA(cudaMemcpyAsync(pl->d_rs, &r, sizeof(r), cudaMemcpyHostToDevice, st));
+  CB_CUDA(cudaStreamSynchronize(st));  // r lives on this stack frame
+}
+
+uint64_t pending_count(cb_plan* pl) {
+  if (!pl->rs_npend) return 0;
+  unsigned long long n = 0;
+  CB_CUDA(cudaMemcpy(&n, pl->rs_npend, 8, cudaMemcpyDeviceToHost));
+  return n;
+}
+
+uint64_t uncertified_total(cb_plan* pl) {
+  uint64_t u = 0;
+  for (uint32_t p = 0; p < pl->P; ++p)
+    for (int l = 0; l < pl->L; ++l) u += host_meta(pl, p, l).uncertified;
+  return u;
+}
+
+void clear_uncertified(cb_plan* pl, cudaStream_t st) {
+  for (uint32_t p = 0; p < pl->P; ++p)
+    for (int l = 0; l <= pl->L; ++l)
+      CB_CUDA(cudaMemsetAsync(&pl->meta_at(p, l)->uncertified, 0, 8, st));
+  if (pl->rs_npend) CB_CUDA(cudaMemsetAsync(pl->rs_npend, 0, 8, st));
 }
 
 void sample_host(cb_plan* pl, int mode, const uint32_t* flat, const uint64_t* off,
@@ -1154,17 +1313,82 @@ int cb_sample_sync(cb_plan* plan, int mode, const uint32_t* seeds_flat,
   return guard([&] {
     require(plan != nullptr && seeds_off != nullptr, "null argument");
     DeviceGuard dg(plan->device);
-    for (int attempt = 0;; ++attempt) {
-      sample_host(plan, mode, seeds_flat, seeds_off, sched);
-      try {
-        check_overflow(plan);
-        return;
-      } catch (const Error& e) {
-        if (e.code != kOverflow || attempt >= 12) throw;
-        plan->grow *= 2.0;
-        plan_alloc(plan);
-      }
+    const bool smooth = smooth_of(plan, sched) && !plan->ext_vtab &&
+                        !(plan->var_source && plan->var_source->smoothed != 1);
+    std::map<std::pair<uint64_t, uint64_t>, double> tab;
+    plan->rs_resolved = plan->rs_reruns = 0;
+    if (smooth) {
+      resolve_alloc(plan);
+      resolve_upload(plan, tab, plan->stream);
     }
+    const Variates var = plan->var_source ? *plan->var_source : make_variates(sched);
+    for (int pass = 0;; ++pass) {
+      for (int attempt = 0;; ++attempt) {
+        sample_host(plan, mode, seeds_flat, seeds_off, sched);
+        try {
+          check_overflow(plan, false);
+          break;
+        } catch (const Error& e) {
+          if (e.code != kOverflow || attempt >= 12) throw;
+          plan->grow *= 2.0;
+          plan_alloc(plan);
+        }
+      }
+      if (!smooth) return;
+      const uint64_t np = pending_count(plan);
+      if (np == 0) return;
+      // decisions the device made inside the guard band: evaluate each with
+      // the reference's arithmetic; if every one agrees, the batch stands
+      std::vector<cbdev::ResolvePend> pend(std::min<uint64_t>(np, kResolvePendCap));
+      CB_CUDA(cudaMemcpy(pend.data(), plan->rs_pend, sizeof(cbdev::ResolvePend) * pend.size(),
+                         cudaMemcpyDeviceToHost));
+      bool differ = np > pend.size();
+      for (const auto& e : pend) {
+        const double ex = hostvar::exact(var, e.k1, e.k2);
+        tab[{e.k1, e.k2}] = ex;
+        ++plan->rs_resolved;
+        if (e.k1 & cbdev::kResolveLabor) {
+          differ |= (ex <= e.aux) != (e.dev <= e.aux);
+        } else {
+          const double y = ex * static_cast<double>(e.k2 + 1);
+          differ |= static_cast<uint64_t>(y) != static_cast<uint64_t>(e.aux);
+        }
+      }
+      if (!differ) {
+        clear_uncertified(plan, plan->stream);
+        CB_CUDA(cudaStreamSynchronize(plan->stream));
+        return;
+      }
+      // some device decision was wrong: sample again with the exact values
+      // (a corrected layer may bring new in-band decisions: repeat)
+      if (pass >= 8) throw Error(kInternal, "smoothed decisions did not converge");
+      ++plan->rs_reruns;
+      resolve_upload(plan, tab, plan->stream);
+    }
+  });
+}
+
+int cb_plan_set_guard(cb_plan* plan, double band, int perturb, int strict) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require(band >= 0.0 && band < 1.0, "guard band must be in [0, 1)");
+    DeviceGuard dg(plan->device);
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    plan->guard = band;
+    plan->perturb = perturb;
+    plan->strict = strict != 0;
+    if (plan->d_rs) {
+      std::map<std::pair<uint64_t, uint64_t>, double> none;
+      resolve_upload(plan, none, plan->stream);
+    }
+  });
+}
+
+int cb_plan_resolve_stats(const cb_plan* plan, uint64_t* resolved, uint64_t* reruns) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    if (resolved) *resolved = plan->rs_resolved;
+    if (reruns) *reruns = plan->rs_reruns;
   });
 }
 
@@ -1854,6 +2078,12 @@ int cb_plan_trace(cb_plan* plan, uint64_t* out, uint64_t n) {
 int cb_plan_captured_launches(const cb_plan* plan, int what, uint64_t* n) {
   return guard([&] {
     require(plan != nullptr && n != nullptr, "null argument");
+    if (what == 4) {  // the captured peer-exchange step (cb_px_capture)
+      require(plan->px != nullptr && plan->px->exec[0] != nullptr,
+              "no captured step (call cb_px_capture)");
+      *n = plan->px->cap_launches;
+      return;
+    }
     require(plan->exec_sample != nullptr, "no captured batch (call cb_plan_capture)");
     if (what == 1) *n = plan->cap_launches_sample;
     else if (what == 2) *n = plan->cap_launches_gather;

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <optional>
 #include <string>
@@ -180,7 +181,23 @@ struct PxState {
   std::vector<const unsigned char*> fbase;
   std::vector<void*> fopened;
   uint64_t frow_bytes = 0;
+  // device barrier: flag array at region + flag_off on every rank
+  uint64_t flag_off = 0;
+  uint32_t* bar_ctr = nullptr;  // [0] epoch counter, [1] timeout flag
+  PxBarrier bar{};
+  // the captured step (one graph per slot parity when L is odd)
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  uint64_t cap_seeds = 0;
+  bool cap_rows = false, cap_smooth = false;
+  uint64_t cap_launches = 0;
+  void drop_graphs() {
+    for (auto& e : exec)
+      if (e) cudaGraphExecDestroy(e);
+    exec[0] = exec[1] = nullptr;
+  }
   ~PxState() {
+    drop_graphs();
+    if (bar_ctr) cudaFree(bar_ctr);
     for (void* p : opened) cudaIpcCloseMemHandle(p);
     for (void* p : fopened) cudaIpcCloseMemHandle(p);
     if (region) cudaFree(region);
@@ -234,6 +251,19 @@ struct cb_plan {
   bool have_batch = false;
   bool have_rows = false;
   std::optional<Variates> var_source;  // cb_plan_set_variate_source override
+  // smoothed decisions inside the guard band, resolved on the host
+  // (resolve_batch in capi.cu; DESIGN.md §Smoothed variates)
+  double guard = cbdev::kGuard;
+  int perturb = 0;
+  bool strict = true;
+  cbdev::Resolve* d_rs = nullptr;
+  uint64_t* rs_k1 = nullptr;
+  uint64_t* rs_k2 = nullptr;
+  double* rs_val = nullptr;
+  uint32_t rs_cap = 0;
+  cbdev::ResolvePend* rs_pend = nullptr;
+  unsigned long long* rs_npend = nullptr;
+  uint64_t rs_resolved = 0, rs_reruns = 0;  // of the last cb_sample_sync
   uint64_t batches = 0;  // device epoch bumps (count_epoch_bumps)
   uint64_t launches = 0;  // kernels enqueued by the last cb_sample (+ cb_gather)
   double* vtab = nullptr;  // smoothed LABOR r_t table [n] (nullptr: per position)
@@ -270,6 +300,10 @@ struct cb_plan {
     for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ext_vtab) cudaFree(ext_vtab);
+    for (void* q : {static_cast<void*>(d_rs), static_cast<void*>(rs_k1),
+                    static_cast<void*>(rs_k2), static_cast<void*>(rs_val),
+                    static_cast<void*>(rs_pend), static_cast<void*>(rs_npend)})
+      if (q) cudaFree(q);
   }
 
   LayerMeta* meta_at(uint32_t p, int l) { return meta + p * (L + 1) + l; }
@@ -293,7 +327,7 @@ uint64_t enqueue_layer(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t
                        uint64_t cap_dst, uint64_t n_dst_param, Bitmap& set_bm,
                        const RelabelArgs& fused, uint64_t fused_work, bool smooth,
                        const ExtractArgs& ex, cudaStream_t stream = nullptr);
-void check_overflow(cb_plan* pl);
+void check_overflow(cb_plan* pl, bool strict_smooth = true);
 const LayerMeta host_meta(cb_plan* pl, uint32_t p, int l);
 void require_batch(const cb_plan* pl, uint32_t p, int l);
 void count_epoch_bumps(cb_plan* pl, cudaStream_t st, uint64_t bumps);

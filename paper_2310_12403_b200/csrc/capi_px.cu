@@ -23,6 +23,90 @@ PxState& px_of(cb_plan* pl) {
   return *pl->px;
 }
 
+// CB_PX_BARRIER_TIMEOUT_MS (default 20000): a barrier wait that long gives up
+// and flags the step as failed instead of hanging the device.
+unsigned long long barrier_timeout_ns() {
+  const char* e = std::getenv("CB_PX_BARRIER_TIMEOUT_MS");
+  const unsigned long long ms = e ? std::strtoull(e, nullptr, 10) : 20000ULL;
+  return (ms ? ms : 20000ULL) * 1000000ULL;
+}
+
+void check_barrier(PxState& px) {
+  uint32_t err = 0;
+  CB_CUDA(cudaMemcpy(&err, px.bar.err, 4, cudaMemcpyDeviceToHost));
+  if (err) throw Error(kCuda, "peer barrier timed out (a rank stopped or ran a different step)");
+}
+
+// Layer l of the cooperative step on the plan stream: sample, then OR every
+// src id into its owner's exchange bitmap (build_exchange, coop.cpp:35-51).
+// Layer 0's seeds are already in plan->seeds.
+void px_enqueue_layer(cb_plan* plan, int layer, uint64_t n_seeds, bool smooth, int s) {
+  PxState& px = *plan->px;
+  PeWork& w = plan->pe[0];
+  LayerBufs& b = w.L[layer];
+  cudaStream_t st = plan->stream;
+  uint32_t* D = (layer == 0) ? plan->seeds : b.dst;
+  const uint64_t cap = (layer == 0) ? plan->max_seeds : b.cap_dst;
+  if (layer == 0) CB_CUDA(cudaMemsetAsync(px.send, 0, plan->L * px.world * 8, st));
+  px.slot_of[layer] = s;
+  launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);
+  const RelabelArgs none{};
+  enqueue_layer(plan, w, 0, layer, D, cap, layer == 0 ? n_seeds : ~0ULL, w.bm[0], none, 0,
+                smooth,
+                extract_args(w, w.bm[0], nullptr, b.src, b.cap_src,
+                             &plan->meta_at(0, layer)->n_src, nullptr, 3 * layer + 2,
+                             8 * layer + 4));
+  launch_relabel(relabel_args(w.bm[0], b, D, plan->meta_at(0, layer)),
+                 std::max(b.cap_edges, b.cap_dst), st);
+  launch_clear(w.bm[0], b.src, &plan->meta_at(0, layer)->n_src, st);
+  launch_px_route(b.src, &plan->meta_at(0, layer)->n_src, b.cap_src, px.owner, px.peers[s],
+                  px.send + static_cast<uint64_t>(layer) * px.world, st);
+}
+
+// The owner's sorted unique set S^{l+1}_q + word ranks (coop.cpp:44-51). The
+// other slot was last read by the previous layer's locates, which every rank
+// finished before the barrier that precedes this.
+void px_enqueue_owner(cb_plan* plan, int layer) {
+  PxState& px = *plan->px;
+  PeWork& w = plan->pe[0];
+  const int s = px.slot_of[layer];
+  uint32_t* next = (layer + 1 < plan->L) ? w.L[layer + 1].dst : w.owner_final;
+  const uint64_t cap = (layer + 1 < plan->L) ? w.L[layer + 1].cap_dst : w.cap_final;
+  launch_extract(extract_args(w, px.slot[s], &px.slot[s ^ 1], next, cap,
+                              &plan->meta_at(0, layer + 1)->n_dst, nullptr,
+                              3 * plan->L + layer, 8 * layer + 5),
+                 plan->stream);
+}
+
+// src_location from the owners' bitmaps (coop.cpp:53-62).
+void px_enqueue_locate(cb_plan* plan, int layer) {
+  PxState& px = *plan->px;
+  PeWork& w = plan->pe[0];
+  LayerBufs& b = w.L[layer];
+  launch_px_locate(b.src, &plan->meta_at(0, layer)->n_src, b.cap_src, px.owner,
+                   px.peers[px.slot_of[layer]], w.loc_part[layer], w.loc_row[layer],
+                   plan->stream);
+}
+
+// The whole cooperative step with device barriers (coop.cpp:92-102 per layer,
+// then all_to_all_forward when f is given), slots starting at parity s0.
+void px_enqueue_step(cb_plan* plan, uint64_t n_seeds, bool smooth, int s0, const cb_features* f) {
+  PxState& px = *plan->px;
+  for (int l = 0; l < plan->L; ++l) {
+    px_enqueue_layer(plan, l, n_seeds, smooth, (s0 + l) & 1);
+    launch_px_barrier(px.bar, plan->stream);
+    px_enqueue_owner(plan, l);
+    launch_px_barrier(px.bar, plan->stream);
+    px_enqueue_locate(plan, l);
+  }
+  if (f) {
+    PeWork& w = plan->pe[0];
+    const int L = plan->L;
+    launch_px_gather(px.d_fbase, px.owner, f->row_map, f->row_bytes, w.L[L - 1].src,
+                     &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, plan->stream);
+  }
+}
+
 }  // namespace
 
 int cb_px_setup(cb_plan* plan, const cb_partition* pm, uint32_t rank, void* handle_out) {
@@ -42,7 +126,8 @@ int cb_px_setup(cb_plan* plan, const cb_partition* pm, uint32_t rank, void* hand
     const uint64_t wp = ceil_div(std::max<uint64_t>(words, 1), kExtractTileWords) * kExtractTileWords;
     const bool summ = wp > kExtractBigWords;
     const uint64_t per = (2 * wp + (summ ? wp / 32 : 0)) * 4;
-    px->region_bytes = 2 * per;
+    px->flag_off = 2 * per;
+    px->region_bytes = 2 * per + kMaxParts * 4;
     CB_CUDA(cudaMalloc(&px->region, px->region_bytes));
     CB_CUDA(cudaMemset(px->region, 0, px->region_bytes));
     for (int s = 0; s < 2; ++s) {
@@ -58,6 +143,15 @@ int cb_px_setup(cb_plan* plan, const cb_partition* pm, uint32_t rank, void* hand
       px->peers[s].summ[rank] = b.summ;
       px->peers[s].pre[rank] = b.wprefix;
     }
+    CB_CUDA(cudaMalloc(&px->bar_ctr, 8));
+    CB_CUDA(cudaMemset(px->bar_ctr, 0, 8));
+    px->bar.ctr = px->bar_ctr;
+    px->bar.err = px->bar_ctr + 1;
+    px->bar.rank = rank;
+    px->bar.world = px->world;
+    px->bar.timeout_ns = barrier_timeout_ns();
+    px->bar.flags[rank] =
+        reinterpret_cast<uint32_t*>(static_cast<char*>(px->region) + px->flag_off);
     CB_CUDA(cudaMalloc(&px->send, plan->L * px->world * 8 + 8));
     CB_CUDA(cudaMemset(px->send, 0, plan->L * px->world * 8 + 8));
     CB_CUDA(cudaMalloc(&px->d_fbase, kMaxParts * sizeof(void*)));
@@ -81,7 +175,8 @@ int cb_px_connect(cb_plan* plan, uint32_t q, const void* handle) {
     void* p = nullptr;
     CB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     px.opened.push_back(p);
-    const uint64_t per = px.region_bytes / 2;
+    const uint64_t per = px.flag_off / 2;
+    px.bar.flags[q] = reinterpret_cast<uint32_t*>(static_cast<char*>(p) + px.flag_off);
     for (int s = 0; s < 2; ++s) {
       uint32_t* base = reinterpret_cast<uint32_t*>(static_cast<char*>(p) + s * per);
       const uint64_t wp = px.slot[s].words_padded;
@@ -101,37 +196,20 @@ int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seed
     require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
     PxState& px = px_of(plan);
     DeviceGuard dg(plan->device);
-    PeWork& w = plan->pe[0];
-    LayerBufs& b = w.L[layer];
     cudaStream_t st = plan->stream;
-    uint32_t* D = (layer == 0) ? plan->seeds : b.dst;
-    const uint64_t cap = (layer == 0) ? plan->max_seeds : b.cap_dst;
     if (layer == 0) {
       require(seeds != nullptr || n_seeds == 0, "null seeds");
       require(n_seeds <= plan->max_seeds, "more seeds than the plan's max_seeds_per_part");
       if (n_seeds)
-        CB_CUDA(cudaMemcpyAsync(D, seeds, n_seeds * 4, cudaMemcpyDefault, st));
+        CB_CUDA(cudaMemcpyAsync(plan->seeds, seeds, n_seeds * 4, cudaMemcpyDefault, st));
       upload_variates(plan, sched, 1, st);
-      CB_CUDA(cudaMemsetAsync(px.send, 0, plan->L * px.world * 8, st));
       plan->seeds_off.assign({0, n_seeds});
       plan->mode = CB_MODE_COOP;
     }
     const bool smooth = smooth_of(plan, sched);
     const int s = static_cast<int>(px.layer_ctr++ & 1);
-    px.slot_of[layer] = s;
     count_epoch_bumps(plan, st, 1);
-    launch_batch_begin(w.sync, nullptr, nullptr, nullptr, nullptr, 0, 0, st);
-    const RelabelArgs none{};
-    enqueue_layer(plan, w, 0, layer, D, cap, layer == 0 ? n_seeds : ~0ULL, w.bm[0], none, 0,
-                  smooth,
-                  extract_args(w, w.bm[0], nullptr, b.src, b.cap_src,
-                               &plan->meta_at(0, layer)->n_src, nullptr, 3 * layer + 2,
-                               8 * layer + 4));
-    launch_relabel(relabel_args(w.bm[0], b, D, plan->meta_at(0, layer)),
-                   std::max(b.cap_edges, b.cap_dst), st);
-    launch_clear(w.bm[0], b.src, &plan->meta_at(0, layer)->n_src, st);
-    launch_px_route(b.src, &plan->meta_at(0, layer)->n_src, b.cap_src, px.owner, px.peers[s],
-                    px.send + static_cast<uint64_t>(layer) * px.world, st);
+    px_enqueue_layer(plan, layer, layer == 0 ? n_seeds : 0, smooth, s);
     plan->have_batch = true;
     plan->have_rows = false;
     plan->dirty_mode = -1;
@@ -143,18 +221,9 @@ int cb_px_owner(cb_plan* plan, int layer) {
   return guard([&] {
     require(plan != nullptr, "null plan");
     require(layer >= 0 && layer < plan->L, "layer index out of range");
-    PxState& px = px_of(plan);
+    px_of(plan);
     DeviceGuard dg(plan->device);
-    PeWork& w = plan->pe[0];
-    const int s = px.slot_of[layer];
-    uint32_t* next = (layer + 1 < plan->L) ? w.L[layer + 1].dst : w.owner_final;
-    const uint64_t cap = (layer + 1 < plan->L) ? w.L[layer + 1].cap_dst : w.cap_final;
-    // the other slot was last read by the previous layer's locates, which
-    // every rank finished before the barrier that precedes this call
-    launch_extract(extract_args(w, px.slot[s], &px.slot[s ^ 1], next, cap,
-                                &plan->meta_at(0, layer + 1)->n_dst, nullptr,
-                                3 * plan->L + layer, 8 * layer + 5),
-                   plan->stream);
+    px_enqueue_owner(plan, layer);
   });
 }
 
@@ -163,13 +232,9 @@ int cb_px_locate(cb_plan* plan, int layer) {
   return guard([&] {
     require(plan != nullptr, "null plan");
     require(layer >= 0 && layer < plan->L, "layer index out of range");
-    PxState& px = px_of(plan);
+    px_of(plan);
     DeviceGuard dg(plan->device);
-    PeWork& w = plan->pe[0];
-    LayerBufs& b = w.L[layer];
-    launch_px_locate(b.src, &plan->meta_at(0, layer)->n_src, b.cap_src, px.owner,
-                     px.peers[px.slot_of[layer]], w.loc_part[layer], w.loc_row[layer],
-                     plan->stream);
+    px_enqueue_locate(plan, layer);
   });
 }
 
@@ -178,6 +243,83 @@ int cb_px_finish(cb_plan* plan) {
     require(plan != nullptr, "null plan");
     DeviceGuard dg(plan->device);
     check_overflow(plan);
+    if (plan->px) check_barrier(*plan->px);
+  });
+}
+
+int cb_px_barrier(cb_plan* plan) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    PxState& px = px_of(plan);
+    DeviceGuard dg(plan->device);
+    launch_px_barrier(px.bar, plan->stream);
+  });
+}
+
+int cb_px_capture(cb_plan* plan, uint64_t n_seeds, const cb_sched* sched,
+                  const cb_features* local) {
+  return guard([&] {
+    require(plan != nullptr && sched != nullptr, "null argument");
+    require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
+    require(n_seeds <= plan->max_seeds, "more seeds than the plan's max_seeds_per_part");
+    PxState& px = px_of(plan);
+    if (local) {
+      for (uint32_t q = 0; q < px.world; ++q)
+        require(px.fbase[q] != nullptr, "feature shard of a rank not connected");
+    }
+    DeviceGuard dg(plan->device);
+    px.drop_graphs();
+    if (local) prepare_rows(plan, local, false);
+    const bool smooth = smooth_of(plan, sched);
+    // kernel attributes are set by the eager layer calls every rank has made
+    // before capturing (the caller's warm-up step); capture is local only
+    const int parities = (plan->L & 1) ? 2 : 1;
+    const unsigned long long k0 = g_kernel_launches.load();
+    for (int par = 0; par < parities; ++par) {
+      cudaGraph_t graph;
+      CB_CUDA(cudaStreamBeginCapture(plan->stream, cudaStreamCaptureModeThreadLocal));
+      px_enqueue_step(plan, n_seeds, smooth, par, local);
+      CB_CUDA(cudaStreamEndCapture(plan->stream, &graph));
+      CB_CUDA(cudaGraphInstantiate(&px.exec[par], graph, 0));
+      CB_CUDA(cudaGraphDestroy(graph));
+    }
+    px.cap_launches = (g_kernel_launches.load() - k0) / parities;
+    px.cap_seeds = n_seeds;
+    px.cap_rows = local != nullptr;
+    px.cap_smooth = smooth;
+  });
+}
+
+int cb_px_replay(cb_plan* plan, const uint32_t* seeds, int seeds_on_device,
+                 const cb_sched* sched) {
+  NvtxRange nvtx_("cb.px_replay");
+  return guard([&] {
+    require(plan != nullptr && sched != nullptr, "null argument");
+    require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
+    PxState& px = px_of(plan);
+    require(px.exec[0] != nullptr, "no captured step (call cb_px_capture)");
+    require(smooth_of(plan, sched) == px.cap_smooth,
+            "schedule smoothing differs from the captured step (re-capture)");
+    require(seeds != nullptr || px.cap_seeds == 0, "null seeds");
+    DeviceGuard dg(plan->device);
+    cudaStream_t st = plan->stream;
+    if (px.cap_seeds)
+      CB_CUDA(cudaMemcpyAsync(plan->seeds, seeds, px.cap_seeds * 4,
+                              seeds_on_device ? cudaMemcpyDeviceToDevice
+                                              : cudaMemcpyHostToDevice,
+                              st));
+    upload_variates(plan, sched, 1, st);
+    count_epoch_bumps(plan, st, plan->L);
+    const int par = (plan->L & 1) ? static_cast<int>(px.layer_ctr & 1) : 0;
+    CB_CUDA(cudaGraphLaunch(px.exec[par], st));
+    px.layer_ctr += plan->L;
+    for (int l = 0; l < plan->L; ++l) px.slot_of[l] = (par + l) & 1;
+    plan->seeds_off.assign({0, px.cap_seeds});
+    plan->mode = CB_MODE_COOP;
+    plan->have_batch = true;
+    plan->have_rows = px.cap_rows;
+    plan->dirty_mode = -1;
+    plan->launches = px.cap_launches;
   });
 }
 

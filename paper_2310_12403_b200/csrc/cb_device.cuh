@@ -115,14 +115,63 @@ __device__ __forceinline__ double dnormal_from_bits(uint64_t bits) {
   return dinverse_phi(__dmul_rn(__dadd_rn(static_cast<double>(bits >> 11), 0.5), 0x1.0p-53));
 }
 
+// Smoothed decisions inside the guard band, resolved on the host with the
+// reference's own arithmetic (glibc erfc/log/exp, no FMA; host_variates in
+// capi.cu). Keys: LABOR (kResolveLabor | part << 48 | layer << 32 | t, 0),
+// NS (part << 48 | layer << 32 | s, i); `val` is the host's exact variate,
+// sorted by key.
+// Decisions not in the table are appended to `pend` for the host.
+constexpr uint64_t kResolveLabor = 1ULL << 63;
+struct ResolvePend {
+  uint64_t k1, k2;
+  double dev;  // the value the device decided with
+  double aux;  // LABOR: the threshold k/d; NS: the device's r = floor(u * (i + 1))
+};
+struct Resolve {
+  const uint64_t* k1;
+  const uint64_t* k2;
+  const double* val;
+  uint32_t n;
+  uint32_t cap_pend;
+  ResolvePend* pend;
+  unsigned long long* n_pend;
+  int perturb;  // test hook: flip every unresolved in-band device decision
+  int pad;
+};
+
 // Per-batch variate parameters (samplers.hpp:53-126 VariateSource), resident
 // in device memory so a captured batch replays with new keys.
 struct Variates {
   uint64_t z1, z2;
   double cos_c, sin_c;
   int smoothed;
-  int pad;
+  int part;            // index of the part these variates belong to
+  double guard;        // relative guard band of smoothed decisions
+  const Resolve* rs;   // host-resolved decisions (nullptr: count only)
 };
+
+__device__ inline bool resolve_lookup(const Resolve* rs, uint64_t k1, uint64_t k2, double& out) {
+  if (rs == nullptr) return false;
+  uint32_t lo = 0, hi = rs->n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const uint64_t a = rs->k1[mid], b = rs->k2[mid];
+    if (a < k1 || (a == k1 && b < k2)) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < rs->n && rs->k1[lo] == k1 && rs->k2[lo] == k2) {
+    out = rs->val[lo];
+    return true;
+  }
+  return false;
+}
+
+__device__ inline void resolve_record(const Resolve* rs, uint64_t k1, uint64_t k2, double dev,
+                                      double aux) {
+  if (rs == nullptr) return;
+  const unsigned long long i = atomicAdd(rs->n_pend, 1ULL);
+  if (i < rs->cap_pend) rs->pend[i] = ResolvePend{k1, k2, dev, aux};
+}
 
 // samplers.hpp:96-100 finish() for the smoothed stream. Out of line: it is
 // FP64-transcendental heavy and only runs for 2 <= kappa < inf.
@@ -132,7 +181,7 @@ static __device__ __noinline__ double smooth_finish(const Variates& v, uint64_t 
   return dphi(n);
 }
 
-// Guard band for smoothed decisions (relative); see DESIGN.md.
+// Default guard band for smoothed decisions (relative); see DESIGN.md.
 constexpr double kGuard = 1e-12;
 
 // ---- memory-order helpers ---------------------------------------------------

@@ -26,6 +26,7 @@ enum Status : int {
   kNccl = 5,
   kOverflow = 6,  // capacity-bounded buffer overflowed on device (retryable)
   kInternal = 7,
+  kUncertified = 8,  // smoothed decisions inside the guard band left unresolved
 };
 
 struct Error : std::runtime_error {
@@ -204,7 +205,6 @@ struct FrontierArgs {
   unsigned* list_ctr;  // [2]: single-record tiles, mixed tiles (zeroed per batch)
   uint64_t list_cap;
   unsigned* ticket;
-  unsigned* exit_ctr;
   unsigned long long *st_a, *st_b, *st_c;
   const unsigned* epoch;
   int slot;
@@ -235,7 +235,6 @@ struct LaborArgs {
   uint64_t n_vert;
   uint64_t cap_edges;
   unsigned* ticket;
-  unsigned* exit_ctr;
   unsigned long long* status;
   const unsigned* epoch;
   int slot;
@@ -281,7 +280,6 @@ struct ExtractArgs {
   unsigned long long* count_out;
   unsigned long long* count_out2;
   unsigned* ticket;
-  unsigned* exit_ctr;
   unsigned long long* status;
   const unsigned* epoch;
   int slot;

@@ -102,6 +102,42 @@ __global__ void px_locate_kernel(const uint32_t* __restrict__ src,
   }
 }
 
+// One warp: publish this rank's arrival to every peer (release at system
+// scope, after the layer's peer-memory writes of the preceding kernels), then
+// lane q waits for rank q's arrival in the local flag array (acquire).
+__global__ void px_barrier_kernel(PxBarrier b) {
+  const uint32_t lane = threadIdx.x;
+  uint32_t e = 0;
+  if (lane == 0) {
+    e = *b.ctr + 1;
+    *b.ctr = e;
+  }
+  e = __shfl_sync(0xffffffffu, e, 0);
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  if (lane < b.world)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(b.flags[lane] + b.rank), "r"(e)
+                 : "memory");
+  if (lane < b.world) {
+    const uint32_t* f = b.flags[b.rank] + lane;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (static_cast<int32_t>(v - e) >= 0) break;
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > b.timeout_ns) {
+        atomicExch(b.err, 1u);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
 template <typename V>
 __global__ void px_gather_kernel(const unsigned char* const* __restrict__ bases,
                                  const uint32_t* __restrict__ owner,
@@ -155,6 +191,11 @@ void launch_px_locate(const uint32_t* src, const unsigned long long* count, uint
   launch_k(px_locate_kernel, grid_for(cap, 256, 8), 256, st, src, count, cap, owner, peers,
            loc_part, loc_row);
   CB_LAUNCH("px_locate");
+}
+
+void launch_px_barrier(const PxBarrier& b, cudaStream_t st) {
+  launch_k(px_barrier_kernel, 1, 32, st, b);
+  CB_LAUNCH("px_barrier");
 }
 
 void launch_px_gather(const unsigned char* const* d_bases, const uint32_t* owner,

@@ -29,6 +29,19 @@ struct PxPeers {
   const uint32_t* pre[kMaxParts];
 };
 
+// Cross-rank barrier in peer memory: flags[q] = rank q's arrival slots
+// (IPC-mapped; entry r of rank q's array is written by rank r). The epoch is a
+// device counter, so a captured graph replays it; ranks run the same number
+// of barriers. A wait longer than timeout_ns sets *err and gives up (no hang).
+struct PxBarrier {
+  uint32_t* flags[kMaxParts];
+  uint32_t* ctr;
+  uint32_t* err;
+  uint32_t rank, world;
+  unsigned long long timeout_ns;
+};
+void launch_px_barrier(const PxBarrier& b, cudaStream_t st);
+
 // Requester side of build_exchange (coop.cpp:35-51): OR every src id into its
 // owner's exchange bitmap over peer memory; send_row[q] += ids sent to q.
 void launch_px_route(const uint32_t* src, const unsigned long long* count, uint64_t cap,

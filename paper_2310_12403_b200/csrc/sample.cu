@@ -33,11 +33,8 @@ namespace {
 
 constexpr int kNT = 256;
 constexpr uint32_t kTileExact = 0x80000000u;
-// labor_mark residency: 4 CTAs/SM so one CTA's staging barrier overlaps
-// another's hashing
-// 6 of the 8 CTAs that fit per SM: leaves registers for other in-flight
-// batches' kernels to co-reside with a running mark (65.5 -> 64.1 us/step at
-// 8 batches in flight; one mark alone 45 -> 47 us).
+// labor_mark residency: 4 CTAs/SM (shared memory: ~50 KB of TMA id rings
+// each), so one CTA's staging barrier overlaps another's hashing.
 #ifndef CB_MARK_CTAS
 #define CB_MARK_CTAS 4  // 4 x ~50 KB of id rings per SM
 #endif
@@ -60,11 +57,8 @@ __device__ __forceinline__ void set_bit(uint32_t* bits, uint32_t* summ, uint32_t
 
 using rbody::bm_rank;
 
-// Reset a ticket counter once every CTA of the launch is done with it, so no
-// per-batch memset of the tickets is needed.
 // Tickets are zeroed by batch_begin_kernel at the start of every batch /
 // per-layer op (stream order), so kernels need no exit bookkeeping.
-__device__ __forceinline__ void retire_ticket(unsigned*, unsigned*, unsigned) {}
 
 using rbody::relabel_range;
 
@@ -322,7 +316,6 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
     meta->n_edges = 0;
     if (is_ns) a.out_prefix[0] = 0;
   }
-  retire_ticket(a.ticket, a.exit_ctr, gridDim.x);
 }
 
 template <int IPT>
@@ -397,15 +390,33 @@ __device__ __forceinline__ uint64_t plain_bound(uint64_t th) {
   return th >= (1ULL << 53) ? ~0ULL : ((th << 11) | 0x7ffULL);
 }
 
+// A smoothed decision inside the guard band takes the host-resolved r_t when
+// the resolve table has it; otherwise it is counted as uncertified and
+// recorded for the host (Variates::rs, DESIGN.md §Smoothed variates).
+__device__ __noinline__ bool labor_in_band(const Variates& v, int layer, uint32_t t, double rr,
+                                           double thr, unsigned long long& uncert) {
+  const uint64_t k1 = kResolveLabor | (static_cast<uint64_t>(v.part) << 48) |
+                      (static_cast<uint64_t>(layer) << 32) | t;
+  double ex;
+  if (resolve_lookup(v.rs, k1, 0, ex)) return ex <= thr;
+  ++uncert;
+  bool keep = rr <= thr;
+  if (v.rs && v.rs->perturb) keep = !keep;  // test hook: a wrong device decision
+  resolve_record(v.rs, k1, 0, keep ? thr : 2.0 * thr + 1.0, thr);
+  return keep;
+}
+
 template <bool SMOOTH>
 __device__ __forceinline__ bool keep_rule(const Variates& v, uint64_t p1, uint64_t p2,
                                           uint32_t t, uint64_t th, unsigned long long& uncert,
-                                          const double* vtab) {
+                                          const double* vtab, int layer) {
   if (!SMOOTH) return (mix64_dev(p1 ^ t) >> 11) <= th;
   if (th == ~0ULL) return true;
   const double thr = __longlong_as_double(static_cast<long long>(th));
   const double rr = vtab ? __ldg(vtab + t) : smooth_finish(v, hstep(p1, t), hstep(p2, t));
-  if (fabs(rr - thr) <= kGuard * thr) ++uncert;
+  // (a caller's variate table, smoothed == 2, is exact by definition)
+  if (v.smoothed != 2 && fabs(rr - thr) <= v.guard * thr)
+    return labor_in_band(v, layer, t, rr, thr, uncert);
   return rr <= thr;
 }
 
@@ -456,7 +467,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
     for (int j = 0; j < IPT; ++j) tv[j] = __ldg(row + j * 32);
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
-      const bool keep = SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab)
+      const bool keep = SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab, a.layer)
                                : mix64_dev(p1 ^ tv[j]) <= T;
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == j) my_word = bal;
@@ -485,7 +496,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
       const uint32_t r = r0 + j * 32 + lane;
       const bool keep =
           (r < rend) &&
-          (SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th_of(li[j]), uncert, vtab)
+          (SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th_of(li[j]), uncert, vtab, a.layer)
                   : mix64_dev(p1 ^ tv[j]) <= plain_bound(th_of(li[j])));
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == j) my_word = bal;
@@ -551,7 +562,7 @@ __device__ __forceinline__ void mark_span_smem(const LaborArgs& a, const Variate
   uint32_t km = 0;
 #pragma unroll
   for (int j = 0; j < IPT; ++j) {
-    const bool keep = SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab)
+    const bool keep = SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab, a.layer)
                              : mix64_dev(p1 ^ tv[j]) <= T;
     km |= (keep ? 1u : 0u) << j;
   }
@@ -1020,13 +1031,31 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned rol
     }
   }
   tstamp(trace, 32 + role, 4);
-  retire_ticket(a.ticket, a.exit_ctr, ncta);
 }
 
 // ---------------------------------------------------------------- NS -------
 // Reservoir (samplers.cpp:75-84) restated per slot: the final content of slot
 // j is the largest i in [k, d) with floor(U_i*(i+1)) == j, else j. Every
 // position is an independent atomicMax, so hub rows split across CTAs.
+// NS slot roll r = floor(u * (i + 1)) near an integer (ns_block,
+// samplers.cpp:80-82): the host-resolved u when the resolve table has it,
+// else counted as uncertified and recorded for the host.
+__device__ __noinline__ uint64_t ns_in_band(const Variates& v, int layer, uint32_t s, uint64_t i,
+                                            double u, uint64_t r, unsigned long long& uncert) {
+  const uint64_t k1 = (static_cast<uint64_t>(v.part) << 48) | (static_cast<uint64_t>(layer) << 32) | s;
+  double ex;
+  if (resolve_lookup(v.rs, k1, i, ex))
+    return __double2ull_rz(__dmul_rn(ex, static_cast<double>(i + 1)));
+  ++uncert;
+  if (v.rs && v.rs->perturb) {  // test hook: the other side of the integer
+    const double y = __dmul_rn(u, static_cast<double>(i + 1));
+    const uint64_t n = static_cast<uint64_t>(floor(y + 0.5));
+    r = (r == n) ? n - 1 : n;
+  }
+  resolve_record(v.rs, k1, i, u, static_cast<double>(r));
+  return r;
+}
+
 template <int IPT, bool SMOOTH>
 __global__ void __launch_bounds__(kNT) ns_reservoir_kernel(LaborArgs a) {
   pdl_begin();
@@ -1055,16 +1084,19 @@ __global__ void __launch_bounds__(kNT) ns_reservoir_kernel(LaborArgs a) {
         const uint64_t i = k + (x - rec.pre);
         const double scale = static_cast<double>(i + 1);
         double u;
+        uint64_t r;
         if (!smooth) {
           u = ufb(hstep(rec.b, i));
+          r = __double2ull_rz(__dmul_rn(u, scale));
         } else {
-          const uint64_t h2 = hstep(z2p, a.D[rec.di]);
+          const uint32_t s = a.D[rec.di];
+          const uint64_t h2 = hstep(z2p, s);
           u = smooth_finish(v, hstep(rec.b, i), hstep(h2, i));
           const double y = __dmul_rn(u, scale);
           const double fr = y - floor(y + 0.5);
-          if (fabs(fr) <= kGuard * y && y >= 0.5) ++uncert;
+          r = __double2ull_rz(y);
+          if (fabs(fr) <= v.guard * y && y >= 0.5) r = ns_in_band(v, a.layer, s, i, u, r, uncert);
         }
-        const uint64_t r = __double2ull_rz(__dmul_rn(u, scale));
         if (r < k) {
           const uint64_t pos = rec.a + r;
           if (pos < a.cap_edges) atomicMax(&a.slots[pos], static_cast<uint32_t>(i));
@@ -1459,7 +1491,6 @@ __device__ __forceinline__ void extract_body(const ExtractArgs& a, unsigned role
                                              unsigned ncta) {
   if (extract_uses_summary(a)) extract_summ(a, role, ncta);
   else extract_flat(a, role, ncta);
-  retire_ticket(a.ticket, a.exit_ctr, ncta);
 }
 
 __global__ void __launch_bounds__(kNT) extract_kernel(ExtractArgs a) {

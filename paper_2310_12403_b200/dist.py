@@ -258,14 +258,19 @@ class PeerCoop:
     owners' bitmaps, and input rows are pulled from the owners' shards
     requester-aligned. No counts cross ranks and the host never waits: the
     only cross-rank operation is a barrier between the three phases of a
-    layer -- an NCCL all-reduce of one element ordered on the plan stream (or,
-    over gloo, a stream sync plus a host barrier)."""
+    layer. `barrier="device"` (default) is cb_px_barrier, a one-warp kernel
+    on flags in the IPC region, so a whole step can be captured as one CUDA
+    graph per rank (`capture` / `step`); "nccl" is an NCCL all-reduce of one
+    element on the plan stream, "host" a stream sync plus a process-group
+    barrier."""
 
     HANDLE = 64
 
     def __init__(self, g: Graph, pm: PartitionMap, rank: int, num_layers: int,
                  cfg: SamplerConfig, max_seeds: int, store: FeatureStore | None = None,
-                 group=None):
+                 group=None, barrier: str = "device"):
+        if barrier not in ("device", "nccl", "host"):
+            raise ValueError("PeerCoop: barrier must be 'device', 'nccl' or 'host'")
         self.L = _lib.load()
         self.g, self.pm, self.rank, self.group = g, pm, rank, group
         self.world = dist.get_world_size(group)
@@ -297,6 +302,10 @@ class PeerCoop:
                 _check(self.L.cb_px_connect_features(h, q, hq, fh[q][1], store._h))
         self.stream = torch.cuda.ExternalStream(self.L.cb_plan_stream(h), device=self.device)
         self._nccl = dist.get_backend(group) == "nccl"
+        if barrier == "nccl" and not self._nccl:
+            raise ValueError("PeerCoop: barrier='nccl' needs an NCCL process group")
+        self._barrier = barrier
+        self._captured = False
         self._tok = torch.zeros(1, device=self.device if self._nccl else "cpu")
         dist.barrier(group=group)  # every mapping is open before anyone writes
 
@@ -309,7 +318,9 @@ class PeerCoop:
             pass
 
     def barrier(self):
-        if self._nccl:
+        if self._barrier == "device":
+            _check(self.L.cb_px_barrier(self._h))
+        elif self._barrier == "nccl":
             with torch.cuda.stream(self.stream):
                 dist.all_reduce(self._tok, group=self.group)
         else:
@@ -335,6 +346,32 @@ class PeerCoop:
             _check(self.L.cb_px_owner(self._h, l))
             self.barrier()
             _check(self.L.cb_px_locate(self._h, l))
+
+    def capture(self, n_seeds: int, schedule: SeedSchedule, rows: bool = True):
+        """Capture the whole step (L layers with their device barriers, plus
+        the row pull when `rows` and a store is set) as one CUDA graph per
+        rank (cb_px_capture). Needs barrier="device" and one eager step
+        (`sample`) on every rank first; every rank captures together."""
+        if self._barrier != "device":
+            raise ValueError("PeerCoop.capture needs barrier='device'")
+        store = self.store._h if (rows and self.store is not None) else None
+        _check(self.L.cb_px_capture(self._h, n_seeds, C.byref(schedule._c()), store))
+        self._captured = True
+
+    def step(self, seeds, schedule: SeedSchedule):
+        """One captured step (cb_px_replay): seeds (host u32 array of the
+        captured length, or a device tensor) and variates copied on the plan
+        stream, then one graph launch; nothing waits on the host."""
+        if not self._captured:
+            raise RuntimeError("PeerCoop.step: call capture() first")
+        if isinstance(seeds, torch.Tensor):
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
+            self._seeds = seeds
+            ptr, on_dev = seeds.data_ptr(), 1
+        else:
+            self._seeds = np.ascontiguousarray(seeds, dtype=np.uint32)
+            ptr, on_dev = self._seeds.ctypes.data, 0
+        _check(self.L.cb_px_replay(self._h, C.c_void_p(ptr), on_dev, C.byref(schedule._c())))
 
     def load_inputs(self):
         """all_to_all_forward: rows of the input vertices pulled from the

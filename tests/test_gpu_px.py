@@ -13,7 +13,7 @@ from tests.dist_harness import check_rank, spawn
 pytestmark = pytest.mark.gpu
 
 
-def _px_worker(rank, world, kind, fanouts, kappa, steps):
+def _px_worker(rank, world, kind, fanouts, kappa, steps, barrier="device", captured=False):
     import numpy as np
 
     import paper_2310_12403_b200 as cb
@@ -28,12 +28,17 @@ def _px_worker(rank, world, kind, fanouts, kappa, steps):
     L, dim, dtype, fseed = len(fanouts), 24, "f16", 5
     store = synth_shard(g, pm, rank, dim, fseed, dtype)
     pc = PeerCoop(g, pm, rank, L, cb.SamplerConfig(cb.SamplerKind(kind), fanouts=fanouts),
-                  max_seeds=4096, store=store)
+                  max_seeds=4096, store=store, barrier=barrier)
     sched = cb.SeedSchedule.make(kappa, 8)
     for step in range(steps):  # consecutive batches reuse the exchange slots
         seeds = O.draw_coop_seeds(owner, world, 128, 6, step)
-        pc.sample(seeds[rank], sched)
-        pc.load_inputs()
+        if captured and step > 0:
+            if step == 1:  # after one eager step on every rank
+                pc.capture(len(seeds[rank]), sched)
+            pc.step(seeds[rank], sched)  # one graph: L layers + barriers + rows
+        else:
+            pc.sample(seeds[rank], sched)
+            pc.load_inputs()
         res, rows = pc.result(), pc.rows()
         exp = O.coop_sample(ref, owner, world, seeds, L, kind, fanouts,
                             O.Sched(sched.kappa, sched.z1, sched.z2, sched.iteration))
@@ -42,13 +47,25 @@ def _px_worker(rank, world, kind, fanouts, kappa, steps):
     del np
 
 
-@pytest.mark.parametrize("world,kind,fanouts,kappa,steps", [
-    (2, 2, [10, 10, 10], 1, 3),
-    (3, 1, [10, 5, 5], 1, 2),
-    (2, 2, [25, 15], 4, 2),
+@pytest.mark.parametrize("world,kind,fanouts,kappa,steps,barrier", [
+    (2, 2, [10, 10, 10], 1, 3, "device"),
+    (3, 1, [10, 5, 5], 1, 2, "device"),
+    (2, 2, [25, 15], 4, 2, "host"),
 ])
-def test_peer_coop(gpu, world, kind, fanouts, kappa, steps):
-    spawn(world, _px_worker, (kind, fanouts, kappa, steps), timeout=600)
+def test_peer_coop(gpu, world, kind, fanouts, kappa, steps, barrier):
+    spawn(world, _px_worker, (kind, fanouts, kappa, steps, barrier), timeout=600)
+
+
+@pytest.mark.parametrize("world,kind,fanouts,kappa,steps", [
+    (2, 2, [10, 10, 10], 1, 5),   # odd L: the two slot-parity graphs alternate
+    (3, 2, [25, 15], 4, 4),       # even L, smoothed variates
+    (2, 1, [10, 5, 5], 1, 3),     # NS
+])
+def test_peer_coop_captured(gpu, world, kind, fanouts, kappa, steps):
+    """The whole cooperative step captured as one CUDA graph per rank (device
+    barriers on IPC flags, no host in the layer loop), replayed over
+    consecutive batches: bit-exact vs the oracle's coop_sample every step."""
+    spawn(world, _px_worker, (kind, fanouts, kappa, steps, "device", True), timeout=600)
 
 
 def _px_nccl_worker():
@@ -71,7 +88,8 @@ def _px_nccl_worker():
         ref = O.rmat(n, m, gseed)
         pm = cb.partition_random(g, 1, 2)
         store = synth_shard(g, pm, 0, 16, 3, "f32")
-        pc = PeerCoop(g, pm, 0, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), 512, store)
+        pc = PeerCoop(g, pm, 0, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), 512, store,
+                      barrier="nccl")
         seeds = O.draw_coop_seeds(pm.owner, 1, 256, 2, 0)
         sched = cb.SeedSchedule.plain(4)
         pc.sample(torch.from_numpy(seeds[0].view(np.int32)).cuda(), sched)  # device seeds
