@@ -381,13 +381,17 @@ int cb_px_finish(cb_plan* plan);
  * flag array and waits for every peer's (acquire). Every rank must issue the
  * same number of barriers. */
 int cb_px_barrier(cb_plan* plan);
-/* The whole cooperative step (coop_sample, coop.cpp:92-102: per layer
- * px_layer -> barrier -> owner -> barrier -> locate; then the row pull of
- * cb_px_gather when local != NULL) captured as one CUDA graph per rank (two
- * when L is odd: the exchange slots alternate across steps). Fixed seed count
- * n_seeds; the schedule fixes only whether variates are smoothed. Every rank
- * must have run one eager step before (kernel attributes) and must capture
- * the same step. */
+/* The whole cooperative step (coop_sample, coop.cpp:92-102; then the row pull
+ * of cb_px_gather when local != NULL) captured as CUDA graphs (2 or 4, replayed
+ * in turn): per layer l, sample + route into exchange slot c % 4 (c = the
+ * run's layer count), ONE device barrier, the owner extracts slot c % 4 and
+ * the requester locates layer l - 1; one more barrier and the last locate end
+ * the step -- L + 1 barriers instead of 2L. Barriers are a signal kernel plus
+ * stream memory waits (cuStreamWaitValue32; CB_PX_BARRIER=spin: the spin
+ * kernel of cb_px_barrier). Fixed seed count n_seeds; the schedule fixes only
+ * whether variates are smoothed. Every rank must have run one eager step
+ * before (kernel attributes), be quiescent (no step in flight on any rank),
+ * and capture the same step. Eager steps after a replay need a new plan. */
 int cb_px_capture(cb_plan* plan, uint64_t n_seeds, const cb_sched* sched,
                   const cb_features* local);
 /* One captured step: seeds (host or device) + the schedule's variates are

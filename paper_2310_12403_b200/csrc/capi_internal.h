@@ -170,8 +170,9 @@ struct PxState {
   const uint32_t* owner = nullptr;  // pm->owner (device)
   void* region = nullptr;           // local cudaMalloc, exported
   uint64_t region_bytes = 0;
-  Bitmap slot[2];                   // local views of the region
-  PxPeers peers[2];                 // per slot, every rank's pointers
+  static constexpr int kSlots = 4;  // eager steps use 0/1; captured steps all 4
+  Bitmap slot[kSlots];              // local views of the region
+  PxPeers peers[kSlots];            // per slot, every rank's pointers
   std::vector<void*> opened;        // IPC mappings to close
   unsigned long long* send = nullptr;  // [L * world] this rank's send_counts rows
   uint64_t layer_ctr = 0;           // slot of a layer = ctr & 1 (alternates across batches)
@@ -185,15 +186,22 @@ struct PxState {
   uint64_t flag_off = 0;
   uint32_t* bar_ctr = nullptr;  // [0] epoch counter, [1] timeout flag
   PxBarrier bar{};
-  // the captured step (one graph per slot parity when L is odd)
-  cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  // the captured step: graph i % n_exec for replay i (the exchange slots
+  // rotate mod 4 over the layers, the barrier value alternates 1/2)
+  cudaGraphExec_t exec[4] = {nullptr, nullptr, nullptr, nullptr};
+  int n_exec = 0;
+  uint64_t replays = 0;
+  bool eager_since_capture = false;
+  bool memop = false;  // captured barriers: signal kernel + cuStreamWaitValue32
   uint64_t cap_seeds = 0;
   bool cap_rows = false, cap_smooth = false;
   uint64_t cap_launches = 0;
   void drop_graphs() {
-    for (auto& e : exec)
+    for (auto& e : exec) {
       if (e) cudaGraphExecDestroy(e);
-    exec[0] = exec[1] = nullptr;
+      e = nullptr;
+    }
+    n_exec = 0;
   }
   ~PxState() {
     drop_graphs();

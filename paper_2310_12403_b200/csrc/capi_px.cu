@@ -1,6 +1,10 @@
 // C-ABI: multi-process peer exchange (cb_px_*), one part per rank over CUDA IPC.
 #include "capi_internal.h"
 
+#include <cuda.h>
+
+#include <numeric>
+
 extern "C" {
 
 // ------------------------------------------------ multi-process peer exchange --
@@ -63,16 +67,14 @@ void px_enqueue_layer(cb_plan* plan, int layer, uint64_t n_seeds, bool smooth, i
                   px.send + static_cast<uint64_t>(layer) * px.world, st);
 }
 
-// The owner's sorted unique set S^{l+1}_q + word ranks (coop.cpp:44-51). The
-// other slot was last read by the previous layer's locates, which every rank
-// finished before the barrier that precedes this.
-void px_enqueue_owner(cb_plan* plan, int layer) {
+// The owner's sorted unique set S^{l+1}_q + word ranks (coop.cpp:44-51) from
+// slot s, clearing slot `clr` (a slot every rank has finished reading).
+void px_enqueue_owner(cb_plan* plan, int layer, int s, int clr) {
   PxState& px = *plan->px;
   PeWork& w = plan->pe[0];
-  const int s = px.slot_of[layer];
   uint32_t* next = (layer + 1 < plan->L) ? w.L[layer + 1].dst : w.owner_final;
   const uint64_t cap = (layer + 1 < plan->L) ? w.L[layer + 1].cap_dst : w.cap_final;
-  launch_extract(extract_args(w, px.slot[s], &px.slot[s ^ 1], next, cap,
+  launch_extract(extract_args(w, px.slot[s], &px.slot[clr], next, cap,
                               &plan->meta_at(0, layer + 1)->n_dst, nullptr,
                               3 * plan->L + layer, 8 * layer + 5),
                  plan->stream);
@@ -88,20 +90,73 @@ void px_enqueue_locate(cb_plan* plan, int layer) {
                    plan->stream);
 }
 
-// The whole cooperative step with device barriers (coop.cpp:92-102 per layer,
-// then all_to_all_forward when f is given), slots starting at parity s0.
-void px_enqueue_step(cb_plan* plan, uint64_t n_seeds, bool smooth, int s0, const cb_features* f) {
+// cuStreamWaitValue32 through the runtime's driver entry point (no -lcuda).
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn wait_value_fn() {
+  static WaitValueFn fn = [] {
+    const char* e = std::getenv("CB_PX_BARRIER");
+    if (e && std::string(e) == "spin") return static_cast<WaitValueFn>(nullptr);
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<WaitValueFn>(nullptr);
+    return reinterpret_cast<WaitValueFn>(p);
+  }();
+  return fn;
+}
+
+// Barrier j of a captured step in graph g: this rank's arrival is stored as
+// g + 1 into row 1 + j of every peer's flag block, and the stream waits (a
+// front-end semaphore wait, no SM spinning) until every peer's entry in the
+// local row equals g + 1. Consecutive replays alternate g, and a rank can be
+// at most one barrier ahead of any peer, so a row is never overwritten while
+// a peer still waits on it.
+void px_enqueue_barrier(cb_plan* plan, int j, int g) {
   PxState& px = *plan->px;
-  for (int l = 0; l < plan->L; ++l) {
-    px_enqueue_layer(plan, l, n_seeds, smooth, (s0 + l) & 1);
+  if (!px.memop) {
     launch_px_barrier(px.bar, plan->stream);
-    px_enqueue_owner(plan, l);
-    launch_px_barrier(px.bar, plan->stream);
-    px_enqueue_locate(plan, l);
+    return;
   }
+  const uint32_t row = 1 + j, val = 1 + g;
+  launch_px_signal(px.bar, row, val, plan->stream);
+  for (uint32_t q = 0; q < px.world; ++q) {
+    if (q == px.rank) continue;
+    const CUdeviceptr a =
+        reinterpret_cast<CUdeviceptr>(px.bar.flags[px.rank] + row * kMaxParts + q);
+    if (wait_value_fn()(reinterpret_cast<CUstream>(plan->stream), a, val,
+                        CU_STREAM_WAIT_VALUE_EQ) != CUDA_SUCCESS)
+      throw Error(kCuda, "cuStreamWaitValue32 failed");
+  }
+}
+
+// The whole cooperative step as captured (coop.cpp:92-102 per layer, then
+// all_to_all_forward when f is given), with ONE barrier per layer plus one at
+// the end. Layer c of the run (c0 + l) routes into slot c % 4; after barrier
+// l the owner extracts slot c % 4 and clears slot (c + 2) % 4, and the
+// requester locates layer l - 1 in slot (c - 1) % 4:
+//  * slot c % 4 is complete at barrier l (every rank's route l precedes it);
+//  * slot (c - 1) % 4 was extracted by every owner before barrier l, and is
+//    cleared only by owner c + 1, after barrier l + 1;
+//  * slot (c + 2) % 4 = (c - 2) % 4 was last read by locate l - 2, before
+//    barrier l, and is next written by route c + 2, after barrier l + 1.
+// Graph g signals barrier value g % 2 + 1 (px_enqueue_barrier).
+void px_enqueue_step(cb_plan* plan, uint64_t n_seeds, bool smooth, uint64_t c0,
+                     const cb_features* f, int g) {
+  PxState& px = *plan->px;
+  const int L = plan->L;
+  for (int l = 0; l < L; ++l) {
+    const uint64_t c = c0 + l;
+    px_enqueue_layer(plan, l, n_seeds, smooth, static_cast<int>(c % 4));
+    px_enqueue_barrier(plan, l, g & 1);
+    px_enqueue_owner(plan, l, static_cast<int>(c % 4), static_cast<int>((c + 2) % 4));
+    if (l > 0) px_enqueue_locate(plan, l - 1);
+  }
+  px_enqueue_barrier(plan, L, g & 1);
+  px_enqueue_locate(plan, L - 1);
   if (f) {
     PeWork& w = plan->pe[0];
-    const int L = plan->L;
     launch_px_gather(px.d_fbase, px.owner, f->row_map, f->row_bytes, w.L[L - 1].src,
                      &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, plan->stream);
   }
@@ -126,11 +181,11 @@ int cb_px_setup(cb_plan* plan, const cb_partition* pm, uint32_t rank, void* hand
     const uint64_t wp = ceil_div(std::max<uint64_t>(words, 1), kExtractTileWords) * kExtractTileWords;
     const bool summ = wp > kExtractBigWords;
     const uint64_t per = (2 * wp + (summ ? wp / 32 : 0)) * 4;
-    px->flag_off = 2 * per;
-    px->region_bytes = 2 * per + kMaxParts * 4;
+    px->flag_off = PxState::kSlots * per;
+    px->region_bytes = px->flag_off + kBarRows * kMaxParts * 4;
     CB_CUDA(cudaMalloc(&px->region, px->region_bytes));
     CB_CUDA(cudaMemset(px->region, 0, px->region_bytes));
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < PxState::kSlots; ++s) {
       uint32_t* base = reinterpret_cast<uint32_t*>(static_cast<char*>(px->region) + s * per);
       Bitmap& b = px->slot[s];
       b.words = words;
@@ -175,9 +230,9 @@ int cb_px_connect(cb_plan* plan, uint32_t q, const void* handle) {
     void* p = nullptr;
     CB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     px.opened.push_back(p);
-    const uint64_t per = px.flag_off / 2;
+    const uint64_t per = px.flag_off / PxState::kSlots;
     px.bar.flags[q] = reinterpret_cast<uint32_t*>(static_cast<char*>(p) + px.flag_off);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < PxState::kSlots; ++s) {
       uint32_t* base = reinterpret_cast<uint32_t*>(static_cast<char*>(p) + s * per);
       const uint64_t wp = px.slot[s].words_padded;
       px.peers[s].bits[q] = base;
@@ -206,8 +261,11 @@ int cb_px_layer(cb_plan* plan, int layer, const uint32_t* seeds, uint64_t n_seed
       plan->seeds_off.assign({0, n_seeds});
       plan->mode = CB_MODE_COOP;
     }
+    require(px.replays == 0,
+            "captured peer-exchange steps ran on this plan (eager steps need a new plan)");
     const bool smooth = smooth_of(plan, sched);
     const int s = static_cast<int>(px.layer_ctr++ & 1);
+    px.eager_since_capture = true;
     count_epoch_bumps(plan, st, 1);
     px_enqueue_layer(plan, layer, layer == 0 ? n_seeds : 0, smooth, s);
     plan->have_batch = true;
@@ -221,9 +279,12 @@ int cb_px_owner(cb_plan* plan, int layer) {
   return guard([&] {
     require(plan != nullptr, "null plan");
     require(layer >= 0 && layer < plan->L, "layer index out of range");
-    px_of(plan);
+    PxState& px = px_of(plan);
     DeviceGuard dg(plan->device);
-    px_enqueue_owner(plan, layer);
+    // eager steps alternate slots 0/1: the other one was last read by the
+    // previous layer's locates, finished before the caller's barrier
+    const int s = px.slot_of[layer];
+    px_enqueue_owner(plan, layer, s, s ^ 1);
   });
 }
 
@@ -273,17 +334,33 @@ int cb_px_capture(cb_plan* plan, uint64_t n_seeds, const cb_sched* sched,
     const bool smooth = smooth_of(plan, sched);
     // kernel attributes are set by the eager layer calls every rank has made
     // before capturing (the caller's warm-up step); capture is local only
-    const int parities = (plan->L & 1) ? 2 : 1;
+    require(plan->L + 2 <= kBarRows, "peer exchange capture: too many layers");
+    px.memop = wait_value_fn() != nullptr;
+    px_preload();
+    // captured steps rotate all four slots: start from clean ones (the caller
+    // keeps every rank quiet around the capture, dist.PeerCoop.capture)
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    CB_CUDA(cudaMemset(px.region, 0, px.flag_off));
+    CB_CUDA(cudaDeviceSynchronize());
+    const int period = 4 / std::gcd(plan->L, 4);  // steps until the slots realign
+    px.n_exec = std::max(period, 2);               // and the barrier value alternates
     const unsigned long long k0 = g_kernel_launches.load();
-    for (int par = 0; par < parities; ++par) {
+    for (int g = 0; g < px.n_exec; ++g) {
       cudaGraph_t graph;
       CB_CUDA(cudaStreamBeginCapture(plan->stream, cudaStreamCaptureModeThreadLocal));
-      px_enqueue_step(plan, n_seeds, smooth, par, local);
+      try {
+        px_enqueue_step(plan, n_seeds, smooth, static_cast<uint64_t>(g) * plan->L, local, g);
+      } catch (...) {
+        cudaStreamEndCapture(plan->stream, &graph);
+        throw;
+      }
       CB_CUDA(cudaStreamEndCapture(plan->stream, &graph));
-      CB_CUDA(cudaGraphInstantiate(&px.exec[par], graph, 0));
+      CB_CUDA(cudaGraphInstantiate(&px.exec[g], graph, 0));
       CB_CUDA(cudaGraphDestroy(graph));
     }
-    px.cap_launches = (g_kernel_launches.load() - k0) / parities;
+    px.cap_launches = (g_kernel_launches.load() - k0) / px.n_exec;
+    px.replays = 0;
+    px.eager_since_capture = false;
     px.cap_seeds = n_seeds;
     px.cap_rows = local != nullptr;
     px.cap_smooth = smooth;
@@ -309,11 +386,13 @@ int cb_px_replay(cb_plan* plan, const uint32_t* seeds, int seeds_on_device,
                                               : cudaMemcpyHostToDevice,
                               st));
     upload_variates(plan, sched, 1, st);
+    require(!px.eager_since_capture, "eager peer-exchange steps ran since the capture (re-capture)");
+    const int g = static_cast<int>(px.replays % px.n_exec);
     count_epoch_bumps(plan, st, plan->L);
-    const int par = (plan->L & 1) ? static_cast<int>(px.layer_ctr & 1) : 0;
-    CB_CUDA(cudaGraphLaunch(px.exec[par], st));
-    px.layer_ctr += plan->L;
-    for (int l = 0; l < plan->L; ++l) px.slot_of[l] = (par + l) & 1;
+    CB_CUDA(cudaGraphLaunch(px.exec[g], st));
+    for (int l = 0; l < plan->L; ++l)
+      px.slot_of[l] = static_cast<int>((static_cast<uint64_t>(g) * plan->L + l) % 4);
+    ++px.replays;
     plan->seeds_off.assign({0, px.cap_seeds});
     plan->mode = CB_MODE_COOP;
     plan->have_batch = true;

@@ -138,6 +138,17 @@ __global__ void px_barrier_kernel(PxBarrier b) {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
+__global__ void px_signal_kernel(PxBarrier b, uint32_t row, uint32_t value) {
+  pdl_begin();
+  const uint32_t q = threadIdx.x;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  if (q < b.world && q != b.rank)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(b.flags[q] + row * kMaxParts +
+                                                           b.rank),
+                 "r"(value)
+                 : "memory");
+}
+
 template <typename V>
 __global__ void px_gather_kernel(const unsigned char* const* __restrict__ bases,
                                  const uint32_t* __restrict__ owner,
@@ -196,6 +207,17 @@ void launch_px_locate(const uint32_t* src, const unsigned long long* count, uint
 void launch_px_barrier(const PxBarrier& b, cudaStream_t st) {
   launch_k(px_barrier_kernel, 1, 32, st, b);
   CB_LAUNCH("px_barrier");
+}
+
+void launch_px_signal(const PxBarrier& b, uint32_t row, uint32_t value, cudaStream_t st) {
+  launch_k(px_signal_kernel, 1, 32, st, b, row, value);
+  CB_LAUNCH("px_signal");
+}
+
+void px_preload() {
+  cudaFuncAttributes fa;
+  cuda_check(cudaFuncGetAttributes(&fa, px_signal_kernel), "cudaFuncGetAttributes");
+  cuda_check(cudaFuncGetAttributes(&fa, px_barrier_kernel), "cudaFuncGetAttributes");
 }
 
 void launch_px_gather(const unsigned char* const* d_bases, const uint32_t* owner,

@@ -33,14 +33,20 @@ struct PxPeers {
 // (IPC-mapped; entry r of rank q's array is written by rank r). The epoch is a
 // device counter, so a captured graph replays it; ranks run the same number
 // of barriers. A wait longer than timeout_ns sets *err and gives up (no hang).
+constexpr int kBarRows = 64;  // flag rows per rank: row 0 epoch barrier, 1.. captured
 struct PxBarrier {
-  uint32_t* flags[kMaxParts];
+  uint32_t* flags[kMaxParts];  // rank q's flag block [kBarRows][kMaxParts]
   uint32_t* ctr;
   uint32_t* err;
   uint32_t rank, world;
   unsigned long long timeout_ns;
 };
 void launch_px_barrier(const PxBarrier& b, cudaStream_t st);
+// Arrival only: store `value` into row `row`, entry rank, of every peer's
+// flag block (release, system scope). The waits are stream memory ops.
+void launch_px_signal(const PxBarrier& b, uint32_t row, uint32_t value, cudaStream_t st);
+// Loads the barrier kernels' module outside any stream capture (lazy loading).
+void px_preload();
 
 // Requester side of build_exchange (coop.cpp:35-51): OR every src id into its
 // owner's exchange bitmap over peer memory; send_row[q] += ids sent to q.

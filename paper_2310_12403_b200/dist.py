@@ -355,7 +355,10 @@ class PeerCoop:
         if self._barrier != "device":
             raise ValueError("PeerCoop.capture needs barrier='device'")
         store = self.store._h if (rows and self.store is not None) else None
+        _check(self.L.cb_px_finish(self._h))
+        dist.barrier(group=self.group)  # no peer writes into our slots while they are reset
         _check(self.L.cb_px_capture(self._h, n_seeds, C.byref(schedule._c()), store))
+        dist.barrier(group=self.group)
         self._captured = True
 
     def step(self, seeds, schedule: SeedSchedule):
