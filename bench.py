@@ -1083,6 +1083,8 @@ def main():
                     help="N>1: cooperative minibatching (one part per GPU) or independent")
     ap.add_argument("--exchange", choices=["px", "a2a"], default="px",
                     help="N>1 coop: peer-memory exchange (cb_px_*) or all-to-allv (DistCoop)")
+    ap.add_argument("--coop-n1", action="store_true",
+                    help="run the cooperative (peer-exchange) step even at N=1 (diagnostics)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: ranks share cuda:0 with CPU-staged exchanges (testing)")
     args = ap.parse_args()
@@ -1095,7 +1097,7 @@ def main():
         return
     if args.impl == "reference":
         run_reference(args, cfg)
-    elif world > 1 and args.mode == "coop":
+    elif (world > 1 or args.coop_n1) and args.mode == "coop":
         run_ours_coop(args, cfg)
         return
     else:

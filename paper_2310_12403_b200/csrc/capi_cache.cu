@@ -200,8 +200,10 @@ int cb_features_set_tier(cb_features* f, int host) {
   return guard([&] {
     require(f != nullptr, "null features");
     DeviceGuard dg(f->device);
-    require(f->shard_rows == 0, "host tier of a single-part shard table is not supported");
-    const uint64_t rows = f->n_rows;
+    // a single-part shard holds shard_rows rows behind a virtual base
+    // (table + shard_r0 rows is the allocation); the tier moves those rows
+    const uint64_t rows = f->shard_rows ? f->shard_rows : f->n_rows;
+    const uint64_t off = f->shard_rows ? f->shard_r0 * f->row_bytes : 0;
     const uint64_t bytes = rows * f->row_bytes;
     const bool on_host = f->host_base != nullptr;
     if (static_cast<bool>(host) == on_host) return;
@@ -209,14 +211,16 @@ int cb_features_set_tier(cb_features* f, int host) {
     if (host) {
       void* h = nullptr;
       CB_CUDA(cudaHostAlloc(&h, bytes + 64, cudaHostAllocMapped | cudaHostAllocPortable));
-      CB_CUDA(cudaMemcpy(h, f->table, bytes, cudaMemcpyDeviceToHost));
+      CB_CUDA(cudaMemcpy(h, static_cast<unsigned char*>(f->table) + off, bytes,
+                         cudaMemcpyDeviceToHost));
       void* d = nullptr;
       CB_CUDA(cudaHostGetDevicePointer(&d, h, 0));
       f->hbm_table = f->table;
       f->host_base = h;
-      f->table = d;
+      f->table = static_cast<unsigned char*>(d) - off;
     } else {
-      CB_CUDA(cudaMemcpy(f->hbm_table, f->host_base, bytes, cudaMemcpyHostToDevice));
+      CB_CUDA(cudaMemcpy(static_cast<unsigned char*>(f->hbm_table) + off, f->host_base, bytes,
+                         cudaMemcpyHostToDevice));
       CB_CUDA(cudaFreeHost(f->host_base));
       f->host_base = nullptr;
       f->table = f->hbm_table;

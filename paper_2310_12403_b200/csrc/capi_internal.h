@@ -182,6 +182,15 @@ struct PxState {
   std::vector<const unsigned char*> fbase;
   std::vector<void*> fopened;
   uint64_t frow_bytes = 0;
+  // owner-side cached fetch (cb_px_setup_cache): the owner's rows of its set
+  // S^L_q staged in an exported buffer, pulled by the requesters
+  cb_cache* cache = nullptr;
+  const cb_features* cache_store = nullptr;
+  void* rstage = nullptr;
+  uint64_t rstage_rows = 0;
+  const unsigned char** d_rstage = nullptr;  // [kMaxParts] every rank's staging
+  std::vector<const unsigned char*> rstage_of;
+  std::vector<void*> ropened;
   // device barrier: flag array at region + flag_off on every rank
   uint64_t flag_off = 0;
   uint32_t* bar_ctr = nullptr;  // [0] epoch counter, [1] timeout flag
@@ -205,6 +214,9 @@ struct PxState {
   }
   ~PxState() {
     drop_graphs();
+    for (void* p : ropened) cudaIpcCloseMemHandle(p);
+    if (rstage) cudaFree(rstage);
+    if (d_rstage) cudaFree(d_rstage);
     if (bar_ctr) cudaFree(bar_ctr);
     for (void* p : opened) cudaIpcCloseMemHandle(p);
     for (void* p : fopened) cudaIpcCloseMemHandle(p);

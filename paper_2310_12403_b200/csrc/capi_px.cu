@@ -495,4 +495,96 @@ int cb_px_gather(cb_plan* plan, const cb_features* local) {
   });
 }
 
+// ---- owner-side cached fetch ------------------------------------------------
+// The per-GPU cache of north_star item 5 at the OWNER: after a step, owner q
+// runs its LRU over its set S^L_q (every requested row it owns, sorted) in
+// access_order(S^L_q, order_key) -- feature_load_sim's per-part loop
+// (cache.cpp:100-110) with S^L_q as part q's accesses -- and stages those rows
+// in an exported buffer: hits from the cache's HBM rows, misses from its
+// shard table (HBM or the pinned host tier, the storage channel). After a
+// barrier the requesters pull row loc_row[j] of rank loc_part[j]'s staging
+// buffer (all_to_all_forward, coop.cpp:145-159): each owned row crosses the
+// storage channel at most once per step however many ranks requested it.
+int cb_px_setup_cache(cb_plan* plan, cb_cache* cache, const cb_features* local,
+                      void* handle_out) {
+  return guard([&] {
+    require(plan != nullptr && cache != nullptr && local != nullptr && handle_out != nullptr,
+            "null argument");
+    PxState& px = px_of(plan);
+    require(local->shard_rows > 0, "the cached fetch needs this rank's shard table");
+    require(cache->lru->row_bytes() == local->row_bytes,
+            "cache row size does not match the feature table");
+    require(cache->lru->n_keys() >= plan->g->g.n, "cache key space smaller than the graph");
+    DeviceGuard dg(plan->device);
+    PeWork& w = plan->pe[0];
+    px.cache = cache;
+    px.cache_store = local;
+    if (px.rstage) CB_CUDA(cudaFree(px.rstage));
+    px.rstage_rows = std::max<uint64_t>(w.cap_final, 1);
+    CB_CUDA(cudaMalloc(&px.rstage, px.rstage_rows * local->row_bytes));
+    if (!px.d_rstage) CB_CUDA(cudaMalloc(&px.d_rstage, kMaxParts * sizeof(void*)));
+    px.rstage_of.assign(kMaxParts, nullptr);
+    px.rstage_of[px.rank] = static_cast<const unsigned char*>(px.rstage);
+    cudaIpcMemHandle_t h;
+    CB_CUDA(cudaIpcGetMemHandle(&h, px.rstage));
+    std::memcpy(handle_out, &h, sizeof(h));
+  });
+}
+
+int cb_px_connect_cache(cb_plan* plan, uint32_t q, const void* handle) {
+  return guard([&] {
+    require(plan != nullptr && handle != nullptr, "null argument");
+    PxState& px = px_of(plan);
+    require(px.rstage != nullptr, "call cb_px_setup_cache first");
+    require(q < px.world && q != px.rank, "peer rank out of range (or self)");
+    DeviceGuard dg(plan->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    CB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    px.ropened.push_back(p);
+    px.rstage_of[q] = static_cast<const unsigned char*>(p);
+    CB_CUDA(cudaMemcpy(px.d_rstage, px.rstage_of.data(), kMaxParts * sizeof(void*),
+                       cudaMemcpyHostToDevice));
+  });
+}
+
+int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint64_t* hits,
+                        uint64_t* misses) {
+  NvtxRange nvtx_("cb.px_gather_cached");
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require(plan->have_batch, "no sampled batch in this plan");
+    PxState& px = px_of(plan);
+    require(px.cache != nullptr, "no cache set up (cb_px_setup_cache)");
+    for (uint32_t q = 0; q < px.world; ++q)
+      require(px.rstage_of[q] != nullptr, "staging buffer of a rank not connected");
+    DeviceGuard dg(plan->device);
+    check_overflow(plan);
+    const int L = plan->L;
+    PeWork& w = plan->pe[0];
+    prepare_rows(plan, px.cache_store, false);
+    const uint64_t n_own = host_meta(plan, 0, L).n_dst;
+    require(n_own <= px.rstage_rows, "owner set larger than the staging buffer");
+    DeviceLru& lru = *px.cache->lru;
+    const uint64_t h0 = lru.hits(), m0 = lru.misses();
+    CacheGatherSrc src;
+    src.table = px.cache_store->table;
+    src.row_map = px.cache_store->row_map;
+    src.rows_out = px.rstage;
+    lru.access_ids(w.owner_final, n_own, order_key, nullptr, 0, src, plan->stream);
+    // every owner's rows are staged before any requester reads them; the
+    // next step's staging comes after that step's barriers, which no rank
+    // reaches before finishing this pull
+    launch_px_barrier(px.bar, plan->stream);
+    launch_px_gather_staged(px.d_rstage, w.loc_part[L - 1], w.loc_row[L - 1],
+                            px.cache_store->row_bytes, &plan->meta_at(0, L - 1)->n_src,
+                            w.cap_rows, w.rows, plan->stream);
+    plan->have_rows = true;
+    if (owned) *owned = n_own;
+    if (hits) *hits = lru.hits() - h0;
+    if (misses) *misses = lru.misses() - m0;
+  });
+}
+
 }  // extern "C"

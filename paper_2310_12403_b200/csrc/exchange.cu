@@ -79,9 +79,11 @@ __global__ void px_route_kernel(const uint32_t* __restrict__ src,
     if (peers.summ[q]) atomicOr(&peers.summ[q][v >> 10], 1u << ((v >> 5) & 31u));
     atomicAdd(&hist[q], 1ULL);
   }
-  // the owner reads these bits after a cross-rank barrier
-  __threadfence_system();
+  // the owner reads these bits after a cross-rank barrier: one system-scope
+  // fence per CTA, cumulative over the CTA's REDs ordered before it by the
+  // barrier (a fence per thread cost ~20 us per launch at c4)
   __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
   for (uint32_t q = threadIdx.x; q < kMaxParts; q += blockDim.x)
     if (hist[q]) atomicAdd(&send_row[q], hist[q]);
 }
@@ -136,6 +138,42 @@ __global__ void px_barrier_kernel(PxBarrier b) {
   }
   __syncwarp();
   asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+template <typename V>
+__global__ void px_gather_staged_kernel(const unsigned char* const* __restrict__ bases,
+                                        const uint32_t* __restrict__ loc_part,
+                                        const uint32_t* __restrict__ loc_row, uint32_t vpr,
+                                        uint64_t row_bytes,
+                                        const unsigned long long* __restrict__ count,
+                                        uint64_t cap, V* __restrict__ out) {
+  pdl_begin();
+  const uint64_t n = min(static_cast<uint64_t>(*count), cap);
+  const uint64_t total = n * vpr;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  constexpr int U = 4;
+  for (uint64_t x0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x0 < total;
+       x0 += stride * U) {
+    V buf[U];
+    const V* srcp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t x = x0 + u * stride;
+      srcp[u] = nullptr;
+      if (x < total) {
+        const uint64_t r = x / vpr, c = x - r * vpr;
+        srcp[u] = reinterpret_cast<const V*>(bases[__ldg(loc_part + r)] +
+                                             static_cast<uint64_t>(__ldg(loc_row + r)) *
+                                                 row_bytes) + c;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (srcp[u]) buf[u] = *srcp[u];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (srcp[u]) __stcs(out + x0 + u * stride, buf[u]);
+  }
 }
 
 __global__ void px_signal_kernel(PxBarrier b, uint32_t row, uint32_t value) {
@@ -246,6 +284,34 @@ void launch_px_gather(const unsigned char* const* d_bases, const uint32_t* owner
                row_bytes, ids, count, cap, static_cast<unsigned short*>(out));
   }
   CB_LAUNCH("px_gather");
+}
+
+void launch_px_gather_staged(const unsigned char* const* d_bases, const uint32_t* loc_part,
+                             const uint32_t* loc_row, uint64_t row_bytes,
+                             const unsigned long long* count, uint64_t cap, void* out,
+                             cudaStream_t st) {
+  int vb = 16;
+  while (row_bytes % vb) vb >>= 1;
+  const uint32_t vpr = static_cast<uint32_t>(row_bytes / vb);
+  const unsigned grid = kNumSMs * 8;
+  switch (vb) {
+    case 16:
+      launch_k(px_gather_staged_kernel<uint4>, grid, 256, st, d_bases, loc_part, loc_row, vpr,
+               row_bytes, count, cap, static_cast<uint4*>(out));
+      break;
+    case 8:
+      launch_k(px_gather_staged_kernel<uint2>, grid, 256, st, d_bases, loc_part, loc_row, vpr,
+               row_bytes, count, cap, static_cast<uint2*>(out));
+      break;
+    case 4:
+      launch_k(px_gather_staged_kernel<uint32_t>, grid, 256, st, d_bases, loc_part, loc_row,
+               vpr, row_bytes, count, cap, static_cast<uint32_t*>(out));
+      break;
+    default:
+      launch_k(px_gather_staged_kernel<unsigned short>, grid, 256, st, d_bases, loc_part,
+               loc_row, vpr, row_bytes, count, cap, static_cast<unsigned short*>(out));
+  }
+  CB_LAUNCH("px_gather_staged");
 }
 
 void launch_route(const PartPtrs& pp, const uint32_t* owner, uint32_t P,

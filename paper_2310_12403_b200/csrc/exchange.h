@@ -66,6 +66,13 @@ void launch_px_gather(const unsigned char* const* d_bases, const uint32_t* owner
                       const unsigned long long* count, uint64_t cap, void* out,
                       cudaStream_t st);
 
+// all_to_all_forward from the owners' staged rows: out[j] = row loc_row[j] of
+// rank loc_part[j]'s staging buffer (bases[q], IPC-mapped).
+void launch_px_gather_staged(const unsigned char* const* d_bases, const uint32_t* loc_part,
+                             const uint32_t* loc_row, uint64_t row_bytes,
+                             const unsigned long long* count, uint64_t cap, void* out,
+                             cudaStream_t st);
+
 void launch_route(const PartPtrs& pp, const uint32_t* owner, uint32_t P,
                   unsigned long long* send_counts, uint64_t max_src, cudaStream_t st);
 void launch_locate(const PartPtrs& pp, const uint32_t* owner, uint32_t P, uint64_t max_src,

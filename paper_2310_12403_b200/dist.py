@@ -376,6 +376,35 @@ class PeerCoop:
             ptr, on_dev = self._seeds.ctypes.data, 0
         _check(self.L.cb_px_replay(self._h, C.c_void_p(ptr), on_dev, C.byref(schedule._c())))
 
+    def enable_cache(self, capacity: int):
+        """Owner-side LRU cache of `capacity` rows (HBM) in front of this rank's
+        shard (cb_px_setup_cache): see load_inputs_cached."""
+        from .cache import LruCache
+        if self.store is None:
+            raise ValueError("PeerCoop.enable_cache needs the rank's feature shard")
+        self.cache = LruCache(capacity, self.g.num_vertices, self.g.device,
+                              row_bytes=self.store.row_bytes)
+        buf = (C.c_ubyte * self.HANDLE)()
+        _check(self.L.cb_px_setup_cache(self._h, self.cache._h, self.store._h, buf))
+        hs = [None] * self.world
+        dist.all_gather_object(hs, bytes(buf), group=self.group)
+        for q in range(self.world):
+            if q != self.rank:
+                hq = (C.c_ubyte * self.HANDLE).from_buffer_copy(hs[q])
+                _check(self.L.cb_px_connect_cache(self._h, q, hq))
+        dist.barrier(group=self.group)
+
+    def load_inputs_cached(self, order_key: int) -> tuple[int, int, int]:
+        """The owner-side cached fetch of this step (cb_px_gather_cached): this
+        owner's set S^L_q goes through its LRU in access_order(S^L_q, order_key)
+        (misses from the shard, HBM or host tier), then every rank pulls its
+        rows from the owners' staged rows. Returns (owned rows, hits, misses)
+        of this owner."""
+        o, h, m = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(self.L.cb_px_gather_cached(self._h, order_key, C.byref(o), C.byref(h),
+                                          C.byref(m)))
+        return o.value, h.value, m.value
+
     def load_inputs(self):
         """all_to_all_forward: rows of the input vertices pulled from the
         owners' shards into the plan's row buffer (shards are static, so no

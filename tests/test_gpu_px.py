@@ -120,3 +120,61 @@ def test_peer_coop_nccl_single_rank(gpu):
     p.start()
     p.join(300)
     assert p.exitcode == 0
+
+
+def _px_cache_worker(rank, world, kappa, steps, captured, host_tier):
+    import paper_2310_12403_b200 as cb
+    from oracle import oracle as O
+    from paper_2310_12403_b200.dist import PeerCoop, synth_shard
+    from tests.dist_harness import check_rank
+
+    n, m, gseed = 1 << 14, 1 << 17, 21
+    g = cb.Graph.generate_rmat(n, m, gseed)
+    ref = O.rmat(n, m, gseed)
+    pm = cb.partition_random(g, world, 6)
+    owner = pm.owner
+    L, dim, dtype, fseed, cap = 2, 24, "f16", 5, 600
+    store = synth_shard(g, pm, rank, dim, fseed, dtype)
+    if host_tier:
+        store.set_tier(True)  # misses cross the host link (the storage channel)
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, fanouts=[10, 10])
+    pc = PeerCoop(g, pm, rank, L, cfg, max_seeds=4096, store=store)
+    pc.enable_cache(cap)
+    lru = O.Lru(cap, impl="reference")  # the reference's LruCache, this owner's
+    sched = cb.SeedSchedule.make(kappa, 8)
+    # dependent minibatches: the same seeds every step, drifting variates
+    seeds = O.draw_coop_seeds(owner, world, 96, 6, 0)
+    total_h = 0
+    for step in range(steps):
+        if captured and step > 0:
+            if step == 1:
+                pc.capture(len(seeds[rank]), sched, rows=False)
+            pc.step(seeds[rank], sched)
+        else:
+            pc.sample(seeds[rank], sched)
+        key = cb.hash_bits(step + 1, [rank])  # feature_load_sim's key (cache.cpp:102)
+        owned, hits, misses = pc.load_inputs_cached(key)
+        res, rows = pc.result(), pc.rows()
+        exp = O.coop_sample(ref, owner, world, seeds, L, O.LABOR0, 10,
+                            O.Sched(sched.kappa, sched.z1, sched.z2, sched.iteration))
+        check_rank(res, rows, exp, rank, world, L, fseed, dim, dtype)
+        own = exp["owner_sets"][rank]
+        want_m = sum(lru.access(int(v)) for v in O.access_order(own, key))
+        assert owned == len(own) and misses == want_m and hits == len(own) - want_m, \
+            (step, owned, hits, misses, len(own), want_m)
+        total_h += hits
+        sched = cb.schedule_advance(sched)
+    assert total_h > 0  # the dependent batches did reuse rows
+
+
+@pytest.mark.parametrize("world,kappa,steps,captured,host_tier", [
+    (2, 4, 5, False, False),
+    (3, 16, 4, True, True),
+])
+def test_peer_coop_owner_cache(gpu, world, kappa, steps, captured, host_tier):
+    """The owner-side cached fetch: per step each owner's set goes through its
+    LRU (hits/misses equal the reference LruCache fed access_order(S^L_q,
+    hash_bits(step, {q})), feature_load_sim's loop, cache.cpp:100-110) and
+    every rank's rows, pulled from the owners' staged rows, equal the
+    oracle's -- with the shard in HBM or in the pinned host tier."""
+    spawn(world, _px_cache_worker, (kappa, steps, captured, host_tier), timeout=600)
