@@ -408,19 +408,21 @@ int cb_px_connect_features(cb_plan* plan, uint32_t peer, const void* handle, uin
 /* Input rows of this rank's last layer into the plan's row buffer
  * (cb_download_rows / cb_rows_device), requester-aligned. */
 int cb_px_gather(cb_plan* plan, const cb_features* local);
-/* Owner-side cached fetch (the per-GPU cache of the dependent-minibatch reuse;
- * feature_load_sim, cache.cpp:88-119, with the owner set S^L_q as part q's
- * accesses): after a step, owner q accesses S^L_q in
- * access_order(S^L_q, order_key) through `cache` (LruCache semantics, its HBM
- * rows) and stages the rows -- misses read from `local`, this rank's shard
- * table, HBM or host tier (cb_features_set_tier) -- in a buffer exported
- * through CUDA IPC; after a device barrier each requester pulls its rows from
- * the owners' staging buffers, requester-aligned. Every rank calls
- * cb_px_gather_cached once per step. *owned / *hits / *misses: this owner's
- * accesses this step. Synchronises with the host (the owner-set size). */
-int cb_px_setup_cache(cb_plan* plan, cb_cache* cache, const cb_features* local,
-                      void* handle_out);
-int cb_px_connect_cache(cb_plan* plan, uint32_t peer, const void* handle);
+/* Owner staging (all_to_all_forward, coop.cpp:145-159, as the reference does
+ * it): with a staging buffer set up and connected on every rank, cb_px_gather
+ * and the captured step's row fetch become: owner q loads the rows of its set
+ * S^L_q from its shard into its staging buffer (exported through CUDA IPC), a
+ * device barrier, then each requester pulls row loc_row[j] of rank
+ * loc_part[j]'s buffer. cb_px_set_cache adds the per-GPU cache at the owner
+ * (feature_load_sim, cache.cpp:88-119, with S^L_q as part q's accesses):
+ * cb_px_gather_cached runs S^L_q through the LRU in access_order(S^L_q,
+ * order_key), hits from the cache's HBM rows, misses from the shard (HBM or
+ * the host tier, cb_features_set_tier); every rank calls it once per step;
+ * *owned / *hits / *misses are this owner's. It synchronises with the host
+ * (the owner-set size). */
+int cb_px_setup_staging(cb_plan* plan, const cb_features* local, void* handle_out);
+int cb_px_connect_staging(cb_plan* plan, uint32_t peer, const void* handle);
+int cb_px_set_cache(cb_plan* plan, cb_cache* cache);
 int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint64_t* hits,
                         uint64_t* misses);
 

@@ -182,10 +182,10 @@ struct PxState {
   std::vector<const unsigned char*> fbase;
   std::vector<void*> fopened;
   uint64_t frow_bytes = 0;
-  // owner-side cached fetch (cb_px_setup_cache): the owner's rows of its set
-  // S^L_q staged in an exported buffer, pulled by the requesters
+  // owner staging (cb_px_setup_staging): the owner's rows of its set S^L_q
+  // staged in an exported buffer, pulled by the requesters; optional cache
   cb_cache* cache = nullptr;
-  const cb_features* cache_store = nullptr;
+  const cb_features* stage_store = nullptr;
   void* rstage = nullptr;
   uint64_t rstage_rows = 0;
   const unsigned char** d_rstage = nullptr;  // [kMaxParts] every rank's staging

@@ -131,6 +131,8 @@ void px_enqueue_barrier(cb_plan* plan, int j, int g) {
   }
 }
 
+void px_enqueue_staged_gather(cb_plan* plan, int g);
+
 // The whole cooperative step as captured (coop.cpp:92-102 per layer, then
 // all_to_all_forward when f is given), with ONE barrier per layer plus one at
 // the end. Layer c of the run (c0 + l) routes into slot c % 4; after barrier
@@ -155,11 +157,35 @@ void px_enqueue_step(cb_plan* plan, uint64_t n_seeds, bool smooth, uint64_t c0,
   }
   px_enqueue_barrier(plan, L, g & 1);
   px_enqueue_locate(plan, L - 1);
-  if (f) {
+  if (f && px.rstage) {
+    px_enqueue_staged_gather(plan, g);
+  } else if (f) {
     PeWork& w = plan->pe[0];
     launch_px_gather(px.d_fbase, px.owner, f->row_map, f->row_bytes, w.L[L - 1].src,
                      &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, plan->stream);
   }
+}
+
+void require_staging(const PxState& px) {
+  require(px.rstage != nullptr, "no staging buffer (cb_px_setup_staging)");
+  for (uint32_t q = 0; q < px.world; ++q)
+    require(px.rstage_of[q] != nullptr, "staging buffer of a rank not connected");
+}
+
+// Owner q gathers the rows of S^L_q from its shard into its staging buffer
+// (device count), barrier, requesters pull from the owners' staging.
+void px_enqueue_staged_gather(cb_plan* plan, int g) {
+  PxState& px = *plan->px;
+  PeWork& w = plan->pe[0];
+  const int L = plan->L;
+  const cb_features* f = px.stage_store;
+  launch_gather(f->table, vec_bytes_for(f->row_bytes), f->row_bytes, w.owner_final,
+                &plan->meta_at(0, L)->n_dst, px.rstage_rows, f->row_map, px.rstage,
+                plan->stream);
+  if (g < 0) launch_px_barrier(px.bar, plan->stream);
+  else px_enqueue_barrier(plan, L + 1, g & 1);
+  launch_px_gather_staged(px.d_rstage, w.loc_part[L - 1], w.loc_row[L - 1], f->row_bytes,
+                          &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, plan->stream);
 }
 
 }  // namespace
@@ -334,7 +360,8 @@ int cb_px_capture(cb_plan* plan, uint64_t n_seeds, const cb_sched* sched,
     const bool smooth = smooth_of(plan, sched);
     // kernel attributes are set by the eager layer calls every rank has made
     // before capturing (the caller's warm-up step); capture is local only
-    require(plan->L + 2 <= kBarRows, "peer exchange capture: too many layers");
+    require(plan->L + 3 <= kBarRows, "peer exchange capture: too many layers");
+    if (local && px.rstage) require_staging(px);
     px.memop = wait_value_fn() != nullptr;
     px_preload();
     // captured steps rotate all four slots: start from clean ones (the caller
@@ -487,6 +514,12 @@ int cb_px_gather(cb_plan* plan, const cb_features* local) {
       require(px.fbase[q] != nullptr, "feature shard of a rank not connected");
     DeviceGuard dg(plan->device);
     prepare_rows(plan, local, false);  // rows come from the owners' shards
+    plan->have_rows = true;
+    if (px.rstage) {  // through the owners' staging buffers
+      require_staging(px);
+      px_enqueue_staged_gather(plan, -1);
+      return;
+    }
     PeWork& w = plan->pe[0];
     const int L = plan->L;
     launch_px_gather(px.d_fbase, px.owner, local->row_map, local->row_bytes, w.L[L - 1].src,
@@ -495,31 +528,33 @@ int cb_px_gather(cb_plan* plan, const cb_features* local) {
   });
 }
 
-// ---- owner-side cached fetch ------------------------------------------------
-// The per-GPU cache of north_star item 5 at the OWNER: after a step, owner q
-// runs its LRU over its set S^L_q (every requested row it owns, sorted) in
+// ---- owner staging: the feature fetch through the owners -------------------
+// all_to_all_forward (coop.cpp:145-159) the way the reference does it: owner
+// q loads the rows of its set S^L_q (every requested row it owns, sorted) from
+// its own shard into a staging buffer exported through CUDA IPC; after a
+// barrier each requester pulls row loc_row[j] of rank loc_part[j]'s staging
+// buffer. Reading a peer's whole shard in place instead costs a translation
+// miss per row once the shards are large (c4: 1.2 ms vs 24 us per step for two
+// ranks sharing one B200), and each owned row crosses the storage channel
+// once however many ranks requested it.
+//
+// With a cache (cb_px_set_cache; the per-GPU cache of the dependent-
+// minibatch reuse at the OWNER) S^L_q goes through the owner's LRU in
 // access_order(S^L_q, order_key) -- feature_load_sim's per-part loop
-// (cache.cpp:100-110) with S^L_q as part q's accesses -- and stages those rows
-// in an exported buffer: hits from the cache's HBM rows, misses from its
-// shard table (HBM or the pinned host tier, the storage channel). After a
-// barrier the requesters pull row loc_row[j] of rank loc_part[j]'s staging
-// buffer (all_to_all_forward, coop.cpp:145-159): each owned row crosses the
-// storage channel at most once per step however many ranks requested it.
-int cb_px_setup_cache(cb_plan* plan, cb_cache* cache, const cb_features* local,
-                      void* handle_out) {
+// (cache.cpp:100-110) with S^L_q as part q's accesses: hits come from the
+// cache's HBM rows, misses from the shard (HBM or the pinned host tier).
+int cb_px_setup_staging(cb_plan* plan, const cb_features* local, void* handle_out) {
   return guard([&] {
-    require(plan != nullptr && cache != nullptr && local != nullptr && handle_out != nullptr,
-            "null argument");
+    require(plan != nullptr && local != nullptr && handle_out != nullptr, "null argument");
     PxState& px = px_of(plan);
-    require(local->shard_rows > 0, "the cached fetch needs this rank's shard table");
-    require(cache->lru->row_bytes() == local->row_bytes,
-            "cache row size does not match the feature table");
-    require(cache->lru->n_keys() >= plan->g->g.n, "cache key space smaller than the graph");
+    require(local->shard_rows > 0, "staging needs this rank's shard table");
     DeviceGuard dg(plan->device);
     PeWork& w = plan->pe[0];
-    px.cache = cache;
-    px.cache_store = local;
+    px.drop_graphs();
+    for (void* p : px.ropened) CB_CUDA(cudaIpcCloseMemHandle(p));
+    px.ropened.clear();
     if (px.rstage) CB_CUDA(cudaFree(px.rstage));
+    px.stage_store = local;
     px.rstage_rows = std::max<uint64_t>(w.cap_final, 1);
     CB_CUDA(cudaMalloc(&px.rstage, px.rstage_rows * local->row_bytes));
     if (!px.d_rstage) CB_CUDA(cudaMalloc(&px.d_rstage, kMaxParts * sizeof(void*)));
@@ -531,11 +566,11 @@ int cb_px_setup_cache(cb_plan* plan, cb_cache* cache, const cb_features* local,
   });
 }
 
-int cb_px_connect_cache(cb_plan* plan, uint32_t q, const void* handle) {
+int cb_px_connect_staging(cb_plan* plan, uint32_t q, const void* handle) {
   return guard([&] {
     require(plan != nullptr && handle != nullptr, "null argument");
     PxState& px = px_of(plan);
-    require(px.rstage != nullptr, "call cb_px_setup_cache first");
+    require(px.rstage != nullptr, "call cb_px_setup_staging first");
     require(q < px.world && q != px.rank, "peer rank out of range (or self)");
     DeviceGuard dg(plan->device);
     cudaIpcMemHandle_t h;
@@ -549,6 +584,20 @@ int cb_px_connect_cache(cb_plan* plan, uint32_t q, const void* handle) {
   });
 }
 
+int cb_px_set_cache(cb_plan* plan, cb_cache* cache) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    PxState& px = px_of(plan);
+    if (cache) {
+      require(px.stage_store != nullptr, "call cb_px_setup_staging first");
+      require(cache->lru->row_bytes() == px.stage_store->row_bytes,
+              "cache row size does not match the feature table");
+      require(cache->lru->n_keys() >= plan->g->g.n, "cache key space smaller than the graph");
+    }
+    px.cache = cache;
+  });
+}
+
 int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint64_t* hits,
                         uint64_t* misses) {
   NvtxRange nvtx_("cb.px_gather_cached");
@@ -556,21 +605,20 @@ int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint
     require(plan != nullptr, "null plan");
     require(plan->have_batch, "no sampled batch in this plan");
     PxState& px = px_of(plan);
-    require(px.cache != nullptr, "no cache set up (cb_px_setup_cache)");
-    for (uint32_t q = 0; q < px.world; ++q)
-      require(px.rstage_of[q] != nullptr, "staging buffer of a rank not connected");
+    require(px.cache != nullptr, "no cache set (cb_px_set_cache)");
+    require_staging(px);
     DeviceGuard dg(plan->device);
     check_overflow(plan);
     const int L = plan->L;
     PeWork& w = plan->pe[0];
-    prepare_rows(plan, px.cache_store, false);
+    prepare_rows(plan, px.stage_store, false);
     const uint64_t n_own = host_meta(plan, 0, L).n_dst;
     require(n_own <= px.rstage_rows, "owner set larger than the staging buffer");
     DeviceLru& lru = *px.cache->lru;
     const uint64_t h0 = lru.hits(), m0 = lru.misses();
     CacheGatherSrc src;
-    src.table = px.cache_store->table;
-    src.row_map = px.cache_store->row_map;
+    src.table = px.stage_store->table;
+    src.row_map = px.stage_store->row_map;
     src.rows_out = px.rstage;
     lru.access_ids(w.owner_final, n_own, order_key, nullptr, 0, src, plan->stream);
     // every owner's rows are staged before any requester reads them; the
@@ -578,7 +626,7 @@ int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint
     // reaches before finishing this pull
     launch_px_barrier(px.bar, plan->stream);
     launch_px_gather_staged(px.d_rstage, w.loc_part[L - 1], w.loc_row[L - 1],
-                            px.cache_store->row_bytes, &plan->meta_at(0, L - 1)->n_src,
+                            px.stage_store->row_bytes, &plan->meta_at(0, L - 1)->n_src,
                             w.cap_rows, w.rows, plan->stream);
     plan->have_rows = true;
     if (owned) *owned = n_own;

@@ -300,6 +300,15 @@ class PeerCoop:
             for q in range(self.world):
                 hq = (C.c_ubyte * self.HANDLE).from_buffer_copy(fh[q][0])
                 _check(self.L.cb_px_connect_features(h, q, hq, fh[q][1], store._h))
+            # owner staging: owners load their requested rows, requesters pull
+            sb = (C.c_ubyte * self.HANDLE)()
+            _check(self.L.cb_px_setup_staging(h, store._h, sb))
+            sh = [None] * self.world
+            dist.all_gather_object(sh, bytes(sb), group=group)
+            for q in range(self.world):
+                if q != rank:
+                    hq = (C.c_ubyte * self.HANDLE).from_buffer_copy(sh[q])
+                    _check(self.L.cb_px_connect_staging(h, q, hq))
         self.stream = torch.cuda.ExternalStream(self.L.cb_plan_stream(h), device=self.device)
         self._nccl = dist.get_backend(group) == "nccl"
         if barrier == "nccl" and not self._nccl:
@@ -384,15 +393,7 @@ class PeerCoop:
             raise ValueError("PeerCoop.enable_cache needs the rank's feature shard")
         self.cache = LruCache(capacity, self.g.num_vertices, self.g.device,
                               row_bytes=self.store.row_bytes)
-        buf = (C.c_ubyte * self.HANDLE)()
-        _check(self.L.cb_px_setup_cache(self._h, self.cache._h, self.store._h, buf))
-        hs = [None] * self.world
-        dist.all_gather_object(hs, bytes(buf), group=self.group)
-        for q in range(self.world):
-            if q != self.rank:
-                hq = (C.c_ubyte * self.HANDLE).from_buffer_copy(hs[q])
-                _check(self.L.cb_px_connect_cache(self._h, q, hq))
-        dist.barrier(group=self.group)
+        _check(self.L.cb_px_set_cache(self._h, self.cache._h))
 
     def load_inputs_cached(self, order_key: int) -> tuple[int, int, int]:
         """The owner-side cached fetch of this step (cb_px_gather_cached): this

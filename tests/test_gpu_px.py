@@ -135,10 +135,10 @@ def _px_cache_worker(rank, world, kappa, steps, captured, host_tier):
     owner = pm.owner
     L, dim, dtype, fseed, cap = 2, 24, "f16", 5, 600
     store = synth_shard(g, pm, rank, dim, fseed, dtype)
-    if host_tier:
-        store.set_tier(True)  # misses cross the host link (the storage channel)
     cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, fanouts=[10, 10])
     pc = PeerCoop(g, pm, rank, L, cfg, max_seeds=4096, store=store)
+    if host_tier:
+        store.set_tier(True)  # misses cross the host link (the storage channel)
     pc.enable_cache(cap)
     lru = O.Lru(cap, impl="reference")  # the reference's LruCache, this owner's
     sched = cb.SeedSchedule.make(kappa, 8)
