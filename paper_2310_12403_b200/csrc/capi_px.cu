@@ -560,6 +560,8 @@ int cb_px_setup_staging(cb_plan* plan, const cb_features* local, void* handle_ou
     if (!px.d_rstage) CB_CUDA(cudaMalloc(&px.d_rstage, kMaxParts * sizeof(void*)));
     px.rstage_of.assign(kMaxParts, nullptr);
     px.rstage_of[px.rank] = static_cast<const unsigned char*>(px.rstage);
+    CB_CUDA(cudaMemcpy(px.d_rstage, px.rstage_of.data(), kMaxParts * sizeof(void*),
+                       cudaMemcpyHostToDevice));
     cudaIpcMemHandle_t h;
     CB_CUDA(cudaIpcGetMemHandle(&h, px.rstage));
     std::memcpy(handle_out, &h, sizeof(h));
