@@ -17,8 +17,10 @@ One process per GPU (torchrun for N>1).
           `value` is not flushed between steps: the inputs (6.5 GB CSR +
           28 GB table at c4) are far larger than the 126 MB L2.
   N > 1 : the cooperative step (one part per GPU, per-layer owner exchange
-          over peer memory, rows pulled from the owners' shards; weak
-          scaling, 1024 seeds per GPU). See DESIGN.md §Multi-GPU.
+          over peer memory, owners stage their requested rows and requesters
+          pull them; the whole step one CUDA graph per rank with device
+          barriers; weak scaling, 1024 seeds per GPU). See DESIGN.md
+          §Multi-GPU.
 
 value  : device time (CUDA events, max over ranks), inputs resident in HBM.
 e2e    : through the C-ABI with host buffers: H2D of the seeds + variate keys
@@ -584,28 +586,62 @@ def kappa_evidence(cb, dev, steps_epochs=2, kappas=(1, 4, 16, 64, 256, None)):
     cap = c["n"] // 10
     spe = c["n"] // c["batch"]
     steps = steps_epochs * spe
+    ref_g, ref_steps = None, 8
+    try:  # the reference beside the GPU sweep (checker only, CPU)
+        from oracle import oracle as O
+        if O.available("reference"):
+            indptr, indices = g.download()
+            ref_g = O.RefGraph(O.CSR(indptr, indices))
+            del indptr, indices
+    except Exception:  # noqa: BLE001 - evidence only
+        ref_g = None
     out = {"workload": c["workload"], "graph_gen_s": round(gen_s, 2), "cache_rows": cap,
            "feature_tier": "pinned host memory (mapped); cache rows in HBM",
            "steps": steps, "steps_per_epoch": spe, "sweep": []}
     for kappa in kappas:
         k = cb.KAPPA_INFINITY if kappa is None else kappa
         tt = time.perf_counter()
+        res_stats = {"resolved": 0, "reruns": 0, "unresolved": 0}
+
+        def on_step(step, plan):
+            a, b_ = plan.resolve_stats()  # in-band decisions settled on the host
+            res_stats["resolved"] += a
+            res_stats["reruns"] += b_
+            res_stats["unresolved"] += sum(plan.layer_sizes(0, l)["uncertified"]
+                                           for l in range(len(c["fanouts"])))
         r = cb.run_dependent_experiment(g, cb.MinibatchSchedule(cb.BatchMode.kSmoothed, k,
                                                                 c["batch"]), steps, cap, cfg,
                                         len(c["fanouts"]), c["dim"], 4, RUN_SEED,
-                                        fingerprints=False, store=store)
+                                        fingerprints=False, store=store, on_step=on_step)
         wall = time.perf_counter() - tt
         steady = r.rows[r.warmup_steps:]
         CSV_ROWS.setdefault("cache", []).append(
             (kappa, [(x.step, x.miss_rate, x.s_l, x.bytes) for x in r.rows]))
-        out["sweep"].append({
+        row = {
             "kappa": "inf" if kappa is None else kappa,
             "steady_miss_rate": r.steady_miss_rate,
             "input_vertices_per_seed": float(np.mean([x.s_l for x in steady])) / c["batch"],
             "storage_bytes_per_step": float(np.mean([x.bytes for x in steady])),
-            "wall_ms_per_step": 1e3 * wall / steps})
+            "wall_ms_per_step": 1e3 * wall / steps,
+            "smoothed_decisions": res_stats}
+        assert res_stats["unresolved"] == 0, "unresolved smoothed decisions"
+        if ref_g is not None:
+            # the reference's own run_dependent_experiment (cache.cpp:137-208),
+            # compiled from its sources, over the first ref_steps steps of the
+            # same experiment: same |S^L| and miss bytes step by step
+            tt = time.perf_counter()
+            ref = O.dependent_experiment(ref_g, 2, k, c["batch"], ref_steps, cap, O.LABOR0, 10,
+                                         len(c["fanouts"]), c["dim"], 4, RUN_SEED)
+            ours_sl = [x.s_l for x in r.rows[:ref_steps]]
+            ours_by = [x.bytes for x in r.rows[:ref_steps]]
+            row["reference"] = {
+                "steps": ref_steps, "cpu_s_per_step": (time.perf_counter() - tt) / ref_steps,
+                "misses": [int(b) // (c["dim"] * 4) for b in ref["bytes"]],
+                "equal_s_l_and_misses": bool(list(map(int, ref["s_l"])) == ours_sl and
+                                             list(map(int, ref["bytes"])) == ours_by)}
+        out["sweep"].append(row)
     store.set_tier(False)
-    del store, g
+    del store, g, ref_g
     return out
 
 
@@ -728,8 +764,9 @@ def run_ours_coop(args, cfg):
         "config": {"workload": cfg["workload"],
                    "mode": f"cooperative (P={world}, one part per GPU; " + (
                        "peer-memory exchange: ids OR-ed into owners' bitmaps over CUDA IPC, "
-                       "ranks read back, rows pulled from owners' shards; device barriers on "
-                       "IPC flags; the whole step is one CUDA graph per rank)"
+                       "ranks read back; owners stage their requested rows, requesters pull "
+                       "them; one device barrier per layer (signal kernel + stream memory "
+                       "wait); the whole step is one CUDA graph per rank)"
                        if args.exchange == "px" else
                        f"{backend} all-to-allv per layer + feature all-to-allv)"),
                    "timing": ("CUDA events on the plan stream around K graph replays, max over "

@@ -36,7 +36,7 @@ constexpr uint32_t kTileExact = 0x80000000u;
 // labor_mark residency: 4 CTAs/SM (shared memory: ~50 KB of TMA id rings
 // each), so one CTA's staging barrier overlaps another's hashing.
 #ifndef CB_MARK_CTAS
-#define CB_MARK_CTAS 4  // 4 x ~50 KB of id rings per SM
+#define CB_MARK_CTAS 6  // 6 x ~33 KB of id rings per SM (2 stages per warp)
 #endif
 constexpr int kMarkCtasPerSM = CB_MARK_CTAS;
 #ifndef CB_MARK_MINB
@@ -596,6 +596,40 @@ __device__ __forceinline__ uint32_t mix64_yhi(uint64_t p1, uint32_t t) {
   return __umulhi(zlo, 0x133111ebu) + zlo * 0x94d049bbu + zhi * 0x133111ebu;
 }
 
+// Carry-split form of mix64_yhi for a layer prefix p1 and a 32-bit id t.
+// x = (p1 ^ t) + C0: t only touches the low word, so the high word is
+// H + cy (cy = the carry out of the low add). After x ^= x >> 30 the high
+// word's contribution to the first product's high half, (hi ^ hi >> 30) *
+// 0x1ce4e5b9, is one of two per-layer constants K[cy]: one select instead of
+// a shift, an xor and a multiply. Bit-exact with mix64_yhi.
+struct YhiConst {
+  uint32_t p1lo, Q0, Q1, K0, K1;
+};
+__host__ __device__ __forceinline__ YhiConst yhi_const(uint64_t p1) {
+  YhiConst k;
+  k.p1lo = static_cast<uint32_t>(p1);
+  const uint32_t h0 = static_cast<uint32_t>(p1 >> 32) + 0x9e3779b9u, h1 = h0 + 1u;
+  k.Q0 = h0 << 2;  // the high word's bits in the low word of x >> 30
+  k.Q1 = h1 << 2;
+  k.K0 = (h0 ^ (h0 >> 30)) * 0x1ce4e5b9u;
+  k.K1 = (h1 ^ (h1 >> 30)) * 0x1ce4e5b9u;
+  return k;
+}
+__device__ __forceinline__ uint32_t mix64_yhi_cs(const YhiConst& k, uint32_t t) {
+  uint32_t lo, cy;
+  asm("add.cc.u32 %0, %2, 0x7f4a7c15;\n\taddc.u32 %1, 0, 0;"
+      : "=r"(lo), "=r"(cy)
+      : "r"(k.p1lo ^ t));
+  const bool c = cy != 0;
+  const uint32_t xl = lo ^ (lo >> 30) ^ (c ? k.Q1 : k.Q0);  // disjoint bits: | == ^
+  const uint32_t hk = c ? k.K1 : k.K0;
+  const uint32_t zl0 = xl * 0x1ce4e5b9u;
+  const uint32_t zh0 = __umulhi(xl, 0x1ce4e5b9u) + xl * 0xbf58476du + hk;
+  const uint32_t zlo = zl0 ^ __funnelshift_r(zl0, zh0, 27);
+  const uint32_t zhi = zh0 ^ (zh0 >> 27);
+  return __umulhi(zlo, 0x133111ebu) + zlo * 0x94d049bbu + zhi * 0x133111ebu;
+}
+
 // acc = 2 * acc + (yhi <= b2): the prefilter pass bit shifted in through
 // the carry of b2 - yhi (one subtract with carry-out, one add with carry-in)
 __device__ __forceinline__ uint32_t shift_in_pass(uint32_t acc, uint32_t b2, uint32_t yhi) {
@@ -627,8 +661,11 @@ __device__ __forceinline__ bool keep_plain(uint64_t p1, uint32_t t, uint64_t T) 
 #define CB_MARK_RECS (kLaborTile / 4)
 #endif
 constexpr int kMarkRecs = CB_MARK_RECS;
+// 2 stages x 6 CTAs/SM beat 3 stages x 4 CTAs/SM (more warps to hide the
+// hash's dependent-issue latency): c4 last-layer mark 103.6 -> 96.7 us,
+// 161.6 -> 149 us/step (A/B on one box)
 #ifndef CB_PURE_STAGES
-#define CB_PURE_STAGES 3
+#define CB_PURE_STAGES 2
 #endif
 constexpr int kPureStages = CB_PURE_STAGES;     // id tiles in flight per warp
 constexpr uint32_t kPureStride = kLaborTile + 8;  // u32 per ring stage (alignment slack)
@@ -666,6 +703,7 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
   const uint64_t W = static_cast<uint64_t>(ncta) * WPC;
   const uint64_t gw = static_cast<uint64_t>(role) * WPC + (threadIdx.x >> 5);
   if (gw >= n_pure) return;
+  const YhiConst yk = yhi_const(p1);
   if (lane == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -723,7 +761,11 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
       const uint32_t b2 = static_cast<uint32_t>(Tq >> 32) | 1u;
       uint32_t cand = 0;  // bit 31 - j: position j passed
 #pragma unroll 8
+#ifdef CB_NO_CARRY_SPLIT
       for (int j = 0; j < 32; ++j) cand = shift_in_pass(cand, b2, mix64_yhi(p1, ids[32 * j]));
+#else
+      for (int j = 0; j < 32; ++j) cand = shift_in_pass(cand, b2, mix64_yhi_cs(yk, ids[32 * j]));
+#endif
       uint32_t km = __brev(cand);
       for (uint32_t kk = km; kk;) {
         const int j = __ffs(kk) - 1;
