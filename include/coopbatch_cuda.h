@@ -210,6 +210,13 @@ int cb_download_block(cb_plan* plan, uint32_t part, int layer, uint32_t* dst, ui
 int cb_plan_result_bytes(const cb_plan* plan, uint32_t part, uint64_t row_bytes,
                          uint64_t* max_bytes);
 int cb_plan_result_async(cb_plan* plan, uint32_t part, void* host_pinned, uint64_t cap_bytes);
+/* The same layout through the copy engines: waits for the batch (its counts),
+ * writes the header on the host, then enqueues one D2H copy per section on
+ * cb_plan_stream (host_pinned should be pinned for asynchrony). Returns once
+ * the copies are enqueued; *total_bytes = the result's size (truncated header
+ * only, as the kernel form, when it exceeds cap_bytes). */
+int cb_plan_result_copy(cb_plan* plan, uint32_t part, void* host_pinned, uint64_t cap_bytes,
+                        uint64_t* total_bytes);
 int cb_owner_set_size(cb_plan* plan, uint32_t part, uint64_t* n);
 int cb_download_owner_set(cb_plan* plan, uint32_t part, uint32_t* ids);
 /* send_counts[P*P] (row = sender), owner_row_counts[P]; loc_* hold part p's

@@ -553,6 +553,14 @@ class Plan:
         host_ptr, ordered on the plan stream (parse_result reads it)."""
         _check(_lib.load().cb_plan_result_async(self._h, p, C.c_void_p(host_ptr), cap))
 
+    def result_copy(self, host_ptr: int, cap: int, p: int = 0) -> int:
+        """Same layout through the copy engines (cb_plan_result_copy): waits for
+        the batch's counts, then enqueues the D2H copies; returns the size."""
+        n = C.c_uint64()
+        _check(_lib.load().cb_plan_result_copy(self._h, p, C.c_void_p(host_ptr), cap,
+                                               C.byref(n)))
+        return n.value
+
     def rows(self, p: int, store: FeatureStore) -> np.ndarray:
         n = self.layer_sizes(p, self.L - 1)["n_src"]
         out = np.zeros((n, store.dim), dtype=_DT[store.dtype][1])

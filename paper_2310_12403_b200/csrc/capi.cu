@@ -1714,6 +1714,75 @@ int cb_plan_result_async(cb_plan* plan, uint32_t part, void* host_pinned, uint64
   });
 }
 
+// The same result layout moved by the copy engines: the host waits for the
+// batch (its counts), writes the header itself and enqueues one D2H copy per
+// section on the plan stream. A copy engine sustains ~56 GB/s over the host
+// link where SM stores into mapped memory reach ~34 GB/s; the price is the
+// host wait, which a caller keeping several batches in flight hides.
+int cb_plan_result_copy(cb_plan* plan, uint32_t part, void* host_pinned, uint64_t cap_bytes,
+                        uint64_t* total_bytes) {
+  NvtxRange nvtx_("cb.result_copy");
+  return guard([&] {
+    require(plan != nullptr && host_pinned != nullptr, "null argument");
+    require_batch(plan, part, 0);
+    require(plan->L <= kResultMaxLayers, "result: too many layers");
+    const int L = plan->L;
+    const uint64_t head = 8ULL * (5 + 3 * L);
+    require(cap_bytes >= head, "result buffer smaller than its header");
+    DeviceGuard dg(plan->device);
+    if (!plan->meta_host) CB_CUDA(cudaHostAlloc(&plan->meta_host, sizeof(LayerMeta) * (kResultMaxLayers + 1), cudaHostAllocDefault));
+    CB_CUDA(cudaMemcpyAsync(plan->meta_host, plan->meta_at(part, 0), sizeof(LayerMeta) * L,
+                            cudaMemcpyDeviceToHost, plan->stream));
+    CB_CUDA(cudaStreamSynchronize(plan->stream));
+    const LayerMeta* m = static_cast<const LayerMeta*>(plan->meta_host);
+    PeWork& w = plan->pe[part];
+    auto pad = [](uint64_t b) { return (b + 15) & ~15ULL; };
+    struct Sec {
+      const void* src;
+      uint64_t bytes, off;
+    };
+    std::vector<Sec> sec;
+    uint64_t off = pad(head);
+    for (int l = 0; l < L; ++l) {
+      const LayerBufs& b = w.L[l];
+      const uint32_t* d_dst;
+      if (l == 0) d_dst = plan->seeds + plan->seeds_off[part];
+      else if (!plan->own_dst()) d_dst = w.L[l - 1].src;
+      else d_dst = b.dst;
+      const void* ptr[4] = {d_dst, b.src, b.edges, b.dst_pos};
+      const uint64_t by[4] = {m[l].n_dst * 4, m[l].n_src * 4, m[l].n_edges * 8, m[l].n_dst * 4};
+      for (int f = 0; f < 4; ++f) {
+        sec.push_back({ptr[f], by[f], off});
+        off += pad(by[f]);
+      }
+    }
+    const uint64_t rb = plan->have_rows ? w.rows_row_bytes : 0;
+    if (plan->have_rows) {
+      const uint64_t by = m[L - 1].n_src * rb;
+      sec.push_back({w.rows, by, off});
+      off += pad(by);
+    }
+    uint64_t* hd = static_cast<uint64_t*>(host_pinned);
+    hd[0] = 0x3153524243ULL;  // "CBRS1", as result.cu
+    hd[1] = static_cast<uint64_t>(L);
+    hd[2] = rb;
+    hd[3] = off;
+    hd[4] = off <= cap_bytes ? 0 : 1;
+    for (int l = 0; l < L; ++l) {
+      hd[5 + 3 * l] = m[l].n_dst;
+      hd[6 + 3 * l] = m[l].n_src;
+      hd[7 + 3 * l] = m[l].n_edges;
+    }
+    if (total_bytes) *total_bytes = off;
+    if (off > cap_bytes) return;
+    unsigned char* out = static_cast<unsigned char*>(host_pinned);
+    for (const Sec& s : sec)
+      if (s.bytes)
+        CB_CUDA(cudaMemcpyAsync(out + s.off, s.src, s.bytes, cudaMemcpyDeviceToHost,
+                                plan->stream));
+  });
+}
+
 int cb_owner_set_size(cb_plan* plan, uint32_t part, uint64_t* n) {
   return guard([&] {
     require(plan != nullptr && n != nullptr, "null argument");

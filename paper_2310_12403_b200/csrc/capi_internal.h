@@ -284,6 +284,7 @@ struct cb_plan {
   cbdev::ResolvePend* rs_pend = nullptr;
   unsigned long long* rs_npend = nullptr;
   uint64_t rs_resolved = 0, rs_reruns = 0;  // of the last cb_sample_sync
+  void* meta_host = nullptr;  // pinned staging of cb_plan_result_copy's counts
   uint64_t batches = 0;  // device epoch bumps (count_epoch_bumps)
   uint64_t launches = 0;  // kernels enqueued by the last cb_sample (+ cb_gather)
   double* vtab = nullptr;  // smoothed LABOR r_t table [n] (nullptr: per position)
@@ -320,6 +321,7 @@ struct cb_plan {
     for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ext_vtab) cudaFree(ext_vtab);
+    if (meta_host) cudaFreeHost(meta_host);
     for (void* q : {static_cast<void*>(d_rs), static_cast<void*>(rs_k1),
                     static_cast<void*>(rs_k2), static_cast<void*>(rs_val),
                     static_cast<void*>(rs_pend), static_cast<void*>(rs_npend)})

@@ -44,6 +44,19 @@ def test_result_buffer_matches_downloads(gpu, c1, kind, dtype, dim):
         plan.result_async(buf.data_ptr(), cap)
         plan.synchronize()
         res = cb.parse_result(buf.numpy(), np.float16 if dtype == "f16" else np.float32)
+        # the copy-engine form: the same bytes (header + every section)
+        buf2 = torch.zeros(cap, dtype=torch.uint8).pin_memory()
+        n = plan.result_copy(buf2.data_ptr(), cap)
+        plan.synchronize()
+        assert n == res["total_bytes"]
+        a, b2 = buf.numpy()[:n], buf2.numpy()[:n]
+        hdr = 8 * (5 + 3 * 3)
+        assert np.array_equal(a[:hdr], b2[:hdr])
+        res2 = cb.parse_result(buf2.numpy(), np.float16 if dtype == "f16" else np.float32)
+        for l in range(3):
+            for k in ("dst", "src", "edges", "dst_pos"):
+                assert np.array_equal(res2["blocks"][l][k], res["blocks"][l][k])
+        assert np.array_equal(res2["rows"].view(np.uint8), res["rows"].view(np.uint8))
         want = O.expand(ref, s, 3, int(kind), 10, osched(sched))
         for l in range(3):
             for k in ("dst", "src", "edges", "dst_pos"):
@@ -56,6 +69,10 @@ def test_result_buffer_matches_downloads(gpu, c1, kind, dtype, dim):
     small = torch.zeros(256, dtype=torch.uint8).pin_memory()
     plan.result_async(small.data_ptr(), 256)
     plan.synchronize()
+    hd = small.numpy()[:40].view(np.uint64)
+    assert int(hd[4]) == 1 and int(hd[3]) == res["total_bytes"]
+    small.zero_()
+    assert plan.result_copy(small.data_ptr(), 256) == res["total_bytes"]
     hd = small.numpy()[:40].view(np.uint64)
     assert int(hd[4]) == 1 and int(hd[3]) == res["total_bytes"]
     with pytest.raises(ValueError):
