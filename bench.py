@@ -931,6 +931,7 @@ def run_ours(args, cfg):
         if i >= S:
             plans[i % S].result_copy(res_bufs[i % S].data_ptr(), res_cap_used)
         plans[i % S].replay(pinned.data_ptr() + (W + i) * b * 4, scheds[W + i], False, 3)
+        plans[i % S].result_pack()  # packed on the device right behind the batch
 
     def e2e_tail():
         for i in range(max(0, K - S), K):

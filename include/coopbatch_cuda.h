@@ -210,11 +210,14 @@ int cb_download_block(cb_plan* plan, uint32_t part, int layer, uint32_t* dst, ui
 int cb_plan_result_bytes(const cb_plan* plan, uint32_t part, uint64_t row_bytes,
                          uint64_t* max_bytes);
 int cb_plan_result_async(cb_plan* plan, uint32_t part, void* host_pinned, uint64_t cap_bytes);
-/* The same layout through the copy engines: waits for the batch (its counts),
- * writes the header on the host, then enqueues one D2H copy per section on
- * cb_plan_stream (host_pinned should be pinned for asynchrony). Returns once
- * the copies are enqueued; *total_bytes = the result's size (truncated header
- * only, as the kernel form, when it exceeds cap_bytes). */
+/* The same layout through a copy engine. cb_plan_result_pack enqueues the
+ * packing of the batch's result into a device staging buffer (asynchronous;
+ * call it right after the batch). cb_plan_result_copy waits for the batch and
+ * its pack (packing first if nothing was packed for this batch), then enqueues
+ * ONE D2H copy of the packed bytes on cb_plan_stream (host_pinned should be
+ * pinned for asynchrony) and returns; *total_bytes = the result's size (a
+ * truncated header only, as the kernel form, when it exceeds cap_bytes). */
+int cb_plan_result_pack(cb_plan* plan, uint32_t part);
 int cb_plan_result_copy(cb_plan* plan, uint32_t part, void* host_pinned, uint64_t cap_bytes,
                         uint64_t* total_bytes);
 int cb_owner_set_size(cb_plan* plan, uint32_t part, uint64_t* n);

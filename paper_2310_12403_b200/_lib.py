@@ -75,6 +75,7 @@ _SIGS = {
     "cb_plan_result_bytes": (C.c_int, [_P, _u32, _u64, C.POINTER(_u64)]),
     "cb_plan_result_async": (C.c_int, [_P, _u32, _P, _u64]),
     "cb_plan_result_copy": (C.c_int, [_P, _u32, _P, _u64, C.POINTER(_u64)]),
+    "cb_plan_result_pack": (C.c_int, [_P, _u32]),
     "cb_download_owner_set": (C.c_int, [_P, _u32, _P]),
     "cb_download_exchange": (C.c_int, [_P, C.c_int, _P, _P, _P, _P]),
     "cb_download_rows": (C.c_int, [_P, _u32, _P]),

@@ -553,9 +553,13 @@ class Plan:
         host_ptr, ordered on the plan stream (parse_result reads it)."""
         _check(_lib.load().cb_plan_result_async(self._h, p, C.c_void_p(host_ptr), cap))
 
+    def result_pack(self, p: int = 0):
+        """Pack the batch's result on the device, asynchronously (for result_copy)."""
+        _check(_lib.load().cb_plan_result_pack(self._h, p))
+
     def result_copy(self, host_ptr: int, cap: int, p: int = 0) -> int:
-        """Same layout through the copy engines (cb_plan_result_copy): waits for
-        the batch's counts, then enqueues the D2H copies; returns the size."""
+        """Same layout through a copy engine (cb_plan_result_copy): waits for the
+        batch and its pack, then enqueues one D2H copy; returns the size."""
         n = C.c_uint64()
         _check(_lib.load().cb_plan_result_copy(self._h, p, C.c_void_p(host_ptr), cap,
                                                C.byref(n)))

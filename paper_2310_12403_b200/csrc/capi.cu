@@ -1714,11 +1714,57 @@ int cb_plan_result_async(cb_plan* plan, uint32_t part, void* host_pinned, uint64
   });
 }
 
-// The same result layout moved by the copy engines: the host waits for the
-// batch (its counts), writes the header itself and enqueues one D2H copy per
-// section on the plan stream. A copy engine sustains ~56 GB/s over the host
-// link where SM stores into mapped memory reach ~34 GB/s; the price is the
-// host wait, which a caller keeping several batches in flight hides.
+// Pack part `part`'s batch result (result.cu layout) into the plan's device
+// staging buffer, sized from the capacities (cb_plan_result_bytes).
+void enqueue_result_pack(cb_plan* plan, uint32_t part) {
+  const int L = plan->L;
+  PeWork& w = plan->pe[part];
+  uint64_t need = 0;
+  cb_plan_result_bytes(plan, part, plan->have_rows ? w.rows_row_bytes : 0, &need);
+  if (plan->pack_bytes < need) {
+    if (plan->pack) CB_CUDA(cudaFree(plan->pack));
+    plan->pack_bytes = need;
+    CB_CUDA(cudaMalloc(&plan->pack, plan->pack_bytes));
+  }
+  ResultArgs a{};
+  a.meta = plan->meta_at(part, 0);
+  a.L = L;
+  for (int l = 0; l < L; ++l) {
+    const LayerBufs& b = w.L[l];
+    const uint32_t* d_dst;
+    if (l == 0) d_dst = plan->seeds + plan->seeds_off[part];
+    else if (!plan->own_dst()) d_dst = w.L[l - 1].src;
+    else d_dst = b.dst;
+    a.ptr[l][0] = d_dst;
+    a.ptr[l][1] = b.src;
+    a.ptr[l][2] = b.edges;
+    a.ptr[l][3] = b.dst_pos;
+  }
+  a.rows = plan->have_rows ? w.rows : nullptr;
+  a.row_bytes = plan->have_rows ? w.rows_row_bytes : 0;
+  a.out = static_cast<unsigned char*>(plan->pack);
+  a.cap = plan->pack_bytes;
+  launch_result(a, plan->stream);
+  plan->pack_part = part;
+  plan->pack_version = plan->batches;
+}
+
+int cb_plan_result_pack(cb_plan* plan, uint32_t part) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    require_batch(plan, part, 0);
+    require(plan->L <= kResultMaxLayers, "result: too many layers");
+    DeviceGuard dg(plan->device);
+    enqueue_result_pack(plan, part);
+  });
+}
+
+// The result moved by a copy engine: the batch packed on the device (by
+// cb_plan_result_pack right after the batch, else here), the host waits for
+// it, and ONE D2H copy of the packed bytes follows on the plan stream. A copy
+// engine sustains ~56 GB/s over the host link where SM stores into mapped
+// memory reach ~34 GB/s; the host wait is hidden by a caller that keeps
+// several batches in flight.
 int cb_plan_result_copy(cb_plan* plan, uint32_t part, void* host_pinned, uint64_t cap_bytes,
                         uint64_t* total_bytes) {
   NvtxRange nvtx_("cb.result_copy");
@@ -1727,59 +1773,25 @@ int cb_plan_result_copy(cb_plan* plan, uint32_t part, void* host_pinned, uint64_
     require_batch(plan, part, 0);
     require(plan->L <= kResultMaxLayers, "result: too many layers");
     const int L = plan->L;
-    const uint64_t head = 8ULL * (5 + 3 * L);
-    require(cap_bytes >= head, "result buffer smaller than its header");
+    require(cap_bytes >= 8ULL * (5 + 3 * L), "result buffer smaller than its header");
     DeviceGuard dg(plan->device);
-    if (!plan->meta_host) CB_CUDA(cudaHostAlloc(&plan->meta_host, sizeof(LayerMeta) * (kResultMaxLayers + 1), cudaHostAllocDefault));
-    CB_CUDA(cudaMemcpyAsync(plan->meta_host, plan->meta_at(part, 0), sizeof(LayerMeta) * L,
-                            cudaMemcpyDeviceToHost, plan->stream));
+    if (plan->pack_version != plan->batches || plan->pack_part != part)
+      enqueue_result_pack(plan, part);
+    if (!plan->meta_host)
+      CB_CUDA(cudaHostAlloc(&plan->meta_host, 64, cudaHostAllocDefault));
+    // the packed header (its total size) once the batch and the pack are done
+    CB_CUDA(cudaMemcpyAsync(plan->meta_host, plan->pack, 40, cudaMemcpyDeviceToHost,
+                            plan->stream));
     CB_CUDA(cudaStreamSynchronize(plan->stream));
-    const LayerMeta* m = static_cast<const LayerMeta*>(plan->meta_host);
-    PeWork& w = plan->pe[part];
-    auto pad = [](uint64_t b) { return (b + 15) & ~15ULL; };
-    struct Sec {
-      const void* src;
-      uint64_t bytes, off;
-    };
-    std::vector<Sec> sec;
-    uint64_t off = pad(head);
-    for (int l = 0; l < L; ++l) {
-      const LayerBufs& b = w.L[l];
-      const uint32_t* d_dst;
-      if (l == 0) d_dst = plan->seeds + plan->seeds_off[part];
-      else if (!plan->own_dst()) d_dst = w.L[l - 1].src;
-      else d_dst = b.dst;
-      const void* ptr[4] = {d_dst, b.src, b.edges, b.dst_pos};
-      const uint64_t by[4] = {m[l].n_dst * 4, m[l].n_src * 4, m[l].n_edges * 8, m[l].n_dst * 4};
-      for (int f = 0; f < 4; ++f) {
-        sec.push_back({ptr[f], by[f], off});
-        off += pad(by[f]);
-      }
+    const uint64_t* hd = static_cast<const uint64_t*>(plan->meta_host);
+    const uint64_t total = hd[3];
+    if (total_bytes) *total_bytes = total;
+    const uint64_t n = total <= cap_bytes ? total : 8ULL * (5 + 3 * L);
+    CB_CUDA(cudaMemcpyAsync(host_pinned, plan->pack, n, cudaMemcpyDeviceToHost, plan->stream));
+    if (total > cap_bytes) {  // header only, flagged truncated, as the kernel form
+      CB_CUDA(cudaStreamSynchronize(plan->stream));
+      static_cast<uint64_t*>(host_pinned)[4] = 1;
     }
-    const uint64_t rb = plan->have_rows ? w.rows_row_bytes : 0;
-    if (plan->have_rows) {
-      const uint64_t by = m[L - 1].n_src * rb;
-      sec.push_back({w.rows, by, off});
-      off += pad(by);
-    }
-    uint64_t* hd = static_cast<uint64_t*>(host_pinned);
-    hd[0] = 0x3153524243ULL;  // "CBRS1", as result.cu
-    hd[1] = static_cast<uint64_t>(L);
-    hd[2] = rb;
-    hd[3] = off;
-    hd[4] = off <= cap_bytes ? 0 : 1;
-    for (int l = 0; l < L; ++l) {
-      hd[5 + 3 * l] = m[l].n_dst;
-      hd[6 + 3 * l] = m[l].n_src;
-      hd[7 + 3 * l] = m[l].n_edges;
-    }
-    if (total_bytes) *total_bytes = off;
-    if (off > cap_bytes) return;
-    unsigned char* out = static_cast<unsigned char*>(host_pinned);
-    for (const Sec& s : sec)
-      if (s.bytes)
-        CB_CUDA(cudaMemcpyAsync(out + s.off, s.src, s.bytes, cudaMemcpyDeviceToHost,
-                                plan->stream));
   });
 }
 

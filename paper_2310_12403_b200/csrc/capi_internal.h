@@ -285,6 +285,10 @@ struct cb_plan {
   unsigned long long* rs_npend = nullptr;
   uint64_t rs_resolved = 0, rs_reruns = 0;  // of the last cb_sample_sync
   void* meta_host = nullptr;  // pinned staging of cb_plan_result_copy's counts
+  void* pack = nullptr;       // cb_plan_result_pack's packed result (device)
+  uint64_t pack_bytes = 0;
+  uint64_t pack_version = ~0ULL;  // plan->batches when packed
+  uint32_t pack_part = 0;
   uint64_t batches = 0;  // device epoch bumps (count_epoch_bumps)
   uint64_t launches = 0;  // kernels enqueued by the last cb_sample (+ cb_gather)
   double* vtab = nullptr;  // smoothed LABOR r_t table [n] (nullptr: per position)
@@ -322,6 +326,7 @@ struct cb_plan {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ext_vtab) cudaFree(ext_vtab);
     if (meta_host) cudaFreeHost(meta_host);
+    if (pack) cudaFree(pack);
     for (void* q : {static_cast<void*>(d_rs), static_cast<void*>(rs_k1),
                     static_cast<void*>(rs_k2), static_cast<void*>(rs_val),
                     static_cast<void*>(rs_pend), static_cast<void*>(rs_npend)})

@@ -46,6 +46,8 @@ def test_result_buffer_matches_downloads(gpu, c1, kind, dtype, dim):
         res = cb.parse_result(buf.numpy(), np.float16 if dtype == "f16" else np.float32)
         # the copy-engine form: the same bytes (header + every section)
         buf2 = torch.zeros(cap, dtype=torch.uint8).pin_memory()
+        if step != 1:
+            plan.result_pack()  # else result_copy packs itself
         n = plan.result_copy(buf2.data_ptr(), cap)
         plan.synchronize()
         assert n == res["total_bytes"]
