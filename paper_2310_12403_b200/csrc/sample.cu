@@ -33,10 +33,14 @@ namespace {
 
 constexpr int kNT = 256;
 constexpr uint32_t kTileExact = 0x80000000u;
-// labor_mark residency: 4 CTAs/SM (shared memory: ~50 KB of TMA id rings
-// each), so one CTA's staging barrier overlaps another's hashing.
+// labor_mark residency: 8 CTAs/SM at 64 registers and ~21 KB of shared
+// memory each (one TMA id stage per warp, 128 staged records): one CTA's
+// staging barrier overlaps another's hashing, and the small footprint leaves
+// room for the other in-flight batches' kernels. A/B on one box (c4, 8
+// batches in flight): 4 CTAs x 3 stages 161.6 us/step, 6 x 2 146-149,
+// 8 x 1 134; the mark alone 103.6 / 93-97 / 91 us.
 #ifndef CB_MARK_CTAS
-#define CB_MARK_CTAS 6  // 6 x ~33 KB of id rings per SM (2 stages per warp)
+#define CB_MARK_CTAS 8
 #endif
 constexpr int kMarkCtasPerSM = CB_MARK_CTAS;
 #ifndef CB_MARK_MINB
@@ -658,14 +662,11 @@ __device__ __forceinline__ bool keep_plain(uint64_t p1, uint32_t t, uint64_t T) 
 }
 
 #ifndef CB_MARK_RECS
-#define CB_MARK_RECS (kLaborTile / 4)
+#define CB_MARK_RECS (kLaborTile / 8)
 #endif
 constexpr int kMarkRecs = CB_MARK_RECS;
-// 2 stages x 6 CTAs/SM beat 3 stages x 4 CTAs/SM (more warps to hide the
-// hash's dependent-issue latency): c4 last-layer mark 103.6 -> 96.7 us,
-// 161.6 -> 149 us/step (A/B on one box)
 #ifndef CB_PURE_STAGES
-#define CB_PURE_STAGES 2
+#define CB_PURE_STAGES 1
 #endif
 constexpr int kPureStages = CB_PURE_STAGES;     // id tiles in flight per warp
 constexpr uint32_t kPureStride = kLaborTile + 8;  // u32 per ring stage (alignment slack)
@@ -981,7 +982,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
 }
 
 template <int IPT, bool SMOOTH>
-__global__ void __launch_bounds__(kMarkNT, kMarkMinBlocks) labor_mark_kernel(LaborArgs a) {
+__global__ void __launch_bounds__(kMarkNT, SMOOTH ? 6 : kMarkMinBlocks) labor_mark_kernel(LaborArgs a) {
   pdl_begin();
   mark_body<IPT, SMOOTH>(a, blockIdx.x, gridDim.x);
 }
