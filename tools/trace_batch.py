@@ -1,5 +1,6 @@
-"""Debug: globaltimer stamps of one c2 batch (CB_TRACE=1). Prints per kernel
-the stamp offsets (us) relative to the first stamp of the batch."""
+"""Debug: globaltimer stamps of one batch (CB_TRACE=1) of a bench config
+(default c2). Prints per kernel the stamp offsets (us) relative to the first
+stamp of the batch.  python tools/trace_batch.py [c4]"""
 import ctypes as C
 import os
 import sys
@@ -11,8 +12,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2310_12403_b200 as cb  # noqa: E402
 from paper_2310_12403_b200 import _lib  # noqa: E402
 from paper_2310_12403_b200.seeds import draw_from_pool  # noqa: E402
+import bench  # noqa: E402
 
-g = cb.Graph.generate_rmat(2449029, 61859140, 42)
+cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+g = cb.Graph.generate_rmat(cfg["n"], cfg["m"], 42)
 plan = cb.Plan(g, None, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), 1024)
 pool = np.arange(g.num_vertices, dtype=np.uint32)
 s = cb.SeedSchedule.make(1, 1234)
