@@ -430,6 +430,7 @@ LaborArgs labor_args(cb_plan* pl, PeWork& w, uint32_t p, int l, const uint32_t* 
   la.slots = b.slots;
   la.tile_list = (pl->kind == CB_LABOR0 || pl->kind == CB_FULL) ? b.tile_list : nullptr;
   la.list_ctr = w.sync.tickets + Sync::kListTicket + 2 * l;
+  la.pure_ticket = w.sync.tickets + Sync::kPureTicket + l;
   la.list_cap = w.sync.max_tiles;
   la.keep_words = w.sync.keep_words;
   la.stage = w.sync.stage;

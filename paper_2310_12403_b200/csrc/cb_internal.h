@@ -149,6 +149,8 @@ struct Sync {
   static constexpr int kMaxTickets = 256;
   // tickets [kListTicket + 2l, +1]: layer l's single-record / mixed tile counts
   static constexpr int kListTicket = 192;
+  // ticket [kPureTicket + l]: layer l's labor_mark phase-A work counter
+  static constexpr int kPureTicket = 128;
 };
 
 // Bitmap dedup structure over the vertex id space.
@@ -228,6 +230,7 @@ struct LaborArgs {
   uint32_t* slots;
   const uint2* tile_list;    // the frontier's tile lists (null: every tile in phase B)
   const unsigned* list_ctr;
+  unsigned* pure_ticket;  // phase A's dynamic split of the single-record tiles
   uint64_t list_cap;
   uint32_t* keep_words;  // 1 bit per scan position (labor_mark -> labor_emit)
   uint2* stage;          // (t, dst index) of each kept scan position

@@ -619,6 +619,13 @@ __host__ __device__ __forceinline__ YhiConst yhi_const(uint64_t p1) {
   k.K1 = (h1 ^ (h1 >> 30)) * 0x1ce4e5b9u;
   return k;
 }
+// K0 / K1 pass through an opaque move: otherwise the compiler sinks their
+// multiply past the select (select(a, b) * c), one IMAD more per position.
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  uint32_t r;
+  asm("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
 __device__ __forceinline__ uint32_t mix64_yhi_cs(const YhiConst& k, uint32_t t) {
   uint32_t lo, cy;
   asm("add.cc.u32 %0, %2, 0x7f4a7c15;\n\taddc.u32 %1, 0, 0;"
@@ -668,6 +675,12 @@ constexpr int kMarkRecs = CB_MARK_RECS;
 #ifndef CB_PURE_STAGES
 #define CB_PURE_STAGES 1
 #endif
+// phase A work split: 0 = static (warp gw takes entries gw, gw + W, ...),
+// G > 0 = G entries at a time from a ticket
+#ifndef CB_PURE_GRAB
+#define CB_PURE_GRAB 0
+#endif
+
 constexpr int kPureStages = CB_PURE_STAGES;     // id tiles in flight per warp
 constexpr uint32_t kPureStride = kLaborTile + 8;  // u32 per ring stage (alignment slack)
 
@@ -704,19 +717,38 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
   const uint64_t W = static_cast<uint64_t>(ncta) * WPC;
   const uint64_t gw = static_cast<uint64_t>(role) * WPC + (threadIdx.x >> 5);
   if (gw >= n_pure) return;
-  const YhiConst yk = yhi_const(p1);
+  YhiConst yk = yhi_const(p1);
+  yk.K0 = opaque(yk.K0);
+  yk.K1 = opaque(yk.K1);
   if (lane == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
   uint32_t phase = 0;  // parity bit per stage
+#if CB_PURE_GRAB > 0
+  // dynamic split (build option): the warp takes CB_PURE_GRAB entries at a
+  // time from the layer's phase-A ticket (zeroed by batch_begin). A/B at c4:
+  // the last-layer mark alone 91.6 -> 85.4 us (warps of a CTA reach the
+  // phase-B barrier together), but 134 -> 145 us/step with 8 batches in
+  // flight, so the static split stays the default.
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(a.pure_ticket, static_cast<unsigned>(CB_PURE_GRAB));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n_pure) break;
+    const uint64_t e = static_cast<uint64_t>(base) + lane;
+    const bool have = lane < static_cast<uint32_t>(CB_PURE_GRAB) && e < n_pure;
+    uint64_t row = 0, T = 0, x0 = 0;
+    uint32_t di = 0;
+#else
   for (uint64_t kb = 0; gw + kb * 32 * W < n_pure; ++kb) {
     // lane i: list entry gw + (32 kb + i) W = (tile, record)
     const uint64_t e = gw + (kb * 32 + lane) * W;
     uint64_t row = 0, T = 0, x0 = 0;
     uint32_t di = 0;
     const bool have = e < n_pure;
+#endif
     if (have) {
       const uint2 tr = a.tile_list[e];
       x0 = static_cast<uint64_t>(tr.x) * TILE;
@@ -843,6 +875,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
     MarkSmemA& sa = *reinterpret_cast<MarkSmemA*>(s_raw);
     mark_pure<kPureStages>(a, p1, n_pure, role, ncta, &sa.ring[warp][0][0], s_rbar[warp]);
     __syncthreads();  // the ring memory becomes phase B's
+    tstamp(a.trace, role, 2);
   }
   const uint64_t nb = listed ? (n_mixed > role ? (n_mixed - role + ncta - 1) / ncta : 0)
                              : (ntiles > role ? (ntiles - role + ncta - 1) / ncta : 0);

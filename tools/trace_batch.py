@@ -29,6 +29,7 @@ t = buf.reshape(32, 64, 8).astype(np.int64)
 t0 = t[t > 0].min()
 names = {0: "frontier0", 1: "mark0", 2: "post0", 3: "frontier1", 4: "mark1", 5: "post1",
          6: "frontier2", 7: "mark2", 8: "post2"}
+# mark stamps: 0 start, 2 end of phase A (single-record tiles), 1 end
 for k, nm in names.items():
     # post: CTAs 0-31 = extract roles, 32-63 = emit roles
     for cta in (list(range(0, 64, 8)) if not nm.startswith("post") else
