@@ -698,8 +698,14 @@ def run_ours_coop(args, cfg):
         from paper_2310_12403_b200.coopbatch import _check
         _check(_lib.load().cb_plan_captured_launches(pc._h, 4, C.byref(n_cap)))
 
+        mb_ = C.c_uint64()
+        _lib.load().cb_plan_meta_async(pc._h, None, C.byref(mb_))
+        meta_pin = torch.empty((W + K, int(mb_.value)), dtype=torch.uint8).pin_memory()
+
         def step(i, seeds):
             pc.step(seeds, scheds[i])
+            if not isinstance(seeds, torch.Tensor):  # e2e: the step's counts come back
+                _lib.load().cb_plan_meta_async(pc._h, C.c_void_p(meta_pin[i].data_ptr()), None)
             return 0  # row bytes read from the device after the timed loop
     else:
         eng = CudaEngine(g, pm, rank, L, scfg, max_seeds=b, store=store,
@@ -749,8 +755,9 @@ def run_ours_coop(args, cfg):
         nr = C.c_uint64()
         _lib.load().cb_px_sizes(pc._h, L - 1, C.byref(nr), None)
         row_bytes_total = nr.value * store.row_bytes * K
-    # e2e: host seeds (H2D inside), rows end on the device, one D2H of the
-    # owned-set size per step (the batch result the trainer reads)
+    # e2e: host seeds (H2D inside each step), rows end on the device, the
+    # step's per-layer counts read back into pinned memory (px) or the split
+    # sizes read by the host-orchestrated exchange (a2a)
     e2e_dt, _, _ = timed(lambda i: seeds_host[i])
     if rank != 0:
         dist.destroy_process_group()
@@ -776,7 +783,7 @@ def run_ours_coop(args, cfg):
                    "graph": {"vertices": cfg["n"], "edges": cfg["m"], "gen_s": round(gen_s, 2)}},
         "feature_gbps": row_bytes_total / dt / 1e9,
         "e2e": {"value": seeds_total / e2e_dt, "unit": "seeds/s", "h2d_bytes_per_step": b * 4,
-                "d2h_bytes_per_step": 8 * (1 + 2 * L)},
+                "d2h_bytes_per_step": int(mb_.value) if args.exchange == "px" else 8 * (1 + 2 * L)},
         "gpu_launches": launches, "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
