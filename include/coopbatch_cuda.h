@@ -433,6 +433,15 @@ int cb_px_gather(cb_plan* plan, const cb_features* local);
 int cb_px_setup_staging(cb_plan* plan, const cb_features* local, void* handle_out);
 int cb_px_connect_staging(cb_plan* plan, uint32_t peer, const void* handle);
 int cb_px_set_cache(cb_plan* plan, cb_cache* cache);
+/* Requester-side cache for cb_px_gather_cached: the requested rows owned by
+ * other ranks go through `cache` (a second LRU, keys = vertex ids) in
+ * access_order(R, hstep(order_key, "REQUE")): hits come from its HBM rows,
+ * only misses cross NVLink (pulled from the owners' staging buffers). NULL
+ * detaches it. cb_px_requester_stats: the last step's remote rows, hits and
+ * misses (misses x row bytes = the peer bytes of the step). */
+int cb_px_set_requester_cache(cb_plan* plan, cb_cache* cache);
+int cb_px_requester_stats(const cb_plan* plan, uint64_t* remote, uint64_t* hits,
+                          uint64_t* misses);
 int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint64_t* hits,
                         uint64_t* misses);
 

@@ -156,6 +156,7 @@ __global__ void decide_kernel(const uint32_t* __restrict__ keys, const uint32_t*
                               const uint32_t* __restrict__ xcnt, uint64_t cap, uint8_t* miss,
                               const int32_t* __restrict__ slot_of, const unsigned char* rows,
                               const unsigned char* table, const uint32_t* __restrict__ row_map,
+                              const void* const* __restrict__ miss_ptr,
                               uint64_t row_bytes, const void** src_ptr,
                               unsigned long long* ctr) {
   unsigned long long h = 0;
@@ -169,9 +170,10 @@ __global__ void decide_kernel(const uint32_t* __restrict__ keys, const uint32_t*
       const uint32_t j = ord ? ord[i] : static_cast<uint32_t>(i);
       const uint32_t v = keys[j];
       src_ptr[j] = hit ? static_cast<const void*>(rows + static_cast<uint64_t>(slot_of[v]) * row_bytes)
-                       : static_cast<const void*>(table + static_cast<uint64_t>(
-                                                              row_map ? row_map[v] : v) *
-                                                              row_bytes);
+                   : miss_ptr ? miss_ptr[j]
+                              : static_cast<const void*>(table + static_cast<uint64_t>(
+                                                                     row_map ? row_map[v] : v) *
+                                                                     row_bytes);
     }
   }
   h = warp_sum(h);
@@ -419,12 +421,13 @@ void DeviceLru::run_batch(const uint32_t* keys, const uint32_t* ord, uint64_t B,
     CB_LAUNCH("cache_merge_level");
     c ^= 1;
   }
-  const bool gather = src && src->rows_out && src->table;
+  const bool gather = src && src->rows_out && (src->table || src->miss_ptr);
   const int vb = vec_of(row_bytes_);
   decide_kernel<<<grid_of(B), 256, 0, st>>>(
       keys, ord, B, rho_, xcnt_, cap_, d_miss, slot_of_, rows_,
       gather ? static_cast<const unsigned char*>(src->table) : nullptr,
-      gather ? src->row_map : nullptr, row_bytes_, gather ? src_ptr_ : nullptr, ctr_);
+      gather ? src->row_map : nullptr, gather ? src->miss_ptr : nullptr, row_bytes_,
+      gather ? src_ptr_ : nullptr, ctr_);
   CB_LAUNCH("cache_decide");
   if (gather) {
     const uint32_t vpr = static_cast<uint32_t>(row_bytes_ / vb);

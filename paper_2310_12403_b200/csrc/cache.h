@@ -25,6 +25,9 @@ struct CacheGatherSrc {
   const void* table = nullptr;      // backing rows (device or mapped host memory)
   const uint32_t* row_map = nullptr;  // row of v in table (nullptr = v)
   void* rows_out = nullptr;         // [kept] rows in kept-id order
+  // instead of table/row_map: the address of each kept key's row on a miss
+  // (device array by kept position; e.g. rows in peers' staging buffers)
+  const void* const* miss_ptr = nullptr;
 };
 
 class DeviceLru {

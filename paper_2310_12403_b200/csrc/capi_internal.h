@@ -186,6 +186,16 @@ struct PxState {
   // staged in an exported buffer, pulled by the requesters; optional cache
   cb_cache* cache = nullptr;
   const cb_features* stage_store = nullptr;
+  // requester-side cache (cb_px_set_requester_cache): rows owned by other
+  // ranks; compaction buffers of the remote requests
+  cb_cache* rcache = nullptr;
+  uint32_t* r_ids = nullptr;
+  uint32_t* r_pos = nullptr;
+  const void** r_miss = nullptr;
+  void* r_rows = nullptr;
+  unsigned long long* r_n = nullptr;
+  uint64_t r_cap = 0, r_row_bytes = 0;
+  uint64_t r_last[3] = {0, 0, 0};  // last step: remote rows, hits, misses
   void* rstage = nullptr;
   uint64_t rstage_rows = 0;
   const unsigned char** d_rstage = nullptr;  // [kMaxParts] every rank's staging
@@ -216,6 +226,9 @@ struct PxState {
     drop_graphs();
     for (void* p : ropened) cudaIpcCloseMemHandle(p);
     if (rstage) cudaFree(rstage);
+    for (void* p : {static_cast<void*>(r_ids), static_cast<void*>(r_pos),
+                    static_cast<void*>(r_miss), r_rows, static_cast<void*>(r_n)})
+      if (p) cudaFree(p);
     if (d_rstage) cudaFree(d_rstage);
     if (bar_ctr) cudaFree(bar_ctr);
     for (void* p : opened) cudaIpcCloseMemHandle(p);

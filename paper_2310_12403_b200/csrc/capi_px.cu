@@ -166,6 +166,10 @@ void px_enqueue_step(cb_plan* plan, uint64_t n_seeds, bool smooth, uint64_t c0,
   }
 }
 
+// access order key of the requester cache (a different stream than the
+// owner's, so the two caches see independent orders)
+uint64_t requester_key(uint64_t order_key) { return cbdev::hstep(order_key, 0x5245515545ULL); }
+
 void require_staging(const PxState& px) {
   require(px.rstage != nullptr, "no staging buffer (cb_px_setup_staging)");
   for (uint32_t q = 0; q < px.world; ++q)
@@ -600,6 +604,32 @@ int cb_px_set_cache(cb_plan* plan, cb_cache* cache) {
   });
 }
 
+int cb_px_set_requester_cache(cb_plan* plan, cb_cache* cache) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    PxState& px = px_of(plan);
+    if (cache) {
+      require(px.stage_store != nullptr, "call cb_px_setup_staging first");
+      require(cache->lru->row_bytes() == px.stage_store->row_bytes,
+              "cache row size does not match the feature table");
+      require(cache->lru->n_keys() >= plan->g->g.n, "cache key space smaller than the graph");
+      require(cache != px.cache, "the requester cache must differ from the owner cache");
+    }
+    px.rcache = cache;
+  });
+}
+
+int cb_px_requester_stats(const cb_plan* plan, uint64_t* remote, uint64_t* hits,
+                          uint64_t* misses) {
+  return guard([&] {
+    require(plan != nullptr && plan->px != nullptr, "peer exchange not set up");
+    const PxState& px = *plan->px;
+    if (remote) *remote = px.r_last[0];
+    if (hits) *hits = px.r_last[1];
+    if (misses) *misses = px.r_last[2];
+  });
+}
+
 int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint64_t* hits,
                         uint64_t* misses) {
   NvtxRange nvtx_("cb.px_gather_cached");
@@ -627,9 +657,48 @@ int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint
     // next step's staging comes after that step's barriers, which no rank
     // reaches before finishing this pull
     launch_px_barrier(px.bar, plan->stream);
-    launch_px_gather_staged(px.d_rstage, w.loc_part[L - 1], w.loc_row[L - 1],
-                            px.stage_store->row_bytes, &plan->meta_at(0, L - 1)->n_src,
-                            w.cap_rows, w.rows, plan->stream);
+    const uint64_t rb = px.stage_store->row_bytes;
+    if (!px.rcache) {
+      launch_px_gather_staged(px.d_rstage, w.loc_part[L - 1], w.loc_row[L - 1], rb,
+                              &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows,
+                              plan->stream);
+    } else {
+      // requester side: own rows from the own staging buffer; rows owned by
+      // other ranks through this rank's LRU in access_order(R, order_key ^
+      // requester tag) -- hits from its HBM rows, misses pulled from the
+      // owners' staging buffers over peer memory, then placed requester-aligned
+      if (px.r_cap < w.cap_rows || px.r_row_bytes != rb) {
+        for (void* p : {static_cast<void*>(px.r_ids), static_cast<void*>(px.r_pos),
+                        static_cast<void*>(px.r_miss), px.r_rows})
+          if (p) CB_CUDA(cudaFree(p));
+        px.r_cap = std::max<uint64_t>(w.cap_rows, 1);
+        px.r_row_bytes = rb;
+        CB_CUDA(cudaMalloc(&px.r_ids, px.r_cap * 4));
+        CB_CUDA(cudaMalloc(&px.r_pos, px.r_cap * 4));
+        CB_CUDA(cudaMalloc(&px.r_miss, px.r_cap * sizeof(void*)));
+        CB_CUDA(cudaMalloc(&px.r_rows, px.r_cap * rb));
+        if (!px.r_n) CB_CUDA(cudaMalloc(&px.r_n, 8));
+      }
+      launch_px_split_remote(w.L[L - 1].src, &plan->meta_at(0, L - 1)->n_src, w.cap_rows,
+                             w.loc_part[L - 1], w.loc_row[L - 1], px.rank, px.d_rstage, rb,
+                             px.r_ids, px.r_pos, px.r_miss, px.r_n, plan->stream);
+      launch_px_gather_staged_local(px.d_rstage, w.loc_part[L - 1], w.loc_row[L - 1], rb,
+                                    &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, px.rank,
+                                    plan->stream);
+      unsigned long long nr = 0;
+      CB_CUDA(cudaMemcpyAsync(&nr, px.r_n, 8, cudaMemcpyDeviceToHost, plan->stream));
+      CB_CUDA(cudaStreamSynchronize(plan->stream));
+      DeviceLru& rl = *px.rcache->lru;
+      const uint64_t rh0 = rl.hits(), rm0 = rl.misses();
+      CacheGatherSrc rs;
+      rs.miss_ptr = px.r_miss;
+      rs.rows_out = px.r_rows;
+      rl.access_ids(px.r_ids, nr, requester_key(order_key), nullptr, 0, rs, plan->stream);
+      launch_px_scatter_rows(px.r_rows, px.r_pos, nr, rb, w.rows, plan->stream);
+      px.r_last[0] = nr;
+      px.r_last[1] = rl.hits() - rh0;
+      px.r_last[2] = rl.misses() - rm0;
+    }
     plan->have_rows = true;
     if (owned) *owned = n_own;
     if (hits) *hits = lru.hits() - h0;

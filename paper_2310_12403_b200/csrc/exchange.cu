@@ -146,7 +146,7 @@ __global__ void px_gather_staged_kernel(const unsigned char* const* __restrict__
                                         const uint32_t* __restrict__ loc_row, uint32_t vpr,
                                         uint64_t row_bytes,
                                         const unsigned long long* __restrict__ count,
-                                        uint64_t cap, V* __restrict__ out) {
+                                        uint64_t cap, V* __restrict__ out, uint32_t only_rank) {
   pdl_begin();
   const uint64_t n = min(static_cast<uint64_t>(*count), cap);
   const uint64_t total = n * vpr;
@@ -162,9 +162,11 @@ __global__ void px_gather_staged_kernel(const unsigned char* const* __restrict__
       srcp[u] = nullptr;
       if (x < total) {
         const uint64_t r = x / vpr, c = x - r * vpr;
-        srcp[u] = reinterpret_cast<const V*>(bases[__ldg(loc_part + r)] +
-                                             static_cast<uint64_t>(__ldg(loc_row + r)) *
-                                                 row_bytes) + c;
+        const uint32_t q = __ldg(loc_part + r);
+        if (only_rank == ~0u || q == only_rank)
+          srcp[u] = reinterpret_cast<const V*>(bases[q] +
+                                               static_cast<uint64_t>(__ldg(loc_row + r)) *
+                                                   row_bytes) + c;
       }
     }
 #pragma unroll
@@ -286,10 +288,10 @@ void launch_px_gather(const unsigned char* const* d_bases, const uint32_t* owner
   CB_LAUNCH("px_gather");
 }
 
-void launch_px_gather_staged(const unsigned char* const* d_bases, const uint32_t* loc_part,
-                             const uint32_t* loc_row, uint64_t row_bytes,
-                             const unsigned long long* count, uint64_t cap, void* out,
-                             cudaStream_t st) {
+namespace {
+void staged(const unsigned char* const* d_bases, const uint32_t* loc_part, const uint32_t* loc_row,
+            uint64_t row_bytes, const unsigned long long* count, uint64_t cap, void* out,
+            uint32_t only_rank, cudaStream_t st) {
   int vb = 16;
   while (row_bytes % vb) vb >>= 1;
   const uint32_t vpr = static_cast<uint32_t>(row_bytes / vb);
@@ -297,21 +299,116 @@ void launch_px_gather_staged(const unsigned char* const* d_bases, const uint32_t
   switch (vb) {
     case 16:
       launch_k(px_gather_staged_kernel<uint4>, grid, 256, st, d_bases, loc_part, loc_row, vpr,
-               row_bytes, count, cap, static_cast<uint4*>(out));
+               row_bytes, count, cap, static_cast<uint4*>(out), only_rank);
       break;
     case 8:
       launch_k(px_gather_staged_kernel<uint2>, grid, 256, st, d_bases, loc_part, loc_row, vpr,
-               row_bytes, count, cap, static_cast<uint2*>(out));
+               row_bytes, count, cap, static_cast<uint2*>(out), only_rank);
       break;
     case 4:
       launch_k(px_gather_staged_kernel<uint32_t>, grid, 256, st, d_bases, loc_part, loc_row,
-               vpr, row_bytes, count, cap, static_cast<uint32_t*>(out));
+               vpr, row_bytes, count, cap, static_cast<uint32_t*>(out), only_rank);
       break;
     default:
       launch_k(px_gather_staged_kernel<unsigned short>, grid, 256, st, d_bases, loc_part,
-               loc_row, vpr, row_bytes, count, cap, static_cast<unsigned short*>(out));
+               loc_row, vpr, row_bytes, count, cap, static_cast<unsigned short*>(out),
+               only_rank);
   }
   CB_LAUNCH("px_gather_staged");
+}
+
+__global__ void px_split_remote_kernel(const uint32_t* __restrict__ src,
+                                       const unsigned long long* __restrict__ count, uint64_t cap,
+                                       const uint32_t* __restrict__ loc_part,
+                                       const uint32_t* __restrict__ loc_row, uint32_t rank,
+                                       const unsigned char* const* __restrict__ bases,
+                                       uint64_t row_bytes, uint32_t* ids, uint32_t* pos,
+                                       const void** miss_ptr, unsigned long long* n_remote) {
+  pdl_begin();
+  const uint64_t n = min(static_cast<uint64_t>(*count), cap);
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t q = loc_part[j];
+    const bool remote = q != rank;
+    const unsigned m = __ballot_sync(__activemask(), remote);
+    if (!m) continue;
+    unsigned long long base = 0;
+    const unsigned leader = __ffs(m) - 1;
+    if (lane_id() == leader) base = atomicAdd(n_remote, static_cast<unsigned long long>(__popc(m)));
+    base = __shfl_sync(__activemask(), base, leader);
+    if (remote) {
+      const uint64_t k = base + __popc(m & ((1u << lane_id()) - 1u));
+      ids[k] = src[j];
+      pos[k] = static_cast<uint32_t>(j);
+      miss_ptr[k] = bases[q] + static_cast<uint64_t>(loc_row[j]) * row_bytes;
+    }
+  }
+}
+
+template <typename V>
+__global__ void px_scatter_rows_kernel(const V* __restrict__ rows, const uint32_t* __restrict__ pos,
+                                       uint64_t n, uint32_t vpr, V* __restrict__ out) {
+  pdl_begin();
+  const uint64_t total = n * vpr;
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = x / vpr, c = x - k * vpr;
+    out[static_cast<uint64_t>(pos[k]) * vpr + c] = rows[x];
+  }
+}
+}  // namespace
+
+void launch_px_gather_staged(const unsigned char* const* d_bases, const uint32_t* loc_part,
+                             const uint32_t* loc_row, uint64_t row_bytes,
+                             const unsigned long long* count, uint64_t cap, void* out,
+                             cudaStream_t st) {
+  staged(d_bases, loc_part, loc_row, row_bytes, count, cap, out, ~0u, st);
+}
+
+void launch_px_gather_staged_local(const unsigned char* const* d_bases, const uint32_t* loc_part,
+                                   const uint32_t* loc_row, uint64_t row_bytes,
+                                   const unsigned long long* count, uint64_t cap, void* out,
+                                   uint32_t rank, cudaStream_t st) {
+  staged(d_bases, loc_part, loc_row, row_bytes, count, cap, out, rank, st);
+}
+
+void launch_px_split_remote(const uint32_t* src, const unsigned long long* count, uint64_t cap,
+                            const uint32_t* loc_part, const uint32_t* loc_row, uint32_t rank,
+                            const unsigned char* const* d_bases, uint64_t row_bytes,
+                            uint32_t* ids, uint32_t* pos, const void** miss_ptr,
+                            unsigned long long* n_remote, cudaStream_t st) {
+  cuda_check(cudaMemsetAsync(n_remote, 0, 8, st), "cudaMemsetAsync");
+  launch_k(px_split_remote_kernel, grid_for(cap, 256, 8), 256, st, src, count, cap, loc_part,
+           loc_row, rank, d_bases, row_bytes, ids, pos, miss_ptr, n_remote);
+  CB_LAUNCH("px_split_remote");
+}
+
+void launch_px_scatter_rows(const void* rows, const uint32_t* pos, uint64_t n, uint64_t row_bytes,
+                            void* out, cudaStream_t st) {
+  if (n == 0) return;
+  int vb = 16;
+  while (row_bytes % vb) vb >>= 1;
+  const uint32_t vpr = static_cast<uint32_t>(row_bytes / vb);
+  const unsigned grid = grid_for(n * vpr, 256, 8);
+  switch (vb) {
+    case 16:
+      launch_k(px_scatter_rows_kernel<uint4>, grid, 256, st, static_cast<const uint4*>(rows), pos,
+               n, vpr, static_cast<uint4*>(out));
+      break;
+    case 8:
+      launch_k(px_scatter_rows_kernel<uint2>, grid, 256, st, static_cast<const uint2*>(rows), pos,
+               n, vpr, static_cast<uint2*>(out));
+      break;
+    case 4:
+      launch_k(px_scatter_rows_kernel<uint32_t>, grid, 256, st,
+               static_cast<const uint32_t*>(rows), pos, n, vpr, static_cast<uint32_t*>(out));
+      break;
+    default:
+      launch_k(px_scatter_rows_kernel<unsigned short>, grid, 256, st,
+               static_cast<const unsigned short*>(rows), pos, n, vpr,
+               static_cast<unsigned short*>(out));
+  }
+  CB_LAUNCH("px_scatter_rows");
 }
 
 void launch_route(const PartPtrs& pp, const uint32_t* owner, uint32_t P,

@@ -73,6 +73,23 @@ void launch_px_gather_staged(const unsigned char* const* d_bases, const uint32_t
                              const unsigned long long* count, uint64_t cap, void* out,
                              cudaStream_t st);
 
+// Requester-side cache support: the requested rows owned by OTHER ranks,
+// compacted (any order): ids[k], their positions pos[k] in the request list
+// and the address of their row in the owner's staging buffer (miss_ptr[k]);
+// *n_remote counts them. skip_rank >= 0 in the staged pull leaves those
+// positions alone (they come from the requester cache instead).
+void launch_px_split_remote(const uint32_t* src, const unsigned long long* count, uint64_t cap,
+                            const uint32_t* loc_part, const uint32_t* loc_row, uint32_t rank,
+                            const unsigned char* const* d_bases, uint64_t row_bytes,
+                            uint32_t* ids, uint32_t* pos, const void** miss_ptr,
+                            unsigned long long* n_remote, cudaStream_t st);
+void launch_px_scatter_rows(const void* rows, const uint32_t* pos, uint64_t n, uint64_t row_bytes,
+                            void* out, cudaStream_t st);
+void launch_px_gather_staged_local(const unsigned char* const* d_bases, const uint32_t* loc_part,
+                                   const uint32_t* loc_row, uint64_t row_bytes,
+                                   const unsigned long long* count, uint64_t cap, void* out,
+                                   uint32_t rank, cudaStream_t st);
+
 void launch_route(const PartPtrs& pp, const uint32_t* owner, uint32_t P,
                   unsigned long long* send_counts, uint64_t max_src, cudaStream_t st);
 void launch_locate(const PartPtrs& pp, const uint32_t* owner, uint32_t P, uint64_t max_src,

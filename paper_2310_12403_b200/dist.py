@@ -385,15 +385,28 @@ class PeerCoop:
             ptr, on_dev = self._seeds.ctypes.data, 0
         _check(self.L.cb_px_replay(self._h, C.c_void_p(ptr), on_dev, C.byref(schedule._c())))
 
-    def enable_cache(self, capacity: int):
+    def enable_cache(self, capacity: int, requester_capacity: int = 0):
         """Owner-side LRU cache of `capacity` rows (HBM) in front of this rank's
-        shard (cb_px_setup_cache): see load_inputs_cached."""
+        shard (cb_px_set_cache) and, with requester_capacity > 0, a
+        requester-side LRU for the rows other ranks own (only its misses cross
+        NVLink; cb_px_set_requester_cache): see load_inputs_cached."""
         from .cache import LruCache
         if self.store is None:
             raise ValueError("PeerCoop.enable_cache needs the rank's feature shard")
         self.cache = LruCache(capacity, self.g.num_vertices, self.g.device,
                               row_bytes=self.store.row_bytes)
         _check(self.L.cb_px_set_cache(self._h, self.cache._h))
+        self.rcache = None
+        if requester_capacity > 0:
+            self.rcache = LruCache(requester_capacity, self.g.num_vertices, self.g.device,
+                                   row_bytes=self.store.row_bytes)
+            _check(self.L.cb_px_set_requester_cache(self._h, self.rcache._h))
+
+    def requester_stats(self) -> tuple[int, int, int]:
+        """Last cached fetch, requester side: (remote rows, hits, misses)."""
+        r, h, m = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(self.L.cb_px_requester_stats(self._h, C.byref(r), C.byref(h), C.byref(m)))
+        return r.value, h.value, m.value
 
     def load_inputs_cached(self, order_key: int) -> tuple[int, int, int]:
         """The owner-side cached fetch of this step (cb_px_gather_cached): this

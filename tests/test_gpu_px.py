@@ -122,7 +122,7 @@ def test_peer_coop_nccl_single_rank(gpu):
     assert p.exitcode == 0
 
 
-def _px_cache_worker(rank, world, kappa, steps, captured, host_tier):
+def _px_cache_worker(rank, world, kappa, steps, captured, host_tier, rcap=0):
     import paper_2310_12403_b200 as cb
     from oracle import oracle as O
     from paper_2310_12403_b200.dist import PeerCoop, synth_shard
@@ -139,8 +139,9 @@ def _px_cache_worker(rank, world, kappa, steps, captured, host_tier):
     pc = PeerCoop(g, pm, rank, L, cfg, max_seeds=4096, store=store)
     if host_tier:
         store.set_tier(True)  # misses cross the host link (the storage channel)
-    pc.enable_cache(cap)
+    pc.enable_cache(cap, rcap)
     lru = O.Lru(cap, impl="reference")  # the reference's LruCache, this owner's
+    rlru = O.Lru(rcap, impl="reference") if rcap else None  # this requester's
     sched = cb.SeedSchedule.make(kappa, 8)
     # dependent minibatches: the same seeds every step, drifting variates
     seeds = O.draw_coop_seeds(owner, world, 96, 6, 0)
@@ -163,18 +164,32 @@ def _px_cache_worker(rank, world, kappa, steps, captured, host_tier):
         assert owned == len(own) and misses == want_m and hits == len(own) - want_m, \
             (step, owned, hits, misses, len(own), want_m)
         total_h += hits
+        if rlru is not None:  # rows of other owners through this requester's LRU
+            src = exp["stacks"][rank][L - 1]["src"]
+            remote = src[owner[src] != rank]
+            rkey = cb.mix64(key ^ 0x5245515545)  # hstep(order_key, "REQUE")
+            want_rm = sum(rlru.access(int(v)) for v in O.access_order(remote, rkey))
+            nr, rh, rm = pc.requester_stats()
+            assert nr == len(remote) and rm == want_rm and rh == nr - rm, \
+                (step, nr, rh, rm, len(remote), want_rm)
+            total_h += rh
         sched = cb.schedule_advance(sched)
     assert total_h > 0  # the dependent batches did reuse rows
 
 
-@pytest.mark.parametrize("world,kappa,steps,captured,host_tier", [
-    (2, 4, 5, False, False),
-    (3, 16, 4, True, True),
+@pytest.mark.parametrize("world,kappa,steps,captured,host_tier,rcap", [
+    (2, 4, 5, False, False, 0),
+    (3, 16, 4, True, True, 0),
+    (2, 4, 5, True, False, 400),   # + requester-side cache
+    (3, 64, 4, False, True, 300),
 ])
-def test_peer_coop_owner_cache(gpu, world, kappa, steps, captured, host_tier):
+def test_peer_coop_owner_cache(gpu, world, kappa, steps, captured, host_tier, rcap):
     """The owner-side cached fetch: per step each owner's set goes through its
     LRU (hits/misses equal the reference LruCache fed access_order(S^L_q,
     hash_bits(step, {q})), feature_load_sim's loop, cache.cpp:100-110) and
     every rank's rows, pulled from the owners' staged rows, equal the
-    oracle's -- with the shard in HBM or in the pinned host tier."""
-    spawn(world, _px_cache_worker, (kappa, steps, captured, host_tier), timeout=600)
+    oracle's -- with the shard in HBM or in the pinned host tier. With a
+    requester-side cache the rows other ranks own go through a second LRU
+    (the reference LruCache fed access_order(remote, hstep(key, tag)) must
+    agree) and only its misses are pulled over peer memory."""
+    spawn(world, _px_cache_worker, (kappa, steps, captured, host_tier, rcap), timeout=600)

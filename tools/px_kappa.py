@@ -7,7 +7,9 @@ per kappa, the steady (second-epoch) miss rate, storage bytes per step (owner
 cache misses x row bytes, the host link) and peer bytes per step (rows pulled
 from other ranks' staging buffers). Run under torchrun (gloo; ranks may share
 cuda:0 under MPS):
-  torchrun --nproc-per-node 2 tools/px_kappa.py c2 [epochs] [batch]"""
+  torchrun --nproc-per-node 2 tools/px_kappa.py c3 [epochs] [batch] [requester_cache_rows]
+With requester_cache_rows > 0 the rows other ranks own go through a second,
+requester-side LRU and only its misses cross peer memory."""
 import ctypes as C
 import json
 import os
@@ -26,6 +28,7 @@ from paper_2310_12403_b200.dist import PeerCoop, synth_shard  # noqa: E402
 cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 b = int(sys.argv[3]) if len(sys.argv) > 3 else cfg["batch"]
+rcap = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 dist.init_process_group("gloo")
 rank, world = dist.get_rank(), dist.get_world_size()
 torch.cuda.set_device(0)
@@ -41,13 +44,14 @@ L = len(cfg["fanouts"])
 scfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, fanouts=cfg["fanouts"])
 out = {"workload": cfg["workload"], "world": world, "batch_per_rank": b,
        "steps_per_epoch": spe, "epochs": epochs, "cache_rows_per_rank": cap,
+       "requester_cache_rows_per_rank": rcap,
        "feature_tier": "shards in pinned host memory; cache rows in HBM", "sweep": []}
 for kappa in (1, 4, 16, 64, 256, None):
     k = cb.KAPPA_INFINITY if kappa is None else kappa
     store = synth_shard(g, pm, rank, cfg["dim"], bench.FEAT_SEED, cfg["dtype"])
     pc = PeerCoop(g, pm, rank, L, scfg, max_seeds=b, store=store)
     store.set_tier(True)
-    pc.enable_cache(cap)
+    pc.enable_cache(cap, rcap)
     sched = cb.SeedSchedule.make(k, bench.RUN_SEED)
     pc.sample(order[:b], sched)
     pc.load_inputs()
@@ -69,7 +73,11 @@ for kappa in (1, 4, 16, 64, 256, None):
             acc["acc"] += owned
             acc["miss"] += misses
             acc["rows"] += n_src.value
-            acc["peer_rows"] += int(np.count_nonzero(lp[:n_src.value] != rank))
+            if rcap:
+                _, _, rmiss = pc.requester_stats()
+                acc["peer_rows"] += rmiss  # only requester-cache misses cross
+            else:
+                acc["peer_rows"] += int(np.count_nonzero(lp[:n_src.value] != rank))
         sched = cb.schedule_advance(sched)
     pc.finish()
     dt = time.perf_counter() - t0
