@@ -680,6 +680,15 @@ constexpr int kMarkRecs = CB_MARK_RECS;
 #ifndef CB_PURE_GRAB
 #define CB_PURE_GRAB 0
 #endif
+// phase B (tiles with record boundaries): one warp per tile without CTA
+// barriers once there are at least CB_MIXED_WARP_MIN tiles per warp of the
+// grid, else CTA-cooperative tiles (staged records, a barrier per tile).
+// A/B at c4: 134 -> 129 us/step in warp mode; the small early layers keep the
+// shorter CTA path (layer-0 mark 16 vs 34 us).
+#ifndef CB_MIXED_WARP_MIN
+#define CB_MIXED_WARP_MIN 1
+#endif
+constexpr int kMixedWarpMin = CB_MIXED_WARP_MIN;
 
 constexpr int kPureStages = CB_PURE_STAGES;     // id tiles in flight per warp
 constexpr uint32_t kPureStride = kLaborTile + 8;  // u32 per ring stage (alignment slack)
@@ -832,6 +841,63 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
   }
 }
 
+// Phase B by warps (CB_MIXED_WARP): each warp takes whole tiles with record
+// boundaries (warp gw: the back of the list, entries gw, gw + W, ...), stages
+// the tile's records in its own shared memory (the phase-A ring of the same
+// warp, so neither phase waits for the CTA) and marks the tile as four spans
+// of 32 * IPT positions (mark_span). No CTA barrier anywhere.
+template <int IPT>
+__device__ __forceinline__ void mark_mixed_warp(const LaborArgs& a, const Variates& v,
+                                                uint64_t p1, uint64_t n_mixed, uint64_t total,
+                                                unsigned role, unsigned ncta, ActRec* wrec) {
+  constexpr uint32_t TILE = kLaborTile;
+  constexpr uint32_t WSPAN = 32 * IPT;
+  constexpr uint32_t WPC = kMarkNT / 32;
+  constexpr uint32_t kRecsW = (kPureStride * 4) / sizeof(ActRec);
+  const uint32_t lane = lane_id();
+  const uint64_t W = static_cast<uint64_t>(ncta) * WPC;
+  const uint64_t gw = static_cast<uint64_t>(role) * WPC + (threadIdx.x >> 5);
+  unsigned long long uncert = 0;
+  for (uint64_t e = gw; e < n_mixed; e += W) {
+    const uint64_t tile = a.tile_list[a.list_cap - 1 - e].x;
+    const uint64_t x0 = tile * TILE;
+    const uint32_t rend = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE), total - x0));
+    uint32_t a0, a1;
+    tile_records(a.act, a.tile_first, 0, tile, 0, a0, a1);
+    const uint32_t nd = a1 - a0 + 1;
+    const bool staged = nd <= kRecsW;
+    __syncwarp();  // every lane is done with the previous tile's records
+    if (staged) {
+      const uint4* src = reinterpret_cast<const uint4*>(a.act + a0);
+      uint4* dst = reinterpret_cast<uint4*>(wrec);
+      for (uint32_t i = lane; i < 2 * nd; i += 32) dst[i] = __ldg(src + i);
+      __syncwarp();
+    }
+    for (uint32_t r0 = 0; r0 < rend; r0 += WSPAN) {
+      if (staged) {
+        // record of the span's first position: 32-ary search over the starts
+        uint32_t lo = 0, hi = nd - 1;
+        while (lo < hi) {
+          const uint32_t step = (hi - lo + 32) / 32;
+          const uint32_t cand = lo + lane * step;
+          const bool le = cand <= hi && wrec[cand].pre <= x0 + r0;
+          const unsigned m = __ballot_sync(0xffffffffu, le);
+          const uint32_t best = lo + (31 - __clz(m)) * step;
+          lo = best;
+          hi = min(hi, best + step - 1);
+          if (step == 1) break;
+        }
+        mark_span<IPT, false, true>(a, v, p1, 0, x0, r0, rend, a0, a1, lo, wrec, nd, uncert,
+                                    nullptr);
+      } else {
+        const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
+        mark_span<IPT, false, false>(a, v, p1, 0, x0, r0, rend, a0, a1, cur, nullptr, 0, uncert,
+                                     nullptr);
+      }
+    }
+  }
+}
+
 // labor_mark: tiles of kNT*IPT scan positions, one 32*IPT span per warp.
 // Plain stream: phase A (mark_pure) first takes the full single-record tiles;
 // phase B then runs the tiles with record boundaries (or a partial last tile),
@@ -874,6 +940,15 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
     n_mixed = min(static_cast<uint64_t>(a.list_ctr[1]), ntiles - n_pure);
     MarkSmemA& sa = *reinterpret_cast<MarkSmemA*>(s_raw);
     mark_pure<kPureStages>(a, p1, n_pure, role, ncta, &sa.ring[warp][0][0], s_rbar[warp]);
+    // many mixed tiles (every warp gets one or more): one warp per tile, no
+    // CTA barriers; few (small layers): four warps per tile, shorter path
+    if (n_mixed >= static_cast<uint64_t>(kMixedWarpMin) * ncta * WPC) {
+      tstamp(a.trace, role, 2);
+      mark_mixed_warp<IPT>(a, v, p1, n_mixed, total, role, ncta,
+                           reinterpret_cast<ActRec*>(&sa.ring[warp][0][0]));
+      tstamp(a.trace, role, 1);
+      return;
+    }
     __syncthreads();  // the ring memory becomes phase B's
     tstamp(a.trace, role, 2);
   }
