@@ -681,14 +681,14 @@ constexpr int kMarkRecs = CB_MARK_RECS;
 #define CB_PURE_GRAB 0
 #endif
 // phase B (tiles with record boundaries): one warp per tile without CTA
-// barriers once there are at least CB_MIXED_WARP_MIN tiles per warp of the
+// barriers once there is at least one tile per CB_MIXED_WARP_DIV warps of the
 // grid, else CTA-cooperative tiles (staged records, a barrier per tile).
 // A/B at c4: 134 -> 129 us/step in warp mode; the small early layers keep the
 // shorter CTA path (layer-0 mark 16 vs 34 us).
-#ifndef CB_MIXED_WARP_MIN
-#define CB_MIXED_WARP_MIN 1
+#ifndef CB_MIXED_WARP_DIV
+#define CB_MIXED_WARP_DIV 1
 #endif
-constexpr int kMixedWarpMin = CB_MIXED_WARP_MIN;
+constexpr int kMixedWarpDiv = CB_MIXED_WARP_DIV;
 
 constexpr int kPureStages = CB_PURE_STAGES;     // id tiles in flight per warp
 constexpr uint32_t kPureStride = kLaborTile + 8;  // u32 per ring stage (alignment slack)
@@ -942,7 +942,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
     mark_pure<kPureStages>(a, p1, n_pure, role, ncta, &sa.ring[warp][0][0], s_rbar[warp]);
     // many mixed tiles (every warp gets one or more): one warp per tile, no
     // CTA barriers; few (small layers): four warps per tile, shorter path
-    if (n_mixed >= static_cast<uint64_t>(kMixedWarpMin) * ncta * WPC) {
+    if (n_mixed * kMixedWarpDiv >= static_cast<uint64_t>(ncta) * WPC) {
       tstamp(a.trace, role, 2);
       mark_mixed_warp<IPT>(a, v, p1, n_mixed, total, role, ncta,
                            reinterpret_cast<ActRec*>(&sa.ring[warp][0][0]));
