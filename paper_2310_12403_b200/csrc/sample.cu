@@ -192,6 +192,35 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
     // (mixed), to the back. A hub starts hundreds of tiles: the whole warp
     // writes each record's tiles, one record after another.
     const bool lists = a.tile_list != nullptr;
+    // list slots for all IPT records of a thread: one warp scan and one
+    // atomic per list per warp (not per record), so the loop below does not
+    // wait on an atomic round trip per j
+    uint32_t bp = 0, bm = 0;
+    if (lists) {
+      uint32_t tnp = 0, tmix = 0;
+      uint64_t e2 = eq;
+#pragma unroll
+      for (int j = 0; j < IPT; ++j) {
+        if (i0 + j < n && q[j] > 0) {
+          const uint64_t f = (e2 + kLaborTile - 1) / kLaborTile;
+          const uint64_t l = min(static_cast<uint64_t>((e2 + q[j] - 1) / kLaborTile), a.cap_tiles);
+          const uint64_t p = min(l + 1, static_cast<uint64_t>((e2 + q[j]) / kLaborTile));
+          if (f <= l) {
+            tnp += p > f ? static_cast<uint32_t>(p - f) : 0u;
+            tmix += (l + 1 > p) ? 1u : 0u;
+          }
+        }
+        e2 += q[j];
+      }
+      const uint32_t ip = warp_inclusive_scan(tnp), im2 = warp_inclusive_scan(tmix);
+      uint32_t base_p = 0, base_m = 0;
+      if (lane_id() == 31) {
+        if (ip) base_p = atomicAdd(&a.list_ctr[0], ip);
+        if (im2) base_m = atomicAdd(&a.list_ctr[1], im2);
+      }
+      bp = __shfl_sync(0xffffffffu, base_p, 31) + ip - tnp;
+      bm = __shfl_sync(0xffffffffu, base_m, 31) + im2 - tmix;
+    }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const uint64_t i = i0 + j;
@@ -239,29 +268,12 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
       }
       eq += q[j];
       eo += o[j];
-      // list slots: one atomic per warp and list for this j
+      // this record's list slots: pure tiles from bp, its mixed tile at bm
       const bool any = tf <= tl;
       const uint32_t np = (lists && any && pe > tf) ? static_cast<uint32_t>(pe - tf) : 0u;
       const bool mixed = lists && any && tl + 1 > pe;
-      uint32_t bp = 0, bm = 0;
-      if (lists) {
-        uint32_t ip = np;
-#pragma unroll
-        for (int o2 = 1; o2 < 32; o2 <<= 1) {
-          const uint32_t x = __shfl_up_sync(0xffffffffu, ip, o2);
-          if (lane_id() >= static_cast<unsigned>(o2)) ip += x;
-        }
-        const unsigned mm = __ballot_sync(0xffffffffu, mixed);
-        uint32_t base_p = 0, base_m = 0;
-        if (lane_id() == 31) {
-          if (ip) base_p = atomicAdd(&a.list_ctr[0], ip);
-          if (mm) base_m = atomicAdd(&a.list_ctr[1], static_cast<unsigned>(__popc(mm)));
-        }
-        bp = __shfl_sync(0xffffffffu, base_p, 31) + ip - np;
-        bm = __shfl_sync(0xffffffffu, base_m, 31) + __popc(mm & ((1u << lane_id()) - 1u));
-        if (mixed && bm < a.list_cap)
-          a.tile_list[a.list_cap - 1 - bm] = make_uint2(static_cast<uint32_t>(tl), rec_idx);
-      }
+      if (mixed && bm < a.list_cap)
+        a.tile_list[a.list_cap - 1 - bm] = make_uint2(static_cast<uint32_t>(tl), rec_idx);
       // a record that starts a few tiles writes them itself; hubs (many
       // tiles) are written by the whole warp
       const bool coop = any && tl >= tf + 4;
@@ -288,6 +300,8 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
             a.tile_list[b2 + (t - f)] = make_uint2(static_cast<uint32_t>(t), r2);
         }
       }
+      bp += np;
+      bm += mixed ? 1u : 0u;
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       uint64_t tot = bq + tq, nact = ba + ta;

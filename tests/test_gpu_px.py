@@ -61,6 +61,7 @@ def test_peer_coop(gpu, world, kind, fanouts, kappa, steps, barrier):
     (3, 2, [25, 15], 4, 4),       # even L, smoothed variates
     (2, 1, [10, 5, 5], 1, 3),     # NS
     (2, 2, [10], 1, 6),           # L = 1: four graphs before the slots realign
+    (4, 2, [10, 10], 4, 3),       # four ranks
 ])
 def test_peer_coop_captured(gpu, world, kind, fanouts, kappa, steps):
     """The whole cooperative step captured as one CUDA graph per rank (device
