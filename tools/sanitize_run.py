@@ -39,4 +39,32 @@ cache.access_trace(rng.integers(0, n, 2000).astype(np.uint32))
 f64 = cb.FeatureStore.synth(g, 6, 1, "f64", pm)
 model = cb.GcnModel.init(6, 5, 4, 2, 2)
 cb.coop_train_step(g, pm, per, 2, cfg, cb.SeedSchedule.plain(3), model, f64, 4)
+# labor_mark phase A (single-record hub tiles by bulk copy) and phase B: a
+# hub with 6000 in-neighbours among ordinary vertices
+nh = 8000
+src = [np.arange(1, 6001, dtype=np.uint32)]
+dst = [np.zeros(6000, np.uint32)]
+src.append(rng.integers(0, nh, 40000).astype(np.uint32))
+dst.append(rng.integers(1, nh, 40000).astype(np.uint32))
+s_all, d_all = np.concatenate(src), np.concatenate(dst)
+order = np.lexsort((s_all, d_all))
+s_all, d_all = s_all[order], d_all[order]
+indptr = np.zeros(nh + 1, np.uint64)
+np.add.at(indptr, d_all.astype(np.int64) + 1, 1)
+indptr = np.cumsum(indptr).astype(np.uint64)
+gh = cb.Graph.from_csr(indptr, s_all)
+hseeds = np.concatenate([[0], rng.choice(np.arange(1, nh), 300, replace=False)]).astype(np.uint32)
+hp = cb.Plan(gh, None, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), len(hseeds))
+hp.sample([hseeds], cb.SeedSchedule.plain(5), cb.MODE_INDEP)
+# the batch result by the result kernel and by pack + copy-engine copy
+hs = cb.FeatureStore.synth(gh, 8, 1, "f16")
+hp.gather(hs)
+pin = torch.empty(8 << 20, dtype=torch.uint8).pin_memory()
+hp.result_async(pin.data_ptr(), pin.numel())
+hp.result_pack()
+hp.result_copy(pin.data_ptr(), pin.numel())
+hp.synchronize()
+# smoothed decisions in a forced guard band, resolved on the host (re-samples)
+hp.set_guard(1e-2, perturb=True)
+hp.sample([hseeds], cb.schedule_advance(cb.SeedSchedule.make(4, 9)), cb.MODE_INDEP)
 print("sanitize workload done")
