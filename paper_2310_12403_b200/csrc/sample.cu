@@ -749,6 +749,7 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
   }
   __syncwarp();
   uint32_t phase = 0;  // parity bit per stage
+  unsigned long long dbg_tiles = 0, dbg_surv = 0;  // trace diagnostics
 #if CB_PURE_GRAB > 0
   // dynamic split (build option): the warp takes CB_PURE_GRAB entries at a
   // time from the layer's phase-A ticket (zeroed by batch_begin). A/B at c4:
@@ -823,6 +824,8 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
       for (int j = 0; j < 32; ++j) cand = shift_in_pass(cand, b2, mix64_yhi_cs(yk, ids[32 * j]));
 #endif
       uint32_t km = __brev(cand);
+      ++dbg_tiles;
+      dbg_surv += __popc(km);
       for (uint32_t kk = km; kk;) {
         const int j = __ffs(kk) - 1;
         kk &= kk - 1;
@@ -851,6 +854,13 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
         im &= im - 1;
       }
       s = s + 1 == NS ? 0 : s + 1;
+    }
+  }
+  if (a.trace && role % 16 == 0 && (threadIdx.x >> 5) == 0) {  // diagnostics (CB_TRACE)
+    const unsigned long long s = warp_sum(dbg_surv);
+    if (lane == 0) {
+      a.trace[(role / 16) * 8 + 5] = dbg_tiles;
+      a.trace[(role / 16) * 8 + 6] = s;
     }
   }
 }
@@ -943,7 +953,8 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   const double* vtab = (SMOOTH && vtab_used(a, total)) ? a.vtab : nullptr;
   const uint32_t warp = threadIdx.x >> 5;
   unsigned long long uncert = 0;
-  tstamp(a.trace, role, 0);
+  const unsigned trole = (role % 16 == 0) ? role / 16 : 64u;  // trace: every 16th CTA
+  tstamp(a.trace, trole, 0);
   // ---- phase A (plain stream with the frontier's tile lists): the
   // single-record tiles, one warp each. Phase B: the tiles with record
   // boundaries (the back of the list), or every tile without lists.
@@ -957,14 +968,14 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
     // many mixed tiles (every warp gets one or more): one warp per tile, no
     // CTA barriers; few (small layers): four warps per tile, shorter path
     if (n_mixed * kMixedWarpDiv >= static_cast<uint64_t>(ncta) * WPC) {
-      tstamp(a.trace, role, 2);
+      tstamp(a.trace, trole, 2);
       mark_mixed_warp<IPT>(a, v, p1, n_mixed, total, role, ncta,
                            reinterpret_cast<ActRec*>(&sa.ring[warp][0][0]));
-      tstamp(a.trace, role, 1);
+      tstamp(a.trace, trole, 1);
       return;
     }
     __syncthreads();  // the ring memory becomes phase B's
-    tstamp(a.trace, role, 2);
+    tstamp(a.trace, trole, 2);
   }
   const uint64_t nb = listed ? (n_mixed > role ? (n_mixed - role + ncta - 1) / ncta : 0)
                              : (ntiles > role ? (ntiles - role + ncta - 1) / ncta : 0);
@@ -1100,7 +1111,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
     if (lane_id() == 0 && uncert) atomicAdd(&meta->uncertified, uncert);
   }
   __syncthreads();
-  tstamp(a.trace, role, 1);
+  tstamp(a.trace, trole, 1);
 }
 
 template <int IPT, bool SMOOTH>

@@ -26,15 +26,19 @@ for step in range(4):
 buf = np.zeros(32 * 64 * 8, np.uint64)
 assert _lib.load().cb_plan_trace(plan._h, buf.ctypes.data_as(C.c_void_p), len(buf)) == 0
 t = buf.reshape(32, 64, 8).astype(np.int64)
-t0 = t[t > 0].min()
+t0 = t[t > 10 ** 12].min()  # globaltimer stamps (the mark rows also carry counts)
 names = {0: "frontier0", 1: "mark0", 2: "post0", 3: "frontier1", 4: "mark1", 5: "post1",
          6: "frontier2", 7: "mark2", 8: "post2"}
-# mark stamps: 0 start, 2 end of phase A (single-record tiles), 1 end
+# mark stamps: 0 start, 2 end of phase A (single-record tiles), 1 end; mark
+# rows are every 16th CTA (row r = CTA 16 r)
 for k, nm in names.items():
     # post: CTAs 0-31 = extract roles, 32-63 = emit roles
-    for cta in (list(range(0, 64, 8)) if not nm.startswith("post") else
+    for cta in ((list(range(0, 64, 4)) if nm.startswith("mark") else list(range(0, 64, 8)))
+                if not nm.startswith("post") else
                 [0, 1, 2, 8, 16, 31, 32, 33, 34, 40, 48, 63]):
         row = t[k, cta]
         if row[0] == 0:
             continue
-        print(nm, cta, [round((x - t0) / 1000, 2) if x else None for x in row[:5]])
+        print(nm, cta, [round((x - t0) / 1000, 2) if x else None for x in row[:5]],
+              # mark: phase-A tiles and prefilter survivors of the row's warp 0
+              list(map(int, row[5:7])) if nm.startswith("mark") else "")
