@@ -687,13 +687,21 @@ def run_ours_coop(args, cfg):
         scheds.append(cb.schedule_advance(scheds[-1]))
     if args.exchange == "px":
         from paper_2310_12403_b200.dist import PeerCoop
-        pc = PeerCoop(g, pm, rank, L, scfg, max_seeds=b, store=store, barrier="device")
-        # one eager step on every rank (kernel attributes), then the whole step
-        # (L layers, device barriers on IPC flags, row pull) as one CUDA graph
-        pc.sample(seeds_dev[0], scheds[0])
-        pc.load_inputs()
-        pc.finish()
-        pc.capture(b, scheds[0])
+        # S cooperative steps in flight (--inflight, as at N=1): S independent
+        # PeerCoops, each with its own plan, exchange regions, barrier flags,
+        # stream and captured graphs; step i runs on pcs[i % S]
+        S = max(1, args.inflight)
+        pcs = []
+        for _ in range(S):
+            pc_ = PeerCoop(g, pm, rank, L, scfg, max_seeds=b, store=store, barrier="device")
+            # one eager step on every rank (kernel attributes), then the whole
+            # step (L layers, device barriers, row pull) as CUDA graphs
+            pc_.sample(seeds_dev[0], scheds[0])
+            pc_.load_inputs()
+            pc_.finish()
+            pc_.capture(b, scheds[0])
+            pcs.append(pc_)
+        pc = pcs[0]
         n_cap = C.c_uint64()
         from paper_2310_12403_b200.coopbatch import _check
         _check(_lib.load().cb_plan_captured_launches(pc._h, 4, C.byref(n_cap)))
@@ -703,9 +711,10 @@ def run_ours_coop(args, cfg):
         meta_pin = torch.empty((W + K, int(mb_.value)), dtype=torch.uint8).pin_memory()
 
         def step(i, seeds):
-            pc.step(seeds, scheds[i])
+            p_ = pcs[i % S]
+            p_.step(seeds, scheds[i])
             if not isinstance(seeds, torch.Tensor):  # e2e: the step's counts come back
-                _lib.load().cb_plan_meta_async(pc._h, C.c_void_p(meta_pin[i].data_ptr()), None)
+                _lib.load().cb_plan_meta_async(p_._h, C.c_void_p(meta_pin[i].data_ptr()), None)
             return 0  # row bytes read from the device after the timed loop
     else:
         eng = CudaEngine(g, pm, rank, L, scfg, max_seeds=b, store=store,
@@ -726,17 +735,24 @@ def run_ours_coop(args, cfg):
         _lib.load().cb_kernel_launches(C.byref(lc))
         l0 = lc.value
         px = args.exchange == "px"
-        if px and device_clock:  # CUDA events on the plan stream (the launching stream)
+        if px:  # CUDA events on a master stream every plan stream waits on / joins
+            master = torch.cuda.current_stream()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(pc.stream)
+            e0.record(master)
+            for p_ in pcs:
+                p_.stream.wait_event(e0)
         t = time.perf_counter()
         n_rows = 0
         for i in range(W, W + K):
             n_rows += step(i, seeds_of(i))
-        if px and device_clock:
-            e1.record(pc.stream)
         if px:
-            pc.finish()
+            for p_ in pcs:
+                ev_ = torch.cuda.Event()
+                ev_.record(p_.stream)
+                master.wait_event(ev_)
+            e1.record(master)
+            for p_ in pcs:
+                p_.finish()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t
         if px and device_clock:
@@ -753,8 +769,10 @@ def run_ours_coop(args, cfg):
         dt, row_bytes_total, launches = timed(lambda i: seeds_dev[i], device_clock=True)
     if args.exchange == "px":  # the last step's rows, times K
         nr = C.c_uint64()
-        _lib.load().cb_px_sizes(pc._h, L - 1, C.byref(nr), None)
-        row_bytes_total = nr.value * store.row_bytes * K
+        row_bytes_total = 0
+        for p_ in pcs:  # the last step of every in-flight slot, times K / S
+            _lib.load().cb_px_sizes(p_._h, L - 1, C.byref(nr), None)
+            row_bytes_total += nr.value * store.row_bytes * K / len(pcs)
     # e2e: host seeds (H2D inside each step), rows end on the device, the
     # step's per-layer counts read back into pinned memory (px) or the split
     # sizes read by the host-orchestrated exchange (a2a)
@@ -776,8 +794,10 @@ def run_ours_coop(args, cfg):
                        "wait); the whole step is one CUDA graph per rank)"
                        if args.exchange == "px" else
                        f"{backend} all-to-allv per layer + feature all-to-allv)"),
-                   "timing": ("CUDA events on the plan stream around K graph replays, max over "
-                              "ranks" if args.exchange == "px" else
+                   "inflight": len(pcs) if args.exchange == "px" else 1,
+                   "timing": ("CUDA events on a master stream joined by the in-flight plans' "
+                              "streams around K graph replays, max over ranks"
+                              if args.exchange == "px" else
                               "wall clock between barriers + device sync, max over ranks "
                               "(host-orchestrated exchange)"),
                    "graph": {"vertices": cfg["n"], "edges": cfg["m"], "gen_s": round(gen_s, 2)}},

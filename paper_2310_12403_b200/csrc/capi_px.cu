@@ -354,7 +354,7 @@ int cb_px_capture(cb_plan* plan, uint64_t n_seeds, const cb_sched* sched,
     require(sched->kappa != 0, "SeedSchedule: kappa must be >= 1 (or infinity)");
     require(n_seeds <= plan->max_seeds, "more seeds than the plan's max_seeds_per_part");
     PxState& px = px_of(plan);
-    if (local) {
+    if (local && !px.rstage) {  // direct pull from the peers' shards
       for (uint32_t q = 0; q < px.world; ++q)
         require(px.fbase[q] != nullptr, "feature shard of a rank not connected");
     }
@@ -514,8 +514,6 @@ int cb_px_gather(cb_plan* plan, const cb_features* local) {
     require(plan != nullptr && local != nullptr, "null argument");
     require(plan->have_batch, "no sampled batch in this plan");
     PxState& px = px_of(plan);
-    for (uint32_t q = 0; q < px.world; ++q)
-      require(px.fbase[q] != nullptr, "feature shard of a rank not connected");
     DeviceGuard dg(plan->device);
     prepare_rows(plan, local, false);  // rows come from the owners' shards
     plan->have_rows = true;
@@ -524,6 +522,8 @@ int cb_px_gather(cb_plan* plan, const cb_features* local) {
       px_enqueue_staged_gather(plan, -1);
       return;
     }
+    for (uint32_t q = 0; q < px.world; ++q)
+      require(px.fbase[q] != nullptr, "feature shard of a rank not connected");
     PeWork& w = plan->pe[0];
     const int L = plan->L;
     launch_px_gather(px.d_fbase, px.owner, local->row_map, local->row_bytes, w.L[L - 1].src,

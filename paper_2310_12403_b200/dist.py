@@ -268,7 +268,7 @@ class PeerCoop:
 
     def __init__(self, g: Graph, pm: PartitionMap, rank: int, num_layers: int,
                  cfg: SamplerConfig, max_seeds: int, store: FeatureStore | None = None,
-                 group=None, barrier: str = "device"):
+                 group=None, barrier: str = "device", direct_rows: bool = False):
         if barrier not in ("device", "nccl", "host"):
             raise ValueError("PeerCoop: barrier must be 'device', 'nccl' or 'host'")
         self.L = _lib.load()
@@ -292,7 +292,10 @@ class PeerCoop:
             if q != rank:
                 hq = (C.c_ubyte * self.HANDLE).from_buffer_copy(handles[q])
                 _check(self.L.cb_px_connect(h, q, hq))
-        if store is not None:
+        if store is not None and direct_rows:
+            # rows read in place from the peers' shards (one mapping of a
+            # shard per process: a second PeerCoop over the same store
+            # cannot map it again)
             fb, r0 = (C.c_ubyte * self.HANDLE)(), C.c_uint64()
             _check(self.L.cb_features_export(store._h, fb, C.byref(r0)))
             fh = [None] * self.world
@@ -300,6 +303,7 @@ class PeerCoop:
             for q in range(self.world):
                 hq = (C.c_ubyte * self.HANDLE).from_buffer_copy(fh[q][0])
                 _check(self.L.cb_px_connect_features(h, q, hq, fh[q][1], store._h))
+        elif store is not None:
             # owner staging: owners load their requested rows, requesters pull
             sb = (C.c_ubyte * self.HANDLE)()
             _check(self.L.cb_px_setup_staging(h, store._h, sb))

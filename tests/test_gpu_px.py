@@ -13,7 +13,8 @@ from tests.dist_harness import check_rank, spawn
 pytestmark = pytest.mark.gpu
 
 
-def _px_worker(rank, world, kind, fanouts, kappa, steps, barrier="device", captured=False):
+def _px_worker(rank, world, kind, fanouts, kappa, steps, barrier="device", captured=False,
+               direct_rows=False):
     import numpy as np
 
     import paper_2310_12403_b200 as cb
@@ -28,7 +29,7 @@ def _px_worker(rank, world, kind, fanouts, kappa, steps, barrier="device", captu
     L, dim, dtype, fseed = len(fanouts), 24, "f16", 5
     store = synth_shard(g, pm, rank, dim, fseed, dtype)
     pc = PeerCoop(g, pm, rank, L, cb.SamplerConfig(cb.SamplerKind(kind), fanouts=fanouts),
-                  max_seeds=4096, store=store, barrier=barrier)
+                  max_seeds=4096, store=store, barrier=barrier, direct_rows=direct_rows)
     sched = cb.SeedSchedule.make(kappa, 8)
     for step in range(steps):  # consecutive batches reuse the exchange slots
         seeds = O.draw_coop_seeds(owner, world, 128, 6, step)
@@ -47,13 +48,13 @@ def _px_worker(rank, world, kind, fanouts, kappa, steps, barrier="device", captu
     del np
 
 
-@pytest.mark.parametrize("world,kind,fanouts,kappa,steps,barrier", [
-    (2, 2, [10, 10, 10], 1, 3, "device"),
-    (3, 1, [10, 5, 5], 1, 2, "device"),
-    (2, 2, [25, 15], 4, 2, "host"),
+@pytest.mark.parametrize("world,kind,fanouts,kappa,steps,barrier,direct", [
+    (2, 2, [10, 10, 10], 1, 3, "device", False),
+    (3, 1, [10, 5, 5], 1, 2, "device", True),   # rows read in place from peer shards
+    (2, 2, [25, 15], 4, 2, "host", False),
 ])
-def test_peer_coop(gpu, world, kind, fanouts, kappa, steps, barrier):
-    spawn(world, _px_worker, (kind, fanouts, kappa, steps, barrier), timeout=600)
+def test_peer_coop(gpu, world, kind, fanouts, kappa, steps, barrier, direct):
+    spawn(world, _px_worker, (kind, fanouts, kappa, steps, barrier, False, direct), timeout=600)
 
 
 @pytest.mark.parametrize("world,kind,fanouts,kappa,steps", [
