@@ -692,7 +692,8 @@ def run_ours_coop(args, cfg):
         # stream and captured graphs; step i runs on pcs[i % S]
         S = max(1, args.inflight)
         pcs = []
-        for _ in range(S):
+
+        def add_peer():
             pc_ = PeerCoop(g, pm, rank, L, scfg, max_seeds=b, store=store, barrier="device")
             # one eager step on every rank (kernel attributes), then the whole
             # step (L layers, device barriers, row pull) as CUDA graphs
@@ -701,6 +702,18 @@ def run_ours_coop(args, cfg):
             pc_.finish()
             pc_.capture(b, scheds[0])
             pcs.append(pc_)
+        free0 = torch.cuda.mem_get_info(dev)[0]
+        add_peer()
+        # as many in flight as a third of the remaining HBM holds (the ranks
+        # agree on the minimum), at most --inflight
+        per = max(1, free0 - torch.cuda.mem_get_info(dev)[0])
+        fit = torch.tensor([max(1, min(S, 1 + int(torch.cuda.mem_get_info(dev)[0] / 3 // per)))],
+                           dtype=torch.int64)
+        dist.all_reduce(fit, op=dist.ReduceOp.MIN)
+        S = int(fit.item())
+        plan_gb = round(per / 1e9, 2)
+        while len(pcs) < S:
+            add_peer()
         pc = pcs[0]
         n_cap = C.c_uint64()
         from paper_2310_12403_b200.coopbatch import _check
@@ -795,6 +808,7 @@ def run_ours_coop(args, cfg):
                        if args.exchange == "px" else
                        f"{backend} all-to-allv per layer + feature all-to-allv)"),
                    "inflight": len(pcs) if args.exchange == "px" else 1,
+                   "plan_gb": plan_gb if args.exchange == "px" else None,
                    "timing": ("CUDA events on a master stream joined by the in-flight plans' "
                               "streams around K graph replays, max over ranks"
                               if args.exchange == "px" else

@@ -840,9 +840,12 @@ void prepare_rows(cb_plan* pl, const cb_features* f, bool any_row) {
   for (uint32_t p = 0; p < pl->P; ++p) {
     PeWork& w = pl->pe[p];
     const LayerBufs& b = w.L[pl->L - 1];
-    if (!w.rows || w.rows_row_bytes != f->row_bytes || w.cap_rows < b.cap_src) {
-      w.rows = pl->rows_mem.alloc<unsigned char>(b.cap_src * f->row_bytes);
-      w.cap_rows = b.cap_src;
+    // peer-exchange plans cap their row buffers (their src capacity is the
+    // world-times worst case); exceeding the cap flags an overflow
+    const uint64_t want = pl->rows_limit ? std::min(b.cap_src, pl->rows_limit) : b.cap_src;
+    if (!w.rows || w.rows_row_bytes != f->row_bytes || w.cap_rows < want) {
+      w.rows = pl->rows_mem.alloc<unsigned char>(want * f->row_bytes);
+      w.cap_rows = want;
       w.rows_row_bytes = f->row_bytes;
     }
   }

@@ -297,6 +297,7 @@ struct cb_plan {
   cbdev::ResolvePend* rs_pend = nullptr;
   unsigned long long* rs_npend = nullptr;
   uint64_t rs_resolved = 0, rs_reruns = 0;  // of the last cb_sample_sync
+  uint64_t rows_limit = 0;    // row-buffer cap in rows (0: the src capacity)
   void* meta_host = nullptr;  // pinned staging of cb_plan_result_copy's counts
   void* pack = nullptr;       // cb_plan_result_pack's packed result (device)
   uint64_t pack_bytes = 0;

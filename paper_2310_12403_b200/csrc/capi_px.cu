@@ -29,6 +29,8 @@ PxState& px_of(cb_plan* pl) {
 
 // CB_PX_BARRIER_TIMEOUT_MS (default 20000): a barrier wait that long gives up
 // and flags the step as failed instead of hanging the device.
+constexpr uint64_t kPxRowsLimit = 1ULL << 22;
+
 unsigned long long barrier_timeout_ns() {
   const char* e = std::getenv("CB_PX_BARRIER_TIMEOUT_MS");
   const unsigned long long ms = e ? std::strtoull(e, nullptr, 10) : 20000ULL;
@@ -188,8 +190,13 @@ void px_enqueue_staged_gather(cb_plan* plan, int g) {
                 plan->stream);
   if (g < 0) launch_px_barrier(px.bar, plan->stream);
   else px_enqueue_barrier(plan, L + 1, g & 1);
+  PxCaps caps;
+  caps.count2 = &plan->meta_at(0, L)->n_dst;
+  caps.cap2 = px.rstage_rows;
+  caps.overflow = w.sync.overflow;
   launch_px_gather_staged(px.d_rstage, w.loc_part[L - 1], w.loc_row[L - 1], f->row_bytes,
-                          &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, plan->stream);
+                          &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, caps,
+                          plan->stream);
 }
 
 }  // namespace
@@ -559,7 +566,12 @@ int cb_px_setup_staging(cb_plan* plan, const cb_features* local, void* handle_ou
     px.ropened.clear();
     if (px.rstage) CB_CUDA(cudaFree(px.rstage));
     px.stage_store = local;
-    px.rstage_rows = std::max<uint64_t>(w.cap_final, 1);
+    // row buffers of a peer-exchange plan: its src / owner-set capacities are
+    // the world-times worst case (c4, 2 ranks: 45M / 90M rows = 11.5 / 23 GB
+    // of fp16 rows per plan) against ~0.1M rows seen; the buffers are capped
+    // at kPxRowsLimit rows and a step that needs more is flagged (CB_OVERFLOW)
+    plan->rows_limit = kPxRowsLimit;
+    px.rstage_rows = std::max<uint64_t>(std::min(w.cap_final, kPxRowsLimit), 1);
     CB_CUDA(cudaMalloc(&px.rstage, px.rstage_rows * local->row_bytes));
     if (!px.d_rstage) CB_CUDA(cudaMalloc(&px.d_rstage, kMaxParts * sizeof(void*)));
     px.rstage_of.assign(kMaxParts, nullptr);
@@ -658,9 +670,11 @@ int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint
     // reaches before finishing this pull
     launch_px_barrier(px.bar, plan->stream);
     const uint64_t rb = px.stage_store->row_bytes;
+    PxCaps caps;
+    caps.overflow = w.sync.overflow;
     if (!px.rcache) {
       launch_px_gather_staged(px.d_rstage, w.loc_part[L - 1], w.loc_row[L - 1], rb,
-                              &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows,
+                              &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, caps,
                               plan->stream);
     } else {
       // requester side: own rows from the own staging buffer; rows owned by
@@ -684,7 +698,7 @@ int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint
                              px.r_ids, px.r_pos, px.r_miss, px.r_n, plan->stream);
       launch_px_gather_staged_local(px.d_rstage, w.loc_part[L - 1], w.loc_row[L - 1], rb,
                                     &plan->meta_at(0, L - 1)->n_src, w.cap_rows, w.rows, px.rank,
-                                    plan->stream);
+                                    caps, plan->stream);
       unsigned long long nr = 0;
       CB_CUDA(cudaMemcpyAsync(&nr, px.r_n, 8, cudaMemcpyDeviceToHost, plan->stream));
       CB_CUDA(cudaStreamSynchronize(plan->stream));

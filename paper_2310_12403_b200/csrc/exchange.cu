@@ -146,8 +146,15 @@ __global__ void px_gather_staged_kernel(const unsigned char* const* __restrict__
                                         const uint32_t* __restrict__ loc_row, uint32_t vpr,
                                         uint64_t row_bytes,
                                         const unsigned long long* __restrict__ count,
-                                        uint64_t cap, V* __restrict__ out, uint32_t only_rank) {
+                                        uint64_t cap, V* __restrict__ out, uint32_t only_rank,
+                                        const unsigned long long* __restrict__ count2,
+                                        uint64_t cap2, unsigned* overflow) {
   pdl_begin();
+  // rows beyond a capped buffer (this pull's, or the owner's staging count2)
+  // are never silently dropped: the step is flagged
+  if (overflow && blockIdx.x == 0 && threadIdx.x == 0 &&
+      (*count > cap || (count2 && *count2 > cap2)))
+    atomicExch(overflow, 1u);
   const uint64_t n = min(static_cast<uint64_t>(*count), cap);
   const uint64_t total = n * vpr;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -291,7 +298,7 @@ void launch_px_gather(const unsigned char* const* d_bases, const uint32_t* owner
 namespace {
 void staged(const unsigned char* const* d_bases, const uint32_t* loc_part, const uint32_t* loc_row,
             uint64_t row_bytes, const unsigned long long* count, uint64_t cap, void* out,
-            uint32_t only_rank, cudaStream_t st) {
+            uint32_t only_rank, const PxCaps& caps, cudaStream_t st) {
   int vb = 16;
   while (row_bytes % vb) vb >>= 1;
   const uint32_t vpr = static_cast<uint32_t>(row_bytes / vb);
@@ -299,20 +306,20 @@ void staged(const unsigned char* const* d_bases, const uint32_t* loc_part, const
   switch (vb) {
     case 16:
       launch_k(px_gather_staged_kernel<uint4>, grid, 256, st, d_bases, loc_part, loc_row, vpr,
-               row_bytes, count, cap, static_cast<uint4*>(out), only_rank);
+               row_bytes, count, cap, static_cast<uint4*>(out), only_rank, caps.count2, caps.cap2, caps.overflow);
       break;
     case 8:
       launch_k(px_gather_staged_kernel<uint2>, grid, 256, st, d_bases, loc_part, loc_row, vpr,
-               row_bytes, count, cap, static_cast<uint2*>(out), only_rank);
+               row_bytes, count, cap, static_cast<uint2*>(out), only_rank, caps.count2, caps.cap2, caps.overflow);
       break;
     case 4:
       launch_k(px_gather_staged_kernel<uint32_t>, grid, 256, st, d_bases, loc_part, loc_row,
-               vpr, row_bytes, count, cap, static_cast<uint32_t*>(out), only_rank);
+               vpr, row_bytes, count, cap, static_cast<uint32_t*>(out), only_rank, caps.count2, caps.cap2, caps.overflow);
       break;
     default:
       launch_k(px_gather_staged_kernel<unsigned short>, grid, 256, st, d_bases, loc_part,
                loc_row, vpr, row_bytes, count, cap, static_cast<unsigned short*>(out),
-               only_rank);
+               only_rank, caps.count2, caps.cap2, caps.overflow);
   }
   CB_LAUNCH("px_gather_staged");
 }
@@ -361,15 +368,15 @@ __global__ void px_scatter_rows_kernel(const V* __restrict__ rows, const uint32_
 void launch_px_gather_staged(const unsigned char* const* d_bases, const uint32_t* loc_part,
                              const uint32_t* loc_row, uint64_t row_bytes,
                              const unsigned long long* count, uint64_t cap, void* out,
-                             cudaStream_t st) {
-  staged(d_bases, loc_part, loc_row, row_bytes, count, cap, out, ~0u, st);
+                             const PxCaps& caps, cudaStream_t st) {
+  staged(d_bases, loc_part, loc_row, row_bytes, count, cap, out, ~0u, caps, st);
 }
 
 void launch_px_gather_staged_local(const unsigned char* const* d_bases, const uint32_t* loc_part,
                                    const uint32_t* loc_row, uint64_t row_bytes,
                                    const unsigned long long* count, uint64_t cap, void* out,
-                                   uint32_t rank, cudaStream_t st) {
-  staged(d_bases, loc_part, loc_row, row_bytes, count, cap, out, rank, st);
+                                   uint32_t rank, const PxCaps& caps, cudaStream_t st) {
+  staged(d_bases, loc_part, loc_row, row_bytes, count, cap, out, rank, caps, st);
 }
 
 void launch_px_split_remote(const uint32_t* src, const unsigned long long* count, uint64_t cap,

@@ -66,12 +66,19 @@ void launch_px_gather(const unsigned char* const* d_bases, const uint32_t* owner
                       const unsigned long long* count, uint64_t cap, void* out,
                       cudaStream_t st);
 
+// Capacity checks of a staged pull: *count (this pull) > cap or *count2 (the
+// owner's staged rows) > cap2 sets *overflow (nullptr: no check).
+struct PxCaps {
+  const unsigned long long* count2 = nullptr;
+  uint64_t cap2 = 0;
+  unsigned* overflow = nullptr;
+};
 // all_to_all_forward from the owners' staged rows: out[j] = row loc_row[j] of
 // rank loc_part[j]'s staging buffer (bases[q], IPC-mapped).
 void launch_px_gather_staged(const unsigned char* const* d_bases, const uint32_t* loc_part,
                              const uint32_t* loc_row, uint64_t row_bytes,
                              const unsigned long long* count, uint64_t cap, void* out,
-                             cudaStream_t st);
+                             const PxCaps& caps, cudaStream_t st);
 
 // Requester-side cache support: the requested rows owned by OTHER ranks,
 // compacted (any order): ids[k], their positions pos[k] in the request list
@@ -88,7 +95,7 @@ void launch_px_scatter_rows(const void* rows, const uint32_t* pos, uint64_t n, u
 void launch_px_gather_staged_local(const unsigned char* const* d_bases, const uint32_t* loc_part,
                                    const uint32_t* loc_row, uint64_t row_bytes,
                                    const unsigned long long* count, uint64_t cap, void* out,
-                                   uint32_t rank, cudaStream_t st);
+                                   uint32_t rank, const PxCaps& caps, cudaStream_t st);
 
 void launch_route(const PartPtrs& pp, const uint32_t* owner, uint32_t P,
                   unsigned long long* send_counts, uint64_t max_src, cudaStream_t st);
