@@ -568,6 +568,27 @@ def work_curve_evidence(cb, dev, cpu: bool, trials=50, layers=3, seed=49):
     return out
 
 
+# ----------------------------------------------------- drop-in e2e evidence --
+def dropin_evidence():
+    """End to end through the C++ drop-in (tools/dropin_bench.cpp, built by
+    tests/cpp/Makefile against libcoopbatch_core_b200): the reference's own
+    coopbatch::expand + FeatureStore::load_rows (f64 rows read in place from
+    the host table) with host objects in and out, on config c2."""
+    exe = os.path.join(ROOT, "tests", "cpp", "_build", "dropin_bench")
+    if not os.path.exists(exe):
+        return {"unavailable": "tests/cpp/_build/dropin_bench not built"}
+    c = CONFIGS["c2"]
+    try:
+        r = subprocess.run([exe, str(c["n"]), str(c["m"]), str(c["dim"]), "40"],
+                           capture_output=True, text=True, timeout=600)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 - evidence only
+        return {"error": str(e)[:200]}
+    d["workload"] = c["workload"] + " (rows as the reference's f64 FeatureStore)"
+    d["api"] = "coopbatch::expand + FeatureStore::load_rows (reference headers, host objects)"
+    return d
+
+
 # ---------------------------------------------------------- kappa evidence --
 def kappa_evidence(cb, dev, steps_epochs=2, kappas=(1, 4, 16, 64, 256, None)):
     """Config 3's kappa sweep (acceptance.cpp:362-390 at full scale): the
@@ -1118,6 +1139,7 @@ def run_ours(args, cfg):
             scale_evidence(cb, dev, other)
         line["evidence"]["mag240m_batch_sweep"] = batch_sweep_evidence(cb, dev)
         line["evidence"]["work_curves"] = work_curve_evidence(cb, dev, not args.no_cpu_baseline)
+        line["evidence"]["dropin_e2e_c2"] = dropin_evidence()
     if world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import oracle as O
