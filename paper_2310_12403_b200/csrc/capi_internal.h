@@ -133,9 +133,18 @@ struct cb_features {
   void* hbm_table = nullptr;    // the HBM table while the host tier is active
   uint32_t* labels = nullptr;   // [n_rows] explicit labels (cb_features_set_labels) or null
   void* registered = nullptr;   // caller's host rows mapped in place (cb_features_wrap_host)
+  // cb_op_load_rows scratch, reused across calls (a cudaMalloc / cudaFree and
+  // a stream per call cost more than the gather)
+  cudaStream_t op_stream = nullptr;
+  void* op_ids = nullptr;
+  void* op_out = nullptr;
+  uint64_t op_cap = 0;
   ~cb_features() {
     if (host_base) cudaFreeHost(host_base);
     if (registered) cudaHostUnregister(registered);
+    if (op_ids) cudaFree(op_ids);
+    if (op_out) cudaFree(op_out);
+    if (op_stream) cudaStreamDestroy(op_stream);
   }
 };
 

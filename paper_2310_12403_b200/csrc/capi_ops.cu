@@ -394,18 +394,21 @@ int cb_op_load_rows(const cb_features* f, const uint32_t* ids, uint64_t n, void*
         throw cb::Error(kInput, "load_rows: vertex id " + std::to_string(ids[i]) +
                                     " out of range [0, " + std::to_string(f->n_rows) + ")");
     DeviceGuard dg(f->device);
-    cudaStream_t st = nullptr;
-    CB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    struct StreamGuard {
-      cudaStream_t s;
-      ~StreamGuard() { cudaStreamDestroy(s); }
-    } sg{st};
-    DevBuf d_ids(n * 4), d_out(n * f->row_bytes);
-    CB_CUDA(cudaMemcpyAsync(d_ids.as<void>(), ids, n * 4, cudaMemcpyHostToDevice, st));
-    launch_gather(f->table, vec_bytes_for(f->row_bytes), f->row_bytes, d_ids.as<uint32_t>(),
-                  nullptr, n, nullptr, d_out.as<void>(), st);
+    auto* fm = const_cast<cb_features*>(f);  // scratch only; the table is not modified
+    if (!fm->op_stream) CB_CUDA(cudaStreamCreateWithFlags(&fm->op_stream, cudaStreamNonBlocking));
+    cudaStream_t st = fm->op_stream;
+    if (fm->op_cap < n) {
+      if (fm->op_ids) CB_CUDA(cudaFree(fm->op_ids));
+      if (fm->op_out) CB_CUDA(cudaFree(fm->op_out));
+      fm->op_cap = n + n / 4;
+      CB_CUDA(cudaMalloc(&fm->op_ids, fm->op_cap * 4));
+      CB_CUDA(cudaMalloc(&fm->op_out, fm->op_cap * f->row_bytes));
+    }
+    CB_CUDA(cudaMemcpyAsync(fm->op_ids, ids, n * 4, cudaMemcpyHostToDevice, st));
+    launch_gather(f->table, vec_bytes_for(f->row_bytes), f->row_bytes,
+                  static_cast<uint32_t*>(fm->op_ids), nullptr, n, nullptr, fm->op_out, st);
     CB_LAUNCH("load_rows");
-    CB_CUDA(cudaMemcpyAsync(out, d_out.as<void>(), n * f->row_bytes, cudaMemcpyDeviceToHost, st));
+    CB_CUDA(cudaMemcpyAsync(out, fm->op_out, n * f->row_bytes, cudaMemcpyDeviceToHost, st));
     CB_CUDA(cudaStreamSynchronize(st));
   });
 }

@@ -427,8 +427,14 @@ FeatureMatrix FeatureStore::load_rows(std::span<const VertexId> ids) const {
   m.dim = dim;
   m.values.resize(ids.size() * dim);
   if (ids.empty() || dim == 0) return m;
-  MappedHostTable t(values.data(), values.size() / dim, dim);
-  check(cb_op_load_rows(t.get(), ids.data(), ids.size(), m.values.data()));
+  const std::uint64_t n_rows = values.size() / dim;
+  if (n_rows * dim * 8 <= (16ULL << 20)) {  // small: copied to HBM per call
+    MappedHostTable t(values.data(), n_rows, dim);
+    check(cb_op_load_rows(t.get(), ids.data(), ids.size(), m.values.data()));
+  } else {  // large: registered once, read in place
+    cb_features* t = cached_host_table(values.data(), n_rows, dim);
+    check(cb_op_load_rows(t, ids.data(), ids.size(), m.values.data()));
+  }
   return m;
 }
 

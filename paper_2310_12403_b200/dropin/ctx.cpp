@@ -44,7 +44,7 @@ int device() {
 namespace {
 
 // 64-bit content hash over a byte range, 4 independent lanes (~10 GB/s per
-// thread); ranges above 64 MiB are split over host threads.
+// thread); ranges above 8 MiB are split over host threads.
 std::uint64_t hash_range(const unsigned char* p, std::size_t n, std::uint64_t seed) {
   constexpr std::uint64_t kM = 0x9E3779B97F4A7C15ULL;
   std::uint64_t a = seed ^ 0x243F6A8885A308D3ULL, b = seed ^ 0x13198A2E03707344ULL,
@@ -70,7 +70,7 @@ std::uint64_t hash_range(const unsigned char* p, std::size_t n, std::uint64_t se
 
 std::uint64_t content_hash(const void* data, std::size_t bytes) {
   const auto* p = static_cast<const unsigned char*>(data);
-  constexpr std::size_t kChunk = 64ULL << 20;
+  constexpr std::size_t kChunk = 8ULL << 20;  // spread over every host thread
   if (bytes <= kChunk) return hash_range(p, bytes, 0);
   const std::size_t chunks = (bytes + kChunk - 1) / kChunk;
   std::vector<std::uint64_t> hs(chunks);
@@ -319,6 +319,59 @@ BipartiteBlock download_block(cb_plan* pl, std::uint32_t part, int l, int layer_
                           reinterpret_cast<std::uint32_t*>(b.edges.data()),
                           b.dst_pos_in_src.data()));
   return b;
+}
+
+namespace {
+
+struct HostTableEntry {
+  const double* rows;
+  std::uint64_t n_rows;
+  std::uint32_t dim;
+  std::uint64_t fp;
+  cb_features* f;
+};
+
+// 64 words spread over the table, plus its shape
+std::uint64_t sampled_fingerprint(const double* rows, std::uint64_t n) {
+  std::uint64_t h = mix64(n);
+  if (n == 0) return h;
+  for (std::uint64_t i = 0; i < 64; ++i) {
+    std::uint64_t w;
+    std::memcpy(&w, rows + (i * (n - 1)) / 63, 8);
+    h = mix64(h ^ w ^ (i << 56));
+  }
+  return h;
+}
+
+std::list<HostTableEntry>& host_tables() {
+  static std::list<HostTableEntry> t;
+  return t;
+}
+
+}  // namespace
+
+cb_features* cached_host_table(const double* rows, std::uint64_t n_rows, std::uint32_t dim) {
+  auto& ts = host_tables();
+  const std::uint64_t fp = sampled_fingerprint(rows, n_rows * dim);
+  for (auto it = ts.begin(); it != ts.end(); ++it) {
+    if (it->rows == rows && it->n_rows == n_rows && it->dim == dim) {
+      if (it->fp == fp) {
+        ts.splice(ts.begin(), ts, it);
+        return ts.front().f;
+      }
+      cb_features_destroy(it->f);  // other contents at the same address
+      ts.erase(it);
+      break;
+    }
+  }
+  while (ts.size() >= 4) {
+    cb_features_destroy(ts.back().f);
+    ts.pop_back();
+  }
+  cb_features* f = nullptr;
+  check(cb_features_wrap_host(device(), n_rows, dim, CB_F64, rows, &f));
+  ts.push_front({rows, n_rows, dim, fp, f});
+  return f;
 }
 
 MappedHostTable::MappedHostTable(const double* rows, std::uint64_t n_rows, std::uint32_t dim) {

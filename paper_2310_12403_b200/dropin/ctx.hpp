@@ -65,6 +65,13 @@ void layer_sizes(cb_plan* pl, std::uint32_t part, int l, std::uint64_t sz[6]);
 // reference's FeatureStore keeps its f64 rows in host memory (coop.hpp:140-155);
 // the device reads them in place over the host link (the paper's storage
 // channel) instead of copying the table.
+// A large host f64 table kept registered (pinned, mapped, read in place)
+// across calls, keyed by (address, rows, dim) and a sampled fingerprint (a
+// table freed and reallocated at the same address with other contents is
+// re-registered). Rows are read in place, so writes to a registered table are
+// seen by the next call. (Registering 2 GB of pages per call cost ~0.3 s.)
+cb_features* cached_host_table(const double* rows, std::uint64_t n_rows, std::uint32_t dim);
+
 class MappedHostTable {
  public:
   MappedHostTable(const double* rows, std::uint64_t n_rows, std::uint32_t dim);

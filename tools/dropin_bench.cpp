@@ -44,15 +44,20 @@ int main(int argc, char** argv) {
   cfg.fanout = 10;
   SeedSchedule sched = SeedSchedule::make(1, 1234);
   std::vector<VertexId> seeds(b);
-  double rows = 0, edges = 0;
+  double rows = 0, edges = 0, t_expand = 0, t_rows = 0;
   auto t0 = std::chrono::steady_clock::now();
   for (int s = 0; s < warmup + steps; ++s) {
     if (s == warmup) t0 = std::chrono::steady_clock::now();
     for (std::uint32_t i = 0; i < b; ++i)
       seeds[i] = static_cast<VertexId>(hash_bits(1234, {static_cast<std::uint64_t>(s), i}) % n);
+    const auto ta = std::chrono::steady_clock::now();
     const LayerStack st = expand(g, seeds, L, cfg, sched);
+    const auto tb = std::chrono::steady_clock::now();
     const FeatureMatrix fm = fs.load_rows(st.input_vertices());
+    const auto tc = std::chrono::steady_clock::now();
     if (s >= warmup) {
+      t_expand += std::chrono::duration<double>(tb - ta).count();
+      t_rows += std::chrono::duration<double>(tc - tb).count();
       rows += static_cast<double>(fm.rows());
       for (const auto& blk : st.blocks) edges += static_cast<double>(blk.edges.size());
     }
@@ -62,8 +67,10 @@ int main(int argc, char** argv) {
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   std::printf(
       "{\"seeds_per_s\": %.1f, \"ms_per_step\": %.4f, \"steps\": %d, \"rows_per_step\": %.1f, "
-      "\"edges_per_step\": %.1f, \"row_bytes\": %u, \"graph\": [%llu, %llu]}\n",
+      "\"edges_per_step\": %.1f, \"row_bytes\": %u, \"graph\": [%llu, %llu], "
+      "\"ms_expand\": %.3f, \"ms_load_rows\": %.3f}\n",
       steps * static_cast<double>(b) / dt, 1e3 * dt / steps, steps, rows / steps, edges / steps,
-      dim * 8, static_cast<unsigned long long>(n), static_cast<unsigned long long>(m));
+      dim * 8, static_cast<unsigned long long>(n), static_cast<unsigned long long>(m),
+      1e3 * t_expand / steps, 1e3 * t_rows / steps);
   return 0;
 }
