@@ -330,6 +330,22 @@ int cb_cache_reset_counters(cb_cache* c);
 int cb_cache_resident(cb_cache* c, uint32_t* out, uint64_t cap_out, uint64_t* n);
 int cb_cache_storage(const cb_cache* c, const void** d_rows);
 
+/* ---- fast per-GPU feature cache: set-associative, CLOCK replacement ----
+ * The production cache mode: three kernels per batch (lookup,
+ * serve, insert), no sort, no host round trip, so it can sit inside a
+ * captured step. Its hit rate is its own (not LruCache's: cb_cache_* is the
+ * batch-exact LRU for parity); rows served are always the table's rows.
+ * cb_ccache_gather_plan: the input rows of part `part` of the plan's last
+ * batch into the plan's row buffer (cb_download_rows / cb_rows_device), hits
+ * from the cache, misses from `backing` (HBM or host tier), misses inserted. */
+typedef struct cb_ccache cb_ccache;
+int cb_ccache_create(int device, uint64_t capacity, uint32_t ways, uint64_t row_bytes,
+                     cb_ccache** out);
+void cb_ccache_destroy(cb_ccache* c);
+int cb_ccache_gather_plan(cb_ccache* c, cb_plan* plan, uint32_t part, const cb_features* backing);
+/* Running totals: hits, inserted rows, slots (synchronises the device). */
+int cb_ccache_stats(cb_ccache* c, uint64_t* hits, uint64_t* inserted, uint64_t* capacity);
+
 /* stack_fingerprint (cache.cpp:123-133) of part `part` of the last batch. */
 int cb_stack_fingerprint(cb_plan* plan, uint32_t part, uint64_t* out);
 /* run_dependent_experiment's fixed training order (cache.cpp:155-162). */

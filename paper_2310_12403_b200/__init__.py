@@ -11,7 +11,8 @@ from .coopbatch import (  # noqa: F401
     sample_block, sample_full, sample_labor0, sample_ns, sample_rw, schedule_advance, LayerMetrics, PeMetrics, step_metrics,
     parse_result)
 from .cache import (  # noqa: F401
-    BatchMode, CacheOutcome, CacheStats, DependentExperimentResult, DependentStepRow, LruCache,
+    BatchMode, CacheOutcome, CacheStats, ClockCache, DependentExperimentResult, DependentStepRow,
+    LruCache,
     MinibatchSchedule, feature_load_sim, lru_access, nested_batches, run_dependent_experiment,
     shuffled_order, stack_fingerprint)
 from .train import GcnModel, TrainStepResult, coop_train_step, indep_train_step  # noqa: F401,E402

@@ -112,6 +112,10 @@ _SIGS = {
     "cb_cache_reset_counters": (C.c_int, [_P]),
     "cb_cache_resident": (C.c_int, [_P, _P, _u64, C.POINTER(_u64)]),
     "cb_cache_storage": (C.c_int, [_P, _PP]),
+    "cb_ccache_create": (C.c_int, [C.c_int, _u64, _u32, _u64, _PP]),
+    "cb_ccache_destroy": (None, [_P]),
+    "cb_ccache_gather_plan": (C.c_int, [_P, _P, _u32, _P]),
+    "cb_ccache_stats": (C.c_int, [_P, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
     "cb_stack_fingerprint": (C.c_int, [_P, _u32, C.POINTER(_u64)]),
     "cb_shuffled_order": (C.c_int, [_u64, _u64, _P]),
     "cb_features_set_tier": (C.c_int, [_P, C.c_int]),

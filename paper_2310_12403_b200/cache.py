@@ -71,6 +71,39 @@ class DependentExperimentResult:  # cache.hpp:93-98
     steady_miss_rate: float = 0.0
 
 
+class ClockCache:
+    """Set-associative feature cache with CLOCK replacement (cb_ccache_*): the
+    fast production mode. Three kernels per batch, no sort and no host round
+    trip; its hit rate is its own (LruCache is the batch-exact LRU for parity),
+    and the rows it serves are always the table's rows."""
+
+    def __init__(self, capacity: int, row_bytes: int, device: int = 0, ways: int = 8):
+        if capacity < 1:
+            raise InputError("ClockCache: capacity must be >= 1")
+        h = C.c_void_p()
+        _check(_lib.load().cb_ccache_create(device, capacity, ways, row_bytes, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                _lib.load().cb_ccache_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown: the loader may be gone
+            pass
+
+    def gather_plan(self, plan: Plan, part: int, store: FeatureStore):
+        """Input rows of `part` of the plan's last batch into the plan's row
+        buffer (Plan.rows): hits from the cache, misses from `store`."""
+        _check(_lib.load().cb_ccache_gather_plan(self._h, plan._h, part, store._h))
+
+    def stats(self) -> tuple[int, int, int]:
+        """(hits, inserted rows, slots) so far."""
+        h, i, s = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(_lib.load().cb_ccache_stats(self._h, C.byref(h), C.byref(i), C.byref(s)))
+        return h.value, i.value, s.value
+
+
 class LruCache:
     """Exact LRU over vertex ids [0, n_keys), resident on `device`. With
     row_bytes > 0 it also holds the rows of its resident keys in HBM."""

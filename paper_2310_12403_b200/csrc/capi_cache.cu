@@ -273,3 +273,58 @@ int cb_plan_input_ids(cb_plan* plan, uint32_t part, const uint32_t** d_ids, uint
 }
 
 }  // extern "C"
+
+// ---- set-associative CLOCK cache (the fast production mode) -----------------
+extern "C" {
+
+int cb_ccache_create(int device, uint64_t capacity, uint32_t ways, uint64_t row_bytes,
+                     cb_ccache** out) {
+  return guard([&] {
+    require(out != nullptr, "null argument");
+    require(capacity >= 1 && row_bytes >= 2, "ClockCache: capacity and row bytes must be > 0");
+    DeviceGuard dg(device);
+    auto c = std::make_unique<cb_ccache>();
+    c->cc = std::make_unique<ClockCache>(device, capacity, ways, row_bytes);
+    CB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *out = c.release();
+  });
+}
+
+void cb_ccache_destroy(cb_ccache* c) {
+  if (!c) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->cc->device());
+  delete c;
+  cudaSetDevice(prev);
+}
+
+int cb_ccache_gather_plan(cb_ccache* c, cb_plan* plan, uint32_t part, const cb_features* backing) {
+  NvtxRange nvtx_("cb.ccache_gather_plan");
+  return guard([&] {
+    require(c != nullptr && plan != nullptr && backing != nullptr, "null argument");
+    require_batch(plan, part, plan->L - 1);
+    require(backing->row_bytes == c->cc->row_bytes(), "cache row size does not match the table");
+    require_full_table(backing);
+    DeviceGuard dg(plan->device);
+    prepare_rows(plan, backing);
+    PeWork& w = plan->pe[part];
+    const LayerBufs& b = w.L[plan->L - 1];
+    // device count, on the plan stream: no host round trip
+    c->cc->gather(backing->table, backing->row_map, b.src, &plan->meta_at(part, plan->L - 1)->n_src,
+                  w.cap_rows, w.rows, plan->stream);
+    plan->have_rows = true;
+  });
+}
+
+int cb_ccache_stats(cb_ccache* c, uint64_t* hits, uint64_t* inserted, uint64_t* capacity) {
+  return guard([&] {
+    require(c != nullptr, "null cache");
+    DeviceGuard dg(c->cc->device());
+    CB_CUDA(cudaDeviceSynchronize());
+    c->cc->counters(c->stream, hits, inserted);
+    if (capacity) *capacity = c->cc->capacity();
+  });
+}
+
+}  // extern "C"

@@ -25,6 +25,7 @@
 #include "gather.h"
 #include "dist.h"
 #include "cache.h"
+#include "clock_cache.h"
 #include "train.h"
 
 using namespace cb;
@@ -145,6 +146,14 @@ struct cb_features {
     if (op_ids) cudaFree(op_ids);
     if (op_out) cudaFree(op_out);
     if (op_stream) cudaStreamDestroy(op_stream);
+  }
+};
+
+struct cb_ccache {
+  std::unique_ptr<ClockCache> cc;
+  cudaStream_t stream = nullptr;
+  ~cb_ccache() {
+    if (stream) cudaStreamDestroy(stream);
   }
 };
 

@@ -153,3 +153,39 @@ def test_nested_batches(small):
             assert np.array_equal(st.blocks[l].src_vertices, want[l]["src"])
     with pytest.raises(cb.InputError):
         cb.nested_batches(g, sup[:199], 4, 50, 2, cfg, 123)
+
+
+def test_clock_cache_rows_and_hit_rate(gpu):
+    """The set-associative CLOCK cache over kappa-dependent batches: every row
+    it serves equals the table's row (hits from its HBM slots, misses from the
+    table in pinned host memory), and its hit rate is close to the exact LRU's
+    of the same capacity on the same sequence."""
+    import numpy as np
+
+    n, m, seed = 1 << 15, 1 << 19, 11
+    g = cb.Graph.generate_rmat(n, m, seed)
+    store = cb.FeatureStore.synth(g, 24, 3, "f16")
+    store.set_tier(True)
+    cap = n // 8
+    cc = cb.ClockCache(cap, store.row_bytes, ways=8)
+    lru = cb.LruCache(cap, n, 0, 0)
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, 10)
+    pl = cb.Plan(g, None, 2, cfg, 512)
+    sched = cb.SeedSchedule.make(4, 5)
+    rng = np.random.default_rng(2)
+    pool = rng.choice(n, 2048, replace=False).astype(np.uint32)
+    accesses = 0
+    for step in range(16):
+        seeds = pool[(step % 4) * 512:(step % 4 + 1) * 512]
+        pl.sample([seeds], sched, cb.MODE_INDEP)
+        cc.gather_plan(pl, 0, store)
+        ids = pl.stack(0).input_vertices()
+        want = O.feature_rows(3, 24, "f16", ids)
+        assert np.array_equal(pl.rows(0, store).view(np.uint8), want.view(np.uint8)), step
+        lru.access_ids(ids, cb.hash_bits(step, [0]))
+        accesses += len(ids)
+        sched = cb.schedule_advance(sched)
+    h, ins, slots = cc.stats()
+    assert slots == cap and 0 < h < accesses and ins <= accesses - h
+    assert h >= 0.8 * lru.hits(), (h, lru.hits(), accesses)
+    store.set_tier(False)
