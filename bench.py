@@ -638,9 +638,18 @@ def kappa_evidence(cb, dev, steps_epochs=2, kappas=(1, 4, 16, 64, 256, None)):
         steady = r.rows[r.warmup_steps:]
         CSV_ROWS.setdefault("cache", []).append(
             (kappa, [(x.step, x.miss_rate, x.s_l, x.bytes) for x in r.rows]))
+        # the same experiment through the fast CLOCK cache (same capacity)
+        tt = time.perf_counter()
+        rc = cb.run_dependent_experiment(g, cb.MinibatchSchedule(cb.BatchMode.kSmoothed, k,
+                                                                 c["batch"]), steps, cap, cfg,
+                                         len(c["fanouts"]), c["dim"], 4, RUN_SEED,
+                                         fingerprints=False, store=store, cache_kind="clock")
+        wall_c = time.perf_counter() - tt
         row = {
             "kappa": "inf" if kappa is None else kappa,
             "steady_miss_rate": r.steady_miss_rate,
+            "clock_cache": {"steady_miss_rate": rc.steady_miss_rate,
+                            "wall_ms_per_step": 1e3 * wall_c / steps},
             "input_vertices_per_seed": float(np.mean([x.s_l for x in steady])) / c["batch"],
             "storage_bytes_per_step": float(np.mean([x.bytes for x in steady])),
             "wall_ms_per_step": 1e3 * wall / steps,

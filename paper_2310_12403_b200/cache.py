@@ -251,7 +251,7 @@ def run_dependent_experiment(g: Graph, schedule: MinibatchSchedule, steps: int,
                              cache_capacity: int, cfg: SamplerConfig, num_layers: int,
                              feature_dim: int, bytes_per_scalar: int, seed: int,
                              fingerprints: bool = True, store: FeatureStore | None = None,
-                             on_step=None) -> DependentExperimentResult:
+                             on_step=None, cache_kind: str = "lru") -> DependentExperimentResult:
     """cache.cpp:137-208 on the GPU: a fixed shuffled order sliced into
     batches, each expanded under the schedule (smoothed kappa variates,
     nested groups or independent), its input rows fetched through the LRU.
@@ -264,7 +264,14 @@ def run_dependent_experiment(g: Graph, schedule: MinibatchSchedule, steps: int,
     order = shuffled_order(n, seed)
     spe = max(1, n // b)
     seeds = SeedSchedule.make(1 if schedule.mode == BatchMode.kNested else schedule.kappa, seed)
-    cache = LruCache(cache_capacity, n, g.device, store.row_bytes if store else 0)
+    if cache_kind not in ("lru", "clock"):
+        raise InputError("run_dependent_experiment: cache_kind must be 'lru' or 'clock'")
+    if cache_kind == "clock" and store is None:
+        raise InputError("run_dependent_experiment: the CLOCK cache moves rows (give a store)")
+    # "lru": the reference's LruCache decisions exactly; "clock": the fast
+    # set-associative cache (its own hit rate, no per-step sort)
+    cache = (LruCache(cache_capacity, n, g.device, store.row_bytes if store else 0)
+             if cache_kind == "lru" else ClockCache(cache_capacity, store.row_bytes, g.device))
     plan = Plan(g, None, num_layers, cfg, b)
     res = DependentExperimentResult(steps_per_epoch=spe, warmup_steps=min(spe, steps // 2))
     steady_hits = steady_miss = 0
@@ -279,9 +286,15 @@ def run_dependent_experiment(g: Graph, schedule: MinibatchSchedule, steps: int,
             plan.sample([batch], seeds, MODE_INDEP)
             seeds = schedule_advance(seeds)
         fp = stack_fingerprint(plan, 0) if fingerprints else 0
-        m0 = cache.misses()
-        s_l = cache.access_plan(plan, 0, hash_bits(seed, [step, 0xACCE55]), store=store)
-        miss = cache.misses() - m0
+        if cache_kind == "lru":
+            m0 = cache.misses()
+            s_l = cache.access_plan(plan, 0, hash_bits(seed, [step, 0xACCE55]), store=store)
+            miss = cache.misses() - m0
+        else:
+            h0 = cache.stats()[0]
+            cache.gather_plan(plan, 0, store)
+            s_l = plan.layer_sizes(0, num_layers - 1)["n_src"]
+            miss = s_l - (cache.stats()[0] - h0)
         res.rows.append(DependentStepRow(step, 0.0 if s_l == 0 else miss / s_l, s_l,
                                          miss * feature_dim * bytes_per_scalar, fp))
         if step >= res.warmup_steps:
