@@ -456,6 +456,11 @@ int cb_px_set_cache(cb_plan* plan, cb_cache* cache);
  * detaches it. cb_px_requester_stats: the last step's remote rows, hits and
  * misses (misses x row bytes = the peer bytes of the step). */
 int cb_px_set_requester_cache(cb_plan* plan, cb_cache* cache);
+/* The CLOCK cache (cb_ccache_*) in front of this owner's staging: cb_px_gather
+ * and the captured step's row fetch serve S^L_q from it (misses from the
+ * shard) -- no host round trip, so the cached fetch is part of the graph.
+ * Drops captured graphs (re-capture); NULL detaches it. */
+int cb_px_set_clock_cache(cb_plan* plan, cb_ccache* cache);
 int cb_px_requester_stats(const cb_plan* plan, uint64_t* remote, uint64_t* hits,
                           uint64_t* misses);
 int cb_px_gather_cached(cb_plan* plan, uint64_t order_key, uint64_t* owned, uint64_t* hits,

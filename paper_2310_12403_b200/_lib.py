@@ -140,6 +140,7 @@ _SIGS = {
     "cb_px_connect_staging": (C.c_int, [_P, _u32, _P]),
     "cb_px_set_cache": (C.c_int, [_P, _P]),
     "cb_px_set_requester_cache": (C.c_int, [_P, _P]),
+    "cb_px_set_clock_cache": (C.c_int, [_P, _P]),
     "cb_px_requester_stats": (C.c_int, [_P, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
     "cb_px_gather_cached": (C.c_int, [_P, _u64, C.POINTER(_u64), C.POINTER(_u64),
                                       C.POINTER(_u64)]),

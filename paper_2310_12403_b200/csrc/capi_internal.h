@@ -203,6 +203,7 @@ struct PxState {
   // owner staging (cb_px_setup_staging): the owner's rows of its set S^L_q
   // staged in an exported buffer, pulled by the requesters; optional cache
   cb_cache* cache = nullptr;
+  cb_ccache* ccache = nullptr;  // CLOCK cache in front of the owner's staging (capturable)
   const cb_features* stage_store = nullptr;
   // requester-side cache (cb_px_set_requester_cache): rows owned by other
   // ranks; compaction buffers of the remote requests

@@ -185,9 +185,14 @@ void px_enqueue_staged_gather(cb_plan* plan, int g) {
   PeWork& w = plan->pe[0];
   const int L = plan->L;
   const cb_features* f = px.stage_store;
-  launch_gather(f->table, vec_bytes_for(f->row_bytes), f->row_bytes, w.owner_final,
-                &plan->meta_at(0, L)->n_dst, px.rstage_rows, f->row_map, px.rstage,
-                plan->stream);
+  if (px.ccache) {  // owner-side CLOCK cache: hits from HBM, misses from the shard
+    px.ccache->cc->gather(f->table, f->row_map, w.owner_final, &plan->meta_at(0, L)->n_dst,
+                          px.rstage_rows, px.rstage, plan->stream);
+  } else {
+    launch_gather(f->table, vec_bytes_for(f->row_bytes), f->row_bytes, w.owner_final,
+                  &plan->meta_at(0, L)->n_dst, px.rstage_rows, f->row_map, px.rstage,
+                  plan->stream);
+  }
   if (g < 0) launch_px_barrier(px.bar, plan->stream);
   else px_enqueue_barrier(plan, L + 1, g & 1);
   PxCaps caps;
@@ -613,6 +618,22 @@ int cb_px_set_cache(cb_plan* plan, cb_cache* cache) {
       require(cache->lru->n_keys() >= plan->g->g.n, "cache key space smaller than the graph");
     }
     px.cache = cache;
+  });
+}
+
+int cb_px_set_clock_cache(cb_plan* plan, cb_ccache* cache) {
+  return guard([&] {
+    require(plan != nullptr, "null plan");
+    PxState& px = px_of(plan);
+    if (cache) {
+      require(px.stage_store != nullptr, "call cb_px_setup_staging first");
+      require(cache->cc->row_bytes() == px.stage_store->row_bytes,
+              "cache row size does not match the feature table");
+      DeviceGuard dg(plan->device);
+      cache->cc->reserve(px.rstage_rows);
+    }
+    px.drop_graphs();  // captured steps baked the uncached staging in
+    px.ccache = cache;
   });
 }
 

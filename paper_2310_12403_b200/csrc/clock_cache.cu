@@ -161,15 +161,18 @@ ClockCache::~ClockCache() {
     if (p) cudaFree(p);
 }
 
+void ClockCache::reserve(uint64_t cap) {
+  if (slot_cap_ >= cap) return;
+  if (slot_) cuda_check(cudaFree(slot_), "cudaFree");
+  slot_cap_ = cap;
+  cuda_check(cudaMalloc(&slot_, cap * 4), "cudaMalloc");
+}
+
 void ClockCache::gather(const void* table, const uint32_t* row_map, const uint32_t* d_ids,
                         const unsigned long long* d_count, uint64_t cap, void* d_out,
                         cudaStream_t st) {
   if (cap == 0) return;
-  if (slot_cap_ < cap) {
-    if (slot_) cuda_check(cudaFree(slot_), "cudaFree");
-    slot_cap_ = cap;
-    cuda_check(cudaMalloc(&slot_, cap * 4), "cudaMalloc");
-  }
+  reserve(cap);
   ++epoch_;
   const unsigned grid = cbdev::kNumSMs * 8;
   launch_k(clock_lookup_kernel, grid, 256, st, view_, d_ids, d_count, cap, slot_, epoch_, ctr_);

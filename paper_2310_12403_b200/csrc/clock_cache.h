@@ -28,6 +28,8 @@ class ClockCache {
   // table + row_map[v] * row_bytes (row_map nullptr: v); misses are inserted.
   void gather(const void* table, const uint32_t* row_map, const uint32_t* d_ids,
               const unsigned long long* d_count, uint64_t cap, void* d_out, cudaStream_t st);
+  // per-batch scratch for up to cap ids, allocated now (before a capture)
+  void reserve(uint64_t cap);
   // running totals (synchronises st)
   void counters(cudaStream_t st, uint64_t* hits, uint64_t* inserted);
   uint64_t capacity() const { return static_cast<uint64_t>(view_.n_sets) * view_.ways; }

@@ -406,6 +406,17 @@ class PeerCoop:
                                    row_bytes=self.store.row_bytes)
             _check(self.L.cb_px_set_requester_cache(self._h, self.rcache._h))
 
+    def enable_clock_cache(self, capacity: int, ways: int = 8):
+        """The CLOCK cache (cb_ccache_*) in front of this owner's staging: the
+        cached fetch becomes part of the captured step (no host round trip).
+        Call before capture()."""
+        from .cache import ClockCache
+        if self.store is None:
+            raise ValueError("PeerCoop.enable_clock_cache needs the rank's feature shard")
+        self.ccache = ClockCache(capacity, self.store.row_bytes, self.g.device, ways)
+        _check(self.L.cb_px_set_clock_cache(self._h, self.ccache._h))
+        self._captured = False
+
     def requester_stats(self) -> tuple[int, int, int]:
         """Last cached fetch, requester side: (remote rows, hits, misses)."""
         r, h, m = C.c_uint64(), C.c_uint64(), C.c_uint64()

@@ -195,3 +195,45 @@ def test_peer_coop_owner_cache(gpu, world, kappa, steps, captured, host_tier, rc
     (the reference LruCache fed access_order(remote, hstep(key, tag)) must
     agree) and only its misses are pulled over peer memory."""
     spawn(world, _px_cache_worker, (kappa, steps, captured, host_tier, rcap), timeout=600)
+
+
+def _px_clock_worker(rank, world, kappa, steps):
+    import paper_2310_12403_b200 as cb
+    from oracle import oracle as O
+    from paper_2310_12403_b200.dist import PeerCoop, synth_shard
+    from tests.dist_harness import check_rank
+
+    n, m, gseed = 1 << 14, 1 << 17, 21
+    g = cb.Graph.generate_rmat(n, m, gseed)
+    ref = O.rmat(n, m, gseed)
+    pm = cb.partition_random(g, world, 6)
+    L, dim, dtype, fseed = 2, 24, "f16", 5
+    store = synth_shard(g, pm, rank, dim, fseed, dtype)
+    cfg = cb.SamplerConfig(cb.SamplerKind.kLabor0, fanouts=[10, 10])
+    pc = PeerCoop(g, pm, rank, L, cfg, max_seeds=4096, store=store)
+    store.set_tier(True)
+    pc.enable_clock_cache(800)
+    sched = cb.SeedSchedule.make(kappa, 8)
+    seeds = O.draw_coop_seeds(pm.owner, world, 96, 6, 0)
+    for step in range(steps):
+        if step == 0:
+            pc.sample(seeds[rank], sched)
+            pc.load_inputs()
+        else:
+            if step == 1:
+                pc.capture(len(seeds[rank]), sched)
+            pc.step(seeds[rank], sched)  # sampling + cached row fetch in one graph
+        res, rows = pc.result(), pc.rows()
+        exp = O.coop_sample(ref, pm.owner, world, seeds, L, O.LABOR0, 10,
+                            O.Sched(sched.kappa, sched.z1, sched.z2, sched.iteration))
+        check_rank(res, rows, exp, rank, world, L, fseed, dim, dtype)
+        sched = cb.schedule_advance(sched)
+    hits, ins, _ = pc.ccache.stats()
+    assert hits > 0 and ins > 0
+
+
+def test_peer_coop_clock_cache_captured(gpu):
+    """The owner-side CLOCK cache inside the captured step (shards in the host
+    tier): rows bit-exact vs the oracle every step, and the dependent batches
+    hit the cache."""
+    spawn(2, _px_clock_worker, (4, 5), timeout=600)
