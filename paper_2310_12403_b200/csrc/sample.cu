@@ -689,6 +689,12 @@ constexpr int kMarkRecs = CB_MARK_RECS;
 #ifndef CB_PURE_STAGES
 #define CB_PURE_STAGES 1
 #endif
+// sub-tiles per single-record tile: the ring holds CB_PURE_STAGES stages of
+// kLaborTile / CB_PURE_PARTS positions per warp
+#ifndef CB_PURE_PARTS
+#define CB_PURE_PARTS 1
+#endif
+constexpr int kPureParts = CB_PURE_PARTS;
 // phase A work split: 0 = static (warp gw takes entries gw, gw + W, ...),
 // G > 0 = G entries at a time from a ticket
 #ifndef CB_PURE_GRAB
@@ -705,7 +711,7 @@ constexpr int kMarkRecs = CB_MARK_RECS;
 constexpr int kMixedWarpDiv = CB_MIXED_WARP_DIV;
 
 constexpr int kPureStages = CB_PURE_STAGES;     // id tiles in flight per warp
-constexpr uint32_t kPureStride = kLaborTile + 8;  // u32 per ring stage (alignment slack)
+constexpr uint32_t kPureStride = kLaborTile / kPureParts + 8;  // u32 per stage (+ alignment slack)
 
 // labor_mark's dynamic shared memory: phase B (records, ids, tile list) and
 // phase A (per-warp id rings) reuse the same bytes one after the other.
@@ -735,6 +741,10 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
                                           unsigned role, unsigned ncta, uint32_t* ring,
                                           uint64_t* bars) {
   constexpr uint32_t TILE = kLaborTile;
+  constexpr uint32_t PARTS = kPureParts;   // sub-tiles per tile (ring stages per tile)
+  constexpr uint32_t SUB = TILE / PARTS;   // positions per sub-tile
+  constexpr uint32_t WPS = SUB / 32;       // keep words per sub-tile
+  static_assert(WPS >= 1 && WPS <= 32 && TILE % PARTS == 0, "sub-tile shape");
   constexpr uint32_t WPC = kMarkNT / 32;
   const uint32_t lane = lane_id();
   const uint64_t W = static_cast<uint64_t>(ncta) * WPC;
@@ -781,32 +791,45 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
       di = __ldg(&a.act[tr.y].di);
     }
     const uint32_t mask = __ballot_sync(0xffffffffu, have);
-    uint32_t im = mask;  // tiles of this batch still to issue, in lane order
-    // bulk copy of the tile owned by lane `src` into stage s (lane 0 issues)
-    auto issue = [&](uint32_t src, int s) {
-      const uint64_t r = __shfl_sync(0xffffffffu, row, src);
+    // work items: each listed tile in lane order, as PARTS sub-tiles of SUB
+    // positions (WPS keep words) each, one ring stage per sub-tile
+    uint32_t im = mask;  // items still to issue: lane __ffs(im) - 1, sub-tile ih
+    uint32_t ih = 0;
+    // bulk copy of item (lane `src`, sub-tile h) into stage s (lane 0 issues)
+    auto issue = [&](uint32_t src, uint32_t h, int s) {
+      const uint64_t r = __shfl_sync(0xffffffffu, row, src) + h * SUB;
       if (lane == 0) {
         const uint32_t* first = a.indices + r;
         const uintptr_t lo = reinterpret_cast<uintptr_t>(first) & ~static_cast<uintptr_t>(15);
         const uint32_t delta = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(first) - lo) >> 2);
         bulk_g2s(ring + s * kPureStride, reinterpret_cast<const void*>(lo),
-                 ((TILE + delta) * 4u + 15u) & ~15u, &bars[s]);
+                 ((SUB + delta) * 4u + 15u) & ~15u, &bars[s]);
+      }
+    };
+    auto issue_next = [&](int s) {
+      issue(__ffs(im) - 1, ih, s);
+      if (++ih == PARTS) {
+        ih = 0;
+        im &= im - 1;
       }
     };
     int s_issue = 0;
     for (int q = 0; q < NS && im; ++q) {
-      issue(__ffs(im) - 1, s_issue);
-      im &= im - 1;
+      issue_next(s_issue);
       s_issue = s_issue + 1 == NS ? 0 : s_issue + 1;
     }
-    uint32_t cm = mask;
+    uint32_t cm = mask, ch = 0;
     int s = 0;
     while (cm) {
       const uint32_t src = __ffs(cm) - 1;
-      cm &= cm - 1;
-      const uint64_t r = __shfl_sync(0xffffffffu, row, src);
+      const uint32_t h = ch;
+      if (++ch == PARTS) {
+        ch = 0;
+        cm &= cm - 1;
+      }
+      const uint64_t r = __shfl_sync(0xffffffffu, row, src) + h * SUB;
       const uint64_t Tq = __shfl_sync(0xffffffffu, T, src);
-      const uint64_t xq = __shfl_sync(0xffffffffu, x0, src);
+      const uint64_t xq = __shfl_sync(0xffffffffu, x0, src) + h * SUB;
       const uint32_t dq = __shfl_sync(0xffffffffu, di, src);
       const uint32_t delta = static_cast<uint32_t>(
           (reinterpret_cast<uintptr_t>(a.indices + r) & 15u) >> 2);
@@ -816,14 +839,15 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
       // prefilter pass bits (yhi <= b2 <=> (yhi >> 1) <= (T >> 33)), then the
       // exact test for the few survivors
       const uint32_t b2 = static_cast<uint32_t>(Tq >> 32) | 1u;
-      uint32_t cand = 0;  // bit 31 - j: position j passed
+      uint32_t cand = 0;  // bit WPS - 1 - j: position j passed
 #pragma unroll 8
 #ifdef CB_NO_CARRY_SPLIT
-      for (int j = 0; j < 32; ++j) cand = shift_in_pass(cand, b2, mix64_yhi(p1, ids[32 * j]));
+      for (uint32_t j = 0; j < WPS; ++j) cand = shift_in_pass(cand, b2, mix64_yhi(p1, ids[32 * j]));
 #else
-      for (int j = 0; j < 32; ++j) cand = shift_in_pass(cand, b2, mix64_yhi_cs(yk, ids[32 * j]));
+      for (uint32_t j = 0; j < WPS; ++j)
+        cand = shift_in_pass(cand, b2, mix64_yhi_cs(yk, ids[32 * j]));
 #endif
-      uint32_t km = __brev(cand);
+      uint32_t km = __brev(cand) >> (32 - WPS);
       ++dbg_tiles;
       dbg_surv += __popc(km);
       for (uint32_t kk = km; kk;) {
@@ -834,9 +858,9 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
       uint32_t my_word = 0;
       if (__any_sync(0xffffffffu, km != 0)) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (uint32_t j = 0; j < WPS; ++j) {
           const unsigned bal = __ballot_sync(0xffffffffu, (km >> j) & 1u);
-          if (lane == static_cast<uint32_t>(j)) my_word = bal;
+          if (lane == j) my_word = bal;
         }
         uint32_t kk = km;
         while (kk) {
@@ -847,12 +871,9 @@ __device__ __forceinline__ void mark_pure(const LaborArgs& a, uint64_t p1, uint6
           a.stage[xq + lane + 32 * j] = make_uint2(v, dq);
         }
       }
-      a.keep_words[(xq >> 5) + lane] = my_word;
+      if (lane < WPS) a.keep_words[(xq >> 5) + lane] = my_word;
       __syncwarp();  // every lane is done with stage s
-      if (im) {
-        issue(__ffs(im) - 1, s);
-        im &= im - 1;
-      }
+      if (im) issue_next(s);
       s = s + 1 == NS ? 0 : s + 1;
     }
   }
@@ -877,7 +898,7 @@ __device__ __forceinline__ void mark_mixed_warp(const LaborArgs& a, const Variat
   constexpr uint32_t TILE = kLaborTile;
   constexpr uint32_t WSPAN = 32 * IPT;
   constexpr uint32_t WPC = kMarkNT / 32;
-  constexpr uint32_t kRecsW = (kPureStride * 4) / sizeof(ActRec);
+  constexpr uint32_t kRecsW = (kPureStages * kPureStride * 4) / sizeof(ActRec);  // the warp ring
   const uint32_t lane = lane_id();
   const uint64_t W = static_cast<uint64_t>(ncta) * WPC;
   const uint64_t gw = static_cast<uint64_t>(role) * WPC + (threadIdx.x >> 5);
