@@ -310,7 +310,11 @@ constexpr uint64_t kExtractBigWords = 256 * 1024;  // summary-mode threshold
 constexpr int kMarkNT = CB_MARK_NT;                // labor_mark block size
 constexpr int kLaborTile = kMarkNT * CB_MARK_IPT;  // scan positions per mark tile
 constexpr uint64_t kVtabMaxVerts = 1ULL << 26;  // smoothed variate table cap (512 MiB)
-constexpr int kFrontierTile = 1024;
+#ifndef CB_FRONTIER_IPT
+#define CB_FRONTIER_IPT 4
+#endif
+constexpr int kFrontierIPT = CB_FRONTIER_IPT;  // destinations per frontier thread
+constexpr int kFrontierTile = 256 * kFrontierIPT;
 // Scan positions one layer may hold before the overflow retry doubles it
 // (stage 8 B + keep bit per position: ~1.1 GB per part).
 constexpr uint64_t kScanBudget = 1ULL << 27;

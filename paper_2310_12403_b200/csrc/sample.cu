@@ -1735,7 +1735,6 @@ __global__ void clear_kernel(uint32_t* bits, uint32_t* summ, const uint32_t* __r
   }
 }
 
-constexpr int kFrontierIPT = 4;
 constexpr int kLaborIPT = kLaborTile / kNT;      // NS reservoir tiles
 constexpr int kMarkIPT = kLaborTile / kMarkNT;   // labor_mark
 
