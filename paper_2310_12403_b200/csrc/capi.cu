@@ -220,7 +220,7 @@ void resolve_alloc(cb_plan* pl) {
   r.pend = pl->rs_pend;
   r.n_pend = pl->rs_npend;
   r.perturb = pl->perturb;
-  CB_CUDA(cudaMemcpy(pl->d_rs, &r, sizeof(r), cudaMemcpyHostToDevice));
+  h2d_sync(pl->d_rs, &r, sizeof(r));
 }
 
 // The same variates for every part (the reference's single schedule), or one
@@ -762,9 +762,9 @@ void resolve_upload(cb_plan* pl, const std::map<std::pair<uint64_t, uint64_t>, d
     val.push_back(x);
   }
   if (n) {
-    CB_CUDA(cudaMemcpy(pl->rs_k1, k1.data(), 8ULL * n, cudaMemcpyHostToDevice));
-    CB_CUDA(cudaMemcpy(pl->rs_k2, k2.data(), 8ULL * n, cudaMemcpyHostToDevice));
-    CB_CUDA(cudaMemcpy(pl->rs_val, val.data(), 8ULL * n, cudaMemcpyHostToDevice));
+    CB_CUDA(cudaMemcpyAsync(pl->rs_k1, k1.data(), 8ULL * n, cudaMemcpyHostToDevice, st));
+    CB_CUDA(cudaMemcpyAsync(pl->rs_k2, k2.data(), 8ULL * n, cudaMemcpyHostToDevice, st));
+    CB_CUDA(cudaMemcpyAsync(pl->rs_val, val.data(), 8ULL * n, cudaMemcpyHostToDevice, st));
   }
   cbdev::Resolve r{};
   r.k1 = pl->rs_k1;
@@ -776,7 +776,7 @@ void resolve_upload(cb_plan* pl, const std::map<std::pair<uint64_t, uint64_t>, d
   r.n_pend = pl->rs_npend;
   r.perturb = pl->perturb;
   CB_CUDA(cudaMemcpyAsync(pl->d_rs, &r, sizeof(r), cudaMemcpyHostToDevice, st));
-  CB_CUDA(cudaStreamSynchronize(st));  // r lives on this stack frame
+  CB_CUDA(cudaStreamSynchronize(st));  // r and the key vectors live on this frame
 }
 
 uint64_t pending_count(cb_plan* pl) {
@@ -916,8 +916,8 @@ int cb_graph_create_from_csr(const uint64_t* indptr, const uint32_t* indices, ui
     CB_CUDA(cudaMalloc(&h->g.indptr, (n + 1) * 8));
     // +16 B: labor_mark bulk-copies 16-byte-aligned supersets of id ranges
     CB_CUDA(cudaMalloc(&h->g.indices, std::max<uint64_t>(m, 1) * 4 + 16));
-    CB_CUDA(cudaMemcpy(h->g.indptr, indptr, (n + 1) * 8, cudaMemcpyHostToDevice));
-    if (m) CB_CUDA(cudaMemcpy(h->g.indices, indices, m * 4, cudaMemcpyHostToDevice));
+    h2d_sync(h->g.indptr, indptr, (n + 1) * 8);
+    if (m) h2d_sync(h->g.indices, indices, m * 4);
     uint64_t md = 0;
     for (uint64_t v = 0; v < n; ++v) md = std::max(md, indptr[v + 1] - indptr[v]);
     h->g.max_degree = md;
@@ -941,7 +941,7 @@ int cb_graph_set_weights(cb_graph* g, const float* weights) {
     g->weights_mem = std::make_unique<Arena>();
     g->g.weights = g->weights_mem->alloc<float>(std::max<uint64_t>(g->g.m, 1));
     if (g->g.m)
-      CB_CUDA(cudaMemcpy(g->g.weights, weights, g->g.m * 4, cudaMemcpyHostToDevice));
+      h2d_sync(g->g.weights, weights, g->g.m * 4);
   });
 }
 
@@ -1081,7 +1081,7 @@ static void finish_partition(cb_partition* pm) {
   CB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   std::vector<uint32_t> iota(n);
   for (uint64_t v = 0; v < n; ++v) iota[v] = static_cast<uint32_t>(v);
-  CB_CUDA(cudaMemcpy(ids, iota.data(), n * 4, cudaMemcpyHostToDevice));
+  h2d_sync(ids, iota.data(), n * 4);
   uint32_t* keys = pm->mem.alloc<uint32_t>(n);
   CB_CUDA(cudaMemcpy(keys, pm->owner, n * 4, cudaMemcpyDeviceToDevice));
   // the copies above run on the legacy stream (D2D and staged pageable H2D
@@ -1106,8 +1106,8 @@ static void finish_partition(cb_partition* pm) {
   for (uint32_t q = 0; q < pm->parts; ++q) pm->shard_off[q + 1] += pm->shard_off[q];
   std::vector<uint32_t> row_map(n);
   for (uint64_t i = 0; i < n; ++i) row_map[members[i]] = static_cast<uint32_t>(i);
-  CB_CUDA(cudaMemcpy(pm->members, members.data(), n * 4, cudaMemcpyHostToDevice));
-  CB_CUDA(cudaMemcpy(pm->row_map, row_map.data(), n * 4, cudaMemcpyHostToDevice));
+  h2d_sync(pm->members, members.data(), n * 4);
+  h2d_sync(pm->row_map, row_map.data(), n * 4);
   CB_CUDA(cudaStreamDestroy(st));
 }
 
@@ -1143,7 +1143,7 @@ int cb_partition_create(const cb_graph* g, const uint32_t* owner, uint32_t parts
     pm->n = g->g.n;
     pm->parts = parts;
     pm->owner = pm->mem.alloc<uint32_t>(pm->n);
-    CB_CUDA(cudaMemcpy(pm->owner, owner, pm->n * 4, cudaMemcpyHostToDevice));
+    h2d_sync(pm->owner, owner, pm->n * 4);
     finish_partition(pm.get());
     *out = pm.release();
   });

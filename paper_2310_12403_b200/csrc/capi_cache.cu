@@ -219,8 +219,7 @@ int cb_features_set_tier(cb_features* f, int host) {
       f->host_base = h;
       f->table = static_cast<unsigned char*>(d) - off;
     } else {
-      CB_CUDA(cudaMemcpy(static_cast<unsigned char*>(f->hbm_table) + off, f->host_base, bytes,
-                         cudaMemcpyHostToDevice));
+      h2d_sync(static_cast<unsigned char*>(f->hbm_table) + off, f->host_base, bytes);
       CB_CUDA(cudaFreeHost(f->host_base));
       f->host_base = nullptr;
       f->table = f->hbm_table;

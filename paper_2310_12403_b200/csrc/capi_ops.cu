@@ -328,7 +328,7 @@ int cb_features_from_host(int device, uint64_t n_rows, uint32_t dim, int dtype, 
     f->n_rows = n_rows;
     f->table = f->mem.alloc<unsigned char>(std::max<uint64_t>(n_rows, 1) * f->row_bytes);
     if (n_rows)
-      CB_CUDA(cudaMemcpy(f->table, rows, n_rows * f->row_bytes, cudaMemcpyHostToDevice));
+      h2d_sync(f->table, rows, n_rows * f->row_bytes);
     *out = f.release();
   });
 }
@@ -345,7 +345,7 @@ int cb_features_set_labels(cb_features* f, const uint32_t* labels) {
     }
     if (!f->labels) f->labels = f->mem.alloc<uint32_t>(std::max<uint64_t>(f->n_rows, 1));
     if (f->n_rows)
-      CB_CUDA(cudaMemcpy(f->labels, labels, f->n_rows * 4, cudaMemcpyHostToDevice));
+      h2d_sync(f->labels, labels, f->n_rows * 4);
   });
 }
 

@@ -515,8 +515,7 @@ int cb_px_connect_features(cb_plan* plan, uint32_t q, const void* handle, uint64
       px.fopened.push_back(p);
       px.fbase[q] = static_cast<const unsigned char*>(p) - shard_r0 * local->row_bytes;
     }
-    CB_CUDA(cudaMemcpy(px.d_fbase, px.fbase.data(), kMaxParts * sizeof(void*),
-                       cudaMemcpyHostToDevice));
+    h2d_sync(px.d_fbase, px.fbase.data(), kMaxParts * sizeof(void*));
   });
 }
 
@@ -581,8 +580,7 @@ int cb_px_setup_staging(cb_plan* plan, const cb_features* local, void* handle_ou
     if (!px.d_rstage) CB_CUDA(cudaMalloc(&px.d_rstage, kMaxParts * sizeof(void*)));
     px.rstage_of.assign(kMaxParts, nullptr);
     px.rstage_of[px.rank] = static_cast<const unsigned char*>(px.rstage);
-    CB_CUDA(cudaMemcpy(px.d_rstage, px.rstage_of.data(), kMaxParts * sizeof(void*),
-                       cudaMemcpyHostToDevice));
+    h2d_sync(px.d_rstage, px.rstage_of.data(), kMaxParts * sizeof(void*));
     cudaIpcMemHandle_t h;
     CB_CUDA(cudaIpcGetMemHandle(&h, px.rstage));
     std::memcpy(handle_out, &h, sizeof(h));
@@ -602,8 +600,7 @@ int cb_px_connect_staging(cb_plan* plan, uint32_t q, const void* handle) {
     CB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     px.ropened.push_back(p);
     px.rstage_of[q] = static_cast<const unsigned char*>(p);
-    CB_CUDA(cudaMemcpy(px.d_rstage, px.rstage_of.data(), kMaxParts * sizeof(void*),
-                       cudaMemcpyHostToDevice));
+    h2d_sync(px.d_rstage, px.rstage_of.data(), kMaxParts * sizeof(void*));
   });
 }
 

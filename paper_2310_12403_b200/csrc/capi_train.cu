@@ -52,7 +52,7 @@ int cb_gcn_model_init(int device, uint32_t in_dim, uint32_t hidden, uint32_t cla
         }
       double* d = nullptr;
       CB_CUDA(cudaMalloc(&d, w.size() * 8));
-      CB_CUDA(cudaMemcpy(d, w.data(), w.size() * 8, cudaMemcpyHostToDevice));
+      h2d_sync(d, w.data(), w.size() * 8);
       m->rows.push_back(rows);
       m->cols.push_back(cols);
       m->w.push_back(d);
@@ -81,7 +81,7 @@ int cb_gcn_model_create(int device, int num_layers, const uint32_t* rows, const 
       double* p = nullptr;
       CB_CUDA(cudaMalloc(&p, std::max<uint64_t>(n, 1) * 8));
       m->w.push_back(p);
-      if (weights && n) CB_CUDA(cudaMemcpy(p, weights + o, n * 8, cudaMemcpyHostToDevice));
+      if (weights && n) h2d_sync(p, weights + o, n * 8);
       o += n;
     }
     *out = m.release();
@@ -98,7 +98,7 @@ int cb_gcn_model_weights(cb_model* m, int layer, double* host, int upload, uint6
     if (rows) *rows = m->rows[layer];
     if (cols) *cols = m->cols[layer];
     if (!host) return;
-    if (upload) CB_CUDA(cudaMemcpy(m->w[layer], host, n * 8, cudaMemcpyHostToDevice));
+    if (upload) h2d_sync(m->w[layer], host, n * 8);
     else CB_CUDA(cudaMemcpy(host, m->w[layer], n * 8, cudaMemcpyDeviceToHost));
   });
 }

@@ -41,6 +41,16 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define CB_CUDA(x) ::cb::cuda_check((x), #x)
 #define CB_LAUNCH(what) ::cb::cuda_check(cudaGetLastError(), what)
 
+// Host-to-device upload that is complete on return. A plain cudaMemcpy from
+// pageable memory runs on the legacy stream and may return while the DMA from
+// its staging buffer is still in flight; the library's kernels run on
+// non-blocking streams that do not wait for the legacy stream.
+inline void h2d_sync(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+  cuda_check(cudaStreamSynchronize(0), "cudaStreamSynchronize(legacy)");
+}
+
 // Scoped device allocation, freed on every exit path (exceptions included).
 class DevBuf {
  public:
