@@ -220,6 +220,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// trace[63*8 + 7] = the latest end of any CTA of the kernel (thread 0 of each)
+__device__ __forceinline__ void tlast(unsigned long long* trace) {
+  if (trace && threadIdx.x == 0) atomicMax(trace + 63 * 8 + 7, gtimer());
+}
 // trace[cta*8 + k] = time stamp k of this CTA (first writer per slot wins)
 __device__ __forceinline__ void tstamp(unsigned long long* trace, unsigned cta, int k) {
   if (trace && cta < 64 && threadIdx.x == 0) trace[cta * 8 + k] = gtimer();

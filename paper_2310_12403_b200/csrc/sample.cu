@@ -221,6 +221,7 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
       bp = __shfl_sync(0xffffffffu, base_p, 31) + ip - tnp;
       bm = __shfl_sync(0xffffffffu, base_m, 31) + im2 - tmix;
     }
+    if (tile == role) tstamp(a.trace, role, 5);  // list slots known
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const uint64_t i = i0 + j;
@@ -324,6 +325,7 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
     }
   }
   tstamp(a.trace, role, 4);
+  tlast(a.trace);
   if (n == 0 && role == 0 && threadIdx.x == 0) {
     ActRec sent{};
     a.act[0] = sent;
@@ -438,6 +440,94 @@ __device__ __forceinline__ bool keep_rule(const Variates& v, uint64_t p1, uint64
   return rr <= thr;
 }
 
+// phase-B spans (mark_span, plain stream) with phase A's high-word
+// prefilter: bit 0 spans inside one record, bit 1 spans across records.
+// Off: A/B at c4, last-layer mark 81.7 (off) / 83.9 (1) / 92.5 (3) us --
+// mixed tiles are mostly low-degree records whose positions pass the
+// prefilter and then pay the exact hash as well.
+#ifndef CB_SPAN_PREFILTER
+#define CB_SPAN_PREFILTER 0
+#endif
+constexpr int kSpanPrefilter = CB_SPAN_PREFILTER;
+
+// High word of y = z * c2, the last SplitMix64 multiply of mix64(p1 ^ t)
+// (z after the second xor-shift): keep_plain's prefilter input.
+__device__ __forceinline__ uint32_t mix64_yhi(uint64_t p1, uint32_t t) {
+  uint64_t x = (p1 ^ t) + 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = x ^ (x >> 27);
+  const uint32_t zlo = static_cast<uint32_t>(x), zhi = static_cast<uint32_t>(x >> 32);
+  return __umulhi(zlo, 0x133111ebu) + zlo * 0x94d049bbu + zhi * 0x133111ebu;
+}
+
+// Carry-split form of mix64_yhi for a layer prefix p1 and a 32-bit id t.
+// x = (p1 ^ t) + C0: t only touches the low word, so the high word is
+// H + cy (cy = the carry out of the low add). After x ^= x >> 30 the high
+// word's contribution to the first product's high half, (hi ^ hi >> 30) *
+// 0x1ce4e5b9, is one of two per-layer constants K[cy]: one select instead of
+// a shift, an xor and a multiply. Bit-exact with mix64_yhi.
+struct YhiConst {
+  uint32_t p1lo, Q0, Q1, K0, K1;
+};
+__host__ __device__ __forceinline__ YhiConst yhi_const(uint64_t p1) {
+  YhiConst k;
+  k.p1lo = static_cast<uint32_t>(p1);
+  const uint32_t h0 = static_cast<uint32_t>(p1 >> 32) + 0x9e3779b9u, h1 = h0 + 1u;
+  k.Q0 = h0 << 2;  // the high word's bits in the low word of x >> 30
+  k.Q1 = h1 << 2;
+  k.K0 = (h0 ^ (h0 >> 30)) * 0x1ce4e5b9u;
+  k.K1 = (h1 ^ (h1 >> 30)) * 0x1ce4e5b9u;
+  return k;
+}
+// K0 / K1 pass through an opaque move: otherwise the compiler sinks their
+// multiply past the select (select(a, b) * c), one IMAD more per position.
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  uint32_t r;
+  asm("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t mix64_yhi_cs(const YhiConst& k, uint32_t t) {
+  uint32_t lo, cy;
+  asm("add.cc.u32 %0, %2, 0x7f4a7c15;\n\taddc.u32 %1, 0, 0;"
+      : "=r"(lo), "=r"(cy)
+      : "r"(k.p1lo ^ t));
+  const bool c = cy != 0;
+  const uint32_t xl = lo ^ (lo >> 30) ^ (c ? k.Q1 : k.Q0);  // disjoint bits: | == ^
+  const uint32_t hk = c ? k.K1 : k.K0;
+  const uint32_t zl0 = xl * 0x1ce4e5b9u;
+  const uint32_t zh0 = __umulhi(xl, 0x1ce4e5b9u) + xl * 0xbf58476du + hk;
+  const uint32_t zlo = zl0 ^ __funnelshift_r(zl0, zh0, 27);
+  const uint32_t zhi = zh0 ^ (zh0 >> 27);
+  return __umulhi(zlo, 0x133111ebu) + zlo * 0x94d049bbu + zhi * 0x133111ebu;
+}
+
+// acc = 2 * acc + (yhi <= b2): the prefilter pass bit shifted in through
+// the carry of b2 - yhi (one subtract with carry-out, one add with carry-in)
+__device__ __forceinline__ uint32_t shift_in_pass(uint32_t acc, uint32_t b2, uint32_t yhi) {
+  uint32_t r;
+  asm("{\n .reg .u32 t;\n sub.cc.u32 t, %1, %2;\n addc.u32 %0, %3, %3;\n}"
+      : "=r"(r)
+      : "r"(b2), "r"(yhi), "r"(acc));
+  return r;
+}
+
+// Plain-stream keep test with a high-word prefilter. out = y ^ (y >> 31) for
+// y = z * c2 (the last SplitMix64 round), so out's top 31 bits are y's: when
+// (y_hi >> 1) > (T_hi >> 1) the position is rejected without the final
+// xor-shift and the 64-bit compare. Only survivors (about T / 2^64 of the
+// positions: k/d of a hub's) finish the hash. Exact: same result as
+// mix64(p1 ^ t) <= T.
+__device__ __forceinline__ bool keep_plain(uint64_t p1, uint32_t t, uint64_t T) {
+  uint64_t x = (p1 ^ t) + 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = x ^ (x >> 27);
+  const uint32_t zlo = static_cast<uint32_t>(x), zhi = static_cast<uint32_t>(x >> 32);
+  const uint32_t yhi = __umulhi(zlo, 0x133111ebu) + zlo * 0x94d049bbu + zhi * 0x133111ebu;
+  if ((yhi >> 1) > static_cast<uint32_t>(T >> 33)) return false;
+  const uint64_t y = x * 0x94d049bb133111ebULL;
+  return (y ^ (y >> 31)) <= T;
+}
+
 // Per-warp body of labor_mark: IPT words of 32 consecutive positions starting
 // at tile-relative offset r0. Records come either from smem (STAGED) or
 // straight from the global record array (tiles spanning > kRecs records).
@@ -449,7 +539,8 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
                                           uint64_t p2, uint64_t x0, uint32_t r0, uint32_t rend,
                                           uint32_t a0, uint32_t a1, uint32_t cur,
                                           const ActRec* s_act, uint32_t nd,
-                                          unsigned long long& uncert, const double* vtab) {
+                                          unsigned long long& uncert, const double* vtab,
+                                          const YhiConst& yk) {
   static_assert(IPT <= 32, "one word per lane");
   const uint32_t lane = lane_id();
   auto nxt_of = [&](uint32_t c) -> uint32_t {  // tile-relative start of record c+1
@@ -483,15 +574,46 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
     uint32_t tv[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) tv[j] = __ldg(row + j * 32);
+    if constexpr (!SMOOTH && (kSpanPrefilter & 1)) {
+      // phase A's test: high-word prefilter, the exact hash for survivors
+      // only (re-read: row is L1-hot), ballots only when the warp kept any
+      const uint32_t b2 = static_cast<uint32_t>(T >> 32) | 1u;
+      uint32_t cand = 0;
 #pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-      const bool keep = SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab, a.layer)
-                               : mix64_dev(p1 ^ tv[j]) <= T;
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (lane == j) my_word = bal;
-      if (keep) {
-        set_bit(a.bits, a.summ, tv[j]);
-        st_lane[j * 32] = make_uint2(tv[j], di);
+      for (int j = 0; j < IPT; ++j) cand = shift_in_pass(cand, b2, mix64_yhi_cs(yk, tv[j]));
+      uint32_t km = __brev(cand) >> (32 - IPT);
+      for (uint32_t kk = km; kk;) {
+        const int j = __ffs(kk) - 1;
+        kk &= kk - 1;
+        if (!keep_plain(p1, __ldg(row + j * 32), T)) km &= ~(1u << j);
+      }
+      if (__any_sync(0xffffffffu, km != 0)) {
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+          const unsigned bal = __ballot_sync(0xffffffffu, (km >> j) & 1u);
+          if (lane == j) my_word = bal;
+        }
+        for (uint32_t kk = km; kk;) {
+          const int j = __ffs(kk) - 1;
+          kk &= kk - 1;
+          const uint32_t t = __ldg(row + j * 32);
+          set_bit(a.bits, a.summ, t);
+          st_lane[j * 32] = make_uint2(t, di);
+        }
+      }
+      if (lane < IPT) a.keep_words[((x0 + r0) >> 5) + lane] = my_word;
+      return;
+    } else {
+#pragma unroll
+      for (int j = 0; j < IPT; ++j) {
+        const bool keep = SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab, a.layer)
+                                 : mix64_dev(p1 ^ tv[j]) <= T;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == j) my_word = bal;
+        if (keep) {
+          set_bit(a.bits, a.summ, tv[j]);
+          st_lane[j * 32] = make_uint2(tv[j], di);
+        }
       }
     }
   } else {
@@ -509,13 +631,23 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
       li[j] = c;
       tv[j] = (r < rend) ? __ldg(row_of(c) + r) : 0u;
     }
+    uint32_t km = 0;  // prefilter survivors (plain stream, kSpanPrefilter & 2)
+    if (!SMOOTH && (kSpanPrefilter & 2)) {
+#pragma unroll
+      for (int j = 0; j < IPT; ++j) {
+        const uint32_t b2 = static_cast<uint32_t>(plain_bound(th_of(li[j])) >> 32) | 1u;
+        const bool pass = r0 + j * 32 + lane < rend && mix64_yhi_cs(yk, tv[j]) <= b2;
+        km |= (pass ? 1u : 0u) << j;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const uint32_t r = r0 + j * 32 + lane;
       const bool keep =
           (r < rend) &&
           (SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th_of(li[j]), uncert, vtab, a.layer)
-                  : mix64_dev(p1 ^ tv[j]) <= plain_bound(th_of(li[j])));
+           : (kSpanPrefilter & 2) ? ((km >> j) & 1u) && keep_plain(p1, tv[j], plain_bound(th_of(li[j])))
+                                  : mix64_dev(p1 ^ tv[j]) <= plain_bound(th_of(li[j])));
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == j) my_word = bal;
       if (keep) {
@@ -602,84 +734,6 @@ __device__ __forceinline__ void mark_span_smem(const LaborArgs& a, const Variate
     }
   }
   if (lane < IPT) a.keep_words[((x0 + r0) >> 5) + lane] = my_word;
-}
-
-// High word of y = z * c2, the last SplitMix64 multiply of mix64(p1 ^ t)
-// (z after the second xor-shift): keep_plain's prefilter input.
-__device__ __forceinline__ uint32_t mix64_yhi(uint64_t p1, uint32_t t) {
-  uint64_t x = (p1 ^ t) + 0x9e3779b97f4a7c15ULL;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  x = x ^ (x >> 27);
-  const uint32_t zlo = static_cast<uint32_t>(x), zhi = static_cast<uint32_t>(x >> 32);
-  return __umulhi(zlo, 0x133111ebu) + zlo * 0x94d049bbu + zhi * 0x133111ebu;
-}
-
-// Carry-split form of mix64_yhi for a layer prefix p1 and a 32-bit id t.
-// x = (p1 ^ t) + C0: t only touches the low word, so the high word is
-// H + cy (cy = the carry out of the low add). After x ^= x >> 30 the high
-// word's contribution to the first product's high half, (hi ^ hi >> 30) *
-// 0x1ce4e5b9, is one of two per-layer constants K[cy]: one select instead of
-// a shift, an xor and a multiply. Bit-exact with mix64_yhi.
-struct YhiConst {
-  uint32_t p1lo, Q0, Q1, K0, K1;
-};
-__host__ __device__ __forceinline__ YhiConst yhi_const(uint64_t p1) {
-  YhiConst k;
-  k.p1lo = static_cast<uint32_t>(p1);
-  const uint32_t h0 = static_cast<uint32_t>(p1 >> 32) + 0x9e3779b9u, h1 = h0 + 1u;
-  k.Q0 = h0 << 2;  // the high word's bits in the low word of x >> 30
-  k.Q1 = h1 << 2;
-  k.K0 = (h0 ^ (h0 >> 30)) * 0x1ce4e5b9u;
-  k.K1 = (h1 ^ (h1 >> 30)) * 0x1ce4e5b9u;
-  return k;
-}
-// K0 / K1 pass through an opaque move: otherwise the compiler sinks their
-// multiply past the select (select(a, b) * c), one IMAD more per position.
-__device__ __forceinline__ uint32_t opaque(uint32_t x) {
-  uint32_t r;
-  asm("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
-  return r;
-}
-__device__ __forceinline__ uint32_t mix64_yhi_cs(const YhiConst& k, uint32_t t) {
-  uint32_t lo, cy;
-  asm("add.cc.u32 %0, %2, 0x7f4a7c15;\n\taddc.u32 %1, 0, 0;"
-      : "=r"(lo), "=r"(cy)
-      : "r"(k.p1lo ^ t));
-  const bool c = cy != 0;
-  const uint32_t xl = lo ^ (lo >> 30) ^ (c ? k.Q1 : k.Q0);  // disjoint bits: | == ^
-  const uint32_t hk = c ? k.K1 : k.K0;
-  const uint32_t zl0 = xl * 0x1ce4e5b9u;
-  const uint32_t zh0 = __umulhi(xl, 0x1ce4e5b9u) + xl * 0xbf58476du + hk;
-  const uint32_t zlo = zl0 ^ __funnelshift_r(zl0, zh0, 27);
-  const uint32_t zhi = zh0 ^ (zh0 >> 27);
-  return __umulhi(zlo, 0x133111ebu) + zlo * 0x94d049bbu + zhi * 0x133111ebu;
-}
-
-// acc = 2 * acc + (yhi <= b2): the prefilter pass bit shifted in through
-// the carry of b2 - yhi (one subtract with carry-out, one add with carry-in)
-__device__ __forceinline__ uint32_t shift_in_pass(uint32_t acc, uint32_t b2, uint32_t yhi) {
-  uint32_t r;
-  asm("{\n .reg .u32 t;\n sub.cc.u32 t, %1, %2;\n addc.u32 %0, %3, %3;\n}"
-      : "=r"(r)
-      : "r"(b2), "r"(yhi), "r"(acc));
-  return r;
-}
-
-// Plain-stream keep test with a high-word prefilter. out = y ^ (y >> 31) for
-// y = z * c2 (the last SplitMix64 round), so out's top 31 bits are y's: when
-// (y_hi >> 1) > (T_hi >> 1) the position is rejected without the final
-// xor-shift and the 64-bit compare. Only survivors (about T / 2^64 of the
-// positions: k/d of a hub's) finish the hash. Exact: same result as
-// mix64(p1 ^ t) <= T.
-__device__ __forceinline__ bool keep_plain(uint64_t p1, uint32_t t, uint64_t T) {
-  uint64_t x = (p1 ^ t) + 0x9e3779b97f4a7c15ULL;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  x = x ^ (x >> 27);
-  const uint32_t zlo = static_cast<uint32_t>(x), zhi = static_cast<uint32_t>(x >> 32);
-  const uint32_t yhi = __umulhi(zlo, 0x133111ebu) + zlo * 0x94d049bbu + zhi * 0x133111ebu;
-  if ((yhi >> 1) > static_cast<uint32_t>(T >> 33)) return false;
-  const uint64_t y = x * 0x94d049bb133111ebULL;
-  return (y ^ (y >> 31)) <= T;
 }
 
 #ifndef CB_MARK_RECS
@@ -903,6 +957,9 @@ __device__ __forceinline__ void mark_mixed_warp(const LaborArgs& a, const Variat
   const uint64_t W = static_cast<uint64_t>(ncta) * WPC;
   const uint64_t gw = static_cast<uint64_t>(role) * WPC + (threadIdx.x >> 5);
   unsigned long long uncert = 0;
+  YhiConst yk = yhi_const(p1);
+  yk.K0 = opaque(yk.K0);
+  yk.K1 = opaque(yk.K1);
   for (uint64_t e = gw; e < n_mixed; e += W) {
     const uint64_t tile = a.tile_list[a.list_cap - 1 - e].x;
     const uint64_t x0 = tile * TILE;
@@ -933,11 +990,11 @@ __device__ __forceinline__ void mark_mixed_warp(const LaborArgs& a, const Variat
           if (step == 1) break;
         }
         mark_span<IPT, false, true>(a, v, p1, 0, x0, r0, rend, a0, a1, lo, wrec, nd, uncert,
-                                    nullptr);
+                                    nullptr, yk);
       } else {
         const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
         mark_span<IPT, false, false>(a, v, p1, 0, x0, r0, rend, a0, a1, cur, nullptr, 0, uncert,
-                                     nullptr);
+                                     nullptr, yk);
       }
     }
   }
@@ -993,11 +1050,15 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
       mark_mixed_warp<IPT>(a, v, p1, n_mixed, total, role, ncta,
                            reinterpret_cast<ActRec*>(&sa.ring[warp][0][0]));
       tstamp(a.trace, trole, 1);
+      tlast(a.trace);
       return;
     }
     __syncthreads();  // the ring memory becomes phase B's
     tstamp(a.trace, trole, 2);
   }
+  YhiConst yk = yhi_const(p1);
+  yk.K0 = opaque(yk.K0);
+  yk.K1 = opaque(yk.K1);
   const uint64_t nb = listed ? (n_mixed > role ? (n_mixed - role + ncta - 1) / ncta : 0)
                              : (ntiles > role ? (ntiles - role + ncta - 1) / ncta : 0);
   // tile of phase-B item i
@@ -1092,7 +1153,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
                                     uncert, vtab);
       } else if (r0 < rend) {
         mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, 0, s_act[rb], nd, uncert,
-                                     vtab);
+                                     vtab, yk);
       }
     } else if (r0 < rend) {
       if (nd <= static_cast<uint32_t>(kRecs)) {
@@ -1110,11 +1171,11 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
           if (step == 1) break;
         }
         mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, sa, nd, uncert,
-                                     vtab);
+                                     vtab, yk);
       } else {
         const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
         mark_span<IPT, SMOOTH, false>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, nullptr, 0,
-                                      uncert, vtab);
+                                      uncert, vtab, yk);
       }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -1133,6 +1194,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   }
   __syncthreads();
   tstamp(a.trace, trole, 1);
+  tlast(a.trace);
 }
 
 template <int IPT, bool SMOOTH>
@@ -1228,6 +1290,7 @@ __device__ __forceinline__ void labor_emit_body(const LaborArgs& a, unsigned rol
     }
   }
   tstamp(trace, 32 + role, 4);
+  tlast(trace_in);
 }
 
 // ---------------------------------------------------------------- NS -------
@@ -1619,6 +1682,7 @@ __device__ __forceinline__ void extract_flat(const ExtractArgs& a, unsigned role
     }
   }
   tstamp(tr, role, 4);
+  tlast(a.trace);
 }
 
 // Summary-driven extraction for large bitmaps: a tile is kNT summary words
@@ -1633,6 +1697,8 @@ __device__ __forceinline__ void extract_summ(const ExtractArgs& a, unsigned role
   const uint64_t swords = a.words_padded / 32;
   const uint64_t ntiles = (swords + kNT - 1) / kNT;
   const unsigned ep = inv_epoch(a.epoch, a.slot);
+  unsigned long long* tr = role < 32 ? a.trace : nullptr;
+  tstamp(tr, role, 0);
   for (unsigned tile = role; tile < ntiles; tile = next_tile_after(a.ticket, &s_tile, ncta, ntiles)) {
     const uint64_t sw = static_cast<uint64_t>(tile) * kNT + threadIdx.x;
     const uint32_t sm = sw < swords ? a.summ[sw] : 0u;
@@ -1654,9 +1720,12 @@ __device__ __forceinline__ void extract_summ(const ExtractArgs& a, unsigned role
         c += __popc(a.bits[sw * 32 + j]);
       }
     }
+    if (tile == role) tstamp(tr, role, 1);
     unsigned long long tot;
     const unsigned long long ex = block_exclusive_scan<kNT>(c, s_scan, tot);
+    if (tile == role) tstamp(tr, role, 2);
     const unsigned long long gb = tile_prefix<4>(a.status, tile, tot, ep, &s_b);
+    if (tile == role) tstamp(tr, role, 3);
     unsigned long long pos = gb + ex;
     uint32_t m = sm;
     while (m) {
@@ -1678,6 +1747,8 @@ __device__ __forceinline__ void extract_summ(const ExtractArgs& a, unsigned role
       if (gb + tot > a.cap_out) atomicExch(a.overflow, 1u);
     }
   }
+  tstamp(tr, role, 4);
+  tlast(a.trace);
 }
 
 __device__ __forceinline__ bool extract_uses_summary(const ExtractArgs& a) {

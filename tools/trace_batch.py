@@ -1,6 +1,6 @@
 """Debug: globaltimer stamps of one batch (CB_TRACE=1) of a bench config
-(default c2). Prints per kernel the stamp offsets (us) relative to the first
-stamp of the batch.  python tools/trace_batch.py [c4]"""
+(default c2; "flush" as a second argument flushes L2 before the batch). Prints per kernel the stamp offsets (us) relative to the first
+stamp of the batch.  python tools/trace_batch.py [c4 [flush]]"""
 import ctypes as C
 import os
 import sys
@@ -19,14 +19,19 @@ g = cb.Graph.generate_rmat(cfg["n"], cfg["m"], 42)
 plan = cb.Plan(g, None, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), 1024)
 pool = np.arange(g.num_vertices, dtype=np.uint32)
 s = cb.SeedSchedule.make(1, 1234)
+flush = len(sys.argv) > 2 and sys.argv[2] == "flush"  # L2 flushed before the traced batch
 for step in range(4):
     seeds = draw_from_pool(pool, 1024, 1234, cb.hash_bits(step, [0]))
+    if flush and step == 3:
+        import torch
+        torch.empty(512 << 20, dtype=torch.uint8, device="cuda").zero_()
+        torch.cuda.synchronize()
     plan.sample([seeds], s, cb.MODE_INDEP)
     s = cb.schedule_advance(s)
 buf = np.zeros(32 * 64 * 8, np.uint64)
 assert _lib.load().cb_plan_trace(plan._h, buf.ctypes.data_as(C.c_void_p), len(buf)) == 0
 t = buf.reshape(32, 64, 8).astype(np.int64)
-t0 = t[t > 10 ** 12].min()  # globaltimer stamps (the mark rows also carry counts)
+t0 = t[0, 0, 0]  # the batch's first stamp: frontier0, CTA 0 (older slots may hold stale stamps)
 names = {0: "frontier0", 1: "mark0", 2: "post0", 3: "frontier1", 4: "mark1", 5: "post1",
          6: "frontier2", 7: "mark2", 8: "post2"}
 # mark stamps: 0 start, 2 end of phase A (single-record tiles), 1 end; mark
@@ -39,6 +44,9 @@ for k, nm in names.items():
         row = t[k, cta]
         if row[0] == 0:
             continue
-        print(nm, cta, [round((x - t0) / 1000, 2) if x else None for x in row[:5]],
+        print(nm, cta, [round((x - t0) / 1000, 2) if x else None for x in row[:6 if nm.startswith("frontier") else 5]],
               # mark: phase-A tiles and prefilter survivors of the row's warp 0
               list(map(int, row[5:7])) if nm.startswith("mark") else "")
+# latest end of any CTA per kernel (slot 63*8+7, atomicMax by every CTA)
+print("kernel ends (us):", {nm: round((int(t[k, 63, 7]) - t0) / 1000, 2)
+                             for k, nm in names.items() if t[k, 63, 7] > t0})
