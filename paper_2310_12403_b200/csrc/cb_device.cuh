@@ -208,11 +208,15 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 
 // Programmatic dependent launch: a kernel launched with programmatic stream
 // serialisation may start while its predecessor drains; it waits here for the
-// predecessor's completion (and memory) before touching its outputs, then lets
-// its own successor begin launching. No-ops for ordinary launches.
+// predecessor's completion (and memory) before touching its outputs. No
+// explicit launch_dependents: a CTA's exit counts as its trigger, so the
+// successor's CTAs are scheduled as this grid's last CTAs retire instead of
+// occupying SM slots for its whole run. No-ops for ordinary launches.
 __device__ __forceinline__ void pdl_begin() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef CB_PDL_EARLY
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {

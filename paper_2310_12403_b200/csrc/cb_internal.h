@@ -321,7 +321,7 @@ constexpr int kMarkNT = CB_MARK_NT;                // labor_mark block size
 constexpr int kLaborTile = kMarkNT * CB_MARK_IPT;  // scan positions per mark tile
 constexpr uint64_t kVtabMaxVerts = 1ULL << 26;  // smoothed variate table cap (512 MiB)
 #ifndef CB_FRONTIER_IPT
-#define CB_FRONTIER_IPT 4
+#define CB_FRONTIER_IPT 1
 #endif
 constexpr int kFrontierIPT = CB_FRONTIER_IPT;  // destinations per frontier thread
 constexpr int kFrontierTile = 256 * kFrontierIPT;

@@ -1,6 +1,7 @@
 """Debug: globaltimer stamps of one batch (CB_TRACE=1) of a bench config
-(default c2; "flush" as a second argument flushes L2 before the batch). Prints per kernel the stamp offsets (us) relative to the first
-stamp of the batch.  python tools/trace_batch.py [c4 [flush]]"""
+(default c2; "flush" flushes L2 before the batch, "graph" replays the captured
+batch). Prints per kernel the stamp offsets (us) relative to the first
+stamp of the batch.  python tools/trace_batch.py [c4 [flush] [graph]]"""
 import ctypes as C
 import os
 import sys
@@ -19,14 +20,21 @@ g = cb.Graph.generate_rmat(cfg["n"], cfg["m"], 42)
 plan = cb.Plan(g, None, 3, cb.SamplerConfig(cb.SamplerKind.kLabor0, 10), 1024)
 pool = np.arange(g.num_vertices, dtype=np.uint32)
 s = cb.SeedSchedule.make(1, 1234)
-flush = len(sys.argv) > 2 and sys.argv[2] == "flush"  # L2 flushed before the traced batch
+flush = "flush" in sys.argv[2:]  # L2 flushed before the traced batch
+graph = "graph" in sys.argv[2:]  # replays of the captured batch instead of eager launches
+if graph:
+    plan.capture([0, 1024], s, cb.MODE_INDEP)
 for step in range(4):
     seeds = draw_from_pool(pool, 1024, 1234, cb.hash_bits(step, [0]))
     if flush and step == 3:
         import torch
         torch.empty(512 << 20, dtype=torch.uint8, device="cuda").zero_()
         torch.cuda.synchronize()
-    plan.sample([seeds], s, cb.MODE_INDEP)
+    if graph:
+        plan.replay(seeds.ctypes.data, s, False, 1)
+        plan.synchronize()
+    else:
+        plan.sample([seeds], s, cb.MODE_INDEP)
     s = cb.schedule_advance(s)
 buf = np.zeros(32 * 64 * 8, np.uint64)
 assert _lib.load().cb_plan_trace(plan._h, buf.ctypes.data_as(C.c_void_p), len(buf)) == 0
