@@ -296,7 +296,11 @@ def run_reference(args, cfg):
                                        coop_parts=coop_parts)
     per_batch = max(probe[0], 1e-3)
     budget = 120.0
-    P = int(max(1, min(threads, budget / max(1, args.steps + args.warmup) / per_batch)))
+    # parts run in parallel over the host threads (coop.cpp:115-117): one
+    # wave of `threads` parts costs about one probe batch, so every step uses
+    # all the threads, with up to 4 waves while the run stays within budget
+    waves = int(max(1, min(4, budget / max(1, args.steps + args.warmup) / per_batch)))
+    P = threads * waves
     value, cores, desc, per_step = cpu_reference_leg(
         cfg, csr, float("inf"), parts_per_step=P, max_steps=args.warmup + args.steps,
         coop_parts=coop_parts)
