@@ -338,10 +338,18 @@ __device__ __forceinline__ void frontier_body(const FrontierArgs& a, const Relab
   }
 }
 
+// CTAs [0, n_front) run the frontier; the rest relabel layer l-1 (independent
+// work on its own CTAs, so the frontier's load chain starts at once).
 template <int IPT>
-__global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelArgs r) {
+__global__ void __launch_bounds__(kNT) frontier_kernel(FrontierArgs a, RelabelArgs r,
+                                                       unsigned n_front) {
   pdl_begin();
-  frontier_body<IPT>(a, r, blockIdx.x, gridDim.x);
+  if (blockIdx.x >= n_front) {
+    relabel_range(r, (blockIdx.x - n_front) * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
+                  static_cast<uint64_t>(gridDim.x - n_front) * blockDim.x);
+    return;
+  }
+  frontier_body<IPT>(a, RelabelArgs{}, blockIdx.x, n_front);
 }
 
 // Largest record index in [lo, hi] whose scan prefix is <= x.
@@ -534,7 +542,11 @@ __device__ __forceinline__ bool keep_plain(uint64_t p1, uint32_t t, uint64_t T) 
 // Lane j keeps word j's ballot; one coalesced store at the end. Every kept
 // position also leaves its finished edge (t, dst index) in the stage array,
 // so the ordered emission is one load per edge.
-template <int IPT, bool SMOOTH, bool STAGED>
+// MODE 0: records read from global memory; 1: the tile's records staged in
+// shared memory (s_act[0] = record a0, nd of them); 2: a window of nd records
+// starting at `cur` in shared memory (s_act[0] = record a0 + cur), global
+// memory past it.
+template <int IPT, bool SMOOTH, int MODE>
 __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v, uint64_t p1,
                                           uint64_t p2, uint64_t x0, uint32_t r0, uint32_t rend,
                                           uint32_t a0, uint32_t a1, uint32_t cur,
@@ -543,23 +555,28 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
                                           const YhiConst& yk) {
   static_assert(IPT <= 32, "one word per lane");
   const uint32_t lane = lane_id();
+  constexpr bool STAGED = MODE == 1;
+  const uint32_t cw = cur;  // MODE 2: window base
+  // record c in shared memory (MODE 1, or inside the MODE-2 window)
+  auto in_smem = [&](uint32_t c) -> bool { return STAGED || (MODE == 2 && c - cw < nd); };
+  auto sm = [&](uint32_t c) -> const ActRec& { return s_act[MODE == 2 ? c - cw : c]; };
   auto nxt_of = [&](uint32_t c) -> uint32_t {  // tile-relative start of record c+1
     if (STAGED)
       return (c + 1 < nd) ? static_cast<uint32_t>(min(static_cast<uint64_t>(s_act[c + 1].pre) - x0,
                                                       static_cast<uint64_t>(0xffffffffu)))
                           : 0xffffffffu;
     if (a0 + c + 1 > a1) return 0xffffffffu;
-    const uint64_t pr = __ldg(&a.act[a0 + c + 1].pre);
+    const uint64_t pr = in_smem(c + 1) ? sm(c + 1).pre : __ldg(&a.act[a0 + c + 1].pre);
     return static_cast<uint32_t>(min(pr - x0, static_cast<uint64_t>(0xffffffffu)));
   };
   auto row_of = [&](uint32_t c) -> const uint32_t* {
-    return a.indices + ((STAGED ? s_act[c].a : __ldg(&a.act[a0 + c].a)) + x0);
+    return a.indices + ((in_smem(c) ? sm(c).a : __ldg(&a.act[a0 + c].a)) + x0);
   };
   auto th_of = [&](uint32_t c) -> uint64_t {
-    return STAGED ? s_act[c].b : __ldg(&a.act[a0 + c].b);
+    return in_smem(c) ? sm(c).b : __ldg(&a.act[a0 + c].b);
   };
   auto di_of = [&](uint32_t c) -> uint32_t {
-    return STAGED ? s_act[c].di : __ldg(&a.act[a0 + c].di);
+    return in_smem(c) ? sm(c).di : __ldg(&a.act[a0 + c].di);
   };
   uint2* stage = a.stage + x0 + r0;
   uint32_t my_word = 0;
@@ -657,6 +674,40 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
     }
   }
   if (lane < IPT && r0 + lane * 32 < rend) a.keep_words[((x0 + r0) >> 5) + lane] = my_word;
+}
+
+// Record (local index from a0) of scan position x for a warp: 32-ary search
+// over the records' starts in global memory (2-3 rounds of 32 parallel loads
+// instead of a dependent binary search), then the next 32 records from there
+// loaded into the warp's shared-memory window `win` (MODE 2 of mark_span).
+// Returns the record; *nw = records in the window.
+__device__ __forceinline__ uint32_t rec_window(const ActRec* __restrict__ act, uint32_t a0,
+                                               uint32_t a1, uint64_t x, ActRec* win,
+                                               uint32_t* nw) {
+  const uint32_t lane = lane_id();
+  uint32_t lo = 0, hi = a1 - a0;
+  while (lo < hi) {
+    const uint32_t step = (hi - lo + 32) / 32;
+    const uint32_t cand = lo + lane * step;
+    const bool le = cand <= hi && __ldg(&act[a0 + cand].pre) <= x;
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    const uint32_t best = lo + (31 - __clz(m)) * step;
+    lo = best;
+    hi = min(hi, best + step - 1);
+    if (step == 1) break;
+  }
+  const uint32_t n = min(32u, a1 - a0 - lo + 1);
+  __syncwarp();  // every lane is done with the window's previous contents
+  if (lane < n) {
+    const uint4* src = reinterpret_cast<const uint4*>(act + a0 + lo + lane);
+    uint4* dst = reinterpret_cast<uint4*>(win + lane);
+    const uint4 u0 = __ldg(src), u1 = __ldg(src + 1);
+    dst[0] = u0;
+    dst[1] = u1;
+  }
+  __syncwarp();
+  *nw = n;
+  return lo;
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -953,6 +1004,7 @@ __device__ __forceinline__ void mark_mixed_warp(const LaborArgs& a, const Variat
   constexpr uint32_t WSPAN = 32 * IPT;
   constexpr uint32_t WPC = kMarkNT / 32;
   constexpr uint32_t kRecsW = (kPureStages * kPureStride * 4) / sizeof(ActRec);  // the warp ring
+  static_assert(kRecsW >= 32, "the 32-record window fits the warp ring");
   const uint32_t lane = lane_id();
   const uint64_t W = static_cast<uint64_t>(ncta) * WPC;
   const uint64_t gw = static_cast<uint64_t>(role) * WPC + (threadIdx.x >> 5);
@@ -989,12 +1041,13 @@ __device__ __forceinline__ void mark_mixed_warp(const LaborArgs& a, const Variat
           hi = min(hi, best + step - 1);
           if (step == 1) break;
         }
-        mark_span<IPT, false, true>(a, v, p1, 0, x0, r0, rend, a0, a1, lo, wrec, nd, uncert,
+        mark_span<IPT, false, 1>(a, v, p1, 0, x0, r0, rend, a0, a1, lo, wrec, nd, uncert,
                                     nullptr, yk);
-      } else {
-        const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
-        mark_span<IPT, false, false>(a, v, p1, 0, x0, r0, rend, a0, a1, cur, nullptr, 0, uncert,
-                                     nullptr, yk);
+      } else {  // more records than the ring holds: a 32-record window of them
+        uint32_t nw;
+        const uint32_t cur = rec_window(a.act, a0, a1, x0 + r0, wrec, &nw);
+        mark_span<IPT, false, 2>(a, v, p1, 0, x0, r0, rend, a0, a1, cur, wrec, nw, uncert,
+                                 nullptr, yk);
       }
     }
   }
@@ -1031,15 +1084,25 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   const double* vtab = (SMOOTH && vtab_used(a, total)) ? a.vtab : nullptr;
   const uint32_t warp = threadIdx.x >> 5;
   unsigned long long uncert = 0;
+#ifdef CB_TRACE_FIRST  // trace the first 64 CTAs instead (small layers)
+  const unsigned trole = role < 64 ? role : 64u;
+#else
   const unsigned trole = (role % 16 == 0) ? role / 16 : 64u;  // trace: every 16th CTA
+#endif
   tstamp(a.trace, trole, 0);
   // ---- phase A (plain stream with the frontier's tile lists): the
   // single-record tiles, one warp each. Phase B: the tiles with record
   // boundaries (the back of the list), or every tile without lists.
   const bool listed = !SMOOTH && a.tile_list != nullptr;
   uint64_t n_mixed = 0;
+  unsigned prole = role;  // this CTA's phase-B slot
   if (listed) {
     const uint64_t n_pure = min(static_cast<uint64_t>(a.list_ctr[0]), ntiles);
+    // phase-B tiles start at the first CTA without a phase-A tile, so a small
+    // layer's CTA never runs a pure and a mixed tile back to back
+    const unsigned off = static_cast<unsigned>(
+        min(static_cast<uint64_t>(ncta), (n_pure + WPC - 1) / WPC) % ncta);
+    prole = (role + ncta - off) % ncta;
     n_mixed = min(static_cast<uint64_t>(a.list_ctr[1]), ntiles - n_pure);
     MarkSmemA& sa = *reinterpret_cast<MarkSmemA*>(s_raw);
     mark_pure<kPureStages>(a, p1, n_pure, role, ncta, &sa.ring[warp][0][0], s_rbar[warp]);
@@ -1059,11 +1122,11 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   YhiConst yk = yhi_const(p1);
   yk.K0 = opaque(yk.K0);
   yk.K1 = opaque(yk.K1);
-  const uint64_t nb = listed ? (n_mixed > role ? (n_mixed - role + ncta - 1) / ncta : 0)
+  const uint64_t nb = listed ? (n_mixed > prole ? (n_mixed - prole + ncta - 1) / ncta : 0)
                              : (ntiles > role ? (ntiles - role + ncta - 1) / ncta : 0);
   // tile of phase-B item i
   auto tile_at = [&](uint64_t i) -> uint64_t {
-    const uint64_t j = role + i * ncta;
+    const uint64_t j = prole + i * ncta;
     return listed ? static_cast<uint64_t>(a.tile_list[a.list_cap - 1 - j].x) : j;
   };
   auto stage = [&](uint32_t a0, uint32_t a1, int buf) {
@@ -1112,6 +1175,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();  // barriers initialised, first records visible
+  tstamp(a.trace, trole, 3);
   uint32_t iphase = 0;  // mbarrier phase bit per id buffer (bit ib)
   uint32_t ipure = 0;   // id buffer ib holds its tile's ids (bit ib)
   if (threadIdx.x == 0 && nb > 0 && c0 == c1) stage_ids(tile_at(0), 0, 0);
@@ -1152,7 +1216,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
         mark_span_smem<IPT, SMOOTH>(a, v, p1, p2, x0, r0, s_ids[ib] + s_delta[ib], s_act[rb][0],
                                     uncert, vtab);
       } else if (r0 < rend) {
-        mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, 0, s_act[rb], nd, uncert,
+        mark_span<IPT, SMOOTH, 1>(a, v, p1, p2, x0, r0, rend, a0, a1, 0, s_act[rb], nd, uncert,
                                      vtab, yk);
       }
     } else if (r0 < rend) {
@@ -1170,14 +1234,18 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
           hi = min(hi, best + step - 1);
           if (step == 1) break;
         }
-        mark_span<IPT, SMOOTH, true>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, sa, nd, uncert,
+        mark_span<IPT, SMOOTH, 1>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, sa, nd, uncert,
                                      vtab, yk);
-      } else {
-        const uint32_t cur = rec_search(a.act, a0, a1, x0 + r0) - a0;
-        mark_span<IPT, SMOOTH, false>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, nullptr, 0,
-                                      uncert, vtab, yk);
+      } else {  // more records than s_act holds: a 32-record window per warp
+        static_assert(kRecs >= 32 * (kMarkNT / 32), "one 32-record window per warp");
+        uint32_t nw;
+        ActRec* win = s_act[rb] + 32 * warp;  // unused by this item (not staged)
+        const uint32_t cur = rec_window(a.act, a0, a1, x0 + r0, win, &nw);
+        mark_span<IPT, SMOOTH, 2>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, win, nw, uncert,
+                                  vtab, yk);
       }
     }
+    if (i == 0) tstamp(a.trace, trole, 4);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();  // this item's buffers are free; the next records are visible
     rb = rb1;
@@ -1850,9 +1918,10 @@ void launch_batch_begin(const Sync& s, uint32_t* clear_bits, uint32_t* clear_sum
 void launch_frontier(const FrontierArgs& a, const RelabelArgs& r, uint64_t cap_dst,
                      uint64_t relabel_work, cudaStream_t st) {
   const int occ = resident_per_sm(frontier_kernel<kFrontierIPT>);
-  const int grid = std::max(grid_for(cap_dst, kNT * kFrontierIPT, occ),
-                            r.edges ? grid_for(relabel_work, kNT * 4, occ) : 1);
-  launch_k(frontier_kernel<kFrontierIPT>, grid, kNT, st, a, r);
+  const int fgrid = grid_for(cap_dst, kNT * kFrontierIPT, occ);
+  const int rgrid = r.edges ? grid_for(relabel_work, kNT * 4, occ) : 0;
+  launch_k(frontier_kernel<kFrontierIPT>, fgrid + rgrid, kNT, st, a, r,
+           static_cast<unsigned>(fgrid));
   CB_LAUNCH("frontier");
 }
 

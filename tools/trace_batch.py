@@ -46,7 +46,8 @@ names = {0: "frontier0", 1: "mark0", 2: "post0", 3: "frontier1", 4: "mark1", 5: 
 # rows are every 16th CTA (row r = CTA 16 r)
 for k, nm in names.items():
     # post: CTAs 0-31 = extract roles, 32-63 = emit roles
-    for cta in ((list(range(0, 64, 4)) if nm.startswith("mark") else list(range(0, 64, 8)))
+    for cta in ((list(range(0, 64, 1 if os.environ.get("TRACE_FIRST") else 4))
+                 if nm.startswith("mark") else list(range(0, 64, 8)))
                 if not nm.startswith("post") else
                 [0, 1, 2, 8, 16, 31, 32, 33, 34, 40, 48, 63]):
         row = t[k, cta]
