@@ -457,6 +457,11 @@ __device__ __forceinline__ bool keep_rule(const Variates& v, uint64_t p1, uint64
 #define CB_SPAN_PREFILTER 0
 #endif
 constexpr int kSpanPrefilter = CB_SPAN_PREFILTER;
+#ifndef CB_COMPACT_SPAN
+#define CB_COMPACT_SPAN 0
+#endif
+// CTA-mode phase B (small layers) with rolled keep loops (latency A/B)
+constexpr bool kCompactSpan = CB_COMPACT_SPAN != 0;
 
 // High word of y = z * c2, the last SplitMix64 multiply of mix64(p1 ^ t)
 // (z after the second xor-shift): keep_plain's prefilter input.
@@ -546,7 +551,7 @@ __device__ __forceinline__ bool keep_plain(uint64_t p1, uint32_t t, uint64_t T) 
 // shared memory (s_act[0] = record a0, nd of them); 2: a window of nd records
 // starting at `cur` in shared memory (s_act[0] = record a0 + cur), global
 // memory past it.
-template <int IPT, bool SMOOTH, int MODE>
+template <int IPT, bool SMOOTH, int MODE, bool COMPACT = false>
 __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v, uint64_t p1,
                                           uint64_t p2, uint64_t x0, uint32_t r0, uint32_t rend,
                                           uint32_t a0, uint32_t a1, uint32_t cur,
@@ -622,7 +627,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
       return;
     } else {
 #pragma unroll
-      for (int j = 0; j < IPT; ++j) {
+      auto keep_at = [&](int j) {
         const bool keep = SMOOTH ? keep_rule<SMOOTH>(v, p1, p2, tv[j], th, uncert, vtab, a.layer)
                                  : mix64_dev(p1 ^ tv[j]) <= T;
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -631,6 +636,13 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
           set_bit(a.bits, a.summ, tv[j]);
           st_lane[j * 32] = make_uint2(tv[j], di);
         }
+      };
+      if constexpr (COMPACT) {
+#pragma unroll 1
+        for (int j = 0; j < IPT; ++j) keep_at(j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) keep_at(j);
       }
     }
   } else {
@@ -657,8 +669,7 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
         km |= (pass ? 1u : 0u) << j;
       }
     }
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
+    auto keep_at = [&](int j) {
       const uint32_t r = r0 + j * 32 + lane;
       const bool keep =
           (r < rend) &&
@@ -671,6 +682,15 @@ __device__ __forceinline__ void mark_span(const LaborArgs& a, const Variates& v,
         set_bit(a.bits, a.summ, tv[j]);
         stage[j * 32 + lane] = make_uint2(tv[j], di_of(li[j]));
       }
+    };
+    // COMPACT (small layers' CTA-mode tiles): one loop body instead of IPT
+    // unrolled copies, so a cold instruction cache fetches less code
+    if constexpr (COMPACT) {
+#pragma unroll 1
+      for (int j = 0; j < IPT; ++j) keep_at(j);
+    } else {
+#pragma unroll
+      for (int j = 0; j < IPT; ++j) keep_at(j);
     }
   }
   if (lane < IPT && r0 + lane * 32 < rend) a.keep_words[((x0 + r0) >> 5) + lane] = my_word;
@@ -1216,7 +1236,7 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
         mark_span_smem<IPT, SMOOTH>(a, v, p1, p2, x0, r0, s_ids[ib] + s_delta[ib], s_act[rb][0],
                                     uncert, vtab);
       } else if (r0 < rend) {
-        mark_span<IPT, SMOOTH, 1>(a, v, p1, p2, x0, r0, rend, a0, a1, 0, s_act[rb], nd, uncert,
+        mark_span<IPT, SMOOTH, 1, kCompactSpan>(a, v, p1, p2, x0, r0, rend, a0, a1, 0, s_act[rb], nd, uncert,
                                      vtab, yk);
       }
     } else if (r0 < rend) {
@@ -1234,14 +1254,14 @@ __device__ __forceinline__ void mark_body(const LaborArgs& a, unsigned role, uns
           hi = min(hi, best + step - 1);
           if (step == 1) break;
         }
-        mark_span<IPT, SMOOTH, 1>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, sa, nd, uncert,
+        mark_span<IPT, SMOOTH, 1, kCompactSpan>(a, v, p1, p2, x0, r0, rend, a0, a1, lo, sa, nd, uncert,
                                      vtab, yk);
       } else {  // more records than s_act holds: a 32-record window per warp
         static_assert(kRecs >= 32 * (kMarkNT / 32), "one 32-record window per warp");
         uint32_t nw;
         ActRec* win = s_act[rb] + 32 * warp;  // unused by this item (not staged)
         const uint32_t cur = rec_window(a.act, a0, a1, x0 + r0, win, &nw);
-        mark_span<IPT, SMOOTH, 2>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, win, nw, uncert,
+        mark_span<IPT, SMOOTH, 2, kCompactSpan>(a, v, p1, p2, x0, r0, rend, a0, a1, cur, win, nw, uncert,
                                   vtab, yk);
       }
     }
